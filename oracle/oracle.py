@@ -1,0 +1,179 @@
+"""FP64 CPU oracle for the CIL hot path — ctypes wrapper around ``cil_oracle.c``.
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and
+``bench.py`` (its ``cpu_baseline`` leg and ``--impl reference``) may import this
+module.  The product package ``paper_2203_14742_b200`` never imports it, and it
+imports nothing from the product package: the two share no code.
+
+Every function follows the plain definition in arXiv 2203.14742:
+Eq. (1), Eq. (2), Eq. (4) PAPER.md:144-148,
+Eqs. (5)-(10) PAPER.md:178-193, Eqs. (11)-(13) and Alg. 3 PAPER.md:236-297.
+Readings of the paper where it is silent: DESIGN.md "Readings" R1..R10.
+Pins (what fixes this oracle to something other than itself): tests/test_oracle_pins.py.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "cil_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+
+# measure bits (bit order = concatenation order)
+L2, LINF, W12SUM, W12, W1INF, W1INFSUM = (1 << i for i in range(6))
+MEASURE_NAMES = ["L2", "LINF", "W12SUM", "W12", "W1INF", "W1INFSUM"]
+ITEM_OK, ITEM_NONFINITE, ITEM_NOTPD = 0, 1, 2
+
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle with plain gcc -O2 (no fast-math, no intrinsics)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-D_GNU_SOURCE", "-fPIC", "-shared",
+                               "-o", _LIB, _SRC, "-lm", "-lpthread"])
+    return _LIB
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        build()
+        lib = ctypes.CDLL(_LIB)
+        P = ctypes.c_void_p
+        i64, i32, u32, f64 = ctypes.c_int64, ctypes.c_int, ctypes.c_uint32, ctypes.c_double
+        lib.oracle_features.argtypes = [P, i64, i64, P, i64, i64, i32, i32, i32, f64, u32, P, i32,
+                                        f64, P, P, P, P, P, i32]
+        lib.oracle_features.restype = i32
+        lib.oracle_distance_matrix.argtypes = [P, i64, i64, P, i64, i64, i32, i32, i32, f64, u32, P]
+        lib.oracle_stats.argtypes = [P, i32, i32, P, P]
+        lib.oracle_stats.restype = i32
+        lib.oracle_loglik.argtypes = [P, P, P, i32, f64, P]
+        lib.oracle_loglik.restype = i32
+        lib.oracle_synth_loglik.argtypes = [P, i64, i32, i32, i32, P, i64, i32, i32, i32, i32, f64,
+                                            u32, P, i32, f64, P, P, i32]
+        lib.oracle_synth_loglik.restype = i32
+        lib.oracle_subnorms.argtypes = [P, P, P, P]
+        _lib = lib
+    return _lib
+
+
+def _f32(x):
+    x = np.ascontiguousarray(np.asarray(x, dtype=np.float32))
+    return x
+
+
+def _ptr(a):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def n_measures(mask: int) -> int:
+    return bin(mask & 0x3F).count("1")
+
+
+def _rows(X, K):
+    X = _f32(X)
+    n = X.shape[0] if X.ndim > 0 else 0
+    X2 = X.reshape(n, -1) if n else X.reshape(0, K)
+    assert X2.shape[1] == K, (X2.shape, K)
+    return X2
+
+
+def default_threads() -> int:
+    return max(1, os.cpu_count() or 1)
+
+
+def features(A, B, grid, mask, radii, band: float = 1e-6, nthreads: int | None = None):
+    """Eq. (1)/(2): counts, band counts lo/hi, y and #ambiguous (pair, radius) cases.
+
+    A: [N][S][H][W] (or [N][K]) float32, B: [Nt][...]; grid = (S, H, W, h);
+    radii: [n_meas][M] strictly decreasing.  Returns dict of numpy arrays.
+    """
+    S, H, W, h = grid
+    K = S * H * W
+    A2, B2 = _rows(A, K), _rows(B, K)
+    nq = n_measures(mask)
+    radii = np.ascontiguousarray(np.asarray(radii, dtype=np.float64).reshape(nq, -1))
+    M = radii.shape[1]
+    cnt = np.zeros((nq, M), np.int64)
+    lo = np.zeros_like(cnt)
+    hi = np.zeros_like(cnt)
+    y = np.zeros((nq, M), np.float64)
+    amb = np.zeros(1, np.int64)
+    st = _load().oracle_features(_ptr(A2), K, A2.shape[0], _ptr(B2), K, B2.shape[0], S, H, W,
+                                 float(h), mask, _ptr(radii), M, float(band), _ptr(cnt), _ptr(lo),
+                                 _ptr(hi), _ptr(y), _ptr(amb), nthreads or default_threads())
+    if st < 0:
+        raise ValueError("oracle_features: invalid arguments")
+    return {"counts": cnt, "lo": lo, "hi": hi, "y": y, "ambiguous": int(amb[0]), "status": st}
+
+
+def distance_matrix(A, B, grid, mask):
+    """All pairwise distances d[q][i][j] for the selected measures (tiny inputs)."""
+    S, H, W, h = grid
+    K = S * H * W
+    A2, B2 = _rows(A, K), _rows(B, K)
+    nq = n_measures(mask)
+    D = np.zeros((nq, A2.shape[0], B2.shape[0]), np.float64)
+    _load().oracle_distance_matrix(_ptr(A2), K, A2.shape[0], _ptr(B2), K, B2.shape[0], S, H, W,
+                                   float(h), mask, _ptr(D))
+    return D
+
+
+class _Grid(ctypes.Structure):
+    _fields_ = [("S", ctypes.c_int), ("H", ctypes.c_int), ("W", ctypes.c_int), ("h", ctypes.c_double)]
+
+
+def subnorms(a, b, grid):
+    """(s0, sx, sy, m0, mx, my) of u = a - b (sums of squares, derivative terms / h^2)."""
+    S, H, W, h = grid
+    a, b = _f32(a).ravel(), _f32(b).ravel()
+    g = _Grid(S, H, W, float(h))
+    out = np.zeros(6, np.float64)
+    _load().oracle_subnorms(_ptr(a), _ptr(b), ctypes.byref(g), _ptr(out))
+    return out
+
+
+def stats(Y):
+    """mu, Sigma (two-pass, 1/(n-1)) of the n realisations Y[n][D]."""
+    Y = np.ascontiguousarray(np.asarray(Y, np.float64))
+    n, D = Y.shape
+    mu = np.zeros(D)
+    Sig = np.zeros((D, D))
+    if _load().oracle_stats(_ptr(Y), n, D, _ptr(mu), _ptr(Sig)) != 0:
+        raise ValueError("oracle_stats needs n >= 2")
+    return mu, Sig
+
+
+def loglik(mu, Sigma, y, ridge: float = 0.0):
+    """(quad, logdet, loglik), status — Eq. (4)/(12) plus the Gaussian log-density [R8]."""
+    mu = np.ascontiguousarray(np.asarray(mu, np.float64))
+    Sigma = np.ascontiguousarray(np.asarray(Sigma, np.float64))
+    y = np.ascontiguousarray(np.asarray(y, np.float64))
+    out = np.zeros(3)
+    st = _load().oracle_loglik(_ptr(mu), _ptr(Sigma), _ptr(y), mu.shape[0], float(ridge), _ptr(out))
+    return out, st
+
+
+def synth_loglik(pool, n_ens, N_set, N_tilde, data, k0, grid, mask, radii, ridge=0.0,
+                 nthreads: int | None = None):
+    """SCIL at one theta (Alg. 3): returns (out[3], status, Y[n_ens^2 + 1][D])."""
+    S, H, W, h = grid
+    K = S * H * W
+    P2 = _rows(pool, K)
+    D2 = _rows(data, K)
+    assert P2.shape[0] >= n_ens * (N_set + N_tilde)
+    assert D2.shape[0] == N_set
+    nq = n_measures(mask)
+    radii = np.ascontiguousarray(np.asarray(radii, np.float64).reshape(nq, -1))
+    M = radii.shape[1]
+    out = np.zeros(3)
+    Y = np.zeros((n_ens * n_ens + 1, nq * M))
+    st = _load().oracle_synth_loglik(_ptr(P2), K, n_ens, N_set, N_tilde, _ptr(D2), K, int(k0), S, H,
+                                     W, float(h), mask, _ptr(radii), M, float(ridge), _ptr(out),
+                                     _ptr(Y), nthreads or default_threads())
+    return out, st, Y
