@@ -1,0 +1,197 @@
+/*
+ * cil.h — C ABI of libcil.so, the B200 (sm_100a) hot path of the Correlation
+ * Integral Likelihood method (arXiv 2203.14742; PAPER.md = /root/reference/PAPER.md).
+ *
+ * Conventions for every call:
+ *  - Pointers are DEVICE pointers unless marked [host].  The caller owns every
+ *    buffer; the library never allocates device memory.  Scratch comes from a
+ *    caller-provided workspace sized by the matching *_workspace_size() call.
+ *  - Calls are asynchronous on `stream` (a cudaStream_t passed as void*; NULL =
+ *    legacy default stream).  They never synchronise the device.
+ *  - The return value reports HOST-side validation only: CIL_OK, CIL_EINVAL (bad
+ *    argument), CIL_EUNSUPPORTED (a valid request this build does not support),
+ *    CIL_ECUDA (a launch failed; cil_last_cuda_error() has the cudaError_t).
+ *    Data-dependent conditions are written to item_status[] on the device:
+ *    CIL_ITEM_NONFINITE (an input pattern value is NaN/Inf), CIL_ITEM_NOTPD (a
+ *    Cholesky pivot <= 0), CIL_ITEM_BADRADII (radii not > 0 and strictly
+ *    decreasing), CIL_ITEM_OVERFLOW (the L2 re-check list overflowed: counts of
+ *    that item are not trustworthy; enlarge the workspace).  Bits OR together.
+ *  - Patterns are FP32, one pattern = S species x H rows x W columns, row-major
+ *    [S][H][W] ("pattern-major then component-major then row-major");
+ *    K = S*H*W, pattern p of a set starts at base + p*ld (ld >= K, in floats).
+ *  - Thread-safe: no global mutable state besides a once-per-device kernel
+ *    attribute setup.
+ */
+#ifndef CIL_H
+#define CIL_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define CIL_API __attribute__((visibility("default")))
+#else
+#define CIL_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    CIL_OK = 0,
+    CIL_EINVAL = 1,
+    CIL_EUNSUPPORTED = 2,
+    CIL_ENOMEM = 3, /* workspace too small */
+    CIL_ECUDA = 4
+} cil_status;
+
+enum {
+    CIL_ITEM_OK = 0,
+    CIL_ITEM_NONFINITE = 1,
+    CIL_ITEM_NOTPD = 2,
+    CIL_ITEM_BADRADII = 4,
+    CIL_ITEM_OVERFLOW = 8
+};
+
+/* Distance measures, a bit mask.  A feature vector concatenates the selected
+ * measures in BIT ORDER (multi-feature CIL), each contributing M
+ * values.  Definitions (discrete equivalents; readings R1-R4 of
+ * DESIGN.md): u = a - b, h = grid spacing, w = h^dim (dim 2 if H > 1 else 1),
+ * D_x u, D_y u = forward differences / h inside each species, last node omitted;
+ * a_al = sqrt(w * sum (D^al u)^2), m_al = max |D^al u| over all species/nodes. */
+typedef enum {
+    CIL_L2 = 1 << 0,        /* Eq. (5)  a_0                          */
+    CIL_LINF = 1 << 1,      /* Eq. (6)  m_0                          */
+    CIL_W12SUM = 1 << 2,    /* Eq. (7)  a_0 + a_x + a_y              */
+    CIL_W12 = 1 << 3,       /* Eq. (8)  sqrt(a_0^2 + a_x^2 + a_y^2)  */
+    CIL_W1INF = 1 << 4,     /* Eq. (9)  max(m_0, m_x, m_y)           */
+    CIL_W1INFSUM = 1 << 5   /* Eq. (10) m_0 + m_x + m_y              */
+} cil_dist;
+#define CIL_ALL_DISTS 0x3Fu
+
+/* Engine for the L2 measure (all other measures always run on the CUDA-core
+ * tile engine).  TC_* = tcgen05 tensor-core Gram g = a~.b~ of centred operands
+ * in split precision (hi.hi + hi.lo + lo.hi), d^2 = |a~|^2 + |b~|^2 - 2g, with
+ * every pair whose d^2 lies within the engine's error bound of a threshold
+ * re-evaluated exactly (FP64) — so counts are exact either way.  SIMT = FP32
+ * differences on CUDA cores with FP64-flushed sums. */
+typedef enum {
+    CIL_ENGINE_AUTO = 0,      /* TC_3XBF16 */
+    CIL_ENGINE_TC_3XBF16 = 1,
+    CIL_ENGINE_TC_3XTF32 = 2,
+    CIL_ENGINE_SIMT = 3
+} cil_engine;
+
+typedef struct {
+    int32_t S, H, W; /* species, rows, columns; H == 1 -> 1-D grid (no y-derivative) */
+    double h;        /* grid spacing; <= 0 -> 1/(W-1) */
+} cil_grid;
+
+/* ------------------------------------------------------------------------ */
+/* cil_features — correlation-integral counts of P independent set pairs.
+ *
+ * For item p, measure slot q (bit order of dist_mask) and radius index m:
+ *   counts[p][q][m] = #{(i,j) : d_q(A_p,i , B_p,j) < radii[p][q][m]}   (Eq. (1), strict <)
+ *   y[p][q][m]      = counts / (N * Nt)                                  (Eq. (1)/(2))
+ * i in [0,N), j in [0,Nt).  A_p,i = A + p*strideA + i*lda; B_p,j = B + p*strideB + j*ldb.
+ *
+ *  radii       [P or 1][n_meas][M] FP64, device; radii_stride = 0 shares one set
+ *              of radii across items, else it is the per-item stride in doubles.
+ *              Each row must be > 0 and strictly decreasing (checked on device).
+ *  counts      [P][n_meas][M] uint64, device, written (not accumulated).
+ *  y           [P][n_meas][M] FP64, device, nullable.
+ *  item_status [P] int32, device, written.
+ *  engine      L2 engine (above).
+ * Constraints (else CIL_EINVAL / CIL_EUNSUPPORTED): P >= 1, N >= 0, Nt >= 0,
+ * S,H,W >= 1, ld >= K, 1 <= M <= 64, dist_mask in [1, 63], measures other than
+ * L2/LINF need W >= 2; strides >= 0; pointers non-NULL (A/B may be NULL when
+ * N resp. Nt is 0).  N*Nt == 0 gives counts 0 and y 0.  Vectorised loads need
+ * K, ld and strides to be multiples of 4 floats and A, B 16-byte aligned
+ * (else CIL_EUNSUPPORTED).
+ * ------------------------------------------------------------------------ */
+CIL_API size_t cil_features_workspace_size(int32_t P, int64_t N, int64_t Nt, cil_grid g,
+                                   uint32_t dist_mask, int32_t M, cil_engine engine);
+
+CIL_API cil_status cil_features(int32_t P,
+                        const float* A, int64_t strideA, int64_t lda, int64_t N,
+                        const float* B, int64_t strideB, int64_t ldb, int64_t Nt,
+                        cil_grid g, uint32_t dist_mask,
+                        const double* radii, int64_t radii_stride, int32_t M,
+                        uint64_t* counts, double* y, int32_t* item_status,
+                        cil_engine engine, void* ws, size_t ws_bytes, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* cil_stats — mu and Sigma of n realisations (Alg. 1 step 3,
+ * PAPER.md:131), batched over P:
+ *   mu[p][a]       = (1/n) sum_v Y[p][v][a]
+ *   Sigma[p][a][b] = 1/(n-1) sum_v (Y[p][v][a]-mu[p][a]) (Y[p][v][b]-mu[p][b])
+ * Two-pass FP64.  Y [P][n][D], mu [P][D], Sigma [P][D][D] row-major, all device.
+ * n >= 2, 1 <= D.
+ * ------------------------------------------------------------------------ */
+CIL_API cil_status cil_stats(int32_t P, const double* Y, int32_t n, int32_t D,
+                     double* mu, double* Sigma, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* cil_loglik — Gaussian log-likelihood of P vectors (Eq. (4), PAPER.md:146;
+ * Eq. (12)):  Sigma + ridge*I = L L^T (Cholesky, no pivoting),
+ * z = L^{-1}(y - mu),  out[p] = {quad = z^T z (the paper's f), logdet = 2 sum ln L_ii,
+ * loglik = -quad/2 - logdet/2 - (D/2) ln 2pi}.
+ *  mu [.][D] with stride mu_stride (0 = shared), Sigma [.][D][D] with stride
+ *  Sigma_stride (0 = shared), y_obs [P][D], out [P][3], item_status [P]
+ *  (CIL_ITEM_NOTPD and out = NaN when a pivot <= 0).  ridge >= 0.  1 <= D <= 192.
+ * ------------------------------------------------------------------------ */
+CIL_API cil_status cil_loglik(int32_t P, const double* mu, int64_t mu_stride,
+                      const double* Sigma, int64_t Sigma_stride,
+                      const double* y_obs, int32_t D, double ridge,
+                      double* out, int32_t* item_status, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* cil_synth_loglik — SCIL (Alg. 3; Eqs. (11)-(13)) for P
+ * parameter proposals theta_p, each with a pool of N_syn = n_ens*(N_set+N_tilde)
+ * synthetic patterns at pools + p*pool_stride (row stride ld):
+ *   subset k = rows [k*N, (k+1)*N), N = N_set + N_tilde;
+ *   s^{k,1} = its first N_set rows, s^{k,2} = its last N_tilde rows;
+ *   y^{k,l} = C(R_p, s^{k,1}, s^{l,2}) for all k,l in [0,n_ens) (k = l included,
+ *   PAPER.md:244), vector index v = k*n_ens + l;  mu_theta, Sigma_theta over the
+ *   n_ens^2 vectors;  y~ = C(R_p, s_data, s^{k0[p],2}) (Eq. (13));
+ *   out[p] = {quad, logdet, loglik} of y~ under N(mu_theta, Sigma_theta + ridge I).
+ *  data   [N_set][K] (row stride ld_data), the observed patterns s_data.
+ *  k0     [P] int32 in [0, n_ens), device (the caller draws it).
+ *  radii  [P][n_meas][M], device (per-theta radii).
+ *  Y_out  nullable [P][n_ens*n_ens + 1][n_meas*M] FP64: the vectors, y~ last.
+ * Constraints: n_ens >= 2, N_set >= 1, N_tilde >= 1, D = n_meas*M <= 192.
+ * ------------------------------------------------------------------------ */
+CIL_API size_t cil_synth_workspace_size(int32_t P, int32_t n_ens, int32_t N_set, int32_t N_tilde,
+                                cil_grid g, uint32_t dist_mask, int32_t M, cil_engine engine);
+
+CIL_API cil_status cil_synth_loglik(int32_t P, const float* pools, int64_t pool_stride, int64_t ld,
+                            int32_t n_ens, int32_t N_set, int32_t N_tilde,
+                            const float* data, int64_t ld_data, const int32_t* k0,
+                            cil_grid g, uint32_t dist_mask, const double* radii, int32_t M,
+                            double ridge, double* out, int32_t* item_status, double* Y_out,
+                            cil_engine engine, void* ws, size_t ws_bytes, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* cil_diag_gram — DIAGNOSTIC (not on the hot path): runs the tensor-core L2 engine on one
+ * set pair without binning and writes d2E[i][j][0] = the engine's FP32 d^2(i,j) (unweighted
+ * sum of squares) and d2E[i][j][1] = its error bound E(i,j) (see cil_engine).  Used by the
+ * tests to measure the Gram error against FP64.  engine must be TC_3XBF16 or TC_3XTF32;
+ * d2E [N][Nt][2] FP32 device; ws_bytes >= cil_features_workspace_size(1, N, Nt, g, CIL_L2,
+ * 1, engine) + 512.
+ * ------------------------------------------------------------------------ */
+CIL_API cil_status cil_diag_gram(const float* A, int64_t lda, int64_t N, const float* B, int64_t ldb,
+                                 int64_t Nt, cil_grid g, cil_engine engine, float* d2E, void* ws,
+                                 size_t ws_bytes, void* stream);
+
+/* ------------------------------------------------------------------------ */
+CIL_API const char* cil_status_string(cil_status s);
+CIL_API int32_t cil_last_cuda_error(void);  /* cudaError_t of the last failed call on this thread */
+CIL_API int32_t cil_version(void);          /* MAJOR*10000 + MINOR*100 + PATCH */
+/* number of kernel launches the last successful call on this thread issued */
+CIL_API int32_t cil_last_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CIL_H */

@@ -1,0 +1,230 @@
+"""paper_2203_14742_b200 — B200-native hot path of the Correlation Integral
+Likelihood (CIL / MCIL / SCIL) method of arXiv 2203.14742.
+
+Python layer = argument marshalling over the C ABI of libcil.so (include/cil.h).
+PyTorch supplies device memory and streams only.  Public calls (same names as the
+C ABI, minus the prefix):
+
+    features(A, B, grid, mask, radii)              -> counts, y, item_status   (Eq. (1)/(2))
+    stats(Y)                                        -> mu, Sigma
+    loglik(mu, Sigma, y_obs, ridge)                 -> out[P,3], item_status    (Eq. (4))
+    synth_loglik(pools, n_ens, N_set, N_tilde, data, k0, grid, mask, radii)     (Alg. 3)
+
+Measures (bit order = concatenation order): L2, LINF, W12SUM, W12,
+W1INF, W1INFSUM (Eqs. (5)-(10)).
+"""
+from __future__ import annotations
+
+import torch
+
+from ._capi import CilError, Grid, check, lib  # noqa: F401  (fails loudly without libcil.so)
+
+L2, LINF, W12SUM, W12, W1INF, W1INFSUM = (1 << i for i in range(6))
+ALL = 0x3F
+MEASURE_NAMES = ["L2", "LINF", "W12SUM", "W12", "W1INF", "W1INFSUM"]
+ENGINE_AUTO, ENGINE_TC_3XBF16, ENGINE_TC_3XTF32, ENGINE_SIMT = 0, 1, 2, 3
+ITEM_OK, ITEM_NONFINITE, ITEM_NOTPD, ITEM_BADRADII, ITEM_OVERFLOW = 0, 1, 2, 4, 8
+
+__all__ = ["features", "stats", "loglik", "synth_loglik", "features_workspace_size",
+           "synth_workspace_size", "n_measures", "Workspace", "CilError"]
+
+
+def n_measures(mask: int) -> int:
+    return bin(mask & ALL).count("1")
+
+
+def _grid(grid) -> Grid:
+    S, H, W = int(grid[0]), int(grid[1]), int(grid[2])
+    h = float(grid[3]) if len(grid) > 3 else 0.0
+    return Grid(S, H, W, h)
+
+
+def _stream(stream=None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def _ptr(t) -> int | None:
+    return t.data_ptr() if t is not None and t.numel() > 0 else None
+
+
+class Workspace:
+    """Grow-only device scratch buffer (the library never allocates)."""
+
+    def __init__(self):
+        self.buf = None
+
+    def get(self, nbytes: int, device) -> torch.Tensor:
+        if self.buf is None or self.buf.numel() < nbytes or self.buf.device != torch.device(device):
+            self.buf = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=device)
+        return self.buf
+
+
+_default_ws = Workspace()
+
+
+def features_workspace_size(P, N, Nt, grid, mask, M, engine=ENGINE_AUTO) -> int:
+    return int(lib.cil_features_workspace_size(P, N, Nt, _grid(grid), mask, M, engine))
+
+
+def synth_workspace_size(P, n_ens, N_set, N_tilde, grid, mask, M, engine=ENGINE_AUTO) -> int:
+    return int(lib.cil_synth_workspace_size(P, n_ens, N_set, N_tilde, _grid(grid), mask, M, engine))
+
+
+def _as_items(X, K):
+    """[N,S,H,W] / [N,K] -> (P=1 view) or [P,N,S,H,W] / [P,N,K] -> P items."""
+    if X.dim() in (2, 4):
+        X = X.unsqueeze(0)
+    P, N = X.shape[0], X.shape[1]
+    if X.shape[2:].numel() != K:
+        raise ValueError(f"pattern size != S*H*W = {K}")
+    return X.reshape(P, N, K)
+
+
+def features(A, B, grid, mask, radii, *, engine=ENGINE_AUTO, want_y=True, stream=None, ws: Workspace | None = None,
+             counts=None, y=None, status=None):
+    """Correlation-integral counts of one or P set pairs (Eq. (1)/(2)).
+
+    A: [N,S,H,W] or [P,N,S,H,W] float32 CUDA; B likewise with Nt rows.
+    radii: [n_meas, M] (shared) or [P, n_meas, M] float64 CUDA, strictly decreasing.
+    Returns counts int64 [P,n_meas,M], y float64 [P,n_meas,M] (or None), item_status int32 [P].
+    """
+    S, H, W = int(grid[0]), int(grid[1]), int(grid[2])
+    K = S * H * W
+    A3, B3 = _as_items(A, K), _as_items(B, K)
+    if A3.dtype != torch.float32 or B3.dtype != torch.float32:
+        raise TypeError("patterns must be float32")
+    if not (A3.is_cuda and B3.is_cuda and radii.is_cuda):
+        raise TypeError("A, B and radii must be CUDA tensors")
+    P, N, Nt = A3.shape[0], A3.shape[1], B3.shape[1]
+    if B3.shape[0] != P:
+        raise ValueError("A and B must have the same number of items")
+    nq = n_measures(mask)
+    radii = radii.to(torch.float64)
+    if radii.dim() == 2:
+        M, rstride = radii.shape[1], 0
+    else:
+        if radii.shape[0] != P:
+            raise ValueError("radii must be [n_meas, M] or [P, n_meas, M]")
+        M, rstride = radii.shape[2], radii.shape[1] * radii.shape[2]
+    if radii.shape[-2] != nq:
+        raise ValueError(f"radii rows {radii.shape[-2]} != n_measures(mask) = {nq}")
+    radii = radii.contiguous()
+    dev = A3.device
+    if counts is None:
+        counts = torch.empty((P, nq, M), dtype=torch.int64, device=dev)
+    if want_y and y is None:
+        y = torch.empty((P, nq, M), dtype=torch.float64, device=dev)
+    if status is None:
+        status = torch.empty((P,), dtype=torch.int32, device=dev)
+    g = _grid(grid)
+    nbytes = lib.cil_features_workspace_size(P, N, Nt, g, mask, M, engine)
+    if nbytes == 0:
+        raise CilError("cil_features_workspace_size: invalid arguments")
+    wbuf = (ws or _default_ws).get(nbytes, dev)
+
+    def stride_ld(X3):
+        if X3.shape[1] == 0:
+            return 0, K
+        if X3.stride(2) != 1:
+            raise ValueError("patterns must be contiguous along S*H*W")
+        return X3.stride(0), X3.stride(1)
+
+    sA, lda = stride_ld(A3)
+    sB, ldb = stride_ld(B3)
+    st = lib.cil_features(P, _ptr(A3), sA, lda, N, _ptr(B3), sB, ldb, Nt, g, mask, radii.data_ptr(), rstride, M,
+                          counts.data_ptr(), y.data_ptr() if want_y else None, status.data_ptr(), engine,
+                          wbuf.data_ptr(), wbuf.numel(), _stream(stream))
+    check(st, "cil_features")
+    return counts, (y if want_y else None), status
+
+
+def stats(Y, *, stream=None):
+    """mu [P,D], Sigma [P,D,D] of Y [P,n,D] (or [n,D]) — PAPER.md:111."""
+    squeeze = Y.dim() == 2
+    Y3 = (Y.unsqueeze(0) if squeeze else Y).to(torch.float64).contiguous()
+    P, n, D = Y3.shape
+    mu = torch.empty((P, D), dtype=torch.float64, device=Y3.device)
+    Sig = torch.empty((P, D, D), dtype=torch.float64, device=Y3.device)
+    check(lib.cil_stats(P, Y3.data_ptr(), n, D, mu.data_ptr(), Sig.data_ptr(), _stream(stream)), "cil_stats")
+    return (mu[0], Sig[0]) if squeeze else (mu, Sig)
+
+
+def loglik(mu, Sigma, y_obs, ridge: float = 0.0, *, stream=None):
+    """Gaussian log-likelihood (Eq. (4)): out[P,3] = (quad, logdet, loglik), item_status [P].
+
+    mu [D] or [P,D]; Sigma [D,D] or [P,D,D]; y_obs [D] or [P,D].
+    """
+    y2 = (y_obs.unsqueeze(0) if y_obs.dim() == 1 else y_obs).to(torch.float64).contiguous()
+    P, D = y2.shape
+    mu = mu.to(torch.float64).contiguous()
+    Sigma = Sigma.to(torch.float64).contiguous()
+    mu_stride = 0 if mu.dim() == 1 else D
+    sig_stride = 0 if Sigma.dim() == 2 else D * D
+    out = torch.empty((P, 3), dtype=torch.float64, device=y2.device)
+    status = torch.empty((P,), dtype=torch.int32, device=y2.device)
+    check(lib.cil_loglik(P, mu.data_ptr(), mu_stride, Sigma.data_ptr(), sig_stride, y2.data_ptr(), D, float(ridge),
+                         out.data_ptr(), status.data_ptr(), _stream(stream)), "cil_loglik")
+    return out, status
+
+
+def synth_loglik(pools, n_ens, N_set, N_tilde, data, k0, grid, mask, radii, ridge: float = 0.0, *,
+                 engine=ENGINE_AUTO, return_Y=False, stream=None, ws: Workspace | None = None, out=None,
+                 status=None):
+    """SCIL (Alg. 3) for P proposals.
+
+    pools [P, N_syn, S,H,W] float32 (N_syn >= n_ens*(N_set+N_tilde)); data [N_set,S,H,W];
+    k0 [P] int32; radii [P, n_meas, M] float64.  Returns out [P,3], item_status [P]
+    (and Y [P, n_ens^2+1, D] if return_Y).
+    """
+    S, H, W = int(grid[0]), int(grid[1]), int(grid[2])
+    K = S * H * W
+    P = pools.shape[0]
+    pools3 = pools.reshape(P, pools.shape[1], -1)
+    data2 = data.reshape(data.shape[0], -1)
+    if pools3.shape[-1] != K or data2.shape[-1] != K or data2.shape[0] != N_set:
+        raise ValueError("pool / data shapes do not match grid and N_set")
+    nq = n_measures(mask)
+    radii = radii.to(torch.float64).contiguous()
+    M = radii.shape[-1]
+    if radii.shape != (P, nq, M):
+        raise ValueError("radii must be [P, n_meas, M]")
+    k0 = k0.to(torch.int32).contiguous()
+    dev = pools.device
+    if out is None:
+        out = torch.empty((P, 3), dtype=torch.float64, device=dev)
+    if status is None:
+        status = torch.empty((P,), dtype=torch.int32, device=dev)
+    Y = torch.empty((P, n_ens * n_ens + 1, nq * M), dtype=torch.float64, device=dev) if return_Y else None
+    g = _grid(grid)
+    nbytes = lib.cil_synth_workspace_size(P, n_ens, N_set, N_tilde, g, mask, M, engine)
+    if nbytes == 0:
+        raise CilError("cil_synth_workspace_size: invalid arguments")
+    wbuf = (ws or _default_ws).get(nbytes, dev)
+    st = lib.cil_synth_loglik(P, pools3.data_ptr(), pools3.stride(0), pools3.stride(1), n_ens, N_set, N_tilde,
+                              data2.data_ptr(), data2.stride(0), k0.data_ptr(), g, mask, radii.data_ptr(), M,
+                              float(ridge), out.data_ptr(), status.data_ptr(), Y.data_ptr() if return_Y else None,
+                              engine, wbuf.data_ptr(), wbuf.numel(), _stream(stream))
+    check(st, "cil_synth_loglik")
+    return (out, status, Y) if return_Y else (out, status)
+
+
+def diag_gram(A, B, grid, engine=ENGINE_TC_3XBF16, *, stream=None):
+    """DIAGNOSTIC: the tensor-core engine's FP32 d^2 and error bound E for every pair
+    of one set pair, shape [N, Nt, 2] (no binning).  Not on the hot path."""
+    S, H, W = int(grid[0]), int(grid[1]), int(grid[2])
+    K = S * H * W
+    A2, B2 = A.reshape(A.shape[0], -1).contiguous(), B.reshape(B.shape[0], -1).contiguous()
+    N, Nt = A2.shape[0], B2.shape[0]
+    g = _grid(grid)
+    out = torch.empty((N, Nt, 2), dtype=torch.float32, device=A2.device)
+    nbytes = lib.cil_features_workspace_size(1, N, Nt, g, L2, 1, engine) + 512
+    wbuf = _default_ws.get(nbytes, A2.device)
+    check(lib.cil_diag_gram(A2.data_ptr(), K, N, B2.data_ptr(), K, Nt, g, engine, out.data_ptr(),
+                            wbuf.data_ptr(), wbuf.numel(), _stream(stream)), "cil_diag_gram")
+    return out
+
+
+def last_launch_count() -> int:
+    """Kernel launches issued by the last library call on this thread."""
+    return int(lib.cil_last_launch_count())

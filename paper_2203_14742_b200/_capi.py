@@ -1,0 +1,66 @@
+"""ctypes binding of libcil.so (include/cil.h) — argument marshalling only.
+
+Every step of the hot path runs in the library's CUDA kernels; this module only
+passes device pointers, sizes and the current CUDA stream.  There is no fallback:
+if libcil.so is missing or cannot be loaded, importing the package fails.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libcil.so")
+
+
+class CilError(RuntimeError):
+    pass
+
+
+class Grid(ctypes.Structure):
+    _fields_ = [("S", ctypes.c_int32), ("H", ctypes.c_int32), ("W", ctypes.c_int32), ("h", ctypes.c_double)]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"libcil.so not built at {LIB_PATH}; run `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = ctypes.CDLL(LIB_PATH)
+    P, i32, i64, u32, f64, sz = (ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32,
+                                 ctypes.c_double, ctypes.c_size_t)
+    lib.cil_features_workspace_size.argtypes = [i32, i64, i64, Grid, u32, i32, ctypes.c_int]
+    lib.cil_features_workspace_size.restype = sz
+    lib.cil_features.argtypes = [i32, P, i64, i64, i64, P, i64, i64, i64, Grid, u32, P, i64, i32, P, P, P,
+                                 ctypes.c_int, P, sz, P]
+    lib.cil_features.restype = ctypes.c_int
+    lib.cil_stats.argtypes = [i32, P, i32, i32, P, P, P]
+    lib.cil_stats.restype = ctypes.c_int
+    lib.cil_loglik.argtypes = [i32, P, i64, P, i64, P, i32, f64, P, P, P]
+    lib.cil_loglik.restype = ctypes.c_int
+    lib.cil_synth_workspace_size.argtypes = [i32, i32, i32, i32, Grid, u32, i32, ctypes.c_int]
+    lib.cil_synth_workspace_size.restype = sz
+    lib.cil_synth_loglik.argtypes = [i32, P, i64, i64, i32, i32, i32, P, i64, P, Grid, u32, P, i32, f64, P, P,
+                                     P, ctypes.c_int, P, sz, P]
+    lib.cil_synth_loglik.restype = ctypes.c_int
+    lib.cil_diag_gram.argtypes = [P, i64, i64, P, i64, i64, Grid, ctypes.c_int, P, P, sz, P]
+    lib.cil_diag_gram.restype = ctypes.c_int
+    lib.cil_status_string.argtypes = [ctypes.c_int]
+    lib.cil_status_string.restype = ctypes.c_char_p
+    lib.cil_last_cuda_error.restype = i32
+    lib.cil_version.restype = i32
+    lib.cil_last_launch_count.restype = i32
+    return lib
+
+
+lib = _load()
+
+EXPORTED = ["cil_features_workspace_size", "cil_features", "cil_stats", "cil_loglik",
+            "cil_synth_workspace_size", "cil_synth_loglik", "cil_status_string", "cil_last_cuda_error",
+            "cil_version", "cil_last_launch_count", "cil_diag_gram"]
+
+
+def check(status: int, what: str):
+    if status != 0:
+        msg = lib.cil_status_string(status).decode()
+        if status == 4:
+            msg += f" (cudaError {lib.cil_last_cuda_error()})"
+        raise CilError(f"{what}: {msg}")

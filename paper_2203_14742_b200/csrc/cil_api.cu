@@ -1,0 +1,384 @@
+// cil_api.cu — the C ABI (include/cil.h): host validation, workspace layout,
+// dispatch of the hot-path kernels on the caller's stream.  No device memory is
+// allocated here and nothing synchronises the device.
+#include <math.h>
+#include <string.h>
+
+#include "cil_internal.cuh"
+
+namespace cil {
+static thread_local int32_t t_last_cuda = 0;
+static thread_local int32_t t_launches = 0;
+void note_launch(int n) { t_launches += n; }
+}  // namespace cil
+
+using namespace cil;
+
+namespace {
+
+struct Slots {
+    int nq = 0;
+    int slot[kMaxMeas] = {0};
+    int q_l2 = -1;
+};
+
+Slots slots_of(uint32_t mask) {
+    Slots s;
+    for (int i = 0; i < kMaxMeas; ++i)
+        if ((mask >> i) & 1u) {
+            if (i == 0) s.q_l2 = s.nq;
+            s.slot[s.nq++] = i;
+        }
+    return s;
+}
+
+double grid_h(const cil_grid& g) {
+    if (g.h > 0) return g.h;
+    return g.W >= 2 ? 1.0 / (double)(g.W - 1) : 1.0;
+}
+
+// Which engines a request uses.
+struct Plan {
+    bool tc = false;        // L2 on tensor cores
+    int split = 1;          // 1 = 3xBF16, 2 = 3xTF32
+    uint32_t simt_mask = 0; // measures on the CUDA-core engine
+    bool do_max = false, do_sum = false;
+    int nreg = 1;
+};
+
+Plan make_plan(uint32_t mask, cil_engine engine, const cil_grid& g) {
+    Plan pl;
+    const bool want_tc = (mask & CIL_L2) && engine != CIL_ENGINE_SIMT;
+    pl.tc = want_tc;
+    pl.split = (engine == CIL_ENGINE_TC_3XTF32) ? 2 : 1;
+    pl.simt_mask = pl.tc ? (mask & ~(uint32_t)CIL_L2) : mask;
+    pl.do_max = pl.simt_mask & (CIL_LINF | CIL_W1INF | CIL_W1INFSUM);
+    pl.do_sum = pl.simt_mask & (CIL_L2 | CIL_W12SUM | CIL_W12);
+    const bool grad = pl.simt_mask & (CIL_W12SUM | CIL_W12 | CIL_W1INF | CIL_W1INFSUM);
+    pl.nreg = grad ? (g.H > 1 ? 3 : 2) : 1;
+    return pl;
+}
+
+// Workspace carve-up (identical in the size query and in the call).
+struct Layout {
+    size_t off_thr, off_thr2, off_hist, off_ctr, off_list, off_center, off_hi, off_lo, off_nrm, off_q4,
+        off_aug, off_Y, off_mu, off_sig, total;
+    int64_t hist_elems = 0;
+    uint32_t list_cap = 0;
+    int64_t Kp = 0;
+    AugGeom geom{};
+};
+
+size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
+
+Layout make_layout(int P, int64_t rowsA, int64_t rowsB, const cil_grid& g, int nq, int M, const Plan& pl,
+                   const SegParams& sp, int64_t nY) {
+    Layout L{};
+    size_t o = 0;
+    auto take = [&](size_t bytes) { size_t r = o; o = al(o + bytes); return r; };
+    const int64_t K = (int64_t)g.S * g.H * g.W;
+    L.off_thr = take(sizeof(double) * (size_t)P * nq * M);
+    L.off_thr2 = take(sizeof(float) * (size_t)P * M);
+    L.hist_elems = (int64_t)P * sp.n_rs * sp.n_cs * nq * (M + 1);
+    L.off_hist = take(sizeof(uint64_t) * (size_t)L.hist_elems);
+    L.off_ctr = take(sizeof(uint32_t) * 2);
+    const int64_t rows = (int64_t)P * (rowsA + rowsB);
+    if (pl.tc) {
+        const double pairs = (double)P * rowsA * rowsB;
+        const double cap = fmin(pairs, pairs / 256.0 + 65536.0);
+        L.list_cap = (uint32_t)fmin(cap, 4.0e9);
+        L.Kp = round_up(K, kTcBK);
+        const size_t esz = pl.split == 2 ? 4 : 2;
+        L.off_list = take(16 * (size_t)L.list_cap);
+        L.off_center = take(sizeof(float) * (size_t)P * L.Kp);
+        L.off_hi = take(esz * (size_t)rows * L.Kp);
+        L.off_lo = take(esz * (size_t)rows * L.Kp);
+        L.off_nrm = take(sizeof(float) * (size_t)rows);
+        L.off_q4 = take(sizeof(float) * (size_t)rows);
+    }
+    if (pl.simt_mask) {
+        L.geom = make_aug_geom(g.S, g.H, g.W, pl.nreg);
+        L.off_aug = take(sizeof(float) * (size_t)rows * L.geom.off[3]);
+    }
+    if (nY > 0) {
+        L.off_Y = take(sizeof(double) * (size_t)nY);
+        const int D = nq * M;
+        L.off_mu = take(sizeof(double) * (size_t)P * D);
+        L.off_sig = take(sizeof(double) * (size_t)P * D * D);
+    }
+    L.total = o + 256;   // slack for base alignment
+    return L;
+}
+
+template <class T>
+T* at(void* base, size_t off) { return reinterpret_cast<T*>(reinterpret_cast<char*>(base) + off); }
+
+bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
+cil_status fail_cuda(cudaError_t e) {
+    t_last_cuda = (int32_t)e;
+    return CIL_ECUDA;
+}
+
+#define CIL_CU(x)                                   \
+    do {                                            \
+        cudaError_t _e = (x);                       \
+        if (_e != cudaSuccess) return fail_cuda(_e); \
+    } while (0)
+
+cil_status check_grid(const cil_grid& g, uint32_t mask) {
+    if (g.S < 1 || g.H < 1 || g.W < 1) return CIL_EINVAL;
+    if (mask == 0 || (mask & ~CIL_ALL_DISTS)) return CIL_EINVAL;
+    if ((mask & (CIL_W12SUM | CIL_W12 | CIL_W1INF | CIL_W1INFSUM)) && g.W < 2) return CIL_EINVAL;
+    if (!(g.h == g.h)) return CIL_EINVAL;
+    return CIL_OK;
+}
+
+// Core: counts for P items of (row panel x col panel), into the workspace histogram.
+cil_status run_engines(int P, const RowSrc& asrc, const RowSrc& bsrc, int64_t rowsA, int64_t rowsB,
+                       const cil_grid& g, uint32_t mask, const Slots& sl, int M, const Plan& pl,
+                       const SegParams& sp, const Layout& L, void* ws, const double* radii,
+                       int64_t radii_stride, int32_t* status, cudaStream_t st, float* diag = nullptr) {
+    const int64_t K = (int64_t)g.S * g.H * g.W;
+    BinParams bp{};
+    bp.nq = sl.nq;
+    bp.M = M;
+    for (int q = 0; q < sl.nq; ++q) bp.slot[q] = sl.slot[q];
+    bp.h = grid_h(g);
+    bp.w = g.H > 1 ? bp.h * bp.h : bp.h;
+    double* thr = at<double>(ws, L.off_thr);
+    float* thr2 = pl.tc ? at<float>(ws, L.off_thr2) : nullptr;
+    uint64_t* hist = at<uint64_t>(ws, L.off_hist);
+    uint32_t* ctr = at<uint32_t>(ws, L.off_ctr);
+    CIL_CU(launch_prep(P, sl.nq, M, radii, radii_stride, bp, thr, thr2, status, hist, L.hist_elems, ctr, st));
+    if (rowsA == 0 || rowsB == 0) return CIL_OK;
+
+    if (pl.simt_mask) {
+        float* aug = at<float>(ws, L.off_aug);
+        float* augB = aug + (size_t)P * rowsA * L.geom.off[3];
+        CIL_CU(launch_pack_aug(P, asrc, rowsA, L.geom, aug, status, st));
+        CIL_CU(launch_pack_aug(P, bsrc, rowsB, L.geom, augB, status, st));
+        SimtArgs a{};
+        a.Aaug = aug; a.Baug = augB;
+        a.rowsA = rowsA; a.rowsB = rowsB; a.Kaug = L.geom.off[3];
+        a.g = L.geom;
+        a.bp = bp;
+        a.sp = sp;
+        a.thr = thr; a.thr_stride = (int64_t)sl.nq * M;
+        a.hist = hist;
+        a.status = status;
+        a.P = P;
+        a.do_max = pl.do_max; a.do_sum = pl.do_sum;
+        // the SIMT engine bins only its own measures (L2 may be on the tensor cores)
+        a.qmask = 0;
+        for (int q = 0; q < sl.nq; ++q)
+            if ((pl.simt_mask >> sl.slot[q]) & 1u) a.qmask |= 1u << q;
+        CIL_CU(launch_simt(a, st));
+    }
+    if (pl.tc) {
+        if (!gram_tc_supported()) return CIL_EUNSUPPORTED;
+        const size_t esz = pl.split == 2 ? 4 : 2;
+        float* center = at<float>(ws, L.off_center);
+        char* hi = at<char>(ws, L.off_hi);
+        char* lo = at<char>(ws, L.off_lo);
+        float* nrm = at<float>(ws, L.off_nrm);
+        float* q4 = at<float>(ws, L.off_q4);
+        const size_t offB = (size_t)P * rowsA;
+        CIL_CU(launch_center(P, bsrc, rowsB < 16 ? rowsB : 16, K, L.Kp, center, st));
+        CIL_CU(launch_pack_tc(P, asrc, rowsA, K, L.Kp, center, pl.split, hi, lo, nrm, q4, status, st));
+        CIL_CU(launch_pack_tc(P, bsrc, rowsB, K, L.Kp, center, pl.split, hi + offB * L.Kp * esz,
+                              lo + offB * L.Kp * esz, nrm + offB, q4 + offB, status, st));
+        TcArgs t{};
+        t.hi = hi; t.lo = lo; t.nrm = nrm; t.q4 = q4;
+        t.rowsA = rowsA; t.rowsB = rowsB; t.Kp = L.Kp; t.K = K;
+        t.P = P; t.split = pl.split;
+        t.thr2 = thr2; t.thr_stride = M; t.M = M;
+        t.q_l2 = sl.q_l2; t.nq = sl.nq;
+        t.sp = sp; t.hist = hist;
+        t.recheck = at<uint4>(ws, L.off_list); t.recheck_ctr = ctr; t.recheck_cap = L.list_cap;
+        t.status = status;
+        // Error bound of the split Gram (DESIGN.md §L2 engine): E = k1 q_a q_b + rel (n_a + n_b)
+        //   k1: 8 sigma of the split residual (2^-16 per product for 3xBF16, 2^-20 for 3xTF32, x2 for d^2)
+        //   rel: FP32 evaluation / threshold rounding / centring + accumulation over K/16 MMA steps
+        t.guard_k1 = (float)(8.0 * (pl.split == 2 ? ldexp(1.0, -18) : ldexp(1.0, -15)));
+        t.guard_rel = (float)(ldexp(1.0, -23) * (8.0 + sqrt((double)K / 16.0)));
+        t.diag = diag;
+        CIL_CU(launch_gram_tc(t, st));
+        if (diag) return CIL_OK;
+        RecheckArgs r{};
+        r.asrc = asrc; r.bsrc = bsrc; r.K = K;
+        r.thr = thr; r.thr_stride = (int64_t)sl.nq * M; r.w = bp.w;
+        r.M = M; r.nq = sl.nq; r.q_l2 = sl.q_l2;
+        r.sp = sp; r.hist = hist;
+        r.list = t.recheck; r.ctr = ctr; r.cap = L.list_cap;
+        r.status = status; r.P = P;
+        CIL_CU(launch_recheck(r, st));
+    }
+    return CIL_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t cil_features_workspace_size(int32_t P, int64_t N, int64_t Nt, cil_grid g, uint32_t dist_mask,
+                                   int32_t M, cil_engine engine) {
+    if (P < 1 || N < 0 || Nt < 0 || M < 1 || check_grid(g, dist_mask) != CIL_OK) return 0;
+    const Slots sl = slots_of(dist_mask);
+    const Plan pl = make_plan(dist_mask, engine, g);
+    SegParams sp{N > 0 ? N : 1, Nt > 0 ? Nt : 1, 1, 1};
+    return make_layout(P, N, Nt, g, sl.nq, M, pl, sp, 0).total;
+}
+
+cil_status cil_features(int32_t P, const float* A, int64_t strideA, int64_t lda, int64_t N, const float* B,
+                        int64_t strideB, int64_t ldb, int64_t Nt, cil_grid g, uint32_t dist_mask,
+                        const double* radii, int64_t radii_stride, int32_t M, uint64_t* counts, double* y,
+                        int32_t* item_status, cil_engine engine, void* ws, size_t ws_bytes, void* stream) {
+    t_launches = 0;
+    if (P < 1 || N < 0 || Nt < 0 || M < 1 || M > kMaxM) return CIL_EINVAL;
+    if (check_grid(g, dist_mask) != CIL_OK) return CIL_EINVAL;
+    if ((int)engine < 0 || (int)engine > 3) return CIL_EINVAL;
+    if (!radii || !counts || !item_status || !ws) return CIL_EINVAL;
+    if ((N > 0 && !A) || (Nt > 0 && !B)) return CIL_EINVAL;
+    if (strideA < 0 || strideB < 0 || radii_stride < 0) return CIL_EINVAL;
+    const int64_t K = (int64_t)g.S * g.H * g.W;
+    if ((N > 0 && lda < K) || (Nt > 0 && ldb < K)) return CIL_EINVAL;
+    if (N > 0 && P > 1 && strideA < (N - 1) * lda + K) return CIL_EINVAL;
+    if (Nt > 0 && P > 1 && strideB < (Nt - 1) * ldb + K) return CIL_EINVAL;
+    if (K % 4 || lda % 4 || ldb % 4 || strideA % 4 || strideB % 4) return CIL_EUNSUPPORTED;
+    if ((A && !aligned16(A)) || (B && !aligned16(B))) return CIL_EUNSUPPORTED;
+    const Slots sl = slots_of(dist_mask);
+    const Plan pl = make_plan(dist_mask, engine, g);
+    SegParams sp{N > 0 ? N : 1, Nt > 0 ? Nt : 1, 1, 1};
+    const Layout L = make_layout(P, N, Nt, g, sl.nq, M, pl, sp, 0);
+    if (ws_bytes < L.total) return CIL_ENOMEM;
+    void* wsa = reinterpret_cast<void*>(((uintptr_t)ws + 255) & ~(uintptr_t)255);
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    RowSrc as{}, bs{};
+    as.base = A; as.stride = strideA; as.ld = lda; as.rows = N; as.mode = MODE_PLAIN;
+    bs.base = B; bs.stride = strideB; bs.ld = ldb; bs.rows = Nt; bs.mode = MODE_PLAIN;
+    cil_status s = run_engines(P, as, bs, N, Nt, g, dist_mask, sl, M, pl, sp, L, wsa, radii, radii_stride,
+                               item_status, st);
+    if (s != CIL_OK) return s;
+    CIL_CU(launch_finalize(P, sl.nq, M, sp, at<uint64_t>(wsa, L.off_hist), counts, y, N, Nt, nullptr,
+                           nullptr, st));
+    return CIL_OK;
+}
+
+cil_status cil_stats(int32_t P, const double* Y, int32_t n, int32_t D, double* mu, double* Sigma,
+                     void* stream) {
+    t_launches = 0;
+    if (P < 1 || n < 2 || D < 1 || !Y || !mu || !Sigma) return CIL_EINVAL;
+    CIL_CU(launch_stats(P, Y, n, D, mu, Sigma, reinterpret_cast<cudaStream_t>(stream)));
+    return CIL_OK;
+}
+
+cil_status cil_loglik(int32_t P, const double* mu, int64_t mu_stride, const double* Sigma, int64_t Sigma_stride,
+                      const double* y_obs, int32_t D, double ridge, double* out, int32_t* item_status,
+                      void* stream) {
+    t_launches = 0;
+    if (P < 1 || D < 1 || !mu || !Sigma || !y_obs || !out || !item_status) return CIL_EINVAL;
+    if (D > kMaxD) return CIL_EUNSUPPORTED;
+    if (mu_stride < 0 || Sigma_stride < 0 || !(ridge >= 0.0)) return CIL_EINVAL;
+    CIL_CU(launch_loglik(P, mu, mu_stride, Sigma, Sigma_stride, y_obs, D, ridge, out, item_status, nullptr,
+                         reinterpret_cast<cudaStream_t>(stream)));
+    return CIL_OK;
+}
+
+size_t cil_synth_workspace_size(int32_t P, int32_t n_ens, int32_t N_set, int32_t N_tilde, cil_grid g,
+                                uint32_t dist_mask, int32_t M, cil_engine engine) {
+    if (P < 1 || n_ens < 2 || N_set < 1 || N_tilde < 1 || M < 1 || check_grid(g, dist_mask) != CIL_OK)
+        return 0;
+    const Slots sl = slots_of(dist_mask);
+    const Plan pl = make_plan(dist_mask, engine, g);
+    const int64_t rowsA = (int64_t)(n_ens + 1) * N_set, rowsB = (int64_t)n_ens * N_tilde;
+    SegParams sp{N_set, N_tilde, n_ens + 1, n_ens};
+    const int64_t nY = (int64_t)P * (n_ens * n_ens + 1) * sl.nq * M;
+    return make_layout(P, rowsA, rowsB, g, sl.nq, M, pl, sp, nY).total;
+}
+
+cil_status cil_synth_loglik(int32_t P, const float* pools, int64_t pool_stride, int64_t ld, int32_t n_ens,
+                            int32_t N_set, int32_t N_tilde, const float* data, int64_t ld_data,
+                            const int32_t* k0, cil_grid g, uint32_t dist_mask, const double* radii, int32_t M,
+                            double ridge, double* out, int32_t* item_status, double* Y_out, cil_engine engine,
+                            void* ws, size_t ws_bytes, void* stream) {
+    t_launches = 0;
+    if (P < 1 || n_ens < 2 || N_set < 1 || N_tilde < 1 || M < 1 || M > kMaxM) return CIL_EINVAL;
+    if (check_grid(g, dist_mask) != CIL_OK) return CIL_EINVAL;
+    if ((int)engine < 0 || (int)engine > 3) return CIL_EINVAL;
+    if (!pools || !data || !k0 || !radii || !out || !item_status || !ws) return CIL_EINVAL;
+    if (!(ridge >= 0.0)) return CIL_EINVAL;
+    const int64_t K = (int64_t)g.S * g.H * g.W;
+    const int64_t Nsyn = (int64_t)n_ens * (N_set + N_tilde);
+    if (ld < K || ld_data < K) return CIL_EINVAL;
+    if (P > 1 && pool_stride < (Nsyn - 1) * ld + K) return CIL_EINVAL;
+    if (K % 4 || ld % 4 || ld_data % 4 || pool_stride % 4) return CIL_EUNSUPPORTED;
+    if (!aligned16(pools) || !aligned16(data)) return CIL_EUNSUPPORTED;
+    const Slots sl = slots_of(dist_mask);
+    if (sl.nq * M > kMaxD) return CIL_EUNSUPPORTED;
+    const Plan pl = make_plan(dist_mask, engine, g);
+    const int64_t rowsA = (int64_t)(n_ens + 1) * N_set, rowsB = (int64_t)n_ens * N_tilde;
+    SegParams sp{N_set, N_tilde, n_ens + 1, n_ens};
+    const int nv = n_ens * n_ens;
+    const int64_t nY = (int64_t)P * (nv + 1) * sl.nq * M;
+    const Layout L = make_layout(P, rowsA, rowsB, g, sl.nq, M, pl, sp, nY);
+    if (ws_bytes < L.total) return CIL_ENOMEM;
+    void* wsa = reinterpret_cast<void*>(((uintptr_t)ws + 255) & ~(uintptr_t)255);
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    RowSrc as{}, bs{};
+    as.base = pools; as.stride = pool_stride; as.ld = ld; as.rows = rowsA; as.mode = MODE_SYN_ROW;
+    as.n_ens = n_ens; as.N_set = N_set; as.N_tilde = N_tilde; as.data = data; as.ld_data = ld_data;
+    bs = as;
+    bs.rows = rowsB; bs.mode = MODE_SYN_COL;
+    cil_status s = run_engines(P, as, bs, rowsA, rowsB, g, dist_mask, sl, M, pl, sp, L, wsa, radii,
+                               (int64_t)sl.nq * M, item_status, st);
+    if (s != CIL_OK) return s;
+    double* Y = Y_out ? Y_out : at<double>(wsa, L.off_Y);
+    CIL_CU(launch_synth_tail(P, n_ens, sl.nq, M, sp, at<uint64_t>(wsa, L.off_hist), N_set, N_tilde, k0, ridge,
+                             out, item_status, Y, at<double>(wsa, L.off_mu), at<double>(wsa, L.off_sig), st));
+    return CIL_OK;
+}
+
+cil_status cil_diag_gram(const float* A, int64_t lda, int64_t N, const float* B, int64_t ldb, int64_t Nt,
+                         cil_grid g, cil_engine engine, float* d2E, void* ws, size_t ws_bytes, void* stream) {
+    t_launches = 0;
+    if (N < 1 || Nt < 1 || !A || !B || !d2E || !ws) return CIL_EINVAL;
+    if (engine != CIL_ENGINE_TC_3XBF16 && engine != CIL_ENGINE_TC_3XTF32) return CIL_EINVAL;
+    if (check_grid(g, CIL_L2) != CIL_OK) return CIL_EINVAL;
+    const int64_t K = (int64_t)g.S * g.H * g.W;
+    if (lda < K || ldb < K) return CIL_EINVAL;
+    if (K % 4 || lda % 4 || ldb % 4 || !aligned16(A) || !aligned16(B)) return CIL_EUNSUPPORTED;
+    const Slots sl = slots_of(CIL_L2);
+    const Plan pl = make_plan(CIL_L2, engine, g);
+    SegParams sp{N, Nt, 1, 1};
+    const Layout L = make_layout(1, N, Nt, g, sl.nq, 1, pl, sp, 0);
+    if (ws_bytes < L.total + 512) return CIL_ENOMEM;
+    void* wsa = reinterpret_cast<void*>(((uintptr_t)ws + 255) & ~(uintptr_t)255);
+    // a single dummy radius (the diagnostic path does not bin); it lives past the layout
+    double* r = at<double>(wsa, L.total);
+    const double one = 1.0;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    CIL_CU(cudaMemcpyAsync(r, &one, sizeof(double), cudaMemcpyHostToDevice, st));
+    int32_t* status = reinterpret_cast<int32_t*>(r + 1);
+    RowSrc as{}, bs{};
+    as.base = A; as.ld = lda; as.rows = N; as.mode = MODE_PLAIN;
+    bs.base = B; bs.ld = ldb; bs.rows = Nt; bs.mode = MODE_PLAIN;
+    return run_engines(1, as, bs, N, Nt, g, CIL_L2, sl, 1, pl, sp, L, wsa, r, 0, status, st, d2E);
+}
+
+const char* cil_status_string(cil_status s) {
+    switch (s) {
+        case CIL_OK: return "CIL_OK";
+        case CIL_EINVAL: return "CIL_EINVAL: invalid argument";
+        case CIL_EUNSUPPORTED: return "CIL_EUNSUPPORTED: valid request not supported by this build";
+        case CIL_ENOMEM: return "CIL_ENOMEM: workspace too small";
+        case CIL_ECUDA: return "CIL_ECUDA: CUDA launch failed (see cil_last_cuda_error)";
+    }
+    return "unknown cil_status";
+}
+
+int32_t cil_last_cuda_error(void) { return t_last_cuda; }
+int32_t cil_version(void) { return 100; }
+int32_t cil_last_launch_count(void) { return t_launches; }
+
+}  // extern "C"

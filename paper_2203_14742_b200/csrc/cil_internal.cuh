@@ -1,0 +1,185 @@
+// cil_internal.cuh — shared device/host definitions of libcil (CUDA path only).
+// Nothing here is shared with oracle/: the oracle is an independent program.
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+#include "../../include/cil.h"
+
+namespace cil {
+
+constexpr int kMaxM = 64;        // radii per measure
+constexpr int kMaxMeas = 6;
+constexpr int kMaxD = 192;       // n_meas * M for loglik (packed Cholesky factor in smem)
+constexpr int kSimtBK = 32;      // SIMT k-chunk (floats); region padding unit
+constexpr int kTcBK = 64;        // bf16 elements per TMA box row (128 B, SWIZZLE_128B)
+
+// Row sources: how panel row r of item p maps to a pattern in caller memory.
+//  MODE_PLAIN : base + p*stride + r*ld
+//  MODE_SYN_ROW: r <  n_ens*N_set : pool + p*stride + (k*N + i)*ld,  k = r / N_set, i = r % N_set
+//                r >= n_ens*N_set : data + (r - n_ens*N_set)*ld_data   (s_data, Eq. (13))
+//  MODE_SYN_COL: pool + p*stride + (l*N + N_set + j)*ld,  l = r / N_tilde, j = r % N_tilde
+enum RowMode : int { MODE_PLAIN = 0, MODE_SYN_ROW = 1, MODE_SYN_COL = 2 };
+
+struct RowSrc {
+    const float* base;
+    int64_t stride;   // per item (floats)
+    int64_t ld;       // per row (floats)
+    int64_t rows;     // rows per item in the panel
+    int mode;
+    // synth parameters
+    int n_ens, N_set, N_tilde;
+    const float* data;
+    int64_t ld_data;
+};
+
+__host__ __device__ inline const float* row_ptr(const RowSrc& s, int64_t p, int64_t r) {
+    if (s.mode == MODE_PLAIN) return s.base + p * s.stride + r * s.ld;
+    const int64_t N = (int64_t)s.N_set + s.N_tilde;
+    if (s.mode == MODE_SYN_ROW) {
+        const int64_t nr = (int64_t)s.n_ens * s.N_set;
+        if (r >= nr) return s.data + (r - nr) * s.ld_data;
+        const int64_t k = r / s.N_set, i = r % s.N_set;
+        return s.base + p * s.stride + (k * N + i) * s.ld;
+    }
+    const int64_t l = r / s.N_tilde, j = r % s.N_tilde;
+    return s.base + p * s.stride + (l * N + s.N_set + j) * s.ld;
+}
+
+// Geometry of the augmented SIMT operand: [value | D_x | D_y] regions, each
+// zero-padded to a multiple of kSimtBK floats.
+struct AugGeom {
+    int S, H, W;
+    int64_t K;          // S*H*W
+    int64_t Kx, Ky;     // S*H*(W-1), S*(H-1)*W
+    int64_t off[4];     // region starts (padded); off[3] = total row length
+    int nreg;           // regions materialised (1 = value only, 2 = +D_x, 3 = +D_y)
+};
+
+inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+inline AugGeom make_aug_geom(int S, int H, int W, int nreg) {
+    AugGeom a{};
+    a.S = S; a.H = H; a.W = W;
+    a.K = (int64_t)S * H * W;
+    a.Kx = (W > 1) ? (int64_t)S * H * (W - 1) : 0;
+    a.Ky = (H > 1) ? (int64_t)S * (H - 1) * W : 0;
+    if (nreg >= 3 && a.Ky == 0) nreg = 2;
+    a.nreg = nreg;
+    a.off[0] = 0;
+    a.off[1] = round_up(a.K, kSimtBK);
+    a.off[2] = a.off[1] + (nreg >= 2 ? round_up(a.Kx, kSimtBK) : 0);
+    a.off[3] = a.off[2] + (nreg >= 3 ? round_up(a.Ky, kSimtBK) : 0);
+    return a;
+}
+
+// Everything the engines need to bin one measure slot.
+struct BinParams {
+    int nq;                 // measures selected
+    int M;
+    int slot[kMaxMeas];     // measure id (0..5) of slot q
+    double h;               // grid spacing
+    double w;               // quadrature weight h^dim
+};
+
+// Segment layout of the count histogram hist[item][rs][cs][q][M+1] (uint64).
+struct SegParams {
+    int64_t row_seg, col_seg;   // rows (cols) per segment
+    int n_rs, n_cs;             // segments per item
+};
+
+__host__ __device__ inline int64_t hist_index(const SegParams& sp, int nq, int M, int64_t p,
+                                              int64_t rs, int64_t cs, int q, int b) {
+    return ((((p * sp.n_rs + rs) * sp.n_cs + cs) * nq + q) * (M + 1)) + b;
+}
+
+// Launch bookkeeping (per host thread).
+void note_launch(int n = 1);
+
+}  // namespace cil
+
+// ---- launchers implemented in the .cu files ----
+namespace cil {
+
+// pack.cu
+cudaError_t launch_prep(int P, int nq, int M, const double* radii, int64_t radii_stride,
+                        const BinParams& bp, double* thr, float* thr2_l2, int32_t* status,
+                        uint64_t* hist, int64_t hist_elems, uint32_t* recheck_ctr, cudaStream_t st);
+cudaError_t launch_pack_aug(int P, const RowSrc& src, int64_t rows, const AugGeom& g,
+                            float* out, int32_t* status, cudaStream_t st);
+cudaError_t launch_center(int P, const RowSrc& colsrc, int64_t nrows_center, int64_t K, int64_t Kp,
+                          float* center, cudaStream_t st);
+cudaError_t launch_pack_tc(int P, const RowSrc& src, int64_t rows, int64_t K, int64_t Kp,
+                           const float* center, int split, void* hi, void* lo, float* nrm, float* q4,
+                           int32_t* status, cudaStream_t st);
+
+// simt_tile.cu
+struct SimtArgs {
+    const float* Aaug; const float* Baug;    // [P][rowsA][Kaug], [P][rowsB][Kaug]
+    int64_t rowsA, rowsB, Kaug;
+    AugGeom g;
+    BinParams bp;
+    SegParams sp;
+    const double* thr;                        // [P or 1][nq][M]
+    int64_t thr_stride;
+    uint64_t* hist;
+    const int32_t* status;                    // skip items flagged BADRADII
+    int P;
+    bool do_max, do_sum;
+    uint32_t qmask;                           // slots binned by this engine
+};
+cudaError_t launch_simt(const SimtArgs& a, cudaStream_t st);
+
+// gram_tc.cu
+struct TcArgs {
+    const void* hi; const void* lo;     // stacked [P*rowsA + P*rowsB][Kp] (A panels then B panels)
+    const float* nrm; const float* q4;  // stacked like hi
+    int64_t rowsA, rowsB, Kp, K;
+    int P;
+    int split;                          // 1 = 3xBF16, 2 = 3xTF32
+    const float* thr2;                  // [P or 1][M] L2 thresholds R^2/w (FP32)
+    int64_t thr_stride;
+    int M;
+    int q_l2;                           // slot of L2 in the hist
+    int nq;
+    SegParams sp;
+    uint64_t* hist;
+    uint4* recheck; uint32_t* recheck_ctr; uint32_t recheck_cap;
+    const int32_t* status;
+    float guard_k1, guard_rel;
+    float* diag;                        // diagnostics only (see cil_diag_gram)
+};
+cudaError_t launch_gram_tc(const TcArgs& a, cudaStream_t st);
+bool gram_tc_supported();
+
+// recheck.cu
+struct RecheckArgs {
+    RowSrc asrc, bsrc;
+    int64_t K;
+    const double* thr;   // FP64 thresholds of slot q_l2 are thr[p*thr_stride + q_l2*M + m] (R)
+    int64_t thr_stride;
+    double w;
+    int M, nq, q_l2;
+    SegParams sp;
+    uint64_t* hist;
+    const uint4* list; const uint32_t* ctr; uint32_t cap;
+    int32_t* status;
+    int P;
+};
+cudaError_t launch_recheck(const RecheckArgs& a, cudaStream_t st);
+
+// stats.cu
+cudaError_t launch_finalize(int P, int nq, int M, const SegParams& sp, const uint64_t* hist,
+                            uint64_t* counts, double* y, int64_t pairs_per_seg_rows,
+                            int64_t pairs_per_seg_cols, const int32_t* status_in,
+                            int32_t* status_out, cudaStream_t st);
+cudaError_t launch_stats(int P, const double* Y, int n, int D, double* mu, double* Sigma,
+                         cudaStream_t st);
+cudaError_t launch_loglik(int P, const double* mu, int64_t mu_stride, const double* Sigma,
+                          int64_t Sigma_stride, const double* y, int D, double ridge, double* out,
+                          int32_t* status, const int32_t* status_in, cudaStream_t st);
+cudaError_t launch_synth_tail(int P, int n_ens, int nq, int M, const SegParams& sp, const uint64_t* hist,
+                              int64_t N_set, int64_t N_tilde, const int32_t* k0, double ridge, double* out,
+                              int32_t* status, double* Y, double* mu, double* Sigma, cudaStream_t st);
+}  // namespace cil

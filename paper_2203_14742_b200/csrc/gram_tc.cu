@@ -1,0 +1,435 @@
+// gram_tc.cu — step a2 of the hot path: L2 distances (Eq. (5)) of all
+// pairs through the Gram identity d^2 = |a~|^2 + |b~|^2 - 2 a~.b~ on the 5th-generation
+// tensor cores, fused with the radius binning of Eq. (1): the
+// N x Nt distance matrix never leaves the SM.
+//
+// Split precision: a~ = hi + lo (3xBF16: bf16 pair; 3xTF32: tf32 pair) and
+//   g = hi_a.hi_b + hi_a.lo_b + lo_a.hi_b        (3 tcgen05.mma per k-step, one FP32 TMEM accumulator)
+// Error control: every pair with |d^2 - T_m| <= E(i,j) for some threshold T_m = R_m^2/w,
+//   E = k1 * q_a * q_b + rel * (n_a + n_b),   q = (sum x~^4)^(1/4),
+// is NOT binned here; it is appended to a re-check list and binned exactly (FP64) by
+// recheck.cu.  All other pairs are classified correctly whenever the Gram error is
+// below E (DESIGN.md §"L2 engine" derives k1, rel and tests their margin).
+//
+// Kernel anatomy (persistent, one CTA per SM, 192 threads):
+//   warp 0      TMA producer: A_hi, A_lo (128 x 128 B) and B_hi, B_lo (BN x 128 B) per stage,
+//               SWIZZLE_128B, mbarrier complete_tx
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=BN, cta_group::1),
+//               tcgen05.commit -> smem-slot release and accumulator-ready barriers
+//   warps 2..5  epilogue: tcgen05.ld 32x32b.x32 -> d^2 -> per-thread cumulative counters,
+//               ambiguous pairs -> re-check list; double-buffered TMEM accumulator so the
+//               epilogue of tile t overlaps the MMAs of tile t+1.
+#include <cuda.h>
+
+#include "cil_internal.cuh"
+
+namespace cil {
+
+namespace tc {
+constexpr int BM = 128;
+constexpr int BN = 256;
+constexpr int STAGES = 2;
+constexpr int ROW_BYTES = 128;                       // K bytes per stage row (one SW128 atom row)
+constexpr int A_BYTES = BM * ROW_BYTES;              // 16 KB
+constexpr int B_BYTES = BN * ROW_BYTES;              // 32 KB
+constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
+constexpr int NTHREADS = 192;
+constexpr int TMEM_COLS = 2 * BN;                    // double-buffered accumulator
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 1024 /*barriers, norms*/ + 2 * BN * 4;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t n) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(n));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            smem_u32(dst)),
+        "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+
+// K-major, SWIZZLE_128B shared-memory matrix descriptor (sm_100 "version 1" format):
+// start>>4 [0,14), LBO>>4 [16,30) (unused for swizzled K-major), SBO>>4 [32,46) = 1024 B
+// between 8-row core groups, version 1 at bit 46, layout SWIZZLE_128B (2) at [61,64).
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
+    return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+           ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+// Instruction descriptor: F32 accumulate, A/B format (BF16 = 1, TF32 = 2), K-major, N>>3, M>>4.
+__host__ __device__ constexpr uint32_t idesc(int fmt, int M, int N) {
+    return (1u << 4) | ((uint32_t)fmt << 7) | ((uint32_t)fmt << 10) | ((uint32_t)(N >> 3) << 17) |
+           ((uint32_t)(M >> 4) << 24);
+}
+__device__ __forceinline__ void mma(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc, int kind_tf32) {
+    if (kind_tf32)
+        asm volatile(
+            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+            "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+            "l"(a), "l"(b), "r"(id), "r"(acc));
+    else
+        asm volatile(
+            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+            "l"(a), "l"(b), "r"(id), "r"(acc));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+          "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+          "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+struct TcParams {
+    int64_t rowsA, rowsB;     // rows per item of the A / B panel
+    int P;
+    int n_kb;                 // k-blocks of 128 bytes
+    int tiles_m, tiles_n;     // per item
+    int split;                // 1 = bf16, 2 = tf32
+    const float* nrm;         // stacked [P*rowsA + P*rowsB]
+    const float* q4;
+    const float* thr2;        // [P][M]
+    int64_t thr_stride;
+    int M, nq, q_l2;
+    SegParams sp;
+    unsigned long long* hist;
+    uint4* list; uint32_t* ctr; uint32_t cap;
+    float k1, rel;
+    float* diag;              // diagnostics: [rowsA][rowsB][2] = (d2, E) of item 0, no binning
+};
+
+template <int MAXM>
+__global__ void __launch_bounds__(NTHREADS, 1)
+k_gram_tc(const __grid_constant__ CUtensorMap mAhi, const __grid_constant__ CUtensorMap mAlo,
+          const __grid_constant__ CUtensorMap mBhi, const __grid_constant__ CUtensorMap mBlo, TcParams prm) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = reinterpret_cast<unsigned char*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    unsigned char* stages = smem;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tfull = empty + STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    float* s_nb = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 1024);
+    float* s_qb = s_nb + BN;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int tiles_per_item = prm.tiles_m * prm.tiles_n;
+    const int total_tiles = prm.P * tiles_per_item;
+
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+        for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 4); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&mAhi) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&mAlo) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&mBhi) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&mBlo) : "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    const int kind_tf32 = prm.split == 2;
+    const int bkE = kind_tf32 ? 32 : 64;    // elements per 128-byte row
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+                const int p = t / tiles_per_item, r = t % tiles_per_item;
+                const int mt = r / prm.tiles_n, nt = r % prm.tiles_n;
+                const int ya = (int)(p * prm.rowsA + (int64_t)mt * BM);
+                const int yb = (int)((int64_t)prm.P * prm.rowsA + p * prm.rowsB + (int64_t)nt * BN);
+                for (int kb = 0; kb < prm.n_kb; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    unsigned char* st = stages + stage * STAGE_BYTES;
+                    mbar_expect_tx(&full[stage], STAGE_BYTES);
+                    const int x = kb * bkE;
+                    tma_load_2d(st, &mAhi, &full[stage], x, ya);
+                    tma_load_2d(st + A_BYTES, &mAlo, &full[stage], x, ya);
+                    tma_load_2d(st + 2 * A_BYTES, &mBhi, &full[stage], x, yb);
+                    tma_load_2d(st + 2 * A_BYTES + B_BYTES, &mBlo, &full[stage], x, yb);
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            const uint32_t id = idesc(kind_tf32 ? 2 : 1, BM, BN);
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+                mbar_wait(&tempty[acc], acc_phase ^ 1);
+                fence_after();
+                const uint32_t d = tmem_base + (uint32_t)(acc * BN);
+                for (int kb = 0; kb < prm.n_kb; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    fence_after();
+                    const uint32_t s0 = smem_u32(stages + stage * STAGE_BYTES);
+                    const uint64_t ahi = sdesc(s0), alo = sdesc(s0 + A_BYTES);
+                    const uint64_t bhi = sdesc(s0 + 2 * A_BYTES), blo = sdesc(s0 + 2 * A_BYTES + B_BYTES);
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {           // 4 x 32 bytes of K per 128-byte row
+                        const uint64_t adv = (uint64_t)(k * 2);  // +32 B in the start-address field (>>4)
+                        mma(d, ahi + adv, bhi + adv, id, (kb | k) != 0, kind_tf32);
+                        mma(d, ahi + adv, blo + adv, id, 1u, kind_tf32);
+                        mma(d, alo + adv, bhi + adv, id, 1u, kind_tf32);
+                    }
+                    mma_commit(&empty[stage]);
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+                mma_commit(&tfull[acc]);
+                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+            }
+        }
+    } else {
+        // ------------------------------------------------------------ epilogue
+        const int quarter = warp & 3;
+        const int et = threadIdx.x - 64;              // 0..127
+        const int M = prm.M;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+            const int p = t / tiles_per_item, r = t % tiles_per_item;
+            const int mt = r / prm.tiles_n, nt = r % prm.tiles_n;
+            const int64_t col0 = (int64_t)nt * BN;
+            const int64_t browbase = (int64_t)prm.P * prm.rowsA + (int64_t)p * prm.rowsB;
+            named_bar(1, 128);
+            for (int j = et; j < BN; j += 128) {
+                const int64_t c = col0 + j;
+                const bool ok = c < prm.rowsB;
+                s_nb[j] = ok ? prm.nrm[browbase + c] : 0.f;
+                s_qb[j] = ok ? prm.q4[browbase + c] : 0.f;
+            }
+            named_bar(1, 128);
+            float T[MAXM];
+#pragma unroll
+            for (int m = 0; m < MAXM; ++m) T[m] = (m < M) ? __ldg(&prm.thr2[(int64_t)p * prm.thr_stride + m]) : -INFINITY;
+            const int64_t row = (int64_t)mt * BM + quarter * 32 + lane;
+            const bool row_ok = row < prm.rowsA;
+            const int64_t arow = (int64_t)p * prm.rowsA + (row_ok ? row : 0);
+            const float na = row_ok ? __ldg(&prm.nrm[arow]) : 0.f;
+            const float k1qa = row_ok ? prm.k1 * __ldg(&prm.q4[arow]) : 0.f;
+            const int64_t rs = row_ok ? row / prm.sp.row_seg : 0;
+            uint32_t cnt[MAXM];
+#pragma unroll
+            for (int m = 0; m < MAXM; ++m) cnt[m] = 0;
+
+            auto flush = [&](int64_t cs) {
+                // all lanes share cs; rows of one warp may span two row segments
+                const int64_t rs0 = __shfl_sync(0xffffffffu, rs, 0);
+                const bool uniform = __all_sync(0xffffffffu, rs == rs0 || !row_ok);
+                if (uniform) {
+                    uint32_t prev = 0;
+#pragma unroll
+                    for (int m = MAXM - 1; m >= 0; --m) {
+                        if (m >= M) continue;
+                        const uint32_t tot = __reduce_add_sync(0xffffffffu, cnt[m]);
+                        if (lane == 0 && tot != prev)
+                            atomicAdd(&prm.hist[hist_index(prm.sp, prm.nq, M, p, rs0, cs, prm.q_l2, m + 1)],
+                                      (unsigned long long)(tot - prev));
+                        prev = tot;
+                        cnt[m] = 0;
+                    }
+                } else {
+                    uint32_t prev = 0;
+#pragma unroll
+                    for (int m = MAXM - 1; m >= 0; --m) {
+                        if (m >= M) continue;
+                        if (row_ok && cnt[m] != prev)
+                            atomicAdd(&prm.hist[hist_index(prm.sp, prm.nq, M, p, rs, cs, prm.q_l2, m + 1)],
+                                      (unsigned long long)(cnt[m] - prev));
+                        prev = cnt[m];
+                        cnt[m] = 0;
+                    }
+                }
+            };
+
+            mbar_wait(&tfull[acc], acc_phase);
+            fence_after();
+            int64_t cur_cs = col0 / prm.sp.col_seg;
+            const uint32_t taddr0 = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN);
+#pragma unroll 1
+            for (int ch = 0; ch < BN / 32; ++ch) {
+                uint32_t v[32];
+                tmem_ld32(taddr0 + ch * 32, v);
+                if (col0 + ch * 32 >= prm.rowsB) break;    // warp-uniform
+#pragma unroll 4
+                for (int jj = 0; jj < 32; ++jj) {
+                    const int j = ch * 32 + jj;
+                    const int64_t c = col0 + j;
+                    if (c >= prm.rowsB) break;             // warp-uniform
+                    const int64_t cs = c / prm.sp.col_seg;
+                    if (cs != cur_cs) { flush(cur_cs); cur_cs = cs; }
+                    if (!row_ok) continue;
+                    const float g = __uint_as_float(v[jj]);
+                    const float nb = s_nb[j];
+                    const float sab = na + nb;
+                    const float d2 = fmaf(-2.f, g, sab);
+                    const float E = fmaf(k1qa, s_qb[j], prm.rel * sab);
+                    if (prm.diag) {
+                        if (p == 0) {
+                            prm.diag[(row * prm.rowsB + c) * 2] = d2;
+                            prm.diag[(row * prm.rowsB + c) * 2 + 1] = E;
+                        }
+                        continue;
+                    }
+                    const float hi = d2 + E, lo = d2 - E;
+                    uint32_t blo = 0;
+#pragma unroll
+                    for (int m = 0; m < MAXM; ++m) {
+                        const uint32_t c1 = hi < T[m] ? 1u : 0u;
+                        cnt[m] += c1;
+                        blo += c1;
+                    }
+                    // ambiguous iff the next threshold below the certain prefix is within reach
+                    float Tn = -INFINITY;
+#pragma unroll
+                    for (int m = 0; m < MAXM; ++m) Tn = (m == (int)blo) ? T[m] : Tn;
+                    if (lo < Tn) {
+                        const uint32_t idx = atomicAdd(prm.ctr, 1u);
+                        if (idx < prm.cap) prm.list[idx] = make_uint4((uint32_t)p, (uint32_t)row, (uint32_t)c, blo);
+                    }
+                }
+            }
+            fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+            flush(cur_cs);
+            if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        }
+    }
+    __syncthreads();
+    if (warp == 1) {
+        fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
+    }
+}
+}  // namespace tc
+
+// ------------------------------------------------------------------ host side
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled get_encode() {
+    static PFN_encodeTiled fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_encodeTiled>(p);
+    }
+    return fn;
+}
+
+bool gram_tc_supported() { return true; }
+
+static bool make_map(CUtensorMap* m, const void* base, int split, int64_t rows, int64_t Kp, int box_rows) {
+    PFN_encodeTiled enc = get_encode();
+    if (!enc) return false;
+    const size_t esz = split == 2 ? 4 : 2;
+    cuuint64_t dims[2] = {(cuuint64_t)Kp, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)(Kp * esz)};
+    cuuint32_t box[2] = {(cuuint32_t)(128 / esz), (cuuint32_t)box_rows};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = enc(m, split == 2 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                     const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+template <int MAXM>
+static cudaError_t launch_t(const TcArgs& a, const tc::TcParams& prm, const CUtensorMap* maps, int grid,
+                            cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(tc::k_gram_tc<MAXM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             tc::SMEM_BYTES);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    tc::k_gram_tc<MAXM><<<grid, tc::NTHREADS, tc::SMEM_BYTES, st>>>(maps[0], maps[1], maps[2], maps[3], prm);
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gram_tc(const TcArgs& a, cudaStream_t st) {
+    if (a.rowsA == 0 || a.rowsB == 0) return cudaSuccess;
+    const int64_t rows = (int64_t)a.P * (a.rowsA + a.rowsB);
+    if (rows >= (1ll << 31)) return cudaErrorInvalidValue;
+    const size_t esz = a.split == 2 ? 4 : 2;
+    const char* hi = static_cast<const char*>(a.hi);
+    const char* lo = static_cast<const char*>(a.lo);
+    CUtensorMap maps[4];
+    if (!make_map(&maps[0], hi, a.split, rows, a.Kp, tc::BM) || !make_map(&maps[1], lo, a.split, rows, a.Kp, tc::BM) ||
+        !make_map(&maps[2], hi, a.split, rows, a.Kp, tc::BN) || !make_map(&maps[3], lo, a.split, rows, a.Kp, tc::BN))
+        return cudaErrorInvalidValue;
+    (void)esz;
+    tc::TcParams prm{};
+    prm.rowsA = a.rowsA; prm.rowsB = a.rowsB; prm.P = a.P;
+    prm.n_kb = (int)((a.Kp * (int64_t)esz) / tc::ROW_BYTES);
+    prm.tiles_m = (int)((a.rowsA + tc::BM - 1) / tc::BM);
+    prm.tiles_n = (int)((a.rowsB + tc::BN - 1) / tc::BN);
+    prm.split = a.split;
+    prm.nrm = a.nrm; prm.q4 = a.q4;
+    prm.thr2 = a.thr2; prm.thr_stride = a.thr_stride;
+    prm.M = a.M; prm.nq = a.nq; prm.q_l2 = a.q_l2;
+    prm.sp = a.sp;
+    prm.hist = reinterpret_cast<unsigned long long*>(a.hist);
+    prm.list = a.recheck; prm.ctr = a.recheck_ctr; prm.cap = a.recheck_cap;
+    prm.k1 = a.guard_k1; prm.rel = a.guard_rel;
+    prm.diag = a.diag;
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t tiles = (int64_t)a.P * prm.tiles_m * prm.tiles_n;
+    const int grid = (int)(tiles < nsm ? tiles : nsm);
+    if (a.M <= 16) return launch_t<16>(a, prm, maps, grid, st);
+    if (a.M <= 32) return launch_t<32>(a, prm, maps, grid, st);
+    return launch_t<64>(a, prm, maps, grid, st);
+}
+
+}  // namespace cil

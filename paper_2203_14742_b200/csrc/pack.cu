@@ -1,0 +1,233 @@
+// pack.cu — step a1 of the hot path: radii validation, centring,
+// split-precision operands for the tensor-core Gram, augmented FP32 operands
+// [value | D_x | D_y] for the CUDA-core engine.  HBM-bound, one pass per row.
+//
+// Definitions followed:
+//  - distances of pattern differences u = a - b (Eq. (1));
+//  - forward difference D_h f = f(x_{j+1}) - f(x_j), taken along
+//    W (D_x) and H (D_y) inside each species; the last node is omitted (Neumann
+//    ghost; reading R3).  The 1/h factor is applied in
+//    the engines' epilogues in FP64, so the fields here are plain differences.
+#include "cil_internal.cuh"
+
+namespace cil {
+
+// -------------------------------------------------------------------------- prep
+// Validates radii (> 0, strictly decreasing) and writes per-item thresholds:
+//   thr[p][q][m]  = R (FP64, compared with the measure value)
+//   thr2[p][m]    = R^2 / w (FP32), the L2 threshold on the unweighted sum of squares
+__global__ void k_prep(int P, int nq, int M, const double* __restrict__ radii, int64_t radii_stride,
+                       BinParams bp, double* __restrict__ thr, float* __restrict__ thr2_l2,
+                       int32_t* __restrict__ status) {
+    const int p = blockIdx.x;
+    const double* R = radii + (int64_t)p * radii_stride;
+    __shared__ int bad;
+    if (threadIdx.x == 0) bad = 0;
+    __syncthreads();
+    for (int t = threadIdx.x; t < nq * M; t += blockDim.x) {
+        const int m = t % M;
+        const double r = R[t];
+        const bool ok = (r > 0.0) && isfinite(r) && (m == 0 || R[t - 1] > r);
+        if (!ok) atomicOr(&bad, 1);
+        thr[(int64_t)p * nq * M + t] = r;
+    }
+    if (thr2_l2 != nullptr) {
+        int ql2 = -1;
+        for (int q = 0; q < nq; ++q)
+            if (bp.slot[q] == 0) ql2 = q;
+        if (ql2 >= 0)
+            for (int m = threadIdx.x; m < M; m += blockDim.x) {
+                const double r = R[ql2 * M + m];
+                thr2_l2[(int64_t)p * M + m] = (float)(r * r / bp.w);
+            }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) status[p] = bad ? CIL_ITEM_BADRADII : 0;
+}
+
+cudaError_t launch_prep(int P, int nq, int M, const double* radii, int64_t radii_stride,
+                        const BinParams& bp, double* thr, float* thr2_l2, int32_t* status,
+                        uint64_t* hist, int64_t hist_elems, uint32_t* recheck_ctr, cudaStream_t st) {
+    cudaError_t e = cudaMemsetAsync(hist, 0, sizeof(uint64_t) * hist_elems, st);
+    if (e != cudaSuccess) return e;
+    if (recheck_ctr) {
+        e = cudaMemsetAsync(recheck_ctr, 0, sizeof(uint32_t) * 2, st);
+        if (e != cudaSuccess) return e;
+    }
+    k_prep<<<P, 128, 0, st>>>(P, nq, M, radii, radii_stride, bp, thr, thr2_l2, status);
+    note_launch();
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------ centre
+// c[p][k] = mean of the first nrc rows of the item's column panel, FP64
+// accumulation, rounded to FP32.  A numerical device only (conditioning of the
+// Gram, DESIGN.md §L2 engine): distances are translation invariant.
+__global__ void k_center(RowSrc src, int64_t nrc, int64_t K, int64_t Kp, float* __restrict__ center) {
+    const int64_t p = blockIdx.y;
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= Kp) return;
+    double s = 0.0;
+    if (k < K)
+        for (int64_t r = 0; r < nrc; ++r) s += (double)__ldg(row_ptr(src, p, r) + k);
+    center[p * Kp + k] = (k < K && nrc > 0) ? (float)(s / (double)nrc) : 0.0f;
+}
+
+cudaError_t launch_center(int P, const RowSrc& colsrc, int64_t nrc, int64_t K, int64_t Kp,
+                          float* center, cudaStream_t st) {
+    dim3 grid((unsigned)((Kp + 255) / 256), (unsigned)P);
+    k_center<<<grid, 256, 0, st>>>(colsrc, nrc, K, Kp, center);
+    note_launch();
+    return cudaGetLastError();
+}
+
+// ----------------------------------------------------------------------- TC pack
+// One CTA per panel row.  x~ = x - c (FP32), split:
+//   split 1 (3xBF16): hi = bf16_rn(x~), lo = bf16_rn(x~ - hi)
+//   split 2 (3xTF32): hi = x~ with the low 13 mantissa bits cleared, lo = x~ - hi (exact)
+// nrm = sum x~^2 (FP64 accumulate -> FP32), q4 = (sum x~^4)^(1/4) (the error-bound scale
+// of the split products, DESIGN.md §L2 engine).
+template <int SPLIT>
+__global__ void __launch_bounds__(256) k_pack_tc(RowSrc src, int64_t rows, int64_t K, int64_t Kp,
+                                                 const float* __restrict__ center,
+                                                 void* __restrict__ hi, void* __restrict__ lo,
+                                                 float* __restrict__ nrm, float* __restrict__ q4,
+                                                 int32_t* __restrict__ status) {
+    const int64_t p = blockIdx.y;
+    const int64_t r = blockIdx.x;
+    const float* x = row_ptr(src, p, r);
+    const float* c = center + p * Kp;
+    const int64_t orow = p * rows + r;
+    double s2 = 0.0, s4 = 0.0;
+    bool nonfinite = false;
+    for (int64_t k = (int64_t)threadIdx.x * 4; k < Kp; k += (int64_t)blockDim.x * 4) {
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (k < K) {
+            float4 xv = __ldg(reinterpret_cast<const float4*>(x + k));
+            float4 cv = *reinterpret_cast<const float4*>(c + k);
+            nonfinite |= !(isfinite(xv.x) && isfinite(xv.y) && isfinite(xv.z) && isfinite(xv.w));
+            v = make_float4(xv.x - cv.x, xv.y - cv.y, xv.z - cv.z, xv.w - cv.w);
+        }
+        const float e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const double d = (double)e[t];
+            s2 += d * d;
+            s4 += (d * d) * (d * d);
+        }
+        if (SPLIT == 1) {
+            __nv_bfloat16 h[4], l[4];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                h[t] = __float2bfloat16_rn(e[t]);
+                l[t] = __float2bfloat16_rn(e[t] - __bfloat162float(h[t]));
+            }
+            uint2 hv, lv;
+            hv.x = (uint32_t)__bfloat16_as_ushort(h[0]) | ((uint32_t)__bfloat16_as_ushort(h[1]) << 16);
+            hv.y = (uint32_t)__bfloat16_as_ushort(h[2]) | ((uint32_t)__bfloat16_as_ushort(h[3]) << 16);
+            lv.x = (uint32_t)__bfloat16_as_ushort(l[0]) | ((uint32_t)__bfloat16_as_ushort(l[1]) << 16);
+            lv.y = (uint32_t)__bfloat16_as_ushort(l[2]) | ((uint32_t)__bfloat16_as_ushort(l[3]) << 16);
+            reinterpret_cast<uint2*>(hi)[(orow * Kp + k) / 4] = hv;
+            reinterpret_cast<uint2*>(lo)[(orow * Kp + k) / 4] = lv;
+        } else {
+            float hh[4], ll[4];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                hh[t] = __uint_as_float(__float_as_uint(e[t]) & 0xFFFFE000u);
+                ll[t] = e[t] - hh[t];
+            }
+            reinterpret_cast<float4*>(hi)[(orow * Kp + k) / 4] = make_float4(hh[0], hh[1], hh[2], hh[3]);
+            reinterpret_cast<float4*>(lo)[(orow * Kp + k) / 4] = make_float4(ll[0], ll[1], ll[2], ll[3]);
+        }
+    }
+    // block reduction of s2, s4
+    __shared__ double red[2][32];
+    __shared__ int nf;
+    if (threadIdx.x == 0) nf = 0;
+    for (int o = 16; o > 0; o >>= 1) {
+        s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+        s4 += __shfl_xor_sync(0xffffffffu, s4, o);
+    }
+    __syncthreads();
+    if (nonfinite) atomicOr(&nf, 1);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) { red[0][w] = s2; red[1][w] = s4; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double a = 0.0, b = 0.0;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) { a += red[0][i]; b += red[1][i]; }
+        nrm[orow] = (float)a;
+        q4[orow] = (float)sqrt(sqrt(b));
+        if (nf) atomicOr(&status[p], CIL_ITEM_NONFINITE);
+    }
+}
+
+cudaError_t launch_pack_tc(int P, const RowSrc& src, int64_t rows, int64_t K, int64_t Kp,
+                           const float* center, int split, void* hi, void* lo, float* nrm, float* q4,
+                           int32_t* status, cudaStream_t st) {
+    if (rows == 0) return cudaSuccess;
+    dim3 grid((unsigned)rows, (unsigned)P);
+    if (split == 2)
+        k_pack_tc<2><<<grid, 256, 0, st>>>(src, rows, K, Kp, center, hi, lo, nrm, q4, status);
+    else
+        k_pack_tc<1><<<grid, 256, 0, st>>>(src, rows, K, Kp, center, hi, lo, nrm, q4, status);
+    note_launch();
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------- aug pack
+// One CTA per panel row: out = [x (K) | D_x x (S*H*(W-1)) | D_y x (S*(H-1)*W)], each
+// region zero-padded to a multiple of kSimtBK, plain FP32 differences.
+__global__ void __launch_bounds__(256) k_pack_aug(RowSrc src, int64_t rows, AugGeom g,
+                                                  float* __restrict__ out, int32_t* __restrict__ status) {
+    const int64_t p = blockIdx.y;
+    const int64_t r = blockIdx.x;
+    const float* x = row_ptr(src, p, r);
+    float* o = out + (p * rows + r) * g.off[3];
+    bool nonfinite = false;
+    // value region
+    for (int64_t k = threadIdx.x; k < g.off[1]; k += blockDim.x) {
+        float v = 0.f;
+        if (k < g.K) {
+            v = __ldg(x + k);
+            nonfinite |= !isfinite(v);
+        }
+        o[k] = v;
+    }
+    if (g.nreg >= 2) {
+        const int W1 = g.W - 1;
+        for (int64_t t = threadIdx.x; t < g.off[2] - g.off[1]; t += blockDim.x) {
+            float v = 0.f;
+            if (t < g.Kx) {
+                const int64_t sr = t / W1, c = t % W1;          // sr = s*H + r
+                const float* row = x + sr * g.W;
+                v = __ldg(row + c + 1) - __ldg(row + c);
+            }
+            o[g.off[1] + t] = v;
+        }
+    }
+    if (g.nreg >= 3) {
+        const int64_t per_s = (int64_t)(g.H - 1) * g.W;
+        for (int64_t t = threadIdx.x; t < g.off[3] - g.off[2]; t += blockDim.x) {
+            float v = 0.f;
+            if (t < g.Ky) {
+                const int64_t s = t / per_s, rc = t % per_s;    // rc = r*W + c, r < H-1
+                const float* base = x + s * (int64_t)g.H * g.W + rc;
+                v = __ldg(base + g.W) - __ldg(base);
+            }
+            o[g.off[2] + t] = v;
+        }
+    }
+    if (__syncthreads_or(nonfinite) && threadIdx.x == 0) atomicOr(&status[p], CIL_ITEM_NONFINITE);
+}
+
+cudaError_t launch_pack_aug(int P, const RowSrc& src, int64_t rows, const AugGeom& g, float* out,
+                            int32_t* status, cudaStream_t st) {
+    if (rows == 0) return cudaSuccess;
+    dim3 grid((unsigned)rows, (unsigned)P);
+    k_pack_aug<<<grid, 256, 0, st>>>(src, rows, g, out, status);
+    note_launch();
+    return cudaGetLastError();
+}
+
+}  // namespace cil

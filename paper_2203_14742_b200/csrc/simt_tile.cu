@@ -1,0 +1,268 @@
+// simt_tile.cu — step a3 of the hot path: the alternative distance measures
+// (Eqs. (6)-(10)) — and L2 when the SIMT engine is chosen —
+// on CUDA cores, fused with radius binning (Eq. (1)) so no N x Nt matrix is stored.
+//
+// Per pair (i,j) and region al in {value, D_x, D_y} of the augmented operands:
+//   m_al = max_e |A_i[e] - B_j[e]|        (FADD2 + 3-input |.|-max)
+//   s_al = sum_e (A_i[e] - B_j[e])^2      (FADD2 + FFMA2; FP32 chunks of 128 flushed to FP64)
+// Epilogue (FP64): a_al = sqrt(w * s_al / h^2[al>0]), m_al /= h[al>0], then
+//   L2 = a_0, Linf = m_0, W12sum = a_0+a_x+a_y, W12 = sqrt(a_0^2+a_x^2+a_y^2),
+//   W1inf = max(m_0,m_x,m_y), W1infsum = m_0+m_x+m_y     (readings R1-R4)
+// and bin b = #{m : d < R_m} (strict <) into a per-segment histogram.
+//
+// Tiling: CTA = 128 threads = 32 A-rows x 64 B-rows of pairs, 4x4 pairs per
+// thread; k-chunks of 32 floats double-buffered in smem with cp.async (rows
+// padded to 36 floats -> conflict-free LDS.128).
+#include "cil_internal.cuh"
+
+namespace cil {
+
+namespace {
+constexpr int TA = 32, TB = 64, BK = kSimtBK, LDS = BK + 4;
+constexpr int NTHR = 128;
+constexpr int FLUSH = 4;   // chunks between FP32 -> FP64 flushes (128 elements per pair)
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+    const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+    const int sz = valid ? 16 : 0;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) {
+    return __fadd2_rn(a, make_float2(-b.x, -b.y));
+}
+__device__ __forceinline__ float absmax3(float m, float x, float y) {
+    return fmaxf(m, fmaxf(fabsf(x), fabsf(y)));
+}
+}  // namespace
+
+template <bool DO_MAX, bool DO_SUM>
+__global__ void __launch_bounds__(NTHR, 2) k_simt(SimtArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    float* As = reinterpret_cast<float*>(smem_raw);                 // [2][TA][LDS]
+    float* Bs = As + 2 * TA * LDS;                                   // [2][TB][LDS]
+    double* thr_s = reinterpret_cast<double*>(Bs + 2 * TB * LDS);    // [nq*M]
+    // per-thread region results for regions 0 and 1 (region 2 stays in registers)
+    double* rs_sum = thr_s + kMaxMeas * kMaxM;                       // [2][16][NTHR]
+    float* rs_max = reinterpret_cast<float*>(rs_sum + (DO_SUM ? 2 * 16 * NTHR : 0));  // [2][16][NTHR]
+    uint32_t* hist_s = reinterpret_cast<uint32_t*>(rs_max + (DO_MAX ? 2 * 16 * NTHR : 0));
+
+    const int p = blockIdx.z;
+    if (a.status[p] & CIL_ITEM_BADRADII) return;
+    const int64_t row0 = (int64_t)blockIdx.y * TA;
+    const int64_t col0 = (int64_t)blockIdx.x * TB;
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int ty = (warp >> 1) * 4 + (lane >> 3);   // 0..7
+    const int tx = (warp & 1) * 8 + (lane & 7);     // 0..15
+    const int nq = a.bp.nq, M = a.bp.M;
+
+    for (int t = tid; t < nq * M; t += NTHR) thr_s[t] = a.thr[(int64_t)p * a.thr_stride + t];
+
+    // local segment window of this tile
+    const int64_t rlast = min(row0 + TA, a.rowsA) - 1, clast = min(col0 + TB, a.rowsB) - 1;
+    const int64_t rs0 = row0 / a.sp.row_seg, cs0 = col0 / a.sp.col_seg;
+    const int nrs = (int)(rlast / a.sp.row_seg - rs0 + 1), ncs = (int)(clast / a.sp.col_seg - cs0 + 1);
+    const int nloc = nrs * ncs;
+    const int hist_len = nloc * nq * (M + 1);
+    const bool use_sh = hist_len <= 4096;
+    if (use_sh)
+        for (int t = tid; t < hist_len; t += NTHR) hist_s[t] = 0u;
+
+    const float* Ag = a.Aaug + ((int64_t)p * a.rowsA) * a.Kaug;
+    const float* Bg = a.Baug + ((int64_t)p * a.rowsB) * a.Kaug;
+    const int nchunks = (int)(a.g.off[a.g.nreg] / BK);
+    const int c_end0 = (int)(a.g.off[1] / BK);
+    const int c_end1 = (int)(a.g.off[2] / BK);
+
+    auto load_chunk = [&](int c, int buf) {
+        const int64_t k0 = (int64_t)c * BK;
+        // A: 32 rows x 8 x 16B = 256 copies, 2 per thread
+#pragma unroll
+        for (int t = 0; t < (TA * BK / 4) / NTHR; ++t) {
+            const int idx = tid + t * NTHR;
+            const int r = idx >> 3, v = idx & 7;
+            const int64_t gr = row0 + r;
+            const bool ok = gr < a.rowsA;
+            cp_async16(As + (buf * TA + r) * LDS + v * 4, Ag + (ok ? gr : 0) * a.Kaug + k0 + v * 4, ok);
+        }
+#pragma unroll
+        for (int t = 0; t < (TB * BK / 4) / NTHR; ++t) {
+            const int idx = tid + t * NTHR;
+            const int r = idx >> 3, v = idx & 7;
+            const int64_t gc = col0 + r;
+            const bool ok = gc < a.rowsB;
+            cp_async16(Bs + (buf * TB + r) * LDS + v * 4, Bg + (ok ? gc : 0) * a.Kaug + k0 + v * 4, ok);
+        }
+        cp_async_commit();
+    };
+
+    float2 acc[4][4];      // FP32 chunk sums (even, odd elements)
+    double tot[4][4];      // FP64 region sums
+    float mx[4][4];        // region maxima
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            acc[i][j] = make_float2(0.f, 0.f);
+            tot[i][j] = 0.0;
+            mx[i][j] = 0.f;
+        }
+
+    load_chunk(0, 0);
+    int region = 0, since_flush = 0;
+    for (int c = 0; c < nchunks; ++c) {
+        const int buf = c & 1;
+        if (c + 1 < nchunks) {
+            load_chunk(c + 1, buf ^ 1);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        const float* Ab = As + buf * TA * LDS;
+        const float* Bb = Bs + buf * TB * LDS;
+#pragma unroll 2
+        for (int kk = 0; kk < BK; kk += 4) {
+            float4 av[4], bv[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) av[i] = *reinterpret_cast<const float4*>(Ab + (ty + 8 * i) * LDS + kk);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) bv[j] = *reinterpret_cast<const float4*>(Bb + (tx + 16 * j) * LDS + kk);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const float2 d0 = sub2(make_float2(av[i].x, av[i].y), make_float2(bv[j].x, bv[j].y));
+                    const float2 d1 = sub2(make_float2(av[i].z, av[i].w), make_float2(bv[j].z, bv[j].w));
+                    if (DO_MAX) {
+                        mx[i][j] = absmax3(mx[i][j], d0.x, d0.y);
+                        mx[i][j] = absmax3(mx[i][j], d1.x, d1.y);
+                    }
+                    if (DO_SUM) {
+                        acc[i][j] = __ffma2_rn(d0, d0, acc[i][j]);
+                        acc[i][j] = __ffma2_rn(d1, d1, acc[i][j]);
+                    }
+                }
+        }
+        __syncthreads();
+        const bool region_end = (c + 1 == c_end0) || (c + 1 == c_end1) || (c + 1 == nchunks);
+        if (DO_SUM && (++since_flush == FLUSH || region_end)) {
+            since_flush = 0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    tot[i][j] += (double)acc[i][j].x + (double)acc[i][j].y;
+                    acc[i][j] = make_float2(0.f, 0.f);
+                }
+        }
+        if (region_end && c + 1 < nchunks) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int e = (region * 16 + i * 4 + j) * NTHR + tid;
+                    if (DO_SUM) { rs_sum[e] = tot[i][j]; tot[i][j] = 0.0; }
+                    if (DO_MAX) { rs_max[e] = mx[i][j]; mx[i][j] = 0.f; }
+                }
+            ++region;
+            since_flush = 0;
+        }
+    }
+
+    // ------------------------------------------------------------- epilogue
+    const double h = a.bp.h, w = a.bp.w, ih = 1.0 / h, ih2 = 1.0 / (h * h);
+    const int nreg = a.g.nreg;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int64_t gi = row0 + ty + 8 * i;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int64_t gj = col0 + tx + 16 * j;
+            if (gi >= a.rowsA || gj >= a.rowsB) continue;
+            double s[3] = {0.0, 0.0, 0.0}, m[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+            for (int r = 0; r < 3; ++r) {
+                if (r >= nreg) break;
+                const bool last = (r == nreg - 1);
+                const int e = (r * 16 + i * 4 + j) * NTHR + tid;
+                if (DO_SUM) s[r] = last ? tot[i][j] : rs_sum[e];
+                if (DO_MAX) m[r] = last ? (double)mx[i][j] : (double)rs_max[e];
+            }
+            const double a0 = sqrt(w * s[0]), ax = sqrt(w * s[1] * ih2), ay = sqrt(w * s[2] * ih2);
+            const double m0 = m[0], mxx = m[1] * ih, myy = m[2] * ih;
+            const int64_t rs = gi / a.sp.row_seg, cs = gj / a.sp.col_seg;
+            for (int q = 0; q < nq; ++q) {
+                if (!((a.qmask >> q) & 1u)) continue;
+                double d;
+                switch (a.bp.slot[q]) {
+                    case 0: d = a0; break;
+                    case 1: d = m0; break;
+                    case 2: d = a0 + ax + ay; break;
+                    case 3: d = sqrt(a0 * a0 + ax * ax + ay * ay); break;
+                    case 4: d = fmax(m0, fmax(mxx, myy)); break;
+                    default: d = m0 + mxx + myy; break;
+                }
+                const double* T = thr_s + q * M;
+                int b = 0;
+                while (b < M && d < T[b]) ++b;
+                if (b == 0) continue;
+                if (use_sh) {
+                    const int loc = (int)((rs - rs0) * ncs + (cs - cs0));
+                    atomicAdd(&hist_s[(loc * nq + q) * (M + 1) + b], 1u);
+                } else {
+                    atomicAdd((unsigned long long*)&a.hist[hist_index(a.sp, nq, M, p, rs, cs, q, b)], 1ull);
+                }
+            }
+        }
+    }
+    if (use_sh) {
+        __syncthreads();
+        for (int t = tid; t < hist_len; t += NTHR) {
+            const uint32_t v = hist_s[t];
+            if (v == 0u) continue;
+            const int b = t % (M + 1);
+            const int q = (t / (M + 1)) % nq;
+            const int loc = t / ((M + 1) * nq);
+            const int64_t rs = rs0 + loc / ncs, cs = cs0 + loc % ncs;
+            atomicAdd((unsigned long long*)&a.hist[hist_index(a.sp, nq, M, p, rs, cs, q, b)],
+                      (unsigned long long)v);
+        }
+    }
+}
+
+static size_t simt_smem(bool do_max, bool do_sum) {
+    size_t s = sizeof(float) * 2 * (TA + TB) * LDS + sizeof(double) * kMaxMeas * kMaxM;
+    if (do_sum) s += sizeof(double) * 2 * 16 * NTHR;
+    if (do_max) s += sizeof(float) * 2 * 16 * NTHR;
+    s += sizeof(uint32_t) * 4096;
+    return s;
+}
+
+template <bool X, bool Y>
+static cudaError_t launch_simt_t(const SimtArgs& a, cudaStream_t st) {
+    const size_t sm = simt_smem(X, Y);
+    static bool attr_done = false;   // benign race: idempotent attribute set
+    if (!attr_done) {
+        cudaError_t e = cudaFuncSetAttribute(k_simt<X, Y>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        if (e != cudaSuccess) return e;
+        attr_done = true;
+    }
+    dim3 grid((unsigned)((a.rowsB + TB - 1) / TB), (unsigned)((a.rowsA + TA - 1) / TA), (unsigned)a.P);
+    k_simt<X, Y><<<grid, NTHR, sm, st>>>(a);
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_simt(const SimtArgs& a, cudaStream_t st) {
+    if (a.rowsA == 0 || a.rowsB == 0) return cudaSuccess;
+    if (a.do_max && a.do_sum) return launch_simt_t<true, true>(a, st);
+    if (a.do_max) return launch_simt_t<true, false>(a, st);
+    return launch_simt_t<false, true>(a, st);
+}
+
+}  // namespace cil

@@ -1,0 +1,221 @@
+// stats.cu — steps a4-a7 tails: histogram -> counts / y (Eq. (1) normalisation),
+// mu / Sigma over realisations, batched Cholesky log-likelihood
+// (Eq. (4); Eq. (12)), and the SCIL per-theta tail (Alg. 3
+// steps 4-6).  All FP64; latency-bound (one CTA per item).
+#include <math_constants.h>
+
+#include "cil_internal.cuh"
+
+namespace cil {
+
+// ------------------------------------------------------------------ finalize
+// counts[p][q][m] = sum_{b > m} hist[p][0][0][q][b];  y = counts / (N * Nt).
+__global__ void k_finalize(int nq, int M, SegParams sp, const uint64_t* __restrict__ hist,
+                           uint64_t* __restrict__ counts, double* __restrict__ y, double npairs) {
+    const int p = blockIdx.x;
+    for (int t = threadIdx.x; t < nq * M; t += blockDim.x) {
+        const int q = t / M, m = t % M;
+        uint64_t c = 0;
+        for (int b = m + 1; b <= M; ++b) c += hist[hist_index(sp, nq, M, p, 0, 0, q, b)];
+        counts[(int64_t)p * nq * M + t] = c;
+        if (y) y[(int64_t)p * nq * M + t] = npairs > 0 ? (double)c / npairs : 0.0;
+    }
+}
+
+cudaError_t launch_finalize(int P, int nq, int M, const SegParams& sp, const uint64_t* hist,
+                            uint64_t* counts, double* y, int64_t rows, int64_t cols,
+                            const int32_t*, int32_t*, cudaStream_t st) {
+    k_finalize<<<P, 128, 0, st>>>(nq, M, sp, hist, counts, y, (double)rows * (double)cols);
+    note_launch();
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ stats
+__global__ void k_mean(const double* __restrict__ Y, int64_t y_stride, int n, int D,
+                       double* __restrict__ mu) {
+    const int p = blockIdx.x;
+    const double* Yp = Y + (int64_t)p * y_stride;
+    for (int a = threadIdx.x; a < D; a += blockDim.x) {
+        double s = 0.0;
+        for (int v = 0; v < n; ++v) s += Yp[(int64_t)v * D + a];
+        mu[(int64_t)p * D + a] = s / n;
+    }
+}
+
+// Sigma[a][b] = 1/(n-1) sum_v (Y[v][a]-mu[a])(Y[v][b]-mu[b]); grid (D rows, P)
+__global__ void k_cov(const double* __restrict__ Y, int64_t y_stride, int n, int D,
+                      const double* __restrict__ mu, double* __restrict__ Sigma) {
+    const int a = blockIdx.x, p = blockIdx.y;
+    const double* Yp = Y + (int64_t)p * y_stride;
+    const double* mp = mu + (int64_t)p * D;
+    for (int b = threadIdx.x; b < D; b += blockDim.x) {
+        double s = 0.0;
+        for (int v = 0; v < n; ++v) s += (Yp[(int64_t)v * D + a] - mp[a]) * (Yp[(int64_t)v * D + b] - mp[b]);
+        Sigma[((int64_t)p * D + a) * D + b] = s / (n - 1);
+    }
+}
+
+static cudaError_t launch_stats_strided(int P, const double* Y, int64_t y_stride, int n, int D,
+                                        double* mu, double* Sigma, cudaStream_t st) {
+    k_mean<<<P, 128, 0, st>>>(Y, y_stride, n, D, mu);
+    note_launch();
+    dim3 g((unsigned)D, (unsigned)P);
+    k_cov<<<g, 128, 0, st>>>(Y, y_stride, n, D, mu, Sigma);
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_stats(int P, const double* Y, int n, int D, double* mu, double* Sigma, cudaStream_t st) {
+    return launch_stats_strided(P, Y, (int64_t)n * D, n, D, mu, Sigma, st);
+}
+
+// ------------------------------------------------------------------ loglik
+// One CTA per item.  Packed lower triangle L[i][j] at i(i+1)/2 + j in smem.
+constexpr int kLogThreads = 256;
+
+__global__ void __launch_bounds__(kLogThreads) k_loglik(const double* __restrict__ mu, int64_t mu_stride,
+                                                        const double* __restrict__ Sigma, int64_t Sigma_stride,
+                                                        const double* __restrict__ y, int64_t y_stride, int D,
+                                                        double ridge, double* __restrict__ out,
+                                                        int32_t* __restrict__ status, const int32_t* status_in) {
+    extern __shared__ double sm[];
+    double* L = sm;                                   // D(D+1)/2
+    double* z = L + (int64_t)D * (D + 1) / 2;         // D
+    __shared__ double piv;
+    __shared__ int fail;
+    const int p = blockIdx.x;
+    const double* S = Sigma + (int64_t)p * Sigma_stride;
+    const double* m = mu + (int64_t)p * mu_stride;
+    const double* yy = y + (int64_t)p * y_stride;
+    for (int t = threadIdx.x; t < D * D; t += blockDim.x) {
+        const int i = t / D, j = t % D;
+        if (j <= i) L[i * (i + 1) / 2 + j] = S[(int64_t)i * D + j] + (i == j ? ridge : 0.0);
+    }
+    for (int i = threadIdx.x; i < D; i += blockDim.x) z[i] = yy[i] - m[i];
+    if (threadIdx.x == 0) fail = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // left-looking Cholesky, column by column
+    for (int j = 0; j < D; ++j) {
+        const int dj = j * (j + 1) / 2;
+        if (warp == 0) {
+            double s = 0.0;
+            for (int k = lane; k < j; k += 32) s += L[dj + k] * L[dj + k];
+            for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+            if (lane == 0) {
+                const double d = L[dj + j] - s;
+                if (!(d > 0.0)) fail = 1;
+                piv = sqrt(d);
+                L[dj + j] = piv;
+            }
+        }
+        __syncthreads();
+        if (fail) break;
+        for (int i = j + 1 + threadIdx.x; i < D; i += blockDim.x) {
+            const int di = i * (i + 1) / 2;
+            double t = L[di + j];
+            for (int k = 0; k < j; ++k) t -= L[di + k] * L[dj + k];
+            L[di + j] = t / piv;
+        }
+        __syncthreads();
+    }
+    const int32_t base = status_in ? status_in[p] : 0;
+    if (fail) {
+        if (threadIdx.x == 0) {
+            out[3 * p + 0] = out[3 * p + 1] = out[3 * p + 2] = CUDART_NAN;
+            status[p] = base | CIL_ITEM_NOTPD;
+        }
+        return;
+    }
+    // forward substitution z = L^{-1} r (warp 0), quad = z^T z, logdet = 2 sum ln L_ii
+    if (warp == 0) {
+        double quad = 0.0, logdet = 0.0;
+        for (int i = 0; i < D; ++i) {
+            const int di = i * (i + 1) / 2;
+            double s = 0.0;
+            for (int k = lane; k < i; k += 32) s += L[di + k] * z[k];
+            for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+            const double zi = (z[i] - s) / L[di + i];
+            __syncwarp();
+            if (lane == 0) z[i] = zi;
+            __syncwarp();
+            quad += zi * zi;
+            logdet += 2.0 * log(L[di + i]);
+        }
+        if (lane == 0) {
+            out[3 * p + 0] = quad;
+            out[3 * p + 1] = logdet;
+            out[3 * p + 2] = -0.5 * quad - 0.5 * logdet - 0.5 * D * log(2.0 * CUDART_PI);
+            status[p] = base;
+        }
+    }
+}
+
+static cudaError_t launch_loglik_strided(int P, const double* mu, int64_t mu_stride, const double* Sigma,
+                                         int64_t Sigma_stride, const double* y, int64_t y_stride, int D,
+                                         double ridge, double* out, int32_t* status,
+                                         const int32_t* status_in, cudaStream_t st) {
+    const size_t smem = sizeof(double) * ((size_t)D * (D + 1) / 2 + D);
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(k_loglik, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)(sizeof(double) * ((size_t)kMaxD * (kMaxD + 1) / 2 + kMaxD)));
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    k_loglik<<<P, kLogThreads, smem, st>>>(mu, mu_stride, Sigma, Sigma_stride, y, y_stride, D, ridge, out,
+                                           status, status_in);
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_loglik(int P, const double* mu, int64_t mu_stride, const double* Sigma,
+                          int64_t Sigma_stride, const double* y, int D, double ridge, double* out,
+                          int32_t* status, const int32_t* status_in, cudaStream_t st) {
+    return launch_loglik_strided(P, mu, mu_stride, Sigma, Sigma_stride, y, D, D, ridge, out, status,
+                                 status_in, st);
+}
+
+// ------------------------------------------------------------------ SCIL tail
+// Y[p][v][q*M + m] for v = k*n_ens + l (Eq. (11)) and v = n_ens^2 for y~ (Eq. (13)):
+//   counts of segment (rs = k, cs = l), resp. (rs = n_ens (the s_data rows), cs = k0[p]),
+//   divided by N_set * N_tilde.
+__global__ void k_build_Y(int n_ens, int nq, int M, SegParams sp, const uint64_t* __restrict__ hist,
+                          double npairs, const int32_t* __restrict__ k0, double* __restrict__ Y,
+                          int32_t* __restrict__ status) {
+    const int p = blockIdx.y;
+    const int v = blockIdx.x;
+    const int nv = n_ens * n_ens;
+    const int D = nq * M;
+    int rs, cs;
+    if (v < nv) { rs = v / n_ens; cs = v % n_ens; }
+    else {
+        rs = n_ens;
+        cs = k0[p];
+        if (cs < 0 || cs >= n_ens) {
+            if (threadIdx.x == 0) atomicOr(&status[p], CIL_ITEM_BADRADII);
+            cs = 0;
+        }
+    }
+    for (int t = threadIdx.x; t < D; t += blockDim.x) {
+        const int q = t / M, m = t % M;
+        uint64_t c = 0;
+        for (int b = m + 1; b <= M; ++b) c += hist[hist_index(sp, nq, M, p, rs, cs, q, b)];
+        Y[((int64_t)p * (nv + 1) + v) * D + t] = (double)c / npairs;
+    }
+}
+
+cudaError_t launch_synth_tail(int P, int n_ens, int nq, int M, const SegParams& sp, const uint64_t* hist,
+                              int64_t N_set, int64_t N_tilde, const int32_t* k0, double ridge, double* out,
+                              int32_t* status, double* Y, double* mu, double* Sigma, cudaStream_t st) {
+    const int nv = n_ens * n_ens, D = nq * M;
+    dim3 g((unsigned)(nv + 1), (unsigned)P);
+    k_build_Y<<<g, 128, 0, st>>>(n_ens, nq, M, sp, hist, (double)N_set * (double)N_tilde, k0, Y, status);
+    note_launch();
+    cudaError_t e = launch_stats_strided(P, Y, (int64_t)(nv + 1) * D, nv, D, mu, Sigma, st);
+    if (e != cudaSuccess) return e;
+    return launch_loglik_strided(P, mu, D, Sigma, (int64_t)D * D, Y + (int64_t)nv * D, (int64_t)(nv + 1) * D,
+                                 D, ridge, out, status, status, st);
+}
+
+}  // namespace cil

@@ -1,0 +1,269 @@
+"""GPU parity: the CUDA path (through the C ABI) against the FP64 oracle on the same
+seeded inputs.  Tolerances (north star, BASELINE.json):
+  counts  bit-exact except (pair, radius) cases within 1e-6 relative of a radius:
+          the oracle's band counts give lo <= gpu <= hi (== when nothing is ambiguous);
+  mu, Sigma within 1e-6 relative (normwise, on the same count vectors);
+  loglik within 1e-6 absolute.
+"""
+import numpy as np
+import pytest
+import torch
+
+import cilgen
+
+pytestmark = pytest.mark.gpu
+
+BAND = 1e-6
+ENGINES = ["SIMT", "TC_3XBF16", "TC_3XTF32"]
+
+
+@pytest.fixture(scope="module")
+def cil():
+    if not torch.cuda.is_available():
+        pytest.skip("needs CUDA")
+    import paper_2203_14742_b200 as cil
+    return cil
+
+
+def _engine(cil, name):
+    return getattr(cil, "ENGINE_" + name)
+
+
+def _radii_from(D, M, lo_q=0.0, hi_q=1.0):
+    """Power-law radii R_0 b^-m spanning the distance range."""
+    out = []
+    for q in range(D.shape[0]):
+        d = D[q].ravel()
+        R0, RM = np.quantile(d, hi_q) * 1.001, max(np.quantile(d, lo_q) * 0.999, 1e-12)
+        out.append(R0 * (RM / R0) ** (np.arange(1, M + 1) / M))
+    return np.array(out)
+
+
+def _check_counts(gpu, ref):
+    gpu = np.asarray(gpu)
+    ok = np.all(ref["lo"] <= gpu) and np.all(gpu <= ref["hi"])
+    assert ok, f"gpu {gpu.tolist()}\noracle {ref['counts'].tolist()}\nlo {ref['lo'].tolist()}\nhi {ref['hi'].tolist()}"
+
+
+def _sel(D, mask):
+    return D[[q for q in range(6) if (mask >> q) & 1]]
+
+
+def _run_features(cil, A, B, grid, mask, radii, engine):
+    dev = torch.device("cuda")
+    counts, y, st = cil.features(A.to(dev), B.to(dev), grid, mask, torch.tensor(radii, device=dev),
+                                 engine=_engine(cil, engine))
+    torch.cuda.synchronize()
+    return counts.cpu().numpy(), y.cpu().numpy(), st.cpu().numpy()
+
+
+# ------------------------------------------------------------------ features
+@pytest.mark.parametrize("engine", ENGINES)
+def test_c1_all_measures(cil, oracle_mod, engine):
+    O = oracle_mod
+    grid = (1, 32, 32, 0.0)
+    seed = cilgen.config_seed(1)
+    A = cilgen.make_set(seed, 0, 20, grid[:3])
+    B = cilgen.make_set(seed, 1, 20, grid[:3])
+    D = O.distance_matrix(A.numpy(), B.numpy(), grid, 0x3F)
+    radii = _radii_from(D, 10)
+    ref = O.features(A.numpy(), B.numpy(), grid, 0x3F, radii, band=BAND)
+    c, y, st = _run_features(cil, A, B, grid, 0x3F, radii, engine)
+    assert st[0] == 0
+    _check_counts(c[0], ref)
+    np.testing.assert_array_equal(y[0], c[0] / 400.0)
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("mask", [0x3F, 0x1, 0x2, 0x0C, 0x30, 0x09])
+def test_ragged_batched(cil, oracle_mod, engine, mask):
+    """P = 3 items, ragged N/Nt spanning several tiles, two species, non-square grid."""
+    O = oracle_mod
+    grid = (2, 10, 12, 0.0)
+    P, N, Nt = 3, 37, 70
+    A = torch.stack([cilgen.make_set(5, 2 * p, N, grid[:3]) for p in range(P)])
+    B = torch.stack([cilgen.make_set(5, 2 * p + 1, Nt, grid[:3]) for p in range(P)])
+    D0 = _sel(O.distance_matrix(A[0].numpy(), B[0].numpy(), grid, 0x3F), mask)
+    radii = _radii_from(D0, 13, 0.02, 0.98)
+    c, y, st = _run_features(cil, A, B, grid, mask, radii, engine)
+    assert np.all(st == 0)
+    for p in range(P):
+        ref = O.features(A[p].numpy(), B[p].numpy(), grid, mask, radii, band=BAND)
+        _check_counts(c[p], ref)
+        np.testing.assert_array_equal(y[p], c[p] / (N * Nt))
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_per_item_radii_and_1d(cil, oracle_mod, engine):
+    O = oracle_mod
+    grid = (2, 1, 64, 0.0)                 # 1-D grid (MC / RD-ODE rows of Table 1)
+    P, N, Nt = 2, 33, 29
+    A = torch.stack([cilgen.make_set(9, 10 + p, N, grid[:3]) for p in range(P)])
+    B = torch.stack([cilgen.make_set(9, 20 + p, Nt, grid[:3]) for p in range(P)])
+    mask = 0x3F
+    radii = np.stack([_radii_from(O.distance_matrix(A[p].numpy(), B[p].numpy(), grid, mask), 7, 0.05, 0.95)
+                      for p in range(P)])
+    c, y, st = _run_features(cil, A, B, grid, mask, radii, engine)
+    for p in range(P):
+        ref = O.features(A[p].numpy(), B[p].numpy(), grid, mask, radii[p], band=BAND)
+        _check_counts(c[p], ref)
+
+
+def test_explicit_h_and_symmetry(cil, oracle_mod):
+    O = oracle_mod
+    grid = (1, 16, 16, 0.37)
+    A = cilgen.make_set(3, 0, 25, grid[:3])
+    D = O.distance_matrix(A.numpy(), A.numpy(), grid, 0x3F)
+    radii = np.array([np.geomspace(D[q][D[q] > 0].max() * 1.001, D[q][D[q] > 0].min() * 0.999, 9)
+                      for q in range(6)])
+    ref = O.features(A.numpy(), A.numpy(), grid, 0x3F, radii, band=BAND)
+    for eng in ENGINES:
+        c, y, st = _run_features(cil, A, A, grid, 0x3F, radii, eng)
+        _check_counts(c[0], ref)
+
+
+def test_edge_cases(cil):
+    dev = torch.device("cuda")
+    grid = (1, 8, 8, 0.0)
+    A = cilgen.make_set(1, 0, 5, grid[:3]).to(dev)
+    B = cilgen.make_set(1, 1, 4, grid[:3]).to(dev)
+    radii = torch.tensor([[100.0, 1.0, 0.01]] * 6, dtype=torch.float64, device=dev)
+    for eng in ENGINES:
+        e = _engine(cil, eng)
+        # empty A
+        c, y, st = cil.features(A[:0], B, grid, 0x3F, radii, engine=e)
+        assert c.abs().sum().item() == 0 and y.abs().sum().item() == 0 and st.item() == 0
+        # single pair; R huge -> counted, tiny -> not
+        c, y, st = cil.features(A[:1], B[:1], grid, 0x3F, radii, engine=e)
+        assert c[0, :, 0].tolist() == [1] * 6 and c[0, :, 2].tolist() == [0] * 6
+        # bad radii (not decreasing) -> device status, no crash
+        bad = radii.clone()
+        bad[0, 2] = 5.0
+        c, y, st = cil.features(A, B, grid, 0x3F, bad, engine=e)
+        torch.cuda.synchronize()
+        assert st.item() & cil.ITEM_BADRADII
+        # non-finite input
+        A2 = A.clone()
+        A2[2, 0, 3, 3] = float("nan")
+        c, y, st = cil.features(A2, B, grid, 0x3F, radii, engine=e)
+        torch.cuda.synchronize()
+        assert st.item() & cil.ITEM_NONFINITE
+
+
+def test_translation_invariance_tc(cil):
+    """Adding a constant field to every pattern must not change counts (pins the centring)."""
+    dev = torch.device("cuda")
+    grid = (2, 16, 16, 0.0)
+    A = cilgen.make_set(4, 0, 40, grid[:3]).to(dev)
+    B = cilgen.make_set(4, 1, 50, grid[:3]).to(dev)
+    radii = torch.tensor([np.geomspace(40.0, 5.0, 12)], dtype=torch.float64, device=dev)
+    base = None
+    for shift in (0.0, 16.0, -64.0):
+        for eng in ENGINES:
+            c, _, _ = cil.features(A + shift, B + shift, grid, 0x1, radii, engine=_engine(cil, eng))
+            if base is None:
+                base = c.clone()
+            assert torch.equal(c, base), (shift, eng)
+
+
+# ------------------------------------------------------------------ stats / loglik
+def test_stats_loglik(cil, oracle_mod):
+    O = oracle_mod
+    dev = torch.device("cuda")
+    rng = np.random.default_rng(0)
+    P, n, D = 5, 45, 13
+    Y = rng.random((P, n, D)) * 0.5 + np.linspace(0.9, 0.1, D)
+    mu, Sig = cil.stats(torch.tensor(Y, device=dev))
+    yo = rng.random((P, D))
+    out, st = cil.loglik(mu, Sig, torch.tensor(yo, device=dev), ridge=1e-9)
+    torch.cuda.synchronize()
+    for p in range(P):
+        mu_r, Sig_r = O.stats(Y[p])
+        assert np.max(np.abs(mu[p].cpu().numpy() - mu_r)) <= 1e-6 * np.max(np.abs(mu_r))
+        assert np.max(np.abs(Sig[p].cpu().numpy() - Sig_r)) <= 1e-6 * np.max(np.abs(Sig_r))
+        ref, rst = O.loglik(mu[p].cpu().numpy(), Sig[p].cpu().numpy(), yo[p], ridge=1e-9)
+        assert rst == st[p].item() == 0
+        np.testing.assert_allclose(out[p].cpu().numpy(), ref, rtol=0, atol=1e-6)
+    # shared mu / Sigma (CIL: fixed mu_0, Sigma_0 against many y(theta))
+    out2, _ = cil.loglik(mu[0], Sig[0], torch.tensor(yo, device=dev), ridge=1e-9)
+    for p in range(P):
+        ref, _ = O.loglik(mu[0].cpu().numpy(), Sig[0].cpu().numpy(), yo[p], ridge=1e-9)
+        np.testing.assert_allclose(out2[p].cpu().numpy(), ref, rtol=0, atol=1e-6)
+
+
+def test_loglik_notpd_and_large_D(cil, oracle_mod):
+    O = oracle_mod
+    dev = torch.device("cuda")
+    v = torch.arange(1.0, 7.0, dtype=torch.float64, device=dev)
+    out, st = cil.loglik(torch.zeros(6, device=dev, dtype=torch.float64), torch.outer(v, v),
+                         torch.ones(6, device=dev, dtype=torch.float64))
+    torch.cuda.synchronize()
+    assert st.item() == cil.ITEM_NOTPD and torch.isnan(out).all()
+    rng = np.random.default_rng(1)
+    D = 192
+    X = rng.standard_normal((D, 2 * D))
+    Sig = X @ X.T / (2 * D) + 0.05 * np.eye(D)
+    mu = rng.standard_normal(D)
+    yo = mu + rng.standard_normal(D) * 0.3
+    out, st = cil.loglik(torch.tensor(mu, device=dev), torch.tensor(Sig, device=dev), torch.tensor(yo, device=dev))
+    ref, _ = O.loglik(mu, Sig, yo)
+    np.testing.assert_allclose(out[0].cpu().numpy(), ref, rtol=0, atol=1e-6)
+
+
+# ------------------------------------------------------------------ SCIL
+@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("mask", [0x1, 0x0B])
+def test_synth_small(cil, oracle_mod, engine, mask):
+    O = oracle_mod
+    dev = torch.device("cuda")
+    grid = (1, 12, 12, 0.0)
+    P, n_ens, N_set, Nt = 3, 4, 5, 7
+    Nsyn = n_ens * (N_set + Nt)
+    pools = torch.stack([cilgen.make_set(21, 100 + p, Nsyn, grid[:3], n_w=4.5 + 0.3 * p) for p in range(P)])
+    data = cilgen.make_set(21, 999, N_set, grid[:3])
+    k0 = np.array([1, 3, 0], np.int32)
+    radii = []
+    for p in range(P):
+        Dp = _sel(O.distance_matrix(pools[p].numpy(), pools[p].numpy(), grid, 0x3F), mask)
+        Dp = np.where(Dp > 0, Dp, np.nan)
+        radii.append(np.array([np.geomspace(np.nanquantile(d, 0.97), np.nanquantile(d, 0.1), 6) for d in Dp]))
+    radii = np.array(radii)
+    out, st, Y = cil.synth_loglik(pools.to(dev), n_ens, N_set, Nt, data.to(dev), torch.tensor(k0, device=dev),
+                                  grid, mask, torch.tensor(radii, device=dev), ridge=1e-4,
+                                  engine=_engine(cil, engine), return_Y=True)
+    torch.cuda.synchronize()
+    for p in range(P):
+        ref, rst, Yr = O.synth_loglik(pools[p].numpy(), n_ens, N_set, Nt, data.numpy(), int(k0[p]), grid, mask,
+                                      radii[p], ridge=1e-4)
+        Yg = Y[p].cpu().numpy()
+        # any count difference must come from ambiguous pairs; with these radii there are none
+        np.testing.assert_array_equal(Yg, Yr)
+        assert rst == st[p].item()
+        np.testing.assert_allclose(out[p].cpu().numpy(), ref, rtol=0, atol=1e-6)
+
+
+# ------------------------------------------------------------------ full-size configs (sampled)
+@pytest.mark.parametrize("engine", ["TC_3XBF16", "SIMT"])
+def test_c2_full_item_vs_oracle(cil, oracle_mod, engine):
+    """One full C2 item (500 x 500, 64x64x2, L2, M = 15) in the batched launch the bench times."""
+    O = oracle_mod
+    dev = torch.device("cuda")
+    grid = (2, 64, 64, 0.0)
+    seed = cilgen.config_seed(2)
+    P = 4
+    A = torch.stack([cilgen.make_set(seed, 2 * p, 500, grid[:3], device=dev) for p in range(P)])
+    B = torch.stack([cilgen.make_set(seed, 2 * p + 1, 500, grid[:3], device=dev) for p in range(P)])
+    a0, b0 = A[0, :64].cpu().numpy(), B[0, :64].cpu().numpy()
+    radii = _radii_from(O.distance_matrix(a0, b0, grid, 0x1), 15)
+    c, y, st = cil.features(A, B, grid, 0x1, torch.tensor(radii, device=dev), engine=_engine(cil, engine))
+    torch.cuda.synchronize()
+    ref = O.features(A[0].cpu().numpy(), B[0].cpu().numpy(), grid, 0x1, radii, band=BAND)
+    _check_counts(c[0].cpu().numpy(), ref)
+    # additivity over row blocks (holds at any size): item 1 counts = sum of two halves
+    c1, _, _ = cil.features(A[1:2, :217], B[1:2], grid, 0x1, torch.tensor(radii, device=dev),
+                            engine=_engine(cil, engine))
+    c2, _, _ = cil.features(A[1:2, 217:], B[1:2], grid, 0x1, torch.tensor(radii, device=dev),
+                            engine=_engine(cil, engine))
+    assert torch.equal(c1[0] + c2[0], c[1])
+    yy = y.cpu().numpy()
+    assert np.all((yy >= 0) & (yy <= 1)) and np.all(np.diff(yy, axis=-1) <= 0)
