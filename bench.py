@@ -1,0 +1,476 @@
+#!/usr/bin/env python
+"""bench.py — the CIL hot path (arXiv 2203.14742) on B200.
+
+One step = one pass of the whole hot path over one batch:
+  C2 (BASELINE.json configs[1], the headline workload): 100 independent set pairs of
+  500 x 500 Gierer-Meinhardt-shaped 64x64x2 patterns, L2, M = 15 radii:
+    cil_features (pack -> tcgen05 Gram + fused binning -> exact re-check -> y)
+    -> [N > 1: all_gather of the feature vectors over NCCL]
+    -> cil_stats (mu_0, Sigma_0 over all vectors) -> cil_loglik (every local vector).
+  value = pattern-pair distances per second over all ranks (weak scaling: every rank owns
+  100 set pairs).  A secondary line item times C4 (SCIL, Alg. 3, 256 proposals) for the
+  "CIL loglik evals/sec" half of the metric.
+
+Launch: python bench.py [--gpus N --steps K --warmup W]  (torchrun for N > 1)
+        python bench.py --impl reference ...  -> the FP64 CPU oracle as it stands.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+import cilgen  # noqa: E402
+
+METRIC = "pattern-pair distances/sec + CIL loglik evals/sec at 1/2/4/8 B200 vs roofline"
+UNIT = "pattern-pair distances/s"
+PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "traffic.json")
+
+C2 = dict(name="C2", grid=(2, 64, 64), P=100, N=500, Nt=500, M=15, mask=1,
+          workload="C2: GM-shaped 64x64x2 patterns, 100 set pairs x (500 x 500), L2, M=15 (BASELINE configs[1])")
+C4 = dict(name="C4", grid=(1, 128, 128), P=256, n_ens=10, N_set=50, N_tilde=50, M=13, mask=1,
+          workload="C4: SCIL Alg. 3, 256 proposals x pool 1000 of 128x128, n_ens=10, 50+50, L2, M=13")
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# --------------------------------------------------------------------------- setup
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def pilot_radii(A0, B0, grid, M):
+    """Power-law radii R_m = R_0 b^-m spanning the distances of a 64 x 64
+    pilot block: R_0 = max (1 + 1e-3), R_M = min (1 - 1e-3).  Harness setup (untimed)."""
+    S, H, W = grid
+    h = 1.0 / (W - 1)
+    w = h * h if H > 1 else h
+    a = A0[:64].reshape(min(64, A0.shape[0]), -1).double()
+    b = B0[:64].reshape(min(64, B0.shape[0]), -1).double()
+    d = torch.cdist(a, b) * math.sqrt(w)
+    d = d[d > 0]
+    R0, RM = float(d.max()) * 1.001, float(d.min()) * 0.999
+    return R0 * (RM / R0) ** (np.arange(1, M + 1) / M)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index):
+        self.dev = device_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            uuid = str(torch.cuda.get_device_properties(self.dev).uuid)
+            sel = uuid if uuid.startswith("GPU-") else "GPU-" + uuid
+        except Exception:
+            sel = str(self.dev)
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", sel, f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def timed(fn, steps, stream):
+    """CUDA-event time of `steps` calls of fn on `stream` (synchronised both sides), ms."""
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(steps):
+        fn()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1)
+
+
+def peaks():
+    try:
+        return json.load(open(PEAKS_FILE))
+    except Exception:
+        return {}
+
+
+def traffic_for(key):
+    try:
+        return json.load(open(TRAFFIC_FILE)).get(key)
+    except Exception:
+        return None
+
+
+# --------------------------------------------------------------------------- oracle (CPU)
+def oracle_sample_rate(A, B, grid, mask, radii, budget_s=12.0):
+    """The FP64 oracle as it stands on the host cores, on whole set pairs of the
+    workload (item 0, 1, ...) until ~budget_s of CPU time: returns (pairs/s, cores,
+    sample description, seconds)."""
+    from oracle import oracle as O
+    O.build()
+    cores = O.default_threads()
+    g = (grid[0], grid[1], grid[2], 0.0)
+    pairs, dt, items = 0, 0.0, 0
+    while dt < budget_s and items < A.shape[0]:
+        a, b = A[items].cpu().numpy(), B[items].cpu().numpy()
+        t0 = time.perf_counter()
+        O.features(a, b, g, mask, radii, band=0.0, nthreads=cores)
+        dt += time.perf_counter() - t0
+        pairs += a.shape[0] * b.shape[0]
+        items += 1
+    return pairs / dt, cores, f"{items} whole set pairs of the workload ({pairs} pairs, L2 counts)", dt
+
+
+# --------------------------------------------------------------------------- main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=400)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--engine", default="TC_3XBF16", choices=["TC_3XBF16", "TC_3XTF32", "SIMT"])
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-c4", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    cfg = C2
+    grid, P, N, Nt, M, mask = cfg["grid"], cfg["P"], cfg["N"], cfg["Nt"], cfg["M"], cfg["mask"]
+    seed = cilgen.config_seed(2)
+    if args.impl == "reference":   # CPU only: rank 0 runs, the other ranks exit 0 without work
+        return reference_arm(args, int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")),
+                             cfg, seed, None)
+
+    world, rank, local = dist_setup()
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+
+    import paper_2203_14742_b200 as cil
+    from paper_2203_14742_b200 import _capi
+
+    engine = getattr(cil, "ENGINE_" + args.engine)
+    # ---- inputs: each rank owns 100 set pairs (sets 2p, 2p+1 offset by rank), resident in HBM
+    t0 = time.time()
+    A = torch.empty((P, N) + grid, dtype=torch.float32, device=dev)
+    B = torch.empty((P, Nt) + grid, dtype=torch.float32, device=dev)
+    for p in range(P):
+        q = rank * P + p
+        cilgen.make_set(seed, 2 * q, N, grid, device=dev, out=A[p])
+        cilgen.make_set(seed, 2 * q + 1, Nt, grid, device=dev, out=B[p])
+    # radii from the pilot block of the config's first set pair (identical on every rank)
+    A00 = cilgen.make_set(seed, 0, 64, grid, device=dev)
+    B00 = cilgen.make_set(seed, 1, 64, grid, device=dev)
+    radii_np = pilot_radii(A00, B00, grid, M)
+    radii = torch.tensor(radii_np[None, :], dtype=torch.float64, device=dev)
+    torch.cuda.synchronize()
+    log(f"[bench] rank {rank}: generated C2 inputs in {time.time() - t0:.1f}s")
+
+    stream = torch.cuda.current_stream()
+    ws = cil.Workspace()
+    counts = torch.empty((P, 1, M), dtype=torch.int64, device=dev)
+    y = torch.empty((P, 1, M), dtype=torch.float64, device=dev)
+    st = torch.empty((P,), dtype=torch.int32, device=dev)
+    Yg = torch.empty((world * P, M), dtype=torch.float64, device=dev)
+    launches = [0]
+
+    def step():
+        cil.features(A, B, grid, mask, radii, engine=engine, ws=ws, counts=counts, y=y, status=st)
+        n = cil.last_launch_count()
+        if world > 1:
+            import torch.distributed as dist
+            dist.all_gather_into_tensor(Yg, y.view(P, M))
+            Y = Yg
+        else:
+            Y = y.view(P, M)
+        mu, Sig = cil.stats(Y)
+        n += cil.last_launch_count()
+        out, lst = cil.loglik(mu, Sig, y.view(P, M), ridge=0.0)
+        n += cil.last_launch_count()
+        launches[0] += n
+        return out, lst
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if int(st.max()) != 0:
+        log(f"[bench] WARNING item status {st.unique().tolist()}")
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    # ---- timed region (device time, max over ranks)
+    launches[0] = 0
+    barrier()
+    _capi.prof_enable(True)
+    with ClockSampler(local) as clk:
+        ms = timed(step, args.steps, stream)
+    _capi.prof_enable(False)
+    prof = _capi.prof_read()
+    barrier()
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    ms_step = ms / args.steps
+    pairs_step = world * P * N * Nt
+    value = pairs_step / (ms_step * 1e-3)
+    gpu_launches = launches[0]
+
+    # ---- roofline of the dominant kernel (the tensor-core Gram), live CUDA events
+    pk = peaks()
+    K = grid[0] * grid[1] * grid[2]
+    gram_ms, gram_n = prof["gram_tc"]
+    roof = None
+    if gram_n > 0:
+        per_launch_ms = gram_ms / gram_n
+        flops = 3 * 2.0 * P * N * Nt * K      # split-accounted: hi.hi + hi.lo + lo.hi
+        achieved = flops / (per_launch_ms * 1e-3) / 1e12
+        split_tf32 = args.engine == "TC_3XTF32"
+        bf16_peak = pk.get("bf16_tflops", 1590.0)
+        peak = bf16_peak * (0.5 if split_tf32 else 1.0)
+        roof = {"kernel": "k_gram_tc (tcgen05 3x%s Gram + fused binning)" % ("TF32" if split_tf32 else "BF16"),
+                "bound": "tensor", "achieved": round(achieved, 2), "peak": peak, "unit": "TFLOP/s",
+                "frac": round(achieved / peak, 4),
+                "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst)" + (" x 0.5 (tf32 nominal ratio)" if split_tf32 else ""),
+                "frac_vs_sustained": round(achieved / (pk.get("bf16_tflops_sustained", peak) *
+                                                       (0.5 if split_tf32 else 1.0)), 4),
+                "flops_per_launch": flops, "algorithmic_1x_flops_per_launch": flops / 3,
+                "kernel_ms_per_launch": round(per_launch_ms, 4),
+                "kernel_share_of_step": round(gram_ms / ms, 4) if rank == 0 else None,
+                "traffic": traffic_for("C2_gram_tc")}
+    kshares = {k: {"ms_per_step": round(v[0] / args.steps, 4), "launches_per_step": v[1] / args.steps}
+               for k, v in prof.items() if v[1] > 0}
+
+    # ---- end-to-end through the public API with HOST buffers
+    e2e = None
+    if not args.no_e2e:
+        A_h = torch.empty(A.shape, dtype=torch.float32, pin_memory=True)
+        B_h = torch.empty(B.shape, dtype=torch.float32, pin_memory=True)
+        A_h.copy_(A)
+        B_h.copy_(B)
+        out_h = torch.empty((P, 3), dtype=torch.float64, pin_memory=True)
+        y_h = torch.empty((P, 1, M), dtype=torch.float64, pin_memory=True)
+
+        def e2e_step():
+            A.copy_(A_h, non_blocking=True)
+            B.copy_(B_h, non_blocking=True)
+            out, _ = step()
+            out_h.copy_(out, non_blocking=True)
+            y_h.copy_(y, non_blocking=True)
+
+        e2e_step()
+        barrier()
+        e_ms = timed(e2e_step, args.e2e_steps, stream)
+        t = torch.tensor([e_ms], dtype=torch.float64, device=dev)
+        if world > 1:
+            import torch.distributed as dist
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e_ms = float(t.item()) / args.e2e_steps
+        e2e = {"value": pairs_step / (e_ms * 1e-3), "unit": UNIT, "ms_per_step": round(e_ms, 3),
+               "h2d_bytes_per_step": int(A.nbytes + B.nbytes), "d2h_bytes_per_step": int(out_h.nbytes + y_h.nbytes),
+               "steps": args.e2e_steps}
+        del A_h, B_h
+
+    # ---- secondary: C4 (SCIL) loglik evals/s
+    c4 = None
+    if not args.no_c4:
+        c4 = bench_c4(cil, args, world, rank, dev, engine, stream)
+
+    # ---- CPU baseline: the oracle as it stands, bounded sample, rank 0 at N = 1 only
+    cpu = None
+    if not args.no_cpu and world == 1 and rank == 0:
+        rate, cores, sample, dt = oracle_sample_rate(A, B, grid, mask, radii_np[None, :])
+        cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample,
+               "seconds": round(dt, 2)}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16x3 split / f32 accumulate / f64 stats"
+            if args.engine == "TC_3XBF16" else ("tf32x3 split / f32 accumulate / f64 stats"
+                                                if args.engine == "TC_3XTF32" else "f32 / f64"),
+            "data": "synthetic (cilgen-v1 seeded generator, resident in HBM)",
+            "config": {"workload": cfg["workload"], "set_pairs_per_gpu": P, "N": N, "Nt": Nt,
+                       "grid_SHW": list(grid), "M": M, "measures": ["L2"], "engine": args.engine,
+                       "parallelism": f"set pairs sharded over {world} GPU(s), all_gather of y over NCCL"
+                       if world > 1 else "1 GPU",
+                       "l2_flush": "inputs (3.28 GB per GPU) exceed the 126 MB L2; no explicit flush",
+                       "radii": [float(r) for r in radii_np]},
+            "loglik_evals_per_s": world * P / (ms_step * 1e-3),
+            "clocks": clk.summary(),
+            "gpu_launches": gpu_launches,
+            "roofline": roof,
+            "kernel_breakdown": kshares,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "secondary": c4,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def bench_c4(cil, args, world, rank, dev, engine, stream):
+    cfg = C4
+    grid, P, n_ens, N_set, Nt, M = cfg["grid"], cfg["P"], cfg["n_ens"], cfg["N_set"], cfg["N_tilde"], cfg["M"]
+    seed = cilgen.config_seed(4)
+    Nsyn = n_ens * (N_set + Nt)
+    t0 = time.time()
+    pools = torch.empty((P, Nsyn) + grid, dtype=torch.float32, device=dev)
+    rng = np.random.default_rng(seed + rank)
+    for p in range(P):
+        # theta-dependence emulated by the wavelength count and amplitude
+        u = cilgen.uniforms(seed, 5000 + rank * P + p, np.array([0]), 2)[0]
+        cilgen.make_set(seed, rank * P + p, Nsyn, grid, device=dev, out=pools[p], n_w=4.5 + u[0], amp_scale=0.8 + 0.4 * u[1])
+    data = cilgen.make_set(seed, 1000, N_set, grid, device=dev)
+    k0 = torch.tensor([p % n_ens for p in range(P)], dtype=torch.int32, device=dev)
+    radii = torch.tensor(np.stack([pilot_radii(pools[p, :64], pools[p, 64:128], grid, M)[None, :] for p in range(P)]),
+                         dtype=torch.float64, device=dev)
+    torch.cuda.synchronize()
+    log(f"[bench] rank {rank}: generated C4 pools in {time.time() - t0:.1f}s")
+    ws = cil.Workspace()
+    out = torch.empty((P, 3), dtype=torch.float64, device=dev)
+    st = torch.empty((P,), dtype=torch.int32, device=dev)
+
+    def step():
+        cil.synth_loglik(pools, n_ens, N_set, Nt, data, k0, grid, cfg["mask"], radii, ridge=1e-10, engine=engine,
+                         ws=ws, out=out, status=st)
+
+    for _ in range(args.warmup):
+        step()
+    steps = max(3, args.steps // 10)
+    from paper_2203_14742_b200 import _capi
+    _capi.prof_enable(True)
+    ms = timed(step, steps, stream)
+    _capi.prof_enable(False)
+    prof = _capi.prof_read()
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_step = float(t.item()) / steps
+    K = grid[0] * grid[1] * grid[2]
+    rowsA, rowsB = (n_ens + 1) * N_set, n_ens * Nt
+    g_ms, g_n = prof["gram_tc"]
+    res = {"workload": cfg["workload"], "metric": "CIL loglik evals/s", "value": world * P / (ms_step * 1e-3),
+           "ms_per_step": round(ms_step, 3), "steps": steps,
+           "pairs_per_s": world * P * rowsA * rowsB / (ms_step * 1e-3),
+           "nonzero_status": int((st != 0).sum())}
+    if g_n:
+        per = g_ms / g_n
+        ach = 3 * 2.0 * P * rowsA * rowsB * K / (per * 1e-3) / 1e12
+        res["gram_tc"] = {"ms_per_launch": round(per, 4), "achieved_tflops": round(ach, 1),
+                          "frac_of_bf16_burst": round(ach / peaks().get("bf16_tflops", 1590.0), 4)}
+    res["kernel_breakdown"] = {k: round(v[0] / steps, 4) for k, v in prof.items() if v[1] > 0}
+    return res
+
+
+def reference_arm(args, world, rank, cfg, seed, dev):
+    """--impl reference: the FP64 oracle as it stands on the host cores (this tier's
+    reference arm), same metric/config; each step a bounded sample of the workload."""
+    if rank != 0:
+        return
+    grid, N, Nt, M, mask = cfg["grid"], cfg["N"], cfg["Nt"], cfg["M"], cfg["mask"]
+    from oracle import oracle as O
+    O.build()
+    A0 = cilgen.make_set(seed, 0, N, grid)
+    B0 = cilgen.make_set(seed, 1, Nt, grid)
+    radii = pilot_radii(A0, B0, grid, M)[None, :]
+    cores = O.default_threads()
+    a, b = A0.numpy(), B0.numpy()
+    g = (grid[0], grid[1], grid[2], 0.0)
+    rows = cores  # one row per core per step: bounded (~seconds) sample of the workload
+    t0 = time.perf_counter()
+    O.features(a[:rows], b, g, mask, radii, band=0.0, nthreads=cores)
+    per = time.perf_counter() - t0
+    total_budget = 150.0
+    steps, warm = args.steps, args.warmup
+    if (steps + warm) * per > total_budget:
+        steps = max(1, int(total_budget / per) - warm)
+    for _ in range(warm):
+        O.features(a[:rows], b, g, mask, radii, band=0.0, nthreads=cores)
+    t0 = time.perf_counter()
+    for s in range(steps):
+        r0 = (s * rows) % (N - rows + 1)
+        O.features(a[r0:r0 + rows], b, g, mask, radii, band=0.0, nthreads=cores)
+    dt = time.perf_counter() - t0
+    value = steps * rows * Nt / dt
+    sample = f"{rows} rows x all {Nt} of set pair 0 per step (L2 counts, FP64 oracle)"
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps,
+            "warmup": warm, "ms_per_step": round(dt / steps * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (cilgen-v1)",
+            "config": {"workload": cfg["workload"], "grid_SHW": list(grid), "M": M, "measures": ["L2"]},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -185,6 +185,16 @@ CIL_API cil_status cil_diag_gram(const float* A, int64_t lda, int64_t N, const f
                                  size_t ws_bytes, void* stream);
 
 /* ------------------------------------------------------------------------ */
+/* Kernel timing (diagnostics, used by bench.py for the live roofline).  While enabled on
+ * the calling host thread, every kernel the library launches is bracketed by CUDA events
+ * recorded on its launching stream.  cil_prof_read waits for those events and returns, per
+ * kernel class (0 prep, 1 pack, 2 tensor-core Gram, 3 CUDA-core tile engine, 4 L2 re-check,
+ * 5 stats/loglik/SCIL tail), the summed milliseconds ms[6] and launch counts launches[6],
+ * then clears the record.  Returns 6 (the number of classes) or -1 on a CUDA error. */
+CIL_API void cil_prof_enable(int32_t on);
+CIL_API int32_t cil_prof_read(double* ms, int64_t* launches);
+
+/* ------------------------------------------------------------------------ */
 CIL_API const char* cil_status_string(cil_status s);
 CIL_API int32_t cil_last_cuda_error(void);  /* cudaError_t of the last failed call on this thread */
 CIL_API int32_t cil_version(void);          /* MAJOR*10000 + MINOR*100 + PATCH */

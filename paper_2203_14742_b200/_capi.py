@@ -43,6 +43,10 @@ def _load():
     lib.cil_synth_loglik.restype = ctypes.c_int
     lib.cil_diag_gram.argtypes = [P, i64, i64, P, i64, i64, Grid, ctypes.c_int, P, P, sz, P]
     lib.cil_diag_gram.restype = ctypes.c_int
+    lib.cil_prof_enable.argtypes = [i32]
+    lib.cil_prof_enable.restype = None
+    lib.cil_prof_read.argtypes = [P, P]
+    lib.cil_prof_read.restype = i32
     lib.cil_status_string.argtypes = [ctypes.c_int]
     lib.cil_status_string.restype = ctypes.c_char_p
     lib.cil_last_cuda_error.restype = i32
@@ -55,7 +59,22 @@ lib = _load()
 
 EXPORTED = ["cil_features_workspace_size", "cil_features", "cil_stats", "cil_loglik",
             "cil_synth_workspace_size", "cil_synth_loglik", "cil_status_string", "cil_last_cuda_error",
-            "cil_version", "cil_last_launch_count", "cil_diag_gram"]
+            "cil_version", "cil_last_launch_count", "cil_diag_gram", "cil_prof_enable", "cil_prof_read"]
+
+KERNEL_CLASSES = ["prep", "pack", "gram_tc", "simt_tile", "recheck", "tail"]
+
+
+def prof_enable(on: bool):
+    lib.cil_prof_enable(1 if on else 0)
+
+
+def prof_read():
+    """{class: (ms, launches)} accumulated since the last read (waits for the events)."""
+    ms = (ctypes.c_double * 6)()
+    n = (ctypes.c_int64 * 6)()
+    if lib.cil_prof_read(ms, n) < 0:
+        raise CilError("cil_prof_read: CUDA error")
+    return {c: (ms[i], n[i]) for i, c in enumerate(KERNEL_CLASSES)}
 
 
 def check(status: int, what: str):

@@ -2,14 +2,52 @@
 // dispatch of the hot-path kernels on the caller's stream.  No device memory is
 // allocated here and nothing synchronises the device.
 #include <math.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include "cil_internal.cuh"
+
+#include <vector>
 
 namespace cil {
 static thread_local int32_t t_last_cuda = 0;
 static thread_local int32_t t_launches = 0;
 void note_launch(int n) { t_launches += n; }
+
+// ---- optional per-kernel-class event timing (diagnostics for the roofline) ----
+struct ProfRec {
+    int cls;
+    cudaEvent_t a, b;
+};
+static thread_local bool t_prof_on = false;
+static thread_local std::vector<ProfRec>* t_prof = nullptr;
+static thread_local std::vector<cudaEvent_t>* t_evpool = nullptr;
+
+static cudaEvent_t ev_get() {
+    if (!t_evpool) t_evpool = new std::vector<cudaEvent_t>();
+    if (!t_evpool->empty()) {
+        cudaEvent_t e = t_evpool->back();
+        t_evpool->pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+ProfScope::ProfScope(int c, cudaStream_t s) : cls(c), st(s), ev0(nullptr) {
+    if (!t_prof_on) return;
+    cudaEvent_t e = ev_get();
+    cudaEventRecord(e, s);
+    ev0 = e;
+}
+ProfScope::~ProfScope() {
+    if (!ev0) return;
+    cudaEvent_t e = ev_get();
+    cudaEventRecord(e, st);
+    if (!t_prof) t_prof = new std::vector<ProfRec>();
+    t_prof->push_back({cls, (cudaEvent_t)ev0, e});
+}
 }  // namespace cil
 
 using namespace cil;
@@ -203,6 +241,10 @@ cil_status run_engines(int P, const RowSrc& asrc, const RowSrc& bsrc, int64_t ro
         t.guard_k1 = (float)(8.0 * (pl.split == 2 ? ldexp(1.0, -18) : ldexp(1.0, -15)));
         t.guard_rel = (float)(ldexp(1.0, -23) * (8.0 + sqrt((double)K / 16.0)));
         t.diag = diag;
+        {   // diagnostic override for A/B measurements of the tile shape (default: CTA pairs)
+            static const char* cg = getenv("CIL_TC_CTA_GROUP");
+            t.cta_group = (cg && cg[0] == '1') ? 1 : 2;
+        }
         CIL_CU(launch_gram_tc(t, st));
         if (diag) return CIL_OK;
         RecheckArgs r{};
@@ -375,6 +417,24 @@ const char* cil_status_string(cil_status s) {
         case CIL_ECUDA: return "CIL_ECUDA: CUDA launch failed (see cil_last_cuda_error)";
     }
     return "unknown cil_status";
+}
+
+void cil_prof_enable(int32_t on) { t_prof_on = on != 0; }
+
+int32_t cil_prof_read(double* ms, int64_t* launches) {
+    for (int c = 0; c < K_NCLASS; ++c) { ms[c] = 0.0; launches[c] = 0; }
+    if (!t_prof) return 0;
+    for (const ProfRec& r : *t_prof) {
+        if (cudaEventSynchronize(r.b) != cudaSuccess) return -1;
+        float t = 0.f;
+        cudaEventElapsedTime(&t, r.a, r.b);
+        ms[r.cls] += t;
+        launches[r.cls] += 1;
+        t_evpool->push_back(r.a);
+        t_evpool->push_back(r.b);
+    }
+    t_prof->clear();
+    return K_NCLASS;
 }
 
 int32_t cil_last_cuda_error(void) { return t_last_cuda; }

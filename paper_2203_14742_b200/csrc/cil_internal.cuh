@@ -97,6 +97,18 @@ __host__ __device__ inline int64_t hist_index(const SegParams& sp, int nq, int M
 // Launch bookkeeping (per host thread).
 void note_launch(int n = 1);
 
+// Kernel classes for the optional event timing (cil_prof_*).
+enum KClass : int { K_PREP = 0, K_PACK = 1, K_GRAM_TC = 2, K_SIMT = 3, K_RECHECK = 4, K_TAIL = 5, K_NCLASS = 6 };
+// RAII: when profiling is enabled on this thread, brackets the enclosed launch with
+// CUDA events recorded on the launching stream.
+struct ProfScope {
+    int cls;
+    cudaStream_t st;
+    void* ev0;
+    ProfScope(int c, cudaStream_t s);
+    ~ProfScope();
+};
+
 }  // namespace cil
 
 // ---- launchers implemented in the .cu files ----
@@ -149,6 +161,7 @@ struct TcArgs {
     const int32_t* status;
     float guard_k1, guard_rel;
     float* diag;                        // diagnostics only (see cil_diag_gram)
+    int cta_group;                      // 2 (default): CTA-pair 256x256 tiles; 1: single-CTA 128x256
 };
 cudaError_t launch_gram_tc(const TcArgs& a, cudaStream_t st);
 bool gram_tc_supported();

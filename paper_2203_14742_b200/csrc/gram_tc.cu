@@ -26,16 +26,23 @@
 namespace cil {
 
 namespace tc {
-constexpr int BM = 128;
-constexpr int BN = 256;
-constexpr int STAGES = 2;
-constexpr int ROW_BYTES = 128;                       // K bytes per stage row (one SW128 atom row)
-constexpr int A_BYTES = BM * ROW_BYTES;              // 16 KB
-constexpr int B_BYTES = BN * ROW_BYTES;              // 32 KB
-constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
+// Tile geometry.  CG = CTAs per MMA (cta_group): the cluster tile is (128*CG) x 256;
+// every CTA holds 128 A-rows and 256/CG B-rows of each operand stage, and its TMEM holds
+// the FP32 accumulator of its own 128 rows x all 256 columns (double-buffered).
+constexpr int A_ROWS = 128;
+constexpr int TILE_N = 256;
+constexpr int ROW_BYTES = 128;                         // K bytes per stage row (one SW128 atom row)
 constexpr int NTHREADS = 192;
-constexpr int TMEM_COLS = 2 * BN;                    // double-buffered accumulator
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 1024 /*barriers, norms*/ + 2 * BN * 4;
+constexpr int TMEM_COLS = 2 * TILE_N;
+template <int CG> struct Geo {
+    static constexpr int TILE_M = 128 * CG;
+    static constexpr int B_ROWS = TILE_N / CG;
+    static constexpr int A_BYTES = A_ROWS * ROW_BYTES;
+    static constexpr int B_BYTES = B_ROWS * ROW_BYTES;
+    static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
+    static constexpr int STAGES = CG == 1 ? 2 : 3;
+    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 1024 /*barriers*/ + 2 * TILE_N * 4;
+};
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -48,6 +55,15 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
 }
+// arrive on the barrier at the same smem offset in cluster CTA `rank` (release at cluster scope)
+__device__ __forceinline__ void mbar_arrive_remote(uint64_t* b, uint32_t rank) {
+    asm volatile(
+        "{\n.reg .b32 ra;\n"
+        "mapa.shared::cluster.u32 ra, %0, %1;\n"
+        "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n}\n" ::"r"(smem_u32(b)),
+        "r"(rank)
+        : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
     asm volatile(
         "{\n"
@@ -59,15 +75,42 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y) {
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* b, uint32_t parity) {
     asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-            smem_u32(dst)),
-        "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar))
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(b)),
+        "r"(parity)
         : "memory");
+}
+template <int CG>
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y) {
+    if (CG == 1)
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+                "r"(smem_u32(dst)),
+            "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar))
+            : "memory");
+    else   // both CTAs of the pair signal the leader's barrier (peer bit cleared)
+        asm volatile(
+            "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes "
+            "[%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+            "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar) & 0xFEFFFFFFu)
+            : "memory");
 }
 __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
 
 // K-major, SWIZZLE_128B shared-memory matrix descriptor (sm_100 "version 1" format):
 // start>>4 [0,14), LBO>>4 [16,30) (unused for swizzled K-major), SBO>>4 [32,46) = 1024 B
@@ -81,21 +124,39 @@ __host__ __device__ constexpr uint32_t idesc(int fmt, int M, int N) {
     return (1u << 4) | ((uint32_t)fmt << 7) | ((uint32_t)fmt << 10) | ((uint32_t)(N >> 3) << 17) |
            ((uint32_t)(M >> 4) << 24);
 }
+template <int CG>
 __device__ __forceinline__ void mma(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc, int kind_tf32) {
-    if (kind_tf32)
-        asm volatile(
-            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-            "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
-            "l"(a), "l"(b), "r"(id), "r"(acc));
-    else
-        asm volatile(
-            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
-            "l"(a), "l"(b), "r"(id), "r"(acc));
+    if (CG == 1) {
+        if (kind_tf32)
+            asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                         "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+                         "l"(a), "l"(b), "r"(id), "r"(acc));
+        else
+            asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                         "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+                         "l"(a), "l"(b), "r"(id), "r"(acc));
+    } else {
+        if (kind_tf32)
+            asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                         "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+                         "l"(a), "l"(b), "r"(id), "r"(acc));
+        else
+            asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                         "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+                         "l"(a), "l"(b), "r"(id), "r"(acc));
+    }
 }
+// MMA completion -> mbarrier (both CTAs of the pair for CG = 2)
+template <int CG>
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-                 : "memory");
+    if (CG == 1)
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                     : "memory");
+    else
+        asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::
+                         "r"(smem_u32(bar)),
+                     "h"((uint16_t)3)
+                     : "memory");
 }
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
     asm volatile(
@@ -115,7 +176,7 @@ struct TcParams {
     int64_t rowsA, rowsB;     // rows per item of the A / B panel
     int P;
     int n_kb;                 // k-blocks of 128 bytes
-    int tiles_m, tiles_n;     // per item
+    int tiles_m, tiles_n;     // per item (cluster tiles)
     int split;                // 1 = bf16, 2 = tf32
     const float* nrm;         // stacked [P*rowsA + P*rowsB]
     const float* q4;
@@ -129,28 +190,31 @@ struct TcParams {
     float* diag;              // diagnostics: [rowsA][rowsB][2] = (d2, E) of item 0, no binning
 };
 
-template <int MAXM>
+template <int MAXM, int CG>
 __global__ void __launch_bounds__(NTHREADS, 1)
 k_gram_tc(const __grid_constant__ CUtensorMap mAhi, const __grid_constant__ CUtensorMap mAlo,
           const __grid_constant__ CUtensorMap mBhi, const __grid_constant__ CUtensorMap mBlo, TcParams prm) {
+    using G = Geo<CG>;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = reinterpret_cast<unsigned char*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     unsigned char* stages = smem;
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
-    uint64_t* empty = full + STAGES;
-    uint64_t* tfull = empty + STAGES;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + G::STAGES * G::STAGE_BYTES);
+    uint64_t* empty = full + G::STAGES;
+    uint64_t* tfull = empty + G::STAGES;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-    float* s_nb = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 1024);
-    float* s_qb = s_nb + BN;
+    float* s_nb = reinterpret_cast<float*>(smem + G::STAGES * G::STAGE_BYTES + 1024);
+    float* s_qb = s_nb + TILE_N;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = CG == 2 ? cluster_rank() : 0u;
+    const int cluster_id = blockIdx.x / CG, n_clusters = gridDim.x / CG;
     const int tiles_per_item = prm.tiles_m * prm.tiles_n;
     const int total_tiles = prm.P * tiles_per_item;
 
     if (warp == 0 && lane == 0) {
-        for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-        for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 4); }
+        for (int s = 0; s < G::STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+        for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 4 * CG); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&mAhi) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&mAlo) : "memory");
@@ -158,12 +222,18 @@ k_gram_tc(const __grid_constant__ CUtensorMap mAhi, const __grid_constant__ CUte
         asm volatile("prefetch.tensormap [%0];" ::"l"(&mBlo) : "memory");
     }
     if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "r"(TMEM_COLS));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        if (CG == 1) {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                         "r"(TMEM_COLS));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                         "r"(TMEM_COLS));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+        }
     }
     fence_before();
-    __syncthreads();
+    if (CG == 2) cluster_sync(); else __syncthreads();
     fence_after();
     const uint32_t tmem_base = *tmem_slot;
     const int kind_tf32 = prm.split == 2;
@@ -173,52 +243,53 @@ k_gram_tc(const __grid_constant__ CUtensorMap mAhi, const __grid_constant__ CUte
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
-            for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+            for (int t = cluster_id; t < total_tiles; t += n_clusters) {
                 const int p = t / tiles_per_item, r = t % tiles_per_item;
                 const int mt = r / prm.tiles_n, nt = r % prm.tiles_n;
-                const int ya = (int)(p * prm.rowsA + (int64_t)mt * BM);
-                const int yb = (int)((int64_t)prm.P * prm.rowsA + p * prm.rowsB + (int64_t)nt * BN);
+                const int ya = (int)(p * prm.rowsA + (int64_t)mt * G::TILE_M + rank * A_ROWS);
+                const int yb = (int)((int64_t)prm.P * prm.rowsA + p * prm.rowsB + (int64_t)nt * TILE_N + rank * G::B_ROWS);
                 for (int kb = 0; kb < prm.n_kb; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
-                    unsigned char* st = stages + stage * STAGE_BYTES;
-                    mbar_expect_tx(&full[stage], STAGE_BYTES);
+                    unsigned char* st = stages + stage * G::STAGE_BYTES;
+                    if (rank == 0) mbar_expect_tx(&full[stage], CG * G::STAGE_BYTES);
                     const int x = kb * bkE;
-                    tma_load_2d(st, &mAhi, &full[stage], x, ya);
-                    tma_load_2d(st + A_BYTES, &mAlo, &full[stage], x, ya);
-                    tma_load_2d(st + 2 * A_BYTES, &mBhi, &full[stage], x, yb);
-                    tma_load_2d(st + 2 * A_BYTES + B_BYTES, &mBlo, &full[stage], x, yb);
-                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                    tma_load_2d<CG>(st, &mAhi, &full[stage], x, ya);
+                    tma_load_2d<CG>(st + G::A_BYTES, &mAlo, &full[stage], x, ya);
+                    tma_load_2d<CG>(st + 2 * G::A_BYTES, &mBhi, &full[stage], x, yb);
+                    tma_load_2d<CG>(st + 2 * G::A_BYTES + G::B_BYTES, &mBlo, &full[stage], x, yb);
+                    if (++stage == G::STAGES) { stage = 0; phase ^= 1; }
                 }
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
-            const uint32_t id = idesc(kind_tf32 ? 2 : 1, BM, BN);
+        if (lane == 0 && rank == 0) {
+            const uint32_t id = idesc(kind_tf32 ? 2 : 1, G::TILE_M, TILE_N);
             int stage = 0;
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
-            for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
-                mbar_wait(&tempty[acc], acc_phase ^ 1);
+            for (int t = cluster_id; t < total_tiles; t += n_clusters) {
+                if (CG == 2) mbar_wait_cluster(&tempty[acc], acc_phase ^ 1);
+                else mbar_wait(&tempty[acc], acc_phase ^ 1);
                 fence_after();
-                const uint32_t d = tmem_base + (uint32_t)(acc * BN);
+                const uint32_t d = tmem_base + (uint32_t)(acc * TILE_N);
                 for (int kb = 0; kb < prm.n_kb; ++kb) {
                     mbar_wait(&full[stage], phase);
                     fence_after();
-                    const uint32_t s0 = smem_u32(stages + stage * STAGE_BYTES);
-                    const uint64_t ahi = sdesc(s0), alo = sdesc(s0 + A_BYTES);
-                    const uint64_t bhi = sdesc(s0 + 2 * A_BYTES), blo = sdesc(s0 + 2 * A_BYTES + B_BYTES);
+                    const uint32_t s0 = smem_u32(stages + stage * G::STAGE_BYTES);
+                    const uint64_t ahi = sdesc(s0), alo = sdesc(s0 + G::A_BYTES);
+                    const uint64_t bhi = sdesc(s0 + 2 * G::A_BYTES), blo = sdesc(s0 + 2 * G::A_BYTES + G::B_BYTES);
 #pragma unroll
                     for (int k = 0; k < 4; ++k) {           // 4 x 32 bytes of K per 128-byte row
                         const uint64_t adv = (uint64_t)(k * 2);  // +32 B in the start-address field (>>4)
-                        mma(d, ahi + adv, bhi + adv, id, (kb | k) != 0, kind_tf32);
-                        mma(d, ahi + adv, blo + adv, id, 1u, kind_tf32);
-                        mma(d, alo + adv, bhi + adv, id, 1u, kind_tf32);
+                        mma<CG>(d, ahi + adv, bhi + adv, id, (kb | k) != 0, kind_tf32);
+                        mma<CG>(d, ahi + adv, blo + adv, id, 1u, kind_tf32);
+                        mma<CG>(d, alo + adv, bhi + adv, id, 1u, kind_tf32);
                     }
-                    mma_commit(&empty[stage]);
-                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                    mma_commit<CG>(&empty[stage]);
+                    if (++stage == G::STAGES) { stage = 0; phase ^= 1; }
                 }
-                mma_commit(&tfull[acc]);
+                mma_commit<CG>(&tfull[acc]);
                 if (++acc == 2) { acc = 0; acc_phase ^= 1; }
             }
         }
@@ -229,13 +300,13 @@ k_gram_tc(const __grid_constant__ CUtensorMap mAhi, const __grid_constant__ CUte
         const int M = prm.M;
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+        for (int t = cluster_id; t < total_tiles; t += n_clusters) {
             const int p = t / tiles_per_item, r = t % tiles_per_item;
             const int mt = r / prm.tiles_n, nt = r % prm.tiles_n;
-            const int64_t col0 = (int64_t)nt * BN;
+            const int64_t col0 = (int64_t)nt * TILE_N;
             const int64_t browbase = (int64_t)prm.P * prm.rowsA + (int64_t)p * prm.rowsB;
             named_bar(1, 128);
-            for (int j = et; j < BN; j += 128) {
+            for (int j = et; j < TILE_N; j += 128) {
                 const int64_t c = col0 + j;
                 const bool ok = c < prm.rowsB;
                 s_nb[j] = ok ? prm.nrm[browbase + c] : 0.f;
@@ -245,7 +316,7 @@ k_gram_tc(const __grid_constant__ CUtensorMap mAhi, const __grid_constant__ CUte
             float T[MAXM];
 #pragma unroll
             for (int m = 0; m < MAXM; ++m) T[m] = (m < M) ? __ldg(&prm.thr2[(int64_t)p * prm.thr_stride + m]) : -INFINITY;
-            const int64_t row = (int64_t)mt * BM + quarter * 32 + lane;
+            const int64_t row = (int64_t)mt * G::TILE_M + rank * A_ROWS + quarter * 32 + lane;
             const bool row_ok = row < prm.rowsA;
             const int64_t arow = (int64_t)p * prm.rowsA + (row_ok ? row : 0);
             const float na = row_ok ? __ldg(&prm.nrm[arow]) : 0.f;
@@ -288,9 +359,9 @@ k_gram_tc(const __grid_constant__ CUtensorMap mAhi, const __grid_constant__ CUte
             mbar_wait(&tfull[acc], acc_phase);
             fence_after();
             int64_t cur_cs = col0 / prm.sp.col_seg;
-            const uint32_t taddr0 = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN);
+            const uint32_t taddr0 = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * TILE_N);
 #pragma unroll 1
-            for (int ch = 0; ch < BN / 32; ++ch) {
+            for (int ch = 0; ch < TILE_N / 32; ++ch) {
                 uint32_t v[32];
                 tmem_ld32(taddr0 + ch * 32, v);
                 if (col0 + ch * 32 >= prm.rowsB) break;    // warp-uniform
@@ -334,15 +405,22 @@ k_gram_tc(const __grid_constant__ CUtensorMap mAhi, const __grid_constant__ CUte
             }
             fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[acc]);
+            if (lane == 0) {
+                if (CG == 2) mbar_arrive_remote(&tempty[acc], 0);
+                else mbar_arrive(&tempty[acc]);
+            }
             flush(cur_cs);
             if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         }
     }
     __syncthreads();
+    if (CG == 2) cluster_sync();
     if (warp == 1) {
         fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
+        if (CG == 1)
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
+        else
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
     }
 }
 }  // namespace tc
@@ -381,38 +459,56 @@ static bool make_map(CUtensorMap* m, const void* base, int split, int64_t rows, 
     return r == CUDA_SUCCESS;
 }
 
-template <int MAXM>
-static cudaError_t launch_t(const TcArgs& a, const tc::TcParams& prm, const CUtensorMap* maps, int grid,
-                            cudaStream_t st) {
+template <int MAXM, int CG>
+static cudaError_t launch_t(const tc::TcParams& prm, const CUtensorMap* maps, int nsm, cudaStream_t st) {
+    using G = tc::Geo<CG>;
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(tc::k_gram_tc<MAXM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             tc::SMEM_BYTES);
+        cudaError_t e = cudaFuncSetAttribute(tc::k_gram_tc<MAXM, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             G::SMEM_BYTES);
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    tc::k_gram_tc<MAXM><<<grid, tc::NTHREADS, tc::SMEM_BYTES, st>>>(maps[0], maps[1], maps[2], maps[3], prm);
+    const int64_t tiles = (int64_t)prm.P * prm.tiles_m * prm.tiles_n;
+    const int clusters = (int)(tiles < nsm / CG ? tiles : nsm / CG);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)(clusters * CG));
+    cfg.blockDim = dim3(tc::NTHREADS);
+    cfg.dynamicSmemBytes = G::SMEM_BYTES;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CG;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    ProfScope ps_(K_GRAM_TC, st);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, tc::k_gram_tc<MAXM, CG>, maps[0], maps[1], maps[2], maps[3], prm);
     note_launch();
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 
-cudaError_t launch_gram_tc(const TcArgs& a, cudaStream_t st) {
-    if (a.rowsA == 0 || a.rowsB == 0) return cudaSuccess;
+template <int CG>
+static cudaError_t launch_cg(const TcArgs& a, cudaStream_t st) {
+    using G = tc::Geo<CG>;
     const int64_t rows = (int64_t)a.P * (a.rowsA + a.rowsB);
     if (rows >= (1ll << 31)) return cudaErrorInvalidValue;
     const size_t esz = a.split == 2 ? 4 : 2;
     const char* hi = static_cast<const char*>(a.hi);
     const char* lo = static_cast<const char*>(a.lo);
     CUtensorMap maps[4];
-    if (!make_map(&maps[0], hi, a.split, rows, a.Kp, tc::BM) || !make_map(&maps[1], lo, a.split, rows, a.Kp, tc::BM) ||
-        !make_map(&maps[2], hi, a.split, rows, a.Kp, tc::BN) || !make_map(&maps[3], lo, a.split, rows, a.Kp, tc::BN))
+    if (!make_map(&maps[0], hi, a.split, rows, a.Kp, tc::A_ROWS) ||
+        !make_map(&maps[1], lo, a.split, rows, a.Kp, tc::A_ROWS) ||
+        !make_map(&maps[2], hi, a.split, rows, a.Kp, G::B_ROWS) ||
+        !make_map(&maps[3], lo, a.split, rows, a.Kp, G::B_ROWS))
         return cudaErrorInvalidValue;
-    (void)esz;
     tc::TcParams prm{};
     prm.rowsA = a.rowsA; prm.rowsB = a.rowsB; prm.P = a.P;
     prm.n_kb = (int)((a.Kp * (int64_t)esz) / tc::ROW_BYTES);
-    prm.tiles_m = (int)((a.rowsA + tc::BM - 1) / tc::BM);
-    prm.tiles_n = (int)((a.rowsB + tc::BN - 1) / tc::BN);
+    prm.tiles_m = (int)((a.rowsA + G::TILE_M - 1) / G::TILE_M);
+    prm.tiles_n = (int)((a.rowsB + tc::TILE_N - 1) / tc::TILE_N);
     prm.split = a.split;
     prm.nrm = a.nrm; prm.q4 = a.q4;
     prm.thr2 = a.thr2; prm.thr_stride = a.thr_stride;
@@ -425,11 +521,16 @@ cudaError_t launch_gram_tc(const TcArgs& a, cudaStream_t st) {
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    const int64_t tiles = (int64_t)a.P * prm.tiles_m * prm.tiles_n;
-    const int grid = (int)(tiles < nsm ? tiles : nsm);
-    if (a.M <= 16) return launch_t<16>(a, prm, maps, grid, st);
-    if (a.M <= 32) return launch_t<32>(a, prm, maps, grid, st);
-    return launch_t<64>(a, prm, maps, grid, st);
+    if (a.M <= 16) return launch_t<16, CG>(prm, maps, nsm, st);
+    if (a.M <= 32) return launch_t<32, CG>(prm, maps, nsm, st);
+    return launch_t<64, CG>(prm, maps, nsm, st);
+}
+
+cudaError_t launch_gram_tc(const TcArgs& a, cudaStream_t st) {
+    if (a.rowsA == 0 || a.rowsB == 0) return cudaSuccess;
+    // CTA pairs (cta_group::2, 256 x 256 tiles) unless explicitly forced to single-CTA tiles
+    if (a.cta_group == 1) return launch_cg<1>(a, st);
+    return launch_cg<2>(a, st);
 }
 
 }  // namespace cil

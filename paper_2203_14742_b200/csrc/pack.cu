@@ -54,6 +54,7 @@ cudaError_t launch_prep(int P, int nq, int M, const double* radii, int64_t radii
         e = cudaMemsetAsync(recheck_ctr, 0, sizeof(uint32_t) * 2, st);
         if (e != cudaSuccess) return e;
     }
+    ProfScope ps_(K_PREP, st);
     k_prep<<<P, 128, 0, st>>>(P, nq, M, radii, radii_stride, bp, thr, thr2_l2, status);
     note_launch();
     return cudaGetLastError();
@@ -76,6 +77,7 @@ __global__ void k_center(RowSrc src, int64_t nrc, int64_t K, int64_t Kp, float* 
 cudaError_t launch_center(int P, const RowSrc& colsrc, int64_t nrc, int64_t K, int64_t Kp,
                           float* center, cudaStream_t st) {
     dim3 grid((unsigned)((Kp + 255) / 256), (unsigned)P);
+    ProfScope ps_(K_PACK, st);
     k_center<<<grid, 256, 0, st>>>(colsrc, nrc, K, Kp, center);
     note_launch();
     return cudaGetLastError();
@@ -167,6 +169,7 @@ cudaError_t launch_pack_tc(int P, const RowSrc& src, int64_t rows, int64_t K, in
                            int32_t* status, cudaStream_t st) {
     if (rows == 0) return cudaSuccess;
     dim3 grid((unsigned)rows, (unsigned)P);
+    ProfScope ps_(K_PACK, st);
     if (split == 2)
         k_pack_tc<2><<<grid, 256, 0, st>>>(src, rows, K, Kp, center, hi, lo, nrm, q4, status);
     else
@@ -225,6 +228,7 @@ cudaError_t launch_pack_aug(int P, const RowSrc& src, int64_t rows, const AugGeo
                             int32_t* status, cudaStream_t st) {
     if (rows == 0) return cudaSuccess;
     dim3 grid((unsigned)rows, (unsigned)P);
+    ProfScope ps_(K_PACK, st);
     k_pack_aug<<<grid, 256, 0, st>>>(src, rows, g, out, status);
     note_launch();
     return cudaGetLastError();

@@ -46,6 +46,7 @@ __global__ void __launch_bounds__(256) k_recheck(RecheckArgs a) {
 }
 
 cudaError_t launch_recheck(const RecheckArgs& a, cudaStream_t st) {
+    ProfScope ps_(K_RECHECK, st);
     k_recheck<<<296, 256, 0, st>>>(a);
     note_launch();
     return cudaGetLastError();

@@ -253,6 +253,7 @@ static cudaError_t launch_simt_t(const SimtArgs& a, cudaStream_t st) {
         attr_done = true;
     }
     dim3 grid((unsigned)((a.rowsB + TB - 1) / TB), (unsigned)((a.rowsA + TA - 1) / TA), (unsigned)a.P);
+    ProfScope ps_(K_SIMT, st);
     k_simt<X, Y><<<grid, NTHR, sm, st>>>(a);
     note_launch();
     return cudaGetLastError();

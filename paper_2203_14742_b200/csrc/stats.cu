@@ -25,6 +25,7 @@ __global__ void k_finalize(int nq, int M, SegParams sp, const uint64_t* __restri
 cudaError_t launch_finalize(int P, int nq, int M, const SegParams& sp, const uint64_t* hist,
                             uint64_t* counts, double* y, int64_t rows, int64_t cols,
                             const int32_t*, int32_t*, cudaStream_t st) {
+    ProfScope ps_(K_TAIL, st);
     k_finalize<<<P, 128, 0, st>>>(nq, M, sp, hist, counts, y, (double)rows * (double)cols);
     note_launch();
     return cudaGetLastError();
@@ -57,6 +58,7 @@ __global__ void k_cov(const double* __restrict__ Y, int64_t y_stride, int n, int
 
 static cudaError_t launch_stats_strided(int P, const double* Y, int64_t y_stride, int n, int D,
                                         double* mu, double* Sigma, cudaStream_t st) {
+    ProfScope ps_(K_TAIL, st);
     k_mean<<<P, 128, 0, st>>>(Y, y_stride, n, D, mu);
     note_launch();
     dim3 g((unsigned)D, (unsigned)P);
@@ -163,6 +165,7 @@ static cudaError_t launch_loglik_strided(int P, const double* mu, int64_t mu_str
         if (e != cudaSuccess) return e;
         attr = true;
     }
+    ProfScope ps_(K_TAIL, st);
     k_loglik<<<P, kLogThreads, smem, st>>>(mu, mu_stride, Sigma, Sigma_stride, y, y_stride, D, ridge, out,
                                            status, status_in);
     note_launch();
@@ -210,7 +213,10 @@ cudaError_t launch_synth_tail(int P, int n_ens, int nq, int M, const SegParams& 
                               int32_t* status, double* Y, double* mu, double* Sigma, cudaStream_t st) {
     const int nv = n_ens * n_ens, D = nq * M;
     dim3 g((unsigned)(nv + 1), (unsigned)P);
-    k_build_Y<<<g, 128, 0, st>>>(n_ens, nq, M, sp, hist, (double)N_set * (double)N_tilde, k0, Y, status);
+    {
+        ProfScope ps_(K_TAIL, st);
+        k_build_Y<<<g, 128, 0, st>>>(n_ens, nq, M, sp, hist, (double)N_set * (double)N_tilde, k0, Y, status);
+    }
     note_launch();
     cudaError_t e = launch_stats_strided(P, Y, (int64_t)(nv + 1) * D, nv, D, mu, Sigma, st);
     if (e != cudaSuccess) return e;
