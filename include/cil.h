@@ -122,6 +122,13 @@ CIL_API cil_status cil_features(int32_t P,
                         cil_engine engine, void* ws, size_t ws_bytes, void* stream);
 
 /* ------------------------------------------------------------------------ */
+/* cil_normalize — y[i] = (double)counts[i] / npairs for i < n (the 1/(N x N~) of Eq. (1),
+ * PAPER.md:98).  Used after an all-reduce of row-block-sharded counts (each rank's
+ * cil_features normalises by its own shard only).  counts uint64 [n], y FP64 [n], device;
+ * npairs > 0. */
+CIL_API cil_status cil_normalize(int64_t n, const uint64_t* counts, double npairs, double* y, void* stream);
+
+/* ------------------------------------------------------------------------ */
 /* cil_stats — mu and Sigma of n realisations (Alg. 1 step 3,
  * PAPER.md:131), batched over P:
  *   mu[p][a]       = (1/n) sum_v Y[p][v][a]

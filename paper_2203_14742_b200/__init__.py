@@ -139,6 +139,14 @@ def features(A, B, grid, mask, radii, *, engine=ENGINE_AUTO, want_y=True, stream
     return counts, (y if want_y else None), status
 
 
+def normalize(counts, npairs: float, *, stream=None):
+    """y = counts / npairs on the device (cil_normalize; Eq. (1) normalisation)."""
+    c = counts.contiguous()
+    y = torch.empty(c.shape, dtype=torch.float64, device=c.device)
+    check(lib.cil_normalize(c.numel(), c.data_ptr(), float(npairs), y.data_ptr(), _stream(stream)), "cil_normalize")
+    return y
+
+
 def stats(Y, *, stream=None):
     """mu [P,D], Sigma [P,D,D] of Y [P,n,D] (or [n,D]) — PAPER.md:111."""
     squeeze = Y.dim() == 2

@@ -43,6 +43,8 @@ def _load():
     lib.cil_synth_loglik.restype = ctypes.c_int
     lib.cil_diag_gram.argtypes = [P, i64, i64, P, i64, i64, Grid, ctypes.c_int, P, P, sz, P]
     lib.cil_diag_gram.restype = ctypes.c_int
+    lib.cil_normalize.argtypes = [i64, P, f64, P, P]
+    lib.cil_normalize.restype = ctypes.c_int
     lib.cil_prof_enable.argtypes = [i32]
     lib.cil_prof_enable.restype = None
     lib.cil_prof_read.argtypes = [P, P]
@@ -59,7 +61,7 @@ lib = _load()
 
 EXPORTED = ["cil_features_workspace_size", "cil_features", "cil_stats", "cil_loglik",
             "cil_synth_workspace_size", "cil_synth_loglik", "cil_status_string", "cil_last_cuda_error",
-            "cil_version", "cil_last_launch_count", "cil_diag_gram", "cil_prof_enable", "cil_prof_read"]
+            "cil_version", "cil_last_launch_count", "cil_diag_gram", "cil_prof_enable", "cil_prof_read", "cil_normalize"]
 
 KERNEL_CLASSES = ["prep", "pack", "gram_tc", "simt_tile", "recheck", "tail"]
 

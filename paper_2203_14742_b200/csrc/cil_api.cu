@@ -238,13 +238,21 @@ cil_status run_engines(int P, const RowSrc& asrc, const RowSrc& bsrc, int64_t ro
         // Error bound of the split Gram (DESIGN.md §L2 engine): E = k1 q_a q_b + rel (n_a + n_b)
         //   k1: 8 sigma of the split residual (2^-16 per product for 3xBF16, 2^-20 for 3xTF32, x2 for d^2)
         //   rel: FP32 evaluation / threshold rounding / centring + accumulation over K/16 MMA steps
-        t.guard_k1 = (float)(8.0 * (pl.split == 2 ? ldexp(1.0, -18) : ldexp(1.0, -15)));
-        t.guard_rel = (float)(ldexp(1.0, -23) * (8.0 + sqrt((double)K / 16.0)));
-        t.diag = diag;
-        {   // diagnostic override for A/B measurements of the tile shape (default: CTA pairs)
+        {   // diagnostic overrides for A/B measurements (defaults: CTA pairs, 4-k-block chunks)
             static const char* cg = getenv("CIL_TC_CTA_GROUP");
+            static const char* ck = getenv("CIL_TC_CHUNK_KB");
             t.cta_group = (cg && cg[0] == '1') ? 1 : 2;
+            t.chunk_kb = ck ? atoi(ck) : 4;
+            if (t.chunk_kb < 1) t.chunk_kb = 1;
         }
+        // E = k1 q_a q_b + rel (n_a + n_b): k1 = 8 sigma of the split residual (2^-16 per product
+        // for 3xBF16, 2^-20 for 3xTF32, x2 for d^2); rel = truncation over the 12*chunk_kb MMA steps
+        // of one chunk + RN adds of the chunk partials + FP32 evaluation / threshold rounding.
+        const int64_t n_kb = (L.Kp * (int64_t)esz) / 128;
+        const double nchunks = (double)((n_kb + t.chunk_kb - 1) / t.chunk_kb);
+        t.guard_k1 = (float)(8.0 * (pl.split == 2 ? ldexp(1.0, -18) : ldexp(1.0, -15)));
+        t.guard_rel = (float)(ldexp(1.0, -24) * (8.0 * t.chunk_kb + 3.0 * sqrt(nchunks) + 8.0));
+        t.diag = diag;
         CIL_CU(launch_gram_tc(t, st));
         if (diag) return CIL_OK;
         RecheckArgs r{};
@@ -304,6 +312,13 @@ cil_status cil_features(int32_t P, const float* A, int64_t strideA, int64_t lda,
     if (s != CIL_OK) return s;
     CIL_CU(launch_finalize(P, sl.nq, M, sp, at<uint64_t>(wsa, L.off_hist), counts, y, N, Nt, nullptr,
                            nullptr, st));
+    return CIL_OK;
+}
+
+cil_status cil_normalize(int64_t n, const uint64_t* counts, double npairs, double* y, void* stream) {
+    t_launches = 0;
+    if (n < 0 || (n > 0 && (!counts || !y)) || !(npairs > 0.0)) return CIL_EINVAL;
+    CIL_CU(launch_normalize(n, counts, npairs, y, reinterpret_cast<cudaStream_t>(stream)));
     return CIL_OK;
 }
 

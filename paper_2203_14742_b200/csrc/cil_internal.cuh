@@ -162,6 +162,7 @@ struct TcArgs {
     float guard_k1, guard_rel;
     float* diag;                        // diagnostics only (see cil_diag_gram)
     int cta_group;                      // 2 (default): CTA-pair 256x256 tiles; 1: single-CTA 128x256
+    int chunk_kb;                       // k-blocks per TMEM partial accumulation (precision control)
 };
 cudaError_t launch_gram_tc(const TcArgs& a, cudaStream_t st);
 bool gram_tc_supported();
@@ -189,6 +190,7 @@ cudaError_t launch_finalize(int P, int nq, int M, const SegParams& sp, const uin
                             int32_t* status_out, cudaStream_t st);
 cudaError_t launch_stats(int P, const double* Y, int n, int D, double* mu, double* Sigma,
                          cudaStream_t st);
+cudaError_t launch_normalize(int64_t n, const uint64_t* counts, double npairs, double* y, cudaStream_t st);
 cudaError_t launch_loglik(int P, const double* mu, int64_t mu_stride, const double* Sigma,
                           int64_t Sigma_stride, const double* y, int D, double ridge, double* out,
                           int32_t* status, const int32_t* status_in, cudaStream_t st);

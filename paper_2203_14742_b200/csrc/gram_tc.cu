@@ -20,6 +20,7 @@
 //               ambiguous pairs -> re-check list; double-buffered TMEM accumulator so the
 //               epilogue of tile t overlaps the MMAs of tile t+1.
 #include <cuda.h>
+#include <stdio.h>
 
 #include "cil_internal.cuh"
 
@@ -32,7 +33,7 @@ namespace tc {
 constexpr int A_ROWS = 128;
 constexpr int TILE_N = 256;
 constexpr int ROW_BYTES = 128;                         // K bytes per stage row (one SW128 atom row)
-constexpr int NTHREADS = 192;
+constexpr int NTHREADS = 320;                          // TMA warp, MMA warp, 8 epilogue warps
 constexpr int TMEM_COLS = 2 * TILE_N;
 template <int CG> struct Geo {
     static constexpr int TILE_M = 128 * CG;
@@ -170,6 +171,15 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
         : "r"(taddr));
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 struct TcParams {
@@ -188,10 +198,25 @@ struct TcParams {
     uint4* list; uint32_t* ctr; uint32_t cap;
     float k1, rel;
     float* diag;              // diagnostics: [rowsA][rowsB][2] = (d2, E) of item 0, no binning
+    int chunk_kb;             // k-blocks accumulated per TMEM partial before the FP32 drain
 };
 
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+        "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+        "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+        "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]),
+        "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]),
+        "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+        : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
 template <int MAXM, int CG>
-__global__ void __launch_bounds__(NTHREADS, 1)
+// 10 warps -> up to 3 per SM sub-partition (16K registers each): <= 168 registers/thread
+__global__ void __maxnreg__(168)
 k_gram_tc(const __grid_constant__ CUtensorMap mAhi, const __grid_constant__ CUtensorMap mAlo,
           const __grid_constant__ CUtensorMap mBhi, const __grid_constant__ CUtensorMap mBlo, TcParams prm) {
     using G = Geo<CG>;
@@ -214,7 +239,7 @@ k_gram_tc(const __grid_constant__ CUtensorMap mAhi, const __grid_constant__ CUte
 
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < G::STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-        for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 4 * CG); }
+        for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 8 * CG); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&mAhi) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&mAlo) : "memory");
@@ -263,56 +288,108 @@ k_gram_tc(const __grid_constant__ CUtensorMap mAhi, const __grid_constant__ CUte
         }
     } else if (warp == 1) {
         if (lane == 0 && rank == 0) {
+            // K is accumulated in chunks of chunk_kb k-blocks into one of two TMEM partial
+            // buffers (columns [0,256) and [256,512)); the epilogue drains each chunk into FP32
+            // running sums in registers (round-to-nearest adds) while the tensor cores fill the
+            // other buffer.  Long in-place tensor-core accumulation loses low bits
+            // systematically (measured ~4e-5 relative d^2 at K = 8192); short
+            // chunks bound that loss.
             const uint32_t id = idesc(kind_tf32 ? 2 : 1, G::TILE_M, TILE_N);
             int stage = 0;
             uint32_t phase = 0;
-            int acc = 0;
-            uint32_t acc_phase = 0;
+            int buf = 0;
+            uint32_t bph = 0u;          // bit b = phase parity of partial buffer b
             for (int t = cluster_id; t < total_tiles; t += n_clusters) {
-                if (CG == 2) mbar_wait_cluster(&tempty[acc], acc_phase ^ 1);
-                else mbar_wait(&tempty[acc], acc_phase ^ 1);
-                fence_after();
-                const uint32_t d = tmem_base + (uint32_t)(acc * TILE_N);
-                for (int kb = 0; kb < prm.n_kb; ++kb) {
-                    mbar_wait(&full[stage], phase);
+                for (int kb0 = 0; kb0 < prm.n_kb; kb0 += prm.chunk_kb) {
+                    const int kb1 = min(kb0 + prm.chunk_kb, prm.n_kb);
+                    if (CG == 2) mbar_wait_cluster(&tempty[buf], ((bph >> buf) & 1u) ^ 1u);
+                    else mbar_wait(&tempty[buf], ((bph >> buf) & 1u) ^ 1u);
                     fence_after();
-                    const uint32_t s0 = smem_u32(stages + stage * G::STAGE_BYTES);
-                    const uint64_t ahi = sdesc(s0), alo = sdesc(s0 + G::A_BYTES);
-                    const uint64_t bhi = sdesc(s0 + 2 * G::A_BYTES), blo = sdesc(s0 + 2 * G::A_BYTES + G::B_BYTES);
+                    const uint32_t d = tmem_base + (uint32_t)(buf * TILE_N);
+                    for (int kb = kb0; kb < kb1; ++kb) {
+                        mbar_wait(&full[stage], phase);
+                        fence_after();
+                        const uint32_t s0 = smem_u32(stages + stage * G::STAGE_BYTES);
+                        const uint64_t ahi = sdesc(s0), alo = sdesc(s0 + G::A_BYTES);
+                        const uint64_t bhi = sdesc(s0 + 2 * G::A_BYTES), blo = sdesc(s0 + 2 * G::A_BYTES + G::B_BYTES);
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) {           // 4 x 32 bytes of K per 128-byte row
-                        const uint64_t adv = (uint64_t)(k * 2);  // +32 B in the start-address field (>>4)
-                        mma<CG>(d, ahi + adv, bhi + adv, id, (kb | k) != 0, kind_tf32);
-                        mma<CG>(d, ahi + adv, blo + adv, id, 1u, kind_tf32);
-                        mma<CG>(d, alo + adv, bhi + adv, id, 1u, kind_tf32);
+                        for (int k = 0; k < 4; ++k) {           // 4 x 32 bytes of K per 128-byte row
+                            const uint64_t adv = (uint64_t)(k * 2);  // +32 B in the start-address field (>>4)
+                            mma<CG>(d, ahi + adv, bhi + adv, id, (kb != kb0 || k != 0) ? 1u : 0u, kind_tf32);
+                            mma<CG>(d, ahi + adv, blo + adv, id, 1u, kind_tf32);
+                            mma<CG>(d, alo + adv, bhi + adv, id, 1u, kind_tf32);
+                        }
+                        mma_commit<CG>(&empty[stage]);
+                        if (++stage == G::STAGES) { stage = 0; phase ^= 1; }
                     }
-                    mma_commit<CG>(&empty[stage]);
-                    if (++stage == G::STAGES) { stage = 0; phase ^= 1; }
+                    mma_commit<CG>(&tfull[buf]);
+                    bph ^= 1u << buf;
+                    buf ^= 1;
                 }
-                mma_commit<CG>(&tfull[acc]);
-                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
             }
         }
     } else {
         // ------------------------------------------------------------ epilogue
+        // 8 warps: warp w owns TMEM lanes 32*(w&3).. (its 32 rows) and the column half
+        // (w-2)>>2 of the 256-column tile; running sums of its 128 pairs live in registers.
         const int quarter = warp & 3;
-        const int et = threadIdx.x - 64;              // 0..127
+        const int half = (warp - 2) >> 2;
+        const int et = threadIdx.x - 64;              // 0..255
         const int M = prm.M;
-        int acc = 0;
-        uint32_t acc_phase = 0;
+        int buf = 0;
+        uint32_t bph = 0u;          // bit b = phase parity of partial buffer b
         for (int t = cluster_id; t < total_tiles; t += n_clusters) {
             const int p = t / tiles_per_item, r = t % tiles_per_item;
             const int mt = r / prm.tiles_n, nt = r % prm.tiles_n;
             const int64_t col0 = (int64_t)nt * TILE_N;
             const int64_t browbase = (int64_t)prm.P * prm.rowsA + (int64_t)p * prm.rowsB;
-            named_bar(1, 128);
-            for (int j = et; j < TILE_N; j += 128) {
-                const int64_t c = col0 + j;
+            named_bar(1, 256);
+            {
+                const int64_t c = col0 + et;
                 const bool ok = c < prm.rowsB;
-                s_nb[j] = ok ? prm.nrm[browbase + c] : 0.f;
-                s_qb[j] = ok ? prm.q4[browbase + c] : 0.f;
+                s_nb[et] = ok ? prm.nrm[browbase + c] : 0.f;
+                s_qb[et] = ok ? prm.q4[browbase + c] : 0.f;
             }
-            named_bar(1, 128);
+            named_bar(1, 256);
+
+            // ---- drain the K-chunks into registers
+            float acc[128];
+#pragma unroll
+            for (int j = 0; j < 128; ++j) acc[j] = 0.f;
+            const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+            for (int kb0 = 0; kb0 < prm.n_kb; kb0 += prm.chunk_kb) {
+                mbar_wait(&tfull[buf], (bph >> buf) & 1u);
+                fence_after();
+                const uint32_t tp = tmem_base + lane_off + (uint32_t)(buf * TILE_N + half * 128);
+#pragma unroll
+                for (int ch = 0; ch < 8; ++ch) {
+                    uint32_t v[16];
+                    tmem_ld16(tp + ch * 16, v);
+#pragma unroll
+                    for (int jj = 0; jj < 16; ++jj) acc[ch * 16 + jj] += __uint_as_float(v[jj]);
+                }
+                if (kb0 + prm.chunk_kb < prm.n_kb) {      // release the buffer; keep the last one
+                    fence_before();
+                    __syncwarp();
+                    if (lane == 0) {
+                        if (CG == 2) mbar_arrive_remote(&tempty[buf], 0);
+                        else mbar_arrive(&tempty[buf]);
+                    }
+                    bph ^= 1u << buf;
+                    buf ^= 1;
+                }
+            }
+            // ---- park the final sums in the (still owned) last buffer, bin from there
+            const uint32_t tp = tmem_base + lane_off + (uint32_t)(buf * TILE_N + half * 128);
+#pragma unroll
+            for (int ch = 0; ch < 4; ++ch) {
+                uint32_t v[32];
+#pragma unroll
+                for (int jj = 0; jj < 32; ++jj) v[jj] = __float_as_uint(acc[ch * 32 + jj]);
+                tmem_st32(tp + ch * 32, v);
+            }
+            tmem_wait_st();
+
             float T[MAXM];
 #pragma unroll
             for (int m = 0; m < MAXM; ++m) T[m] = (m < M) ? __ldg(&prm.thr2[(int64_t)p * prm.thr_stride + m]) : -INFINITY;
@@ -356,18 +433,16 @@ k_gram_tc(const __grid_constant__ CUtensorMap mAhi, const __grid_constant__ CUte
                 }
             };
 
-            mbar_wait(&tfull[acc], acc_phase);
-            fence_after();
-            int64_t cur_cs = col0 / prm.sp.col_seg;
-            const uint32_t taddr0 = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * TILE_N);
+            const int64_t hcol0 = col0 + half * 128;
+            int64_t cur_cs = hcol0 / prm.sp.col_seg;
 #pragma unroll 1
-            for (int ch = 0; ch < TILE_N / 32; ++ch) {
+            for (int ch = 0; ch < 4; ++ch) {
                 uint32_t v[32];
-                tmem_ld32(taddr0 + ch * 32, v);
-                if (col0 + ch * 32 >= prm.rowsB) break;    // warp-uniform
+                tmem_ld32(tp + ch * 32, v);
+                if (hcol0 + ch * 32 >= prm.rowsB) break;   // warp-uniform
 #pragma unroll 4
                 for (int jj = 0; jj < 32; ++jj) {
-                    const int j = ch * 32 + jj;
+                    const int j = half * 128 + ch * 32 + jj;
                     const int64_t c = col0 + j;
                     if (c >= prm.rowsB) break;             // warp-uniform
                     const int64_t cs = c / prm.sp.col_seg;
@@ -403,14 +478,16 @@ k_gram_tc(const __grid_constant__ CUtensorMap mAhi, const __grid_constant__ CUte
                     }
                 }
             }
+            // release the last buffer of this tile
             fence_before();
             __syncwarp();
             if (lane == 0) {
-                if (CG == 2) mbar_arrive_remote(&tempty[acc], 0);
-                else mbar_arrive(&tempty[acc]);
+                if (CG == 2) mbar_arrive_remote(&tempty[buf], 0);
+                else mbar_arrive(&tempty[buf]);
             }
+            bph ^= 1u << buf;
+            buf ^= 1;
             flush(cur_cs);
-            if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         }
     }
     __syncthreads();
@@ -486,7 +563,13 @@ static cudaError_t launch_t(const tc::TcParams& prm, const CUtensorMap* maps, in
     ProfScope ps_(K_GRAM_TC, st);
     cudaError_t e = cudaLaunchKernelEx(&cfg, tc::k_gram_tc<MAXM, CG>, maps[0], maps[1], maps[2], maps[3], prm);
     note_launch();
-    if (e != cudaSuccess) return e;
+    if (e != cudaSuccess) {
+        cudaFuncAttributes fa{};
+        cudaFuncGetAttributes(&fa, tc::k_gram_tc<MAXM, CG>);
+        fprintf(stderr, "[libcil] k_gram_tc launch failed (%s): regs=%d maxThreads=%d local=%zu smem_dyn=%d\n",
+                cudaGetErrorString(e), fa.numRegs, fa.maxThreadsPerBlock, fa.localSizeBytes, G::SMEM_BYTES);
+        return e;
+    }
     return cudaGetLastError();
 }
 
@@ -518,6 +601,7 @@ static cudaError_t launch_cg(const TcArgs& a, cudaStream_t st) {
     prm.list = a.recheck; prm.ctr = a.recheck_ctr; prm.cap = a.recheck_cap;
     prm.k1 = a.guard_k1; prm.rel = a.guard_rel;
     prm.diag = a.diag;
+    prm.chunk_kb = a.chunk_kb > 0 ? a.chunk_kb : 4;
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);

@@ -31,6 +31,20 @@ cudaError_t launch_finalize(int P, int nq, int M, const SegParams& sp, const uin
     return cudaGetLastError();
 }
 
+__global__ void k_normalize(int64_t n, const uint64_t* __restrict__ counts, double npairs, double* __restrict__ y) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        y[i] = (double)counts[i] / npairs;
+}
+
+cudaError_t launch_normalize(int64_t n, const uint64_t* counts, double npairs, double* y, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    ProfScope ps_(K_TAIL, st);
+    const int blocks = (int)((n + 255) / 256 < 1024 ? (n + 255) / 256 : 1024);
+    k_normalize<<<blocks, 256, 0, st>>>(n, counts, npairs, y);
+    note_launch();
+    return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ stats
 __global__ void k_mean(const double* __restrict__ Y, int64_t y_stride, int n, int D,
                        double* __restrict__ mu) {

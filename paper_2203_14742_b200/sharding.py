@@ -1,0 +1,67 @@
+"""Multi-GPU sharding of the CIL hot path; one process per GPU,
+torch.distributed for the plumbing (NCCL over NVLink on B200).
+
+Two partitions:
+  * independent problems (set pairs of Alg. 1/2, proposals theta of Alg. 3): each rank
+    owns a contiguous slice of items (`item_range`) — no data-path collective;
+    `gather_vectors` all-gathers the per-item feature vectors when mu_0 / Sigma_0 over
+    all items are needed (Alg. 1 step 3).
+  * one large set pair (C5): rank r takes A rows [r N / G, (r+1) N / G) against all of B
+    (`row_range`), runs cil_features on its shard, then one all_reduce(SUM) of the int64
+    count vectors — the only exchange (<= n_meas * M * 8 bytes).  Integer sums are
+    order-free, so counts are bit-identical for every G.
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+
+def row_range(n: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous, balanced block [lo, hi) of n rows for `rank` of `world`."""
+    return (n * rank) // world, (n * (rank + 1)) // world
+
+
+def item_range(p: int, world: int, rank: int) -> tuple[int, int]:
+    return row_range(p, world, rank)
+
+
+def _world(group):
+    if not dist.is_available() or not dist.is_initialized():
+        return 1, 0
+    return dist.get_world_size(group), dist.get_rank(group)
+
+
+def sharded_features(A_local, B, grid, mask, radii, N_total: int, *, group=None, features_fn=None,
+                     normalize_fn=None, **kw):
+    """Counts / y of ONE large set pair whose A rows are sharded across the group.
+
+    A_local: this rank's rows of A ([n_r, S, H, W]); B: all of B ([Nt, S, H, W]) on every
+    rank.  features_fn(A, B, grid, mask, radii, **kw) -> (counts [1,q,M] int64, y, status)
+    defaults to the CUDA path (`paper_2203_14742_b200.features`); normalize_fn(counts,
+    npairs) -> y defaults to `cil_normalize`.  Returns (counts, y, status) of the whole
+    pair, identical on every rank.
+    """
+    if features_fn is None:
+        from . import features as features_fn  # CUDA path
+    counts, _, status = features_fn(A_local, B, grid, mask, radii, want_y=False, **kw)
+    world, _ = _world(group)
+    if world > 1:
+        dist.all_reduce(counts, op=dist.ReduceOp.SUM, group=group)
+        dist.all_reduce(status, op=dist.ReduceOp.MAX, group=group)   # bits are sticky per rank
+    npairs = float(N_total) * float(B.shape[0])
+    if normalize_fn is None:
+        from . import normalize as normalize_fn
+    y = normalize_fn(counts, npairs)
+    return counts, y, status
+
+
+def gather_vectors(y_local: torch.Tensor, *, group=None) -> torch.Tensor:
+    """All-gather per-item feature vectors [P_local, D] -> [world * P_local, D] (equal P_local)."""
+    world, _ = _world(group)
+    if world == 1:
+        return y_local
+    out = torch.empty((world * y_local.shape[0],) + tuple(y_local.shape[1:]), dtype=y_local.dtype,
+                      device=y_local.device)
+    dist.all_gather_into_tensor(out, y_local.contiguous(), group=group)
+    return out

@@ -166,6 +166,34 @@ def test_translation_invariance_tc(cil):
             assert torch.equal(c, base), (shift, eng)
 
 
+@pytest.mark.parametrize("engine", ["TC_3XBF16", "TC_3XTF32"])
+@pytest.mark.parametrize("case", ["C2", "C4", "offset", "C1"])
+def test_gram_error_bound(cil, oracle_mod, engine, case):
+    """The tensor-core d^2 error must stay well inside the per-pair bound E that decides
+    which pairs are re-checked exactly (DESIGN.md §6 L2 engine)."""
+    O = oracle_mod
+    dev = torch.device("cuda")
+    if case == "C2":
+        grid, N, Nt, shift = (2, 64, 64, 0.0), 128, 500, 0.0
+    elif case == "C4":
+        grid, N, Nt, shift = (1, 128, 128, 0.0), 96, 300, 0.0
+    elif case == "C1":
+        grid, N, Nt, shift = (1, 32, 32, 0.0), 20, 20, 0.0
+    else:
+        grid, N, Nt, shift = (2, 32, 32, 0.0), 100, 300, 50.0     # large common offset: centring stress
+    A = cilgen.make_set(31, 0, N, grid[:3]) + shift
+    B = cilgen.make_set(31, 1, Nt, grid[:3]) + shift
+    d2E = cil.diag_gram(A.to(dev), B.to(dev), grid, _engine(cil, engine)).cpu().numpy().astype(np.float64)
+    h = 1.0 / (grid[2] - 1)
+    w = h * h
+    exact = O.distance_matrix(A.numpy(), B.numpy(), grid, 0x1)[0] ** 2 / w
+    err = np.abs(d2E[..., 0] - exact)
+    ratio = err / d2E[..., 1]
+    print(f"{case} {engine}: max err/E = {ratio.max():.3e}, max rel err d2 = {(err / exact).max():.3e}, "
+          f"median E/d2 = {np.median(d2E[..., 1] / exact):.3e}")
+    assert ratio.max() < 0.25
+
+
 # ------------------------------------------------------------------ stats / loglik
 def test_stats_loglik(cil, oracle_mod):
     O = oracle_mod
