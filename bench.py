@@ -193,6 +193,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-c4", action="store_true")
+    ap.add_argument("--config", default="C2", choices=["C2", "C3"],
+                    help="C2 = the headline bench line; C3 = evidence run of the CUDA-core measures")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -206,6 +208,8 @@ def main():
     world, rank, local = dist_setup()
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
+    if args.config == "C3":
+        return bench_c3(args, dev)
 
     import paper_2203_14742_b200 as cil
     from paper_2203_14742_b200 import _capi
@@ -375,6 +379,76 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
+
+
+def pilot_radii_all(A0, B0, grid, M, mask):
+    """Harness radii for every selected measure from a 64 x 64 pilot block (torch, untimed,
+    harness setup only): power law between max (1 + 1e-3) and min (1 - 1e-3)."""
+    S, H, W = grid
+    h = 1.0 / (W - 1)
+    w = h * h if H > 1 else h
+    a = A0[:64].double()
+    rows = []
+    for i in range(a.shape[0]):
+        u = a[i:i + 1] - B0[:64].double()                      # [64, S, H, W]
+        dx = torch.diff(u, dim=-1) / h
+        dy = torch.diff(u, dim=-2) / h
+        a0 = (w * (u ** 2).flatten(1).sum(1)).sqrt()
+        ax = (w * (dx ** 2).flatten(1).sum(1)).sqrt()
+        ay = (w * (dy ** 2).flatten(1).sum(1)).sqrt() if H > 1 else torch.zeros_like(a0)
+        m0 = u.abs().flatten(1).amax(1)
+        mx = dx.abs().flatten(1).amax(1)
+        my = dy.abs().flatten(1).amax(1) if H > 1 else torch.zeros_like(m0)
+        rows.append(torch.stack([a0, m0, a0 + ax + ay, (a0 ** 2 + ax ** 2 + ay ** 2).sqrt(),
+                                 torch.maximum(m0, torch.maximum(mx, my)), m0 + mx + my]))
+    d = torch.cat(rows, dim=1)                                 # [6, 64*64]
+    out = []
+    for q in range(6):
+        if (mask >> q) & 1:
+            R0, RM = float(d[q].max()) * 1.001, float(d[q].min()) * 0.999
+            out.append(R0 * (RM / R0) ** (np.arange(1, M + 1) / M))
+    return np.array(out)
+
+
+def bench_c3(args, dev):
+    """Evidence run for SURVEY §8 config C3 (the alternative measures on CUDA cores):
+    2000 x 2000 patterns of 128x128x2, all six measures, M = 20 (L2 on tensor cores)."""
+    import paper_2203_14742_b200 as cil
+    from paper_2203_14742_b200 import _capi
+    grid, N, M, mask = (2, 128, 128), 2000, 20, 0x3F
+    seed = cilgen.config_seed(3)
+    A = cilgen.make_set(seed, 0, N, grid, device=dev)
+    B = cilgen.make_set(seed, 1, N, grid, device=dev)
+    radii = torch.tensor(pilot_radii_all(A, B, grid, M, mask), dtype=torch.float64, device=dev)
+    engine = getattr(cil, "ENGINE_" + args.engine)
+    ws = cil.Workspace()
+    stream = torch.cuda.current_stream()
+
+    def step():
+        cil.features(A, B, grid, mask, radii, engine=engine, ws=ws)
+
+    for _ in range(2):
+        step()
+    torch.cuda.synchronize()
+    steps = max(2, min(args.steps, 5))
+    _capi.prof_enable(True)
+    ms = timed(step, steps, stream) / steps
+    _capi.prof_enable(False)
+    prof = _capi.prof_read()
+    S, H, W = grid
+    K = S * H * W
+    Kaug = K + S * H * (W - 1) + S * (H - 1) * W
+    simt_ms = prof["simt_tile"][0] / max(1, prof["simt_tile"][1])
+    ep = float(N) * N * Kaug                                  # element-pairs per family per launch
+    ceil_both, _ = _capi.alu_ceiling(0)
+    res = {"workload": "C3: 2000 x 2000 of 128x128x2, L2 (tensor) + Linf, W12sum, W12, W1inf, W1infsum (CUDA cores), M=20",
+           "ms_per_step": round(ms, 3), "pairs_per_s": N * N / (ms * 1e-3),
+           "simt_tile": {"ms_per_launch": round(simt_ms, 3), "element_pairs_per_s": ep / (simt_ms * 1e-3),
+                         "alu_ceiling_element_pairs_per_s (measured, mix FADD2+FMNMX3+FFMA2)": ceil_both,
+                         "frac": round(ep / (simt_ms * 1e-3) / ceil_both, 4),
+                         "K_aug": Kaug},
+           "kernel_breakdown": {k: round(v[0] / steps, 3) for k, v in prof.items() if v[1] > 0}}
+    print(json.dumps(res), flush=True)
 
 
 def bench_c4(cil, args, world, rank, dev, engine, stream):

@@ -192,6 +192,13 @@ CIL_API cil_status cil_diag_gram(const float* A, int64_t lda, int64_t N, const f
                                  size_t ws_bytes, void* stream);
 
 /* ------------------------------------------------------------------------ */
+/* cil_diag_alu_ceiling — DIAGNOSTIC: measured issue ceiling of the CUDA-core engine's
+ * inner-loop instruction mix (mix 0: FADD2+FMNMX3+FFMA2, 1: FADD2+FMNMX3, 2: FADD2+FFMA2)
+ * in element-pairs per second on the current device (register-only kernel on the legacy
+ * stream, synchronous).  Returns 0, or -1 on a CUDA error. */
+CIL_API int32_t cil_diag_alu_ceiling(int32_t mix, int32_t iters, double* element_pairs_per_s, double* ms);
+
+/* ------------------------------------------------------------------------ */
 /* Kernel timing (diagnostics, used by bench.py for the live roofline).  While enabled on
  * the calling host thread, every kernel the library launches is bracketed by CUDA events
  * recorded on its launching stream.  cil_prof_read waits for those events and returns, per

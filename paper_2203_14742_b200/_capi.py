@@ -45,6 +45,8 @@ def _load():
     lib.cil_diag_gram.restype = ctypes.c_int
     lib.cil_normalize.argtypes = [i64, P, f64, P, P]
     lib.cil_normalize.restype = ctypes.c_int
+    lib.cil_diag_alu_ceiling.argtypes = [i32, i32, P, P]
+    lib.cil_diag_alu_ceiling.restype = i32
     lib.cil_prof_enable.argtypes = [i32]
     lib.cil_prof_enable.restype = None
     lib.cil_prof_read.argtypes = [P, P]
@@ -61,7 +63,16 @@ lib = _load()
 
 EXPORTED = ["cil_features_workspace_size", "cil_features", "cil_stats", "cil_loglik",
             "cil_synth_workspace_size", "cil_synth_loglik", "cil_status_string", "cil_last_cuda_error",
-            "cil_version", "cil_last_launch_count", "cil_diag_gram", "cil_prof_enable", "cil_prof_read", "cil_normalize"]
+            "cil_version", "cil_last_launch_count", "cil_diag_gram", "cil_prof_enable", "cil_prof_read", "cil_normalize", "cil_diag_alu_ceiling"]
+
+
+def alu_ceiling(mix: int = 0, iters: int = 20000):
+    """Measured element-pairs/s ceiling of the CUDA-core inner-loop mix (diagnostic)."""
+    eps = ctypes.c_double()
+    ms = ctypes.c_double()
+    if lib.cil_diag_alu_ceiling(mix, iters, ctypes.byref(eps), ctypes.byref(ms)) != 0:
+        raise CilError("cil_diag_alu_ceiling failed")
+    return eps.value, ms.value
 
 KERNEL_CLASSES = ["prep", "pack", "gram_tc", "simt_tile", "recheck", "tail"]
 
