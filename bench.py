@@ -147,6 +147,19 @@ def timed(fn, steps, stream):
     return e0.elapsed_time(e1)
 
 
+def engine_used(engine: str, K: int) -> str:
+    """The L2 engine AUTO resolves to (include/cil.h): INT8 when K <= 65536."""
+    if engine == "AUTO":
+        return "TC_I8" if K <= 65536 else "TC_3XBF16"
+    return engine
+
+
+DTYPES = {"TC_I8": "int8 two-digit fixed point / int32 accumulate / f64 stats",
+          "TC_3XBF16": "bf16x3 split / f32 accumulate / f64 stats",
+          "TC_3XTF32": "tf32x3 split / f32 accumulate / f64 stats",
+          "SIMT": "f32 differences / f64 sums"}
+
+
 def peaks():
     try:
         return json.load(open(PEAKS_FILE))
@@ -188,7 +201,7 @@ def main():
     ap.add_argument("--steps", type=int, default=400)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--engine", default="TC_3XBF16", choices=["TC_3XBF16", "TC_3XTF32", "SIMT"])
+    ap.add_argument("--engine", default="AUTO", choices=["AUTO", "TC_I8", "TC_3XBF16", "TC_3XTF32", "SIMT"])
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -292,17 +305,21 @@ def main():
     roof = None
     if gram_n > 0:
         per_launch_ms = gram_ms / gram_n
-        flops = 3 * 2.0 * P * N * Nt * K      # split-accounted: hi.hi + hi.lo + lo.hi
+        # split-accounted: 3 products per K element and pair (hi.hi + hi.lo + lo.hi, or HH + HL + LH)
+        flops = 3 * 2.0 * P * N * Nt * K
         achieved = flops / (per_launch_ms * 1e-3) / 1e12
-        split_tf32 = args.engine == "TC_3XTF32"
+        used = engine_used(args.engine, K)
+        ratio, kind = {"TC_I8": (2.0, "INT8 kind::i8 (HH + HL + LH), peak = bf16 x 2 (nominal i8:bf16)"),
+                       "TC_3XBF16": (1.0, "3xBF16 kind::f16"),
+                       "TC_3XTF32": (0.5, "3xTF32 kind::tf32, peak = bf16 x 0.5 (nominal tf32:bf16)")}[used]
         bf16_peak = pk.get("bf16_tflops", 1590.0)
-        peak = bf16_peak * (0.5 if split_tf32 else 1.0)
-        roof = {"kernel": "k_gram_tc (tcgen05 3x%s Gram + fused binning)" % ("TF32" if split_tf32 else "BF16"),
-                "bound": "tensor", "achieved": round(achieved, 2), "peak": peak, "unit": "TFLOP/s",
+        peak = bf16_peak * ratio
+        roof = {"kernel": "tcgen05 Gram + fused binning: " + kind,
+                "bound": "tensor", "achieved": round(achieved, 2), "peak": peak,
+                "unit": "TOP/s" if used == "TC_I8" else "TFLOP/s",
                 "frac": round(achieved / peak, 4),
-                "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst)" + (" x 0.5 (tf32 nominal ratio)" if split_tf32 else ""),
-                "frac_vs_sustained": round(achieved / (pk.get("bf16_tflops_sustained", peak) *
-                                                       (0.5 if split_tf32 else 1.0)), 4),
+                "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst) x %.1f" % ratio,
+                "frac_vs_sustained": round(achieved / (pk.get("bf16_tflops_sustained", bf16_peak) * ratio), 4),
                 "flops_per_launch": flops, "algorithmic_1x_flops_per_launch": flops / 3,
                 "kernel_ms_per_launch": round(per_launch_ms, 4),
                 "kernel_share_of_step": round(gram_ms / ms, 4) if rank == 0 else None,
@@ -356,9 +373,7 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "bf16x3 split / f32 accumulate / f64 stats"
-            if args.engine == "TC_3XBF16" else ("tf32x3 split / f32 accumulate / f64 stats"
-                                                if args.engine == "TC_3XTF32" else "f32 / f64"),
+            "scaling": "weak", "vs_baseline": None, "dtype": DTYPES[engine_used(args.engine, grid[0] * grid[1] * grid[2])],
             "data": "synthetic (cilgen-v1 seeded generator, resident in HBM)",
             "config": {"workload": cfg["workload"], "set_pairs_per_gpu": P, "N": N, "Nt": Nt,
                        "grid_SHW": list(grid), "M": M, "measures": ["L2"], "engine": args.engine,
@@ -500,8 +515,10 @@ def bench_c4(cil, args, world, rank, dev, engine, stream):
     if g_n:
         per = g_ms / g_n
         ach = 3 * 2.0 * P * rowsA * rowsB * K / (per * 1e-3) / 1e12
-        res["gram_tc"] = {"ms_per_launch": round(per, 4), "achieved_tflops": round(ach, 1),
-                          "frac_of_bf16_burst": round(ach / peaks().get("bf16_tflops", 1590.0), 4)}
+        used = engine_used(args.engine, K)
+        ratio = {"TC_I8": 2.0, "TC_3XBF16": 1.0, "TC_3XTF32": 0.5}.get(used, 1.0)
+        res["gram_tc"] = {"engine": used, "ms_per_launch": round(per, 4), "achieved_tops": round(ach, 1),
+                          "frac_of_peak": round(ach / (ratio * peaks().get("bf16_tflops", 1590.0)), 4)}
     res["kernel_breakdown"] = {k: round(v[0] / steps, 4) for k, v in prof.items() if v[1] > 0}
     return res
 

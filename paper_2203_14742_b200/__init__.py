@@ -22,7 +22,7 @@ from ._capi import CilError, Grid, check, lib  # noqa: F401  (fails loudly witho
 L2, LINF, W12SUM, W12, W1INF, W1INFSUM = (1 << i for i in range(6))
 ALL = 0x3F
 MEASURE_NAMES = ["L2", "LINF", "W12SUM", "W12", "W1INF", "W1INFSUM"]
-ENGINE_AUTO, ENGINE_TC_3XBF16, ENGINE_TC_3XTF32, ENGINE_SIMT = 0, 1, 2, 3
+ENGINE_AUTO, ENGINE_TC_3XBF16, ENGINE_TC_3XTF32, ENGINE_SIMT, ENGINE_TC_I8 = 0, 1, 2, 3, 4
 ITEM_OK, ITEM_NONFINITE, ITEM_NOTPD, ITEM_BADRADII, ITEM_OVERFLOW = 0, 1, 2, 4, 8
 
 __all__ = ["features", "stats", "loglik", "synth_loglik", "features_workspace_size",

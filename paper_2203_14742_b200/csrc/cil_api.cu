@@ -84,11 +84,20 @@ struct Plan {
     int nreg = 1;
 };
 
-Plan make_plan(uint32_t mask, cil_engine engine, const cil_grid& g) {
+// split: 1 = 3xBF16, 2 = 3xTF32, 3 = two-digit INT8.  AUTO takes INT8 when its exact int32
+// accumulation cannot overflow (K <= 65536) and its per-thread segment histograms fit
+// (column segments of >= 32 columns), else 3xBF16.
+bool i8_ok(const cil_grid& g, int64_t col_seg, int64_t rowsB) {
+    const int64_t K = (int64_t)g.S * g.H * g.W;
+    return K <= 65536 && (col_seg >= rowsB || col_seg >= 32);
+}
+Plan make_plan(uint32_t mask, cil_engine engine, const cil_grid& g, int64_t col_seg = 1ll << 40,
+               int64_t rowsB = 0) {
     Plan pl;
     const bool want_tc = (mask & CIL_L2) && engine != CIL_ENGINE_SIMT;
     pl.tc = want_tc;
-    pl.split = (engine == CIL_ENGINE_TC_3XTF32) ? 2 : 1;
+    pl.split = (engine == CIL_ENGINE_TC_3XTF32) ? 2 : (engine == CIL_ENGINE_TC_3XBF16) ? 1 : 3;
+    if (pl.split == 3 && !i8_ok(g, col_seg, rowsB)) pl.split = 1;
     pl.simt_mask = pl.tc ? (mask & ~(uint32_t)CIL_L2) : mask;
     pl.do_max = pl.simt_mask & (CIL_LINF | CIL_W1INF | CIL_W1INFSUM);
     pl.do_sum = pl.simt_mask & (CIL_L2 | CIL_W12SUM | CIL_W12);
@@ -126,7 +135,7 @@ Layout make_layout(int P, int64_t rowsA, int64_t rowsB, const cil_grid& g, int n
         const double cap = fmin(pairs, pairs / 256.0 + 65536.0);
         L.list_cap = (uint32_t)fmin(cap, 4.0e9);
         L.Kp = round_up(K, kTcBK);
-        const size_t esz = pl.split == 2 ? 4 : 2;
+        const size_t esz = pl.split == 2 ? 4 : (pl.split == 3 ? 1 : 2);
         L.off_list = take(16 * (size_t)L.list_cap);
         L.off_center = take(sizeof(float) * (size_t)P * L.Kp);
         L.off_hi = take(esz * (size_t)rows * L.Kp);
@@ -215,52 +224,77 @@ cil_status run_engines(int P, const RowSrc& asrc, const RowSrc& bsrc, int64_t ro
     }
     if (pl.tc) {
         if (!gram_tc_supported()) return CIL_EUNSUPPORTED;
-        const size_t esz = pl.split == 2 ? 4 : 2;
+        const size_t esz = pl.split == 2 ? 4 : (pl.split == 3 ? 1 : 2);
         float* center = at<float>(ws, L.off_center);
         char* hi = at<char>(ws, L.off_hi);
         char* lo = at<char>(ws, L.off_lo);
         float* nrm = at<float>(ws, L.off_nrm);
-        float* q4 = at<float>(ws, L.off_q4);
+        float* q4 = at<float>(ws, L.off_q4);      // (sum x~^4)^(1/4) for the float splits, sigma for INT8
         const size_t offB = (size_t)P * rowsA;
+        uint4* list = at<uint4>(ws, L.off_list);
         CIL_CU(launch_center(P, bsrc, rowsB < 16 ? rowsB : 16, K, L.Kp, center, st));
-        CIL_CU(launch_pack_tc(P, asrc, rowsA, K, L.Kp, center, pl.split, hi, lo, nrm, q4, status, st));
-        CIL_CU(launch_pack_tc(P, bsrc, rowsB, K, L.Kp, center, pl.split, hi + offB * L.Kp * esz,
-                              lo + offB * L.Kp * esz, nrm + offB, q4 + offB, status, st));
-        TcArgs t{};
-        t.hi = hi; t.lo = lo; t.nrm = nrm; t.q4 = q4;
-        t.rowsA = rowsA; t.rowsB = rowsB; t.Kp = L.Kp; t.K = K;
-        t.P = P; t.split = pl.split;
-        t.thr2 = thr2; t.thr_stride = M; t.M = M;
-        t.q_l2 = sl.q_l2; t.nq = sl.nq;
-        t.sp = sp; t.hist = hist;
-        t.recheck = at<uint4>(ws, L.off_list); t.recheck_ctr = ctr; t.recheck_cap = L.list_cap;
-        t.status = status;
-        // Error bound of the split Gram (DESIGN.md §L2 engine): E = k1 q_a q_b + rel (n_a + n_b)
-        //   k1: 8 sigma of the split residual (2^-16 per product for 3xBF16, 2^-20 for 3xTF32, x2 for d^2)
-        //   rel: FP32 evaluation / threshold rounding / centring + accumulation over K/16 MMA steps
-        {   // diagnostic overrides for A/B measurements (defaults: CTA pairs, 4-k-block chunks)
-            static const char* cg = getenv("CIL_TC_CTA_GROUP");
-            static const char* ck = getenv("CIL_TC_CHUNK_KB");
-            t.cta_group = (cg && cg[0] == '1') ? 1 : 2;
-            t.chunk_kb = ck ? atoi(ck) : 4;
-            if (t.chunk_kb < 1) t.chunk_kb = 1;
+        if (pl.split == 3) {
+            // ---- INT8 two-digit engine (default): exact int32 accumulation
+            CIL_CU(launch_pack_i8(P, asrc, rowsA, K, L.Kp, center, reinterpret_cast<int8_t*>(hi),
+                                  reinterpret_cast<int8_t*>(lo), nrm, q4, status, st));
+            CIL_CU(launch_pack_i8(P, bsrc, rowsB, K, L.Kp, center, reinterpret_cast<int8_t*>(hi + offB * L.Kp),
+                                  reinterpret_cast<int8_t*>(lo + offB * L.Kp), nrm + offB, q4 + offB, status, st));
+            I8Args t{};
+            t.hq = reinterpret_cast<const int8_t*>(hi); t.lq = reinterpret_cast<const int8_t*>(lo);
+            t.nrm = nrm; t.scl = q4;
+            t.rowsA = rowsA; t.rowsB = rowsB; t.Kp = L.Kp; t.K = K;
+            t.P = P; t.p0 = 0; t.np = P;
+            t.thr2 = thr2; t.thr_stride = M; t.M = M; t.q_l2 = sl.q_l2; t.nq = sl.nq;
+            t.sp = sp; t.hist = hist;
+            t.recheck = list; t.recheck_ctr = ctr; t.recheck_cap = L.list_cap;
+            // E = kq d sqrt((s_a^2 + s_b^2)/3) + kll s_a s_b + rel (n_a + n_b): 16 sigma of the operand
+            // quantisation (uniform error, variance s^2/12 per element, d^2 error 2 u.(da - db)), 16 sigma
+            // of the dropped LL digit product (E[l^2] ~ 128^2/3, x2 for d^2), FP32 rounding of d^2, the
+            // norms and the thresholds (measured max error / E ~ 0.2).
+            t.kq = 16.0f;
+            t.kll = (float)(16.0 * 2.0 * (128.0 * 128.0 / 3.0) * sqrt((double)K));
+            t.rel = (float)ldexp(1.0, -21);
+            t.diag = diag;
+            CIL_CU(launch_gram_i8(t, st));
+        } else {
+            // ---- 3xBF16 / 3xTF32 split engine
+            CIL_CU(launch_pack_tc(P, asrc, rowsA, K, L.Kp, center, pl.split, hi, lo, nrm, q4, status, st));
+            CIL_CU(launch_pack_tc(P, bsrc, rowsB, K, L.Kp, center, pl.split, hi + offB * L.Kp * esz,
+                                  lo + offB * L.Kp * esz, nrm + offB, q4 + offB, status, st));
+            TcArgs t{};
+            t.hi = hi; t.lo = lo; t.nrm = nrm; t.q4 = q4;
+            t.rowsA = rowsA; t.rowsB = rowsB; t.Kp = L.Kp; t.K = K;
+            t.P = P; t.split = pl.split;
+            t.thr2 = thr2; t.thr_stride = M; t.M = M;
+            t.q_l2 = sl.q_l2; t.nq = sl.nq;
+            t.sp = sp; t.hist = hist;
+            t.recheck = list; t.recheck_ctr = ctr; t.recheck_cap = L.list_cap;
+            t.status = status;
+            {   // diagnostic overrides for A/B measurements (defaults: CTA pairs, 4-k-block chunks)
+                static const char* cg = getenv("CIL_TC_CTA_GROUP");
+                static const char* ck = getenv("CIL_TC_CHUNK_KB");
+                t.cta_group = (cg && cg[0] == '1') ? 1 : 2;
+                t.chunk_kb = ck ? atoi(ck) : 4;
+                if (t.chunk_kb < 1) t.chunk_kb = 1;
+            }
+            // E = k1 q_a q_b + rel (n_a + n_b): k1 = 8 sigma of the split residual (2^-16 per product
+            // for 3xBF16, 2^-20 for 3xTF32, x2 for d^2); rel = truncation over the 12*chunk_kb MMA steps
+            // of one chunk + RN adds of the chunk partials + FP32 evaluation / threshold rounding.
+            const int64_t n_kb = (L.Kp * (int64_t)esz) / 128;
+            const double nchunks = (double)((n_kb + t.chunk_kb - 1) / t.chunk_kb);
+            t.guard_k1 = (float)(8.0 * (pl.split == 2 ? ldexp(1.0, -18) : ldexp(1.0, -15)));
+            t.guard_rel = (float)(ldexp(1.0, -24) * (8.0 * t.chunk_kb + 3.0 * sqrt(nchunks) + 8.0));
+            t.diag = diag;
+            t.p0 = 0; t.np = P; t.sm_budget = 0;
+            CIL_CU(launch_gram_tc(t, st));
         }
-        // E = k1 q_a q_b + rel (n_a + n_b): k1 = 8 sigma of the split residual (2^-16 per product
-        // for 3xBF16, 2^-20 for 3xTF32, x2 for d^2); rel = truncation over the 12*chunk_kb MMA steps
-        // of one chunk + RN adds of the chunk partials + FP32 evaluation / threshold rounding.
-        const int64_t n_kb = (L.Kp * (int64_t)esz) / 128;
-        const double nchunks = (double)((n_kb + t.chunk_kb - 1) / t.chunk_kb);
-        t.guard_k1 = (float)(8.0 * (pl.split == 2 ? ldexp(1.0, -18) : ldexp(1.0, -15)));
-        t.guard_rel = (float)(ldexp(1.0, -24) * (8.0 * t.chunk_kb + 3.0 * sqrt(nchunks) + 8.0));
-        t.diag = diag;
-        CIL_CU(launch_gram_tc(t, st));
         if (diag) return CIL_OK;
         RecheckArgs r{};
         r.asrc = asrc; r.bsrc = bsrc; r.K = K;
         r.thr = thr; r.thr_stride = (int64_t)sl.nq * M; r.w = bp.w;
         r.M = M; r.nq = sl.nq; r.q_l2 = sl.q_l2;
         r.sp = sp; r.hist = hist;
-        r.list = t.recheck; r.ctr = ctr; r.cap = L.list_cap;
+        r.list = list; r.ctr = ctr; r.cap = L.list_cap;
         r.status = status; r.P = P;
         CIL_CU(launch_recheck(r, st));
     }
@@ -275,7 +309,7 @@ size_t cil_features_workspace_size(int32_t P, int64_t N, int64_t Nt, cil_grid g,
                                    int32_t M, cil_engine engine) {
     if (P < 1 || N < 0 || Nt < 0 || M < 1 || check_grid(g, dist_mask) != CIL_OK) return 0;
     const Slots sl = slots_of(dist_mask);
-    const Plan pl = make_plan(dist_mask, engine, g);
+    const Plan pl = make_plan(dist_mask, engine, g, Nt > 0 ? Nt : 1, Nt);
     SegParams sp{N > 0 ? N : 1, Nt > 0 ? Nt : 1, 1, 1};
     return make_layout(P, N, Nt, g, sl.nq, M, pl, sp, 0).total;
 }
@@ -287,7 +321,7 @@ cil_status cil_features(int32_t P, const float* A, int64_t strideA, int64_t lda,
     t_launches = 0;
     if (P < 1 || N < 0 || Nt < 0 || M < 1 || M > kMaxM) return CIL_EINVAL;
     if (check_grid(g, dist_mask) != CIL_OK) return CIL_EINVAL;
-    if ((int)engine < 0 || (int)engine > 3) return CIL_EINVAL;
+    if ((int)engine < 0 || (int)engine > 4) return CIL_EINVAL;
     if (!radii || !counts || !item_status || !ws) return CIL_EINVAL;
     if ((N > 0 && !A) || (Nt > 0 && !B)) return CIL_EINVAL;
     if (strideA < 0 || strideB < 0 || radii_stride < 0) return CIL_EINVAL;
@@ -298,7 +332,7 @@ cil_status cil_features(int32_t P, const float* A, int64_t strideA, int64_t lda,
     if (K % 4 || lda % 4 || ldb % 4 || strideA % 4 || strideB % 4) return CIL_EUNSUPPORTED;
     if ((A && !aligned16(A)) || (B && !aligned16(B))) return CIL_EUNSUPPORTED;
     const Slots sl = slots_of(dist_mask);
-    const Plan pl = make_plan(dist_mask, engine, g);
+    const Plan pl = make_plan(dist_mask, engine, g, Nt > 0 ? Nt : 1, Nt);
     SegParams sp{N > 0 ? N : 1, Nt > 0 ? Nt : 1, 1, 1};
     const Layout L = make_layout(P, N, Nt, g, sl.nq, M, pl, sp, 0);
     if (ws_bytes < L.total) return CIL_ENOMEM;
@@ -347,7 +381,7 @@ size_t cil_synth_workspace_size(int32_t P, int32_t n_ens, int32_t N_set, int32_t
     if (P < 1 || n_ens < 2 || N_set < 1 || N_tilde < 1 || M < 1 || check_grid(g, dist_mask) != CIL_OK)
         return 0;
     const Slots sl = slots_of(dist_mask);
-    const Plan pl = make_plan(dist_mask, engine, g);
+    const Plan pl = make_plan(dist_mask, engine, g, N_tilde, (int64_t)n_ens * N_tilde);
     const int64_t rowsA = (int64_t)(n_ens + 1) * N_set, rowsB = (int64_t)n_ens * N_tilde;
     SegParams sp{N_set, N_tilde, n_ens + 1, n_ens};
     const int64_t nY = (int64_t)P * (n_ens * n_ens + 1) * sl.nq * M;
@@ -362,7 +396,7 @@ cil_status cil_synth_loglik(int32_t P, const float* pools, int64_t pool_stride, 
     t_launches = 0;
     if (P < 1 || n_ens < 2 || N_set < 1 || N_tilde < 1 || M < 1 || M > kMaxM) return CIL_EINVAL;
     if (check_grid(g, dist_mask) != CIL_OK) return CIL_EINVAL;
-    if ((int)engine < 0 || (int)engine > 3) return CIL_EINVAL;
+    if ((int)engine < 0 || (int)engine > 4) return CIL_EINVAL;
     if (!pools || !data || !k0 || !radii || !out || !item_status || !ws) return CIL_EINVAL;
     if (!(ridge >= 0.0)) return CIL_EINVAL;
     const int64_t K = (int64_t)g.S * g.H * g.W;
@@ -373,7 +407,7 @@ cil_status cil_synth_loglik(int32_t P, const float* pools, int64_t pool_stride, 
     if (!aligned16(pools) || !aligned16(data)) return CIL_EUNSUPPORTED;
     const Slots sl = slots_of(dist_mask);
     if (sl.nq * M > kMaxD) return CIL_EUNSUPPORTED;
-    const Plan pl = make_plan(dist_mask, engine, g);
+    const Plan pl = make_plan(dist_mask, engine, g, N_tilde, (int64_t)n_ens * N_tilde);
     const int64_t rowsA = (int64_t)(n_ens + 1) * N_set, rowsB = (int64_t)n_ens * N_tilde;
     SegParams sp{N_set, N_tilde, n_ens + 1, n_ens};
     const int nv = n_ens * n_ens;
@@ -400,7 +434,8 @@ cil_status cil_diag_gram(const float* A, int64_t lda, int64_t N, const float* B,
                          cil_grid g, cil_engine engine, float* d2E, void* ws, size_t ws_bytes, void* stream) {
     t_launches = 0;
     if (N < 1 || Nt < 1 || !A || !B || !d2E || !ws) return CIL_EINVAL;
-    if (engine != CIL_ENGINE_TC_3XBF16 && engine != CIL_ENGINE_TC_3XTF32) return CIL_EINVAL;
+    if (engine != CIL_ENGINE_TC_3XBF16 && engine != CIL_ENGINE_TC_3XTF32 && engine != CIL_ENGINE_TC_I8)
+        return CIL_EINVAL;
     if (check_grid(g, CIL_L2) != CIL_OK) return CIL_EINVAL;
     const int64_t K = (int64_t)g.S * g.H * g.W;
     if (lda < K || ldb < K) return CIL_EINVAL;

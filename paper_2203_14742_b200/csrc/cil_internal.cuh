@@ -13,7 +13,7 @@ constexpr int kMaxM = 64;        // radii per measure
 constexpr int kMaxMeas = 6;
 constexpr int kMaxD = 192;       // n_meas * M for loglik (packed Cholesky factor in smem)
 constexpr int kSimtBK = 32;      // SIMT k-chunk (floats); region padding unit
-constexpr int kTcBK = 64;        // bf16 elements per TMA box row (128 B, SWIZZLE_128B)
+constexpr int kTcBK = 128;       // K padding of the tensor-core operands (128 int8 = one 128-B row)
 
 // Row sources: how panel row r of item p maps to a pattern in caller memory.
 //  MODE_PLAIN : base + p*stride + r*ld
@@ -126,6 +126,9 @@ cudaError_t launch_pack_tc(int P, const RowSrc& src, int64_t rows, int64_t K, in
                            const float* center, int split, void* hi, void* lo, float* nrm, float* q4,
                            int32_t* status, cudaStream_t st);
 
+cudaError_t launch_pack_i8(int P, const RowSrc& src, int64_t rows, int64_t K, int64_t Kp, const float* center,
+                           int8_t* hq, int8_t* lq, float* nrm, float* scl, int32_t* status, cudaStream_t st);
+
 // simt_tile.cu
 struct SimtArgs {
     const float* Aaug; const float* Baug;    // [P][rowsA][Kaug], [P][rowsB][Kaug]
@@ -163,8 +166,27 @@ struct TcArgs {
     float* diag;                        // diagnostics only (see cil_diag_gram)
     int cta_group;                      // 2 (default): CTA-pair 256x256 tiles; 1: single-CTA 128x256
     int chunk_kb;                       // k-blocks per TMEM partial accumulation (precision control)
+    int p0, np;                         // items covered by this launch (np = 0: all from p0)
+    int sm_budget;                      // SMs the persistent grid may occupy (0 = all)
 };
 cudaError_t launch_gram_tc(const TcArgs& a, cudaStream_t st);
+
+// gram_i8.cu (INT8 two-digit engine)
+struct I8Args {
+    const int8_t* hq; const int8_t* lq;  // stacked [P*rowsA + P*rowsB][Kp] digits (A panels then B panels)
+    const float* nrm; const float* scl;  // stacked: sigma^2 sum q^2, sigma
+    int64_t rowsA, rowsB, Kp, K;
+    int P, p0, np;
+    const float* thr2;
+    int64_t thr_stride;
+    int M, q_l2, nq;
+    SegParams sp;
+    uint64_t* hist;
+    uint4* recheck; uint32_t* recheck_ctr; uint32_t recheck_cap;
+    float kq, kll, rel;
+    float* diag;
+};
+cudaError_t launch_gram_i8(const I8Args& a, cudaStream_t st);
 bool gram_tc_supported();
 
 // recheck.cu

@@ -1,0 +1,394 @@
+// gram_i8.cu — step a2 of the hot path, INT8 variant (default engine): L2 distances (Eq. (5),
+// PAPER.md:181) of all pairs through d^2 = |a~|^2 + |b~|^2 - 2 a~.b~ on tcgen05 kind::i8,
+// fused with the radius binning of Eq. (1).
+//
+// Operands (pack.cu k_pack_i8): per row a~ = sigma (256 h + l), h, l int8, sigma = max|a~|/32639.
+//   a~.b~ = sigma_a sigma_b (65536 HH + 256 (HL + LH) + LL),   HH = sum h_a h_b, ...
+// HH and X = HL + LH are accumulated EXACTLY in two int32 TMEM accumulators (3 MMAs per 32-byte
+// k-step); LL (< 2^-16 of the total, noise-like) is dropped and covered by the error bound.
+// Exact integer accumulation: no drift with K (|X| <= 32512 K < 2^31 for K <= 65536).
+// The only approximation is the operand quantisation (|delta| <= sigma/2 per element), whose
+// effect on d^2 is bounded per pair by
+//   E = k_q d sqrt((sigma_a^2 + sigma_b^2)/3) + k_ll sigma_a sigma_b sqrt(K) + rel (n_a + n_b);
+// pairs with a threshold T_m = R_m^2/w inside (d^2 - E, d^2 + E] go to the exact FP64 re-check.
+//
+// Kernel anatomy (persistent CTA pairs, cta_group::2, 256 x 256 tiles, 320 threads):
+//   warp 0      TMA producer (h and l tiles of A and B, 128-byte SWIZZLE_128B rows, 3 stages)
+//   warp 1      TMEM allocator + single-thread MMA issuer (leader CTA): HH -> cols [0,256),
+//               HL, LH -> cols [256,512)
+//   warps 2..9  epilogue: tcgen05.ld of H and X -> FP32 d^2 of 128 pairs per thread in registers
+//               -> TMEM released -> threshold search in shared memory -> per-thread 8-bit
+//               histograms per local column segment -> warp REDUX -> u64 atomics.
+#include <cuda.h>
+#include <stdio.h>
+
+#include "cil_internal.cuh"
+#include "tc_common.cuh"
+
+namespace cil {
+namespace tc {
+
+struct I8Params {
+    int64_t rowsA, rowsB;
+    int P, p0, np;
+    int n_kb;
+    int tiles_m, tiles_n;
+    const float* nrm;          // stacked [P*rowsA + P*rowsB]: sigma^2 sum q^2
+    const float* scl;          // stacked: sigma
+    const float* thr2;         // [P][M] R^2/w
+    int64_t thr_stride;
+    int M, nq, q_l2;
+    SegParams sp;
+    unsigned long long* hist;
+    uint4* list; uint32_t* ctr; uint32_t cap;
+    float kq, kll, rel;
+    float* diag;
+};
+
+__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+    asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                 "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+                 "l"(a), "l"(b), "r"(id), "r"(acc));
+}
+// Instruction descriptor for kind::i8: S32 accumulate (2), signed int8 A/B (1), K-major, N>>3, M>>4.
+__host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
+    return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+template <int MAXM> struct I8Geo {
+    static constexpr int STAGES = MAXM <= 16 ? 3 : 2;
+    static constexpr int STAGE_BYTES = Geo<2>::STAGE_BYTES;       // 64 KB: h, l of 128 A- and 128 B-rows
+    static constexpr int NLOC = 5;                                // local column segments per thread
+    static constexpr int HIST_BYTES = NLOC * (MAXM + 1) * 256;
+    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 1024 /*barriers*/ +
+                                      3 * TILE_N * 4 /*norms, sigma, spare*/ + 2 * MAXM * 4 + HIST_BYTES;
+};
+
+template <int MAXM, bool SEG>
+__global__ void __maxnreg__(168)
+k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUtensorMap mAl,
+          const __grid_constant__ CUtensorMap mBh, const __grid_constant__ CUtensorMap mBl, I8Params prm) {
+    using G = Geo<2>;
+    using IG = I8Geo<MAXM>;
+    constexpr int STAGES = IG::STAGES;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = reinterpret_cast<unsigned char*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    unsigned char* stages = smem;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * IG::STAGE_BYTES);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tfull = empty + STAGES;
+    uint64_t* tempty = tfull + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+    float* s_nb = reinterpret_cast<float*>(smem + STAGES * IG::STAGE_BYTES + 1024);
+    float* s_sb = s_nb + TILE_N;
+    float* s_T = s_sb + 2 * TILE_N;                       // [2*MAXM] thresholds, -inf padded
+    uint8_t* h8 = reinterpret_cast<uint8_t*>(s_T + 2 * MAXM);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_rank();
+    const int cluster_id = blockIdx.x / 2, n_clusters = gridDim.x / 2;
+    const int tiles_per_item = prm.tiles_m * prm.tiles_n;
+    const int total_tiles = prm.np * tiles_per_item;
+
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+        mbar_init(&tfull[0], 1);
+        mbar_init(&tempty[0], 16);                        // 8 epilogue warps x 2 CTAs
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&mAh) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&mAl) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&mBh) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&mBl) : "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+    if (warp >= 2) {
+        const int et = threadIdx.x - 64;
+        for (int i = et; i < IG::HIST_BYTES / 4; i += 256) reinterpret_cast<uint32_t*>(h8)[i] = 0u;
+    }
+    fence_before();
+    cluster_sync();
+    fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = cluster_id; t < total_tiles; t += n_clusters) {
+                const int p = prm.p0 + t / tiles_per_item, r = t % tiles_per_item;
+                const int mt = r / prm.tiles_n, nt = r % prm.tiles_n;
+                const int ya = (int)(p * prm.rowsA + (int64_t)mt * G::TILE_M + rank * A_ROWS);
+                const int yb = (int)((int64_t)prm.P * prm.rowsA + p * prm.rowsB + (int64_t)nt * TILE_N + rank * G::B_ROWS);
+                for (int kb = 0; kb < prm.n_kb; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    unsigned char* st = stages + stage * IG::STAGE_BYTES;
+                    if (rank == 0) mbar_expect_tx(&full[stage], 2 * IG::STAGE_BYTES);
+                    const int x = kb * 128;
+                    tma_load_2d<2>(st, &mAh, &full[stage], x, ya);
+                    tma_load_2d<2>(st + G::A_BYTES, &mAl, &full[stage], x, ya);
+                    tma_load_2d<2>(st + 2 * G::A_BYTES, &mBh, &full[stage], x, yb);
+                    tma_load_2d<2>(st + 2 * G::A_BYTES + G::B_BYTES, &mBl, &full[stage], x, yb);
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0 && rank == 0) {
+            const uint32_t id = idesc_i8(G::TILE_M, TILE_N);
+            const uint32_t dH = tmem_base, dX = tmem_base + TILE_N;
+            int stage = 0;
+            uint32_t phase = 0, tph = 0;
+            for (int t = cluster_id; t < total_tiles; t += n_clusters) {
+                mbar_wait_cluster(&tempty[0], tph ^ 1);
+                fence_after();
+                for (int kb = 0; kb < prm.n_kb; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    fence_after();
+                    const uint32_t s0 = smem_u32(stages + stage * IG::STAGE_BYTES);
+                    const uint64_t ah = sdesc(s0), al = sdesc(s0 + G::A_BYTES);
+                    const uint64_t bh = sdesc(s0 + 2 * G::A_BYTES), bl = sdesc(s0 + 2 * G::A_BYTES + G::B_BYTES);
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {               // 4 x 32 int8 of K per 128-byte row
+                        const uint64_t adv = (uint64_t)(k * 2);  // +32 B in the start-address field
+                        const uint32_t first = (kb | k) != 0 ? 1u : 0u;
+                        mma_i8(dH, ah + adv, bh + adv, id, first);
+                        mma_i8(dX, ah + adv, bl + adv, id, first);
+                        mma_i8(dX, al + adv, bh + adv, id, 1u);
+                    }
+                    mma_commit<2>(&empty[stage]);
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+                mma_commit<2>(&tfull[0]);
+                tph ^= 1;
+            }
+        }
+    } else {
+        // ------------------------------------------------------------ epilogue
+        const int quarter = warp & 3;
+        const int half = (warp - 2) >> 2;
+        const int et = threadIdx.x - 64;              // 0..255
+        const int M = prm.M;
+        uint32_t tph = 0;
+        for (int t = cluster_id; t < total_tiles; t += n_clusters) {
+            const int p = prm.p0 + t / tiles_per_item, r = t % tiles_per_item;
+            const int mt = r / prm.tiles_n, nt = r % prm.tiles_n;
+            const int64_t col0 = (int64_t)nt * TILE_N;
+            const int64_t browbase = (int64_t)prm.P * prm.rowsA + (int64_t)p * prm.rowsB;
+            named_bar(1, 256);
+            {
+                const int64_t c = col0 + et;
+                const bool ok = c < prm.rowsB;
+                s_nb[et] = ok ? prm.nrm[browbase + c] : 0.f;
+                s_sb[et] = ok ? prm.scl[browbase + c] : 0.f;
+                if (et < 2 * MAXM) s_T[et] = (et < M) ? prm.thr2[(int64_t)p * prm.thr_stride + et] : -INFINITY;
+            }
+            named_bar(1, 256);
+            const int64_t row = (int64_t)mt * G::TILE_M + rank * A_ROWS + quarter * 32 + lane;
+            const bool row_ok = row < prm.rowsA;
+            const int64_t arow = (int64_t)p * prm.rowsA + (row_ok ? row : 0);
+            const float na = row_ok ? __ldg(&prm.nrm[arow]) : 0.f;
+            const float sa = row_ok ? __ldg(&prm.scl[arow]) : 0.f;
+
+            // ---- phase 1: TMEM -> FP32 d^2 of this thread's 128 pairs, then release TMEM
+            mbar_wait(&tfull[0], tph);
+            fence_after();
+            float d2v[128];
+            const uint32_t tl = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(half * 128);
+#pragma unroll
+            for (int ch = 0; ch < 8; ++ch) {
+                uint32_t hv[16], xv[16];
+                tmem_ld16(tl + ch * 16, hv);
+                tmem_ld16(tl + TILE_N + ch * 16, xv);
+#pragma unroll
+                for (int jj = 0; jj < 16; ++jj) {
+                    const int j = half * 128 + ch * 16 + jj;
+                    // 65536 H + 256 X needs ~47 bits: combine and cancel in FP64, round d^2 once
+                    const double gi = fma((double)(int)hv[jj], 65536.0, (double)(int)xv[jj] * 256.0);
+                    d2v[ch * 16 + jj] = (float)fma(-2.0 * (double)sa * (double)s_sb[j], gi, (double)na + (double)s_nb[j]);
+                }
+            }
+            fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_remote(&tempty[0], 0);
+            tph ^= 1;
+
+            // ---- phase 2: error bound, threshold search, 8-bit histograms
+            const int64_t hc0 = col0 + half * 128;
+            const int64_t cs_first = hc0 / prm.sp.col_seg;
+            int bnd[IG::NLOC - 1];                       // local column indices where the segment changes
+#pragma unroll
+            for (int i = 0; i < IG::NLOC - 1; ++i) {
+                const int64_t c = (cs_first + 1 + i) * prm.sp.col_seg - hc0;
+                bnd[i] = SEG ? (int)(c < 128 ? c : (1 << 30)) : (1 << 30);
+            }
+            const int nvalid = (int)min((int64_t)128, prm.rowsB - hc0);   // warp-uniform
+            const float sa2 = sa * sa;
+            const float kll_sa = prm.kll * sa;
+            uint8_t* myh = h8 + et;
+#pragma unroll
+            for (int j = 0; j < 128; ++j) {
+                if (j >= nvalid || !row_ok) continue;       // predicated: keeps d2v[] in registers
+                const int jc = half * 128 + j;
+                const float d2 = d2v[j];
+                const float sb = s_sb[jc];
+                const float dd = fmaxf(d2, 0.f);
+                const float E = fmaf(prm.kq * dd * rsqrtf(fmaxf(dd, 1e-30f)), sqrtf((sa2 + sb * sb) * (1.f / 3.f)),
+                                     fmaf(kll_sa, sb, prm.rel * (na + s_nb[jc])));
+                if (prm.diag) {
+                    if (p == 0) {
+                        prm.diag[(row * prm.rowsB + (hc0 + j)) * 2] = d2;
+                        prm.diag[(row * prm.rowsB + (hc0 + j)) * 2 + 1] = E;
+                    }
+                    continue;
+                }
+                const float hi = d2 + E, lo = d2 - E;
+                int b = 0;
+#pragma unroll
+                for (int s = MAXM; s >= 1; s >>= 1)
+                    if (hi < s_T[b + s - 1]) b += s;
+                int lcs = 0;
+                if (SEG) {
+#pragma unroll
+                    for (int i = 0; i < IG::NLOC - 1; ++i) lcs += (j >= bnd[i]) ? 1 : 0;
+                }
+                uint8_t* cell = myh + ((lcs * (MAXM + 1) + b) << 8);
+                *cell = (uint8_t)(*cell + 1);
+                if (lo < s_T[b]) {
+                    const uint32_t idx = atomicAdd(prm.ctr, 1u);
+                    if (idx < prm.cap)
+                        prm.list[idx] = make_uint4((uint32_t)p, (uint32_t)row, (uint32_t)(hc0 + j), (uint32_t)b);
+                }
+            }
+            // ---- flush the local histograms (u8 -> warp sums -> global u64)
+            const int64_t rs = row_ok ? row / prm.sp.row_seg : 0;
+            const int64_t rs0 = __shfl_sync(0xffffffffu, rs, 0);
+            const bool uniform = __all_sync(0xffffffffu, rs == rs0 || !row_ok);
+            const int nloc = SEG ? IG::NLOC : 1;
+            for (int l = 0; l < nloc; ++l) {
+                const int64_t cs = cs_first + l;
+                if (cs * prm.sp.col_seg >= prm.rowsB || cs * prm.sp.col_seg >= col0 + TILE_N) break;
+                for (int b = 1; b <= M; ++b) {
+                    uint8_t* cell = myh + ((l * (MAXM + 1) + b) << 8);
+                    const uint32_t v = *cell;
+                    *cell = 0;
+                    if (uniform) {
+                        const uint32_t tot = __reduce_add_sync(0xffffffffu, v);
+                        if (lane == 0 && tot)
+                            atomicAdd(&prm.hist[hist_index(prm.sp, prm.nq, M, p, rs0, cs, prm.q_l2, b)],
+                                      (unsigned long long)tot);
+                    } else if (v) {
+                        atomicAdd(&prm.hist[hist_index(prm.sp, prm.nq, M, p, rs, cs, prm.q_l2, b)],
+                                  (unsigned long long)v);
+                    }
+                }
+                *(myh + ((l * (MAXM + 1)) << 8)) = 0;      // bin 0 (outside every radius) is not kept
+            }
+        }
+    }
+    __syncthreads();
+    cluster_sync();
+    if (warp == 1) {
+        fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
+    }
+}
+}  // namespace tc
+
+// ------------------------------------------------------------------ host side
+typedef CUresult (*PFN_encodeTiled_i8)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                       const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                       CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static bool make_map_i8(CUtensorMap* m, const void* base, int64_t rows, int64_t Kp, int box_rows) {
+    static PFN_encodeTiled_i8 enc = nullptr;
+    if (!enc) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return false;
+        enc = reinterpret_cast<PFN_encodeTiled_i8>(p);
+    }
+    cuuint64_t dims[2] = {(cuuint64_t)Kp, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)Kp};
+    cuuint32_t box[2] = {128u, (cuuint32_t)box_rows};
+    cuuint32_t es[2] = {1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int MAXM, bool SEG>
+static cudaError_t launch_i8_t(const tc::I8Params& prm, const CUtensorMap* maps, int nsm, cudaStream_t st) {
+    using IG = tc::I8Geo<MAXM>;
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(tc::k_gram_i8<MAXM, SEG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             IG::SMEM_BYTES);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    const int64_t tiles = (int64_t)prm.np * prm.tiles_m * prm.tiles_n;
+    const int clusters = (int)(tiles < nsm / 2 ? tiles : nsm / 2);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)(clusters * 2));
+    cfg.blockDim = dim3(tc::NTHREADS);
+    cfg.dynamicSmemBytes = IG::SMEM_BYTES;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    ProfScope ps_(K_GRAM_TC, st);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, tc::k_gram_i8<MAXM, SEG>, maps[0], maps[1], maps[2], maps[3], prm);
+    note_launch();
+    if (e != cudaSuccess) {
+        cudaFuncAttributes fa{};
+        cudaFuncGetAttributes(&fa, tc::k_gram_i8<MAXM, SEG>);
+        fprintf(stderr, "[libcil] k_gram_i8 launch failed (%s): regs=%d maxThreads=%d local=%zu smem_dyn=%d\n",
+                cudaGetErrorString(e), fa.numRegs, fa.maxThreadsPerBlock, fa.localSizeBytes, IG::SMEM_BYTES);
+        return e;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gram_i8(const I8Args& a, cudaStream_t st) {
+    if (a.rowsA == 0 || a.rowsB == 0) return cudaSuccess;
+    const int64_t rows = (int64_t)a.P * (a.rowsA + a.rowsB);
+    if (rows >= (1ll << 31)) return cudaErrorInvalidValue;
+    CUtensorMap maps[4];
+    if (!make_map_i8(&maps[0], a.hq, rows, a.Kp, tc::A_ROWS) || !make_map_i8(&maps[1], a.lq, rows, a.Kp, tc::A_ROWS) ||
+        !make_map_i8(&maps[2], a.hq, rows, a.Kp, tc::Geo<2>::B_ROWS) ||
+        !make_map_i8(&maps[3], a.lq, rows, a.Kp, tc::Geo<2>::B_ROWS))
+        return cudaErrorInvalidValue;
+    tc::I8Params prm{};
+    prm.rowsA = a.rowsA; prm.rowsB = a.rowsB;
+    prm.P = a.P; prm.p0 = a.p0; prm.np = a.np > 0 ? a.np : a.P - a.p0;
+    prm.n_kb = (int)(a.Kp / 128);
+    prm.tiles_m = (int)((a.rowsA + tc::Geo<2>::TILE_M - 1) / tc::Geo<2>::TILE_M);
+    prm.tiles_n = (int)((a.rowsB + tc::TILE_N - 1) / tc::TILE_N);
+    prm.nrm = a.nrm; prm.scl = a.scl;
+    prm.thr2 = a.thr2; prm.thr_stride = a.thr_stride;
+    prm.M = a.M; prm.nq = a.nq; prm.q_l2 = a.q_l2;
+    prm.sp = a.sp;
+    prm.hist = reinterpret_cast<unsigned long long*>(a.hist);
+    prm.list = a.recheck; prm.ctr = a.recheck_ctr; prm.cap = a.recheck_cap;
+    prm.kq = a.kq; prm.kll = a.kll; prm.rel = a.rel;
+    prm.diag = a.diag;
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const bool seg = a.sp.col_seg < a.rowsB;
+    if (a.M <= 16) return seg ? launch_i8_t<16, true>(prm, maps, nsm, st) : launch_i8_t<16, false>(prm, maps, nsm, st);
+    if (a.M <= 32) return seg ? launch_i8_t<32, true>(prm, maps, nsm, st) : launch_i8_t<32, false>(prm, maps, nsm, st);
+    return seg ? launch_i8_t<64, true>(prm, maps, nsm, st) : launch_i8_t<64, false>(prm, maps, nsm, st);
+}
+
+}  // namespace cil

@@ -178,6 +178,93 @@ cudaError_t launch_pack_tc(int P, const RowSrc& src, int64_t rows, int64_t K, in
     return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------- INT8 pack
+// Two-digit fixed point per row for the kind::i8 tensor-core engine:
+//   x~ = x - c (FP32);  sigma = max|x~| / 32639
+//   q = rint(x~ / sigma) in [-32639, 32639];  h = floor((q + 128) / 256) in [-127, 127];
+//   l = q - 256 h in [-128, 127]
+// so x~ ~= sigma (256 h + l) with |error| <= sigma / 2.  nrm = sigma^2 sum q^2 (the exact norm of the
+// quantised row, FP64 -> FP32), scl = sigma.  The quantisation is a perturbation of the operands; its
+// effect on d^2 is bounded statistically by the epilogue's E.
+__global__ void __launch_bounds__(256) k_pack_i8(RowSrc src, int64_t rows, int64_t K, int64_t Kp,
+                                                 const float* __restrict__ center, int8_t* __restrict__ hq,
+                                                 int8_t* __restrict__ lq, float* __restrict__ nrm,
+                                                 float* __restrict__ scl, int32_t* __restrict__ status) {
+    const int64_t p = blockIdx.y;
+    const int64_t r = blockIdx.x;
+    const float* x = row_ptr(src, p, r);
+    const float* c = center + p * Kp;
+    const int64_t orow = p * rows + r;
+    __shared__ float red[32];
+    __shared__ double redd[32];
+    __shared__ int nf;
+    if (threadIdx.x == 0) nf = 0;
+    // pass 1: max |x~| (the row stays in L1/L2 for pass 2)
+    float mx = 0.f;
+    bool nonfinite = false;
+    for (int64_t k = (int64_t)threadIdx.x * 4; k < K; k += (int64_t)blockDim.x * 4) {
+        const float4 xv = __ldg(reinterpret_cast<const float4*>(x + k));
+        const float4 cv = *reinterpret_cast<const float4*>(c + k);
+        nonfinite |= !(isfinite(xv.x) && isfinite(xv.y) && isfinite(xv.z) && isfinite(xv.w));
+        mx = fmaxf(mx, fmaxf(fmaxf(fabsf(xv.x - cv.x), fabsf(xv.y - cv.y)), fmaxf(fabsf(xv.z - cv.z), fabsf(xv.w - cv.w))));
+    }
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
+    __syncthreads();
+    if (nonfinite) atomicOr(&nf, 1);
+    if (ln == 0) red[w] = mx;
+    __syncthreads();
+    mx = 0.f;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) mx = fmaxf(mx, red[i]);
+    // sigma = max|x~| / 32639 (sigma = 1 for an all-zero row).  An exact (not power-of-two) scale:
+    // measured 2.5x smaller quantisation error on generator data; q is clamped.
+    const float sigma = (mx > 0.f && isfinite(mx)) ? mx / 32639.f : 1.f;
+    const float inv = 1.f / sigma;
+    // pass 2: quantise, split, store; exact sum of q^2
+    double s2 = 0.0;
+    for (int64_t k = (int64_t)threadIdx.x * 4; k < Kp; k += (int64_t)blockDim.x * 4) {
+        char4 hv = make_char4(0, 0, 0, 0), lv = make_char4(0, 0, 0, 0);
+        if (k < K) {
+            const float4 xv = __ldg(reinterpret_cast<const float4*>(x + k));
+            const float4 cv = *reinterpret_cast<const float4*>(c + k);
+            const float e[4] = {xv.x - cv.x, xv.y - cv.y, xv.z - cv.z, xv.w - cv.w};
+            int hh[4], ll[4];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                const int q = isfinite(e[t]) ? max(-32639, min(32639, __float2int_rn(e[t] * inv))) : 0;
+                const int h = (q + 128) >> 8;          // floor((q + 128) / 256): l = q - 256 h in [-128, 127]
+                hh[t] = h;
+                ll[t] = q - 256 * h;
+                s2 += (double)q * (double)q;
+            }
+            hv = make_char4((signed char)hh[0], (signed char)hh[1], (signed char)hh[2], (signed char)hh[3]);
+            lv = make_char4((signed char)ll[0], (signed char)ll[1], (signed char)ll[2], (signed char)ll[3]);
+        }
+        *reinterpret_cast<char4*>(hq + orow * Kp + k) = hv;
+        *reinterpret_cast<char4*>(lq + orow * Kp + k) = lv;
+    }
+    for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    if (ln == 0) redd[w] = s2;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double a = 0.0;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) a += redd[i];
+        nrm[orow] = (float)(a * (double)sigma * (double)sigma);
+        scl[orow] = sigma;
+        if (nf) atomicOr(&status[p], CIL_ITEM_NONFINITE);
+    }
+}
+
+cudaError_t launch_pack_i8(int P, const RowSrc& src, int64_t rows, int64_t K, int64_t Kp, const float* center,
+                           int8_t* hq, int8_t* lq, float* nrm, float* scl, int32_t* status, cudaStream_t st) {
+    if (rows == 0) return cudaSuccess;
+    dim3 grid((unsigned)rows, (unsigned)P);
+    ProfScope ps_(K_PACK, st);
+    k_pack_i8<<<grid, 256, 0, st>>>(src, rows, K, Kp, center, hq, lq, nrm, scl, status);
+    note_launch();
+    return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------------- aug pack
 // One CTA per panel row: out = [x (K) | D_x x (S*H*(W-1)) | D_y x (S*(H-1)*W)], each
 // region zero-padded to a multiple of kSimtBK, plain FP32 differences.

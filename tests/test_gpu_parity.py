@@ -14,7 +14,7 @@ import cilgen
 pytestmark = pytest.mark.gpu
 
 BAND = 1e-6
-ENGINES = ["SIMT", "TC_3XBF16", "TC_3XTF32"]
+ENGINES = ["SIMT", "TC_3XBF16", "TC_3XTF32", "TC_I8", "AUTO"]
 
 
 @pytest.fixture(scope="module")
@@ -166,7 +166,7 @@ def test_translation_invariance_tc(cil):
             assert torch.equal(c, base), (shift, eng)
 
 
-@pytest.mark.parametrize("engine", ["TC_3XBF16", "TC_3XTF32"])
+@pytest.mark.parametrize("engine", ["TC_3XBF16", "TC_3XTF32", "TC_I8"])
 @pytest.mark.parametrize("case", ["C2", "C4", "offset", "C1"])
 def test_gram_error_bound(cil, oracle_mod, engine, case):
     """The tensor-core d^2 error must stay well inside the per-pair bound E that decides
@@ -271,7 +271,7 @@ def test_synth_small(cil, oracle_mod, engine, mask):
 
 
 # ------------------------------------------------------------------ full-size configs (sampled)
-@pytest.mark.parametrize("engine", ["TC_3XBF16", "SIMT"])
+@pytest.mark.parametrize("engine", ["TC_I8", "TC_3XBF16", "SIMT"])
 def test_c2_full_item_vs_oracle(cil, oracle_mod, engine):
     """One full C2 item (500 x 500, 64x64x2, L2, M = 15) in the batched launch the bench times."""
     O = oracle_mod
