@@ -2,6 +2,7 @@
 // dispatch of the hot-path kernels on the caller's stream.  No device memory is
 // allocated here and nothing synchronises the device.
 #include <math.h>
+#include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -297,6 +298,14 @@ cil_status run_engines(int P, const RowSrc& asrc, const RowSrc& bsrc, int64_t ro
         r.list = list; r.ctr = ctr; r.cap = L.list_cap;
         r.status = status; r.P = P;
         CIL_CU(launch_recheck(r, st));
+        static const char* dbg = getenv("CIL_DEBUG_RECHECK");   // diagnostic: synchronising count print
+        if (dbg && dbg[0] == '1') {
+            uint32_t n = 0;
+            cudaMemcpyAsync(&n, ctr, sizeof(n), cudaMemcpyDeviceToHost, st);
+            cudaStreamSynchronize(st);
+            fprintf(stderr, "[libcil] re-checked pairs: %u of %.0f (%.2e)\n", n, (double)P * rowsA * rowsB,
+                    n / ((double)P * rowsA * rowsB));
+        }
     }
     return CIL_OK;
 }

@@ -21,6 +21,7 @@
 //               histograms per local column segment -> warp REDUX -> u64 atomics.
 #include <cuda.h>
 #include <stdio.h>
+#include <stdlib.h>
 
 #include "cil_internal.cuh"
 #include "tc_common.cuh"
@@ -43,6 +44,7 @@ struct I8Params {
     uint4* list; uint32_t* ctr; uint32_t cap;
     float kq, kll, rel;
     float* diag;
+    int dbg;                   // diagnostic timing knob (CIL_DEBUG_I8): 1 skip binning, 2 skip the epilogue
 };
 
 __device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
@@ -72,7 +74,9 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
     using IG = I8Geo<MAXM>;
     constexpr int STAGES = IG::STAGES;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    unsigned char* smem = reinterpret_cast<unsigned char*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    // 1024-B alignment by offsetting the shared pointer itself (keeps the shared address space, so
+    // the epilogue's threshold / histogram accesses compile to LDS/STS, not generic loads)
+    unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     unsigned char* stages = smem;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * IG::STAGE_BYTES);
     uint64_t* empty = full + STAGES;
@@ -196,6 +200,13 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
             // ---- phase 1: TMEM -> FP32 d^2 of this thread's 128 pairs, then release TMEM
             mbar_wait(&tfull[0], tph);
             fence_after();
+            if (prm.dbg == 2) {
+                fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive_remote(&tempty[0], 0);
+                tph ^= 1;
+                continue;
+            }
             float d2v[128];
             const uint32_t tl = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(half * 128);
 #pragma unroll
@@ -216,6 +227,13 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
             if (lane == 0) mbar_arrive_remote(&tempty[0], 0);
             tph ^= 1;
 
+            if (prm.dbg == 1) {
+                float s = 0.f;
+#pragma unroll
+                for (int j = 0; j < 128; ++j) s += d2v[j];
+                if (s == 1.2345f) prm.hist[0] = 1;
+                continue;
+            }
             // ---- phase 2: error bound, threshold search, 8-bit histograms
             const int64_t hc0 = col0 + half * 128;
             const int64_t cs_first = hc0 / prm.sp.col_seg;
@@ -226,7 +244,10 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
                 bnd[i] = SEG ? (int)(c < 128 ? c : (1 << 30)) : (1 << 30);
             }
             const int nvalid = (int)min((int64_t)128, prm.rowsB - hc0);   // warp-uniform
-            const float sa2 = sa * sa;
+            const bool diag_mode = prm.diag != nullptr;  // diagnostics (item 0 only), uniform per kernel
+            float* diag_row = diag_mode ? prm.diag + (size_t)(row_ok ? row : 0) * prm.rowsB * 2 : nullptr;
+            if (diag_mode && p != 0) continue;
+            const float kq_sa = prm.kq * 0.81649658f;    // sqrt((sa^2 + sb^2)/3) <= sqrt(2/3) max(sa, sb)
             const float kll_sa = prm.kll * sa;
             uint8_t* myh = h8 + et;
 #pragma unroll
@@ -235,14 +256,12 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
                 const int jc = half * 128 + j;
                 const float d2 = d2v[j];
                 const float sb = s_sb[jc];
-                const float dd = fmaxf(d2, 0.f);
-                const float E = fmaf(prm.kq * dd * rsqrtf(fmaxf(dd, 1e-30f)), sqrtf((sa2 + sb * sb) * (1.f / 3.f)),
+                const float dd = fmaxf(d2, 1e-30f);
+                const float E = fmaf(kq_sa * dd * rsqrtf(dd), fmaxf(sa, sb),
                                      fmaf(kll_sa, sb, prm.rel * (na + s_nb[jc])));
-                if (prm.diag) {
-                    if (p == 0) {
-                        prm.diag[(row * prm.rowsB + (hc0 + j)) * 2] = d2;
-                        prm.diag[(row * prm.rowsB + (hc0 + j)) * 2 + 1] = E;
-                    }
+                if (diag_mode) {
+                    diag_row[2 * (hc0 + j)] = d2;
+                    diag_row[2 * (hc0 + j) + 1] = E;
                     continue;
                 }
                 const float hi = d2 + E, lo = d2 - E;
@@ -382,6 +401,10 @@ cudaError_t launch_gram_i8(const I8Args& a, cudaStream_t st) {
     prm.list = a.recheck; prm.ctr = a.recheck_ctr; prm.cap = a.recheck_cap;
     prm.kq = a.kq; prm.kll = a.kll; prm.rel = a.rel;
     prm.diag = a.diag;
+    {
+        static const char* dbg = getenv("CIL_DEBUG_I8");
+        prm.dbg = dbg ? atoi(dbg) : 0;
+    }
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);

@@ -255,12 +255,94 @@ __global__ void __launch_bounds__(256) k_pack_i8(RowSrc src, int64_t rows, int64
     }
 }
 
+// Single-pass variant: the whole row is held in registers (NV float4 per thread, 256 threads,
+// K <= NV * 1024), so HBM is read once; same arithmetic as k_pack_i8.
+template <int NV>
+__global__ void __launch_bounds__(256) k_pack_i8r(RowSrc src, int64_t rows, int64_t K, int64_t Kp,
+                                                  const float* __restrict__ center, int8_t* __restrict__ hq,
+                                                  int8_t* __restrict__ lq, float* __restrict__ nrm,
+                                                  float* __restrict__ scl, int32_t* __restrict__ status) {
+    const int64_t p = blockIdx.y;
+    const int64_t r = blockIdx.x;
+    const float* x = row_ptr(src, p, r);
+    const float* c = center + p * Kp;
+    const int64_t orow = p * rows + r;
+    __shared__ float red[8];
+    __shared__ double redd[8];
+    float4 v[NV];
+    float mx = 0.f;
+    bool nonfinite = false;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+        const int64_t k = ((int64_t)i * 256 + threadIdx.x) * 4;
+        if (k < K) {
+            const float4 xv = __ldg(reinterpret_cast<const float4*>(x + k));
+            const float4 cv = __ldg(reinterpret_cast<const float4*>(c + k));
+            nonfinite |= !(isfinite(xv.x) && isfinite(xv.y) && isfinite(xv.z) && isfinite(xv.w));
+            v[i] = make_float4(xv.x - cv.x, xv.y - cv.y, xv.z - cv.z, xv.w - cv.w);
+        } else {
+            v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v[i].x), fabsf(v[i].y)), fmaxf(fabsf(v[i].z), fabsf(v[i].w))));
+    }
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
+    const bool anynf = __syncthreads_or(nonfinite);
+    if (ln == 0) red[w] = mx;
+    __syncthreads();
+    mx = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) mx = fmaxf(mx, red[i]);
+    const float sigma = (mx > 0.f && isfinite(mx)) ? mx / 32639.f : 1.f;
+    const float inv = 1.f / sigma;
+    double s2 = 0.0;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+        const int64_t k = ((int64_t)i * 256 + threadIdx.x) * 4;
+        if (k >= Kp) continue;
+        const float e[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+        int hh[4], ll[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const int q = isfinite(e[t]) ? max(-32639, min(32639, __float2int_rn(e[t] * inv))) : 0;
+            const int h = (q + 128) >> 8;
+            hh[t] = h;
+            ll[t] = q - 256 * h;
+            s2 += (double)(q * q);                   // q^2 < 2^30: exact in int32
+        }
+        *reinterpret_cast<char4*>(hq + orow * Kp + k) =
+            make_char4((signed char)hh[0], (signed char)hh[1], (signed char)hh[2], (signed char)hh[3]);
+        *reinterpret_cast<char4*>(lq + orow * Kp + k) =
+            make_char4((signed char)ll[0], (signed char)ll[1], (signed char)ll[2], (signed char)ll[3]);
+    }
+    for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    if (ln == 0) redd[w] = s2;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double a = 0.0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) a += redd[i];
+        nrm[orow] = (float)(a * (double)sigma * (double)sigma);
+        scl[orow] = sigma;
+        if (anynf) atomicOr(&status[p], CIL_ITEM_NONFINITE);
+    }
+}
+
 cudaError_t launch_pack_i8(int P, const RowSrc& src, int64_t rows, int64_t K, int64_t Kp, const float* center,
                            int8_t* hq, int8_t* lq, float* nrm, float* scl, int32_t* status, cudaStream_t st) {
     if (rows == 0) return cudaSuccess;
     dim3 grid((unsigned)rows, (unsigned)P);
     ProfScope ps_(K_PACK, st);
-    k_pack_i8<<<grid, 256, 0, st>>>(src, rows, K, Kp, center, hq, lq, nrm, scl, status);
+    if (Kp <= 4096)
+        k_pack_i8r<4><<<grid, 256, 0, st>>>(src, rows, K, Kp, center, hq, lq, nrm, scl, status);
+    else if (Kp <= 8192)
+        k_pack_i8r<8><<<grid, 256, 0, st>>>(src, rows, K, Kp, center, hq, lq, nrm, scl, status);
+    else if (Kp <= 16384)
+        k_pack_i8r<16><<<grid, 256, 0, st>>>(src, rows, K, Kp, center, hq, lq, nrm, scl, status);
+    else if (Kp <= 32768)
+        k_pack_i8r<32><<<grid, 256, 0, st>>>(src, rows, K, Kp, center, hq, lq, nrm, scl, status);
+    else
+        k_pack_i8<<<grid, 256, 0, st>>>(src, rows, K, Kp, center, hq, lq, nrm, scl, status);
     note_launch();
     return cudaGetLastError();
 }

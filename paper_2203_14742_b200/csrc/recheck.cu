@@ -1,9 +1,9 @@
-// recheck.cu — exact re-evaluation of the L2 pairs the tensor-core epilogue could
-// not classify with certainty (|d^2_approx - R_m^2/w| within the Gram error bound).
-// One warp per listed pair: s0 = sum_e ((double)a_e - (double)b_e)^2 in FP64 from the
-// caller's original FP32 patterns, bin b = #{m : s0 < R_m^2 / w} (Eq. (1), strict <,
-// PAPER.md:98; L2 = sqrt(w s0), Eq. (5)), then the pair is moved from the provisional
-// bin b_lo the epilogue gave it to b:  hist[b_lo] -= 1, hist[b] += 1.
+// recheck.cu — exact re-evaluation of the L2 pairs the tensor-core epilogue could not
+// classify with certainty (|d^2_approx - R_m^2/w| within the engine's error bound E).
+// One CTA per listed pair (256 threads, grid-stride over the list): s0 = sum_e ((double)a_e -
+// (double)b_e)^2 in FP64 from the caller's original FP32 patterns, bin b = #{m : s0 < R_m^2/w}
+// (Eq. (1), strict <; L2 = sqrt(w s0), Eq. (5)); the pair is then moved from the
+// provisional bin b_lo the epilogue gave it to b:  hist[b_lo] -= 1, hist[b] += 1.
 #include "cil_internal.cuh"
 
 namespace cil {
@@ -14,16 +14,16 @@ __global__ void __launch_bounds__(256) k_recheck(RecheckArgs a) {
         // overflow: flag every item (we do not know which pairs were dropped)
         for (int p = 0; p < a.P; ++p) atomicOr(&a.status[p], CIL_ITEM_OVERFLOW);
     }
-    const int lane = threadIdx.x & 31;
-    const uint32_t warps = gridDim.x * (blockDim.x >> 5);
-    for (uint32_t e = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); e < n; e += warps) {
+    __shared__ double red[8];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (uint32_t e = blockIdx.x; e < n; e += gridDim.x) {
         const uint4 ent = a.list[e];
         const int64_t p = ent.x, i = ent.y, j = ent.z;
         const int b_lo = (int)ent.w;
         const float* x = row_ptr(a.asrc, p, i);
         const float* y = row_ptr(a.bsrc, p, j);
         double s = 0.0;
-        for (int64_t k = lane * 4; k < a.K; k += 32 * 4) {
+        for (int64_t k = (int64_t)threadIdx.x * 4; k < a.K; k += 256 * 4) {
             const float4 u = __ldg(reinterpret_cast<const float4*>(x + k));
             const float4 v = __ldg(reinterpret_cast<const float4*>(y + k));
             const double d0 = (double)u.x - (double)v.x, d1 = (double)u.y - (double)v.y;
@@ -31,7 +31,11 @@ __global__ void __launch_bounds__(256) k_recheck(RecheckArgs a) {
             s = fma(d0, d0, s); s = fma(d1, d1, s); s = fma(d2, d2, s); s = fma(d3, d3, s);
         }
         for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if (lane == 0) {
+        if (lane == 0) red[w] = s;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            s = 0.0;
+            for (int t = 0; t < 8; ++t) s += red[t];
             const double* R = a.thr + p * a.thr_stride + (int64_t)a.q_l2 * a.M;
             int b = 0;
             while (b < a.M && s < R[b] * R[b] / a.w) ++b;
@@ -42,12 +46,16 @@ __global__ void __launch_bounds__(256) k_recheck(RecheckArgs a) {
                 if (b > 0) atomicAdd(&H[hist_index(a.sp, a.nq, a.M, p, rs, cs, a.q_l2, b)], 1ull);
             }
         }
+        __syncthreads();
     }
 }
 
 cudaError_t launch_recheck(const RecheckArgs& a, cudaStream_t st) {
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     ProfScope ps_(K_RECHECK, st);
-    k_recheck<<<296, 256, 0, st>>>(a);
+    k_recheck<<<nsm * 8, 256, 0, st>>>(a);
     note_launch();
     return cudaGetLastError();
 }
