@@ -248,12 +248,12 @@ cil_status run_engines(int P, const RowSrc& asrc, const RowSrc& bsrc, int64_t ro
             t.thr2 = thr2; t.thr_stride = M; t.M = M; t.q_l2 = sl.q_l2; t.nq = sl.nq;
             t.sp = sp; t.hist = hist;
             t.recheck = list; t.recheck_ctr = ctr; t.recheck_cap = L.list_cap;
-            // E = kq d sqrt((s_a^2 + s_b^2)/3) + kll s_a s_b + rel (n_a + n_b): 16 sigma of the operand
-            // quantisation (uniform error, variance s^2/12 per element, d^2 error 2 u.(da - db)), 16 sigma
-            // of the dropped LL digit product (E[l^2] ~ 128^2/3, x2 for d^2), FP32 rounding of d^2, the
+            // E = kq d sqrt((s_a^2 + s_b^2)/3) + kll s_a s_b + rel (n_a + n_b): 20 sigma of the operand
+            // quantisation (uniform error, variance s^2/12 per element, d^2 error 2 u.(da - db)), 8 sigma
+            // of the dropped LL digit product (Gaussian-like: mean |LL| / (sqrt(K) E[l^2]) = 0.80 measured) (E[l^2] ~ 128^2/3, x2 for d^2), FP32 rounding of d^2, the
             // norms and the thresholds (measured max error / E ~ 0.2).
-            t.kq = 16.0f;
-            t.kll = (float)(16.0 * 2.0 * (128.0 * 128.0 / 3.0) * sqrt((double)K));
+            t.kq = 20.0f;
+            t.kll = (float)(8.0 * 2.0 * (128.0 * 128.0 / 3.0) * sqrt((double)K));
             t.rel = (float)ldexp(1.0, -21);
             t.diag = diag;
             CIL_CU(launch_gram_i8(t, st));

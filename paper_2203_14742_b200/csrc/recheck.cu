@@ -23,7 +23,23 @@ __global__ void __launch_bounds__(256) k_recheck(RecheckArgs a) {
         const float* x = row_ptr(a.asrc, p, i);
         const float* y = row_ptr(a.bsrc, p, j);
         double s = 0.0;
-        for (int64_t k = (int64_t)threadIdx.x * 4; k < a.K; k += 256 * 4) {
+        // 4 independent float4 pairs in flight per thread (memory-level parallelism)
+        int64_t k = (int64_t)threadIdx.x * 4;
+        for (; k + 3 * 1024 < a.K; k += 4 * 1024) {
+            float4 u[4], v[4];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                u[t] = __ldg(reinterpret_cast<const float4*>(x + k + t * 1024));
+                v[t] = __ldg(reinterpret_cast<const float4*>(y + k + t * 1024));
+            }
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                const double d0 = (double)u[t].x - (double)v[t].x, d1 = (double)u[t].y - (double)v[t].y;
+                const double d2 = (double)u[t].z - (double)v[t].z, d3 = (double)u[t].w - (double)v[t].w;
+                s = fma(d0, d0, s); s = fma(d1, d1, s); s = fma(d2, d2, s); s = fma(d3, d3, s);
+            }
+        }
+        for (; k < a.K; k += 1024) {
             const float4 u = __ldg(reinterpret_cast<const float4*>(x + k));
             const float4 v = __ldg(reinterpret_cast<const float4*>(y + k));
             const double d0 = (double)u.x - (double)v.x, d1 = (double)u.y - (double)v.y;
