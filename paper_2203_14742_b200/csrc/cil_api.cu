@@ -87,10 +87,10 @@ struct Plan {
 
 // split: 1 = 3xBF16, 2 = 3xTF32, 3 = two-digit INT8.  AUTO takes INT8 when its exact int32
 // accumulation cannot overflow (K <= 65536) and its per-thread segment histograms fit
-// (column segments of >= 32 columns), else 3xBF16.
+// (column segments of >= 43 columns: a 128-column half meets <= 4), else 3xBF16.
 bool i8_ok(const cil_grid& g, int64_t col_seg, int64_t rowsB) {
     const int64_t K = (int64_t)g.S * g.H * g.W;
-    return K <= 65536 && (col_seg >= rowsB || col_seg >= 32);
+    return K <= 65536 && (col_seg >= rowsB || col_seg >= 43);
 }
 Plan make_plan(uint32_t mask, cil_engine engine, const cil_grid& g, int64_t col_seg = 1ll << 40,
                int64_t rowsB = 0) {

@@ -17,11 +17,12 @@
 //   warp 1      TMEM allocator + single-thread MMA issuer (leader CTA): HH -> cols [0,256),
 //               HL, LH -> cols [256,512)
 //   warps 2..9  epilogue: tcgen05.ld of H and X -> FP32 d^2 of 128 pairs per thread in registers
-//               -> TMEM released -> threshold search in shared memory -> per-thread 8-bit
-//               histograms per local column segment -> warp REDUX -> u64 atomics.
+//               -> branch-free threshold compares, cumulative per-thread counters -> warp REDUX
+//               -> u64 atomics per (row segment, column segment).
 #include <cuda.h>
 #include <stdio.h>
 #include <stdlib.h>
+
 
 #include "cil_internal.cuh"
 #include "tc_common.cuh"
@@ -57,11 +58,14 @@ __host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
     return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
-template <int MAXM> struct I8Geo {
+template <int MAXM, bool SEG> struct I8Geo {
     static constexpr int STAGES = MAXM <= 16 ? 3 : 2;
     static constexpr int STAGE_BYTES = Geo<2>::STAGE_BYTES;       // 64 KB: h, l of 128 A- and 128 B-rows
-    static constexpr int NLOC = 5;                                // local column segments per thread
-    static constexpr int HIST_BYTES = NLOC * (MAXM + 1) * 256;
+    // per-thread histograms [bin][thread] of u32 cells (bank = thread, conflict-free); with column
+    // segments (SCIL blocks of >= 43 columns, so a 128-column half meets <= 4) byte l of a cell
+    // counts local segment l (<= 128 pairs per tile, flushed every tile)
+    static constexpr int NLOC = SEG ? 4 : 1;
+    static constexpr int HIST_BYTES = (MAXM + 1) * 256 * 4;
     static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 1024 /*barriers*/ +
                                       3 * TILE_N * 4 /*norms, sigma, spare*/ + 2 * MAXM * 4 + HIST_BYTES;
 };
@@ -71,7 +75,7 @@ __global__ void __maxnreg__(168)
 k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUtensorMap mAl,
           const __grid_constant__ CUtensorMap mBh, const __grid_constant__ CUtensorMap mBl, I8Params prm) {
     using G = Geo<2>;
-    using IG = I8Geo<MAXM>;
+    using IG = I8Geo<MAXM, SEG>;
     constexpr int STAGES = IG::STAGES;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     // 1024-B alignment by offsetting the shared pointer itself (keeps the shared address space, so
@@ -86,7 +90,7 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
     float* s_nb = reinterpret_cast<float*>(smem + STAGES * IG::STAGE_BYTES + 1024);
     float* s_sb = s_nb + TILE_N;
     float* s_T = s_sb + 2 * TILE_N;                       // [2*MAXM] thresholds, -inf padded
-    uint8_t* h8 = reinterpret_cast<uint8_t*>(s_T + 2 * MAXM);
+    uint32_t* hist_s = reinterpret_cast<uint32_t*>(s_T + 2 * MAXM);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_rank();
@@ -109,10 +113,8 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
                      "r"(TMEM_COLS));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
     }
-    if (warp >= 2) {
-        const int et = threadIdx.x - 64;
-        for (int i = et; i < IG::HIST_BYTES / 4; i += 256) reinterpret_cast<uint32_t*>(h8)[i] = 0u;
-    }
+    if (warp >= 2)
+        for (int i = threadIdx.x - 64; i < IG::HIST_BYTES / 4; i += 256) reinterpret_cast<uint32_t*>(hist_s)[i] = 0u;
     fence_before();
     cluster_sync();
     fence_after();
@@ -197,114 +199,127 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
             const float na = row_ok ? __ldg(&prm.nrm[arow]) : 0.f;
             const float sa = row_ok ? __ldg(&prm.scl[arow]) : 0.f;
 
-            // ---- phase 1: TMEM -> FP32 d^2 of this thread's 128 pairs, then release TMEM
+            // ---- bin straight from TMEM in 8 rolled groups of 16 columns (compact loop body: an
+            // unrolled 128-pair body thrashed the instruction cache).  Per pair: d^2 and its bound E,
+            // bin b = #{m : d^2 + E < T_m} by a 5-level binary search (2 levels on registers, the rest
+            // in shared memory), one LDS for the ambiguity test, one per-thread shared histogram
+            // update; histograms are flushed once per tile (warp REDUX -> u64 atomics).
             mbar_wait(&tfull[0], tph);
             fence_after();
-            if (prm.dbg == 2) {
-                fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive_remote(&tempty[0], 0);
-                tph ^= 1;
-                continue;
-            }
-            float d2v[128];
+            const int hc0 = (int)(col0 + half * 128);
+            const int nvalid = (int)min((int64_t)128, prm.rowsB - hc0);   // warp-uniform
+            const bool diag_mode = prm.diag != nullptr && p == 0;          // diagnostics (item 0 only)
+            float* diag_row = diag_mode ? prm.diag + (size_t)(row_ok ? row : 0) * prm.rowsB * 2 : nullptr;
+            const float kq_sa = prm.kq * 0.81649658f;    // sqrt((sa^2 + sb^2)/3) <= sqrt(2/3) max(sa, sb)
+            const float kll_sa = prm.kll * sa;
+            const float m2sa = -2.f * sa;
+            const float reln = prm.rel;
             const uint32_t tl = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(half * 128);
+            const bool skip = prm.dbg == 2 || (prm.diag != nullptr && p != 0);
+            const float T_top = s_T[MAXM - 1], T_mid = s_T[MAXM / 2 - 1];
+            const float T_q1 = s_T[MAXM / 4 - 1], T_q3 = s_T[MAXM / 2 + MAXM / 4 - 1];
+            const int64_t cs_first = (int64_t)hc0 / prm.sp.col_seg;
+            int bnd[IG::NLOC > 1 ? IG::NLOC - 1 : 1];    // local column indices where the segment changes
 #pragma unroll
-            for (int ch = 0; ch < 8; ++ch) {
+            for (int i = 0; i < IG::NLOC - 1; ++i) {
+                const int64_t c = (cs_first + 1 + i) * prm.sp.col_seg - hc0;
+                bnd[i] = SEG ? (int)(c < 128 ? c : (1 << 30)) : (1 << 30);
+            }
+            uint32_t* myh = hist_s + et;
+
+#pragma unroll 1
+            for (int g = 0; g < 8 && !skip; ++g) {
+                if (g * 16 >= nvalid) break;                        // warp-uniform
                 uint32_t hv[16], xv[16];
-                tmem_ld16(tl + ch * 16, hv);
-                tmem_ld16(tl + TILE_N + ch * 16, xv);
+                tmem_ld16(tl + g * 16, hv);
+                tmem_ld16(tl + TILE_N + g * 16, xv);
+                if (prm.dbg == 1 || !row_ok) continue;
+                // phase A (loads + ALU only, so the compiler overlaps the 16 pairs' search chains):
+                // bin b_j = #{m : hi_j < T_m} and the ambiguity bit of every pair of the group
+                int bin[16];                                // b | (local column segment << 8)
+                uint32_t amb = 0;
 #pragma unroll
                 for (int jj = 0; jj < 16; ++jj) {
-                    const int j = half * 128 + ch * 16 + jj;
-                    // 65536 H + 256 X needs ~47 bits: combine and cancel in FP64, round d^2 once
-                    const double gi = fma((double)(int)hv[jj], 65536.0, (double)(int)xv[jj] * 256.0);
-                    d2v[ch * 16 + jj] = (float)fma(-2.0 * (double)sa * (double)s_sb[j], gi, (double)na + (double)s_nb[j]);
+                    const int j = g * 16 + jj;
+                    const int jc = half * 128 + j;
+                    const float sb = s_sb[jc], nb = s_nb[jc];
+                    // 65536 H + 256 X in FP32 (relative rounding 2^-24 of g, inside rel): measured
+                    // identical to an FP64 combination on generator data
+                    const float gi = fmaf((float)(int)hv[jj], 65536.f, (float)(int)xv[jj] * 256.f);
+                    const float d2 = fmaf(m2sa * sb, gi, na + nb);
+                    const float dd = fmaxf(d2, 1e-30f);
+                    const float E = fmaf(kq_sa * dd * rsqrtf(dd), fmaxf(sa, sb), fmaf(kll_sa, sb, reln * (na + nb)));
+                    if (diag_mode) {
+                        if (j < nvalid) {
+                            diag_row[2 * (hc0 + j)] = d2;
+                            diag_row[2 * (hc0 + j) + 1] = E;
+                        }
+                        continue;
+                    }
+                    const float hi = d2 + E, lo = d2 - E;
+                    // binary search over the decreasing thresholds (s_T[MAXM..2 MAXM) = -inf):
+                    // two levels from registers, the remaining log2(MAXM) - 2 from shared memory
+                    int b = (hi < T_mid) ? MAXM / 2 : 0;
+                    b += (hi < (b ? T_q3 : T_q1)) ? MAXM / 4 : 0;
+#pragma unroll
+                    for (int s = MAXM / 8; s >= 1; s >>= 1)
+                        if (hi < s_T[b + s - 1]) b += s;
+                    b = (hi < T_top) ? MAXM : b;
+                    int lcs = 0;
+                    if (SEG) {
+#pragma unroll
+                        for (int i = 0; i < IG::NLOC - 1; ++i) lcs += (j >= bnd[i]) ? 1 : 0;
+                    }
+                    bin[jj] = b | (lcs << 8);
+                    // a threshold in (lo, hi]: provisional bin b, exact re-check
+                    amb |= (lo < s_T[b] && j < nvalid) ? (1u << jj) : 0u;
+                }
+                if (diag_mode) continue;
+                // phase B: per-thread histogram increments (fire-and-forget shared atomics)
+#pragma unroll
+                for (int jj = 0; jj < 16; ++jj)
+                    if (g * 16 + jj < nvalid)
+                        atomicAdd(myh + ((bin[jj] & 255) << 8), SEG ? 1u << ((bin[jj] >> 5) & 24) : 1u);
+                if (amb) {                                  // rare (~1e-4 of the pairs)
+#pragma unroll
+                    for (int jj = 0; jj < 16; ++jj) {
+                        if (!((amb >> jj) & 1u)) continue;
+                        const uint32_t idx = atomicAdd(prm.ctr, 1u);
+                        if (idx < prm.cap)
+                            prm.list[idx] = make_uint4((uint32_t)p, (uint32_t)row, (uint32_t)(hc0 + g * 16 + jj),
+                                                       (uint32_t)(bin[jj] & 255));
+                    }
                 }
             }
             fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_remote(&tempty[0], 0);
             tph ^= 1;
-
-            if (prm.dbg == 1) {
-                float s = 0.f;
-#pragma unroll
-                for (int j = 0; j < 128; ++j) s += d2v[j];
-                if (s == 1.2345f) prm.hist[0] = 1;
-                continue;
-            }
-            // ---- phase 2: error bound, threshold search, 8-bit histograms
-            const int64_t hc0 = col0 + half * 128;
-            const int64_t cs_first = hc0 / prm.sp.col_seg;
-            int bnd[IG::NLOC - 1];                       // local column indices where the segment changes
-#pragma unroll
-            for (int i = 0; i < IG::NLOC - 1; ++i) {
-                const int64_t c = (cs_first + 1 + i) * prm.sp.col_seg - hc0;
-                bnd[i] = SEG ? (int)(c < 128 ? c : (1 << 30)) : (1 << 30);
-            }
-            const int nvalid = (int)min((int64_t)128, prm.rowsB - hc0);   // warp-uniform
-            const bool diag_mode = prm.diag != nullptr;  // diagnostics (item 0 only), uniform per kernel
-            float* diag_row = diag_mode ? prm.diag + (size_t)(row_ok ? row : 0) * prm.rowsB * 2 : nullptr;
-            if (diag_mode && p != 0) continue;
-            const float kq_sa = prm.kq * 0.81649658f;    // sqrt((sa^2 + sb^2)/3) <= sqrt(2/3) max(sa, sb)
-            const float kll_sa = prm.kll * sa;
-            uint8_t* myh = h8 + et;
-#pragma unroll
-            for (int j = 0; j < 128; ++j) {
-                if (j >= nvalid || !row_ok) continue;       // predicated: keeps d2v[] in registers
-                const int jc = half * 128 + j;
-                const float d2 = d2v[j];
-                const float sb = s_sb[jc];
-                const float dd = fmaxf(d2, 1e-30f);
-                const float E = fmaf(kq_sa * dd * rsqrtf(dd), fmaxf(sa, sb),
-                                     fmaf(kll_sa, sb, prm.rel * (na + s_nb[jc])));
-                if (diag_mode) {
-                    diag_row[2 * (hc0 + j)] = d2;
-                    diag_row[2 * (hc0 + j) + 1] = E;
-                    continue;
-                }
-                const float hi = d2 + E, lo = d2 - E;
-                int b = 0;
-#pragma unroll
-                for (int s = MAXM; s >= 1; s >>= 1)
-                    if (hi < s_T[b + s - 1]) b += s;
-                int lcs = 0;
-                if (SEG) {
-#pragma unroll
-                    for (int i = 0; i < IG::NLOC - 1; ++i) lcs += (j >= bnd[i]) ? 1 : 0;
-                }
-                uint8_t* cell = myh + ((lcs * (MAXM + 1) + b) << 8);
-                *cell = (uint8_t)(*cell + 1);
-                if (lo < s_T[b]) {
-                    const uint32_t idx = atomicAdd(prm.ctr, 1u);
-                    if (idx < prm.cap)
-                        prm.list[idx] = make_uint4((uint32_t)p, (uint32_t)row, (uint32_t)(hc0 + j), (uint32_t)b);
-                }
-            }
-            // ---- flush the local histograms (u8 -> warp sums -> global u64)
+            if (skip || prm.dbg == 1) continue;
+            // ---- flush the per-thread histograms (warp sums -> global u64 atomics), reset them.
+            // Cell [b][thread] is a u32; with column segments (SEG) byte l counts local segment l.
             const int64_t rs = row_ok ? row / prm.sp.row_seg : 0;
             const int64_t rs0 = __shfl_sync(0xffffffffu, rs, 0);
             const bool uniform = __all_sync(0xffffffffu, rs == rs0 || !row_ok);
-            const int nloc = SEG ? IG::NLOC : 1;
-            for (int l = 0; l < nloc; ++l) {
-                const int64_t cs = cs_first + l;
-                if (cs * prm.sp.col_seg >= prm.rowsB || cs * prm.sp.col_seg >= col0 + TILE_N) break;
-                for (int b = 1; b <= M; ++b) {
-                    uint8_t* cell = myh + ((l * (MAXM + 1) + b) << 8);
-                    const uint32_t v = *cell;
-                    *cell = 0;
+            myh[0] = 0u;                                    // bin 0 (outside every radius) is not kept
+            for (int bb = 1; bb <= M; ++bb) {
+                const uint32_t cell = myh[bb << 8];
+                myh[bb << 8] = 0u;
+#pragma unroll
+                for (int l = 0; l < IG::NLOC; ++l) {
+                    const int64_t cs = cs_first + l;
+                    if (cs * prm.sp.col_seg >= prm.rowsB || cs * prm.sp.col_seg >= hc0 + 128) break;
+                    const uint32_t v = SEG ? ((cell >> (8 * l)) & 255u) : cell;
                     if (uniform) {
                         const uint32_t tot = __reduce_add_sync(0xffffffffu, v);
                         if (lane == 0 && tot)
-                            atomicAdd(&prm.hist[hist_index(prm.sp, prm.nq, M, p, rs0, cs, prm.q_l2, b)],
+                            atomicAdd(&prm.hist[hist_index(prm.sp, prm.nq, M, p, rs0, cs, prm.q_l2, bb)],
                                       (unsigned long long)tot);
                     } else if (v) {
-                        atomicAdd(&prm.hist[hist_index(prm.sp, prm.nq, M, p, rs, cs, prm.q_l2, b)],
+                        atomicAdd(&prm.hist[hist_index(prm.sp, prm.nq, M, p, rs, cs, prm.q_l2, bb)],
                                   (unsigned long long)v);
                     }
                 }
-                *(myh + ((l * (MAXM + 1)) << 8)) = 0;      // bin 0 (outside every radius) is not kept
             }
         }
     }
@@ -343,7 +358,7 @@ static bool make_map_i8(CUtensorMap* m, const void* base, int64_t rows, int64_t 
 
 template <int MAXM, bool SEG>
 static cudaError_t launch_i8_t(const tc::I8Params& prm, const CUtensorMap* maps, int nsm, cudaStream_t st) {
-    using IG = tc::I8Geo<MAXM>;
+    using IG = tc::I8Geo<MAXM, SEG>;
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(tc::k_gram_i8<MAXM, SEG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
