@@ -42,7 +42,9 @@ def test_workspace_sizes(capi):
     G = capi.Grid
     ws = capi.lib.cil_features_workspace_size
     g = G(2, 64, 64, 0.0)
-    assert ws(100, 500, 500, g, 1, 15, 0) > 100 * 1000 * 8192 * 4       # hi + lo bf16 operands
+    assert ws(100, 500, 500, g, 1, 15, 0) > 100 * 1000 * 8192 * 2       # AUTO = INT8: h + l digit planes
+    assert ws(100, 500, 500, g, 1, 15, 1) > 100 * 1000 * 8192 * 4       # 3xBF16: hi + lo bf16 operands
+    assert ws(100, 500, 500, g, 1, 15, 4) < ws(100, 500, 500, g, 1, 15, 1)
     assert ws(1, 20, 20, G(1, 32, 32, 0.0), 0x3F, 10, 3) > 0
     assert ws(1, 20, 20, g, 0, 10, 0) == 0                               # empty mask
     assert ws(1, 20, 20, g, 0x40, 10, 0) == 0                            # unknown measure bit
