@@ -236,10 +236,8 @@ cil_status run_engines(int P, const RowSrc& asrc, const RowSrc& bsrc, int64_t ro
         CIL_CU(launch_center(P, bsrc, rowsB < 16 ? rowsB : 16, K, L.Kp, center, st));
         if (pl.split == 3) {
             // ---- INT8 two-digit engine (default): exact int32 accumulation
-            CIL_CU(launch_pack_i8(P, asrc, rowsA, K, L.Kp, center, reinterpret_cast<int8_t*>(hi),
-                                  reinterpret_cast<int8_t*>(lo), nrm, q4, status, st));
-            CIL_CU(launch_pack_i8(P, bsrc, rowsB, K, L.Kp, center, reinterpret_cast<int8_t*>(hi + offB * L.Kp),
-                                  reinterpret_cast<int8_t*>(lo + offB * L.Kp), nrm + offB, q4 + offB, status, st));
+            CIL_CU(launch_pack_i8_pair(P, asrc, rowsA, bsrc, rowsB, K, L.Kp, center, reinterpret_cast<int8_t*>(hi),
+                                       reinterpret_cast<int8_t*>(lo), nrm, q4, status, st));
             I8Args t{};
             t.hq = reinterpret_cast<const int8_t*>(hi); t.lq = reinterpret_cast<const int8_t*>(lo);
             t.nrm = nrm; t.scl = q4;

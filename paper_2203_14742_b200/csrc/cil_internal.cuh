@@ -128,6 +128,9 @@ cudaError_t launch_pack_tc(int P, const RowSrc& src, int64_t rows, int64_t K, in
 
 cudaError_t launch_pack_i8(int P, const RowSrc& src, int64_t rows, int64_t K, int64_t Kp, const float* center,
                            int8_t* hq, int8_t* lq, float* nrm, float* scl, int32_t* status, cudaStream_t st);
+cudaError_t launch_pack_i8_pair(int P, const RowSrc& asrc, int64_t rowsA, const RowSrc& bsrc, int64_t rowsB,
+                                int64_t K, int64_t Kp, const float* center, int8_t* hq, int8_t* lq, float* nrm,
+                                float* scl, int32_t* status, cudaStream_t st);
 
 // simt_tile.cu
 struct SimtArgs {

@@ -45,7 +45,8 @@ struct I8Params {
     uint4* list; uint32_t* ctr; uint32_t cap;
     float kq, kll, rel;
     float* diag;
-    int dbg;                   // diagnostic timing knob (CIL_DEBUG_I8): 1 skip binning, 2 skip the epilogue
+    int dbg;                   // diagnostic timing knob (CIL_DEBUG_I8): 1 skip binning, 2 skip the epilogue,
+                               // 3 also skip the B loads, 4 all loads
 };
 
 __device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
@@ -132,12 +133,19 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
                 for (int kb = 0; kb < prm.n_kb; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     unsigned char* st = stages + stage * IG::STAGE_BYTES;
-                    if (rank == 0) mbar_expect_tx(&full[stage], 2 * IG::STAGE_BYTES);
+                    // diagnostics: dbg 3 skips the B loads, dbg 4 all loads (MMA rate alone)
+                    const bool only_a = prm.dbg == 3, none = prm.dbg == 4;
+                    if (rank == 0)
+                        mbar_expect_tx(&full[stage], none ? 0 : only_a ? 4 * G::A_BYTES : 2 * IG::STAGE_BYTES);
                     const int x = kb * 128;
-                    tma_load_2d<2>(st, &mAh, &full[stage], x, ya);
-                    tma_load_2d<2>(st + G::A_BYTES, &mAl, &full[stage], x, ya);
-                    tma_load_2d<2>(st + 2 * G::A_BYTES, &mBh, &full[stage], x, yb);
-                    tma_load_2d<2>(st + 2 * G::A_BYTES + G::B_BYTES, &mBl, &full[stage], x, yb);
+                    if (!none) {
+                        tma_load_2d<2>(st, &mAh, &full[stage], x, ya);
+                        tma_load_2d<2>(st + G::A_BYTES, &mAl, &full[stage], x, ya);
+                    }
+                    if (!only_a && !none) {
+                        tma_load_2d<2>(st + 2 * G::A_BYTES, &mBh, &full[stage], x, yb);
+                        tma_load_2d<2>(st + 2 * G::A_BYTES + G::B_BYTES, &mBl, &full[stage], x, yb);
+                    }
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
             }
@@ -215,7 +223,7 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
             const float m2sa = -2.f * sa;
             const float reln = prm.rel;
             const uint32_t tl = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(half * 128);
-            const bool skip = prm.dbg == 2 || (prm.diag != nullptr && p != 0);
+            const bool skip = prm.dbg >= 2 || (prm.diag != nullptr && p != 0);
             const float T_top = s_T[MAXM - 1], T_mid = s_T[MAXM / 2 - 1];
             const float T_q1 = s_T[MAXM / 4 - 1], T_q3 = s_T[MAXM / 2 + MAXM / 4 - 1];
             const int64_t cs_first = (int64_t)hc0 / prm.sp.col_seg;

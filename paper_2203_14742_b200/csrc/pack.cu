@@ -255,10 +255,29 @@ __global__ void __launch_bounds__(256) k_pack_i8(RowSrc src, int64_t rows, int64
     }
 }
 
-// Single-pass variant: the whole row is held in registers (NV float4 per thread, 256 threads,
-// K <= NV * 1024), so HBM is read once; same arithmetic as k_pack_i8.
-template <int NV>
-__global__ void __launch_bounds__(256) k_pack_i8r(RowSrc src, int64_t rows, int64_t K, int64_t Kp,
+// rint(e * inv) as q (the 1.5 * 2^23 constant: one FFMA, ties to even, exact for |q| < 2^22;
+// |e * inv| <= 32639 by construction of sigma), then the two signed digits h = (q + 128) >> 8,
+// l = q - 256 h, and q^2 (4 x 32639^2 < 2^32).  Non-finite e gives garbage digits, never a
+// fault; the item is flagged NONFINITE by the caller.
+__device__ __forceinline__ void quant4(const float4 e, float inv, char4& h4, char4& l4, uint32_t& sq) {
+    const float ev[4] = {e.x, e.y, e.z, e.w};
+    int hh[4], ll[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+        const int q = __float_as_int(fmaf(ev[t], inv, 12582912.f)) - 0x4B400000;
+        const int h = (q + 128) >> 8;
+        hh[t] = h;
+        ll[t] = q - 256 * h;
+        sq += (uint32_t)(q * q);
+    }
+    h4 = make_char4((signed char)hh[0], (signed char)hh[1], (signed char)hh[2], (signed char)hh[3]);
+    l4 = make_char4((signed char)ll[0], (signed char)ll[1], (signed char)ll[2], (signed char)ll[3]);
+}
+
+// Single-pass variant: the whole row is held in registers (NV float4 per thread, NT threads,
+// K <= NV * NT * 4), so HBM is read once; same arithmetic as k_pack_i8.
+template <int NV, int NT>
+__global__ void __launch_bounds__(NT) k_pack_i8r(RowSrc src, int64_t rows, int64_t K, int64_t Kp,
                                                   const float* __restrict__ center, int8_t* __restrict__ hq,
                                                   int8_t* __restrict__ lq, float* __restrict__ nrm,
                                                   float* __restrict__ scl, int32_t* __restrict__ status) {
@@ -267,18 +286,17 @@ __global__ void __launch_bounds__(256) k_pack_i8r(RowSrc src, int64_t rows, int6
     const float* x = row_ptr(src, p, r);
     const float* c = center + p * Kp;
     const int64_t orow = p * rows + r;
-    __shared__ float red[8];
-    __shared__ double redd[8];
+    __shared__ float red[NT / 32];
+    __shared__ unsigned long long redd[NT / 32];
     float4 v[NV];
-    float mx = 0.f;
-    bool nonfinite = false;
+    float mx = 0.f, nfa = 0.f;                // nfa = sum of x * 0: NaN iff some x is not finite
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
-        const int64_t k = ((int64_t)i * 256 + threadIdx.x) * 4;
+        const int64_t k = ((int64_t)i * NT + threadIdx.x) * 4;
         if (k < K) {
             const float4 xv = __ldg(reinterpret_cast<const float4*>(x + k));
             const float4 cv = __ldg(reinterpret_cast<const float4*>(c + k));
-            nonfinite |= !(isfinite(xv.x) && isfinite(xv.y) && isfinite(xv.z) && isfinite(xv.w));
+            nfa = fmaf(xv.x, 0.f, fmaf(xv.y, 0.f, fmaf(xv.z, 0.f, fmaf(xv.w, 0.f, nfa))));
             v[i] = make_float4(xv.x - cv.x, xv.y - cv.y, xv.z - cv.z, xv.w - cv.w);
         } else {
             v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -287,42 +305,34 @@ __global__ void __launch_bounds__(256) k_pack_i8r(RowSrc src, int64_t rows, int6
     }
     for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
-    const bool anynf = __syncthreads_or(nonfinite);
+    const bool anynf = __syncthreads_or(nfa != nfa);
     if (ln == 0) red[w] = mx;
     __syncthreads();
     mx = 0.f;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) mx = fmaxf(mx, red[i]);
+    for (int i = 0; i < NT / 32; ++i) mx = fmaxf(mx, red[i]);
     const float sigma = (mx > 0.f && isfinite(mx)) ? mx / 32639.f : 1.f;
     const float inv = 1.f / sigma;
-    double s2 = 0.0;
+    unsigned long long s2 = 0ull;
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
-        const int64_t k = ((int64_t)i * 256 + threadIdx.x) * 4;
+        const int64_t k = ((int64_t)i * NT + threadIdx.x) * 4;
         if (k >= Kp) continue;
-        const float e[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
-        int hh[4], ll[4];
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-            const int q = isfinite(e[t]) ? max(-32639, min(32639, __float2int_rn(e[t] * inv))) : 0;
-            const int h = (q + 128) >> 8;
-            hh[t] = h;
-            ll[t] = q - 256 * h;
-            s2 += (double)(q * q);                   // q^2 < 2^30: exact in int32
-        }
-        *reinterpret_cast<char4*>(hq + orow * Kp + k) =
-            make_char4((signed char)hh[0], (signed char)hh[1], (signed char)hh[2], (signed char)hh[3]);
-        *reinterpret_cast<char4*>(lq + orow * Kp + k) =
-            make_char4((signed char)ll[0], (signed char)ll[1], (signed char)ll[2], (signed char)ll[3]);
+        char4 h4, l4;
+        uint32_t sq = 0;
+        quant4(v[i], inv, h4, l4, sq);
+        s2 += sq;
+        *reinterpret_cast<char4*>(hq + orow * Kp + k) = h4;
+        *reinterpret_cast<char4*>(lq + orow * Kp + k) = l4;
     }
     for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
     if (ln == 0) redd[w] = s2;
     __syncthreads();
     if (threadIdx.x == 0) {
-        double a = 0.0;
+        unsigned long long a = 0ull;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) a += redd[i];
-        nrm[orow] = (float)(a * (double)sigma * (double)sigma);
+        for (int i = 0; i < NT / 32; ++i) a += redd[i];
+        nrm[orow] = (float)((double)a * (double)sigma * (double)sigma);
         scl[orow] = sigma;
         if (anynf) atomicOr(&status[p], CIL_ITEM_NONFINITE);
     }
@@ -334,17 +344,28 @@ cudaError_t launch_pack_i8(int P, const RowSrc& src, int64_t rows, int64_t K, in
     dim3 grid((unsigned)rows, (unsigned)P);
     ProfScope ps_(K_PACK, st);
     if (Kp <= 4096)
-        k_pack_i8r<4><<<grid, 256, 0, st>>>(src, rows, K, Kp, center, hq, lq, nrm, scl, status);
+        k_pack_i8r<4, 256><<<grid, 256, 0, st>>>(src, rows, K, Kp, center, hq, lq, nrm, scl, status);
     else if (Kp <= 8192)
-        k_pack_i8r<8><<<grid, 256, 0, st>>>(src, rows, K, Kp, center, hq, lq, nrm, scl, status);
+        k_pack_i8r<8, 256><<<grid, 256, 0, st>>>(src, rows, K, Kp, center, hq, lq, nrm, scl, status);
     else if (Kp <= 16384)
-        k_pack_i8r<16><<<grid, 256, 0, st>>>(src, rows, K, Kp, center, hq, lq, nrm, scl, status);
+        k_pack_i8r<8, 512><<<grid, 512, 0, st>>>(src, rows, K, Kp, center, hq, lq, nrm, scl, status);
     else if (Kp <= 32768)
-        k_pack_i8r<32><<<grid, 256, 0, st>>>(src, rows, K, Kp, center, hq, lq, nrm, scl, status);
+        k_pack_i8r<8, 1024><<<grid, 1024, 0, st>>>(src, rows, K, Kp, center, hq, lq, nrm, scl, status);
     else
         k_pack_i8<<<grid, 256, 0, st>>>(src, rows, K, Kp, center, hq, lq, nrm, scl, status);
     note_launch();
     return cudaGetLastError();
+}
+
+// Both panels (A rows then B rows in the stacked layout the Gram's TMA maps expect).
+cudaError_t launch_pack_i8_pair(int P, const RowSrc& asrc, int64_t rowsA, const RowSrc& bsrc, int64_t rowsB,
+                                int64_t K, int64_t Kp, const float* center, int8_t* hq, int8_t* lq, float* nrm,
+                                float* scl, int32_t* status, cudaStream_t st) {
+    const int64_t offB = (int64_t)P * rowsA;
+    const cudaError_t e = launch_pack_i8(P, asrc, rowsA, K, Kp, center, hq, lq, nrm, scl, status, st);
+    if (e != cudaSuccess) return e;
+    return launch_pack_i8(P, bsrc, rowsB, K, Kp, center, hq + offB * Kp, lq + offB * Kp, nrm + offB, scl + offB,
+                          status, st);
 }
 
 // ---------------------------------------------------------------------- aug pack
