@@ -69,13 +69,19 @@ __global__ void k_center(RowSrc src, int64_t nrc, int64_t K, int64_t Kp, float* 
     const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= Kp) return;
     double s = 0.0;
-    if (k < K)
-        for (int64_t r = 0; r < nrc; ++r) s += (double)__ldg(row_ptr(src, p, r) + k);
+    if (k < K) {
+        float v[16];                                  // nrc <= 16: all loads in flight, then the sum
+#pragma unroll
+        for (int r = 0; r < 16; ++r) v[r] = r < nrc ? __ldg(row_ptr(src, p, r) + k) : 0.f;
+#pragma unroll
+        for (int r = 0; r < 16; ++r) s += (double)v[r];
+    }
     center[p * Kp + k] = (k < K && nrc > 0) ? (float)(s / (double)nrc) : 0.0f;
 }
 
 cudaError_t launch_center(int P, const RowSrc& colsrc, int64_t nrc, int64_t K, int64_t Kp,
                           float* center, cudaStream_t st) {
+    if (nrc > 16) return cudaErrorInvalidValue;
     dim3 grid((unsigned)((Kp + 255) / 256), (unsigned)P);
     ProfScope ps_(K_PACK, st);
     k_center<<<grid, 256, 0, st>>>(colsrc, nrc, K, Kp, center);

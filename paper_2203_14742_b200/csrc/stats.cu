@@ -70,9 +70,63 @@ __global__ void k_cov(const double* __restrict__ Y, int64_t y_stride, int n, int
     }
 }
 
+// Fused mu + Sigma for one item per CTA when Y[p] fits in shared memory (n*D*8 <= 40 KB):
+// the same two-pass sums as k_mean / k_cov, with the n-long sums split over the lanes of a
+// warp (one warp per column a, then one warp per pair b <= a) and reduced by shuffles.
+constexpr int kStatsSmem = 40 * 1024;
+__global__ void __launch_bounds__(256) k_stats_smem(const double* __restrict__ Y, int64_t y_stride, int n, int D,
+                                                    double* __restrict__ mu, double* __restrict__ Sigma) {
+    extern __shared__ double ys[];                   // [n][D], centred in place after pass 1
+    __shared__ double mus[kMaxD];
+    const int p = blockIdx.x, lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const double* Yp = Y + (int64_t)p * y_stride;
+    for (int i = threadIdx.x; i < n * D; i += blockDim.x) ys[i] = Yp[i];
+    __syncthreads();
+    for (int a = w; a < D; a += nw) {
+        double s = 0.0;
+        for (int v = lane; v < n; v += 32) s += ys[v * D + a];
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) {
+            mus[a] = s / n;
+            mu[(int64_t)p * D + a] = s / n;
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < n * D; i += blockDim.x) ys[i] -= mus[i % D];
+    __syncthreads();
+    const int npair = D * (D + 1) / 2;
+    for (int t = w; t < npair; t += nw) {
+        int a = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);    // t = a(a+1)/2 + b, b <= a
+        while (a * (a + 1) / 2 > t) --a;
+        while ((a + 1) * (a + 2) / 2 <= t) ++a;
+        const int b = t - a * (a + 1) / 2;
+        double s = 0.0;
+        for (int v = lane; v < n; v += 32) s += ys[v * D + a] * ys[v * D + b];
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) {
+            const double c = s / (n - 1);
+            Sigma[((int64_t)p * D + a) * D + b] = c;
+            Sigma[((int64_t)p * D + b) * D + a] = c;
+        }
+    }
+}
+
 static cudaError_t launch_stats_strided(int P, const double* Y, int64_t y_stride, int n, int D,
                                         double* mu, double* Sigma, cudaStream_t st) {
     ProfScope ps_(K_TAIL, st);
+    const size_t smem = sizeof(double) * (size_t)n * D;
+    if (smem <= (size_t)kStatsSmem) {
+        static bool attr = false;
+        if (!attr) {
+            const cudaError_t e =
+                cudaFuncSetAttribute(k_stats_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, kStatsSmem);
+            if (e != cudaSuccess) return e;
+            attr = true;
+        }
+        k_stats_smem<<<P, 256, smem, st>>>(Y, y_stride, n, D, mu, Sigma);
+        note_launch();
+        return cudaGetLastError();
+    }
     k_mean<<<P, 128, 0, st>>>(Y, y_stride, n, D, mu);
     note_launch();
     dim3 g((unsigned)D, (unsigned)P);
