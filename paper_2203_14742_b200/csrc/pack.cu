@@ -64,25 +64,33 @@ cudaError_t launch_prep(int P, int nq, int M, const double* radii, int64_t radii
 // c[p][k] = mean of the first nrc rows of the item's column panel, FP64
 // accumulation, rounded to FP32.  A numerical device only (conditioning of the
 // Gram, DESIGN.md §L2 engine): distances are translation invariant.
-__global__ void k_center(RowSrc src, int64_t nrc, int64_t K, int64_t Kp, float* __restrict__ center) {
+__global__ void __launch_bounds__(256) k_center(RowSrc src, int64_t nrc, int64_t K, int64_t Kp,
+                                                float* __restrict__ center) {
     const int64_t p = blockIdx.y;
-    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t k = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;   // K % 4 == 0, Kp % 128 == 0
     if (k >= Kp) return;
-    double s = 0.0;
+    double s[4] = {0.0, 0.0, 0.0, 0.0};
     if (k < K) {
-        float v[16];                                  // nrc <= 16: all loads in flight, then the sum
+        float4 v[16];                                 // nrc <= 16: all loads in flight, then the sums
 #pragma unroll
-        for (int r = 0; r < 16; ++r) v[r] = r < nrc ? __ldg(row_ptr(src, p, r) + k) : 0.f;
+        for (int r = 0; r < 16; ++r)
+            v[r] = r < nrc ? __ldg(reinterpret_cast<const float4*>(row_ptr(src, p, r) + k)) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-        for (int r = 0; r < 16; ++r) s += (double)v[r];
+        for (int r = 0; r < 16; ++r) {
+            s[0] += (double)v[r].x; s[1] += (double)v[r].y; s[2] += (double)v[r].z; s[3] += (double)v[r].w;
+        }
     }
-    center[p * Kp + k] = (k < K && nrc > 0) ? (float)(s / (double)nrc) : 0.0f;
+    float4 c = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (k < K && nrc > 0)
+        c = make_float4((float)(s[0] / (double)nrc), (float)(s[1] / (double)nrc), (float)(s[2] / (double)nrc),
+                        (float)(s[3] / (double)nrc));
+    *reinterpret_cast<float4*>(center + p * Kp + k) = c;
 }
 
 cudaError_t launch_center(int P, const RowSrc& colsrc, int64_t nrc, int64_t K, int64_t Kp,
                           float* center, cudaStream_t st) {
     if (nrc > 16) return cudaErrorInvalidValue;
-    dim3 grid((unsigned)((Kp + 255) / 256), (unsigned)P);
+    dim3 grid((unsigned)((Kp / 4 + 255) / 256), (unsigned)P);
     ProfScope ps_(K_PACK, st);
     k_center<<<grid, 256, 0, st>>>(colsrc, nrc, K, Kp, center);
     note_launch();
