@@ -77,12 +77,13 @@ typedef enum {
  * re-evaluated exactly (FP64) — so counts are exact either way.  SIMT = FP32
  * differences on CUDA cores with FP64-flushed sums. */
 typedef enum {
-    CIL_ENGINE_AUTO = 0,      /* TC_I8 when K <= 65536 and column segments >= 32, else TC_3XBF16 */
+    CIL_ENGINE_AUTO = 0,      /* TC_I8 when K <= 65536 and column segments >= 43 (SCIL blocks), else TC_3XBF16 */
     CIL_ENGINE_TC_3XBF16 = 1,
     CIL_ENGINE_TC_3XTF32 = 2,
     CIL_ENGINE_SIMT = 3,
     CIL_ENGINE_TC_I8 = 4      /* two-digit INT8 fixed point per row (x~ = sigma (256 h + l)), exact int32
-                                 tcgen05 kind::i8 accumulation; K <= 65536 */
+                                 tcgen05 kind::i8 accumulation; K <= 65536, column segments >= 43
+                                 (else it runs as TC_3XBF16) */
 } cil_engine;
 
 typedef struct {
