@@ -128,3 +128,42 @@ def make_set(seed: int, set_id: int, n: int, grid, profile: str = "GM", device="
 # Seeds per config: 22031474200 + config number.
 def config_seed(config_number: int) -> int:
     return 22031474200 + int(config_number)
+
+
+# --------------------------------------------------------------------------- bootstrap draws
+# The random draws of the bootstrap estimators (Alg. A1 / A2) are inputs
+# of both the library and the oracle (reading R14 of DESIGN.md): seeded, host-side, no
+# method arithmetic.  Uniforms come from the same splitmix64 counters as the patterns.
+def _draw_uniforms(seed: int, stream: int, shape) -> np.ndarray:
+    n = int(np.prod(shape))
+    u = uniforms(seed, 1_000_000 + stream, np.arange(1, dtype=np.int64), n)[0]
+    return u.reshape(shape)
+
+
+def boot_draws_a2(seed: int, stream: int, n_rep: int, N_syn: int, N_set: int):
+    """Alg. A2 draws for one theta: I1 [n_rep][N_set] with replacement from the pool
+    (step 2.1); I2 [n_rep][N_syn - N_set] with replacement from the patterns NOT drawn
+    into s^1 of the same replicate (step 2.2, "the remaining patterns"); J [N_syn - N_set]
+    a subset of the pool without replacement (step 4)."""
+    Nt = N_syn - N_set
+    u1 = _draw_uniforms(seed, 3 * stream, (n_rep, N_set))
+    I1 = np.minimum((u1 * N_syn).astype(np.int64), N_syn - 1)
+    drawn = np.zeros((n_rep, N_syn), dtype=bool)
+    np.put_along_axis(drawn, I1, True, axis=1)
+    rest = (~drawn).sum(axis=1)                                   # >= N_syn - N_set >= 1
+    order = np.argsort(drawn, axis=1, kind="stable")              # undrawn indices first, increasing
+    u2 = _draw_uniforms(seed, 3 * stream + 1, (n_rep, Nt))
+    pos = np.minimum((u2 * rest[:, None]).astype(np.int64), rest[:, None] - 1)
+    I2 = np.take_along_axis(order, pos, axis=1)
+    u3 = _draw_uniforms(seed, 3 * stream + 2, (N_syn,))
+    J = np.argsort(u3, kind="stable")[:Nt]
+    return I1.astype(np.int32), I2.astype(np.int32), J.astype(np.int32)
+
+
+def boot_draws_a1(seed: int, stream: int, n_rep: int, half: int):
+    """Alg. A1 draws: I1, I2 [n_rep][half] with replacement from s~1 and s~2 (step 2.1)."""
+    u1 = _draw_uniforms(seed, 3 * stream, (n_rep, half))
+    u2 = _draw_uniforms(seed, 3 * stream + 1, (n_rep, half))
+    I1 = np.minimum((u1 * half).astype(np.int64), half - 1)
+    I2 = np.minimum((u2 * half).astype(np.int64), half - 1)
+    return I1.astype(np.int32), I2.astype(np.int32)

@@ -13,6 +13,7 @@
  *   Eq. (4)  PAPER.md:144-148  f = (y-mu)^T Sigma^{-1} (y-mu)
  *   Eqs. (5)-(10) PAPER.md:178-193  the six norms (discrete equivalents)
  *   Eq. (11)-(13) PAPER.md:236-258, Alg. 3 PAPER.md:260-297  SCIL
+ *   Alg. A1 / A2 PAPER.md:648-723  bootstrap (resampled set pairs)
  *   mu/Sigma: PAPER.md:111, 131 (mean and covariance of the realisations)
  * Readings where the paper is silent are listed in DESIGN.md "Readings" (R1..R10)
  * and cited inline as [Rn].
@@ -348,6 +349,88 @@ int oracle_synth_loglik(const float *pool, int64_t ld, int n_ens, int N_set, int
     oracle_stats(Yv, nv, D, mu, Sig);
     int status = oracle_loglik(mu, Sig, Yv + (size_t)nv * D, D, ridge, out);
     if (Y) memcpy(Y, Yv, sizeof(double) * (size_t)(nv + 1) * D);
+    free(mu); free(Sig); free(Yv); free(cnt);
+    if (nonfinite) return OR_NONFINITE;
+    return status;
+}
+
+/* ---------------------------------------------------------------------------
+ * Bootstrap step 2 (Alg. A1 steps 2.1-2.3 PAPER.md:660-672, Alg. A2 steps 2.1-2.4
+ * PAPER.md:698-712), written out literally: for replicate k the sets
+ *   s^1 = { A[I1[k][i]] : i < n1 },  s^2 = { B[I2[k][j]] : j < n2 }
+ * are CONSTRUCTED (copies of the drawn patterns, repetitions included; the draws are
+ * the caller's [R14]) and the correlation-integral vector of (s^1, s^2) is computed
+ * from their distances exactly as in Eq. (1) (oracle_features).  cnt / lo / hi receive
+ * [n_rep][nq*M] (band counts as in oracle_features), y [n_rep][nq*M] (nullable).
+ * Returns 0, OR_NONFINITE, or -1 (bad argument / index out of range).
+ * ------------------------------------------------------------------------- */
+int oracle_resample_features(const float *A, int64_t lda, int64_t N, const float *B, int64_t ldb, int64_t Nt,
+                             int S, int H, int W, double h, uint32_t mask, const double *radii, int M,
+                             int n_rep, const int32_t *I1, int64_t n1, const int32_t *I2, int64_t n2,
+                             double band, int64_t *cnt, int64_t *lo, int64_t *hi, double *y, int nthreads) {
+    const int64_t K = (int64_t)S * H * W;
+    const int nq = popcount6(mask);
+    const size_t D = (size_t)nq * M;
+    if (n_rep < 1 || n1 < 1 || n2 < 1) return -1;
+    for (int64_t t = 0; t < (int64_t)n_rep * n1; ++t) if (I1[t] < 0 || I1[t] >= N) return -1;
+    for (int64_t t = 0; t < (int64_t)n_rep * n2; ++t) if (I2[t] < 0 || I2[t] >= Nt) return -1;
+    float *s1 = (float *)malloc(sizeof(float) * (size_t)(n1 * K));
+    float *s2 = (float *)malloc(sizeof(float) * (size_t)(n2 * K));
+    int nonfinite = 0;
+    for (int k = 0; k < n_rep; ++k) {
+        /* step 2.1 (and 2.2): construct the resampled sets */
+        for (int64_t i = 0; i < n1; ++i)
+            memcpy(s1 + i * K, A + (int64_t)I1[(int64_t)k * n1 + i] * lda, sizeof(float) * (size_t)K);
+        for (int64_t j = 0; j < n2; ++j)
+            memcpy(s2 + j * K, B + (int64_t)I2[(int64_t)k * n2 + j] * ldb, sizeof(float) * (size_t)K);
+        /* distances between all patterns of s^1 and s^2 -> y^k via Eq. (1) */
+        int st = oracle_features(s1, K, n1, s2, K, n2, S, H, W, h, mask, radii, M, band,
+                                 cnt + (size_t)k * D, lo ? lo + (size_t)k * D : NULL,
+                                 hi ? hi + (size_t)k * D : NULL, y ? y + (size_t)k * D : NULL, NULL, nthreads);
+        if (st == OR_NONFINITE) nonfinite = 1;
+        if (st < 0) { free(s1); free(s2); return -1; }
+    }
+    free(s1); free(s2);
+    return nonfinite ? OR_NONFINITE : OR_OK;
+}
+
+/* ---------------------------------------------------------------------------
+ * SCIL with bootstrapping at one theta, Alg. A2:
+ *   step 1: the pool s_syn (N_syn patterns) is given;
+ *   step 2: for k < n_rep: s^1 = pool[I1[k]] (N_set draws), s^2 = pool[I2[k]] (N~ = N_syn - N_set
+ *           draws), y^k = C(R, s^1, s^2)   (oracle_resample_features);
+ *   step 3: mu_theta, Sigma_theta of the n_rep vectors (oracle_stats);
+ *   step 4: s^2_theta = pool[J] (N~ patterns);
+ *   step 5: y~ = C(R, s_data, s^2_theta) (Eq. (13) with s^2_theta), f from Eq. (12) ->
+ *           out = {quad, logdet, loglik} (oracle_loglik).
+ * Y (optional) receives the n_rep + 1 vectors (y~ last).
+ * ------------------------------------------------------------------------- */
+int oracle_synth_boot(const float *pool, int64_t ld, int N_syn, const float *data, int64_t ld_data, int N_set,
+                      int n_rep, const int32_t *I1, const int32_t *I2, const int32_t *J,
+                      int S, int H, int W, double h, uint32_t mask, const double *radii, int M,
+                      double ridge, double out[3], double *Y, int nthreads) {
+    const int nq = popcount6(mask);
+    const int D = nq * M;
+    const int Nt = N_syn - N_set;
+    double *Yv = (double *)calloc((size_t)(n_rep + 1) * D, sizeof(double));
+    int64_t *cnt = (int64_t *)calloc((size_t)n_rep * D, sizeof(int64_t));
+    int st = oracle_resample_features(pool, ld, N_syn, pool, ld, N_syn, S, H, W, h, mask, radii, M, n_rep,
+                                      I1, N_set, I2, Nt, 0.0, cnt, NULL, NULL, Yv, nthreads);
+    if (st < 0) { free(Yv); free(cnt); return -1; }
+    int nonfinite = st == OR_NONFINITE;
+    /* steps 4-5: y~ from s_data and the subset pool[J] */
+    int32_t *I0 = (int32_t *)malloc(sizeof(int32_t) * (size_t)N_set);
+    for (int i = 0; i < N_set; ++i) I0[i] = i;                 /* s_data itself, no resampling */
+    st = oracle_resample_features(data, ld_data, N_set, pool, ld, N_syn, S, H, W, h, mask, radii, M, 1,
+                                  I0, N_set, J, Nt, 0.0, cnt, NULL, NULL, Yv + (size_t)n_rep * D, nthreads);
+    free(I0);
+    if (st < 0) { free(Yv); free(cnt); return -1; }
+    if (st == OR_NONFINITE) nonfinite = 1;
+    double *mu = (double *)calloc((size_t)D, sizeof(double));
+    double *Sig = (double *)calloc((size_t)D * D, sizeof(double));
+    oracle_stats(Yv, n_rep, D, mu, Sig);
+    int status = oracle_loglik(mu, Sig, Yv + (size_t)n_rep * D, D, ridge, out);
+    if (Y) memcpy(Y, Yv, sizeof(double) * (size_t)(n_rep + 1) * D);
     free(mu); free(Sig); free(Yv); free(cnt);
     if (nonfinite) return OR_NONFINITE;
     return status;

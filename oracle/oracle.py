@@ -58,6 +58,12 @@ def _load():
                                             u32, P, i32, f64, P, P, i32]
         lib.oracle_synth_loglik.restype = i32
         lib.oracle_subnorms.argtypes = [P, P, P, P]
+        lib.oracle_resample_features.argtypes = [P, i64, i64, P, i64, i64, i32, i32, i32, f64, u32, P, i32, i32,
+                                                 P, i64, P, i64, f64, P, P, P, P, i32]
+        lib.oracle_resample_features.restype = i32
+        lib.oracle_synth_boot.argtypes = [P, i64, i32, P, i64, i32, i32, P, P, P, i32, i32, i32, f64, u32, P,
+                                          i32, f64, P, P, i32]
+        lib.oracle_synth_boot.restype = i32
         _lib = lib
     return _lib
 
@@ -176,4 +182,53 @@ def synth_loglik(pool, n_ens, N_set, N_tilde, data, k0, grid, mask, radii, ridge
     st = _load().oracle_synth_loglik(_ptr(P2), K, n_ens, N_set, N_tilde, _ptr(D2), K, int(k0), S, H,
                                      W, float(h), mask, _ptr(radii), M, float(ridge), _ptr(out),
                                      _ptr(Y), nthreads or default_threads())
+    return out, st, Y
+
+
+def resample_features(A, B, grid, mask, radii, I1, I2, band: float = 1e-6, nthreads: int | None = None):
+    """Bootstrap step 2 (Alg. A1 / A2): for replicate k, s^1 = A[I1[k]], s^2 = B[I2[k]]
+    constructed explicitly, then Eq. (1).  I1 [n_rep][n1], I2 [n_rep][n2] int.
+    Returns dict counts / lo / hi [n_rep][nq][M], y [n_rep][nq*M], status."""
+    S, H, W, h = grid
+    K = S * H * W
+    A2, B2 = _rows(A, K), _rows(B, K)
+    nq = n_measures(mask)
+    radii = np.ascontiguousarray(np.asarray(radii, dtype=np.float64).reshape(nq, -1))
+    M = radii.shape[1]
+    I1 = np.ascontiguousarray(np.asarray(I1, np.int32))
+    I2 = np.ascontiguousarray(np.asarray(I2, np.int32))
+    n_rep, n1, n2 = I1.shape[0], I1.shape[1], I2.shape[1]
+    cnt = np.zeros((n_rep, nq, M), np.int64)
+    lo = np.zeros_like(cnt)
+    hi = np.zeros_like(cnt)
+    y = np.zeros((n_rep, nq * M), np.float64)
+    st = _load().oracle_resample_features(_ptr(A2), K, A2.shape[0], _ptr(B2), K, B2.shape[0], S, H, W, float(h),
+                                          mask, _ptr(radii), M, n_rep, _ptr(I1), n1, _ptr(I2), n2, float(band),
+                                          _ptr(cnt), _ptr(lo), _ptr(hi), _ptr(y), nthreads or default_threads())
+    if st < 0:
+        raise ValueError("oracle_resample_features: invalid arguments or index out of range")
+    return {"counts": cnt, "lo": lo, "hi": hi, "y": y, "status": st}
+
+
+def synth_boot(pool, data, N_set, I1, I2, J, grid, mask, radii, ridge=0.0, nthreads: int | None = None):
+    """SCIL with bootstrapping at one theta (Alg. A2): returns (out[3], status, Y[n_rep + 1][D])."""
+    S, H, W, h = grid
+    K = S * H * W
+    P2 = _rows(pool, K)
+    D2 = _rows(data, K)
+    assert D2.shape[0] == N_set
+    nq = n_measures(mask)
+    radii = np.ascontiguousarray(np.asarray(radii, np.float64).reshape(nq, -1))
+    M = radii.shape[1]
+    I1 = np.ascontiguousarray(np.asarray(I1, np.int32))
+    I2 = np.ascontiguousarray(np.asarray(I2, np.int32))
+    J = np.ascontiguousarray(np.asarray(J, np.int32))
+    n_rep = I1.shape[0]
+    out = np.zeros(3)
+    Y = np.zeros((n_rep + 1, nq * M))
+    st = _load().oracle_synth_boot(_ptr(P2), K, P2.shape[0], _ptr(D2), K, N_set, n_rep, _ptr(I1), _ptr(I2),
+                                   _ptr(J), S, H, W, float(h), mask, _ptr(radii), M, float(ridge), _ptr(out),
+                                   _ptr(Y), nthreads or default_threads())
+    if st < 0:
+        raise ValueError("oracle_synth_boot: invalid arguments or index out of range")
     return out, st, Y
