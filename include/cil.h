@@ -51,7 +51,8 @@ enum {
     CIL_ITEM_NONFINITE = 1,
     CIL_ITEM_NOTPD = 2,
     CIL_ITEM_BADRADII = 4,
-    CIL_ITEM_OVERFLOW = 8
+    CIL_ITEM_OVERFLOW = 8,
+    CIL_ITEM_BADINDEX = 16 /* a resampling / subset index outside its set (bootstrap calls) */
 };
 
 /* Distance measures, a bit mask.  A feature vector concatenates the selected
@@ -183,10 +184,75 @@ CIL_API cil_status cil_synth_loglik(int32_t P, const float* pools, int64_t pool_
                             cil_engine engine, void* ws, size_t ws_bytes, void* stream);
 
 /* ------------------------------------------------------------------------ */
+/* Bootstrap estimators (Alg. A1 / A2).  The
+ * resampled sets of the bootstrap are drawn WITH repetition from fixed sets, so every
+ * distance they need is a distance between two patterns of the fixed sets: the library
+ * computes each pair's bin index once (cil_bin_matrix) and reads the correlation-integral
+ * vector of any resampled pair of sets off it (cil_resample_counts) — the counts of
+ * Eq. (1) on the resampled sets, exactly (repeated patterns count once per draw).
+ * The random draws are the caller's (index lists), so the library is deterministic.
+ *
+ * cil_bin_matrix — for item p, measure slot q (bit order), i < N, j < Nt:
+ *   bins[p][q][i][j] = #{m : d_q(A_p,i , B_p,j) < radii[p*radii_stride + q*M + m]}  in [0, M]
+ * (radii strictly decreasing, so d < R_m  <=>  bins > m).  Arguments as cil_features;
+ * strideA / strideB may be 0 (the same set for every item).  bins [P][n_meas][N][Nt] uint8,
+ * device, row-major, written completely.  engine: AUTO / TC_I8 (L2 on the INT8 tensor-core
+ * engine when K <= 65536 — pairs within its error bound of a radius are re-evaluated in
+ * FP64 — else on the CUDA cores) or SIMT; TC_3XBF16 / TC_3XTF32 -> CIL_EUNSUPPORTED.
+ * ------------------------------------------------------------------------ */
+CIL_API size_t cil_bin_matrix_workspace_size(int32_t P, int64_t N, int64_t Nt, cil_grid g, uint32_t dist_mask,
+                                             int32_t M, cil_engine engine);
+CIL_API cil_status cil_bin_matrix(int32_t P, const float* A, int64_t strideA, int64_t lda, int64_t N,
+                                  const float* B, int64_t strideB, int64_t ldb, int64_t Nt, cil_grid g,
+                                  uint32_t dist_mask, const double* radii, int64_t radii_stride, int32_t M,
+                                  uint8_t* bins, int32_t* item_status, cil_engine engine, void* ws,
+                                  size_t ws_bytes, void* stream);
+
+/* cil_resample_counts — Alg. A1 step 2 / Alg. A2 steps 2.1-2.4: replicate k < n_rep of
+ * item p takes the row draws I1[p][k][0..n1) (indices into the N rows of bins[p]) and
+ * the column draws I2[p][k][0..n2) (indices into its Nt columns);
+ *   counts[p][k][q][m] = #{(i, j) in [0,n1) x [0,n2) : bins[p][q][I1[p][k][i]][I2[p][k][j]] > m}
+ *   y[p*y_item_stride + k*n_meas*M + q*M + m] = counts / (n1*n2)          (Eq. (1))
+ * bins [P][n_meas][N][Nt] uint8 (cil_bin_matrix); I1 [P][n_rep][n1], I2 [P][n_rep][n2] int32;
+ * counts [P][n_rep][n_meas][M] uint64 (nullable), y FP64 (nullable, not both null);
+ * y_item_stride 0 -> n_rep*n_meas*M.  An index outside its range sets CIL_ITEM_BADINDEX
+ * on the item and the draw is skipped.  No workspace.
+ * ------------------------------------------------------------------------ */
+CIL_API cil_status cil_resample_counts(int32_t P, const uint8_t* bins, int64_t N, int64_t Nt, int32_t n_meas,
+                                       int32_t M, int32_t n_rep, const int32_t* I1, int64_t n1,
+                                       const int32_t* I2, int64_t n2, uint64_t* counts, double* y,
+                                       int64_t y_item_stride, int32_t* item_status, void* stream);
+
+/* cil_synth_loglik_boot — SCIL with bootstrapping (Alg. A2) for P
+ * proposals theta_p, each with a pool of N_syn synthetic patterns at pools + p*pool_stride
+ * (row stride ld); N_t = N_syn - N_set:
+ *   bins_p = cil_bin_matrix(pool_p x pool_p) (all pool pairs, once; step 2.4's distances)
+ *   for k < n_rep: s^1 = pool rows I1[p][k][0..N_set), s^2 = pool rows I2[p][k][0..N_t)
+ *     (steps 2.1-2.2: the caller draws with replacement, s^2 from the patterns not drawn
+ *     into s^1), y^k = C(R_p, s^1, s^2) read off bins_p            (steps 2.3-2.4)
+ *   mu_theta, Sigma_theta over the n_rep vectors (two-pass, 1/(n_rep - 1))    (step 3)
+ *   y~ = C(R_p, s_data, pool rows J[p][0..N_t)), J a subset drawn by the caller (step 4)
+ *   out[p] = {quad, logdet, loglik} of y~ under N(mu_theta, Sigma_theta + ridge I) (step 5)
+ * data [N_set][K] (row stride ld_data); I1 [P][n_rep][N_set], I2 [P][n_rep][N_t],
+ * J [P][N_t] int32 device; radii [P][n_meas][M]; Y_out nullable
+ * [P][n_rep + 1][n_meas*M] FP64 (the replicate vectors, y~ last).
+ * Constraints: 1 <= N_set < N_syn, n_rep >= 2, D = n_meas*M <= 192; the workspace holds
+ * the P bin matrices (P * n_meas * N_syn^2 bytes).
+ * ------------------------------------------------------------------------ */
+CIL_API size_t cil_synth_boot_workspace_size(int32_t P, int32_t N_syn, int32_t N_set, int32_t n_rep,
+                                             cil_grid g, uint32_t dist_mask, int32_t M, cil_engine engine);
+CIL_API cil_status cil_synth_loglik_boot(int32_t P, const float* pools, int64_t pool_stride, int64_t ld,
+                                         int32_t N_syn, const float* data, int64_t ld_data, int32_t N_set,
+                                         int32_t n_rep, const int32_t* I1, const int32_t* I2, const int32_t* J,
+                                         cil_grid g, uint32_t dist_mask, const double* radii, int32_t M,
+                                         double ridge, double* out, int32_t* item_status, double* Y_out,
+                                         cil_engine engine, void* ws, size_t ws_bytes, void* stream);
+
+/* ------------------------------------------------------------------------ */
 /* cil_diag_gram — DIAGNOSTIC (not on the hot path): runs the tensor-core L2 engine on one
  * set pair without binning and writes d2E[i][j][0] = the engine's FP32 d^2(i,j) (unweighted
  * sum of squares) and d2E[i][j][1] = its error bound E(i,j) (see cil_engine).  Used by the
- * tests to measure the Gram error against FP64.  engine must be TC_3XBF16 or TC_3XTF32;
+ * tests to measure the Gram error against FP64.  engine must be TC_3XBF16, TC_3XTF32 or TC_I8;
  * d2E [N][Nt][2] FP32 device; ws_bytes >= cil_features_workspace_size(1, N, Nt, g, CIL_L2,
  * 1, engine) + 512.
  * ------------------------------------------------------------------------ */
@@ -206,8 +272,9 @@ CIL_API int32_t cil_diag_alu_ceiling(int32_t mix, int32_t iters, double* element
  * the calling host thread, every kernel the library launches is bracketed by CUDA events
  * recorded on its launching stream.  cil_prof_read waits for those events and returns, per
  * kernel class (0 prep, 1 pack, 2 tensor-core Gram, 3 CUDA-core tile engine, 4 L2 re-check,
- * 5 stats/loglik/SCIL tail), the summed milliseconds ms[6] and launch counts launches[6],
- * then clears the record.  Returns 6 (the number of classes) or -1 on a CUDA error. */
+ * 5 stats/loglik/SCIL tail, 6 bootstrap resampling), the summed milliseconds ms[7] and launch
+ * counts launches[7], then clears the record.  Returns 7 (the number of classes) or -1 on a
+ * CUDA error. */
 CIL_API void cil_prof_enable(int32_t on);
 CIL_API int32_t cil_prof_read(double* ms, int64_t* launches);
 

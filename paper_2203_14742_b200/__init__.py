@@ -9,6 +9,9 @@ C ABI, minus the prefix):
     stats(Y)                                        -> mu, Sigma                (PAPER.md:111)
     loglik(mu, Sigma, y_obs, ridge)                 -> out[P,3], item_status    (Eq. (4))
     synth_loglik(pools, n_ens, N_set, N_tilde, data, k0, grid, mask, radii)     (Alg. 3)
+    bin_matrix(A, B, grid, mask, radii)             -> bins[P,n_meas,N,Nt] uint8 (bootstrap)
+    resample_counts(bins, I1, I2, M)                -> counts, y               (Alg. A1/A2 step 2)
+    synth_loglik_boot(pools, data, N_set, I1, I2, J, grid, mask, radii)         (Alg. A2)
 
 Measures (bit order = concatenation order): L2, LINF, W12SUM, W12,
 W1INF, W1INFSUM (Eqs. (5)-(10)).
@@ -23,10 +26,11 @@ L2, LINF, W12SUM, W12, W1INF, W1INFSUM = (1 << i for i in range(6))
 ALL = 0x3F
 MEASURE_NAMES = ["L2", "LINF", "W12SUM", "W12", "W1INF", "W1INFSUM"]
 ENGINE_AUTO, ENGINE_TC_3XBF16, ENGINE_TC_3XTF32, ENGINE_SIMT, ENGINE_TC_I8 = 0, 1, 2, 3, 4
-ITEM_OK, ITEM_NONFINITE, ITEM_NOTPD, ITEM_BADRADII, ITEM_OVERFLOW = 0, 1, 2, 4, 8
+ITEM_OK, ITEM_NONFINITE, ITEM_NOTPD, ITEM_BADRADII, ITEM_OVERFLOW, ITEM_BADINDEX = 0, 1, 2, 4, 8, 16
 
 __all__ = ["features", "stats", "loglik", "synth_loglik", "features_workspace_size",
-           "synth_workspace_size", "n_measures", "Workspace", "CilError"]
+           "synth_workspace_size", "n_measures", "Workspace", "CilError", "bin_matrix", "resample_counts",
+           "synth_loglik_boot", "mcil_boot_stats"]
 
 
 def n_measures(mask: int) -> int:
@@ -214,6 +218,142 @@ def synth_loglik(pools, n_ens, N_set, N_tilde, data, k0, grid, mask, radii, ridg
                               float(ridge), out.data_ptr(), status.data_ptr(), Y.data_ptr() if return_Y else None,
                               engine, wbuf.data_ptr(), wbuf.numel(), _stream(stream))
     check(st, "cil_synth_loglik")
+    return (out, status, Y) if return_Y else (out, status)
+
+
+def _radii_arg(radii, P, nq):
+    radii = radii.to(torch.float64).contiguous()
+    if radii.dim() == 2:
+        M, rstride = radii.shape[1], 0
+    elif radii.dim() == 3 and radii.shape[0] == P:
+        M, rstride = radii.shape[2], radii.shape[1] * radii.shape[2]
+    else:
+        raise ValueError("radii must be [n_meas, M] or [P, n_meas, M]")
+    if radii.shape[-2] != nq:
+        raise ValueError(f"radii rows {radii.shape[-2]} != n_measures(mask) = {nq}")
+    return radii, M, rstride
+
+
+def bin_matrix(A, B, grid, mask, radii, *, engine=ENGINE_AUTO, stream=None, ws: Workspace | None = None,
+               bins=None, status=None):
+    """Per-pair bin indices bins[p,q,i,j] = #{m : d_q(A_p,i, B_p,j) < R_p,q,m} (uint8), the
+    first half of the bootstrap estimators (Alg. A1 / A2).
+
+    A: [N,S,H,W] or [P,N,S,H,W] float32 CUDA (a 4-D A with 5-D B is shared by every item);
+    B likewise.  radii [n_meas, M] or [P, n_meas, M].  Returns bins, item_status.
+    """
+    S, H, W = int(grid[0]), int(grid[1]), int(grid[2])
+    K = S * H * W
+    shareA = A.dim() in (2, 4) and B.dim() in (3, 5)
+    A3, B3 = _as_items(A, K), _as_items(B, K)
+    P = B3.shape[0] if shareA else A3.shape[0]
+    if not shareA and B3.shape[0] != P:
+        raise ValueError("A and B must have the same number of items")
+    N, Nt = A3.shape[1], B3.shape[1]
+    nq = n_measures(mask)
+    radii, M, rstride = _radii_arg(radii, P, nq)
+    dev = B3.device
+    if bins is None:
+        bins = torch.empty((P, nq, N, Nt), dtype=torch.uint8, device=dev)
+    if status is None:
+        status = torch.empty((P,), dtype=torch.int32, device=dev)
+    g = _grid(grid)
+    nbytes = lib.cil_bin_matrix_workspace_size(P, N, Nt, g, mask, M, engine)
+    if nbytes == 0:
+        raise CilError("cil_bin_matrix_workspace_size: invalid arguments or engine")
+    wbuf = (ws or _default_ws).get(nbytes, dev)
+    sA = 0 if shareA else A3.stride(0)
+    st = lib.cil_bin_matrix(P, _ptr(A3), sA, A3.stride(1), N, _ptr(B3), B3.stride(0), B3.stride(1), Nt, g, mask,
+                            radii.data_ptr(), rstride, M, bins.data_ptr(), status.data_ptr(), engine,
+                            wbuf.data_ptr(), wbuf.numel(), _stream(stream))
+    check(st, "cil_bin_matrix")
+    return bins, status
+
+
+def resample_counts(bins, I1, I2, M, *, want_counts=True, stream=None, status=None):
+    """Correlation-integral vectors of resampled set pairs (Alg. A1 step 2 / Alg. A2 steps
+    2.1-2.4) read off a bin matrix: bins [P, n_meas, N, Nt] uint8; I1 [P, n_rep, n1] and
+    I2 [P, n_rep, n2] int32 draws (row / column indices, repetition allowed).
+    Returns counts int64 [P, n_rep, n_meas, M] (or None), y float64 [P, n_rep, n_meas*M],
+    item_status [P] (ITEM_BADINDEX for an index out of range)."""
+    P, nq, N, Nt = bins.shape
+    I1 = I1.to(torch.int32).contiguous()
+    I2 = I2.to(torch.int32).contiguous()
+    n_rep, n1, n2 = I1.shape[1], I1.shape[2], I2.shape[2]
+    if I1.shape[0] != P or I2.shape[:2] != (P, n_rep):
+        raise ValueError("I1 [P, n_rep, n1], I2 [P, n_rep, n2]")
+    dev = bins.device
+    counts = torch.empty((P, n_rep, nq, M), dtype=torch.int64, device=dev) if want_counts else None
+    y = torch.empty((P, n_rep, nq * M), dtype=torch.float64, device=dev)
+    if status is None:
+        status = torch.zeros((P,), dtype=torch.int32, device=dev)
+    st = lib.cil_resample_counts(P, bins.contiguous().data_ptr(), N, Nt, nq, M, n_rep, I1.data_ptr(), n1,
+                                 I2.data_ptr(), n2, counts.data_ptr() if want_counts else None, y.data_ptr(), 0,
+                                 status.data_ptr(), _stream(stream))
+    check(st, "cil_resample_counts")
+    return counts, y, status
+
+
+def mcil_boot_stats(data, grid, mask, radii, I1, I2, *, engine=ENGINE_AUTO, stream=None):
+    """MCIL with bootstrapping, Alg. A1: s~1 = first N_set/2 patterns of
+    data, s~2 = the next N_set/2 (step 1); I1, I2 [n_rep, N_set/2] draws with replacement
+    into s~1 and s~2 (step 2.1); y^k from the bin matrix (2.2-2.3); mu_0, Sigma_0 (step 3).
+    Returns mu [D], Sigma [D, D], Y [n_rep, D], item_status."""
+    D2 = data.reshape(data.shape[0], -1)
+    h = D2.shape[0] // 2
+    bins, st = bin_matrix(D2[:h].reshape((h,) + tuple(data.shape[1:])), D2[h:2 * h].reshape((h,) + tuple(data.shape[1:])),
+                          grid, mask, radii, engine=engine, stream=stream)
+    M = radii.shape[-1]
+    _, Y, st = resample_counts(bins, I1.unsqueeze(0), I2.unsqueeze(0), M, want_counts=False, stream=stream,
+                               status=st)
+    mu, Sig = stats(Y[0], stream=stream)
+    return mu, Sig, Y[0], st
+
+
+def synth_loglik_boot(pools, data, N_set, I1, I2, J, grid, mask, radii, ridge: float = 0.0, *,
+                      engine=ENGINE_AUTO, return_Y=False, stream=None, ws: Workspace | None = None, out=None,
+                      status=None):
+    """SCIL with bootstrapping, Alg. A2, for P proposals.
+
+    pools [P, N_syn, S,H,W] float32; data [N_set, S,H,W]; I1 [P, n_rep, N_set],
+    I2 [P, n_rep, N_syn - N_set], J [P, N_syn - N_set] int32 draws; radii [P, n_meas, M].
+    Returns out [P,3] = (quad, logdet, loglik), item_status [P] (and Y [P, n_rep+1, D])."""
+    S, H, W = int(grid[0]), int(grid[1]), int(grid[2])
+    K = S * H * W
+    P, N_syn = pools.shape[0], pools.shape[1]
+    pools3 = pools.reshape(P, N_syn, -1)
+    data2 = data.reshape(data.shape[0], -1)
+    if pools3.shape[-1] != K or data2.shape[-1] != K or data2.shape[0] != N_set:
+        raise ValueError("pool / data shapes do not match grid and N_set")
+    nq = n_measures(mask)
+    radii = radii.to(torch.float64).contiguous()
+    M = radii.shape[-1]
+    if radii.shape != (P, nq, M):
+        raise ValueError("radii must be [P, n_meas, M]")
+    I1 = I1.to(torch.int32).contiguous()
+    I2 = I2.to(torch.int32).contiguous()
+    J = J.to(torch.int32).contiguous()
+    n_rep = I1.shape[1]
+    Nt = N_syn - N_set
+    if I1.shape != (P, n_rep, N_set) or I2.shape != (P, n_rep, Nt) or J.shape != (P, Nt):
+        raise ValueError("I1 [P, n_rep, N_set], I2 [P, n_rep, N_syn-N_set], J [P, N_syn-N_set]")
+    dev = pools.device
+    if out is None:
+        out = torch.empty((P, 3), dtype=torch.float64, device=dev)
+    if status is None:
+        status = torch.empty((P,), dtype=torch.int32, device=dev)
+    Y = torch.empty((P, n_rep + 1, nq * M), dtype=torch.float64, device=dev) if return_Y else None
+    g = _grid(grid)
+    nbytes = lib.cil_synth_boot_workspace_size(P, N_syn, N_set, n_rep, g, mask, M, engine)
+    if nbytes == 0:
+        raise CilError("cil_synth_boot_workspace_size: invalid arguments or engine")
+    wbuf = (ws or _default_ws).get(nbytes, dev)
+    st = lib.cil_synth_loglik_boot(P, pools3.data_ptr(), pools3.stride(0), pools3.stride(1), N_syn,
+                                   data2.data_ptr(), data2.stride(0), N_set, n_rep, I1.data_ptr(), I2.data_ptr(),
+                                   J.data_ptr(), g, mask, radii.data_ptr(), M, float(ridge), out.data_ptr(),
+                                   status.data_ptr(), Y.data_ptr() if return_Y else None, engine, wbuf.data_ptr(),
+                                   wbuf.numel(), _stream(stream))
+    check(st, "cil_synth_loglik_boot")
     return (out, status, Y) if return_Y else (out, status)
 
 

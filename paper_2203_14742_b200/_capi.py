@@ -51,6 +51,18 @@ def _load():
     lib.cil_prof_enable.restype = None
     lib.cil_prof_read.argtypes = [P, P]
     lib.cil_prof_read.restype = i32
+    lib.cil_bin_matrix_workspace_size.argtypes = [i32, i64, i64, Grid, u32, i32, ctypes.c_int]
+    lib.cil_bin_matrix_workspace_size.restype = sz
+    lib.cil_bin_matrix.argtypes = [i32, P, i64, i64, i64, P, i64, i64, i64, Grid, u32, P, i64, i32, P, P,
+                                   ctypes.c_int, P, sz, P]
+    lib.cil_bin_matrix.restype = ctypes.c_int
+    lib.cil_resample_counts.argtypes = [i32, P, i64, i64, i32, i32, i32, P, i64, P, i64, P, P, i64, P, P]
+    lib.cil_resample_counts.restype = ctypes.c_int
+    lib.cil_synth_boot_workspace_size.argtypes = [i32, i32, i32, i32, Grid, u32, i32, ctypes.c_int]
+    lib.cil_synth_boot_workspace_size.restype = sz
+    lib.cil_synth_loglik_boot.argtypes = [i32, P, i64, i64, i32, P, i64, i32, i32, P, P, P, Grid, u32, P, i32,
+                                          f64, P, P, P, ctypes.c_int, P, sz, P]
+    lib.cil_synth_loglik_boot.restype = ctypes.c_int
     lib.cil_status_string.argtypes = [ctypes.c_int]
     lib.cil_status_string.restype = ctypes.c_char_p
     lib.cil_last_cuda_error.restype = i32
@@ -63,7 +75,9 @@ lib = _load()
 
 EXPORTED = ["cil_features_workspace_size", "cil_features", "cil_stats", "cil_loglik",
             "cil_synth_workspace_size", "cil_synth_loglik", "cil_status_string", "cil_last_cuda_error",
-            "cil_version", "cil_last_launch_count", "cil_diag_gram", "cil_prof_enable", "cil_prof_read", "cil_normalize", "cil_diag_alu_ceiling"]
+            "cil_version", "cil_last_launch_count", "cil_diag_gram", "cil_prof_enable", "cil_prof_read", "cil_normalize", "cil_diag_alu_ceiling",
+            "cil_bin_matrix_workspace_size", "cil_bin_matrix", "cil_resample_counts",
+            "cil_synth_boot_workspace_size", "cil_synth_loglik_boot"]
 
 
 def alu_ceiling(mix: int = 0, iters: int = 20000):
@@ -74,7 +88,7 @@ def alu_ceiling(mix: int = 0, iters: int = 20000):
         raise CilError("cil_diag_alu_ceiling failed")
     return eps.value, ms.value
 
-KERNEL_CLASSES = ["prep", "pack", "gram_tc", "simt_tile", "recheck", "tail"]
+KERNEL_CLASSES = ["prep", "pack", "gram_tc", "simt_tile", "recheck", "tail", "resample"]
 
 
 def prof_enable(on: bool):
@@ -83,8 +97,8 @@ def prof_enable(on: bool):
 
 def prof_read():
     """{class: (ms, launches)} accumulated since the last read (waits for the events)."""
-    ms = (ctypes.c_double * 6)()
-    n = (ctypes.c_int64 * 6)()
+    ms = (ctypes.c_double * len(KERNEL_CLASSES))()
+    n = (ctypes.c_int64 * len(KERNEL_CLASSES))()
     if lib.cil_prof_read(ms, n) < 0:
         raise CilError("cil_prof_read: CUDA error")
     return {c: (ms[i], n[i]) for i, c in enumerate(KERNEL_CLASSES)}

@@ -107,6 +107,30 @@ Plan make_plan(uint32_t mask, cil_engine engine, const cil_grid& g, int64_t col_
     return pl;
 }
 
+// Bin-matrix mode (bootstrap): L2 on the INT8 engine when its accumulation is exact, else on
+// the CUDA cores; the float split engines have no bin-matrix epilogue.
+bool plan_bins(uint32_t mask, cil_engine engine, const cil_grid& g, Plan* out) {
+    if (engine == CIL_ENGINE_TC_3XBF16 || engine == CIL_ENGINE_TC_3XTF32) return false;
+    const int64_t K = (int64_t)g.S * g.H * g.W;
+    const cil_engine e = (engine == CIL_ENGINE_SIMT || K > 65536) ? CIL_ENGINE_SIMT : CIL_ENGINE_TC_I8;
+    *out = make_plan(mask, e, g);
+    return true;
+}
+
+// Union of two plans (one workspace serving two engine runs in sequence).
+Plan plan_union(const Plan& a, const Plan& b) {
+    Plan u = a;
+    u.tc = a.tc || b.tc;
+    // operand element size: split 2 (tf32) 4 B > split 1 (bf16) 2 B > split 3 (int8) 1 B
+    auto esz = [](const Plan& p) { return !p.tc ? 0 : p.split == 2 ? 4 : p.split == 3 ? 1 : 2; };
+    u.split = esz(a) >= esz(b) ? a.split : b.split;
+    u.simt_mask = a.simt_mask | b.simt_mask;
+    u.do_max = a.do_max || b.do_max;
+    u.do_sum = a.do_sum || b.do_sum;
+    u.nreg = a.nreg > b.nreg ? a.nreg : b.nreg;
+    return u;
+}
+
 // Workspace carve-up (identical in the size query and in the call).
 struct Layout {
     size_t off_thr, off_thr2, off_hist, off_ctr, off_list, off_center, off_hi, off_lo, off_nrm, off_q4,
@@ -186,7 +210,8 @@ cil_status check_grid(const cil_grid& g, uint32_t mask) {
 cil_status run_engines(int P, const RowSrc& asrc, const RowSrc& bsrc, int64_t rowsA, int64_t rowsB,
                        const cil_grid& g, uint32_t mask, const Slots& sl, int M, const Plan& pl,
                        const SegParams& sp, const Layout& L, void* ws, const double* radii,
-                       int64_t radii_stride, int32_t* status, cudaStream_t st, float* diag = nullptr) {
+                       int64_t radii_stride, int32_t* status, cudaStream_t st, float* diag = nullptr,
+                       uint8_t* binout = nullptr, bool keep_status = false) {
     const int64_t K = (int64_t)g.S * g.H * g.W;
     BinParams bp{};
     bp.nq = sl.nq;
@@ -198,7 +223,8 @@ cil_status run_engines(int P, const RowSrc& asrc, const RowSrc& bsrc, int64_t ro
     float* thr2 = pl.tc ? at<float>(ws, L.off_thr2) : nullptr;
     uint64_t* hist = at<uint64_t>(ws, L.off_hist);
     uint32_t* ctr = at<uint32_t>(ws, L.off_ctr);
-    CIL_CU(launch_prep(P, sl.nq, M, radii, radii_stride, bp, thr, thr2, status, hist, L.hist_elems, ctr, st));
+    CIL_CU(launch_prep(P, sl.nq, M, radii, radii_stride, bp, thr, thr2, status, hist, L.hist_elems, ctr, st,
+                       keep_status));
     if (rowsA == 0 || rowsB == 0) return CIL_OK;
 
     if (pl.simt_mask) {
@@ -221,6 +247,7 @@ cil_status run_engines(int P, const RowSrc& asrc, const RowSrc& bsrc, int64_t ro
         a.qmask = 0;
         for (int q = 0; q < sl.nq; ++q)
             if ((pl.simt_mask >> sl.slot[q]) & 1u) a.qmask |= 1u << q;
+        a.binout = binout;
         CIL_CU(launch_simt(a, st));
     }
     if (pl.tc) {
@@ -254,9 +281,11 @@ cil_status run_engines(int P, const RowSrc& asrc, const RowSrc& bsrc, int64_t ro
             t.kll = (float)(8.0 * 2.0 * (128.0 * 128.0 / 3.0) * sqrt((double)K));
             t.rel = (float)ldexp(1.0, -21);
             t.diag = diag;
+            t.binout = binout;
             CIL_CU(launch_gram_i8(t, st));
         } else {
-            // ---- 3xBF16 / 3xTF32 split engine
+            // ---- 3xBF16 / 3xTF32 split engine (histogram mode only)
+            if (binout) return CIL_EUNSUPPORTED;
             CIL_CU(launch_pack_tc(P, asrc, rowsA, K, L.Kp, center, pl.split, hi, lo, nrm, q4, status, st));
             CIL_CU(launch_pack_tc(P, bsrc, rowsB, K, L.Kp, center, pl.split, hi + offB * L.Kp * esz,
                                   lo + offB * L.Kp * esz, nrm + offB, q4 + offB, status, st));
@@ -295,6 +324,7 @@ cil_status run_engines(int P, const RowSrc& asrc, const RowSrc& bsrc, int64_t ro
         r.sp = sp; r.hist = hist;
         r.list = list; r.ctr = ctr; r.cap = L.list_cap;
         r.status = status; r.P = P;
+        r.binout = binout; r.rowsA = rowsA; r.rowsB = rowsB;
         CIL_CU(launch_recheck(r, st));
         static const char* dbg = getenv("CIL_DEBUG_RECHECK");   // diagnostic: synchronising count print
         if (dbg && dbg[0] == '1') {
@@ -434,6 +464,158 @@ cil_status cil_synth_loglik(int32_t P, const float* pools, int64_t pool_stride, 
     double* Y = Y_out ? Y_out : at<double>(wsa, L.off_Y);
     CIL_CU(launch_synth_tail(P, n_ens, sl.nq, M, sp, at<uint64_t>(wsa, L.off_hist), N_set, N_tilde, k0, ridge,
                              out, item_status, Y, at<double>(wsa, L.off_mu), at<double>(wsa, L.off_sig), st));
+    return CIL_OK;
+}
+
+// ------------------------------------------------------------------ bootstrap (Alg. A1 / A2)
+static cil_status check_sets(int32_t P, const float* A, int64_t strideA, int64_t lda, int64_t N, const float* B,
+                             int64_t strideB, int64_t ldb, int64_t Nt, const cil_grid& g) {
+    if ((N > 0 && !A) || (Nt > 0 && !B)) return CIL_EINVAL;
+    if (strideA < 0 || strideB < 0) return CIL_EINVAL;
+    const int64_t K = (int64_t)g.S * g.H * g.W;
+    if ((N > 0 && lda < K) || (Nt > 0 && ldb < K)) return CIL_EINVAL;
+    if (N > 0 && P > 1 && strideA > 0 && strideA < (N - 1) * lda + K) return CIL_EINVAL;
+    if (Nt > 0 && P > 1 && strideB > 0 && strideB < (Nt - 1) * ldb + K) return CIL_EINVAL;
+    if (K % 4 || lda % 4 || ldb % 4 || strideA % 4 || strideB % 4) return CIL_EUNSUPPORTED;
+    if ((A && !aligned16(A)) || (B && !aligned16(B))) return CIL_EUNSUPPORTED;
+    return CIL_OK;
+}
+
+size_t cil_bin_matrix_workspace_size(int32_t P, int64_t N, int64_t Nt, cil_grid g, uint32_t dist_mask, int32_t M,
+                                     cil_engine engine) {
+    if (P < 1 || N < 0 || Nt < 0 || M < 1 || check_grid(g, dist_mask) != CIL_OK) return 0;
+    Plan pl;
+    if (!plan_bins(dist_mask, engine, g, &pl)) return 0;
+    const Slots sl = slots_of(dist_mask);
+    SegParams sp{N > 0 ? N : 1, Nt > 0 ? Nt : 1, 1, 1};
+    return make_layout(P, N, Nt, g, sl.nq, M, pl, sp, 0).total;
+}
+
+cil_status cil_bin_matrix(int32_t P, const float* A, int64_t strideA, int64_t lda, int64_t N, const float* B,
+                          int64_t strideB, int64_t ldb, int64_t Nt, cil_grid g, uint32_t dist_mask,
+                          const double* radii, int64_t radii_stride, int32_t M, uint8_t* bins,
+                          int32_t* item_status, cil_engine engine, void* ws, size_t ws_bytes, void* stream) {
+    t_launches = 0;
+    if (P < 1 || N < 0 || Nt < 0 || M < 1 || M > kMaxM) return CIL_EINVAL;
+    if (check_grid(g, dist_mask) != CIL_OK) return CIL_EINVAL;
+    if ((int)engine < 0 || (int)engine > 4) return CIL_EINVAL;
+    if (!radii || !item_status || !ws || (N > 0 && Nt > 0 && !bins) || radii_stride < 0) return CIL_EINVAL;
+    cil_status s = check_sets(P, A, strideA, lda, N, B, strideB, ldb, Nt, g);
+    if (s != CIL_OK) return s;
+    Plan pl;
+    if (!plan_bins(dist_mask, engine, g, &pl)) return CIL_EUNSUPPORTED;
+    const Slots sl = slots_of(dist_mask);
+    SegParams sp{N > 0 ? N : 1, Nt > 0 ? Nt : 1, 1, 1};
+    const Layout L = make_layout(P, N, Nt, g, sl.nq, M, pl, sp, 0);
+    if (ws_bytes < L.total) return CIL_ENOMEM;
+    void* wsa = reinterpret_cast<void*>(((uintptr_t)ws + 255) & ~(uintptr_t)255);
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    RowSrc as{}, bs{};
+    as.base = A; as.stride = strideA; as.ld = lda; as.rows = N; as.mode = MODE_PLAIN;
+    bs.base = B; bs.stride = strideB; bs.ld = ldb; bs.rows = Nt; bs.mode = MODE_PLAIN;
+    return run_engines(P, as, bs, N, Nt, g, dist_mask, sl, M, pl, sp, L, wsa, radii, radii_stride, item_status,
+                       st, nullptr, bins);
+}
+
+cil_status cil_resample_counts(int32_t P, const uint8_t* bins, int64_t N, int64_t Nt, int32_t n_meas, int32_t M,
+                               int32_t n_rep, const int32_t* I1, int64_t n1, const int32_t* I2, int64_t n2,
+                               uint64_t* counts, double* y, int64_t y_item_stride, int32_t* item_status,
+                               void* stream) {
+    t_launches = 0;
+    if (P < 1 || N < 1 || Nt < 1 || n_meas < 1 || n_meas > kMaxMeas || M < 1 || M > kMaxM) return CIL_EINVAL;
+    if (n_rep < 1 || n1 < 1 || n2 < 1 || !bins || !I1 || !I2 || !item_status || (!counts && !y)) return CIL_EINVAL;
+    if (y_item_stride < 0 || (y && y_item_stride > 0 && y_item_stride < (int64_t)n_rep * n_meas * M))
+        return CIL_EINVAL;
+    if (y_item_stride == 0) y_item_stride = (int64_t)n_rep * n_meas * M;
+    CIL_CU(launch_resample(P, bins, N, Nt, n_meas, M, n_rep, I1, n1, I2, n2, counts, y, y_item_stride,
+                           item_status, reinterpret_cast<cudaStream_t>(stream)));
+    return CIL_OK;
+}
+
+namespace {
+struct BootLayout {
+    Layout L;
+    size_t off_bins, total;
+    Plan pb, ph;
+};
+bool boot_layout(int32_t P, int32_t N_syn, int32_t N_set, int32_t n_rep, const cil_grid& g, uint32_t mask,
+                 int32_t M, cil_engine engine, BootLayout* B) {
+    if (!plan_bins(mask, engine, g, &B->pb)) return false;
+    const int32_t Nt = N_syn - N_set;
+    B->ph = make_plan(mask, engine, g, Nt, Nt);
+    const Plan u = plan_union(B->pb, B->ph);
+    const Slots sl = slots_of(mask);
+    SegParams sp{N_syn, N_syn, 1, 1};
+    const int64_t nY = (int64_t)P * (n_rep + 1) * sl.nq * M;
+    B->L = make_layout(P, N_syn, N_syn, g, sl.nq, M, u, sp, nY);
+    B->off_bins = al(B->L.total);
+    B->total = B->off_bins + al((size_t)P * sl.nq * N_syn * (size_t)N_syn) + 256;
+    return true;
+}
+}  // namespace
+
+size_t cil_synth_boot_workspace_size(int32_t P, int32_t N_syn, int32_t N_set, int32_t n_rep, cil_grid g,
+                                     uint32_t dist_mask, int32_t M, cil_engine engine) {
+    if (P < 1 || N_set < 1 || N_syn <= N_set || n_rep < 2 || M < 1 || check_grid(g, dist_mask) != CIL_OK) return 0;
+    BootLayout B;
+    if (!boot_layout(P, N_syn, N_set, n_rep, g, dist_mask, M, engine, &B)) return 0;
+    return B.total;
+}
+
+cil_status cil_synth_loglik_boot(int32_t P, const float* pools, int64_t pool_stride, int64_t ld, int32_t N_syn,
+                                 const float* data, int64_t ld_data, int32_t N_set, int32_t n_rep,
+                                 const int32_t* I1, const int32_t* I2, const int32_t* J, cil_grid g,
+                                 uint32_t dist_mask, const double* radii, int32_t M, double ridge, double* out,
+                                 int32_t* item_status, double* Y_out, cil_engine engine, void* ws, size_t ws_bytes,
+                                 void* stream) {
+    t_launches = 0;
+    if (P < 1 || N_set < 1 || N_syn <= N_set || n_rep < 2 || M < 1 || M > kMaxM) return CIL_EINVAL;
+    if (check_grid(g, dist_mask) != CIL_OK) return CIL_EINVAL;
+    if ((int)engine < 0 || (int)engine > 4) return CIL_EINVAL;
+    if (!pools || !data || !I1 || !I2 || !J || !radii || !out || !item_status || !ws) return CIL_EINVAL;
+    if (!(ridge >= 0.0)) return CIL_EINVAL;
+    const int64_t K = (int64_t)g.S * g.H * g.W;
+    if (ld < K || ld_data < K) return CIL_EINVAL;
+    if (P > 1 && pool_stride < ((int64_t)N_syn - 1) * ld + K) return CIL_EINVAL;
+    if (K % 4 || ld % 4 || ld_data % 4 || pool_stride % 4) return CIL_EUNSUPPORTED;
+    if (!aligned16(pools) || !aligned16(data)) return CIL_EUNSUPPORTED;
+    const Slots sl = slots_of(dist_mask);
+    const int D = sl.nq * M;
+    if (D > kMaxD) return CIL_EUNSUPPORTED;
+    BootLayout B;
+    if (!boot_layout(P, N_syn, N_set, n_rep, g, dist_mask, M, engine, &B)) return CIL_EUNSUPPORTED;
+    if (ws_bytes < B.total) return CIL_ENOMEM;
+    void* wsa = reinterpret_cast<void*>(((uintptr_t)ws + 255) & ~(uintptr_t)255);
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const int32_t Nt = N_syn - N_set;
+    uint8_t* bins = at<uint8_t>(wsa, B.off_bins);
+    double* Y = Y_out ? Y_out : at<double>(wsa, B.L.off_Y);
+    const int64_t Ystride = (int64_t)(n_rep + 1) * D;
+    // step 2 (all pool pairs once): bin matrix of pool x pool
+    RowSrc ps{};
+    ps.base = pools; ps.stride = pool_stride; ps.ld = ld; ps.rows = N_syn; ps.mode = MODE_PLAIN;
+    SegParams spb{N_syn, N_syn, 1, 1};
+    cil_status s = run_engines(P, ps, ps, N_syn, N_syn, g, dist_mask, sl, M, B.pb, spb, B.L, wsa, radii, D,
+                               item_status, st, nullptr, bins);
+    if (s != CIL_OK) return s;
+    // steps 2.1-2.4: the n_rep resampled vectors, straight into Y rows [0, n_rep)
+    CIL_CU(launch_resample(P, bins, N_syn, N_syn, sl.nq, M, n_rep, I1, N_set, I2, Nt, nullptr, Y, Ystride,
+                           item_status, st));
+    // steps 4-5: y~ = C(R, s_data, pool rows J[p]) into Y row n_rep
+    CIL_CU(launch_check_index(P, J, Nt, N_syn, item_status, st));
+    RowSrc ds{}, js{};
+    ds.base = data; ds.stride = 0; ds.ld = ld_data; ds.rows = N_set; ds.mode = MODE_PLAIN;
+    js.base = pools; js.stride = pool_stride; js.ld = ld; js.rows = Nt; js.mode = MODE_INDEXED;
+    js.idx = J; js.idx_stride = Nt; js.idx_range = N_syn;
+    SegParams sph{N_set, Nt, 1, 1};
+    s = run_engines(P, ds, js, N_set, Nt, g, dist_mask, sl, M, B.ph, sph, B.L, wsa, radii, D, item_status, st,
+                    nullptr, nullptr, /*keep_status=*/true);
+    if (s != CIL_OK) return s;
+    CIL_CU(launch_finalize_y(P, sl.nq, M, sph, at<uint64_t>(wsa, B.L.off_hist), Y + (int64_t)n_rep * D, Ystride,
+                             (double)N_set * (double)Nt, st));
+    // step 3 and 5: mu_theta, Sigma_theta over the n_rep vectors, loglik of y~
+    CIL_CU(launch_boot_tail(P, n_rep, D, ridge, out, item_status, Y, at<double>(wsa, B.L.off_mu),
+                            at<double>(wsa, B.L.off_sig), st));
     return CIL_OK;
 }
 

@@ -20,7 +20,9 @@ constexpr int kTcBK = 128;       // K padding of the tensor-core operands (128 i
 //  MODE_SYN_ROW: r <  n_ens*N_set : pool + p*stride + (k*N + i)*ld,  k = r / N_set, i = r % N_set
 //                r >= n_ens*N_set : data + (r - n_ens*N_set)*ld_data   (s_data, Eq. (13))
 //  MODE_SYN_COL: pool + p*stride + (l*N + N_set + j)*ld,  l = r / N_tilde, j = r % N_tilde
-enum RowMode : int { MODE_PLAIN = 0, MODE_SYN_ROW = 1, MODE_SYN_COL = 2 };
+//  MODE_INDEXED: base + p*stride + idx[p*idx_stride + r]*ld  (an index outside [0, idx_range)
+//                reads row 0; k_check_index flags the item CIL_ITEM_BADINDEX)
+enum RowMode : int { MODE_PLAIN = 0, MODE_SYN_ROW = 1, MODE_SYN_COL = 2, MODE_INDEXED = 3 };
 
 struct RowSrc {
     const float* base;
@@ -32,10 +34,18 @@ struct RowSrc {
     int n_ens, N_set, N_tilde;
     const float* data;
     int64_t ld_data;
+    // indexed mode
+    const int32_t* idx;
+    int64_t idx_stride, idx_range;
 };
 
 __host__ __device__ inline const float* row_ptr(const RowSrc& s, int64_t p, int64_t r) {
     if (s.mode == MODE_PLAIN) return s.base + p * s.stride + r * s.ld;
+    if (s.mode == MODE_INDEXED) {
+        int64_t i = s.idx[p * s.idx_stride + r];
+        if (i < 0 || i >= s.idx_range) i = 0;
+        return s.base + p * s.stride + i * s.ld;
+    }
     const int64_t N = (int64_t)s.N_set + s.N_tilde;
     if (s.mode == MODE_SYN_ROW) {
         const int64_t nr = (int64_t)s.n_ens * s.N_set;
@@ -98,7 +108,8 @@ __host__ __device__ inline int64_t hist_index(const SegParams& sp, int nq, int M
 void note_launch(int n = 1);
 
 // Kernel classes for the optional event timing (cil_prof_*).
-enum KClass : int { K_PREP = 0, K_PACK = 1, K_GRAM_TC = 2, K_SIMT = 3, K_RECHECK = 4, K_TAIL = 5, K_NCLASS = 6 };
+enum KClass : int { K_PREP = 0, K_PACK = 1, K_GRAM_TC = 2, K_SIMT = 3, K_RECHECK = 4, K_TAIL = 5, K_RESAMPLE = 6,
+                    K_NCLASS = 7 };
 // RAII: when profiling is enabled on this thread, brackets the enclosed launch with
 // CUDA events recorded on the launching stream.
 struct ProfScope {
@@ -117,7 +128,8 @@ namespace cil {
 // pack.cu
 cudaError_t launch_prep(int P, int nq, int M, const double* radii, int64_t radii_stride,
                         const BinParams& bp, double* thr, float* thr2_l2, int32_t* status,
-                        uint64_t* hist, int64_t hist_elems, uint32_t* recheck_ctr, cudaStream_t st);
+                        uint64_t* hist, int64_t hist_elems, uint32_t* recheck_ctr, cudaStream_t st,
+                        bool keep_status = false);
 cudaError_t launch_pack_aug(int P, const RowSrc& src, int64_t rows, const AugGeom& g,
                             float* out, int32_t* status, cudaStream_t st);
 cudaError_t launch_center(int P, const RowSrc& colsrc, int64_t nrows_center, int64_t K, int64_t Kp,
@@ -146,6 +158,7 @@ struct SimtArgs {
     int P;
     bool do_max, do_sum;
     uint32_t qmask;                           // slots binned by this engine
+    uint8_t* binout;                          // non-null: bins[p][q][i][j] instead of counts
 };
 cudaError_t launch_simt(const SimtArgs& a, cudaStream_t st);
 
@@ -188,6 +201,7 @@ struct I8Args {
     uint4* recheck; uint32_t* recheck_ctr; uint32_t recheck_cap;
     float kq, kll, rel;
     float* diag;
+    uint8_t* binout;                     // non-null: bins[p][q_l2][i][j] instead of counts
 };
 cudaError_t launch_gram_i8(const I8Args& a, cudaStream_t st);
 bool gram_tc_supported();
@@ -205,6 +219,8 @@ struct RecheckArgs {
     const uint4* list; const uint32_t* ctr; uint32_t cap;
     int32_t* status;
     int P;
+    uint8_t* binout;     // non-null: write the exact bin to bins[p][q_l2][i][j] instead of moving counts
+    int64_t rowsA, rowsB;
 };
 cudaError_t launch_recheck(const RecheckArgs& a, cudaStream_t st);
 
@@ -213,9 +229,20 @@ cudaError_t launch_finalize(int P, int nq, int M, const SegParams& sp, const uin
                             uint64_t* counts, double* y, int64_t pairs_per_seg_rows,
                             int64_t pairs_per_seg_cols, const int32_t* status_in,
                             int32_t* status_out, cudaStream_t st);
+cudaError_t launch_finalize_y(int P, int nq, int M, const SegParams& sp, const uint64_t* hist, double* y,
+                              int64_t y_stride, double npairs, cudaStream_t st);
 cudaError_t launch_stats(int P, const double* Y, int n, int D, double* mu, double* Sigma,
                          cudaStream_t st);
 cudaError_t launch_normalize(int64_t n, const uint64_t* counts, double npairs, double* y, cudaStream_t st);
+
+// resample.cu (bootstrap estimators, Alg. A1 / A2)
+cudaError_t launch_check_index(int P, const int32_t* idx, int64_t per_item, int64_t range, int32_t* status,
+                               cudaStream_t st);
+cudaError_t launch_resample(int P, const uint8_t* bins, int64_t N, int64_t Nt, int nq, int M, int n_rep,
+                            const int32_t* I1, int64_t n1, const int32_t* I2, int64_t n2, uint64_t* counts,
+                            double* y, int64_t y_item_stride, int32_t* status, cudaStream_t st);
+cudaError_t launch_boot_tail(int P, int n_rep, int D, double ridge, double* out, int32_t* status, double* Y,
+                             double* mu, double* Sigma, cudaStream_t st);
 cudaError_t launch_loglik(int P, const double* mu, int64_t mu_stride, const double* Sigma,
                           int64_t Sigma_stride, const double* y, int D, double ridge, double* out,
                           int32_t* status, const int32_t* status_in, cudaStream_t st);

@@ -45,6 +45,7 @@ struct I8Params {
     uint4* list; uint32_t* ctr; uint32_t cap;
     float kq, kll, rel;
     float* diag;
+    uint8_t* binout;           // non-null: bins[p][q_l2][i][j] (provisional; re-check fixes ambiguous ones)
     int dbg;                   // diagnostic timing knob (CIL_DEBUG_I8): 1 skip binning, 2 skip the epilogue,
                                // 3 also skip the B loads, 4 all loads
 };
@@ -234,6 +235,9 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
                 bnd[i] = SEG ? (int)(c < 128 ? c : (1 << 30)) : (1 << 30);
             }
             uint32_t* myh = hist_s + et;
+            uint8_t* binrow = (prm.binout != nullptr && row_ok)
+                                  ? prm.binout + (((int64_t)p * prm.nq + prm.q_l2) * prm.rowsA + row) * prm.rowsB
+                                  : nullptr;
 
 #pragma unroll 1
             for (int g = 0; g < 8 && !skip; ++g) {
@@ -283,11 +287,28 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
                     amb |= (lo < s_T[b] && j < nvalid) ? (1u << jj) : 0u;
                 }
                 if (diag_mode) continue;
-                // phase B: per-thread histogram increments (fire-and-forget shared atomics)
+                // phase B: per-thread histogram increments (fire-and-forget shared atomics), or
+                // in bin-matrix mode the 16 provisional bins of the group as bytes
+                if (binrow != nullptr) {
+                    uint8_t* dst = binrow + hc0 + g * 16;
+                    if (g * 16 + 16 <= nvalid && ((reinterpret_cast<uintptr_t>(dst) & 15u) == 0)) {
+                        uint32_t wv[4];
 #pragma unroll
-                for (int jj = 0; jj < 16; ++jj)
-                    if (g * 16 + jj < nvalid)
-                        atomicAdd(myh + ((bin[jj] & 255) << 8), SEG ? 1u << ((bin[jj] >> 5) & 24) : 1u);
+                        for (int v = 0; v < 4; ++v)
+                            wv[v] = (uint32_t)(bin[4 * v] & 255) | ((uint32_t)(bin[4 * v + 1] & 255) << 8) |
+                                    ((uint32_t)(bin[4 * v + 2] & 255) << 16) | ((uint32_t)(bin[4 * v + 3] & 255) << 24);
+                        *reinterpret_cast<uint4*>(dst) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+                    } else {
+#pragma unroll
+                        for (int jj = 0; jj < 16; ++jj)
+                            if (g * 16 + jj < nvalid) dst[jj] = (uint8_t)(bin[jj] & 255);
+                    }
+                } else {
+#pragma unroll
+                    for (int jj = 0; jj < 16; ++jj)
+                        if (g * 16 + jj < nvalid)
+                            atomicAdd(myh + ((bin[jj] & 255) << 8), SEG ? 1u << ((bin[jj] >> 5) & 24) : 1u);
+                }
                 if (amb) {                                  // rare (~1e-4 of the pairs)
 #pragma unroll
                     for (int jj = 0; jj < 16; ++jj) {
@@ -303,7 +324,7 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
             __syncwarp();
             if (lane == 0) mbar_arrive_remote(&tempty[0], 0);
             tph ^= 1;
-            if (skip || prm.dbg == 1) continue;
+            if (skip || prm.dbg == 1 || prm.binout != nullptr) continue;
             // ---- flush the per-thread histograms (warp sums -> global u64 atomics), reset them.
             // Cell [b][thread] is a u32; with column segments (SEG) byte l counts local segment l.
             const int64_t rs = row_ok ? row / prm.sp.row_seg : 0;
@@ -424,6 +445,7 @@ cudaError_t launch_gram_i8(const I8Args& a, cudaStream_t st) {
     prm.list = a.recheck; prm.ctr = a.recheck_ctr; prm.cap = a.recheck_cap;
     prm.kq = a.kq; prm.kll = a.kll; prm.rel = a.rel;
     prm.diag = a.diag;
+    prm.binout = a.binout;
     {
         static const char* dbg = getenv("CIL_DEBUG_I8");
         prm.dbg = dbg ? atoi(dbg) : 0;

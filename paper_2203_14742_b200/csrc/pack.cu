@@ -18,7 +18,7 @@ namespace cil {
 //   thr2[p][m]    = R^2 / w (FP32), the L2 threshold on the unweighted sum of squares
 __global__ void k_prep(int P, int nq, int M, const double* __restrict__ radii, int64_t radii_stride,
                        BinParams bp, double* __restrict__ thr, float* __restrict__ thr2_l2,
-                       int32_t* __restrict__ status) {
+                       int32_t* __restrict__ status, int keep_status) {
     const int p = blockIdx.x;
     const double* R = radii + (int64_t)p * radii_stride;
     __shared__ int bad;
@@ -42,12 +42,13 @@ __global__ void k_prep(int P, int nq, int M, const double* __restrict__ radii, i
             }
     }
     __syncthreads();
-    if (threadIdx.x == 0) status[p] = bad ? CIL_ITEM_BADRADII : 0;
+    if (threadIdx.x == 0) status[p] = (keep_status ? status[p] : 0) | (bad ? CIL_ITEM_BADRADII : 0);
 }
 
 cudaError_t launch_prep(int P, int nq, int M, const double* radii, int64_t radii_stride,
                         const BinParams& bp, double* thr, float* thr2_l2, int32_t* status,
-                        uint64_t* hist, int64_t hist_elems, uint32_t* recheck_ctr, cudaStream_t st) {
+                        uint64_t* hist, int64_t hist_elems, uint32_t* recheck_ctr, cudaStream_t st,
+                        bool keep_status) {
     cudaError_t e = cudaMemsetAsync(hist, 0, sizeof(uint64_t) * hist_elems, st);
     if (e != cudaSuccess) return e;
     if (recheck_ctr) {
@@ -55,7 +56,7 @@ cudaError_t launch_prep(int P, int nq, int M, const double* radii, int64_t radii
         if (e != cudaSuccess) return e;
     }
     ProfScope ps_(K_PREP, st);
-    k_prep<<<P, 128, 0, st>>>(P, nq, M, radii, radii_stride, bp, thr, thr2_l2, status);
+    k_prep<<<P, 128, 0, st>>>(P, nq, M, radii, radii_stride, bp, thr, thr2_l2, status, keep_status ? 1 : 0);
     note_launch();
     return cudaGetLastError();
 }

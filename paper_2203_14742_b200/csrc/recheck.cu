@@ -3,7 +3,8 @@
 // One CTA per listed pair (256 threads, grid-stride over the list): s0 = sum_e ((double)a_e -
 // (double)b_e)^2 in FP64 from the caller's original FP32 patterns, bin b = #{m : s0 < R_m^2/w}
 // (Eq. (1), strict <; L2 = sqrt(w s0), Eq. (5)); the pair is then moved from the
-// provisional bin b_lo the epilogue gave it to b:  hist[b_lo] -= 1, hist[b] += 1.
+// provisional bin b_lo the epilogue gave it to b:  hist[b_lo] -= 1, hist[b] += 1 — or, in
+// bin-matrix mode, b is written to the pair's entry.
 #include "cil_internal.cuh"
 
 namespace cil {
@@ -55,7 +56,9 @@ __global__ void __launch_bounds__(256) k_recheck(RecheckArgs a) {
             const double* R = a.thr + p * a.thr_stride + (int64_t)a.q_l2 * a.M;
             int b = 0;
             while (b < a.M && s < R[b] * R[b] / a.w) ++b;
-            if (b != b_lo) {
+            if (a.binout) {
+                a.binout[(((int64_t)p * a.nq + a.q_l2) * a.rowsA + i) * a.rowsB + j] = (uint8_t)b;
+            } else if (b != b_lo) {
                 const int64_t rs = i / a.sp.row_seg, cs = j / a.sp.col_seg;
                 unsigned long long* H = (unsigned long long*)a.hist;
                 if (b_lo > 0) atomicAdd(&H[hist_index(a.sp, a.nq, a.M, p, rs, cs, a.q_l2, b_lo)], ~0ull);

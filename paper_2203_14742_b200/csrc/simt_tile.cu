@@ -210,6 +210,10 @@ __global__ void __launch_bounds__(NTHR, 2) k_simt(SimtArgs a) {
                 const double* T = thr_s + q * M;
                 int b = 0;
                 while (b < M && d < T[b]) ++b;
+                if (a.binout) {              // bin-matrix mode (bootstrap, Alg. A1 / A2)
+                    a.binout[(((int64_t)p * nq + q) * a.rowsA + gi) * a.rowsB + gj] = (uint8_t)b;
+                    continue;
+                }
                 if (b == 0) continue;
                 if (use_sh) {
                     const int loc = (int)((rs - rs0) * ncs + (cs - cs0));

@@ -11,14 +11,14 @@ namespace cil {
 // ------------------------------------------------------------------ finalize
 // counts[p][q][m] = sum_{b > m} hist[p][0][0][q][b];  y = counts / (N * Nt).
 __global__ void k_finalize(int nq, int M, SegParams sp, const uint64_t* __restrict__ hist,
-                           uint64_t* __restrict__ counts, double* __restrict__ y, double npairs) {
+                           uint64_t* __restrict__ counts, double* __restrict__ y, int64_t y_stride, double npairs) {
     const int p = blockIdx.x;
     for (int t = threadIdx.x; t < nq * M; t += blockDim.x) {
         const int q = t / M, m = t % M;
         uint64_t c = 0;
         for (int b = m + 1; b <= M; ++b) c += hist[hist_index(sp, nq, M, p, 0, 0, q, b)];
-        counts[(int64_t)p * nq * M + t] = c;
-        if (y) y[(int64_t)p * nq * M + t] = npairs > 0 ? (double)c / npairs : 0.0;
+        if (counts) counts[(int64_t)p * nq * M + t] = c;
+        if (y) y[(int64_t)p * y_stride + t] = npairs > 0 ? (double)c / npairs : 0.0;
     }
 }
 
@@ -26,7 +26,16 @@ cudaError_t launch_finalize(int P, int nq, int M, const SegParams& sp, const uin
                             uint64_t* counts, double* y, int64_t rows, int64_t cols,
                             const int32_t*, int32_t*, cudaStream_t st) {
     ProfScope ps_(K_TAIL, st);
-    k_finalize<<<P, 128, 0, st>>>(nq, M, sp, hist, counts, y, (double)rows * (double)cols);
+    k_finalize<<<P, 128, 0, st>>>(nq, M, sp, hist, counts, y, (int64_t)nq * M, (double)rows * (double)cols);
+    note_launch();
+    return cudaGetLastError();
+}
+
+// y only, item stride y_stride (e.g. the y~ row of a bootstrap Y block)
+cudaError_t launch_finalize_y(int P, int nq, int M, const SegParams& sp, const uint64_t* hist, double* y,
+                              int64_t y_stride, double npairs, cudaStream_t st) {
+    ProfScope ps_(K_TAIL, st);
+    k_finalize<<<P, 128, 0, st>>>(nq, M, sp, hist, nullptr, y, y_stride, npairs);
     note_launch();
     return cudaGetLastError();
 }
@@ -70,10 +79,10 @@ __global__ void k_cov(const double* __restrict__ Y, int64_t y_stride, int n, int
     }
 }
 
-// Fused mu + Sigma for one item per CTA when Y[p] fits in shared memory (n*D*8 <= 40 KB):
+// Fused mu + Sigma for one item per CTA when Y[p] fits in shared memory (n*D*8 <= 200 KB):
 // the same two-pass sums as k_mean / k_cov, with the n-long sums split over the lanes of a
 // warp (one warp per column a, then one warp per pair b <= a) and reduced by shuffles.
-constexpr int kStatsSmem = 40 * 1024;
+constexpr int kStatsSmem = 200 * 1024;
 __global__ void __launch_bounds__(256) k_stats_smem(const double* __restrict__ Y, int64_t y_stride, int n, int D,
                                                     double* __restrict__ mu, double* __restrict__ Sigma) {
     extern __shared__ double ys[];                   // [n][D], centred in place after pass 1
@@ -289,6 +298,15 @@ cudaError_t launch_synth_tail(int P, int n_ens, int nq, int M, const SegParams& 
     cudaError_t e = launch_stats_strided(P, Y, (int64_t)(nv + 1) * D, nv, D, mu, Sigma, st);
     if (e != cudaSuccess) return e;
     return launch_loglik_strided(P, mu, D, Sigma, (int64_t)D * D, Y + (int64_t)nv * D, (int64_t)(nv + 1) * D,
+                                 D, ridge, out, status, status, st);
+}
+
+// Bootstrap tail (Alg. A2 steps 3-5): Y[p] = [n_rep replicate vectors ; y~], D each.
+cudaError_t launch_boot_tail(int P, int n_rep, int D, double ridge, double* out, int32_t* status, double* Y,
+                             double* mu, double* Sigma, cudaStream_t st) {
+    cudaError_t e = launch_stats_strided(P, Y, (int64_t)(n_rep + 1) * D, n_rep, D, mu, Sigma, st);
+    if (e != cudaSuccess) return e;
+    return launch_loglik_strided(P, mu, D, Sigma, (int64_t)D * D, Y + (int64_t)n_rep * D, (int64_t)(n_rep + 1) * D,
                                  D, ridge, out, status, status, st);
 }
 
