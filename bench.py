@@ -41,6 +41,9 @@ C2 = dict(name="C2", grid=(2, 64, 64), P=100, N=500, Nt=500, M=15, mask=1,
           workload="C2: GM-shaped 64x64x2 patterns, 100 set pairs x (500 x 500), L2, M=15 (BASELINE configs[1])")
 C4 = dict(name="C4", grid=(1, 128, 128), P=256, n_ens=10, N_set=50, N_tilde=50, M=13, mask=1,
           workload="C4: SCIL Alg. 3, 256 proposals x pool 1000 of 128x128, n_ens=10, 50+50, L2, M=13")
+C6 = dict(name="C6", grid=(2, 64, 64), P=64, N_syn=1000, N_set=50, n_rep=1000, M=13, mask=1,
+          workload="C6: SCIL with bootstrapping (Alg. A2), 64 proposals x pool 1000 of 64x64x2, N_set=50, "
+                   "n_CIL=1000 replicates, L2, M=13 (PAPER.md:563-564)")
 
 
 def log(*a):
@@ -206,6 +209,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-c4", action="store_true")
+    ap.add_argument("--no-c6", action="store_true")
     ap.add_argument("--config", default="C2", choices=["C2", "C3"],
                     help="C2 = the headline bench line; C3 = evidence run of the CUDA-core measures")
     args = ap.parse_args()
@@ -383,6 +387,9 @@ def main():
     c4 = None
     if not args.no_c4:
         c4 = bench_c4(cil, args, world, rank, dev, engine, stream)
+    c6 = None
+    if not args.no_c6:
+        c6 = bench_c6(cil, args, world, rank, dev, engine, stream)
 
     # ---- CPU baseline: the oracle as it stands, bounded sample, rank 0 at N = 1 only
     cpu = None
@@ -412,6 +419,7 @@ def main():
             "e2e": e2e,
             "cpu_baseline": cpu,
             "secondary": c4,
+            "secondary_bootstrap": c6,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -487,6 +495,74 @@ def bench_c3(args, dev):
                          "K_aug": Kaug},
            "kernel_breakdown": {k: round(v[0] / steps, 3) for k, v in prof.items() if v[1] > 0}}
     print(json.dumps(res), flush=True)
+
+
+def bench_c6(cil, args, world, rank, dev, engine, stream):
+    """Secondary line for the bootstrap row: Alg. A2 loglik evals/s at the
+    paper's sizes (N_syn = 1000, n_CIL = 1000 replicates), L2, per-theta
+    radii; draws seeded on the host (untimed inputs, like the patterns)."""
+    cfg = C6
+    grid, P, N_syn, N_set, n_rep, M = cfg["grid"], cfg["P"], cfg["N_syn"], cfg["N_set"], cfg["n_rep"], cfg["M"]
+    seed = cilgen.config_seed(6)
+    t0 = time.time()
+    pools = torch.empty((P, N_syn) + grid, dtype=torch.float32, device=dev)
+    for p in range(P):
+        u = cilgen.uniforms(seed, 5000 + rank * P + p, np.array([0]), 2)[0]
+        cilgen.make_set(seed, rank * P + p, N_syn, grid, device=dev, out=pools[p], n_w=4.5 + u[0],
+                        amp_scale=0.8 + 0.4 * u[1])
+    data = cilgen.make_set(seed, 100000, N_set, grid, device=dev)
+    draws = [cilgen.boot_draws_a2(seed, rank * P + p, n_rep, N_syn, N_set) for p in range(P)]
+    I1 = torch.tensor(np.stack([d[0] for d in draws]), device=dev)
+    I2 = torch.tensor(np.stack([d[1] for d in draws]), device=dev)
+    J = torch.tensor(np.stack([d[2] for d in draws]), device=dev)
+    radii = torch.tensor(np.stack([pilot_radii(pools[p, :64], pools[p, 64:128], grid, M)[None, :] for p in range(P)]),
+                         dtype=torch.float64, device=dev)
+    torch.cuda.synchronize()
+    log(f"[bench] rank {rank}: generated C6 pools + draws in {time.time() - t0:.1f}s")
+    ws = cil.Workspace()
+    out = torch.empty((P, 3), dtype=torch.float64, device=dev)
+    st = torch.empty((P,), dtype=torch.int32, device=dev)
+
+    def step():
+        cil.synth_loglik_boot(pools, data, N_set, I1, I2, J, grid, cfg["mask"], radii, ridge=1e-10, engine=engine,
+                              ws=ws, out=out, status=st)
+
+    for _ in range(args.warmup):
+        step()
+    steps = max(3, args.steps // 40)
+    from paper_2203_14742_b200 import _capi
+    _capi.prof_enable(True)
+    ms = timed(step, steps, stream)
+    _capi.prof_enable(False)
+    prof = _capi.prof_read()
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_step = float(t.item()) / steps
+    K = grid[0] * grid[1] * grid[2]
+    Nt = N_syn - N_set
+    res = {"workload": cfg["workload"], "metric": "SCIL-bootstrap loglik evals/s", "value": world * P / (ms_step * 1e-3),
+           "ms_per_step": round(ms_step, 3), "steps": steps,
+           "pool_pairs_per_s": world * P * N_syn * N_syn / (ms_step * 1e-3),
+           "resampled_pairs_per_s": world * P * n_rep * N_set * Nt / (ms_step * 1e-3),
+           "nonzero_status": int((st != 0).sum())}
+    g_ms, g_n = prof["gram_tc"]
+    if g_n:
+        per_step = g_ms / steps
+        # both Gram launches of a step: the pool x pool bin matrix and the y~ counts (s_data x pool[J])
+        ach = 3 * 2.0 * P * (N_syn * N_syn + N_set * Nt) * K / (per_step * 1e-3) / 1e12
+        used = engine_used(args.engine, K)
+        ratio = {"TC_I8": 2.0, "TC_3XBF16": 1.0, "TC_3XTF32": 0.5}.get(used, 1.0)
+        res["gram_tc"] = {"engine": used, "ms_per_step": round(per_step, 4), "launches_per_step": g_n / steps,
+                          "achieved_tops": round(ach, 1),
+                          "frac_of_peak": round(ach / (ratio * peaks().get("bf16_tflops", 1590.0)), 4)}
+    r_ms, r_n = prof["resample"]
+    if r_n:
+        res["resample"] = {"ms_per_step": round(r_ms / steps, 4),
+                           "lookups_per_s": P * n_rep * N_set * Nt / (r_ms / steps * 1e-3)}
+    res["kernel_breakdown"] = {k: round(v[0] / steps, 4) for k, v in prof.items() if v[1] > 0}
+    return res
 
 
 def bench_c4(cil, args, world, rank, dev, engine, stream):

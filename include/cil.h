@@ -216,7 +216,8 @@ CIL_API cil_status cil_bin_matrix(int32_t P, const float* A, int64_t strideA, in
  * bins [P][n_meas][N][Nt] uint8 (cil_bin_matrix); I1 [P][n_rep][n1], I2 [P][n_rep][n2] int32;
  * counts [P][n_rep][n_meas][M] uint64 (nullable), y FP64 (nullable, not both null);
  * y_item_stride 0 -> n_rep*n_meas*M.  An index outside its range sets CIL_ITEM_BADINDEX
- * on the item and the draw is skipped.  No workspace.
+ * on the item and the draw is skipped.  No workspace.  Shared-memory limit:
+ * 4*((M+1)*256 + N + Nt) <= 200 KB (N + Nt <= ~47 000 at M = 13), else CIL_EUNSUPPORTED.
  * ------------------------------------------------------------------------ */
 CIL_API cil_status cil_resample_counts(int32_t P, const uint8_t* bins, int64_t N, int64_t Nt, int32_t n_meas,
                                        int32_t M, int32_t n_rep, const int32_t* I1, int64_t n1,

@@ -187,6 +187,12 @@ T* at(void* base, size_t off) { return reinterpret_cast<T*>(reinterpret_cast<cha
 
 bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
 
+// shared-memory budget of k_resample: per-thread histograms + the two multiplicity tables
+bool resample_fits(int64_t N, int64_t Nt, int M) {
+    // histograms + m1 + m2 + the distinct-row list (<= N)
+    return 4 * ((int64_t)(M + 1) * 256 + ((N + 3) & ~(int64_t)3) + ((Nt + 15) & ~(int64_t)15) + N) <= 200 * 1024;
+}
+
 cil_status fail_cuda(cudaError_t e) {
     t_last_cuda = (int32_t)e;
     return CIL_ECUDA;
@@ -527,6 +533,7 @@ cil_status cil_resample_counts(int32_t P, const uint8_t* bins, int64_t N, int64_
     if (y_item_stride < 0 || (y && y_item_stride > 0 && y_item_stride < (int64_t)n_rep * n_meas * M))
         return CIL_EINVAL;
     if (y_item_stride == 0) y_item_stride = (int64_t)n_rep * n_meas * M;
+    if (!resample_fits(N, Nt, M)) return CIL_EUNSUPPORTED;
     CIL_CU(launch_resample(P, bins, N, Nt, n_meas, M, n_rep, I1, n1, I2, n2, counts, y, y_item_stride,
                            item_status, reinterpret_cast<cudaStream_t>(stream)));
     return CIL_OK;
@@ -584,6 +591,7 @@ cil_status cil_synth_loglik_boot(int32_t P, const float* pools, int64_t pool_str
     if (D > kMaxD) return CIL_EUNSUPPORTED;
     BootLayout B;
     if (!boot_layout(P, N_syn, N_set, n_rep, g, dist_mask, M, engine, &B)) return CIL_EUNSUPPORTED;
+    if (!resample_fits(N_syn, N_syn, M)) return CIL_EUNSUPPORTED;
     if (ws_bytes < B.total) return CIL_ENOMEM;
     void* wsa = reinterpret_cast<void*>(((uintptr_t)ws + 255) & ~(uintptr_t)255);
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);

@@ -34,36 +34,95 @@ cudaError_t launch_check_index(int P, const int32_t* idx, int64_t per_item, int6
 
 constexpr int kRsThreads = 256;
 
+// Multiplicity form of the same count: with m1[a] = #{i : I1[i] = a}, m2[b] = #{j : I2[j] = b},
+//   counts[q][m] = sum_a m1[a] sum_b m2[b] [bins[q][a][b] > m]
+// (a regrouping of the (i, j) double sum; repeated draws count once per draw).  The rows a
+// with m1[a] > 0 are streamed with 16-byte loads (coalesced, no byte gathers); m1, m2 live
+// in shared memory; the per-thread histograms take weighted fire-and-forget atomics.
 __global__ void __launch_bounds__(kRsThreads) k_resample(const uint8_t* __restrict__ bins, int64_t N, int64_t Nt,
                                                           int nq, int M, int n_rep, const int32_t* __restrict__ I1,
                                                           int64_t n1, const int32_t* __restrict__ I2, int64_t n2,
                                                           uint64_t* __restrict__ counts, double* __restrict__ y,
                                                           int64_t y_item_stride) {
-    extern __shared__ uint32_t hs[];              // [M+1][kRsThreads]
+    extern __shared__ uint32_t rs_smem[];
+    uint32_t* hs = rs_smem;                                   // [M+1][kRsThreads]
+    uint32_t* m1 = hs + (M + 1) * kRsThreads;                 // [round_up(N, 4)]
+    uint32_t* m2 = m1 + ((N + 3) & ~(int64_t)3);              // [round_up(Nt, 16)], 16-byte aligned
     __shared__ uint32_t red[8][kMaxM + 1];
     const int k = blockIdx.x, p = blockIdx.y;
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const int32_t* i1 = I1 + ((int64_t)p * n_rep + k) * n1;
     const int32_t* i2 = I2 + ((int64_t)p * n_rep + k) * n2;
+    const int64_t Nt16 = (Nt + 15) & ~(int64_t)15;
+    for (int64_t a = tid; a < N; a += kRsThreads) m1[a] = 0u;
+    for (int64_t b = tid; b < Nt16; b += kRsThreads) m2[b] = 0u;
+    __syncthreads();
+    for (int64_t i = tid; i < n1; i += kRsThreads) {
+        const int32_t r = __ldg(&i1[i]);
+        if (r >= 0 && r < N) atomicAdd(&m1[r], 1u);          // invalid draws: flagged, skipped
+    }
+    for (int64_t j = tid; j < n2; j += kRsThreads) {
+        const int32_t c = __ldg(&i2[j]);
+        if (c >= 0 && c < Nt) atomicAdd(&m2[c], 1u);
+    }
+    __syncthreads();
+    // compact list of the distinct drawn rows (order irrelevant: integer sums)
+    __shared__ int nrows;
+    int32_t* rows = reinterpret_cast<int32_t*>(m2 + Nt16);   // [min(N, n1)]
+    if (tid == 0) nrows = 0;
+    __syncthreads();
+    for (int64_t a = tid; a < N; a += kRsThreads)
+        if (m1[a] != 0u) rows[atomicAdd(&nrows, 1)] = (int32_t)a;
+    __syncthreads();
+    const int nr = nrows;
     const double npairs = (double)n1 * (double)n2;
+    // row loads: 16 B when rows are 16-byte aligned, 8 B when 8-byte aligned, else bytes
+    const int align = (reinterpret_cast<uintptr_t>(bins) & 15u) ? 1 : (Nt % 16 == 0) ? 16 : (Nt % 8 == 0) ? 8 : 1;
     for (int q = 0; q < nq; ++q) {
         for (int b = 0; b <= M; ++b) hs[b * kRsThreads + tid] = 0u;
         __syncthreads();
         const uint8_t* Bq = bins + ((int64_t)p * nq + q) * N * Nt;
-        // warp w takes draws i = w, w+8, ...; lanes stride over the column draws
-        for (int64_t i = w; i < n1; i += kRsThreads / 32) {
-            const int64_t r = __ldg(&i1[i]);
-            if (r < 0 || r >= N) continue;          // flagged CIL_ITEM_BADINDEX by k_check_index
-            const uint8_t* row = Bq + r * Nt;
-            for (int64_t j = lane; j < n2; j += 32) {
-                const int64_t c = __ldg(&i2[j]);
-                if (c < 0 || c >= Nt) continue;
-                const uint32_t b = __ldg(&row[c]);
-                atomicAdd(&hs[(b <= (uint32_t)M ? b : (uint32_t)M) * kRsThreads + tid], 1u);
+        uint32_t* myh = hs + tid;
+        for (int ri = w; ri < nr; ri += kRsThreads / 32) {
+            const int64_t a = rows[ri];
+            const uint32_t wa = m1[a];
+            const uint8_t* row = Bq + a * Nt;
+            for (int64_t c0 = (int64_t)lane * 16; c0 < Nt; c0 += 32 * 16) {
+                uint32_t bw[4];
+                if (align == 16) {
+                    const uint4 v = __ldg(reinterpret_cast<const uint4*>(row + c0));
+                    bw[0] = v.x; bw[1] = v.y; bw[2] = v.z; bw[3] = v.w;
+                } else if (align == 8) {
+                    const uint2 v0 = __ldg(reinterpret_cast<const uint2*>(row + c0));
+                    const uint2 v1 = c0 + 8 < Nt ? __ldg(reinterpret_cast<const uint2*>(row + c0 + 8)) : make_uint2(0u, 0u);
+                    bw[0] = v0.x; bw[1] = v0.y; bw[2] = v1.x; bw[3] = v1.y;
+                } else {
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) {
+                        uint32_t x = 0;
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const int64_t c = c0 + 4 * t + u;
+                            if (c < Nt) x |= (uint32_t)__ldg(&row[c]) << (8 * u);
+                        }
+                        bw[t] = x;
+                    }
+                }
+                const uint4* mv = reinterpret_cast<const uint4*>(m2 + c0);
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const uint4 mm = mv[t];
+                    const uint32_t ms[4] = {mm.x, mm.y, mm.z, mm.w};
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        // branch-free: an undrawn column (and the padding past Nt) adds 0
+                        const uint32_t b = min((bw[t] >> (8 * u)) & 255u, (uint32_t)M);
+                        atomicAdd(myh + b * kRsThreads, ms[u] * wa);
+                    }
+                }
             }
         }
         __syncthreads();
-        // per bin: block sum of the per-thread counters
         for (int b = 0; b <= M; ++b) {
             uint32_t v = hs[b * kRsThreads + tid];
             v = __reduce_add_sync(0xffffffffu, v);
@@ -89,11 +148,12 @@ cudaError_t launch_resample(int P, const uint8_t* bins, int64_t N, int64_t Nt, i
     if (e != cudaSuccess) return e;
     e = launch_check_index(P, I2, (int64_t)n_rep * n2, Nt, status, st);
     if (e != cudaSuccess) return e;
-    const size_t smem = sizeof(uint32_t) * (size_t)(M + 1) * kRsThreads;
+    const size_t smem = sizeof(uint32_t) * ((size_t)(M + 1) * kRsThreads + (size_t)((N + 3) & ~3ll) + (size_t)((Nt + 15) & ~15ll) +
+                                            (size_t)(n1 < N ? n1 : N));
+    if (smem > 200 * 1024) return cudaErrorInvalidValue;     // N + Nt <= ~47 k (host-checked)
     static bool attr = false;
     if (!attr) {
-        e = cudaFuncSetAttribute(k_resample, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)(sizeof(uint32_t) * (kMaxM + 1) * kRsThreads));
+        e = cudaFuncSetAttribute(k_resample, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         if (e != cudaSuccess) return e;
         attr = true;
     }
