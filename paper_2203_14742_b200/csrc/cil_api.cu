@@ -187,6 +187,12 @@ T* at(void* base, size_t off) { return reinterpret_cast<T*>(reinterpret_cast<cha
 
 bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
 
+// the two panels address the same pattern rows (plain mode, same base / strides)
+bool same_rows(const RowSrc& a, const RowSrc& b) {
+    return a.mode == MODE_PLAIN && b.mode == MODE_PLAIN && a.base == b.base && a.stride == b.stride &&
+           a.ld == b.ld && a.rows == b.rows;
+}
+
 // shared-memory budget of k_resample: per-thread histograms + the two multiplicity tables
 bool resample_fits(int64_t N, int64_t Nt, int M) {
     // histograms + m1 + m2 + the distinct-row list (<= N)
@@ -269,8 +275,15 @@ cil_status run_engines(int P, const RowSrc& asrc, const RowSrc& bsrc, int64_t ro
         CIL_CU(launch_center(P, bsrc, rowsB < 16 ? rowsB : 16, K, L.Kp, center, st));
         if (pl.split == 3) {
             // ---- INT8 two-digit engine (default): exact int32 accumulation
-            CIL_CU(launch_pack_i8_pair(P, asrc, rowsA, bsrc, rowsB, K, L.Kp, center, reinterpret_cast<int8_t*>(hi),
-                                       reinterpret_cast<int8_t*>(lo), nrm, q4, status, st));
+            // B = A (pool x pool bin matrices of the bootstrap): the rows are packed once
+            const bool b_same = same_rows(asrc, bsrc) && rowsA == rowsB;
+            if (b_same)
+                CIL_CU(launch_pack_i8(P, asrc, rowsA, K, L.Kp, center, reinterpret_cast<int8_t*>(hi),
+                                      reinterpret_cast<int8_t*>(lo), nrm, q4, status, st));
+            else
+                CIL_CU(launch_pack_i8_pair(P, asrc, rowsA, bsrc, rowsB, K, L.Kp, center,
+                                           reinterpret_cast<int8_t*>(hi), reinterpret_cast<int8_t*>(lo), nrm, q4,
+                                           status, st));
             I8Args t{};
             t.hq = reinterpret_cast<const int8_t*>(hi); t.lq = reinterpret_cast<const int8_t*>(lo);
             t.nrm = nrm; t.scl = q4;
@@ -288,6 +301,7 @@ cil_status run_engines(int P, const RowSrc& asrc, const RowSrc& bsrc, int64_t ro
             t.rel = (float)ldexp(1.0, -21);
             t.diag = diag;
             t.binout = binout;
+            t.b_same = b_same;
             CIL_CU(launch_gram_i8(t, st));
         } else {
             // ---- 3xBF16 / 3xTF32 split engine (histogram mode only)

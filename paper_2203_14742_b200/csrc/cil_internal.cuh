@@ -202,6 +202,7 @@ struct I8Args {
     float kq, kll, rel;
     float* diag;
     uint8_t* binout;                     // non-null: bins[p][q_l2][i][j] instead of counts
+    bool b_same;                         // B panel = A panel (rows packed once, B reads the A planes)
 };
 cudaError_t launch_gram_i8(const I8Args& a, cudaStream_t st);
 bool gram_tc_supported();

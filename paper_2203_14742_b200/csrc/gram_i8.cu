@@ -32,6 +32,7 @@ namespace tc {
 
 struct I8Params {
     int64_t rowsA, rowsB;
+    int64_t b_off;             // first B row in the stacked planes: P*rowsA, or 0 when B = A (packed once)
     int P, p0, np;
     int n_kb;
     int tiles_m, tiles_n;
@@ -130,7 +131,7 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
                 const int p = prm.p0 + t / tiles_per_item, r = t % tiles_per_item;
                 const int mt = r / prm.tiles_n, nt = r % prm.tiles_n;
                 const int ya = (int)(p * prm.rowsA + (int64_t)mt * G::TILE_M + rank * A_ROWS);
-                const int yb = (int)((int64_t)prm.P * prm.rowsA + p * prm.rowsB + (int64_t)nt * TILE_N + rank * G::B_ROWS);
+                const int yb = (int)(prm.b_off + p * prm.rowsB + (int64_t)nt * TILE_N + rank * G::B_ROWS);
                 for (int kb = 0; kb < prm.n_kb; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     unsigned char* st = stages + stage * IG::STAGE_BYTES;
@@ -192,7 +193,7 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
             const int p = prm.p0 + t / tiles_per_item, r = t % tiles_per_item;
             const int mt = r / prm.tiles_n, nt = r % prm.tiles_n;
             const int64_t col0 = (int64_t)nt * TILE_N;
-            const int64_t browbase = (int64_t)prm.P * prm.rowsA + (int64_t)p * prm.rowsB;
+            const int64_t browbase = prm.b_off + (int64_t)p * prm.rowsB;
             named_bar(1, 256);
             {
                 const int64_t c = col0 + et;
@@ -424,8 +425,8 @@ static cudaError_t launch_i8_t(const tc::I8Params& prm, const CUtensorMap* maps,
 
 cudaError_t launch_gram_i8(const I8Args& a, cudaStream_t st) {
     if (a.rowsA == 0 || a.rowsB == 0) return cudaSuccess;
-    const int64_t rows = (int64_t)a.P * (a.rowsA + a.rowsB);
-    if (rows >= (1ll << 31)) return cudaErrorInvalidValue;
+    const int64_t rows = (int64_t)a.P * (a.b_same ? a.rowsA : a.rowsA + a.rowsB);
+    if (rows >= (1ll << 31) || (a.b_same && a.rowsA != a.rowsB)) return cudaErrorInvalidValue;
     CUtensorMap maps[4];
     if (!make_map_i8(&maps[0], a.hq, rows, a.Kp, tc::A_ROWS) || !make_map_i8(&maps[1], a.lq, rows, a.Kp, tc::A_ROWS) ||
         !make_map_i8(&maps[2], a.hq, rows, a.Kp, tc::Geo<2>::B_ROWS) ||
@@ -433,6 +434,7 @@ cudaError_t launch_gram_i8(const I8Args& a, cudaStream_t st) {
         return cudaErrorInvalidValue;
     tc::I8Params prm{};
     prm.rowsA = a.rowsA; prm.rowsB = a.rowsB;
+    prm.b_off = a.b_same ? 0 : (int64_t)a.P * a.rowsA;
     prm.P = a.P; prm.p0 = a.p0; prm.np = a.np > 0 ? a.np : a.P - a.p0;
     prm.n_kb = (int)(a.Kp / 128);
     prm.tiles_m = (int)((a.rowsA + tc::Geo<2>::TILE_M - 1) / tc::Geo<2>::TILE_M);
