@@ -8,6 +8,8 @@
 //    W (D_x) and H (D_y) inside each species; the last node is omitted (Neumann
 //    ghost; reading R3).  The 1/h factor is applied in
 //    the engines' epilogues in FP64, so the fields here are plain differences.
+#include <stdlib.h>
+
 #include "cil_internal.cuh"
 
 namespace cil {
@@ -295,12 +297,22 @@ template <int NV, int NT>
 __global__ void __launch_bounds__(NT) k_pack_i8r(RowSrc src, int64_t rows, int64_t K, int64_t Kp,
                                                   const float* __restrict__ center, int8_t* __restrict__ hq,
                                                   int8_t* __restrict__ lq, float* __restrict__ nrm,
-                                                  float* __restrict__ scl, int32_t* __restrict__ status) {
+                                                  float* __restrict__ scl, int32_t* __restrict__ status,
+                                                  int64_t pf_dist) {
     const int64_t p = blockIdx.y;
     const int64_t r = blockIdx.x;
     const float* x = row_ptr(src, p, r);
     const float* c = center + p * Kp;
     const int64_t orow = p * rows + r;
+    if (threadIdx.x == 0 && pf_dist > 0) {
+        // L2 prefetch of the row the CTA pf_dist launches later will read (about two waves
+        // ahead), so HBM keeps streaming while resident CTAs reduce / quantise / store
+        const int64_t lin = (int64_t)blockIdx.y * gridDim.x + blockIdx.x + pf_dist;
+        if (lin < (int64_t)gridDim.x * gridDim.y) {
+            const float* xn = row_ptr(src, lin / gridDim.x, lin % gridDim.x);
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(xn), "r"((uint32_t)(K * 4)) : "memory");
+        }
+    }
     __shared__ float red[NT / 32];
     __shared__ unsigned long long redd[NT / 32];
     float4 v[NV];
@@ -358,14 +370,29 @@ cudaError_t launch_pack_i8(int P, const RowSrc& src, int64_t rows, int64_t K, in
     if (rows == 0) return cudaSuccess;
     dim3 grid((unsigned)rows, (unsigned)P);
     ProfScope ps_(K_PACK, st);
+    // prefetch distance: PF_X8 / 8 resident-CTA waves ahead (diagnostic override CIL_PACK_PF)
+    static const char* pfe = getenv("CIL_PACK_PF");
+    const int pf_x8 = pfe ? atoi(pfe) : 4;
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    auto pf = [&](int nt) {
+        int per_sm = 0;                                          // resident CTAs per SM
+        switch (nt) {
+            case 256: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pack_i8r<8, 256>, 256, 0); break;
+            case 512: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pack_i8r<8, 512>, 512, 0); break;
+            default: per_sm = 2048 / nt;
+        }
+        return (int64_t)pf_x8 * nsm * (per_sm > 0 ? per_sm : 1) / 8;
+    };
     if (Kp <= 4096)
-        k_pack_i8r<4, 256><<<grid, 256, 0, st>>>(src, rows, K, Kp, center, hq, lq, nrm, scl, status);
+        k_pack_i8r<4, 256><<<grid, 256, 0, st>>>(src, rows, K, Kp, center, hq, lq, nrm, scl, status, pf(256));
     else if (Kp <= 8192)
-        k_pack_i8r<8, 256><<<grid, 256, 0, st>>>(src, rows, K, Kp, center, hq, lq, nrm, scl, status);
+        k_pack_i8r<8, 256><<<grid, 256, 0, st>>>(src, rows, K, Kp, center, hq, lq, nrm, scl, status, pf(256));
     else if (Kp <= 16384)
-        k_pack_i8r<8, 512><<<grid, 512, 0, st>>>(src, rows, K, Kp, center, hq, lq, nrm, scl, status);
+        k_pack_i8r<8, 512><<<grid, 512, 0, st>>>(src, rows, K, Kp, center, hq, lq, nrm, scl, status, pf(512));
     else if (Kp <= 32768)
-        k_pack_i8r<8, 1024><<<grid, 1024, 0, st>>>(src, rows, K, Kp, center, hq, lq, nrm, scl, status);
+        k_pack_i8r<8, 1024><<<grid, 1024, 0, st>>>(src, rows, K, Kp, center, hq, lq, nrm, scl, status, pf(1024));
     else
         k_pack_i8<<<grid, 256, 0, st>>>(src, rows, K, Kp, center, hq, lq, nrm, scl, status);
     note_launch();
