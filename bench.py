@@ -457,8 +457,10 @@ def pilot_radii_all(A0, B0, grid, M, mask):
 
 
 def bench_c3(args, dev):
-    """Evidence run for SURVEY §8 config C3 (the alternative measures on CUDA cores):
-    2000 x 2000 patterns of 128x128x2, all six measures, M = 20 (L2 on tensor cores)."""
+    """Evidence run for SURVEY §8 config C3 (the alternative measures): 2000 x 2000 patterns of
+    128x128x2, all six measures, M = 20.  AUTO: L2, W12, W12SUM on the three-phase INT8 tensor-core
+    engine, the max family (Linf, W1inf, W1infsum) on the CUDA-core engine; SIMT: everything on
+    CUDA cores."""
     import paper_2203_14742_b200 as cil
     from paper_2203_14742_b200 import _capi
     grid, N, M, mask = (2, 128, 128), 2000, 20, 0x3F
@@ -486,14 +488,26 @@ def bench_c3(args, dev):
     Kaug = K + S * H * (W - 1) + S * (H - 1) * W
     simt_ms = prof["simt_tile"][0] / max(1, prof["simt_tile"][1])
     ep = float(N) * N * Kaug                                  # element-pairs per family per launch
-    ceil_both, _ = _capi.alu_ceiling(0)
-    res = {"workload": "C3: 2000 x 2000 of 128x128x2, L2 (tensor) + Linf, W12sum, W12, W1inf, W1infsum (CUDA cores), M=20",
+    tc_family = args.engine in ("AUTO", "TC_I8")
+    mix = 1 if tc_family else 0                               # max family only / both families
+    ceil, _ = _capi.alu_ceiling(mix)
+    res = {"workload": "C3: 2000 x 2000 of 128x128x2, all six measures, M=20",
+           "engine": args.engine,
            "ms_per_step": round(ms, 3), "pairs_per_s": N * N / (ms * 1e-3),
-           "simt_tile": {"ms_per_launch": round(simt_ms, 3), "element_pairs_per_s": ep / (simt_ms * 1e-3),
-                         "alu_ceiling_element_pairs_per_s (measured, mix FADD2+FMNMX3+FFMA2)": ceil_both,
-                         "frac": round(ep / (simt_ms * 1e-3) / ceil_both, 4),
-                         "K_aug": Kaug},
+           "simt_tile": {"families": "max (Linf, W1inf, W1infsum)" if tc_family else "max + L2-type",
+                         "ms_per_launch": round(simt_ms, 3), "element_pairs_per_s": ep / (simt_ms * 1e-3),
+                         "alu_ceiling_element_pairs_per_s": ceil,
+                         "ceiling_mix": "FADD2+FMNMX3" if mix == 1 else "FADD2+FMNMX3+FFMA2",
+                         "frac": round(ep / (simt_ms * 1e-3) / ceil, 4), "K_aug": Kaug},
            "kernel_breakdown": {k: round(v[0] / steps, 3) for k, v in prof.items() if v[1] > 0}}
+    g_ms, g_n = prof["gram_tc"]
+    if g_n and tc_family:
+        per = g_ms / g_n
+        ops = 3 * 2.0 * N * N * Kaug                          # three-phase Gram over [x | D_x x | D_y x]
+        ach = ops / (per * 1e-3) / 1e12
+        res["gram_tc"] = {"engine": "TC_I8 three-phase (L2, W12, W12SUM)", "ms_per_launch": round(per, 3),
+                          "achieved_tops": round(ach, 1),
+                          "frac_of_peak": round(ach / (2.0 * peaks().get("bf16_tflops", 1590.0)), 4)}
     print(json.dumps(res), flush=True)
 
 

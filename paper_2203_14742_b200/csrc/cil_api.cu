@@ -80,6 +80,7 @@ double grid_h(const cil_grid& g) {
 struct Plan {
     bool tc = false;        // L2 on tensor cores
     int split = 1;          // 1 = 3xBF16, 2 = 3xTF32
+    bool aug = false;       // three-phase INT8 engine: L2, W12, W12SUM on tensor cores
     uint32_t simt_mask = 0; // measures on the CUDA-core engine
     bool do_max = false, do_sum = false;
     int nreg = 1;
@@ -92,9 +93,32 @@ bool i8_ok(const cil_grid& g, int64_t col_seg, int64_t rowsB) {
     const int64_t K = (int64_t)g.S * g.H * g.W;
     return K <= 65536 && (col_seg >= rowsB || col_seg >= 43);
 }
+// The L2-type family (L2, W12, W12SUM) on the three-phase INT8 engine when the
+// request has W12 or W12SUM, the engine is AUTO / TC_I8, every block fits the exact int32
+// accumulation and the per-thread histograms fit (column segments: M <= 16).
+bool aug_ok(uint32_t mask, cil_engine engine, const cil_grid& g, int64_t col_seg, int64_t rowsB, int M) {
+    if (!(mask & (CIL_W12 | CIL_W12SUM))) return false;
+    if (engine != CIL_ENGINE_AUTO && engine != CIL_ENGINE_TC_I8) return false;
+    if (g.W < 2) return false;
+    const int64_t K = (int64_t)g.S * g.H * g.W;
+    if (K > 65536) return false;                               // Kx, Ky < K
+    const bool seg = col_seg < rowsB;
+    if (seg && (col_seg < 43 || M > 16)) return false;
+    return M <= 64;
+}
 Plan make_plan(uint32_t mask, cil_engine engine, const cil_grid& g, int64_t col_seg = 1ll << 40,
-               int64_t rowsB = 0) {
+               int64_t rowsB = 0, int M = 1, bool allow_aug = true) {
     Plan pl;
+    if (allow_aug && aug_ok(mask, engine, g, col_seg, rowsB, M)) {
+        pl.tc = true;
+        pl.aug = true;
+        pl.split = 3;
+        pl.simt_mask = mask & ~(uint32_t)(CIL_L2 | CIL_W12 | CIL_W12SUM);
+        pl.do_max = pl.simt_mask & (CIL_LINF | CIL_W1INF | CIL_W1INFSUM);
+        pl.do_sum = false;
+        pl.nreg = (pl.simt_mask & (CIL_W1INF | CIL_W1INFSUM)) ? (g.H > 1 ? 3 : 2) : 1;
+        return pl;
+    }
     const bool want_tc = (mask & CIL_L2) && engine != CIL_ENGINE_SIMT;
     pl.tc = want_tc;
     pl.split = (engine == CIL_ENGINE_TC_3XTF32) ? 2 : (engine == CIL_ENGINE_TC_3XBF16) ? 1 : 3;
@@ -113,7 +137,7 @@ bool plan_bins(uint32_t mask, cil_engine engine, const cil_grid& g, Plan* out) {
     if (engine == CIL_ENGINE_TC_3XBF16 || engine == CIL_ENGINE_TC_3XTF32) return false;
     const int64_t K = (int64_t)g.S * g.H * g.W;
     const cil_engine e = (engine == CIL_ENGINE_SIMT || K > 65536) ? CIL_ENGINE_SIMT : CIL_ENGINE_TC_I8;
-    *out = make_plan(mask, e, g);
+    *out = make_plan(mask, e, g, 1ll << 40, 0, 1, /*allow_aug=*/false);
     return true;
 }
 
@@ -121,6 +145,7 @@ bool plan_bins(uint32_t mask, cil_engine engine, const cil_grid& g, Plan* out) {
 Plan plan_union(const Plan& a, const Plan& b) {
     Plan u = a;
     u.tc = a.tc || b.tc;
+    u.aug = a.aug || b.aug;
     // operand element size: split 2 (tf32) 4 B > split 1 (bf16) 2 B > split 3 (int8) 1 B
     auto esz = [](const Plan& p) { return !p.tc ? 0 : p.split == 2 ? 4 : p.split == 3 ? 1 : 2; };
     u.split = esz(a) >= esz(b) ? a.split : b.split;
@@ -134,10 +159,11 @@ Plan plan_union(const Plan& a, const Plan& b) {
 // Workspace carve-up (identical in the size query and in the call).
 struct Layout {
     size_t off_thr, off_thr2, off_hist, off_ctr, off_list, off_center, off_hi, off_lo, off_nrm, off_q4,
-        off_aug, off_Y, off_mu, off_sig, total;
+        off_aug, off_Y, off_mu, off_sig, off_part, total;
     int64_t hist_elems = 0;
     uint32_t list_cap = 0;
     int64_t Kp = 0;
+    int64_t kp[4] = {0, 0, 0, 0};   // three-phase engine: block starts of the augmented planes, kp[3] = row length
     AugGeom geom{};
 };
 
@@ -150,7 +176,7 @@ Layout make_layout(int P, int64_t rowsA, int64_t rowsB, const cil_grid& g, int n
     auto take = [&](size_t bytes) { size_t r = o; o = al(o + bytes); return r; };
     const int64_t K = (int64_t)g.S * g.H * g.W;
     L.off_thr = take(sizeof(double) * (size_t)P * nq * M);
-    L.off_thr2 = take(sizeof(float) * (size_t)P * M);
+    L.off_thr2 = take(sizeof(float) * (size_t)P * 3 * M);      // [P][kind][M] tensor-core thresholds
     L.hist_elems = (int64_t)P * sp.n_rs * sp.n_cs * nq * (M + 1);
     L.off_hist = take(sizeof(uint64_t) * (size_t)L.hist_elems);
     L.off_ctr = take(sizeof(uint32_t) * 2);
@@ -161,12 +187,23 @@ Layout make_layout(int P, int64_t rowsA, int64_t rowsB, const cil_grid& g, int n
         L.list_cap = (uint32_t)fmin(cap, 4.0e9);
         L.Kp = round_up(K, kTcBK);
         const size_t esz = pl.split == 2 ? 4 : (pl.split == 3 ? 1 : 2);
+        int64_t Krow = L.Kp;
+        if (pl.aug) {
+            const AugGeom ag = make_aug_geom(g.S, g.H, g.W, 3);
+            L.kp[0] = 0;
+            L.kp[1] = L.Kp;
+            L.kp[2] = L.kp[1] + round_up(ag.Kx, kTcBK);
+            L.kp[3] = L.kp[2] + round_up(ag.Ky, kTcBK);
+            Krow = L.kp[3];
+            L.list_cap = (uint32_t)fmin(fmin(pairs, 3.0 * pairs / 256.0 + 65536.0), 4.0e9);
+        }
         L.off_list = take(16 * (size_t)L.list_cap);
         L.off_center = take(sizeof(float) * (size_t)P * L.Kp);
-        L.off_hi = take(esz * (size_t)rows * L.Kp);
-        L.off_lo = take(esz * (size_t)rows * L.Kp);
-        L.off_nrm = take(sizeof(float) * (size_t)rows);
-        L.off_q4 = take(sizeof(float) * (size_t)rows);
+        L.off_hi = take(esz * (size_t)rows * Krow);
+        L.off_lo = take(esz * (size_t)rows * Krow);
+        L.off_nrm = take(sizeof(float) * (size_t)rows * (pl.aug ? 4 : 1));
+        L.off_q4 = take(sizeof(float) * (size_t)rows * (pl.aug ? 4 : 1));
+        if (pl.aug) L.off_part = take(sizeof(float) * 4 * (size_t)P * rowsA * rowsB);
     }
     if (pl.simt_mask) {
         L.geom = make_aug_geom(g.S, g.H, g.W, pl.nreg);
@@ -273,7 +310,48 @@ cil_status run_engines(int P, const RowSrc& asrc, const RowSrc& bsrc, int64_t ro
         const size_t offB = (size_t)P * rowsA;
         uint4* list = at<uint4>(ws, L.off_list);
         CIL_CU(launch_center(P, bsrc, rowsB < 16 ? rowsB : 16, K, L.Kp, center, st));
-        if (pl.split == 3) {
+        int q_tc[3] = {-1, -1, -1};
+        if (pl.aug) {
+            // ---- three-phase INT8 engine: L2, W12, W12SUM from the Grams of [x~ | D_x x~ | D_y x~]
+            if (binout || diag) return CIL_EUNSUPPORTED;
+            for (int q = 0; q < sl.nq; ++q) {
+                if (sl.slot[q] == 0) q_tc[0] = q;
+                if (sl.slot[q] == 3) q_tc[1] = q;
+                if (sl.slot[q] == 2) q_tc[2] = q;
+            }
+            const AugGeom ag = make_aug_geom(g.S, g.H, g.W, 3);
+            const int64_t Kr = L.kp[3];
+            const bool b_same = same_rows(asrc, bsrc) && rowsA == rowsB;
+            CIL_CU(launch_pack_i8_aug(P, asrc, rowsA, ag, L.kp, center, L.Kp, reinterpret_cast<int8_t*>(hi),
+                                      reinterpret_cast<int8_t*>(lo), Kr, nrm, q4, status, st));
+            if (!b_same)
+                CIL_CU(launch_pack_i8_aug(P, bsrc, rowsB, ag, L.kp, center, L.Kp,
+                                          reinterpret_cast<int8_t*>(hi + offB * Kr),
+                                          reinterpret_cast<int8_t*>(lo + offB * Kr), Kr, nrm + offB * 4,
+                                          q4 + offB * 4, status, st));
+            I8Args t{};
+            t.hq = reinterpret_cast<const int8_t*>(hi); t.lq = reinterpret_cast<const int8_t*>(lo);
+            t.rowsA = rowsA; t.rowsB = rowsB; t.Kp = Kr; t.K = K;
+            t.P = P; t.p0 = 0; t.np = P;
+            t.thr2 = thr2; t.thr_stride = 3 * M; t.M = M; t.q_l2 = sl.q_l2; t.nq = sl.nq;
+            t.sp = sp; t.hist = hist;
+            t.recheck = list; t.recheck_ctr = ctr; t.recheck_cap = L.list_cap;
+            t.kq = 20.0f;
+            t.rel = (float)ldexp(1.0, -21);
+            t.b_same = b_same;
+            t.nph = 3;
+            const int64_t klen[3] = {ag.K, ag.Kx, ag.Ky};
+            for (int a = 0; a < 3; ++a) {
+                t.kb_end[a] = (int)(L.kp[a + 1] / kTcBK);
+                t.kll3[a] = (float)(8.0 * 2.0 * (128.0 * 128.0 / 3.0) * sqrt((double)klen[a]));
+                t.q_tc[a] = q_tc[a];
+            }
+            t.kll = t.kll3[0];
+            t.nrm3 = nrm; t.scl3 = q4;
+            t.part = at<float>(ws, L.off_part);
+            t.ih = (float)(1.0 / bp.h);
+            CIL_CU(launch_gram_i8(t, st));
+        } else if (pl.split == 3) {
             // ---- INT8 two-digit engine (default): exact int32 accumulation
             // B = A (pool x pool bin matrices of the bootstrap): the rows are packed once
             const bool b_same = same_rows(asrc, bsrc) && rowsA == rowsB;
@@ -289,7 +367,7 @@ cil_status run_engines(int P, const RowSrc& asrc, const RowSrc& bsrc, int64_t ro
             t.nrm = nrm; t.scl = q4;
             t.rowsA = rowsA; t.rowsB = rowsB; t.Kp = L.Kp; t.K = K;
             t.P = P; t.p0 = 0; t.np = P;
-            t.thr2 = thr2; t.thr_stride = M; t.M = M; t.q_l2 = sl.q_l2; t.nq = sl.nq;
+            t.thr2 = thr2; t.thr_stride = 3 * M; t.M = M; t.q_l2 = sl.q_l2; t.nq = sl.nq;
             t.sp = sp; t.hist = hist;
             t.recheck = list; t.recheck_ctr = ctr; t.recheck_cap = L.list_cap;
             // E = kq d sqrt((s_a^2 + s_b^2)/3) + kll s_a s_b + rel (n_a + n_b): 20 sigma of the operand
@@ -313,7 +391,7 @@ cil_status run_engines(int P, const RowSrc& asrc, const RowSrc& bsrc, int64_t ro
             t.hi = hi; t.lo = lo; t.nrm = nrm; t.q4 = q4;
             t.rowsA = rowsA; t.rowsB = rowsB; t.Kp = L.Kp; t.K = K;
             t.P = P; t.split = pl.split;
-            t.thr2 = thr2; t.thr_stride = M; t.M = M;
+            t.thr2 = thr2; t.thr_stride = 3 * M; t.M = M;
             t.q_l2 = sl.q_l2; t.nq = sl.nq;
             t.sp = sp; t.hist = hist;
             t.recheck = list; t.recheck_ctr = ctr; t.recheck_cap = L.list_cap;
@@ -345,6 +423,8 @@ cil_status run_engines(int P, const RowSrc& asrc, const RowSrc& bsrc, int64_t ro
         r.list = list; r.ctr = ctr; r.cap = L.list_cap;
         r.status = status; r.P = P;
         r.binout = binout; r.rowsA = rowsA; r.rowsB = rowsB;
+        for (int a = 0; a < 3; ++a) r.q_tc[a] = q_tc[a];
+        r.S = g.S; r.H = g.H; r.W = g.W; r.h = bp.h;
         CIL_CU(launch_recheck(r, st));
         static const char* dbg = getenv("CIL_DEBUG_RECHECK");   // diagnostic: synchronising count print
         if (dbg && dbg[0] == '1') {
@@ -366,7 +446,7 @@ size_t cil_features_workspace_size(int32_t P, int64_t N, int64_t Nt, cil_grid g,
                                    int32_t M, cil_engine engine) {
     if (P < 1 || N < 0 || Nt < 0 || M < 1 || check_grid(g, dist_mask) != CIL_OK) return 0;
     const Slots sl = slots_of(dist_mask);
-    const Plan pl = make_plan(dist_mask, engine, g, Nt > 0 ? Nt : 1, Nt);
+    const Plan pl = make_plan(dist_mask, engine, g, Nt > 0 ? Nt : 1, Nt, M);
     SegParams sp{N > 0 ? N : 1, Nt > 0 ? Nt : 1, 1, 1};
     return make_layout(P, N, Nt, g, sl.nq, M, pl, sp, 0).total;
 }
@@ -389,7 +469,7 @@ cil_status cil_features(int32_t P, const float* A, int64_t strideA, int64_t lda,
     if (K % 4 || lda % 4 || ldb % 4 || strideA % 4 || strideB % 4) return CIL_EUNSUPPORTED;
     if ((A && !aligned16(A)) || (B && !aligned16(B))) return CIL_EUNSUPPORTED;
     const Slots sl = slots_of(dist_mask);
-    const Plan pl = make_plan(dist_mask, engine, g, Nt > 0 ? Nt : 1, Nt);
+    const Plan pl = make_plan(dist_mask, engine, g, Nt > 0 ? Nt : 1, Nt, M);
     SegParams sp{N > 0 ? N : 1, Nt > 0 ? Nt : 1, 1, 1};
     const Layout L = make_layout(P, N, Nt, g, sl.nq, M, pl, sp, 0);
     if (ws_bytes < L.total) return CIL_ENOMEM;
@@ -438,7 +518,7 @@ size_t cil_synth_workspace_size(int32_t P, int32_t n_ens, int32_t N_set, int32_t
     if (P < 1 || n_ens < 2 || N_set < 1 || N_tilde < 1 || M < 1 || check_grid(g, dist_mask) != CIL_OK)
         return 0;
     const Slots sl = slots_of(dist_mask);
-    const Plan pl = make_plan(dist_mask, engine, g, N_tilde, (int64_t)n_ens * N_tilde);
+    const Plan pl = make_plan(dist_mask, engine, g, N_tilde, (int64_t)n_ens * N_tilde, M);
     const int64_t rowsA = (int64_t)(n_ens + 1) * N_set, rowsB = (int64_t)n_ens * N_tilde;
     SegParams sp{N_set, N_tilde, n_ens + 1, n_ens};
     const int64_t nY = (int64_t)P * (n_ens * n_ens + 1) * sl.nq * M;
@@ -464,7 +544,7 @@ cil_status cil_synth_loglik(int32_t P, const float* pools, int64_t pool_stride, 
     if (!aligned16(pools) || !aligned16(data)) return CIL_EUNSUPPORTED;
     const Slots sl = slots_of(dist_mask);
     if (sl.nq * M > kMaxD) return CIL_EUNSUPPORTED;
-    const Plan pl = make_plan(dist_mask, engine, g, N_tilde, (int64_t)n_ens * N_tilde);
+    const Plan pl = make_plan(dist_mask, engine, g, N_tilde, (int64_t)n_ens * N_tilde, M);
     const int64_t rowsA = (int64_t)(n_ens + 1) * N_set, rowsB = (int64_t)n_ens * N_tilde;
     SegParams sp{N_set, N_tilde, n_ens + 1, n_ens};
     const int nv = n_ens * n_ens;
@@ -563,7 +643,7 @@ bool boot_layout(int32_t P, int32_t N_syn, int32_t N_set, int32_t n_rep, const c
                  int32_t M, cil_engine engine, BootLayout* B) {
     if (!plan_bins(mask, engine, g, &B->pb)) return false;
     const int32_t Nt = N_syn - N_set;
-    B->ph = make_plan(mask, engine, g, Nt, Nt);
+    B->ph = make_plan(mask, engine, g, Nt, Nt, M);
     const Plan u = plan_union(B->pb, B->ph);
     const Slots sl = slots_of(mask);
     SegParams sp{N_syn, N_syn, 1, 1};

@@ -203,8 +203,21 @@ struct I8Args {
     float* diag;
     uint8_t* binout;                     // non-null: bins[p][q_l2][i][j] instead of counts
     bool b_same;                         // B panel = A panel (rows packed once, B reads the A planes)
+    // ---- three-phase mode (the L2 family on tensor cores): the planes hold the
+    // augmented rows [x~ | D_x x~ | D_y x~], each block padded to 128 columns and quantised with
+    // its own scale; phase a = the Gram of block a (k-blocks [kb_end[a-1], kb_end[a]))
+    int nph;                             // 1 (value block only, L2) or 3
+    int kb_end[3];
+    const float* nrm3; const float* scl3;   // [rows][4]: block norms / scales (nph == 3)
+    float kll3[3];                       // kll of each block (sqrt of its length)
+    float* part;                         // [P*rowsA*rowsB][4] FP32 phase partials (d2_0, E_0, d2_x, E_x)
+    int q_tc[3];                         // histogram slot of L2, W12, W12SUM (-1: not requested)
+    float ih;                            // 1/h
 };
 cudaError_t launch_gram_i8(const I8Args& a, cudaStream_t st);
+cudaError_t launch_pack_i8_aug(int P, const RowSrc& src, int64_t rows, const AugGeom& g, const int64_t* kp,
+                               const float* center, int64_t Kc, int8_t* hq, int8_t* lq, int64_t Kp_aug,
+                               float* nrm3, float* scl3, int32_t* status, cudaStream_t st);
 bool gram_tc_supported();
 
 // recheck.cu
@@ -222,6 +235,11 @@ struct RecheckArgs {
     int P;
     uint8_t* binout;     // non-null: write the exact bin to bins[p][q_l2][i][j] instead of moving counts
     int64_t rowsA, rowsB;
+    // entries of the three-phase engine carry the measure kind in bits 8-15 of .w
+    // (0 L2, 1 W12, 2 W12SUM); q_tc = their histogram slots, S/H/W the grid, h the spacing
+    int q_tc[3];
+    int S, H, W;
+    double h;
 };
 cudaError_t launch_recheck(const RecheckArgs& a, cudaStream_t st);
 

@@ -47,6 +47,15 @@ struct I8Params {
     float kq, kll, rel;
     float* diag;
     uint8_t* binout;           // non-null: bins[p][q_l2][i][j] (provisional; re-check fixes ambiguous ones)
+    int pf;                    // L2 prefetch distance of the TMA producer in k-blocks (0 = off)
+    // three-phase mode (AUG): blocks value / D_x / D_y, k-block ends per phase
+    int nph;
+    int kb_end[3];
+    const float* nrm3; const float* scl3;   // [rows][4]
+    float kll3[3];
+    float2* part;              // [2][P*rowsA*rowsB] (d2, E) of phases 0 and 1
+    int q_tc[3];               // histogram slots of L2, W12, W12SUM (-1: absent)
+    float ih;                  // 1/h
     int dbg;                   // diagnostic timing knob (CIL_DEBUG_I8): 1 skip binning, 2 skip the epilogue,
                                // 3 also skip the B loads, 4 all loads
 };
@@ -61,24 +70,196 @@ __host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
     return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
-template <int MAXM, bool SEG> struct I8Geo {
-    static constexpr int STAGES = MAXM <= 16 ? 3 : 2;
+template <int MAXM, bool SEG, bool AUG = false> struct I8Geo {
+    static constexpr int STAGES = (MAXM <= 16 && !AUG) ? 3 : 2;
     static constexpr int STAGE_BYTES = Geo<2>::STAGE_BYTES;       // 64 KB: h, l of 128 A- and 128 B-rows
     // per-thread histograms [bin][thread] of u32 cells (bank = thread, conflict-free); with column
     // segments (SCIL blocks of >= 43 columns, so a 128-column half meets <= 4) byte l of a cell
-    // counts local segment l (<= 128 pairs per tile, flushed every tile)
+    // counts local segment l (<= 128 pairs per tile, flushed every tile).  AUG (three measure
+    // kinds): without segments byte k of a cell counts kind k; with segments one cell array
+    // per kind.
     static constexpr int NLOC = SEG ? 4 : 1;
-    static constexpr int HIST_BYTES = (MAXM + 1) * 256 * 4;
+    static constexpr int NKIND = AUG ? 3 : 1;
+    static constexpr int HIST_BYTES = (AUG && SEG ? 3 : 1) * (MAXM + 1) * 256 * 4;
     static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 1024 /*barriers*/ +
-                                      3 * TILE_N * 4 /*norms, sigma, spare*/ + 2 * MAXM * 4 + HIST_BYTES;
+                                      3 * TILE_N * 4 /*norms, sigma, spare*/ + NKIND * 2 * MAXM * 4 + HIST_BYTES;
 };
 
+// b = #{m : v < T_m} for decreasing thresholds T[0..MAXM) padded with -inf to 2*MAXM
+template <int MAXM>
+__device__ __forceinline__ int bin_search(float v, const float* T) {
+    int b = 0;
+#pragma unroll
+    for (int s = MAXM; s >= 1; s >>= 1)
+        if (v < T[b + s - 1]) b += s;
+    return b;
+}
+
+// Three-phase epilogue (the L2-type family on tensor cores): phase a drains the Gram of block a
+// (value, D_x, D_y) into (d2_a, E_a); phases 0 and 1 park theirs in global memory (L2-resident
+// partials), phase 2 forms
+//   L2^2/w = d2_0,   W12^2/w = d2_0 + (d2_x + d2_y)/h^2,   W12SUM/sqrt(w) = sqrt d2_0 + (sqrt d2_x + sqrt d2_y)/h
+// (Eqs. (5), (8), (7) with readings R1, R3) with their bounds, bins the requested ones and
+// sends pairs with a threshold inside the bound to the FP64 re-check (kind in bits 8-15).
 template <int MAXM, bool SEG>
+__device__ __forceinline__ void epilogue_aug(const I8Params& prm, uint32_t tmem_base, uint64_t* tfull,
+                                             uint64_t* tempty, float* s_nb, float* s_sb, float* s_T,
+                                             uint32_t* hist_s, int cluster_id, int n_clusters, int total_tiles,
+                                             int tiles_per_item, uint32_t rank, int warp, int lane) {
+    using G = Geo<2>;
+    using IG = I8Geo<MAXM, SEG, true>;
+    const int quarter = warp & 3;
+    const int half = (warp - 2) >> 2;
+    const int et = threadIdx.x - 64;
+    const int M = prm.M;
+    const int64_t npairs = (int64_t)prm.P * prm.rowsA * prm.rowsB;
+    uint32_t tph = 0;
+    for (int t = cluster_id; t < total_tiles; t += n_clusters) {
+        const int p = prm.p0 + t / tiles_per_item, r = t % tiles_per_item;
+        const int mt = r / prm.tiles_n, nt = r % prm.tiles_n;
+        const int64_t col0 = (int64_t)nt * TILE_N;
+        const int64_t browbase = prm.b_off + (int64_t)p * prm.rowsB;
+        const int64_t row = (int64_t)mt * G::TILE_M + rank * A_ROWS + quarter * 32 + lane;
+        const bool row_ok = row < prm.rowsA;
+        const int64_t arow = (int64_t)p * prm.rowsA + (row_ok ? row : 0);
+        const int hc0 = (int)(col0 + half * 128);
+        const int nvalid = (int)min((int64_t)128, prm.rowsB - hc0);
+        const uint32_t tl = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(half * 128);
+        const int64_t cs_first = (int64_t)hc0 / prm.sp.col_seg;
+        int bnd[IG::NLOC > 1 ? IG::NLOC - 1 : 1];
+#pragma unroll
+        for (int i = 0; i < IG::NLOC - 1; ++i) {
+            const int64_t c = (cs_first + 1 + i) * prm.sp.col_seg - hc0;
+            bnd[i] = SEG ? (int)(c < 128 ? c : (1 << 30)) : (1 << 30);
+        }
+        uint32_t* myh = hist_s + et;
+        const int64_t pbase = (int64_t)p * prm.rowsA * prm.rowsB + (row_ok ? row : 0) * prm.rowsB;
+        for (int ph = 0; ph < 3; ++ph) {
+            named_bar(1, 256);
+            {
+                const int64_t c = col0 + et;
+                const bool ok = c < prm.rowsB;
+                s_nb[et] = ok ? prm.nrm3[(browbase + c) * 4 + ph] : 0.f;
+                s_sb[et] = ok ? prm.scl3[(browbase + c) * 4 + ph] : 0.f;
+                if (ph == 0 && et < 2 * MAXM)
+#pragma unroll
+                    for (int k = 0; k < 3; ++k)
+                        s_T[k * 2 * MAXM + et] = (et < M && prm.q_tc[k] >= 0)
+                                                     ? prm.thr2[(int64_t)p * prm.thr_stride + k * M + et]
+                                                     : -INFINITY;
+            }
+            named_bar(1, 256);
+            const float na = row_ok ? __ldg(&prm.nrm3[arow * 4 + ph]) : 0.f;
+            const float sa = row_ok ? __ldg(&prm.scl3[arow * 4 + ph]) : 0.f;
+            const float kq_sa = prm.kq * 0.81649658f;
+            const float kll_sa = prm.kll3[ph] * sa;
+            const float m2sa = -2.f * sa;
+            const bool empty_ph = prm.kb_end[ph] == (ph ? prm.kb_end[ph - 1] : 0);
+            mbar_wait(&tfull[0], tph);
+            fence_after();
+#pragma unroll 1
+            for (int g = 0; g < 8; ++g) {
+                if (g * 16 >= nvalid) break;
+                uint32_t hv[16], xv[16];
+                tmem_ld16(tl + g * 16, hv);
+                tmem_ld16(tl + TILE_N + g * 16, xv);
+                if (!row_ok) continue;
+#pragma unroll
+                for (int jj = 0; jj < 16; ++jj) {
+                    const int j = g * 16 + jj;
+                    if (j >= nvalid) break;
+                    const int jc = half * 128 + j;
+                    const float sb = s_sb[jc], nb = s_nb[jc];
+                    const float gi = empty_ph ? 0.f : fmaf((float)(int)hv[jj], 65536.f, (float)(int)xv[jj] * 256.f);
+                    const float d2 = fmaxf(fmaf(m2sa * sb, gi, na + nb), 0.f);
+                    const float dd = fmaxf(d2, 1e-30f);
+                    const float E = fmaf(kq_sa * dd * rsqrtf(dd), fmaxf(sa, sb), fmaf(kll_sa, sb, prm.rel * (na + nb)));
+                    const int64_t pi = pbase + hc0 + j;
+                    if (ph < 2) {
+                        prm.part[ph * npairs + pi] = make_float2(d2, E);
+                        continue;
+                    }
+                    const float2 p0 = prm.part[pi], p1 = prm.part[npairs + pi];
+                    const float ih = prm.ih, ih2 = ih * ih;
+                    int lcs = 0;
+                    if (SEG) {
+#pragma unroll
+                        for (int i = 0; i < IG::NLOC - 1; ++i) lcs += (j >= bnd[i]) ? 1 : 0;
+                    }
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) {
+                        if (prm.q_tc[k] < 0) continue;
+                        float v, e;
+                        if (k == 0) {
+                            v = p0.x; e = p0.y;
+                        } else if (k == 1) {
+                            v = p0.x + (p1.x + d2) * ih2;
+                            e = p0.y + (p1.y + E) * ih2 + v * 2.4e-7f;
+                        } else {
+                            // |sqrt(u) - sqrt(d)| <= E / max(sqrt d, sqrt E) for |u - d| <= E
+                            const float r0 = sqrtf(p0.x), rx = sqrtf(p1.x), ry = sqrtf(d2);
+                            const float e0 = p0.y / fmaxf(r0, sqrtf(p0.y)), ex = p1.y / fmaxf(rx, sqrtf(p1.y)),
+                                        ey = E / fmaxf(ry, sqrtf(E));
+                            v = r0 + (rx + ry) * ih;
+                            e = e0 + (ex + ey) * ih + v * 2.4e-7f;
+                        }
+                        const float* T = s_T + k * 2 * MAXM;
+                        const int b = bin_search<MAXM>(v + e, T);
+                        if (SEG)
+                            atomicAdd(myh + ((k * (MAXM + 1) + b) << 8), 1u << (8 * lcs));
+                        else
+                            atomicAdd(myh + (b << 8), 1u << (8 * k));
+                        if (v - e < T[b]) {
+                            const uint32_t idx = atomicAdd(prm.ctr, 1u);
+                            if (idx < prm.cap)
+                                prm.list[idx] = make_uint4((uint32_t)p, (uint32_t)row, (uint32_t)(hc0 + j),
+                                                           (uint32_t)(b | (k << 8)));
+                        }
+                    }
+                }
+            }
+            fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_remote(&tempty[0], 0);
+            tph ^= 1;
+        }
+        // ---- flush the per-thread histograms of the requested kinds
+        const int64_t rs = row_ok ? row / prm.sp.row_seg : 0;
+        const int64_t rs0 = __shfl_sync(0xffffffffu, rs, 0);
+        const bool uniform = __all_sync(0xffffffffu, rs == rs0 || !row_ok);
+        for (int bb = 0; bb <= M; ++bb) {
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                uint32_t* cp = SEG ? myh + ((k * (MAXM + 1) + bb) << 8) : myh + (bb << 8);
+                const uint32_t cell = *cp;
+                if (SEG || k == 2) *cp = 0u;
+                if (bb == 0 || prm.q_tc[k] < 0) continue;          // bin 0 (outside every radius) is not kept
+#pragma unroll
+                for (int l = 0; l < IG::NLOC; ++l) {
+                    const int64_t cs = cs_first + l;
+                    if (cs * prm.sp.col_seg >= prm.rowsB || cs * prm.sp.col_seg >= hc0 + 128) break;
+                    const uint32_t v = SEG ? ((cell >> (8 * l)) & 255u) : ((cell >> (8 * k)) & 255u);
+                    if (uniform) {
+                        const uint32_t tot = __reduce_add_sync(0xffffffffu, v);
+                        if (lane == 0 && tot)
+                            atomicAdd(&prm.hist[hist_index(prm.sp, prm.nq, M, p, rs0, cs, prm.q_tc[k], bb)],
+                                      (unsigned long long)tot);
+                    } else if (v) {
+                        atomicAdd(&prm.hist[hist_index(prm.sp, prm.nq, M, p, rs, cs, prm.q_tc[k], bb)],
+                                  (unsigned long long)v);
+                    }
+                }
+            }
+        }
+    }
+}
+
+template <int MAXM, bool SEG, bool AUG>
 __global__ void __maxnreg__(168)
 k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUtensorMap mAl,
           const __grid_constant__ CUtensorMap mBh, const __grid_constant__ CUtensorMap mBl, I8Params prm) {
     using G = Geo<2>;
-    using IG = I8Geo<MAXM, SEG>;
+    using IG = I8Geo<MAXM, SEG, AUG>;
     constexpr int STAGES = IG::STAGES;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     // 1024-B alignment by offsetting the shared pointer itself (keeps the shared address space, so
@@ -92,8 +273,8 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
     float* s_nb = reinterpret_cast<float*>(smem + STAGES * IG::STAGE_BYTES + 1024);
     float* s_sb = s_nb + TILE_N;
-    float* s_T = s_sb + 2 * TILE_N;                       // [2*MAXM] thresholds, -inf padded
-    uint32_t* hist_s = reinterpret_cast<uint32_t*>(s_T + 2 * MAXM);
+    float* s_T = s_sb + 2 * TILE_N;                       // [NKIND][2*MAXM] thresholds, -inf padded
+    uint32_t* hist_s = reinterpret_cast<uint32_t*>(s_T + IG::NKIND * 2 * MAXM);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_rank();
@@ -140,6 +321,13 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
                     if (rank == 0)
                         mbar_expect_tx(&full[stage], none ? 0 : only_a ? 4 * G::A_BYTES : 2 * IG::STAGE_BYTES);
                     const int x = kb * 128;
+                    if (prm.pf > 0 && kb + prm.pf < prm.n_kb) {   // L2 prefetch pf k-blocks ahead
+                        const int xp = (kb + prm.pf) * 128;
+                        tma_prefetch_2d(&mAh, xp, ya);
+                        tma_prefetch_2d(&mAl, xp, ya);
+                        tma_prefetch_2d(&mBh, xp, yb);
+                        tma_prefetch_2d(&mBl, xp, yb);
+                    }
                     if (!none) {
                         tma_load_2d<2>(st, &mAh, &full[stage], x, ya);
                         tma_load_2d<2>(st + G::A_BYTES, &mAl, &full[stage], x, ya);
@@ -159,29 +347,36 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
             int stage = 0;
             uint32_t phase = 0, tph = 0;
             for (int t = cluster_id; t < total_tiles; t += n_clusters) {
-                mbar_wait_cluster(&tempty[0], tph ^ 1);
-                fence_after();
-                for (int kb = 0; kb < prm.n_kb; ++kb) {
-                    mbar_wait(&full[stage], phase);
+                // one accumulation (and one epilogue hand-off) per phase; nph = 1: the whole K
+                for (int ph = 0; ph < prm.nph; ++ph) {
+                    mbar_wait_cluster(&tempty[0], tph ^ 1);
                     fence_after();
-                    const uint32_t s0 = smem_u32(stages + stage * IG::STAGE_BYTES);
-                    const uint64_t ah = sdesc(s0), al = sdesc(s0 + G::A_BYTES);
-                    const uint64_t bh = sdesc(s0 + 2 * G::A_BYTES), bl = sdesc(s0 + 2 * G::A_BYTES + G::B_BYTES);
+                    const int kb0 = ph ? prm.kb_end[ph - 1] : 0, kb1 = prm.kb_end[ph];
+                    for (int kb = kb0; kb < kb1; ++kb) {
+                        mbar_wait(&full[stage], phase);
+                        fence_after();
+                        const uint32_t s0 = smem_u32(stages + stage * IG::STAGE_BYTES);
+                        const uint64_t ah = sdesc(s0), al = sdesc(s0 + G::A_BYTES);
+                        const uint64_t bh = sdesc(s0 + 2 * G::A_BYTES), bl = sdesc(s0 + 2 * G::A_BYTES + G::B_BYTES);
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) {               // 4 x 32 int8 of K per 128-byte row
-                        const uint64_t adv = (uint64_t)(k * 2);  // +32 B in the start-address field
-                        const uint32_t first = (kb | k) != 0 ? 1u : 0u;
-                        mma_i8(dH, ah + adv, bh + adv, id, first);
-                        mma_i8(dX, ah + adv, bl + adv, id, first);
-                        mma_i8(dX, al + adv, bh + adv, id, 1u);
+                        for (int k = 0; k < 4; ++k) {               // 4 x 32 int8 of K per 128-byte row
+                            const uint64_t adv = (uint64_t)(k * 2);  // +32 B in the start-address field
+                            const uint32_t first = (kb != kb0 || k != 0) ? 1u : 0u;
+                            mma_i8(dH, ah + adv, bh + adv, id, first);
+                            mma_i8(dX, ah + adv, bl + adv, id, first);
+                            mma_i8(dX, al + adv, bh + adv, id, 1u);
+                        }
+                        mma_commit<2>(&empty[stage]);
+                        if (++stage == STAGES) { stage = 0; phase ^= 1; }
                     }
-                    mma_commit<2>(&empty[stage]);
-                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                    mma_commit<2>(&tfull[0]);
+                    tph ^= 1;
                 }
-                mma_commit<2>(&tfull[0]);
-                tph ^= 1;
             }
         }
+    } else if constexpr (AUG) {
+        epilogue_aug<MAXM, SEG>(prm, tmem_base, tfull, tempty, s_nb, s_sb, s_T, hist_s, cluster_id, n_clusters,
+                                total_tiles, tiles_per_item, rank, warp, lane);
     } else {
         // ------------------------------------------------------------ epilogue
         const int quarter = warp & 3;
@@ -386,12 +581,12 @@ static bool make_map_i8(CUtensorMap* m, const void* base, int64_t rows, int64_t 
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int MAXM, bool SEG>
+template <int MAXM, bool SEG, bool AUG = false>
 static cudaError_t launch_i8_t(const tc::I8Params& prm, const CUtensorMap* maps, int nsm, cudaStream_t st) {
-    using IG = tc::I8Geo<MAXM, SEG>;
+    using IG = tc::I8Geo<MAXM, SEG, AUG>;
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(tc::k_gram_i8<MAXM, SEG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaError_t e = cudaFuncSetAttribute(tc::k_gram_i8<MAXM, SEG, AUG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              IG::SMEM_BYTES);
         if (e != cudaSuccess) return e;
         attr = true;
@@ -411,11 +606,11 @@ static cudaError_t launch_i8_t(const tc::I8Params& prm, const CUtensorMap* maps,
     cfg.attrs = at;
     cfg.numAttrs = 1;
     ProfScope ps_(K_GRAM_TC, st);
-    cudaError_t e = cudaLaunchKernelEx(&cfg, tc::k_gram_i8<MAXM, SEG>, maps[0], maps[1], maps[2], maps[3], prm);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, tc::k_gram_i8<MAXM, SEG, AUG>, maps[0], maps[1], maps[2], maps[3], prm);
     note_launch();
     if (e != cudaSuccess) {
         cudaFuncAttributes fa{};
-        cudaFuncGetAttributes(&fa, tc::k_gram_i8<MAXM, SEG>);
+        cudaFuncGetAttributes(&fa, tc::k_gram_i8<MAXM, SEG, AUG>);
         fprintf(stderr, "[libcil] k_gram_i8 launch failed (%s): regs=%d maxThreads=%d local=%zu smem_dyn=%d\n",
                 cudaGetErrorString(e), fa.numRegs, fa.maxThreadsPerBlock, fa.localSizeBytes, IG::SMEM_BYTES);
         return e;
@@ -448,14 +643,33 @@ cudaError_t launch_gram_i8(const I8Args& a, cudaStream_t st) {
     prm.kq = a.kq; prm.kll = a.kll; prm.rel = a.rel;
     prm.diag = a.diag;
     prm.binout = a.binout;
+    prm.nph = a.nph == 3 ? 3 : 1;
+    if (prm.nph == 3) {
+        for (int i = 0; i < 3; ++i) { prm.kb_end[i] = a.kb_end[i]; prm.kll3[i] = a.kll3[i]; prm.q_tc[i] = a.q_tc[i]; }
+        prm.nrm3 = a.nrm3; prm.scl3 = a.scl3;
+        prm.part = reinterpret_cast<float2*>(a.part);
+        prm.ih = a.ih;
+        prm.n_kb = a.kb_end[2];
+    } else {
+        prm.kb_end[0] = prm.n_kb;
+    }
     {
         static const char* dbg = getenv("CIL_DEBUG_I8");
         prm.dbg = dbg ? atoi(dbg) : 0;
+        static const char* pfe = getenv("CIL_I8_PF");
+        prm.pf = pfe ? atoi(pfe) : 0;
     }
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     const bool seg = a.sp.col_seg < a.rowsB;
+    if (prm.nph == 3) {
+        if (a.M <= 16)
+            return seg ? launch_i8_t<16, true, true>(prm, maps, nsm, st) : launch_i8_t<16, false, true>(prm, maps, nsm, st);
+        if (seg) return cudaErrorInvalidValue;                 // host routes these to the CUDA cores
+        if (a.M <= 32) return launch_i8_t<32, false, true>(prm, maps, nsm, st);
+        return launch_i8_t<64, false, true>(prm, maps, nsm, st);
+    }
     if (a.M <= 16) return seg ? launch_i8_t<16, true>(prm, maps, nsm, st) : launch_i8_t<16, false>(prm, maps, nsm, st);
     if (a.M <= 32) return seg ? launch_i8_t<32, true>(prm, maps, nsm, st) : launch_i8_t<32, false>(prm, maps, nsm, st);
     return seg ? launch_i8_t<64, true>(prm, maps, nsm, st) : launch_i8_t<64, false>(prm, maps, nsm, st);

@@ -34,14 +34,16 @@ __global__ void k_prep(int P, int nq, int M, const double* __restrict__ radii, i
         thr[(int64_t)p * nq * M + t] = r;
     }
     if (thr2_l2 != nullptr) {
-        int ql2 = -1;
-        for (int q = 0; q < nq; ++q)
-            if (bp.slot[q] == 0) ql2 = q;
-        if (ql2 >= 0)
+        // tensor-core thresholds [p][kind][M] (FP32): kind 0 L2 and kind 1 W12 compare the
+        // unweighted sums of squares with R^2/w, kind 2 W12SUM compares W12SUM/sqrt(w) with R/sqrt(w)
+        for (int q = 0; q < nq; ++q) {
+            const int kind = bp.slot[q] == 0 ? 0 : bp.slot[q] == 3 ? 1 : bp.slot[q] == 2 ? 2 : -1;
+            if (kind < 0) continue;
             for (int m = threadIdx.x; m < M; m += blockDim.x) {
-                const double r = R[ql2 * M + m];
-                thr2_l2[(int64_t)p * M + m] = (float)(r * r / bp.w);
+                const double r = R[q * M + m];
+                thr2_l2[((int64_t)p * 3 + kind) * M + m] = (float)(kind == 2 ? r / sqrt(bp.w) : r * r / bp.w);
             }
+        }
     }
     __syncthreads();
     if (threadIdx.x == 0) status[p] = (keep_status ? status[p] : 0) | (bad ? CIL_ITEM_BADRADII : 0);
@@ -408,6 +410,112 @@ cudaError_t launch_pack_i8_pair(int P, const RowSrc& asrc, int64_t rowsA, const 
     if (e != cudaSuccess) return e;
     return launch_pack_i8(P, bsrc, rowsB, K, Kp, center, hq + offB * Kp, lq + offB * Kp, nrm + offB, scl + offB,
                           status, st);
+}
+
+// ------------------------------------------------------------- INT8 augmented pack
+// Three-phase tensor-core route for the L2-type family: row x~ = x - c
+// is expanded into the blocks  value x~ (K),  D_x x~ = x~[s][r][c+1] - x~[s][r][c]
+// (S*H*(W-1), c < W-1),  D_y x~ = x~[s][r+1][c] - x~[s][r][c]  (S*(H-1)*W, r < H-1)
+// (forward differences, last node omitted, reading R3; raw differences, the 1/h is applied
+// to the distances), each block quantised with its own scale sigma_a = max|block| / 32639
+// into the two INT8 digits (h, l) at columns kp[a] + idx, zero-padded to kp[a+1];
+// norms n_a = sigma_a^2 sum q^2 (exact integer sum).  One CTA per row, two passes over the
+// (L1/L2-resident) row: block maxima, then quantisation.
+__global__ void __launch_bounds__(256) k_pack_i8_aug(RowSrc src, int64_t rows, AugGeom g, int64_t kp0, int64_t kp1,
+                                                     int64_t kp2, int64_t kp3, const float* __restrict__ center,
+                                                     int64_t Kc, int8_t* __restrict__ hq, int8_t* __restrict__ lq,
+                                                     int64_t Kp_aug, float* __restrict__ nrm3,
+                                                     float* __restrict__ scl3, int32_t* __restrict__ status) {
+    const int64_t p = blockIdx.y;
+    const int64_t r = blockIdx.x;
+    const float* x = row_ptr(src, p, r);
+    const float* c = center + p * Kc;
+    const int64_t orow = p * rows + r;
+    const int W = g.W, H = g.H;
+    const int64_t K = g.K;
+    __shared__ float red[3][8];
+    __shared__ unsigned long long redd[3][8];
+    float m0 = 0.f, mx = 0.f, my = 0.f, nfa = 0.f;
+    for (int64_t e = threadIdx.x; e < K; e += 256) {
+        const float v = __ldg(x + e), ce = __ldg(c + e);
+        nfa = fmaf(v, 0.f, nfa);
+        const float xe = v - ce;
+        m0 = fmaxf(m0, fabsf(xe));
+        const int col = (int)(e % W), row = (int)((e / W) % H);
+        if (col < W - 1) mx = fmaxf(mx, fabsf((__ldg(x + e + 1) - __ldg(c + e + 1)) - xe));
+        if (row < H - 1) my = fmaxf(my, fabsf((__ldg(x + e + W) - __ldg(c + e + W)) - xe));
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        m0 = fmaxf(m0, __shfl_xor_sync(0xffffffffu, m0, o));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        my = fmaxf(my, __shfl_xor_sync(0xffffffffu, my, o));
+    }
+    const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
+    const bool anynf = __syncthreads_or(nfa != nfa);
+    if (ln == 0) { red[0][w] = m0; red[1][w] = mx; red[2][w] = my; }
+    __syncthreads();
+    float sg[3], inv[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        float m = 0.f;
+        for (int i = 0; i < 8; ++i) m = fmaxf(m, red[a][i]);
+        sg[a] = (m > 0.f && isfinite(m)) ? m / 32639.f : 1.f;
+        inv[a] = 1.f / sg[a];
+    }
+    int8_t* ho = hq + orow * Kp_aug;
+    int8_t* lo = lq + orow * Kp_aug;
+    uint64_t s2[3] = {0ull, 0ull, 0ull};
+    auto put = [&](int a, int64_t col, float v) {
+        const int q = __float_as_int(fmaf(v, inv[a], 12582912.f)) - 0x4B400000;
+        const int hd = (q + 128) >> 8;
+        ho[col] = (int8_t)hd;
+        lo[col] = (int8_t)(q - 256 * hd);
+        s2[a] += (uint64_t)((uint32_t)(q * q));
+    };
+    for (int64_t e = threadIdx.x; e < K; e += 256) {
+        const float xe = __ldg(x + e) - __ldg(c + e);
+        const int col = (int)(e % W), row = (int)((e / W) % H);
+        const int64_t sr = e / W;                       // s*H + row
+        put(0, kp0 + e, xe);
+        if (col < W - 1) put(1, kp1 + sr * (W - 1) + col, (__ldg(x + e + 1) - __ldg(c + e + 1)) - xe);
+        if (row < H - 1) put(2, kp2 + e - (sr / H) * W, (__ldg(x + e + W) - __ldg(c + e + W)) - xe);
+    }
+    // zero padding of every block
+    const int64_t len[3] = {K, g.Kx, g.Ky}, beg[3] = {kp0, kp1, kp2}, end[3] = {kp1, kp2, kp3};
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+        for (int64_t col = beg[a] + len[a] + threadIdx.x; col < end[a]; col += 256) { ho[col] = 0; lo[col] = 0; }
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        uint64_t v = s2[a];
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (ln == 0) redd[a][w] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < 3) {
+        const int a = threadIdx.x;
+        unsigned long long v = 0ull;
+        for (int i = 0; i < 8; ++i) v += redd[a][i];
+        nrm3[orow * 4 + a] = (float)((double)v * (double)sg[a] * (double)sg[a]);
+        scl3[orow * 4 + a] = sg[a];
+    }
+    if (threadIdx.x == 0) {
+        nrm3[orow * 4 + 3] = 0.f;
+        scl3[orow * 4 + 3] = 0.f;
+        if (anynf) atomicOr(&status[p], CIL_ITEM_NONFINITE);
+    }
+}
+
+cudaError_t launch_pack_i8_aug(int P, const RowSrc& src, int64_t rows, const AugGeom& g, const int64_t* kp,
+                               const float* center, int64_t Kc, int8_t* hq, int8_t* lq, int64_t Kp_aug,
+                               float* nrm3, float* scl3, int32_t* status, cudaStream_t st) {
+    if (rows == 0) return cudaSuccess;
+    dim3 grid((unsigned)rows, (unsigned)P);
+    ProfScope ps_(K_PACK, st);
+    k_pack_i8_aug<<<grid, 256, 0, st>>>(src, rows, g, kp[0], kp[1], kp[2], kp[3], center, Kc, hq, lq, Kp_aug, nrm3,
+                                        scl3, status);
+    note_launch();
+    return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------- aug pack

@@ -16,13 +16,67 @@ __global__ void __launch_bounds__(256) k_recheck(RecheckArgs a) {
         for (int p = 0; p < a.P; ++p) atomicOr(&a.status[p], CIL_ITEM_OVERFLOW);
     }
     __shared__ double red[8];
+    __shared__ double red3[3][8];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     for (uint32_t e = blockIdx.x; e < n; e += gridDim.x) {
         const uint4 ent = a.list[e];
         const int64_t p = ent.x, i = ent.y, j = ent.z;
-        const int b_lo = (int)ent.w;
+        const int b_lo = (int)(ent.w & 255u);
+        const int kind = (int)((ent.w >> 8) & 255u);
         const float* x = row_ptr(a.asrc, p, i);
         const float* y = row_ptr(a.bsrc, p, j);
+        if (kind != 0) {
+            // W12 (kind 1) / W12SUM (kind 2): the FP64 sub-norms of u = a - b exactly as the plain
+            // definition (forward differences inside each species, last node omitted, R3)
+            const int W = a.W, H = a.H, SH = a.S * a.H;
+            const double h = a.h;
+            double s0 = 0.0, sx = 0.0, sy = 0.0;
+            // warp per grid row (s, r), lanes along the columns: coalesced, no index division
+            for (int sr = w; sr < SH; sr += 8) {
+                const bool has_dy = (sr % H) + 1 < H;
+                const float* xr = x + (int64_t)sr * W;
+                const float* yr = y + (int64_t)sr * W;
+                for (int c = lane; c < W; c += 32) {
+                    const double u = (double)__ldg(xr + c) - (double)__ldg(yr + c);
+                    s0 += u * u;
+                    if (c + 1 < W) {                       // raw differences; the 1/h^2 is applied once
+                        const double dx = ((double)__ldg(xr + c + 1) - (double)__ldg(yr + c + 1)) - u;
+                        sx += dx * dx;
+                    }
+                    if (has_dy) {
+                        const double dy = ((double)__ldg(xr + W + c) - (double)__ldg(yr + W + c)) - u;
+                        sy += dy * dy;
+                    }
+                }
+            }
+            for (int o = 16; o > 0; o >>= 1) {
+                s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+                sx += __shfl_xor_sync(0xffffffffu, sx, o);
+                sy += __shfl_xor_sync(0xffffffffu, sy, o);
+            }
+            if (lane == 0) { red3[0][w] = s0; red3[1][w] = sx; red3[2][w] = sy; }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                s0 = sx = sy = 0.0;
+                for (int t = 0; t < 8; ++t) { s0 += red3[0][t]; sx += red3[1][t]; sy += red3[2][t]; }
+                sx /= h * h;
+                sy /= h * h;
+                const double a0 = sqrt(a.w * s0), ax = sqrt(a.w * sx), ay = sqrt(a.w * sy);
+                const double d = kind == 1 ? sqrt(a0 * a0 + ax * ax + ay * ay) : a0 + ax + ay;   // Eqs. (8), (7)
+                const int q = a.q_tc[kind];
+                const double* R = a.thr + p * a.thr_stride + (int64_t)q * a.M;
+                int b = 0;
+                while (b < a.M && d < R[b]) ++b;
+                if (b != b_lo) {
+                    const int64_t rs = i / a.sp.row_seg, cs = j / a.sp.col_seg;
+                    unsigned long long* Hh = (unsigned long long*)a.hist;
+                    if (b_lo > 0) atomicAdd(&Hh[hist_index(a.sp, a.nq, a.M, p, rs, cs, q, b_lo)], ~0ull);
+                    if (b > 0) atomicAdd(&Hh[hist_index(a.sp, a.nq, a.M, p, rs, cs, q, b)], 1ull);
+                }
+            }
+            __syncthreads();
+            continue;
+        }
         double s = 0.0;
         // 4 independent float4 pairs in flight per thread (memory-level parallelism)
         int64_t k = (int64_t)threadIdx.x * 4;
@@ -53,7 +107,8 @@ __global__ void __launch_bounds__(256) k_recheck(RecheckArgs a) {
         if (threadIdx.x == 0) {
             s = 0.0;
             for (int t = 0; t < 8; ++t) s += red[t];
-            const double* R = a.thr + p * a.thr_stride + (int64_t)a.q_l2 * a.M;
+            const int ql = a.q_tc[0] >= 0 ? a.q_tc[0] : a.q_l2;
+            const double* R = a.thr + p * a.thr_stride + (int64_t)ql * a.M;
             int b = 0;
             while (b < a.M && s < R[b] * R[b] / a.w) ++b;
             if (a.binout) {
