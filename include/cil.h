@@ -261,6 +261,15 @@ CIL_API cil_status cil_diag_gram(const float* A, int64_t lda, int64_t N, const f
                                  int64_t Nt, cil_grid g, cil_engine engine, float* d2E, void* ws,
                                  size_t ws_bytes, void* stream);
 
+/* cil_diag_gram_family — DIAGNOSTIC: the three-phase INT8 engine (L2, W12SUM, W12 on tensor
+ * cores) on one set pair without binning: vE[k][i][j][0] = its FP32 value and vE[k][i][j][1]
+ * its error bound for kind k = 0: L2^2/w (unweighted sum of squares), 1: W12^2/w, 2: W12SUM/sqrt(w).
+ * vE [3][N][Nt][2] FP32 device; needs W >= 2 and K <= 65536; ws_bytes >=
+ * cil_features_workspace_size(1, N, Nt, g, CIL_L2|CIL_W12SUM|CIL_W12, 1, CIL_ENGINE_TC_I8) + 512.
+ * ------------------------------------------------------------------------ */
+CIL_API cil_status cil_diag_gram_family(const float* A, int64_t lda, int64_t N, const float* B, int64_t ldb,
+                                        int64_t Nt, cil_grid g, float* vE, void* ws, size_t ws_bytes, void* stream);
+
 /* ------------------------------------------------------------------------ */
 /* cil_diag_alu_ceiling — DIAGNOSTIC: measured issue ceiling of the CUDA-core engine's
  * inner-loop instruction mix (mix 0: FADD2+FMNMX3+FFMA2, 1: FADD2+FMNMX3, 2: FADD2+FFMA2)

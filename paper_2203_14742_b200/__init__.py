@@ -373,6 +373,22 @@ def diag_gram(A, B, grid, engine=ENGINE_TC_3XBF16, *, stream=None):
     return out
 
 
+def diag_gram_family(A, B, grid, *, stream=None):
+    """DIAGNOSTIC: the three-phase INT8 engine's FP32 values and bounds for every pair of one
+    set pair, shape [3, N, Nt, 2] for (L2^2/w, W12^2/w, W12SUM/sqrt(w)).  Not on the hot path."""
+    S, H, W = int(grid[0]), int(grid[1]), int(grid[2])
+    K = S * H * W
+    A2, B2 = A.reshape(A.shape[0], -1).contiguous(), B.reshape(B.shape[0], -1).contiguous()
+    N, Nt = A2.shape[0], B2.shape[0]
+    g = _grid(grid)
+    out = torch.empty((3, N, Nt, 2), dtype=torch.float32, device=A2.device)
+    nbytes = lib.cil_features_workspace_size(1, N, Nt, g, L2 | W12SUM | W12, 1, ENGINE_TC_I8) + 512
+    wbuf = _default_ws.get(nbytes, A2.device)
+    check(lib.cil_diag_gram_family(A2.data_ptr(), K, N, B2.data_ptr(), K, Nt, g, out.data_ptr(), wbuf.data_ptr(),
+                                   wbuf.numel(), _stream(stream)), "cil_diag_gram_family")
+    return out
+
+
 def last_launch_count() -> int:
     """Kernel launches issued by the last library call on this thread."""
     return int(lib.cil_last_launch_count())

@@ -313,7 +313,7 @@ cil_status run_engines(int P, const RowSrc& asrc, const RowSrc& bsrc, int64_t ro
         int q_tc[3] = {-1, -1, -1};
         if (pl.aug) {
             // ---- three-phase INT8 engine: L2, W12, W12SUM from the Grams of [x~ | D_x x~ | D_y x~]
-            if (binout || diag) return CIL_EUNSUPPORTED;
+            if (binout) return CIL_EUNSUPPORTED;
             for (int q = 0; q < sl.nq; ++q) {
                 if (sl.slot[q] == 0) q_tc[0] = q;
                 if (sl.slot[q] == 3) q_tc[1] = q;
@@ -350,6 +350,7 @@ cil_status run_engines(int P, const RowSrc& asrc, const RowSrc& bsrc, int64_t ro
             t.nrm3 = nrm; t.scl3 = q4;
             t.part = at<float>(ws, L.off_part);
             t.ih = (float)(1.0 / bp.h);
+            t.diag = diag;
             CIL_CU(launch_gram_i8(t, st));
         } else if (pl.split == 3) {
             // ---- INT8 two-digit engine (default): exact int32 accumulation
@@ -747,6 +748,34 @@ cil_status cil_diag_gram(const float* A, int64_t lda, int64_t N, const float* B,
     as.base = A; as.ld = lda; as.rows = N; as.mode = MODE_PLAIN;
     bs.base = B; bs.ld = ldb; bs.rows = Nt; bs.mode = MODE_PLAIN;
     return run_engines(1, as, bs, N, Nt, g, CIL_L2, sl, 1, pl, sp, L, wsa, r, 0, status, st, d2E);
+}
+
+cil_status cil_diag_gram_family(const float* A, int64_t lda, int64_t N, const float* B, int64_t ldb, int64_t Nt,
+                                cil_grid g, float* vE, void* ws, size_t ws_bytes, void* stream) {
+    t_launches = 0;
+    if (N < 1 || Nt < 1 || !A || !B || !vE || !ws) return CIL_EINVAL;
+    const uint32_t mask = CIL_L2 | CIL_W12SUM | CIL_W12;
+    if (check_grid(g, mask) != CIL_OK) return CIL_EINVAL;
+    const int64_t K = (int64_t)g.S * g.H * g.W;
+    if (lda < K || ldb < K) return CIL_EINVAL;
+    if (K % 4 || lda % 4 || ldb % 4 || !aligned16(A) || !aligned16(B)) return CIL_EUNSUPPORTED;
+    const Slots sl = slots_of(mask);
+    const int M = 1;
+    const Plan pl = make_plan(mask, CIL_ENGINE_TC_I8, g, Nt, Nt, M);
+    if (!pl.aug) return CIL_EUNSUPPORTED;
+    SegParams sp{N, Nt, 1, 1};
+    const Layout L = make_layout(1, N, Nt, g, sl.nq, M, pl, sp, 0);
+    if (ws_bytes < L.total + 512) return CIL_ENOMEM;
+    void* wsa = reinterpret_cast<void*>(((uintptr_t)ws + 255) & ~(uintptr_t)255);
+    double* r = at<double>(wsa, L.total);                 // one dummy radius per measure (not binned)
+    const double ones[3] = {1.0, 1.0, 1.0};
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    CIL_CU(cudaMemcpyAsync(r, ones, sizeof(ones), cudaMemcpyHostToDevice, st));
+    int32_t* status = reinterpret_cast<int32_t*>(r + 3);
+    RowSrc as{}, bs{};
+    as.base = A; as.ld = lda; as.rows = N; as.mode = MODE_PLAIN;
+    bs.base = B; bs.ld = ldb; bs.rows = Nt; bs.mode = MODE_PLAIN;
+    return run_engines(1, as, bs, N, Nt, g, mask, sl, M, pl, sp, L, wsa, r, 0, status, st, vE);
 }
 
 const char* cil_status_string(cil_status s) {

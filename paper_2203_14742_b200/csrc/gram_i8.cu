@@ -203,6 +203,14 @@ __device__ __forceinline__ void epilogue_aug(const I8Params& prm, uint32_t tmem_
                             v = r0 + (rx + ry) * ih;
                             e = e0 + (ex + ey) * ih + v * 2.4e-7f;
                         }
+                        if (prm.diag != nullptr) {        // diagnostics: (value, bound) per kind, item 0
+                            if (p == 0) {
+                                float* dg = prm.diag + (((int64_t)k * prm.rowsA + row) * prm.rowsB + hc0 + j) * 2;
+                                dg[0] = v;
+                                dg[1] = e;
+                            }
+                            continue;
+                        }
                         const float* T = s_T + k * 2 * MAXM;
                         const int b = bin_search<MAXM>(v + e, T);
                         if (SEG)

@@ -295,3 +295,55 @@ def test_c2_full_item_vs_oracle(cil, oracle_mod, engine):
     assert torch.equal(c1[0] + c2[0], c[1])
     yy = y.cpu().numpy()
     assert np.all((yy >= 0) & (yy <= 1)) and np.all(np.diff(yy, axis=-1) <= 0)
+
+
+# ------------------------------------------------------------------ L2-type family on tensor cores
+@pytest.mark.parametrize("engine", ["AUTO", "TC_I8"])
+def test_l2_family_tensor_cores_vs_oracle(cil, oracle_mod, engine):
+    """L2, W12SUM (7), W12 (8) on the three-phase INT8 engine: a C2-shaped
+    grid, 300 x 260 patterns (two column tiles, ragged), radii at dense quantiles of the pair
+    distances so that many pairs sit near a radius and go through the bound / re-check."""
+    O = oracle_mod
+    dev = torch.device("cuda")
+    grid = (2, 64, 64, 0.0)
+    A = cilgen.make_set(71, 0, 300, grid[:3])
+    B = cilgen.make_set(71, 1, 260, grid[:3])
+    mask = 0x0D
+    D = _sel(O.distance_matrix(A[:80].numpy(), B[:80].numpy(), grid, 0x3F), mask)
+    radii = np.array([np.quantile(d, np.linspace(0.97, 0.03, 15)) for d in D])
+    c, y, st = cil.features(A.to(dev), B.to(dev), grid, mask, torch.tensor(radii, device=dev),
+                            engine=_engine(cil, engine))
+    torch.cuda.synchronize()
+    assert int(st[0]) == 0
+    ref = O.features(A.numpy(), B.numpy(), grid, mask, radii, band=BAND)
+    _check_counts(c[0].cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("case", ["C2", "C4", "offset", "C1", "1D"])
+def test_gram_family_error_bound(cil, oracle_mod, case):
+    """The three-phase engine's values of L2^2/w, W12^2/w and W12SUM/sqrt(w) must stay well
+    inside their per-pair bounds (L2-type family on tensor cores)."""
+    O = oracle_mod
+    dev = torch.device("cuda")
+    if case == "C2":
+        grid, N, Nt, shift = (2, 64, 64, 0.0), 96, 300, 0.0
+    elif case == "C4":
+        grid, N, Nt, shift = (1, 128, 128, 0.0), 64, 200, 0.0
+    elif case == "C1":
+        grid, N, Nt, shift = (1, 32, 32, 0.0), 20, 20, 0.0
+    elif case == "1D":
+        grid, N, Nt, shift = (2, 1, 64, 0.0), 60, 90, 0.0
+    else:
+        grid, N, Nt, shift = (2, 32, 32, 0.0), 100, 300, 50.0
+    A = cilgen.make_set(33, 0, N, grid[:3]) + shift
+    B = cilgen.make_set(33, 1, Nt, grid[:3]) + shift
+    vE = cil.diag_gram_family(A.to(dev), B.to(dev), grid).cpu().numpy().astype(np.float64)
+    h = 1.0 / (grid[2] - 1)
+    w = h * h if grid[1] > 1 else h
+    D = O.distance_matrix(A.numpy(), B.numpy(), grid, 0x0D)        # L2, W12SUM, W12 (bit order)
+    exact = [D[0] ** 2 / w, D[2] ** 2 / w, D[1] / np.sqrt(w)]       # kinds 0 L2, 1 W12, 2 W12SUM
+    for k, name in enumerate(["L2", "W12", "W12SUM"]):
+        err = np.abs(vE[k, ..., 0] - exact[k])
+        ratio = err / vE[k, ..., 1]
+        print(f"{case} {name}: max err/E = {ratio.max():.3e}, median E/value = {np.median(vE[k, ..., 1] / exact[k]):.3e}")
+        assert ratio.max() < 0.25, name
