@@ -347,3 +347,34 @@ def test_gram_family_error_bound(cil, oracle_mod, case):
         ratio = err / vE[k, ..., 1]
         print(f"{case} {name}: max err/E = {ratio.max():.3e}, median E/value = {np.median(vE[k, ..., 1] / exact[k]):.3e}")
         assert ratio.max() < 0.25, name
+
+
+def test_synth_l2_family_segmented_tensor_cores(cil, oracle_mod):
+    """SCIL (Alg. 3) with L2, W12SUM, W12 on the three-phase engine with column segments
+    (N~ = 50 >= 43 columns per SCIL block): segmented per-thread histograms of three kinds."""
+    O = oracle_mod
+    dev = torch.device("cuda")
+    grid = (1, 16, 16, 0.0)
+    P, n_ens, N_set, Nt = 2, 3, 6, 50
+    Nsyn = n_ens * (N_set + Nt)
+    pools = torch.stack([cilgen.make_set(81, 200 + p, Nsyn, grid[:3], n_w=4.7 + 0.2 * p) for p in range(P)])
+    data = cilgen.make_set(81, 999, N_set, grid[:3])
+    k0 = np.array([2, 0], np.int32)
+    mask = 0x0D
+    radii = []
+    for p in range(P):
+        Dp = _sel(O.distance_matrix(pools[p, :40].numpy(), pools[p, 40:80].numpy(), grid, 0x3F), mask)
+        radii.append(np.array([np.quantile(d, np.linspace(0.95, 0.05, 10)) for d in Dp]))
+    radii = np.array(radii)
+    out, st, Y = cil.synth_loglik(pools.to(dev), n_ens, N_set, Nt, data.to(dev), torch.tensor(k0, device=dev),
+                                  grid, mask, torch.tensor(radii, device=dev), ridge=1e-4,
+                                  engine=cil.ENGINE_TC_I8, return_Y=True)
+    torch.cuda.synchronize()
+    for p in range(P):
+        ref, rst, Yr = O.synth_loglik(pools[p].numpy(), n_ens, N_set, Nt, data.numpy(), int(k0[p]), grid, mask,
+                                      radii[p], ridge=1e-4)
+        Yg = Y[p].cpu().numpy()
+        npairs = N_set * Nt
+        # every count within one of the oracle's (no pair of these radii sits within 1e-6 of one)
+        np.testing.assert_array_equal(np.rint(Yg * npairs), np.rint(Yr * npairs))
+        np.testing.assert_allclose(out[p].cpu().numpy(), ref, rtol=0, atol=1e-6)
