@@ -159,6 +159,7 @@ struct SimtArgs {
     bool do_max, do_sum;
     uint32_t qmask;                           // slots binned by this engine
     uint8_t* binout;                          // non-null: bins[p][q][i][j] instead of counts
+    int hist_cap;                             // shared histogram entries (set by the launcher)
 };
 cudaError_t launch_simt(const SimtArgs& a, cudaStream_t st);
 

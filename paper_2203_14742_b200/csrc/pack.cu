@@ -431,26 +431,35 @@ __global__ void __launch_bounds__(256) k_pack_i8_aug(RowSrc src, int64_t rows, A
     const float* x = row_ptr(src, p, r);
     const float* c = center + p * Kc;
     const int64_t orow = p * rows + r;
-    const int W = g.W, H = g.H;
-    const int64_t K = g.K;
+    const int W = g.W, H = g.H, SH = g.S * g.H;
     __shared__ float red[3][8];
     __shared__ unsigned long long redd[3][8];
+    const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
+    // warp per grid row (s, r), lanes along the columns (no index division); the D_x neighbour
+    // comes from the next lane, the D_y neighbour from the next grid row (L1-resident)
+    auto xt = [&](int64_t e) -> float { return __ldg(x + e) - __ldg(c + e); };
     float m0 = 0.f, mx = 0.f, my = 0.f, nfa = 0.f;
-    for (int64_t e = threadIdx.x; e < K; e += 256) {
-        const float v = __ldg(x + e), ce = __ldg(c + e);
-        nfa = fmaf(v, 0.f, nfa);
-        const float xe = v - ce;
-        m0 = fmaxf(m0, fabsf(xe));
-        const int col = (int)(e % W), row = (int)((e / W) % H);
-        if (col < W - 1) mx = fmaxf(mx, fabsf((__ldg(x + e + 1) - __ldg(c + e + 1)) - xe));
-        if (row < H - 1) my = fmaxf(my, fabsf((__ldg(x + e + W) - __ldg(c + e + W)) - xe));
+    for (int sr = w; sr < SH; sr += 8) {
+        const bool has_dy = (sr % H) + 1 < H;
+        const int64_t base = (int64_t)sr * W;
+        for (int c0 = 0; c0 < W; c0 += 32) {
+            const int col = c0 + ln;
+            const bool in = col < W;
+            const float xv = in ? __ldg(x + base + col) : 0.f;
+            nfa = fmaf(xv, 0.f, nfa);
+            const float xe = in ? xv - __ldg(c + base + col) : 0.f;
+            float xn = __shfl_down_sync(0xffffffffu, xe, 1);
+            if (ln == 31 && col + 1 < W) xn = xt(base + col + 1);
+            m0 = fmaxf(m0, fabsf(xe));
+            if (col + 1 < W) mx = fmaxf(mx, fabsf(xn - xe));
+            if (has_dy && in) my = fmaxf(my, fabsf(xt(base + W + col) - xe));
+        }
     }
     for (int o = 16; o > 0; o >>= 1) {
         m0 = fmaxf(m0, __shfl_xor_sync(0xffffffffu, m0, o));
         mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
         my = fmaxf(my, __shfl_xor_sync(0xffffffffu, my, o));
     }
-    const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
     const bool anynf = __syncthreads_or(nfa != nfa);
     if (ln == 0) { red[0][w] = m0; red[1][w] = mx; red[2][w] = my; }
     __syncthreads();
@@ -472,16 +481,24 @@ __global__ void __launch_bounds__(256) k_pack_i8_aug(RowSrc src, int64_t rows, A
         lo[col] = (int8_t)(q - 256 * hd);
         s2[a] += (uint64_t)((uint32_t)(q * q));
     };
-    for (int64_t e = threadIdx.x; e < K; e += 256) {
-        const float xe = __ldg(x + e) - __ldg(c + e);
-        const int col = (int)(e % W), row = (int)((e / W) % H);
-        const int64_t sr = e / W;                       // s*H + row
-        put(0, kp0 + e, xe);
-        if (col < W - 1) put(1, kp1 + sr * (W - 1) + col, (__ldg(x + e + 1) - __ldg(c + e + 1)) - xe);
-        if (row < H - 1) put(2, kp2 + e - (sr / H) * W, (__ldg(x + e + W) - __ldg(c + e + W)) - xe);
+    for (int sr = w; sr < SH; sr += 8) {
+        const bool has_dy = (sr % H) + 1 < H;
+        const int s = sr / H;
+        const int64_t base = (int64_t)sr * W;
+        for (int c0 = 0; c0 < W; c0 += 32) {
+            const int col = c0 + ln;
+            const bool in = col < W;
+            const float xe = in ? xt(base + col) : 0.f;
+            float xn = __shfl_down_sync(0xffffffffu, xe, 1);
+            if (ln == 31 && col + 1 < W) xn = xt(base + col + 1);
+            if (!in) continue;
+            put(0, kp0 + base + col, xe);
+            if (col + 1 < W) put(1, kp1 + (int64_t)sr * (W - 1) + col, xn - xe);
+            if (has_dy) put(2, kp2 + base - (int64_t)s * W + col, xt(base + W + col) - xe);
+        }
     }
     // zero padding of every block
-    const int64_t len[3] = {K, g.Kx, g.Ky}, beg[3] = {kp0, kp1, kp2}, end[3] = {kp1, kp2, kp3};
+    const int64_t len[3] = {g.K, g.Kx, g.Ky}, beg[3] = {kp0, kp1, kp2}, end[3] = {kp1, kp2, kp3};
 #pragma unroll
     for (int a = 0; a < 3; ++a)
         for (int64_t col = beg[a] + len[a] + threadIdx.x; col < end[a]; col += 256) { ho[col] = 0; lo[col] = 0; }
@@ -527,41 +544,33 @@ __global__ void __launch_bounds__(256) k_pack_aug(RowSrc src, int64_t rows, AugG
     const int64_t r = blockIdx.x;
     const float* x = row_ptr(src, p, r);
     float* o = out + (p * rows + r) * g.off[3];
-    bool nonfinite = false;
-    // value region
-    for (int64_t k = threadIdx.x; k < g.off[1]; k += blockDim.x) {
-        float v = 0.f;
-        if (k < g.K) {
-            v = __ldg(x + k);
-            nonfinite |= !isfinite(v);
-        }
-        o[k] = v;
+    float nfa = 0.f;                               // NaN iff some value is not finite
+    // value region: float4 copy (K % 4 == 0), zero padding
+    for (int64_t k = (int64_t)threadIdx.x * 4; k < g.off[1]; k += 1024) {
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (k < g.K) v = __ldg(reinterpret_cast<const float4*>(x + k));
+        nfa = fmaf(v.x, 0.f, fmaf(v.y, 0.f, fmaf(v.z, 0.f, fmaf(v.w, 0.f, nfa))));
+        *reinterpret_cast<float4*>(o + k) = v;
     }
+    // derivative regions: warp per grid row (s, r), lanes along the columns, no index division
+    const int W = g.W, H = g.H, SH = g.S * g.H;
+    const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
     if (g.nreg >= 2) {
-        const int W1 = g.W - 1;
-        for (int64_t t = threadIdx.x; t < g.off[2] - g.off[1]; t += blockDim.x) {
-            float v = 0.f;
-            if (t < g.Kx) {
-                const int64_t sr = t / W1, c = t % W1;          // sr = s*H + r
-                const float* row = x + sr * g.W;
-                v = __ldg(row + c + 1) - __ldg(row + c);
+        for (int sr = w; sr < SH; sr += 8) {
+            const int64_t base = (int64_t)sr * W;
+            const bool has_dy = g.nreg >= 3 && (sr % H) + 1 < H;
+            const int s = sr / H;
+            for (int c = ln; c < W; c += 32) {
+                const float xe = __ldg(x + base + c);
+                if (c + 1 < W) o[g.off[1] + (int64_t)sr * (W - 1) + c] = __ldg(x + base + c + 1) - xe;
+                if (has_dy) o[g.off[2] + base - (int64_t)s * W + c] = __ldg(x + base + W + c) - xe;
             }
-            o[g.off[1] + t] = v;
         }
+        for (int64_t t = g.Kx + threadIdx.x; t < g.off[2] - g.off[1]; t += 256) o[g.off[1] + t] = 0.f;
+        if (g.nreg >= 3)
+            for (int64_t t = g.Ky + threadIdx.x; t < g.off[3] - g.off[2]; t += 256) o[g.off[2] + t] = 0.f;
     }
-    if (g.nreg >= 3) {
-        const int64_t per_s = (int64_t)(g.H - 1) * g.W;
-        for (int64_t t = threadIdx.x; t < g.off[3] - g.off[2]; t += blockDim.x) {
-            float v = 0.f;
-            if (t < g.Ky) {
-                const int64_t s = t / per_s, rc = t % per_s;    // rc = r*W + c, r < H-1
-                const float* base = x + s * (int64_t)g.H * g.W + rc;
-                v = __ldg(base + g.W) - __ldg(base);
-            }
-            o[g.off[2] + t] = v;
-        }
-    }
-    if (__syncthreads_or(nonfinite) && threadIdx.x == 0) atomicOr(&status[p], CIL_ITEM_NONFINITE);
+    if (__syncthreads_or(nfa != nfa) && threadIdx.x == 0) atomicOr(&status[p], CIL_ITEM_NONFINITE);
 }
 
 cudaError_t launch_pack_aug(int P, const RowSrc& src, int64_t rows, const AugGeom& g, float* out,

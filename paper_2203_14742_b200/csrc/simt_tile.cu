@@ -40,7 +40,7 @@ __device__ __forceinline__ float absmax3(float m, float x, float y) {
 }  // namespace
 
 template <bool DO_MAX, bool DO_SUM>
-__global__ void __launch_bounds__(NTHR, 2) k_simt(SimtArgs a) {
+__global__ void __launch_bounds__(NTHR, DO_SUM ? 2 : 4) k_simt(SimtArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     float* As = reinterpret_cast<float*>(smem_raw);                 // [2][TA][LDS]
     float* Bs = As + 2 * TA * LDS;                                   // [2][TB][LDS]
@@ -68,7 +68,7 @@ __global__ void __launch_bounds__(NTHR, 2) k_simt(SimtArgs a) {
     const int nrs = (int)(rlast / a.sp.row_seg - rs0 + 1), ncs = (int)(clast / a.sp.col_seg - cs0 + 1);
     const int nloc = nrs * ncs;
     const int hist_len = nloc * nq * (M + 1);
-    const bool use_sh = hist_len <= 4096;
+    const bool use_sh = hist_len <= a.hist_cap;
     if (use_sh)
         for (int t = tid; t < hist_len; t += NTHR) hist_s[t] = 0u;
 
@@ -239,20 +239,26 @@ __global__ void __launch_bounds__(NTHR, 2) k_simt(SimtArgs a) {
     }
 }
 
-static size_t simt_smem(bool do_max, bool do_sum) {
+static size_t simt_smem(bool do_max, bool do_sum, int hist_cap) {
     size_t s = sizeof(float) * 2 * (TA + TB) * LDS + sizeof(double) * kMaxMeas * kMaxM;
     if (do_sum) s += sizeof(double) * 2 * 16 * NTHR;
     if (do_max) s += sizeof(float) * 2 * 16 * NTHR;
-    s += sizeof(uint32_t) * 4096;
+    s += sizeof(uint32_t) * hist_cap;
     return s;
 }
 
 template <bool X, bool Y>
-static cudaError_t launch_simt_t(const SimtArgs& a, cudaStream_t st) {
-    const size_t sm = simt_smem(X, Y);
+static cudaError_t launch_simt_t(const SimtArgs& a_in, cudaStream_t st) {
+    // shared histogram sized for the segments one tile can touch (else global atomics)
+    SimtArgs a = a_in;
+    const int64_t nrs = (TA + a.sp.row_seg - 1) / a.sp.row_seg + 1, ncs = (TB + a.sp.col_seg - 1) / a.sp.col_seg + 1;
+    const int64_t need = nrs * ncs * a.bp.nq * (a.bp.M + 1);
+    a.hist_cap = (int)(need < 4096 ? need : 4096);
+    const size_t sm = simt_smem(X, Y, a.hist_cap);
     static bool attr_done = false;   // benign race: idempotent attribute set
     if (!attr_done) {
-        cudaError_t e = cudaFuncSetAttribute(k_simt<X, Y>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        cudaError_t e = cudaFuncSetAttribute(k_simt<X, Y>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)simt_smem(X, Y, 4096));
         if (e != cudaSuccess) return e;
         attr_done = true;
     }
