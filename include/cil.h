@@ -184,6 +184,25 @@ CIL_API cil_status cil_synth_loglik(int32_t P, const float* pools, int64_t pool_
                             cil_engine engine, void* ws, size_t ws_bytes, void* stream);
 
 /* ------------------------------------------------------------------------ */
+/* cil_train_vectors — the training vectors of Alg. 1 (CIL) and Alg. 2
+ * (MCIL): for item p the set X_p (n_ens*N patterns at X + p*stride, row
+ * stride ld) is divided into the subsets s^k = rows [kN, (k+1)N) (step 1), and for the
+ * C(n_ens, 2) unordered subset pairs k < l (reading R15)
+ *   Y[p][v][q*M + m] = C(R_p,q,m, s^k, s^l) = #{(i,j) : d_q(s^k_i, s^l_j) < R} / N^2   (Eq. (1))
+ * with v the index of (k, l) in lexicographic order (v = 0 for (0,1), 1 for (0,2), ...).
+ * mu_0, Sigma_0 (step 3) are cil_stats of the n_ens*(n_ens-1)/2 vectors of an item.
+ * radii [P or shared][n_meas][M] (radii_stride 0 = shared); Y [P][n_ens(n_ens-1)/2][n_meas*M]
+ * FP64 device.  Engines as cil_features (AUTO: INT8 tensor cores for the L2-type family when
+ * N >= 43 columns per subset, else CUDA cores / 3xBF16).
+ * ------------------------------------------------------------------------ */
+CIL_API size_t cil_train_workspace_size(int32_t P, int32_t n_ens, int32_t N, cil_grid g, uint32_t dist_mask,
+                                        int32_t M, cil_engine engine);
+CIL_API cil_status cil_train_vectors(int32_t P, const float* X, int64_t stride, int64_t ld, int32_t n_ens,
+                                     int32_t N, cil_grid g, uint32_t dist_mask, const double* radii,
+                                     int64_t radii_stride, int32_t M, double* Y, int32_t* item_status,
+                                     cil_engine engine, void* ws, size_t ws_bytes, void* stream);
+
+/* ------------------------------------------------------------------------ */
 /* Bootstrap estimators (Alg. A1 / A2).  The
  * resampled sets of the bootstrap are drawn WITH repetition from fixed sets, so every
  * distance they need is a distance between two patterns of the fixed sets: the library

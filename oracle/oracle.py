@@ -232,3 +232,24 @@ def synth_boot(pool, data, N_set, I1, I2, J, grid, mask, radii, ridge=0.0, nthre
     if st < 0:
         raise ValueError("oracle_synth_boot: invalid arguments or index out of range")
     return out, st, Y
+
+
+def train_vectors(X, n_ens, grid, mask, radii, band: float = 1e-6, nthreads: int | None = None):
+    """Alg. 1 / Alg. 2 steps 1-2: divide X into n_ens subsets of
+    N = len(X) / n_ens rows (step 1); for every unordered pair k < l (lexicographic order,
+    C(n_ens, 2) realisations) the correlation-integral vector of (s^k, s^l) by
+    Eq. (1) (step 2).  Returns dict counts / lo / hi [n_pairs][nq][M], y [n_pairs][nq*M]."""
+    S, H, W, h = grid
+    K = S * H * W
+    X2 = _rows(X, K)
+    N = X2.shape[0] // n_ens
+    out = {"counts": [], "lo": [], "hi": [], "y": []}
+    for k in range(n_ens):
+        for l in range(k + 1, n_ens):
+            r = features(X2[k * N:(k + 1) * N], X2[l * N:(l + 1) * N], grid, mask, radii, band=band,
+                         nthreads=nthreads)
+            out["counts"].append(r["counts"])
+            out["lo"].append(r["lo"])
+            out["hi"].append(r["hi"])
+            out["y"].append(r["y"].ravel())
+    return {k: np.array(v) for k, v in out.items()}

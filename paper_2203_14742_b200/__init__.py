@@ -30,7 +30,7 @@ ITEM_OK, ITEM_NONFINITE, ITEM_NOTPD, ITEM_BADRADII, ITEM_OVERFLOW, ITEM_BADINDEX
 
 __all__ = ["features", "stats", "loglik", "synth_loglik", "features_workspace_size",
            "synth_workspace_size", "n_measures", "Workspace", "CilError", "bin_matrix", "resample_counts",
-           "synth_loglik_boot", "mcil_boot_stats"]
+           "synth_loglik_boot", "mcil_boot_stats", "train_vectors", "gaussianity_chi2"]
 
 
 def n_measures(mask: int) -> int:
@@ -371,6 +371,55 @@ def diag_gram(A, B, grid, engine=ENGINE_TC_3XBF16, *, stream=None):
     check(lib.cil_diag_gram(A2.data_ptr(), K, N, B2.data_ptr(), K, Nt, g, engine, out.data_ptr(),
                             wbuf.data_ptr(), wbuf.numel(), _stream(stream)), "cil_diag_gram")
     return out
+
+
+def train_vectors(X, n_ens, grid, mask, radii, *, engine=ENGINE_AUTO, stream=None, ws: Workspace | None = None,
+                  status=None):
+    """Training vectors of Alg. 1 / Alg. 2: X [n_ens*N, S,H,W] or
+    [P, n_ens*N, S,H,W] float32, divided into n_ens subsets of N rows; returns
+    Y [P, n_ens(n_ens-1)/2, n_meas*M] for the subset pairs k < l (lexicographic) and item_status."""
+    S, H, W = int(grid[0]), int(grid[1]), int(grid[2])
+    K = S * H * W
+    X3 = _as_items(X, K)
+    P, rows = X3.shape[0], X3.shape[1]
+    if rows % n_ens:
+        raise ValueError("rows must be n_ens * N")
+    N = rows // n_ens
+    nq = n_measures(mask)
+    radii, M, rstride = _radii_arg(radii, P, nq)
+    dev = X3.device
+    nv = n_ens * (n_ens - 1) // 2
+    Y = torch.empty((P, nv, nq * M), dtype=torch.float64, device=dev)
+    if status is None:
+        status = torch.empty((P,), dtype=torch.int32, device=dev)
+    g = _grid(grid)
+    nbytes = lib.cil_train_workspace_size(P, n_ens, N, g, mask, M, engine)
+    if nbytes == 0:
+        raise CilError("cil_train_workspace_size: invalid arguments")
+    wbuf = (ws or _default_ws).get(nbytes, dev)
+    check(lib.cil_train_vectors(P, X3.data_ptr(), X3.stride(0), X3.stride(1), n_ens, N, g, mask, radii.data_ptr(),
+                                rstride, M, Y.data_ptr(), status.data_ptr(), engine, wbuf.data_ptr(), wbuf.numel(),
+                                _stream(stream)), "cil_train_vectors")
+    return Y, status
+
+
+def gaussianity_chi2(Y, *, bins: int = 10, ridge: float = 0.0, stream=None):
+    """Numerical Gaussianity check of CIL vectors: the squared Mahalanobis
+    distances d_k^2 = (y_k - mu)^T Sigma^-1 (y_k - mu) of the n vectors (cil_stats + cil_loglik,
+    on the device) against the chi^2_D distribution: Pearson's statistic over `bins`
+    equiprobable chi^2_D bins.  Returns (statistic, degrees of freedom, d2 [n])."""
+    from scipy import stats as _sps          # host-side: quantiles of chi^2_D only
+    Y2 = Y.to(torch.float64).contiguous()
+    n, D = Y2.shape
+    mu, Sig = stats(Y2, stream=stream)
+    out, _ = loglik(mu, Sig, Y2, ridge, stream=stream)
+    d2 = out[:, 0].cpu().numpy()
+    edges = _sps.chi2.ppf([i / bins for i in range(1, bins)], D)
+    import numpy as _np
+    counts = _np.bincount(_np.searchsorted(edges, d2), minlength=bins)
+    expect = n / bins
+    stat = float(((counts - expect) ** 2 / expect).sum())
+    return stat, bins - 1, d2
 
 
 def diag_gram_family(A, B, grid, *, stream=None):

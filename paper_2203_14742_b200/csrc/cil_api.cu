@@ -568,6 +568,47 @@ cil_status cil_synth_loglik(int32_t P, const float* pools, int64_t pool_stride, 
     return CIL_OK;
 }
 
+// ------------------------------------------------------------------ Alg. 1 / Alg. 2 training vectors
+size_t cil_train_workspace_size(int32_t P, int32_t n_ens, int32_t N, cil_grid g, uint32_t dist_mask, int32_t M,
+                                cil_engine engine) {
+    if (P < 1 || n_ens < 2 || N < 1 || M < 1 || check_grid(g, dist_mask) != CIL_OK) return 0;
+    const Slots sl = slots_of(dist_mask);
+    const int64_t rows = (int64_t)n_ens * N;
+    const Plan pl = make_plan(dist_mask, engine, g, N, rows, M);
+    SegParams sp{N, N, n_ens, n_ens};
+    return make_layout(P, rows, rows, g, sl.nq, M, pl, sp, 0).total;
+}
+
+cil_status cil_train_vectors(int32_t P, const float* X, int64_t stride, int64_t ld, int32_t n_ens, int32_t N,
+                             cil_grid g, uint32_t dist_mask, const double* radii, int64_t radii_stride, int32_t M,
+                             double* Y, int32_t* item_status, cil_engine engine, void* ws, size_t ws_bytes,
+                             void* stream) {
+    t_launches = 0;
+    if (P < 1 || n_ens < 2 || N < 1 || M < 1 || M > kMaxM) return CIL_EINVAL;
+    if (check_grid(g, dist_mask) != CIL_OK) return CIL_EINVAL;
+    if ((int)engine < 0 || (int)engine > 4) return CIL_EINVAL;
+    if (!X || !radii || !Y || !item_status || !ws || radii_stride < 0 || stride < 0) return CIL_EINVAL;
+    const int64_t K = (int64_t)g.S * g.H * g.W;
+    const int64_t rows = (int64_t)n_ens * N;
+    if (ld < K || (P > 1 && stride < (rows - 1) * ld + K)) return CIL_EINVAL;
+    if (K % 4 || ld % 4 || stride % 4 || !aligned16(X)) return CIL_EUNSUPPORTED;
+    const Slots sl = slots_of(dist_mask);
+    const Plan pl = make_plan(dist_mask, engine, g, N, rows, M);
+    SegParams sp{N, N, n_ens, n_ens};
+    const Layout L = make_layout(P, rows, rows, g, sl.nq, M, pl, sp, 0);
+    if (ws_bytes < L.total) return CIL_ENOMEM;
+    void* wsa = reinterpret_cast<void*>(((uintptr_t)ws + 255) & ~(uintptr_t)255);
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    RowSrc xs{};
+    xs.base = X; xs.stride = stride; xs.ld = ld; xs.rows = rows; xs.mode = MODE_PLAIN;
+    // one panel against itself, segmented by subset: block (k, l) = C(R, s^k, s^l)
+    cil_status s = run_engines(P, xs, xs, rows, rows, g, dist_mask, sl, M, pl, sp, L, wsa, radii, radii_stride,
+                               item_status, st);
+    if (s != CIL_OK) return s;
+    CIL_CU(launch_build_pairs(P, n_ens, sl.nq, M, sp, at<uint64_t>(wsa, L.off_hist), N, Y, st));
+    return CIL_OK;
+}
+
 // ------------------------------------------------------------------ bootstrap (Alg. A1 / A2)
 static cil_status check_sets(int32_t P, const float* A, int64_t strideA, int64_t lda, int64_t N, const float* B,
                              int64_t strideB, int64_t ldb, int64_t Nt, const cil_grid& g) {

@@ -261,6 +261,8 @@ cudaError_t launch_check_index(int P, const int32_t* idx, int64_t per_item, int6
 cudaError_t launch_resample(int P, const uint8_t* bins, int64_t N, int64_t Nt, int nq, int M, int n_rep,
                             const int32_t* I1, int64_t n1, const int32_t* I2, int64_t n2, uint64_t* counts,
                             double* y, int64_t y_item_stride, int32_t* status, cudaStream_t st);
+cudaError_t launch_build_pairs(int P, int n_ens, int nq, int M, const SegParams& sp, const uint64_t* hist,
+                               int64_t N, double* Y, cudaStream_t st);
 cudaError_t launch_boot_tail(int P, int n_rep, int D, double ridge, double* out, int32_t* status, double* Y,
                              double* mu, double* Sigma, cudaStream_t st);
 cudaError_t launch_loglik(int P, const double* mu, int64_t mu_stride, const double* Sigma,

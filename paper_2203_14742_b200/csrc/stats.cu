@@ -310,4 +310,33 @@ cudaError_t launch_boot_tail(int P, int n_rep, int D, double ridge, double* out,
                                  D, ridge, out, status, status, st);
 }
 
+// Alg. 1 / Alg. 2 training vectors: Y[p][v][q*M + m] for the unordered subset pairs k < l
+// (lexicographic v), counts of segment (rs = k, cs = l) divided by N*N.
+__global__ void k_build_pairs(int n_ens, int nq, int M, SegParams sp, const uint64_t* __restrict__ hist,
+                              double npairs, double* __restrict__ Y) {
+    const int p = blockIdx.y;
+    const int v = blockIdx.x;
+    int k = 0, rem = v;
+    while (rem >= n_ens - 1 - k) { rem -= n_ens - 1 - k; ++k; }
+    const int l = k + 1 + rem;
+    const int D = nq * M;
+    const int nv = n_ens * (n_ens - 1) / 2;
+    for (int t = threadIdx.x; t < D; t += blockDim.x) {
+        const int q = t / M, m = t % M;
+        uint64_t c = 0;
+        for (int b = m + 1; b <= M; ++b) c += hist[hist_index(sp, nq, M, p, k, l, q, b)];
+        Y[((int64_t)p * nv + v) * D + t] = (double)c / npairs;
+    }
+}
+
+cudaError_t launch_build_pairs(int P, int n_ens, int nq, int M, const SegParams& sp, const uint64_t* hist,
+                               int64_t N, double* Y, cudaStream_t st) {
+    const int nv = n_ens * (n_ens - 1) / 2;
+    dim3 g((unsigned)nv, (unsigned)P);
+    ProfScope ps_(K_TAIL, st);
+    k_build_pairs<<<g, 128, 0, st>>>(n_ens, nq, M, sp, hist, (double)N * (double)N, Y);
+    note_launch();
+    return cudaGetLastError();
+}
+
 }  // namespace cil

@@ -378,3 +378,44 @@ def test_synth_l2_family_segmented_tensor_cores(cil, oracle_mod):
         # every count within one of the oracle's (no pair of these radii sits within 1e-6 of one)
         np.testing.assert_array_equal(np.rint(Yg * npairs), np.rint(Yr * npairs))
         np.testing.assert_allclose(out[p].cpu().numpy(), ref, rtol=0, atol=1e-6)
+
+
+@pytest.mark.parametrize("engine,N,mask", [("AUTO", 50, 0x3F), ("AUTO", 12, 0x0D), ("SIMT", 20, 0x3F),
+                                           ("TC_3XBF16", 30, 0x01), ("TC_I8", 60, 0x01)])
+def test_train_vectors_vs_oracle(cil, oracle_mod, engine, N, mask):
+    """Alg. 1 / Alg. 2 training vectors: one panel against itself, segmented by subset, the
+    k < l blocks (triangle) in lexicographic order, against the oracle's per-pair counts."""
+    O = oracle_mod
+    dev = torch.device("cuda")
+    grid = (1, 16, 16, 0.0)
+    n_ens, P = 5, 2
+    X = torch.stack([cilgen.make_set(91, p, n_ens * N, grid[:3]) for p in range(P)])
+    sel = [q for q in range(6) if (mask >> q) & 1]
+    D = O.distance_matrix(X[0, :40].numpy(), X[0, 40:80].numpy(), grid, mask)
+    radii = np.array([np.quantile(d, np.linspace(0.95, 0.05, 9)) for d in D])
+    Y, st = cil.train_vectors(X.to(dev), n_ens, grid, mask, torch.tensor(radii, device=dev),
+                              engine=_engine(cil, engine))
+    torch.cuda.synchronize()
+    assert Y.shape == (P, n_ens * (n_ens - 1) // 2, len(sel) * 9)
+    for p in range(P):
+        ref = O.train_vectors(X[p].numpy(), n_ens, grid, mask, radii, band=BAND)
+        c = np.rint(Y[p].cpu().numpy() * N * N).astype(np.int64).reshape(ref["lo"].shape)
+        assert np.all(ref["lo"] <= c) and np.all(c <= ref["hi"]), f"item {p}"
+
+
+def test_gaussianity_chi2(cil, oracle_mod):
+    """The chi^2 Gaussianity diagnostic: Mahalanobis distances of the vectors
+    from the device match the oracle's quad for each vector; Gaussian samples pass the test."""
+    O = oracle_mod
+    dev = torch.device("cuda")
+    rng = np.random.default_rng(3)
+    D, n = 8, 400
+    L = rng.standard_normal((D, D)) * 0.3 + np.eye(D)
+    Y = rng.standard_normal((n, D)) @ L.T + 0.5
+    stat, dof, d2 = cil.gaussianity_chi2(torch.tensor(Y, device=dev))
+    mu, Sig = O.stats(Y)
+    for k in range(0, n, 37):
+        out, st = O.loglik(mu, Sig, Y[k])
+        assert d2[k] == pytest.approx(out[0], rel=1e-9)
+    from scipy import stats as sps
+    assert sps.chi2.sf(stat, dof) > 1e-4           # Gaussian data: no rejection at any sane level

@@ -299,3 +299,23 @@ def test_nonfinite_status(oracle_mod):
     B[1, 0, 2, 2] = np.nan
     r = oracle_mod.features(A, B, (1, 4, 4, 0.0), 1, [[10.0, 1.0]])
     assert r["status"] == 1
+
+
+def test_train_vectors_vs_brute(oracle_mod):
+    """Alg. 1 steps 1-2: the C(n_ens,2) subset-pair vectors in lexicographic (k, l) order equal
+    the brute-force counts of each pair of subsets."""
+    O = oracle_mod
+    grid = (2, 4, 5, 0.0)
+    n_ens, N = 4, 5
+    X = cilgen.make_patterns(12, 0, n_ens * N, grid[:3]).numpy()
+    Db = brute.distances(X, X, grid)
+    radii = np.array([np.quantile(Db[q][Db[q] > 0], np.linspace(0.9, 0.1, 5)) for q in range(6)])
+    r = O.train_vectors(X, n_ens, grid, ALL, radii, band=0.0)
+    assert r["counts"].shape[0] == n_ens * (n_ens - 1) // 2
+    v = 0
+    for k in range(n_ens):
+        for l in range(k + 1, n_ens):
+            want = brute.counts(X[k * N:(k + 1) * N], X[l * N:(l + 1) * N], grid, ALL, radii)
+            np.testing.assert_array_equal(r["counts"][v], want)
+            v += 1
+    np.testing.assert_allclose(r["y"], r["counts"].reshape(v, -1) / (N * N), rtol=0, atol=0)
