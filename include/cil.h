@@ -184,6 +184,28 @@ CIL_API cil_status cil_synth_loglik(int32_t P, const float* pools, int64_t pool_
                             cil_engine engine, void* ws, size_t ws_bytes, void* stream);
 
 /* ------------------------------------------------------------------------ */
+/* Adaptive radii: "R_0 (resp. R_M) the maximum (resp.
+ * minimum) distance of any two patterns", then the power law R_m = R_0 b^-m with
+ * R_M / R_0 = b^-M, or the linear law R_m = R_0 - m (R_0 - R_M)/M, m = 1..M.
+ *
+ * cil_distance_range — range[p][q][0] = min over pairs (i, j) of d_q(A_p,i, B_p,j) among the
+ * positive distances (a pattern against itself is not a pair of two patterns; reading R16),
+ * range[p][q][1] = the maximum; FP64, from the exact per-pair measures of the CUDA-core
+ * engine (FP32 differences, FP64 sums).  Arguments as cil_features (strides may be 0);
+ * range [P][n_meas][2] FP64 device.
+ * cil_radii_from_range — radii[p][q][m-1] from range with R_0 = max (1 + margin),
+ * R_M = min (1 - margin) (reading R5; margin in [0, 1)); law 0 = power, 1 = linear; an
+ * item without a positive distance gets CIL_ITEM_BADRADII and NaN radii.
+ * ------------------------------------------------------------------------ */
+CIL_API size_t cil_range_workspace_size(int32_t P, int64_t N, int64_t Nt, cil_grid g, uint32_t dist_mask);
+CIL_API cil_status cil_distance_range(int32_t P, const float* A, int64_t strideA, int64_t lda, int64_t N,
+                                      const float* B, int64_t strideB, int64_t ldb, int64_t Nt, cil_grid g,
+                                      uint32_t dist_mask, double* range, int32_t* item_status, void* ws,
+                                      size_t ws_bytes, void* stream);
+CIL_API cil_status cil_radii_from_range(int32_t P, int32_t n_meas, int32_t M, const double* range, int32_t law,
+                                        double margin, double* radii, int32_t* item_status, void* stream);
+
+/* ------------------------------------------------------------------------ */
 /* cil_train_vectors — the training vectors of Alg. 1 (CIL) and Alg. 2
  * (MCIL): for item p the set X_p (n_ens*N patterns at X + p*stride, row
  * stride ld) is divided into the subsets s^k = rows [kN, (k+1)N) (step 1), and for the

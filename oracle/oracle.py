@@ -253,3 +253,33 @@ def train_vectors(X, n_ens, grid, mask, radii, band: float = 1e-6, nthreads: int
             out["hi"].append(r["hi"])
             out["y"].append(r["y"].ravel())
     return {k: np.array(v) for k, v in out.items()}
+
+
+def distance_range(A, B, grid, mask):
+    """(min positive, max) distance of every selected measure over all pairs (PAPER.md:109, 246;
+    a pattern against itself is excluded from the minimum, reading R16).  Tiny inputs."""
+    D = distance_matrix(A, B, grid, mask)
+    out = np.zeros((D.shape[0], 2))
+    for q in range(D.shape[0]):
+        d = D[q].ravel()
+        pos = d[d > 0]
+        out[q, 0] = pos.min() if pos.size else np.inf
+        out[q, 1] = d.max()
+    return out
+
+
+def radii_from_range(rng, M, law: str = "power", margin: float = 1e-3):
+    """R_0 = max (1 + margin), R_M = min (1 - margin) [R5]; power law
+    R_m = R_0 b^-m with R_M / R_0 = b^-M, or linear R_m = R_0 - m h with h = (R_0 - R_M)/M,
+    m = 1..M."""
+    rng = np.asarray(rng, np.float64)
+    out = np.zeros((rng.shape[0], M))
+    for q in range(rng.shape[0]):
+        R0, RM = rng[q, 1] * (1 + margin), rng[q, 0] * (1 - margin)
+        for m in range(1, M + 1):
+            if law == "power":
+                b = (R0 / RM) ** (1.0 / M)
+                out[q, m - 1] = R0 * b ** (-m)
+            else:
+                out[q, m - 1] = R0 - m * (R0 - RM) / M
+    return out

@@ -30,7 +30,8 @@ ITEM_OK, ITEM_NONFINITE, ITEM_NOTPD, ITEM_BADRADII, ITEM_OVERFLOW, ITEM_BADINDEX
 
 __all__ = ["features", "stats", "loglik", "synth_loglik", "features_workspace_size",
            "synth_workspace_size", "n_measures", "Workspace", "CilError", "bin_matrix", "resample_counts",
-           "synth_loglik_boot", "mcil_boot_stats", "train_vectors", "gaussianity_chi2"]
+           "synth_loglik_boot", "mcil_boot_stats", "train_vectors", "gaussianity_chi2",
+           "distance_range", "radii_from_range"]
 
 
 def n_measures(mask: int) -> int:
@@ -371,6 +372,44 @@ def diag_gram(A, B, grid, engine=ENGINE_TC_3XBF16, *, stream=None):
     check(lib.cil_diag_gram(A2.data_ptr(), K, N, B2.data_ptr(), K, Nt, g, engine, out.data_ptr(),
                             wbuf.data_ptr(), wbuf.numel(), _stream(stream)), "cil_diag_gram")
     return out
+
+
+def distance_range(A, B, grid, mask, *, stream=None, ws: Workspace | None = None, status=None):
+    """[P, n_meas, 2] FP64: (min positive, max) distance over all pairs of each set pair
+    (PAPER.md:109, 246).  A, B as in features (a 4-D A with 5-D B is shared)."""
+    S, H, W = int(grid[0]), int(grid[1]), int(grid[2])
+    K = S * H * W
+    shareA = A.dim() in (2, 4) and B.dim() in (3, 5)
+    A3, B3 = _as_items(A, K), _as_items(B, K)
+    P = B3.shape[0] if shareA else A3.shape[0]
+    N, Nt = A3.shape[1], B3.shape[1]
+    nq = n_measures(mask)
+    dev = B3.device
+    rng = torch.empty((P, nq, 2), dtype=torch.float64, device=dev)
+    if status is None:
+        status = torch.empty((P,), dtype=torch.int32, device=dev)
+    g = _grid(grid)
+    nbytes = lib.cil_range_workspace_size(P, N, Nt, g, mask)
+    if nbytes == 0:
+        raise CilError("cil_range_workspace_size: invalid arguments")
+    wbuf = (ws or _default_ws).get(nbytes, dev)
+    check(lib.cil_distance_range(P, _ptr(A3), 0 if shareA else A3.stride(0), A3.stride(1), N, _ptr(B3), B3.stride(0),
+                                 B3.stride(1), Nt, g, mask, rng.data_ptr(), status.data_ptr(), wbuf.data_ptr(),
+                                 wbuf.numel(), _stream(stream)), "cil_distance_range")
+    return rng, status
+
+
+def radii_from_range(rng, M, law: str = "power", margin: float = 1e-3, *, stream=None, status=None):
+    """Radii [P, n_meas, M] from a distance range: power law R_0 b^-m or linear
+    R_0 - m h, R_0 = max (1 + margin), R_M = min (1 - margin)."""
+    r = rng.to(torch.float64).contiguous()
+    P, nq = r.shape[0], r.shape[1]
+    radii = torch.empty((P, nq, M), dtype=torch.float64, device=r.device)
+    if status is None:
+        status = torch.zeros((P,), dtype=torch.int32, device=r.device)
+    check(lib.cil_radii_from_range(P, nq, M, r.data_ptr(), {"power": 0, "linear": 1}[law], float(margin),
+                                   radii.data_ptr(), status.data_ptr(), _stream(stream)), "cil_radii_from_range")
+    return radii, status
 
 
 def train_vectors(X, n_ens, grid, mask, radii, *, engine=ENGINE_AUTO, stream=None, ws: Workspace | None = None,

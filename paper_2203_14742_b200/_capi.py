@@ -43,6 +43,12 @@ def _load():
     lib.cil_synth_loglik.restype = ctypes.c_int
     lib.cil_diag_gram.argtypes = [P, i64, i64, P, i64, i64, Grid, ctypes.c_int, P, P, sz, P]
     lib.cil_diag_gram.restype = ctypes.c_int
+    lib.cil_range_workspace_size.argtypes = [i32, i64, i64, Grid, u32]
+    lib.cil_range_workspace_size.restype = sz
+    lib.cil_distance_range.argtypes = [i32, P, i64, i64, i64, P, i64, i64, i64, Grid, u32, P, P, P, sz, P]
+    lib.cil_distance_range.restype = ctypes.c_int
+    lib.cil_radii_from_range.argtypes = [i32, i32, i32, P, i32, f64, P, P, P]
+    lib.cil_radii_from_range.restype = ctypes.c_int
     lib.cil_train_workspace_size.argtypes = [i32, i32, i32, Grid, u32, i32, ctypes.c_int]
     lib.cil_train_workspace_size.restype = sz
     lib.cil_train_vectors.argtypes = [i32, P, i64, i64, i32, i32, Grid, u32, P, i64, i32, P, P, ctypes.c_int, P, sz, P]
@@ -84,7 +90,8 @@ EXPORTED = ["cil_features_workspace_size", "cil_features", "cil_stats", "cil_log
             "cil_version", "cil_last_launch_count", "cil_diag_gram", "cil_prof_enable", "cil_prof_read", "cil_normalize", "cil_diag_alu_ceiling",
             "cil_bin_matrix_workspace_size", "cil_bin_matrix", "cil_resample_counts",
             "cil_synth_boot_workspace_size", "cil_synth_loglik_boot", "cil_diag_gram_family",
-            "cil_train_workspace_size", "cil_train_vectors"]
+            "cil_train_workspace_size", "cil_train_vectors", "cil_range_workspace_size", "cil_distance_range",
+            "cil_radii_from_range"]
 
 
 def alu_ceiling(mix: int = 0, iters: int = 20000):

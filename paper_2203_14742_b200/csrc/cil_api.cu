@@ -255,12 +255,26 @@ cil_status check_grid(const cil_grid& g, uint32_t mask) {
     return CIL_OK;
 }
 
+cil_status check_sets(int32_t P, const float* A, int64_t strideA, int64_t lda, int64_t N, const float* B,
+                             int64_t strideB, int64_t ldb, int64_t Nt, const cil_grid& g) {
+    if ((N > 0 && !A) || (Nt > 0 && !B)) return CIL_EINVAL;
+    if (strideA < 0 || strideB < 0) return CIL_EINVAL;
+    const int64_t K = (int64_t)g.S * g.H * g.W;
+    if ((N > 0 && lda < K) || (Nt > 0 && ldb < K)) return CIL_EINVAL;
+    if (N > 0 && P > 1 && strideA > 0 && strideA < (N - 1) * lda + K) return CIL_EINVAL;
+    if (Nt > 0 && P > 1 && strideB > 0 && strideB < (Nt - 1) * ldb + K) return CIL_EINVAL;
+    if (K % 4 || lda % 4 || ldb % 4 || strideA % 4 || strideB % 4) return CIL_EUNSUPPORTED;
+    if ((A && !aligned16(A)) || (B && !aligned16(B))) return CIL_EUNSUPPORTED;
+    return CIL_OK;
+}
+
 // Core: counts for P items of (row panel x col panel), into the workspace histogram.
 cil_status run_engines(int P, const RowSrc& asrc, const RowSrc& bsrc, int64_t rowsA, int64_t rowsB,
                        const cil_grid& g, uint32_t mask, const Slots& sl, int M, const Plan& pl,
                        const SegParams& sp, const Layout& L, void* ws, const double* radii,
                        int64_t radii_stride, int32_t* status, cudaStream_t st, float* diag = nullptr,
-                       uint8_t* binout = nullptr, bool keep_status = false) {
+                       uint8_t* binout = nullptr, bool keep_status = false,
+                       unsigned long long* range = nullptr) {
     const int64_t K = (int64_t)g.S * g.H * g.W;
     BinParams bp{};
     bp.nq = sl.nq;
@@ -297,6 +311,7 @@ cil_status run_engines(int P, const RowSrc& asrc, const RowSrc& bsrc, int64_t ro
         for (int q = 0; q < sl.nq; ++q)
             if ((pl.simt_mask >> sl.slot[q]) & 1u) a.qmask |= 1u << q;
         a.binout = binout;
+        a.range = range;
         CIL_CU(launch_simt(a, st));
     }
     if (pl.tc) {
@@ -568,6 +583,53 @@ cil_status cil_synth_loglik(int32_t P, const float* pools, int64_t pool_stride, 
     return CIL_OK;
 }
 
+// ------------------------------------------------------------------ adaptive radii
+size_t cil_range_workspace_size(int32_t P, int64_t N, int64_t Nt, cil_grid g, uint32_t dist_mask) {
+    if (P < 1 || N < 0 || Nt < 0 || check_grid(g, dist_mask) != CIL_OK) return 0;
+    const Slots sl = slots_of(dist_mask);
+    const Plan pl = make_plan(dist_mask, CIL_ENGINE_SIMT, g);
+    SegParams sp{N > 0 ? N : 1, Nt > 0 ? Nt : 1, 1, 1};
+    return make_layout(P, N, Nt, g, sl.nq, 1, pl, sp, 0).total + 512;
+}
+
+cil_status cil_distance_range(int32_t P, const float* A, int64_t strideA, int64_t lda, int64_t N, const float* B,
+                              int64_t strideB, int64_t ldb, int64_t Nt, cil_grid g, uint32_t dist_mask,
+                              double* range, int32_t* item_status, void* ws, size_t ws_bytes, void* stream) {
+    t_launches = 0;
+    if (P < 1 || N < 1 || Nt < 1) return CIL_EINVAL;
+    if (check_grid(g, dist_mask) != CIL_OK) return CIL_EINVAL;
+    if (!range || !item_status || !ws) return CIL_EINVAL;
+    cil_status s = check_sets(P, A, strideA, lda, N, B, strideB, ldb, Nt, g);
+    if (s != CIL_OK) return s;
+    const Slots sl = slots_of(dist_mask);
+    const Plan pl = make_plan(dist_mask, CIL_ENGINE_SIMT, g);     // exact FP64 measures on CUDA cores
+    SegParams sp{N, Nt, 1, 1};
+    const Layout L = make_layout(P, N, Nt, g, sl.nq, 1, pl, sp, 0);
+    if (ws_bytes < L.total + 512) return CIL_ENOMEM;
+    void* wsa = reinterpret_cast<void*>(((uintptr_t)ws + 255) & ~(uintptr_t)255);
+    double* r = at<double>(wsa, L.total);                 // a dummy radius per measure (not binned)
+    const double ones[kMaxMeas] = {1.0, 1.0, 1.0, 1.0, 1.0, 1.0};
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    CIL_CU(cudaMemcpyAsync(r, ones, sizeof(double) * sl.nq, cudaMemcpyHostToDevice, st));
+    unsigned long long* rg = reinterpret_cast<unsigned long long*>(range);   // non-negative FP64 bits: ordered
+    CIL_CU(launch_range_init(P, sl.nq, rg, st));
+    RowSrc as{}, bs{};
+    as.base = A; as.stride = strideA; as.ld = lda; as.rows = N; as.mode = MODE_PLAIN;
+    bs.base = B; bs.stride = strideB; bs.ld = ldb; bs.rows = Nt; bs.mode = MODE_PLAIN;
+    return run_engines(P, as, bs, N, Nt, g, dist_mask, sl, 1, pl, sp, L, wsa, r, 0, item_status, st, nullptr,
+                       nullptr, false, rg);
+}
+
+cil_status cil_radii_from_range(int32_t P, int32_t n_meas, int32_t M, const double* range, int32_t law,
+                                double margin, double* radii, int32_t* item_status, void* stream) {
+    t_launches = 0;
+    if (P < 1 || n_meas < 1 || n_meas > kMaxMeas || M < 1 || M > kMaxM || (law != 0 && law != 1)) return CIL_EINVAL;
+    if (!range || !radii || !item_status || !(margin >= 0.0 && margin < 1.0)) return CIL_EINVAL;
+    CIL_CU(launch_radii(P, n_meas, M, reinterpret_cast<const unsigned long long*>(range), law, margin, radii,
+                        item_status, reinterpret_cast<cudaStream_t>(stream)));
+    return CIL_OK;
+}
+
 // ------------------------------------------------------------------ Alg. 1 / Alg. 2 training vectors
 size_t cil_train_workspace_size(int32_t P, int32_t n_ens, int32_t N, cil_grid g, uint32_t dist_mask, int32_t M,
                                 cil_engine engine) {
@@ -610,18 +672,6 @@ cil_status cil_train_vectors(int32_t P, const float* X, int64_t stride, int64_t 
 }
 
 // ------------------------------------------------------------------ bootstrap (Alg. A1 / A2)
-static cil_status check_sets(int32_t P, const float* A, int64_t strideA, int64_t lda, int64_t N, const float* B,
-                             int64_t strideB, int64_t ldb, int64_t Nt, const cil_grid& g) {
-    if ((N > 0 && !A) || (Nt > 0 && !B)) return CIL_EINVAL;
-    if (strideA < 0 || strideB < 0) return CIL_EINVAL;
-    const int64_t K = (int64_t)g.S * g.H * g.W;
-    if ((N > 0 && lda < K) || (Nt > 0 && ldb < K)) return CIL_EINVAL;
-    if (N > 0 && P > 1 && strideA > 0 && strideA < (N - 1) * lda + K) return CIL_EINVAL;
-    if (Nt > 0 && P > 1 && strideB > 0 && strideB < (Nt - 1) * ldb + K) return CIL_EINVAL;
-    if (K % 4 || lda % 4 || ldb % 4 || strideA % 4 || strideB % 4) return CIL_EUNSUPPORTED;
-    if ((A && !aligned16(A)) || (B && !aligned16(B))) return CIL_EUNSUPPORTED;
-    return CIL_OK;
-}
 
 size_t cil_bin_matrix_workspace_size(int32_t P, int64_t N, int64_t Nt, cil_grid g, uint32_t dist_mask, int32_t M,
                                      cil_engine engine) {

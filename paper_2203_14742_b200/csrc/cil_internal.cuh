@@ -159,6 +159,7 @@ struct SimtArgs {
     bool do_max, do_sum;
     uint32_t qmask;                           // slots binned by this engine
     uint8_t* binout;                          // non-null: bins[p][q][i][j] instead of counts
+    unsigned long long* range;                // non-null: [P][nq][2] min (d > 0) / max of d as FP64 bits
     int hist_cap;                             // shared histogram entries (set by the launcher)
 };
 cudaError_t launch_simt(const SimtArgs& a, cudaStream_t st);
@@ -261,6 +262,9 @@ cudaError_t launch_check_index(int P, const int32_t* idx, int64_t per_item, int6
 cudaError_t launch_resample(int P, const uint8_t* bins, int64_t N, int64_t Nt, int nq, int M, int n_rep,
                             const int32_t* I1, int64_t n1, const int32_t* I2, int64_t n2, uint64_t* counts,
                             double* y, int64_t y_item_stride, int32_t* status, cudaStream_t st);
+cudaError_t launch_range_init(int P, int nq, unsigned long long* range, cudaStream_t st);
+cudaError_t launch_radii(int P, int nq, int M, const unsigned long long* range, int law, double margin, double* radii,
+                         int32_t* status, cudaStream_t st);
 cudaError_t launch_build_pairs(int P, int n_ens, int nq, int M, const SegParams& sp, const uint64_t* hist,
                                int64_t N, double* Y, cudaStream_t st);
 cudaError_t launch_boot_tail(int P, int n_rep, int D, double ridge, double* out, int32_t* status, double* Y,

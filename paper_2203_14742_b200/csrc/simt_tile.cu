@@ -207,6 +207,12 @@ __global__ void __launch_bounds__(NTHR, DO_SUM ? 2 : 4) k_simt(SimtArgs a) {
                     case 4: d = fmax(m0, fmax(mxx, myy)); break;
                     default: d = m0 + mxx + myy; break;
                 }
+                if (a.range) {               // distance-range mode (adaptive radii)
+                    unsigned long long* rg = a.range + ((int64_t)p * nq + q) * 2;
+                    if (d > 0.0) atomicMin(&rg[0], (unsigned long long)__double_as_longlong(d));
+                    atomicMax(&rg[1], (unsigned long long)__double_as_longlong(d));
+                    continue;
+                }
                 const double* T = thr_s + q * M;
                 int b = 0;
                 while (b < M && d < T[b]) ++b;

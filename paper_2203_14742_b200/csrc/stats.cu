@@ -339,4 +339,50 @@ cudaError_t launch_build_pairs(int P, int n_ens, int nq, int M, const SegParams&
     return cudaGetLastError();
 }
 
+// ---- adaptive radii: R_0, R_M from the range of the distances
+__global__ void k_range_init(int n, unsigned long long* __restrict__ range) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        range[i] = (i & 1) ? 0ull : (unsigned long long)__double_as_longlong(INFINITY);
+}
+
+cudaError_t launch_range_init(int P, int nq, unsigned long long* range, cudaStream_t st) {
+    const int n = 2 * P * nq;
+    ProfScope ps_(K_PREP, st);
+    k_range_init<<<(n + 255) / 256 < 1024 ? (n + 255) / 256 : 1024, 256, 0, st>>>(n, range);
+    note_launch();
+    return cudaGetLastError();
+}
+
+// R_0 = d_max (1 + margin), R_M = d_min (1 - margin) (reading R5: R_0 is not a bin, R_M is),
+// law 0 = power  R_m = R_0 b^-m, b = (R_0/R_M)^(1/M);  law 1 = linear  R_m = R_0 - m (R_0 - R_M)/M;
+// m = 1..M.  An item without a positive distance gets BADRADII.
+__global__ void k_radii(int nq, int M, const unsigned long long* __restrict__ range, int law, double margin,
+                        double* __restrict__ radii, int32_t* __restrict__ status) {
+    const int p = blockIdx.x;
+    for (int t = threadIdx.x; t < nq * M; t += blockDim.x) {
+        const int q = t / M, m = t % M + 1;
+        const double dmin = __longlong_as_double((long long)range[((int64_t)p * nq + q) * 2]);
+        const double dmax = __longlong_as_double((long long)range[((int64_t)p * nq + q) * 2 + 1]);
+        const double R0 = dmax * (1.0 + margin), RM = dmin * (1.0 - margin);
+        double r;
+        if (!(dmin > 0.0) || !(dmax >= dmin) || !isfinite(dmax)) {
+            r = NAN;
+            if (threadIdx.x == 0) atomicOr(&status[p], CIL_ITEM_BADRADII);
+        } else if (law == 0) {
+            r = R0 * pow(RM / R0, (double)m / M);
+        } else {
+            r = R0 - m * (R0 - RM) / M;
+        }
+        radii[(int64_t)p * nq * M + t] = r;
+    }
+}
+
+cudaError_t launch_radii(int P, int nq, int M, const unsigned long long* range, int law, double margin, double* radii,
+                         int32_t* status, cudaStream_t st) {
+    ProfScope ps_(K_TAIL, st);
+    k_radii<<<P, 128, 0, st>>>(nq, M, range, law, margin, radii, status);
+    note_launch();
+    return cudaGetLastError();
+}
+
 }  // namespace cil

@@ -419,3 +419,27 @@ def test_gaussianity_chi2(cil, oracle_mod):
         assert d2[k] == pytest.approx(out[0], rel=1e-9)
     from scipy import stats as sps
     assert sps.chi2.sf(stat, dof) > 1e-4           # Gaussian data: no rejection at any sane level
+
+
+@pytest.mark.parametrize("law", ["power", "linear"])
+def test_adaptive_radii_vs_oracle(cil, oracle_mod, law):
+    """Per-item distance ranges (exact per-pair measures) and the radii laws of PAPER.md:109."""
+    O = oracle_mod
+    dev = torch.device("cuda")
+    grid = (2, 12, 12, 0.0)
+    P, N, Nt = 3, 40, 33
+    A = torch.stack([cilgen.make_set(95, 2 * p, N, grid[:3], n_w=4.6 + 0.3 * p) for p in range(P)])
+    B = torch.stack([cilgen.make_set(95, 2 * p + 1, Nt, grid[:3], n_w=4.6 + 0.3 * p) for p in range(P)])
+    rng, st = cil.distance_range(A.to(dev), B.to(dev), grid, 0x3F)
+    radii, st2 = cil.radii_from_range(rng, 11, law)
+    torch.cuda.synchronize()
+    assert int(st.max()) == 0 and int(st2.max()) == 0
+    for p in range(P):
+        ref = O.distance_range(A[p].numpy(), B[p].numpy(), grid, 0x3F)
+        np.testing.assert_allclose(rng[p].cpu().numpy(), ref, rtol=1e-6)
+        np.testing.assert_allclose(radii[p].cpu().numpy(), O.radii_from_range(rng[p].cpu().numpy(), 11, law),
+                                   rtol=1e-12)
+    # a set against itself: the zero self-distances are not the minimum
+    rs, _ = cil.distance_range(A[0].to(dev), A[0].to(dev), grid, 0x1)
+    torch.cuda.synchronize()
+    assert float(rs[0, 0, 0]) > 0

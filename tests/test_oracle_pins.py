@@ -319,3 +319,29 @@ def test_train_vectors_vs_brute(oracle_mod):
             np.testing.assert_array_equal(r["counts"][v], want)
             v += 1
     np.testing.assert_allclose(r["y"], r["counts"].reshape(v, -1) / (N * N), rtol=0, atol=0)
+
+
+def test_radii_laws(oracle_mod):
+    """power law with constant ratio b and R_M/R_0 = b^-M; linear law with
+    constant step h = (R_0 - R_M)/M; the margins of reading R5; ranges from brute force."""
+    O = oracle_mod
+    grid = (1, 5, 6, 0.0)
+    A = cilgen.make_patterns(14, 0, 7, grid[:3]).numpy()
+    rng = O.distance_range(A, A, grid, ALL)
+    Db = brute.distances(A, A, grid)
+    for q in range(6):
+        assert rng[q, 1] == pytest.approx(Db[q].max(), rel=1e-12)
+        assert rng[q, 0] == pytest.approx(Db[q][Db[q] > 0].min(), rel=1e-12)
+    M = 8
+    P_ = O.radii_from_range(rng, M, "power", 1e-3)
+    L_ = O.radii_from_range(rng, M, "linear", 1e-3)
+    for q in range(6):
+        R0, RM = rng[q, 1] * 1.001, rng[q, 0] * 0.999
+        ratios = P_[q][1:] / P_[q][:-1]
+        np.testing.assert_allclose(ratios, ratios[0], rtol=1e-12)
+        assert P_[q][-1] == pytest.approx(RM, rel=1e-12)
+        assert P_[q][0] == pytest.approx(R0 * ratios[0], rel=1e-12)
+        steps = np.diff(L_[q])
+        np.testing.assert_allclose(steps, -(R0 - RM) / M, rtol=1e-10)
+        assert L_[q][-1] == pytest.approx(RM, rel=1e-12)
+        assert np.all(np.diff(P_[q]) < 0) and np.all(np.diff(L_[q]) < 0)
