@@ -184,6 +184,16 @@ CIL_API cil_status cil_synth_loglik(int32_t P, const float* pools, int64_t pool_
                             cil_engine engine, void* ws, size_t ws_bytes, void* stream);
 
 /* ------------------------------------------------------------------------ */
+/* cil_minmax_scale — the scaled-pattern mode: for each of
+ * the n patterns X + r*ldx and each species s,
+ *   Y_s(x) = (X_s(x) - min_x X_s) / (max_x X_s - min_x X_s)   over the species' H x W values,
+ * in FP64, rounded to FP32; a constant species maps to 0 (reading R17).  Y + r*ldy may be X
+ * (in place).  The paper restricts scaled data to the L2-type norms.
+ * ------------------------------------------------------------------------ */
+CIL_API cil_status cil_minmax_scale(int64_t n, const float* X, int64_t ldx, float* Y, int64_t ldy, cil_grid g,
+                                    void* stream);
+
+/* ------------------------------------------------------------------------ */
 /* Adaptive radii: "R_0 (resp. R_M) the maximum (resp.
  * minimum) distance of any two patterns", then the power law R_m = R_0 b^-m with
  * R_M / R_0 = b^-M, or the linear law R_m = R_0 - m (R_0 - R_M)/M, m = 1..M.

@@ -283,3 +283,16 @@ def radii_from_range(rng, M, law: str = "power", margin: float = 1e-3):
             else:
                 out[q, m - 1] = R0 - m * (R0 - RM) / M
     return out
+
+
+def minmax_scale(X, grid):
+    """Scaled patterns: per pattern and species
+    (s - s_min) / (s_max - s_min) over the species' grid values, FP64 then FP32; a constant
+    species maps to 0 (reading R17)."""
+    S, H, W, _ = grid
+    X = np.asarray(X, np.float32).reshape(-1, S, H * W).astype(np.float64)
+    mn = X.min(axis=2, keepdims=True)
+    mx = X.max(axis=2, keepdims=True)
+    span = mx - mn
+    Y = np.where(span > 0, (X - mn) / np.where(span > 0, span, 1.0), 0.0)
+    return Y.astype(np.float32).reshape(-1, S, H, W)

@@ -31,7 +31,7 @@ ITEM_OK, ITEM_NONFINITE, ITEM_NOTPD, ITEM_BADRADII, ITEM_OVERFLOW, ITEM_BADINDEX
 __all__ = ["features", "stats", "loglik", "synth_loglik", "features_workspace_size",
            "synth_workspace_size", "n_measures", "Workspace", "CilError", "bin_matrix", "resample_counts",
            "synth_loglik_boot", "mcil_boot_stats", "train_vectors", "gaussianity_chi2",
-           "distance_range", "radii_from_range"]
+           "distance_range", "radii_from_range", "minmax_scale"]
 
 
 def n_measures(mask: int) -> int:
@@ -372,6 +372,19 @@ def diag_gram(A, B, grid, engine=ENGINE_TC_3XBF16, *, stream=None):
     check(lib.cil_diag_gram(A2.data_ptr(), K, N, B2.data_ptr(), K, Nt, g, engine, out.data_ptr(),
                             wbuf.data_ptr(), wbuf.numel(), _stream(stream)), "cil_diag_gram")
     return out
+
+
+def minmax_scale(X, grid, *, out=None, stream=None):
+    """Scaled patterns: per pattern and species, (x - min) / (max - min)."""
+    S, H, W = int(grid[0]), int(grid[1]), int(grid[2])
+    K = S * H * W
+    X2 = X.reshape(-1, K)
+    if X2.stride(1) != 1:
+        raise ValueError("patterns must be contiguous")
+    Y = torch.empty_like(X2) if out is None else out.reshape(-1, K)
+    check(lib.cil_minmax_scale(X2.shape[0], X2.data_ptr(), X2.stride(0), Y.data_ptr(), Y.stride(0), _grid(grid),
+                               _stream(stream)), "cil_minmax_scale")
+    return Y.reshape(X.shape)
 
 
 def distance_range(A, B, grid, mask, *, stream=None, ws: Workspace | None = None, status=None):

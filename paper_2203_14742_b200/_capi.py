@@ -43,6 +43,8 @@ def _load():
     lib.cil_synth_loglik.restype = ctypes.c_int
     lib.cil_diag_gram.argtypes = [P, i64, i64, P, i64, i64, Grid, ctypes.c_int, P, P, sz, P]
     lib.cil_diag_gram.restype = ctypes.c_int
+    lib.cil_minmax_scale.argtypes = [i64, P, i64, P, i64, Grid, P]
+    lib.cil_minmax_scale.restype = ctypes.c_int
     lib.cil_range_workspace_size.argtypes = [i32, i64, i64, Grid, u32]
     lib.cil_range_workspace_size.restype = sz
     lib.cil_distance_range.argtypes = [i32, P, i64, i64, i64, P, i64, i64, i64, Grid, u32, P, P, P, sz, P]
@@ -91,7 +93,7 @@ EXPORTED = ["cil_features_workspace_size", "cil_features", "cil_stats", "cil_log
             "cil_bin_matrix_workspace_size", "cil_bin_matrix", "cil_resample_counts",
             "cil_synth_boot_workspace_size", "cil_synth_loglik_boot", "cil_diag_gram_family",
             "cil_train_workspace_size", "cil_train_vectors", "cil_range_workspace_size", "cil_distance_range",
-            "cil_radii_from_range"]
+            "cil_radii_from_range", "cil_minmax_scale"]
 
 
 def alu_ceiling(mix: int = 0, iters: int = 20000):

@@ -583,6 +583,17 @@ cil_status cil_synth_loglik(int32_t P, const float* pools, int64_t pool_stride, 
     return CIL_OK;
 }
 
+// ------------------------------------------------------------------ min-max scaled patterns
+cil_status cil_minmax_scale(int64_t n, const float* X, int64_t ldx, float* Y, int64_t ldy, cil_grid g,
+                            void* stream) {
+    t_launches = 0;
+    if (n < 0 || g.S < 1 || g.H < 1 || g.W < 1) return CIL_EINVAL;
+    const int64_t K = (int64_t)g.S * g.H * g.W;
+    if (n > 0 && (!X || !Y || ldx < K || ldy < K)) return CIL_EINVAL;
+    CIL_CU(launch_minmax(n, X, ldx, Y, ldy, g.S, (int64_t)g.H * g.W, reinterpret_cast<cudaStream_t>(stream)));
+    return CIL_OK;
+}
+
 // ------------------------------------------------------------------ adaptive radii
 size_t cil_range_workspace_size(int32_t P, int64_t N, int64_t Nt, cil_grid g, uint32_t dist_mask) {
     if (P < 1 || N < 0 || Nt < 0 || check_grid(g, dist_mask) != CIL_OK) return 0;

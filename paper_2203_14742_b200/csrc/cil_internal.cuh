@@ -262,6 +262,8 @@ cudaError_t launch_check_index(int P, const int32_t* idx, int64_t per_item, int6
 cudaError_t launch_resample(int P, const uint8_t* bins, int64_t N, int64_t Nt, int nq, int M, int n_rep,
                             const int32_t* I1, int64_t n1, const int32_t* I2, int64_t n2, uint64_t* counts,
                             double* y, int64_t y_item_stride, int32_t* status, cudaStream_t st);
+cudaError_t launch_minmax(int64_t n, const float* X, int64_t ldx, float* Y, int64_t ldy, int S, int64_t HW,
+                          cudaStream_t st);
 cudaError_t launch_range_init(int P, int nq, unsigned long long* range, cudaStream_t st);
 cudaError_t launch_radii(int P, int nq, int M, const unsigned long long* range, int law, double margin, double* radii,
                          int32_t* status, cudaStream_t st);

@@ -535,6 +535,52 @@ cudaError_t launch_pack_i8_aug(int P, const RowSrc& src, int64_t rows, const Aug
     return cudaGetLastError();
 }
 
+// ------------------------------------------------------------- min-max scaling
+// Scaled-pattern mode: per pattern and species s,
+//   y_s(x) = (s(x) - s_min) / (s_max - s_min)  over the species' H x W grid values,
+// evaluated in FP64 and rounded to FP32; a constant species maps to 0 (reading R17).
+// One CTA per pattern.
+__global__ void __launch_bounds__(256) k_minmax(const float* __restrict__ X, int64_t ldx, float* __restrict__ Y,
+                                                int64_t ldy, int S, int64_t HW) {
+    const int64_t r = blockIdx.x;
+    const float* x = X + r * ldx;
+    float* y = Y + r * ldy;
+    __shared__ float smin[8], smax[8];
+    const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
+    for (int s = 0; s < S; ++s) {
+        const float* xs = x + (int64_t)s * HW;
+        float mn = INFINITY, mx = -INFINITY;
+        for (int64_t e = threadIdx.x; e < HW; e += 256) {
+            const float v = xs[e];
+            mn = fminf(mn, v);
+            mx = fmaxf(mx, v);
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        }
+        if (ln == 0) { smin[w] = mn; smax[w] = mx; }
+        __syncthreads();
+        mn = smin[0];
+        mx = smax[0];
+        for (int i = 1; i < 8; ++i) { mn = fminf(mn, smin[i]); mx = fmaxf(mx, smax[i]); }
+        __syncthreads();                                    // smin/smax reused by the next species
+        const double lo = mn, span = (double)mx - (double)mn;
+        float* ys = y + (int64_t)s * HW;
+        for (int64_t e = threadIdx.x; e < HW; e += 256)
+            ys[e] = span > 0.0 ? (float)(((double)xs[e] - lo) / span) : 0.f;
+    }
+}
+
+cudaError_t launch_minmax(int64_t n, const float* X, int64_t ldx, float* Y, int64_t ldy, int S, int64_t HW,
+                          cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    ProfScope ps_(K_PACK, st);
+    k_minmax<<<(unsigned)n, 256, 0, st>>>(X, ldx, Y, ldy, S, HW);
+    note_launch();
+    return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------------- aug pack
 // One CTA per panel row: out = [x (K) | D_x x (S*H*(W-1)) | D_y x (S*(H-1)*W)], each
 // region zero-padded to a multiple of kSimtBK, plain FP32 differences.

@@ -443,3 +443,22 @@ def test_adaptive_radii_vs_oracle(cil, oracle_mod, law):
     rs, _ = cil.distance_range(A[0].to(dev), A[0].to(dev), grid, 0x1)
     torch.cuda.synchronize()
     assert float(rs[0, 0, 0]) > 0
+
+
+def test_minmax_scale_bit_exact(cil, oracle_mod):
+    """Scaled patterns: FP64 (x - min)/(max - min) rounded to FP32 on both
+    sides is bit-identical; then the scaled-data counts (L2-type norms)."""
+    O = oracle_mod
+    dev = torch.device("cuda")
+    grid = (2, 16, 16, 0.0)
+    X = cilgen.make_set(97, 0, 50, grid[:3])
+    X[3, 1] = 2.5                                         # a constant species
+    Yg = cil.minmax_scale(X.to(dev), grid)
+    torch.cuda.synchronize()
+    Yr = O.minmax_scale(X.numpy(), grid)
+    np.testing.assert_array_equal(Yg.cpu().numpy(), Yr)
+    mask = 0x0D
+    D = O.distance_matrix(Yr[:25], Yr[25:], grid, mask)
+    radii = np.array([np.quantile(d, np.linspace(0.95, 0.05, 8)) for d in D])
+    c, _, _ = _run_features(cil, torch.tensor(Yr[:25]), torch.tensor(Yr[25:]), grid, mask, radii, "AUTO")
+    _check_counts(c[0], O.features(Yr[:25], Yr[25:], grid, mask, radii, band=BAND))

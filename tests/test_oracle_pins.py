@@ -345,3 +345,21 @@ def test_radii_laws(oracle_mod):
         np.testing.assert_allclose(steps, -(R0 - RM) / M, rtol=1e-10)
         assert L_[q][-1] == pytest.approx(RM, rel=1e-12)
         assert np.all(np.diff(P_[q]) < 0) and np.all(np.diff(L_[q]) < 0)
+
+
+def test_minmax_scale(oracle_mod):
+    """every species of every pattern spans exactly [0, 1]; a positive affine
+    change of a species leaves the scaled pattern unchanged (to FP32 rounding); constant -> 0."""
+    O = oracle_mod
+    grid = (2, 6, 7, 0.0)
+    X = cilgen.make_patterns(17, 0, 5, grid[:3]).numpy()
+    Y = O.minmax_scale(X, grid)
+    for s in range(2):
+        assert np.all(Y[:, s].reshape(5, -1).min(axis=1) == 0.0)
+        assert np.all(Y[:, s].reshape(5, -1).max(axis=1) == 1.0)
+    X2 = X.copy()
+    X2[:, 1] = 3.0 * X2[:, 1] - 7.0
+    np.testing.assert_allclose(O.minmax_scale(X2, grid), Y, atol=2e-6)
+    X3 = X.copy()
+    X3[2, 0] = 4.0
+    assert np.all(O.minmax_scale(X3, grid)[2, 0] == 0.0)
