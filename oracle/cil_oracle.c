@@ -38,6 +38,7 @@ enum { M_L2 = 0, M_LINF = 1, M_W12SUM = 2, M_W12 = 3, M_W1INF = 4, M_W1INFSUM = 
 typedef struct {
     int S, H, W;   /* species, rows, columns of one pattern; layout [S][H][W] row-major */
     double h;      /* grid spacing; <=0 -> 1/(W-1) [R2] */
+    unsigned gs;   /* species with derivative terms (bit s); 0 = all [R18] */
 } or_grid;
 
 static double grid_h(const or_grid *g) {
@@ -61,12 +62,14 @@ void oracle_subnorms(const float *a, const float *b, const or_grid *g, double ou
     const double h = grid_h(g);
     double s0 = 0, sx = 0, sy = 0, m0 = 0, mx = 0, my = 0;
     for (int s = 0; s < S; ++s) {
+        const int grad = g->gs == 0 || ((g->gs >> s) & 1u);   /* derivative terms of species s [R18] */
         for (int r = 0; r < H; ++r) {
             for (int c = 0; c < W; ++c) {
                 size_t e = ((size_t)s * H + r) * W + c;
                 double u = (double)a[e] - (double)b[e];
                 s0 += u * u;
                 if (fabs(u) > m0) m0 = fabs(u);
+                if (!grad) continue;
                 if (c + 1 < W) {
                     double u1 = (double)a[e + 1] - (double)b[e + 1];
                     double dx = (u1 - u) / h;
@@ -175,12 +178,12 @@ static void *feat_worker(void *arg) {
 /* returns 0 ok, 1 if any input is non-finite (counts still computed), -1 on bad args */
 int oracle_features(const float *A, int64_t lda, int64_t N,
                     const float *B, int64_t ldb, int64_t Nt,
-                    int S, int H, int W, double h, uint32_t mask,
+                    int S, int H, int W, double h, unsigned gs, uint32_t mask,
                     const double *radii, int M, double band,
                     int64_t *cnt, int64_t *lo, int64_t *hi, double *y,
                     int64_t *n_amb, int nthreads) {
     if (!A || !B || !radii || !cnt || N < 0 || Nt < 0 || M < 1 || mask == 0 || (mask >> 6)) return -1;
-    or_grid g = {S, H, W, h};
+    or_grid g = {S, H, W, h, gs};
     const int nq = popcount6(mask);
     const size_t nc = (size_t)nq * M;
     if (nthreads < 1) nthreads = 1;
@@ -228,8 +231,8 @@ int oracle_features(const float *A, int64_t lda, int64_t N,
 /* All pairwise distances for the selected measures, d[q][i][j] (tiny inputs only). */
 int oracle_distance_matrix(const float *A, int64_t lda, int64_t N,
                            const float *B, int64_t ldb, int64_t Nt,
-                           int S, int H, int W, double h, uint32_t mask, double *D) {
-    or_grid g = {S, H, W, h};
+                           int S, int H, int W, double h, unsigned gs, uint32_t mask, double *D) {
+    or_grid g = {S, H, W, h, gs};
     int slot[N_MEAS_MAX], nq = 0;
     for (int i = 0; i < N_MEAS_MAX; ++i)
         if ((mask >> i) & 1u) slot[nq++] = i;
@@ -319,7 +322,7 @@ int oracle_loglik(const double *mu, const double *Sigma, const double *y, int D,
  * ------------------------------------------------------------------------- */
 int oracle_synth_loglik(const float *pool, int64_t ld, int n_ens, int N_set, int N_tilde,
                         const float *data, int64_t ld_data, int k0,
-                        int S, int H, int W, double h, uint32_t mask,
+                        int S, int H, int W, double h, unsigned gs, uint32_t mask,
                         const double *radii, int M, double ridge, double out[3],
                         double *Y, int nthreads) {
     const int nq = popcount6(mask);
@@ -333,14 +336,14 @@ int oracle_synth_loglik(const float *pool, int64_t ld, int n_ens, int N_set, int
         for (int l = 0; l < n_ens; ++l) {
             const float *s1 = pool + (int64_t)k * N * ld;
             const float *s2 = pool + ((int64_t)l * N + N_set) * ld;
-            int st = oracle_features(s1, ld, N_set, s2, ld, N_tilde, S, H, W, h, mask, radii, M,
+            int st = oracle_features(s1, ld, N_set, s2, ld, N_tilde, S, H, W, h, gs, mask, radii, M,
                                      0.0, cnt, NULL, NULL, Yv + (size_t)(k * n_ens + l) * D,
                                      NULL, nthreads);
             if (st == OR_NONFINITE) nonfinite = 1;
         }
     {
         const float *s2 = pool + ((int64_t)k0 * N + N_set) * ld;
-        int st = oracle_features(data, ld_data, N_set, s2, ld, N_tilde, S, H, W, h, mask, radii, M,
+        int st = oracle_features(data, ld_data, N_set, s2, ld, N_tilde, S, H, W, h, gs, mask, radii, M,
                                  0.0, cnt, NULL, NULL, Yv + (size_t)nv * D, NULL, nthreads);
         if (st == OR_NONFINITE) nonfinite = 1;
     }
@@ -365,7 +368,7 @@ int oracle_synth_loglik(const float *pool, int64_t ld, int n_ens, int N_set, int
  * Returns 0, OR_NONFINITE, or -1 (bad argument / index out of range).
  * ------------------------------------------------------------------------- */
 int oracle_resample_features(const float *A, int64_t lda, int64_t N, const float *B, int64_t ldb, int64_t Nt,
-                             int S, int H, int W, double h, uint32_t mask, const double *radii, int M,
+                             int S, int H, int W, double h, unsigned gs, uint32_t mask, const double *radii, int M,
                              int n_rep, const int32_t *I1, int64_t n1, const int32_t *I2, int64_t n2,
                              double band, int64_t *cnt, int64_t *lo, int64_t *hi, double *y, int nthreads) {
     const int64_t K = (int64_t)S * H * W;
@@ -384,7 +387,7 @@ int oracle_resample_features(const float *A, int64_t lda, int64_t N, const float
         for (int64_t j = 0; j < n2; ++j)
             memcpy(s2 + j * K, B + (int64_t)I2[(int64_t)k * n2 + j] * ldb, sizeof(float) * (size_t)K);
         /* distances between all patterns of s^1 and s^2 -> y^k via Eq. (1) */
-        int st = oracle_features(s1, K, n1, s2, K, n2, S, H, W, h, mask, radii, M, band,
+        int st = oracle_features(s1, K, n1, s2, K, n2, S, H, W, h, gs, mask, radii, M, band,
                                  cnt + (size_t)k * D, lo ? lo + (size_t)k * D : NULL,
                                  hi ? hi + (size_t)k * D : NULL, y ? y + (size_t)k * D : NULL, NULL, nthreads);
         if (st == OR_NONFINITE) nonfinite = 1;
@@ -407,21 +410,21 @@ int oracle_resample_features(const float *A, int64_t lda, int64_t N, const float
  * ------------------------------------------------------------------------- */
 int oracle_synth_boot(const float *pool, int64_t ld, int N_syn, const float *data, int64_t ld_data, int N_set,
                       int n_rep, const int32_t *I1, const int32_t *I2, const int32_t *J,
-                      int S, int H, int W, double h, uint32_t mask, const double *radii, int M,
+                      int S, int H, int W, double h, unsigned gs, uint32_t mask, const double *radii, int M,
                       double ridge, double out[3], double *Y, int nthreads) {
     const int nq = popcount6(mask);
     const int D = nq * M;
     const int Nt = N_syn - N_set;
     double *Yv = (double *)calloc((size_t)(n_rep + 1) * D, sizeof(double));
     int64_t *cnt = (int64_t *)calloc((size_t)n_rep * D, sizeof(int64_t));
-    int st = oracle_resample_features(pool, ld, N_syn, pool, ld, N_syn, S, H, W, h, mask, radii, M, n_rep,
+    int st = oracle_resample_features(pool, ld, N_syn, pool, ld, N_syn, S, H, W, h, gs, mask, radii, M, n_rep,
                                       I1, N_set, I2, Nt, 0.0, cnt, NULL, NULL, Yv, nthreads);
     if (st < 0) { free(Yv); free(cnt); return -1; }
     int nonfinite = st == OR_NONFINITE;
     /* steps 4-5: y~ from s_data and the subset pool[J] */
     int32_t *I0 = (int32_t *)malloc(sizeof(int32_t) * (size_t)N_set);
     for (int i = 0; i < N_set; ++i) I0[i] = i;                 /* s_data itself, no resampling */
-    st = oracle_resample_features(data, ld_data, N_set, pool, ld, N_syn, S, H, W, h, mask, radii, M, 1,
+    st = oracle_resample_features(data, ld_data, N_set, pool, ld, N_syn, S, H, W, h, gs, mask, radii, M, 1,
                                   I0, N_set, J, Nt, 0.0, cnt, NULL, NULL, Yv + (size_t)n_rep * D, nthreads);
     free(I0);
     if (st < 0) { free(Yv); free(cnt); return -1; }

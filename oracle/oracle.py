@@ -46,22 +46,22 @@ def _load():
         lib = ctypes.CDLL(_LIB)
         P = ctypes.c_void_p
         i64, i32, u32, f64 = ctypes.c_int64, ctypes.c_int, ctypes.c_uint32, ctypes.c_double
-        lib.oracle_features.argtypes = [P, i64, i64, P, i64, i64, i32, i32, i32, f64, u32, P, i32,
+        lib.oracle_features.argtypes = [P, i64, i64, P, i64, i64, i32, i32, i32, f64, u32, u32, P, i32,
                                         f64, P, P, P, P, P, i32]
         lib.oracle_features.restype = i32
-        lib.oracle_distance_matrix.argtypes = [P, i64, i64, P, i64, i64, i32, i32, i32, f64, u32, P]
+        lib.oracle_distance_matrix.argtypes = [P, i64, i64, P, i64, i64, i32, i32, i32, f64, u32, u32, P]
         lib.oracle_stats.argtypes = [P, i32, i32, P, P]
         lib.oracle_stats.restype = i32
         lib.oracle_loglik.argtypes = [P, P, P, i32, f64, P]
         lib.oracle_loglik.restype = i32
         lib.oracle_synth_loglik.argtypes = [P, i64, i32, i32, i32, P, i64, i32, i32, i32, i32, f64,
-                                            u32, P, i32, f64, P, P, i32]
+                                            u32, u32, P, i32, f64, P, P, i32]
         lib.oracle_synth_loglik.restype = i32
         lib.oracle_subnorms.argtypes = [P, P, P, P]
-        lib.oracle_resample_features.argtypes = [P, i64, i64, P, i64, i64, i32, i32, i32, f64, u32, P, i32, i32,
+        lib.oracle_resample_features.argtypes = [P, i64, i64, P, i64, i64, i32, i32, i32, f64, u32, u32, P, i32, i32,
                                                  P, i64, P, i64, f64, P, P, P, P, i32]
         lib.oracle_resample_features.restype = i32
-        lib.oracle_synth_boot.argtypes = [P, i64, i32, P, i64, i32, i32, P, P, P, i32, i32, i32, f64, u32, P,
+        lib.oracle_synth_boot.argtypes = [P, i64, i32, P, i64, i32, i32, P, P, P, i32, i32, i32, f64, u32, u32, P,
                                           i32, f64, P, P, i32]
         lib.oracle_synth_boot.restype = i32
         _lib = lib
@@ -99,7 +99,8 @@ def features(A, B, grid, mask, radii, band: float = 1e-6, nthreads: int | None =
     A: [N][S][H][W] (or [N][K]) float32, B: [Nt][...]; grid = (S, H, W, h);
     radii: [n_meas][M] strictly decreasing.  Returns dict of numpy arrays.
     """
-    S, H, W, h = grid
+    S, H, W, h = grid[:4]
+    gs = int(grid[4]) if len(grid) > 4 else 0
     K = S * H * W
     A2, B2 = _rows(A, K), _rows(B, K)
     nq = n_measures(mask)
@@ -111,7 +112,7 @@ def features(A, B, grid, mask, radii, band: float = 1e-6, nthreads: int | None =
     y = np.zeros((nq, M), np.float64)
     amb = np.zeros(1, np.int64)
     st = _load().oracle_features(_ptr(A2), K, A2.shape[0], _ptr(B2), K, B2.shape[0], S, H, W,
-                                 float(h), mask, _ptr(radii), M, float(band), _ptr(cnt), _ptr(lo),
+                                 float(h), gs, mask, _ptr(radii), M, float(band), _ptr(cnt), _ptr(lo),
                                  _ptr(hi), _ptr(y), _ptr(amb), nthreads or default_threads())
     if st < 0:
         raise ValueError("oracle_features: invalid arguments")
@@ -120,25 +121,28 @@ def features(A, B, grid, mask, radii, band: float = 1e-6, nthreads: int | None =
 
 def distance_matrix(A, B, grid, mask):
     """All pairwise distances d[q][i][j] for the selected measures (tiny inputs)."""
-    S, H, W, h = grid
+    S, H, W, h = grid[:4]
+    gs = int(grid[4]) if len(grid) > 4 else 0
     K = S * H * W
     A2, B2 = _rows(A, K), _rows(B, K)
     nq = n_measures(mask)
     D = np.zeros((nq, A2.shape[0], B2.shape[0]), np.float64)
     _load().oracle_distance_matrix(_ptr(A2), K, A2.shape[0], _ptr(B2), K, B2.shape[0], S, H, W,
-                                   float(h), mask, _ptr(D))
+                                   float(h), gs, mask, _ptr(D))
     return D
 
 
 class _Grid(ctypes.Structure):
-    _fields_ = [("S", ctypes.c_int), ("H", ctypes.c_int), ("W", ctypes.c_int), ("h", ctypes.c_double)]
+    _fields_ = [("S", ctypes.c_int), ("H", ctypes.c_int), ("W", ctypes.c_int), ("h", ctypes.c_double),
+                ("gs", ctypes.c_uint)]
 
 
 def subnorms(a, b, grid):
     """(s0, sx, sy, m0, mx, my) of u = a - b (sums of squares, derivative terms / h^2)."""
-    S, H, W, h = grid
+    S, H, W, h = grid[:4]
+    gs = int(grid[4]) if len(grid) > 4 else 0
     a, b = _f32(a).ravel(), _f32(b).ravel()
-    g = _Grid(S, H, W, float(h))
+    g = _Grid(S, H, W, float(h), gs)
     out = np.zeros(6, np.float64)
     _load().oracle_subnorms(_ptr(a), _ptr(b), ctypes.byref(g), _ptr(out))
     return out
@@ -168,7 +172,8 @@ def loglik(mu, Sigma, y, ridge: float = 0.0):
 def synth_loglik(pool, n_ens, N_set, N_tilde, data, k0, grid, mask, radii, ridge=0.0,
                  nthreads: int | None = None):
     """SCIL at one theta (Alg. 3): returns (out[3], status, Y[n_ens^2 + 1][D])."""
-    S, H, W, h = grid
+    S, H, W, h = grid[:4]
+    gs = int(grid[4]) if len(grid) > 4 else 0
     K = S * H * W
     P2 = _rows(pool, K)
     D2 = _rows(data, K)
@@ -180,7 +185,7 @@ def synth_loglik(pool, n_ens, N_set, N_tilde, data, k0, grid, mask, radii, ridge
     out = np.zeros(3)
     Y = np.zeros((n_ens * n_ens + 1, nq * M))
     st = _load().oracle_synth_loglik(_ptr(P2), K, n_ens, N_set, N_tilde, _ptr(D2), K, int(k0), S, H,
-                                     W, float(h), mask, _ptr(radii), M, float(ridge), _ptr(out),
+                                     W, float(h), gs, mask, _ptr(radii), M, float(ridge), _ptr(out),
                                      _ptr(Y), nthreads or default_threads())
     return out, st, Y
 
@@ -189,7 +194,8 @@ def resample_features(A, B, grid, mask, radii, I1, I2, band: float = 1e-6, nthre
     """Bootstrap step 2 (Alg. A1 / A2): for replicate k, s^1 = A[I1[k]], s^2 = B[I2[k]]
     constructed explicitly, then Eq. (1).  I1 [n_rep][n1], I2 [n_rep][n2] int.
     Returns dict counts / lo / hi [n_rep][nq][M], y [n_rep][nq*M], status."""
-    S, H, W, h = grid
+    S, H, W, h = grid[:4]
+    gs = int(grid[4]) if len(grid) > 4 else 0
     K = S * H * W
     A2, B2 = _rows(A, K), _rows(B, K)
     nq = n_measures(mask)
@@ -203,7 +209,7 @@ def resample_features(A, B, grid, mask, radii, I1, I2, band: float = 1e-6, nthre
     hi = np.zeros_like(cnt)
     y = np.zeros((n_rep, nq * M), np.float64)
     st = _load().oracle_resample_features(_ptr(A2), K, A2.shape[0], _ptr(B2), K, B2.shape[0], S, H, W, float(h),
-                                          mask, _ptr(radii), M, n_rep, _ptr(I1), n1, _ptr(I2), n2, float(band),
+                                          gs, mask, _ptr(radii), M, n_rep, _ptr(I1), n1, _ptr(I2), n2, float(band),
                                           _ptr(cnt), _ptr(lo), _ptr(hi), _ptr(y), nthreads or default_threads())
     if st < 0:
         raise ValueError("oracle_resample_features: invalid arguments or index out of range")
@@ -212,7 +218,8 @@ def resample_features(A, B, grid, mask, radii, I1, I2, band: float = 1e-6, nthre
 
 def synth_boot(pool, data, N_set, I1, I2, J, grid, mask, radii, ridge=0.0, nthreads: int | None = None):
     """SCIL with bootstrapping at one theta (Alg. A2): returns (out[3], status, Y[n_rep + 1][D])."""
-    S, H, W, h = grid
+    S, H, W, h = grid[:4]
+    gs = int(grid[4]) if len(grid) > 4 else 0
     K = S * H * W
     P2 = _rows(pool, K)
     D2 = _rows(data, K)
@@ -227,7 +234,7 @@ def synth_boot(pool, data, N_set, I1, I2, J, grid, mask, radii, ridge=0.0, nthre
     out = np.zeros(3)
     Y = np.zeros((n_rep + 1, nq * M))
     st = _load().oracle_synth_boot(_ptr(P2), K, P2.shape[0], _ptr(D2), K, N_set, n_rep, _ptr(I1), _ptr(I2),
-                                   _ptr(J), S, H, W, float(h), mask, _ptr(radii), M, float(ridge), _ptr(out),
+                                   _ptr(J), S, H, W, float(h), gs, mask, _ptr(radii), M, float(ridge), _ptr(out),
                                    _ptr(Y), nthreads or default_threads())
     if st < 0:
         raise ValueError("oracle_synth_boot: invalid arguments or index out of range")
@@ -239,7 +246,8 @@ def train_vectors(X, n_ens, grid, mask, radii, band: float = 1e-6, nthreads: int
     N = len(X) / n_ens rows (step 1); for every unordered pair k < l (lexicographic order,
     C(n_ens, 2) realisations) the correlation-integral vector of (s^k, s^l) by
     Eq. (1) (step 2).  Returns dict counts / lo / hi [n_pairs][nq][M], y [n_pairs][nq*M]."""
-    S, H, W, h = grid
+    S, H, W, h = grid[:4]
+    gs = int(grid[4]) if len(grid) > 4 else 0
     K = S * H * W
     X2 = _rows(X, K)
     N = X2.shape[0] // n_ens

@@ -12,8 +12,10 @@ import numpy as np
 
 
 def distances(A, B, grid):
-    """d[6][N][Nt] for (L2, Linf, W12sum, W12, W1inf, W1infsum)."""
-    S, H, W, h = grid
+    """d[6][N][Nt] for (L2, Linf, W12sum, W12, W1inf, W1infsum); grid[4] (optional) = species
+    mask of the derivative terms (0 = all)."""
+    S, H, W, h = grid[:4]
+    gs = int(grid[4]) if len(grid) > 4 else 0
     if h <= 0:
         h = 1.0 / (W - 1) if W > 1 else 1.0
     dim = 2 if H > 1 else 1
@@ -21,8 +23,9 @@ def distances(A, B, grid):
     A = np.asarray(A, np.float64).reshape(-1, S, H, W)
     B = np.asarray(B, np.float64).reshape(-1, S, H, W)
     U = A[:, None] - B[None, :]                      # [N, Nt, S, H, W]
-    DX = np.diff(U, axis=-1) / h                     # [.., W-1]  last node dropped
-    DY = np.diff(U, axis=-2) / h                     # [.., H-1, W]
+    sel = [s for s in range(S) if gs == 0 or (gs >> s) & 1]
+    DX = np.diff(U[:, :, sel], axis=-1) / h          # [.., W-1]  last node dropped
+    DY = np.diff(U[:, :, sel], axis=-2) / h          # [.., H-1, W]
     red = lambda X, f: f(X.reshape(X.shape[0], X.shape[1], -1), axis=-1) if X.size else np.zeros(U.shape[:2])
     s0, sx, sy = red(U ** 2, np.sum), red(DX ** 2, np.sum), red(DY ** 2, np.sum)
     m0, mx, my = red(np.abs(U), np.max), red(np.abs(DX), np.max), red(np.abs(DY), np.max)

@@ -363,3 +363,21 @@ def test_minmax_scale(oracle_mod):
     X3 = X.copy()
     X3[2, 0] = 4.0
     assert np.all(O.minmax_scale(X3, grid)[2, 0] == 0.0)
+
+
+def test_gradient_species_mask(oracle_mod):
+    """PAPER.md:526 (RD-ODE): gradient-based norms w.r.t. selected species only.  With only
+    species 1 selected, the derivative sub-norms equal those of the one-species pattern made
+    of species 1; the value terms are unchanged; brute force agrees."""
+    O = oracle_mod
+    grid = (2, 1, 20, 0.0)
+    X = cilgen.make_patterns(19, 0, 6, grid[:3]).numpy()
+    a, b = X[0], X[1]
+    s_all = O.subnorms(a, b, grid)
+    s_m = O.subnorms(a, b, grid + (0b10,))
+    s_1 = O.subnorms(a[1:2], b[1:2], (1, 1, 20, 1.0 / 19))
+    assert s_m[0] == pytest.approx(s_all[0], rel=1e-14) and s_m[3] == s_all[3]
+    assert s_m[1] == pytest.approx(s_1[1], rel=1e-14) and s_m[4] == pytest.approx(s_1[4], rel=1e-14)
+    assert s_m[1] < s_all[1]
+    D = O.distance_matrix(X[:3], X[3:], grid + (0b10,), ALL)
+    np.testing.assert_allclose(D, brute.distances(X[:3], X[3:], grid + (0b10,)), rtol=1e-12)
