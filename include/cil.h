@@ -90,6 +90,8 @@ typedef enum {
 typedef struct {
     int32_t S, H, W; /* species, rows, columns; H == 1 -> 1-D grid (no y-derivative) */
     double h;        /* grid spacing; <= 0 -> 1/(W-1) */
+    uint32_t gs;     /* species whose derivative terms enter the gradient-based norms (bit s);
+                        0 = all species (RD-ODE, the diffusive component only) */
 } cil_grid;
 
 /* ------------------------------------------------------------------------ */

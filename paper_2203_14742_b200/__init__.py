@@ -39,9 +39,11 @@ def n_measures(mask: int) -> int:
 
 
 def _grid(grid) -> Grid:
+    """(S, H, W[, h[, gs]]): gs = species mask of the derivative terms (0 = all)."""
     S, H, W = int(grid[0]), int(grid[1]), int(grid[2])
     h = float(grid[3]) if len(grid) > 3 else 0.0
-    return Grid(S, H, W, h)
+    gs = int(grid[4]) if len(grid) > 4 else 0
+    return Grid(S, H, W, h, gs)
 
 
 def _stream(stream=None) -> int:

@@ -18,7 +18,8 @@ class CilError(RuntimeError):
 
 
 class Grid(ctypes.Structure):
-    _fields_ = [("S", ctypes.c_int32), ("H", ctypes.c_int32), ("W", ctypes.c_int32), ("h", ctypes.c_double)]
+    _fields_ = [("S", ctypes.c_int32), ("H", ctypes.c_int32), ("W", ctypes.c_int32), ("h", ctypes.c_double),
+                ("gs", ctypes.c_uint32)]
 
 
 def _load():

@@ -206,7 +206,7 @@ Layout make_layout(int P, int64_t rowsA, int64_t rowsB, const cil_grid& g, int n
         if (pl.aug) L.off_part = take(sizeof(float) * 4 * (size_t)P * rowsA * rowsB);
     }
     if (pl.simt_mask) {
-        L.geom = make_aug_geom(g.S, g.H, g.W, pl.nreg);
+        L.geom = make_aug_geom(g.S, g.H, g.W, pl.nreg, g.gs);
         L.off_aug = take(sizeof(float) * (size_t)rows * L.geom.off[3]);
     }
     if (nY > 0) {
@@ -334,7 +334,7 @@ cil_status run_engines(int P, const RowSrc& asrc, const RowSrc& bsrc, int64_t ro
                 if (sl.slot[q] == 3) q_tc[1] = q;
                 if (sl.slot[q] == 2) q_tc[2] = q;
             }
-            const AugGeom ag = make_aug_geom(g.S, g.H, g.W, 3);
+            const AugGeom ag = make_aug_geom(g.S, g.H, g.W, 3, g.gs);
             const int64_t Kr = L.kp[3];
             const bool b_same = same_rows(asrc, bsrc) && rowsA == rowsB;
             CIL_CU(launch_pack_i8_aug(P, asrc, rowsA, ag, L.kp, center, L.Kp, reinterpret_cast<int8_t*>(hi),
@@ -440,7 +440,7 @@ cil_status run_engines(int P, const RowSrc& asrc, const RowSrc& bsrc, int64_t ro
         r.status = status; r.P = P;
         r.binout = binout; r.rowsA = rowsA; r.rowsB = rowsB;
         for (int a = 0; a < 3; ++a) r.q_tc[a] = q_tc[a];
-        r.S = g.S; r.H = g.H; r.W = g.W; r.h = bp.h;
+        r.S = g.S; r.H = g.H; r.W = g.W; r.h = bp.h; r.gs = g.gs;
         CIL_CU(launch_recheck(r, st));
         static const char* dbg = getenv("CIL_DEBUG_RECHECK");   // diagnostic: synchronising count print
         if (dbg && dbg[0] == '1') {

@@ -65,13 +65,15 @@ struct AugGeom {
     int64_t Kx, Ky;     // S*H*(W-1), S*(H-1)*W
     int64_t off[4];     // region starts (padded); off[3] = total row length
     int nreg;           // regions materialised (1 = value only, 2 = +D_x, 3 = +D_y)
+    uint32_t gs;        // species with derivative terms (bit s; 0 = all): others get 0 derivatives
 };
 
 inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
-inline AugGeom make_aug_geom(int S, int H, int W, int nreg) {
+inline AugGeom make_aug_geom(int S, int H, int W, int nreg, uint32_t gs = 0) {
     AugGeom a{};
     a.S = S; a.H = H; a.W = W;
+    a.gs = gs;
     a.K = (int64_t)S * H * W;
     a.Kx = (W > 1) ? (int64_t)S * H * (W - 1) : 0;
     a.Ky = (H > 1) ? (int64_t)S * (H - 1) * W : 0;
@@ -242,6 +244,7 @@ struct RecheckArgs {
     int q_tc[3];
     int S, H, W;
     double h;
+    uint32_t gs;
 };
 cudaError_t launch_recheck(const RecheckArgs& a, cudaStream_t st);
 

@@ -440,7 +440,8 @@ __global__ void __launch_bounds__(256) k_pack_i8_aug(RowSrc src, int64_t rows, A
     auto xt = [&](int64_t e) -> float { return __ldg(x + e) - __ldg(c + e); };
     float m0 = 0.f, mx = 0.f, my = 0.f, nfa = 0.f;
     for (int sr = w; sr < SH; sr += 8) {
-        const bool has_dy = (sr % H) + 1 < H;
+        const bool grad = g.gs == 0 || ((g.gs >> (sr / H)) & 1u);    // species mask (R18)
+        const bool has_dy = grad && (sr % H) + 1 < H;
         const int64_t base = (int64_t)sr * W;
         for (int c0 = 0; c0 < W; c0 += 32) {
             const int col = c0 + ln;
@@ -451,7 +452,7 @@ __global__ void __launch_bounds__(256) k_pack_i8_aug(RowSrc src, int64_t rows, A
             float xn = __shfl_down_sync(0xffffffffu, xe, 1);
             if (ln == 31 && col + 1 < W) xn = xt(base + col + 1);
             m0 = fmaxf(m0, fabsf(xe));
-            if (col + 1 < W) mx = fmaxf(mx, fabsf(xn - xe));
+            if (grad && col + 1 < W) mx = fmaxf(mx, fabsf(xn - xe));
             if (has_dy && in) my = fmaxf(my, fabsf(xt(base + W + col) - xe));
         }
     }
@@ -482,8 +483,9 @@ __global__ void __launch_bounds__(256) k_pack_i8_aug(RowSrc src, int64_t rows, A
         s2[a] += (uint64_t)((uint32_t)(q * q));
     };
     for (int sr = w; sr < SH; sr += 8) {
-        const bool has_dy = (sr % H) + 1 < H;
         const int s = sr / H;
+        const bool grad = g.gs == 0 || ((g.gs >> s) & 1u);
+        const bool has_dy = (sr % H) + 1 < H;
         const int64_t base = (int64_t)sr * W;
         for (int c0 = 0; c0 < W; c0 += 32) {
             const int col = c0 + ln;
@@ -493,8 +495,8 @@ __global__ void __launch_bounds__(256) k_pack_i8_aug(RowSrc src, int64_t rows, A
             if (ln == 31 && col + 1 < W) xn = xt(base + col + 1);
             if (!in) continue;
             put(0, kp0 + base + col, xe);
-            if (col + 1 < W) put(1, kp1 + (int64_t)sr * (W - 1) + col, xn - xe);
-            if (has_dy) put(2, kp2 + base - (int64_t)s * W + col, xt(base + W + col) - xe);
+            if (col + 1 < W) put(1, kp1 + (int64_t)sr * (W - 1) + col, grad ? xn - xe : 0.f);
+            if (has_dy) put(2, kp2 + base - (int64_t)s * W + col, grad ? xt(base + W + col) - xe : 0.f);
         }
     }
     // zero padding of every block
@@ -606,10 +608,11 @@ __global__ void __launch_bounds__(256) k_pack_aug(RowSrc src, int64_t rows, AugG
             const int64_t base = (int64_t)sr * W;
             const bool has_dy = g.nreg >= 3 && (sr % H) + 1 < H;
             const int s = sr / H;
+            const bool grad = g.gs == 0 || ((g.gs >> s) & 1u);     // species mask (R18): else 0
             for (int c = ln; c < W; c += 32) {
                 const float xe = __ldg(x + base + c);
-                if (c + 1 < W) o[g.off[1] + (int64_t)sr * (W - 1) + c] = __ldg(x + base + c + 1) - xe;
-                if (has_dy) o[g.off[2] + base - (int64_t)s * W + c] = __ldg(x + base + W + c) - xe;
+                if (c + 1 < W) o[g.off[1] + (int64_t)sr * (W - 1) + c] = grad ? __ldg(x + base + c + 1) - xe : 0.f;
+                if (has_dy) o[g.off[2] + base - (int64_t)s * W + c] = grad ? __ldg(x + base + W + c) - xe : 0.f;
             }
         }
         for (int64_t t = g.Kx + threadIdx.x; t < g.off[2] - g.off[1]; t += 256) o[g.off[1] + t] = 0.f;

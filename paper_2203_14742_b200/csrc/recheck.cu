@@ -33,13 +33,14 @@ __global__ void __launch_bounds__(256) k_recheck(RecheckArgs a) {
             double s0 = 0.0, sx = 0.0, sy = 0.0;
             // warp per grid row (s, r), lanes along the columns: coalesced, no index division
             for (int sr = w; sr < SH; sr += 8) {
-                const bool has_dy = (sr % H) + 1 < H;
+                const bool grad = a.gs == 0 || ((a.gs >> (sr / H)) & 1u);   // species mask (R18)
+                const bool has_dy = grad && (sr % H) + 1 < H;
                 const float* xr = x + (int64_t)sr * W;
                 const float* yr = y + (int64_t)sr * W;
                 for (int c = lane; c < W; c += 32) {
                     const double u = (double)__ldg(xr + c) - (double)__ldg(yr + c);
                     s0 += u * u;
-                    if (c + 1 < W) {                       // raw differences; the 1/h^2 is applied once
+                    if (grad && c + 1 < W) {               // raw differences; the 1/h^2 is applied once
                         const double dx = ((double)__ldg(xr + c + 1) - (double)__ldg(yr + c + 1)) - u;
                         sx += dx * dx;
                     }

@@ -462,3 +462,19 @@ def test_minmax_scale_bit_exact(cil, oracle_mod):
     radii = np.array([np.quantile(d, np.linspace(0.95, 0.05, 8)) for d in D])
     c, _, _ = _run_features(cil, torch.tensor(Yr[:25]), torch.tensor(Yr[25:]), grid, mask, radii, "AUTO")
     _check_counts(c[0], O.features(Yr[:25], Yr[25:], grid, mask, radii, band=BAND))
+
+
+@pytest.mark.parametrize("engine", ["AUTO", "SIMT"])
+@pytest.mark.parametrize("grid", [(2, 1, 64, 0.0, 0b10), (2, 16, 16, 0.0, 0b01)])
+def test_gradient_species_mask(cil, oracle_mod, engine, grid):
+    """Gradient-based norms w.r.t. selected species only (reading R18), all six
+    measures, on both the tensor-core and the CUDA-core engines."""
+    O = oracle_mod
+    dev = torch.device("cuda")
+    A = cilgen.make_set(99, 0, 70, grid[:3])
+    B = cilgen.make_set(99, 1, 55, grid[:3])
+    D = O.distance_matrix(A[:40].numpy(), B[:40].numpy(), grid, 0x3F)
+    radii = np.array([np.quantile(d, np.linspace(0.95, 0.05, 9)) for d in D])
+    c, _, st = _run_features(cil, A, B, grid, 0x3F, radii, engine)
+    assert int(st[0]) == 0
+    _check_counts(c[0], O.features(A.numpy(), B.numpy(), grid, 0x3F, radii, band=BAND))
