@@ -274,7 +274,7 @@ cil_status run_engines(int P, const RowSrc& asrc, const RowSrc& bsrc, int64_t ro
                        const SegParams& sp, const Layout& L, void* ws, const double* radii,
                        int64_t radii_stride, int32_t* status, cudaStream_t st, float* diag = nullptr,
                        uint8_t* binout = nullptr, bool keep_status = false,
-                       unsigned long long* range = nullptr) {
+                       unsigned long long* range = nullptr, int tile_skip = 0) {
     const int64_t K = (int64_t)g.S * g.H * g.W;
     BinParams bp{};
     bp.nq = sl.nq;
@@ -366,6 +366,7 @@ cil_status run_engines(int P, const RowSrc& asrc, const RowSrc& bsrc, int64_t ro
             t.part = at<float>(ws, L.off_part);
             t.ih = (float)(1.0 / bp.h);
             t.diag = diag;
+            t.skip = b_same ? tile_skip : 0;
             CIL_CU(launch_gram_i8(t, st));
         } else if (pl.split == 3) {
             // ---- INT8 two-digit engine (default): exact int32 accumulation
@@ -396,6 +397,8 @@ cil_status run_engines(int P, const RowSrc& asrc, const RowSrc& bsrc, int64_t ro
             t.diag = diag;
             t.binout = binout;
             t.b_same = b_same;
+            // symmetric bin matrix of one panel against itself: the upper tile triangle, mirrored
+            t.skip = (binout && b_same) ? 1 : (b_same ? tile_skip : 0);
             CIL_CU(launch_gram_i8(t, st));
         } else {
             // ---- 3xBF16 / 3xTF32 split engine (histogram mode only)
@@ -439,6 +442,7 @@ cil_status run_engines(int P, const RowSrc& asrc, const RowSrc& bsrc, int64_t ro
         r.list = list; r.ctr = ctr; r.cap = L.list_cap;
         r.status = status; r.P = P;
         r.binout = binout; r.rowsA = rowsA; r.rowsB = rowsB;
+        r.mirror = binout != nullptr && pl.split == 3 && !pl.aug && same_rows(asrc, bsrc) && rowsA == rowsB;
         for (int a = 0; a < 3; ++a) r.q_tc[a] = q_tc[a];
         r.S = g.S; r.H = g.H; r.W = g.W; r.h = bp.h; r.gs = g.gs;
         CIL_CU(launch_recheck(r, st));
@@ -676,7 +680,7 @@ cil_status cil_train_vectors(int32_t P, const float* X, int64_t stride, int64_t 
     xs.base = X; xs.stride = stride; xs.ld = ld; xs.rows = rows; xs.mode = MODE_PLAIN;
     // one panel against itself, segmented by subset: block (k, l) = C(R, s^k, s^l)
     cil_status s = run_engines(P, xs, xs, rows, rows, g, dist_mask, sl, M, pl, sp, L, wsa, radii, radii_stride,
-                               item_status, st);
+                               item_status, st, nullptr, nullptr, false, nullptr, /*tile_skip=*/2);
     if (s != CIL_OK) return s;
     CIL_CU(launch_build_pairs(P, n_ens, sl.nq, M, sp, at<uint64_t>(wsa, L.off_hist), N, Y, st));
     return CIL_OK;

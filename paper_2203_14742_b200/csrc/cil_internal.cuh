@@ -217,6 +217,7 @@ struct I8Args {
     float* part;                         // [P*rowsA*rowsB][4] FP32 phase partials (d2_0, E_0, d2_x, E_x)
     int q_tc[3];                         // histogram slot of L2, W12, W12SUM (-1: not requested)
     float ih;                            // 1/h
+    int skip;                            // tile skipping: 0 none, 1 symmetric bins, 2 Alg. 1 triangle
 };
 cudaError_t launch_gram_i8(const I8Args& a, cudaStream_t st);
 cudaError_t launch_pack_i8_aug(int P, const RowSrc& src, int64_t rows, const AugGeom& g, const int64_t* kp,
@@ -238,6 +239,7 @@ struct RecheckArgs {
     int32_t* status;
     int P;
     uint8_t* binout;     // non-null: write the exact bin to bins[p][q_l2][i][j] instead of moving counts
+    bool mirror;         // symmetric bin matrix: also write [j][i]
     int64_t rowsA, rowsB;
     // entries of the three-phase engine carry the measure kind in bits 8-15 of .w
     // (0 L2, 1 W12, 2 W12SUM); q_tc = their histogram slots, S/H/W the grid, h the spacing

@@ -56,6 +56,9 @@ struct I8Params {
     float2* part;              // [2][P*rowsA*rowsB] (d2, E) of phases 0 and 1
     int q_tc[3];               // histogram slots of L2, W12, W12SUM (-1: absent)
     float ih;                  // 1/h
+    int tiles_act;             // active tiles per item (tiles_m * tiles_n without skipping)
+    int skip;                  // 0 all tiles; 1 symmetric bin matrix (tiles mt > nt skipped, mirrored
+                               // by mt < nt); 2 only tiles meeting a block k < l (Alg. 1 triangle)
     int dbg;                   // diagnostic timing knob (CIL_DEBUG_I8): 1 skip binning, 2 skip the epilogue,
                                // 3 also skip the B loads, 4 all loads
 };
@@ -84,6 +87,40 @@ template <int MAXM, bool SEG, bool AUG = false> struct I8Geo {
     static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 1024 /*barriers*/ +
                                       3 * TILE_N * 4 /*norms, sigma, spare*/ + NKIND * 2 * MAXM * 4 + HIST_BYTES;
 };
+
+// Which tiles a launch computes.  With tile skipping the active tiles of a tile row mt are a
+// suffix [start(mt), tiles_n) of the row, so they are enumerated compactly (no idle clusters):
+//   skip 1 (symmetric bin matrix, mirrored writes): start = mt (upper triangle incl. diagonal);
+//   skip 2 (Alg. 1: blocks k < l only): start = first tile whose last column lies in a later
+//          column segment than the tile's first row's segment.
+__host__ __device__ inline int tile_row_start(int skip, int mt, int64_t row_seg, int64_t col_seg, int64_t rowsB) {
+    if (skip == 1) return mt;
+    const int64_t k0 = (int64_t)mt * Geo<2>::TILE_M / row_seg;      // segment of the tile's first row
+    // smallest nt with min((nt+1)*TILE_N, rowsB) - 1 >= (k0 + 1) * col_seg
+    const int64_t need = (k0 + 1) * col_seg;                         // first column of segment k0 + 1
+    if (need > rowsB - 1) return 1 << 30;
+    return (int)(need / TILE_N);
+}
+__host__ __device__ inline int tiles_active(int skip, int tiles_m, int tiles_n, int64_t row_seg, int64_t col_seg,
+                                            int64_t rowsB) {
+    if (skip == 0) return tiles_m * tiles_n;
+    int n = 0;
+    for (int mt = 0; mt < tiles_m; ++mt) {
+        const int s = tile_row_start(skip, mt, row_seg, col_seg, rowsB);
+        if (s < tiles_n) n += tiles_n - s;
+    }
+    return n;
+}
+__device__ __forceinline__ void tile_of(const I8Params& prm, int u, int& mt, int& nt) {
+    if (prm.skip == 0) { mt = u / prm.tiles_n; nt = u % prm.tiles_n; return; }
+    for (mt = 0; mt < prm.tiles_m; ++mt) {
+        const int s = tile_row_start(prm.skip, mt, prm.sp.row_seg, prm.sp.col_seg, prm.rowsB);
+        const int cnt = s < prm.tiles_n ? prm.tiles_n - s : 0;
+        if (u < cnt) { nt = s + u; return; }
+        u -= cnt;
+    }
+    mt = nt = 0;                                                     // not reached
+}
 
 // b = #{m : v < T_m} for decreasing thresholds T[0..MAXM) padded with -inf to 2*MAXM
 template <int MAXM>
@@ -115,8 +152,9 @@ __device__ __forceinline__ void epilogue_aug(const I8Params& prm, uint32_t tmem_
     const int64_t npairs = (int64_t)prm.P * prm.rowsA * prm.rowsB;
     uint32_t tph = 0;
     for (int t = cluster_id; t < total_tiles; t += n_clusters) {
-        const int p = prm.p0 + t / tiles_per_item, r = t % tiles_per_item;
-        const int mt = r / prm.tiles_n, nt = r % prm.tiles_n;
+        const int p = prm.p0 + t / tiles_per_item;
+        int mt, nt;
+        tile_of(prm, t % tiles_per_item, mt, nt);
         const int64_t col0 = (int64_t)nt * TILE_N;
         const int64_t browbase = prm.b_off + (int64_t)p * prm.rowsB;
         const int64_t row = (int64_t)mt * G::TILE_M + rank * A_ROWS + quarter * 32 + lane;
@@ -287,7 +325,7 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_rank();
     const int cluster_id = blockIdx.x / 2, n_clusters = gridDim.x / 2;
-    const int tiles_per_item = prm.tiles_m * prm.tiles_n;
+    const int tiles_per_item = prm.tiles_act;
     const int total_tiles = prm.np * tiles_per_item;
 
     if (warp == 0 && lane == 0) {
@@ -317,8 +355,9 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
             int stage = 0;
             uint32_t phase = 0;
             for (int t = cluster_id; t < total_tiles; t += n_clusters) {
-                const int p = prm.p0 + t / tiles_per_item, r = t % tiles_per_item;
-                const int mt = r / prm.tiles_n, nt = r % prm.tiles_n;
+                const int p = prm.p0 + t / tiles_per_item;
+                int mt, nt;
+                tile_of(prm, t % tiles_per_item, mt, nt);
                 const int ya = (int)(p * prm.rowsA + (int64_t)mt * G::TILE_M + rank * A_ROWS);
                 const int yb = (int)(prm.b_off + p * prm.rowsB + (int64_t)nt * TILE_N + rank * G::B_ROWS);
                 for (int kb = 0; kb < prm.n_kb; ++kb) {
@@ -393,8 +432,9 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
         const int M = prm.M;
         uint32_t tph = 0;
         for (int t = cluster_id; t < total_tiles; t += n_clusters) {
-            const int p = prm.p0 + t / tiles_per_item, r = t % tiles_per_item;
-            const int mt = r / prm.tiles_n, nt = r % prm.tiles_n;
+            const int p = prm.p0 + t / tiles_per_item;
+            int mt, nt;
+            tile_of(prm, t % tiles_per_item, mt, nt);
             const int64_t col0 = (int64_t)nt * TILE_N;
             const int64_t browbase = prm.b_off + (int64_t)p * prm.rowsB;
             named_bar(1, 256);
@@ -442,6 +482,8 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
             uint8_t* binrow = (prm.binout != nullptr && row_ok)
                                   ? prm.binout + (((int64_t)p * prm.nq + prm.q_l2) * prm.rowsA + row) * prm.rowsB
                                   : nullptr;
+            const bool mirror = binrow != nullptr && prm.skip == 1 && mt < nt;
+            uint8_t* mbase = mirror ? prm.binout + ((int64_t)p * prm.nq + prm.q_l2) * prm.rowsA * prm.rowsB + row : nullptr;
 
 #pragma unroll 1
             for (int g = 0; g < 8 && !skip; ++g) {
@@ -506,6 +548,11 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
 #pragma unroll
                         for (int jj = 0; jj < 16; ++jj)
                             if (g * 16 + jj < nvalid) dst[jj] = (uint8_t)(bin[jj] & 255);
+                    }
+                    if (mirror) {        // symmetric bin matrix: (j, i) from the upper tile (i, j)
+#pragma unroll
+                        for (int jj = 0; jj < 16; ++jj)
+                            if (g * 16 + jj < nvalid) mbase[(int64_t)(hc0 + g * 16 + jj) * prm.rowsB] = (uint8_t)(bin[jj] & 255);
                     }
                 } else {
 #pragma unroll
@@ -599,7 +646,7 @@ static cudaError_t launch_i8_t(const tc::I8Params& prm, const CUtensorMap* maps,
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    const int64_t tiles = (int64_t)prm.np * prm.tiles_m * prm.tiles_n;
+    const int64_t tiles = (int64_t)prm.np * prm.tiles_act;
     const int clusters = (int)(tiles < nsm / 2 ? tiles : nsm / 2);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)(clusters * 2));
@@ -651,6 +698,9 @@ cudaError_t launch_gram_i8(const I8Args& a, cudaStream_t st) {
     prm.kq = a.kq; prm.kll = a.kll; prm.rel = a.rel;
     prm.diag = a.diag;
     prm.binout = a.binout;
+    prm.skip = a.skip;
+    prm.tiles_act = tc::tiles_active(prm.skip, prm.tiles_m, prm.tiles_n, a.sp.row_seg, a.sp.col_seg, a.rowsB);
+    if (prm.tiles_act == 0) return cudaSuccess;
     prm.nph = a.nph == 3 ? 3 : 1;
     if (prm.nph == 3) {
         for (int i = 0; i < 3; ++i) { prm.kb_end[i] = a.kb_end[i]; prm.kll3[i] = a.kll3[i]; prm.q_tc[i] = a.q_tc[i]; }

@@ -114,6 +114,7 @@ __global__ void __launch_bounds__(256) k_recheck(RecheckArgs a) {
             while (b < a.M && s < R[b] * R[b] / a.w) ++b;
             if (a.binout) {
                 a.binout[(((int64_t)p * a.nq + a.q_l2) * a.rowsA + i) * a.rowsB + j] = (uint8_t)b;
+                if (a.mirror) a.binout[(((int64_t)p * a.nq + a.q_l2) * a.rowsA + j) * a.rowsB + i] = (uint8_t)b;
             } else if (b != b_lo) {
                 const int64_t rs = i / a.sp.row_seg, cs = j / a.sp.col_seg;
                 unsigned long long* H = (unsigned long long*)a.hist;
