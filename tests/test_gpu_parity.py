@@ -478,3 +478,19 @@ def test_gradient_species_mask(cil, oracle_mod, engine, grid):
     c, _, st = _run_features(cil, A, B, grid, 0x3F, radii, engine)
     assert int(st[0]) == 0
     _check_counts(c[0], O.features(A.numpy(), B.numpy(), grid, 0x3F, radii, band=BAND))
+
+
+def test_c5_shape_large_K(cil, oracle_mod):
+    """C5-shaped patterns (256x256x2, K = 131072 > 65536: AUTO takes the chunked 3xBF16 engine
+    for L2, the CUDA cores for the rest), ragged 200 x 150 pairs, L2 + W12 + Linf."""
+    O = oracle_mod
+    dev = torch.device("cuda")
+    grid = (2, 256, 256, 0.0)
+    A = cilgen.make_set(101, 0, 200, grid[:3])
+    B = cilgen.make_set(101, 1, 150, grid[:3])
+    mask = 0x0B
+    D = O.distance_matrix(A[:30].numpy(), B[:30].numpy(), grid, mask)
+    radii = np.array([np.quantile(d, np.linspace(0.97, 0.03, 12)) for d in D])
+    c, _, st = _run_features(cil, A, B, grid, mask, radii, "AUTO")
+    assert int(st[0]) == 0
+    _check_counts(c[0], O.features(A.numpy(), B.numpy(), grid, mask, radii, band=BAND))
