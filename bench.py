@@ -44,6 +44,9 @@ C4 = dict(name="C4", grid=(1, 128, 128), P=256, n_ens=10, N_set=50, N_tilde=50, 
 C6 = dict(name="C6", grid=(2, 64, 64), P=64, N_syn=1000, N_set=50, n_rep=1000, M=13, mask=1,
           workload="C6: SCIL with bootstrapping (Alg. A2), 64 proposals x pool 1000 of 64x64x2, N_set=50, "
                    "n_CIL=1000 replicates, L2, M=13 (PAPER.md:563-564)")
+C7 = dict(name="C7", grid=(2, 64, 64), N_set=3000, n_ens=10, M=13, mask=0x3F,
+          workload="C7: MCIL-6 training vectors (Alg. 2 steps 1-2) of N_set=3000 GM 64x64x2 patterns, "
+                   "n_ens=10 subsets of 300, all six measures, M=13 (PAPER.md:199, 206-226)")
 
 
 def log(*a):
@@ -210,6 +213,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-c4", action="store_true")
     ap.add_argument("--no-c6", action="store_true")
+    ap.add_argument("--no-c7", action="store_true")
     ap.add_argument("--config", default="C2", choices=["C2", "C3"],
                     help="C2 = the headline bench line; C3 = evidence run of the CUDA-core measures")
     args = ap.parse_args()
@@ -390,6 +394,9 @@ def main():
     c6 = None
     if not args.no_c6:
         c6 = bench_c6(cil, args, world, rank, dev, engine, stream)
+    c7 = None
+    if not args.no_c7:
+        c7 = bench_c7(cil, args, world, rank, dev, engine, stream)
 
     # ---- CPU baseline: the oracle as it stands, bounded sample, rank 0 at N = 1 only
     cpu = None
@@ -420,6 +427,7 @@ def main():
             "cpu_baseline": cpu,
             "secondary": c4,
             "secondary_bootstrap": c6,
+            "secondary_train": c7,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -577,6 +585,37 @@ def bench_c6(cil, args, world, rank, dev, engine, stream):
                            "lookups_per_s": P * n_rep * N_set * Nt / (r_ms / steps * 1e-3)}
     res["kernel_breakdown"] = {k: round(v[0] / steps, 4) for k, v in prof.items() if v[1] > 0}
     return res
+
+
+def bench_c7(cil, args, world, rank, dev, engine, stream):
+    """Secondary line for the Alg. 1 / Alg. 2 training row: the C(n_ens, 2)
+    subset-pair vectors of one large data set, all six measures (L2-type family on the
+    tensor cores, max family on the CUDA cores, k >= l tiles skipped)."""
+    cfg = C7
+    grid, N_set, n_ens, M, mask = cfg["grid"], cfg["N_set"], cfg["n_ens"], cfg["M"], cfg["mask"]
+    seed = cilgen.config_seed(7)
+    X = cilgen.make_set(seed, rank, N_set, grid, device=dev)
+    N = N_set // n_ens
+    radii = torch.tensor(pilot_radii_all(X[:N], X[N:2 * N], grid, M, mask), dtype=torch.float64, device=dev)
+    ws = cil.Workspace()
+
+    def step():
+        cil.train_vectors(X, n_ens, grid, mask, radii, engine=engine, ws=ws)
+
+    for _ in range(max(2, args.warmup)):
+        step()
+    steps = max(3, args.steps // 80)
+    from paper_2203_14742_b200 import _capi
+    _capi.prof_enable(True)
+    ms = timed(step, steps, stream)
+    _capi.prof_enable(False)
+    prof = _capi.prof_read()
+    ms_step = ms / steps
+    nv = n_ens * (n_ens - 1) // 2
+    return {"workload": cfg["workload"], "metric": "training vectors/s", "value": world * nv / (ms_step * 1e-3),
+            "ms_per_step": round(ms_step, 3), "steps": steps,
+            "pairs_per_s": world * nv * N * N / (ms_step * 1e-3),
+            "kernel_breakdown": {k: round(v[0] / steps, 4) for k, v in prof.items() if v[1] > 0}}
 
 
 def bench_c4(cil, args, world, rank, dev, engine, stream):

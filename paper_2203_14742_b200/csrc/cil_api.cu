@@ -312,6 +312,7 @@ cil_status run_engines(int P, const RowSrc& asrc, const RowSrc& bsrc, int64_t ro
             if ((pl.simt_mask >> sl.slot[q]) & 1u) a.qmask |= 1u << q;
         a.binout = binout;
         a.range = range;
+        a.tri = tile_skip == 2;
         CIL_CU(launch_simt(a, st));
     }
     if (pl.tc) {

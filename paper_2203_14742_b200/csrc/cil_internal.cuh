@@ -162,6 +162,7 @@ struct SimtArgs {
     uint32_t qmask;                           // slots binned by this engine
     uint8_t* binout;                          // non-null: bins[p][q][i][j] instead of counts
     unsigned long long* range;                // non-null: [P][nq][2] min (d > 0) / max of d as FP64 bits
+    bool tri;                                 // skip tiles without a block k < l (Alg. 1 training)
     int hist_cap;                             // shared histogram entries (set by the launcher)
 };
 cudaError_t launch_simt(const SimtArgs& a, cudaStream_t st);

@@ -54,6 +54,8 @@ __global__ void __launch_bounds__(NTHR, DO_SUM ? 2 : 4) k_simt(SimtArgs a) {
     if (a.status[p] & CIL_ITEM_BADRADII) return;
     const int64_t row0 = (int64_t)blockIdx.y * TA;
     const int64_t col0 = (int64_t)blockIdx.x * TB;
+    // Alg. 1 triangle: a tile without any block k < l has nothing to count
+    if (a.tri && row0 / a.sp.row_seg >= (min(col0 + TB, a.rowsB) - 1) / a.sp.col_seg) return;
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
     const int ty = (warp >> 1) * 4 + (lane >> 3);   // 0..7
