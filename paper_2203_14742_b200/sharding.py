@@ -10,6 +10,11 @@ Two partitions:
     (`row_range`), runs cil_features on its shard, then one all_reduce(SUM) of the int64
     count vectors — the only exchange (<= n_meas * M * 8 bytes).  Integer sums are
     order-free, so counts are bit-identical for every G.
+  * a pair too large for one GPU's memory ("ring-pass of B shards"): every
+    rank holds one shard of A and one of B; in G steps the B shards travel around the ring
+    (send to rank r+1, receive from r-1, double-buffered so the transfer of the next shard
+    overlaps the counts of the current one), each rank counting its A shard against every
+    B shard; then the same all_reduce(SUM).  No rank ever holds more than 2 B shards.
 """
 from __future__ import annotations
 
@@ -65,3 +70,46 @@ def gather_vectors(y_local: torch.Tensor, *, group=None) -> torch.Tensor:
                       device=y_local.device)
     dist.all_gather_into_tensor(out, y_local.contiguous(), group=group)
     return out
+
+
+def ring_features(A_local, B_local, grid, mask, radii, N_total: int, Nt_total: int, *, group=None,
+                  features_fn=None, normalize_fn=None, **kw):
+    """Counts / y of ONE set pair with both A and B row-sharded across the group (ring-pass).
+
+    A_local: this rank's rows of A; B_local: this rank's rows of B, shard r = rows
+    row_range(Nt_total, G, r) of B ([n, S, H, W] tensors on the compute device).
+    features_fn / normalize_fn as in `sharded_features`.  Returns (counts, y, status) of the
+    whole pair, identical on every rank."""
+    if features_fn is None:
+        from . import features as features_fn  # CUDA path
+    world, rank = _world(group)
+    sizes = [row_range(Nt_total, world, r)[1] - row_range(Nt_total, world, r)[0] for r in range(world)]
+    if B_local.shape[0] != sizes[rank]:
+        raise ValueError("B_local must be shard row_range(Nt_total, world, rank) of B")
+    shape = (max(sizes),) + tuple(B_local.shape[1:])
+    cur = torch.zeros(shape, dtype=B_local.dtype, device=B_local.device)
+    nxt = torch.zeros_like(cur)
+    cur[:sizes[rank]].copy_(B_local)
+    counts = None
+    status = None
+    src = rank                                   # owner of the shard in `cur`
+    for step in range(world):
+        reqs = []
+        if step + 1 < world:                     # start passing this shard on before counting it
+            reqs.append(dist.isend(cur, (rank + 1) % world, group=group))
+            reqs.append(dist.irecv(nxt, (rank - 1) % world, group=group))
+        c, _, st = features_fn(A_local, cur[:sizes[src]], grid, mask, radii, want_y=False, **kw)
+        counts = c if counts is None else counts + c
+        status = st if status is None else torch.maximum(status, st)
+        for r in reqs:
+            r.wait()
+        cur, nxt = nxt, cur
+        src = (src - 1) % world
+    if world > 1:
+        dist.all_reduce(counts, op=dist.ReduceOp.SUM, group=group)
+        dist.all_reduce(status, op=dist.ReduceOp.MAX, group=group)
+    npairs = float(N_total) * float(Nt_total)
+    if normalize_fn is None:
+        from . import normalize as normalize_fn
+    y = normalize_fn(counts, npairs)
+    return counts, y, status

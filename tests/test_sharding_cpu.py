@@ -95,3 +95,51 @@ def test_row_range_partition():
             assert rs[0][0] == 0 and rs[-1][1] == n
             assert all(rs[i][1] == rs[i + 1][0] for i in range(w - 1))
             assert max(h - l for l, h in rs) - min(h - l for l, h in rs) <= 1
+
+
+def _ring_worker(rank, world, port, q):
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import cilgen
+        from paper_2203_14742_b200 import sharding
+        grid = (1, 6, 6, 0.0)
+        N, Nt = 17, 11
+        A = cilgen.make_set(78, 0, N, grid[:3])
+        B = cilgen.make_set(78, 1, Nt, grid[:3])
+        radii = torch.tensor([np.geomspace(3.0, 0.5, 6), np.geomspace(3.0, 0.3, 6)])
+        a0, a1 = sharding.row_range(N, world, rank)
+        b0, b1 = sharding.row_range(Nt, world, rank)
+        counts, y, st = sharding.ring_features(A[a0:a1], B[b0:b1].clone(), grid, 0b11, radii, N, Nt,
+                                               features_fn=_oracle_features, normalize_fn=_normalize)
+        q.put((rank, counts.numpy(), y.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_ring_pass_counts_equal_unsharded(oracle_mod, world):
+    """Both A and B sharded; B shards travel around the ring: the counts on
+    every rank equal the unsharded oracle counts (uneven shards: 17 and 11 rows)."""
+    import cilgen
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ring_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    grid = (1, 6, 6, 0.0)
+    A = cilgen.make_set(78, 0, 17, grid[:3]).numpy()
+    B = cilgen.make_set(78, 1, 11, grid[:3]).numpy()
+    radii = np.array([np.geomspace(3.0, 0.5, 6), np.geomspace(3.0, 0.3, 6)])
+    full = oracle_mod.features(A, B, grid, 0b11, radii, band=0.0)
+    for rank, counts, y in res:
+        np.testing.assert_array_equal(counts[0], full["counts"])
+        np.testing.assert_array_equal(y[0], full["counts"] / (17 * 11))
