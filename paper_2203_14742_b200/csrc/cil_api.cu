@@ -534,16 +534,51 @@ cil_status cil_loglik(int32_t P, const double* mu, int64_t mu_stride, const doub
     return CIL_OK;
 }
 
+namespace {
+// SCIL panel geometry.  The Gram tiles 256 rows x (256 or 192) columns; when the row panel
+// ((n_ens+1) N_set rows, e.g. 550) pads worse on the 256-row axis than the column panel
+// (n_ens N~, e.g. 500), the panels are swapped (the column panel runs as the Gram's rows;
+// segments become [l][k], k_build_Y reads them transposed).  Only for the INT8 engine.
+struct SynthGeo {
+    bool swap;
+    int64_t rowsA, rowsB;     // Gram rows / columns
+    SegParams sp;
+    Plan pl;
+};
+int64_t pad_cols(int64_t n) {
+    const int64_t a = (n + 255) / 256 * 256, b = (n + 191) / 192 * 192;
+    return a < b ? a : b;
+}
+SynthGeo synth_geo(int32_t n_ens, int32_t N_set, int32_t N_tilde, const cil_grid& g, uint32_t mask, int32_t M,
+                   cil_engine engine) {
+    SynthGeo s{};
+    const int64_t R = (int64_t)(n_ens + 1) * N_set, C = (int64_t)n_ens * N_tilde;
+    s.swap = false;
+    s.rowsA = R; s.rowsB = C;
+    s.sp = SegParams{N_set, N_tilde, n_ens + 1, n_ens};
+    s.pl = make_plan(mask, engine, g, N_tilde, C, M);
+    const int64_t cost = (R + 255) / 256 * 256 * pad_cols(C), cost_sw = (C + 255) / 256 * 256 * pad_cols(R);
+    if (cost_sw < cost && s.pl.tc && s.pl.split == 3) {
+        const Plan ps = make_plan(mask, engine, g, N_set, R, M);
+        if (ps.tc && ps.split == 3 && ps.aug == s.pl.aug) {
+            s.swap = true;
+            s.rowsA = C; s.rowsB = R;
+            s.sp = SegParams{N_tilde, N_set, n_ens, n_ens + 1};
+            s.pl = ps;
+        }
+    }
+    return s;
+}
+}  // namespace
+
 size_t cil_synth_workspace_size(int32_t P, int32_t n_ens, int32_t N_set, int32_t N_tilde, cil_grid g,
                                 uint32_t dist_mask, int32_t M, cil_engine engine) {
     if (P < 1 || n_ens < 2 || N_set < 1 || N_tilde < 1 || M < 1 || check_grid(g, dist_mask) != CIL_OK)
         return 0;
     const Slots sl = slots_of(dist_mask);
-    const Plan pl = make_plan(dist_mask, engine, g, N_tilde, (int64_t)n_ens * N_tilde, M);
-    const int64_t rowsA = (int64_t)(n_ens + 1) * N_set, rowsB = (int64_t)n_ens * N_tilde;
-    SegParams sp{N_set, N_tilde, n_ens + 1, n_ens};
+    const SynthGeo sg = synth_geo(n_ens, N_set, N_tilde, g, dist_mask, M, engine);
     const int64_t nY = (int64_t)P * (n_ens * n_ens + 1) * sl.nq * M;
-    return make_layout(P, rowsA, rowsB, g, sl.nq, M, pl, sp, nY).total;
+    return make_layout(P, sg.rowsA, sg.rowsB, g, sl.nq, M, sg.pl, sg.sp, nY).total;
 }
 
 cil_status cil_synth_loglik(int32_t P, const float* pools, int64_t pool_stride, int64_t ld, int32_t n_ens,
@@ -565,12 +600,13 @@ cil_status cil_synth_loglik(int32_t P, const float* pools, int64_t pool_stride, 
     if (!aligned16(pools) || !aligned16(data)) return CIL_EUNSUPPORTED;
     const Slots sl = slots_of(dist_mask);
     if (sl.nq * M > kMaxD) return CIL_EUNSUPPORTED;
-    const Plan pl = make_plan(dist_mask, engine, g, N_tilde, (int64_t)n_ens * N_tilde, M);
+    const SynthGeo sg = synth_geo(n_ens, N_set, N_tilde, g, dist_mask, M, engine);
+    const Plan& pl = sg.pl;
     const int64_t rowsA = (int64_t)(n_ens + 1) * N_set, rowsB = (int64_t)n_ens * N_tilde;
-    SegParams sp{N_set, N_tilde, n_ens + 1, n_ens};
+    const SegParams& sp = sg.sp;
     const int nv = n_ens * n_ens;
     const int64_t nY = (int64_t)P * (nv + 1) * sl.nq * M;
-    const Layout L = make_layout(P, rowsA, rowsB, g, sl.nq, M, pl, sp, nY);
+    const Layout L = make_layout(P, sg.rowsA, sg.rowsB, g, sl.nq, M, pl, sp, nY);
     if (ws_bytes < L.total) return CIL_ENOMEM;
     void* wsa = reinterpret_cast<void*>(((uintptr_t)ws + 255) & ~(uintptr_t)255);
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
@@ -579,12 +615,15 @@ cil_status cil_synth_loglik(int32_t P, const float* pools, int64_t pool_stride, 
     as.n_ens = n_ens; as.N_set = N_set; as.N_tilde = N_tilde; as.data = data; as.ld_data = ld_data;
     bs = as;
     bs.rows = rowsB; bs.mode = MODE_SYN_COL;
-    cil_status s = run_engines(P, as, bs, rowsA, rowsB, g, dist_mask, sl, M, pl, sp, L, wsa, radii,
-                               (int64_t)sl.nq * M, item_status, st);
+    cil_status s = sg.swap ? run_engines(P, bs, as, rowsB, rowsA, g, dist_mask, sl, M, pl, sp, L, wsa, radii,
+                                         (int64_t)sl.nq * M, item_status, st)
+                           : run_engines(P, as, bs, rowsA, rowsB, g, dist_mask, sl, M, pl, sp, L, wsa, radii,
+                                         (int64_t)sl.nq * M, item_status, st);
     if (s != CIL_OK) return s;
     double* Y = Y_out ? Y_out : at<double>(wsa, L.off_Y);
     CIL_CU(launch_synth_tail(P, n_ens, sl.nq, M, sp, at<uint64_t>(wsa, L.off_hist), N_set, N_tilde, k0, ridge,
-                             out, item_status, Y, at<double>(wsa, L.off_mu), at<double>(wsa, L.off_sig), st));
+                             out, item_status, Y, at<double>(wsa, L.off_mu), at<double>(wsa, L.off_sig), st,
+                             sg.swap));
     return CIL_OK;
 }
 

@@ -282,5 +282,6 @@ cudaError_t launch_loglik(int P, const double* mu, int64_t mu_stride, const doub
                           int32_t* status, const int32_t* status_in, cudaStream_t st);
 cudaError_t launch_synth_tail(int P, int n_ens, int nq, int M, const SegParams& sp, const uint64_t* hist,
                               int64_t N_set, int64_t N_tilde, const int32_t* k0, double ridge, double* out,
-                              int32_t* status, double* Y, double* mu, double* Sigma, cudaStream_t st);
+                              int32_t* status, double* Y, double* mu, double* Sigma, cudaStream_t st,
+                              bool swapped = false);
 }  // namespace cil

@@ -56,6 +56,7 @@ struct I8Params {
     float2* part;              // [2][P*rowsA*rowsB] (d2, E) of phases 0 and 1
     int q_tc[3];               // histogram slots of L2, W12, W12SUM (-1: absent)
     float ih;                  // 1/h
+    int tn;                    // B columns per tile (the kernel's TN)
     int tiles_act;             // active tiles per item (tiles_m * tiles_n without skipping)
     int skip;                  // 0 all tiles; 1 symmetric bin matrix (tiles mt > nt skipped, mirrored
                                // by mt < nt); 2 only tiles meeting a block k < l (Alg. 1 triangle)
@@ -73,9 +74,15 @@ __host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
     return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
-template <int MAXM, bool SEG, bool AUG = false> struct I8Geo {
-    static constexpr int STAGES = (MAXM <= 16 && !AUG) ? 3 : 2;
-    static constexpr int STAGE_BYTES = Geo<2>::STAGE_BYTES;       // 64 KB: h, l of 128 A- and 128 B-rows
+template <int MAXM, bool SEG, bool AUG = false, int TN = 256> struct I8Geo {
+    // tile = 256 A rows (CTA pair) x TN B columns (TN = 256, or 192 to cut padding of ~550-row
+    // panels); each CTA stages 128 A rows and TN/2 B rows per 128-byte K block
+    static constexpr int B_ROWS = TN / 2;
+    static constexpr int A_BYTES = A_ROWS * ROW_BYTES;
+    static constexpr int B_BYTES = B_ROWS * ROW_BYTES;
+    static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;  // 64 KB (TN 256) / 56 KB (TN 192)
+    static constexpr int HALF = TN / 2;                             // columns per epilogue warp
+    static constexpr int NG = HALF / 16;                            // 16-column TMEM groups per warp
     // per-thread histograms [bin][thread] of u32 cells (bank = thread, conflict-free); with column
     // segments (SCIL blocks of >= 43 columns, so a 128-column half meets <= 4) byte l of a cell
     // counts local segment l (<= 128 pairs per tile, flushed every tile).  AUG (three measure
@@ -84,8 +91,10 @@ template <int MAXM, bool SEG, bool AUG = false> struct I8Geo {
     static constexpr int NLOC = SEG ? 4 : 1;
     static constexpr int NKIND = AUG ? 3 : 1;
     static constexpr int HIST_BYTES = (AUG && SEG ? 3 : 1) * (MAXM + 1) * 256 * 4;
-    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 1024 /*barriers*/ +
-                                      3 * TILE_N * 4 /*norms, sigma, spare*/ + NKIND * 2 * MAXM * 4 + HIST_BYTES;
+    static constexpr int FIXED = 1024 /*align*/ + 1024 /*barriers*/ + 3 * TN * 4 /*norms, sigma, spare*/ +
+                                 NKIND * 2 * MAXM * 4 + HIST_BYTES;
+    static constexpr int STAGES = (3 * STAGE_BYTES + FIXED <= 227 * 1024) ? 3 : 2;
+    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + FIXED;
 };
 
 // Which tiles a launch computes.  With tile skipping the active tiles of a tile row mt are a
@@ -93,20 +102,21 @@ template <int MAXM, bool SEG, bool AUG = false> struct I8Geo {
 //   skip 1 (symmetric bin matrix, mirrored writes): start = mt (upper triangle incl. diagonal);
 //   skip 2 (Alg. 1: blocks k < l only): start = first tile whose last column lies in a later
 //          column segment than the tile's first row's segment.
-__host__ __device__ inline int tile_row_start(int skip, int mt, int64_t row_seg, int64_t col_seg, int64_t rowsB) {
+__host__ __device__ inline int tile_row_start(int skip, int mt, int64_t row_seg, int64_t col_seg, int64_t rowsB,
+                                              int tn) {
     if (skip == 1) return mt;
     const int64_t k0 = (int64_t)mt * Geo<2>::TILE_M / row_seg;      // segment of the tile's first row
-    // smallest nt with min((nt+1)*TILE_N, rowsB) - 1 >= (k0 + 1) * col_seg
+    // smallest nt with min((nt+1)*tn, rowsB) - 1 >= (k0 + 1) * col_seg
     const int64_t need = (k0 + 1) * col_seg;                         // first column of segment k0 + 1
     if (need > rowsB - 1) return 1 << 30;
-    return (int)(need / TILE_N);
+    return (int)(need / tn);
 }
 __host__ __device__ inline int tiles_active(int skip, int tiles_m, int tiles_n, int64_t row_seg, int64_t col_seg,
-                                            int64_t rowsB) {
+                                            int64_t rowsB, int tn) {
     if (skip == 0) return tiles_m * tiles_n;
     int n = 0;
     for (int mt = 0; mt < tiles_m; ++mt) {
-        const int s = tile_row_start(skip, mt, row_seg, col_seg, rowsB);
+        const int s = tile_row_start(skip, mt, row_seg, col_seg, rowsB, tn);
         if (s < tiles_n) n += tiles_n - s;
     }
     return n;
@@ -114,7 +124,7 @@ __host__ __device__ inline int tiles_active(int skip, int tiles_m, int tiles_n, 
 __device__ __forceinline__ void tile_of(const I8Params& prm, int u, int& mt, int& nt) {
     if (prm.skip == 0) { mt = u / prm.tiles_n; nt = u % prm.tiles_n; return; }
     for (mt = 0; mt < prm.tiles_m; ++mt) {
-        const int s = tile_row_start(prm.skip, mt, prm.sp.row_seg, prm.sp.col_seg, prm.rowsB);
+        const int s = tile_row_start(prm.skip, mt, prm.sp.row_seg, prm.sp.col_seg, prm.rowsB, prm.tn);
         const int cnt = s < prm.tiles_n ? prm.tiles_n - s : 0;
         if (u < cnt) { nt = s + u; return; }
         u -= cnt;
@@ -146,13 +156,13 @@ __device__ __forceinline__ int bin_search(float v, const float* T) {
 //   L2^2/w = d2_0,   W12^2/w = d2_0 + (d2_x + d2_y)/h^2,   W12SUM/sqrt(w) = sqrt d2_0 + (sqrt d2_x + sqrt d2_y)/h
 // (Eqs. (5), (8), (7) with readings R1, R3) with their bounds, bins the requested ones and
 // sends pairs with a threshold inside the bound to the FP64 re-check (kind in bits 8-15).
-template <int MAXM, bool SEG>
+template <int MAXM, bool SEG, int TN>
 __device__ __forceinline__ void epilogue_aug(const I8Params& prm, uint32_t tmem_base, uint64_t* tfull,
                                              uint64_t* tempty, float* s_nb, float* s_sb, float* s_T,
                                              uint32_t* hist_s, int cluster_id, int n_clusters, int total_tiles,
                                              int tiles_per_item, uint32_t rank, int warp, int lane) {
     using G = Geo<2>;
-    using IG = I8Geo<MAXM, SEG, true>;
+    using IG = I8Geo<MAXM, SEG, true, TN>;
     const int quarter = warp & 3;
     const int half = (warp - 2) >> 2;
     const int et = threadIdx.x - 64;
@@ -163,20 +173,20 @@ __device__ __forceinline__ void epilogue_aug(const I8Params& prm, uint32_t tmem_
         const int p = prm.p0 + t / tiles_per_item;
         int mt, nt;
         tile_of(prm, t % tiles_per_item, mt, nt);
-        const int64_t col0 = (int64_t)nt * TILE_N;
+        const int64_t col0 = (int64_t)nt * TN;
         const int64_t browbase = prm.b_off + (int64_t)p * prm.rowsB;
         const int64_t row = (int64_t)mt * G::TILE_M + rank * A_ROWS + quarter * 32 + lane;
         const bool row_ok = row < prm.rowsA;
         const int64_t arow = (int64_t)p * prm.rowsA + (row_ok ? row : 0);
-        const int hc0 = (int)(col0 + half * 128);
-        const int nvalid = (int)min((int64_t)128, prm.rowsB - hc0);
-        const uint32_t tl = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(half * 128);
+        const int hc0 = (int)(col0 + half * IG::HALF);
+        const int nvalid = (int)min((int64_t)IG::HALF, prm.rowsB - hc0);
+        const uint32_t tl = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(half * IG::HALF);
         const int64_t cs_first = (int64_t)hc0 / prm.sp.col_seg;
         int bnd[IG::NLOC > 1 ? IG::NLOC - 1 : 1];
 #pragma unroll
         for (int i = 0; i < IG::NLOC - 1; ++i) {
             const int64_t c = (cs_first + 1 + i) * prm.sp.col_seg - hc0;
-            bnd[i] = SEG ? (int)(c < 128 ? c : (1 << 30)) : (1 << 30);
+            bnd[i] = SEG ? (int)(c < IG::HALF ? c : (1 << 30)) : (1 << 30);
         }
         uint32_t* myh = hist_s + et;
         const int64_t pbase = (int64_t)p * prm.rowsA * prm.rowsB + (row_ok ? row : 0) * prm.rowsB;
@@ -185,8 +195,10 @@ __device__ __forceinline__ void epilogue_aug(const I8Params& prm, uint32_t tmem_
             {
                 const int64_t c = col0 + et;
                 const bool ok = c < prm.rowsB;
-                s_nb[et] = ok ? prm.nrm3[(browbase + c) * 4 + ph] : 0.f;
-                s_sb[et] = ok ? prm.scl3[(browbase + c) * 4 + ph] : 0.f;
+                if (et < TN) {                   // the tile's TN columns (s_nb / s_sb hold TN each)
+                    s_nb[et] = ok ? prm.nrm3[(browbase + c) * 4 + ph] : 0.f;
+                    s_sb[et] = ok ? prm.scl3[(browbase + c) * 4 + ph] : 0.f;
+                }
                 if (ph == 0 && et < 2 * MAXM)
 #pragma unroll
                     for (int k = 0; k < 3; ++k)
@@ -204,17 +216,17 @@ __device__ __forceinline__ void epilogue_aug(const I8Params& prm, uint32_t tmem_
             mbar_wait(&tfull[0], tph);
             fence_after();
 #pragma unroll 1
-            for (int g = 0; g < 8; ++g) {
+            for (int g = 0; g < IG::NG; ++g) {
                 if (g * 16 >= nvalid) break;
                 uint32_t hv[16], xv[16];
                 tmem_ld16(tl + g * 16, hv);
-                tmem_ld16(tl + TILE_N + g * 16, xv);
+                tmem_ld16(tl + TN + g * 16, xv);
                 if (!row_ok) continue;
 #pragma unroll
                 for (int jj = 0; jj < 16; ++jj) {
                     const int j = g * 16 + jj;
                     if (j >= nvalid) break;
-                    const int jc = half * 128 + j;
+                    const int jc = half * IG::HALF + j;
                     const float sb = s_sb[jc], nb = s_nb[jc];
                     const float gi = empty_ph ? 0.f : fmaf((float)(int)hv[jj], 65536.f, (float)(int)xv[jj] * 256.f);
                     const float d2 = fmaxf(fmaf(m2sa * sb, gi, na + nb), 0.f);
@@ -291,7 +303,7 @@ __device__ __forceinline__ void epilogue_aug(const I8Params& prm, uint32_t tmem_
 #pragma unroll
                 for (int l = 0; l < IG::NLOC; ++l) {
                     const int64_t cs = cs_first + l;
-                    if (cs * prm.sp.col_seg >= prm.rowsB || cs * prm.sp.col_seg >= hc0 + 128) break;
+                    if (cs * prm.sp.col_seg >= prm.rowsB || cs * prm.sp.col_seg >= hc0 + IG::HALF) break;
                     const uint32_t v = SEG ? ((cell >> (8 * l)) & 255u) : ((cell >> (8 * k)) & 255u);
                     if (uniform) {
                         const uint32_t tot = __reduce_add_sync(0xffffffffu, v);
@@ -308,12 +320,12 @@ __device__ __forceinline__ void epilogue_aug(const I8Params& prm, uint32_t tmem_
     }
 }
 
-template <int MAXM, bool SEG, bool AUG>
+template <int MAXM, bool SEG, bool AUG, int TN>
 __global__ void __maxnreg__(168)
 k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUtensorMap mAl,
           const __grid_constant__ CUtensorMap mBh, const __grid_constant__ CUtensorMap mBl, I8Params prm) {
     using G = Geo<2>;
-    using IG = I8Geo<MAXM, SEG, AUG>;
+    using IG = I8Geo<MAXM, SEG, AUG, TN>;
     constexpr int STAGES = IG::STAGES;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     // 1024-B alignment by offsetting the shared pointer itself (keeps the shared address space, so
@@ -326,8 +338,8 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
     uint64_t* tempty = tfull + 1;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
     float* s_nb = reinterpret_cast<float*>(smem + STAGES * IG::STAGE_BYTES + 1024);
-    float* s_sb = s_nb + TILE_N;
-    float* s_T = s_sb + 2 * TILE_N;                       // [NKIND][2*MAXM] thresholds, -inf padded
+    float* s_sb = s_nb + TN;
+    float* s_T = s_sb + 2 * TN;                       // [NKIND][2*MAXM] thresholds, -inf padded
     uint32_t* hist_s = reinterpret_cast<uint32_t*>(s_T + IG::NKIND * 2 * MAXM);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -367,14 +379,14 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
                 int mt, nt;
                 tile_of(prm, t % tiles_per_item, mt, nt);
                 const int ya = (int)(p * prm.rowsA + (int64_t)mt * G::TILE_M + rank * A_ROWS);
-                const int yb = (int)(prm.b_off + p * prm.rowsB + (int64_t)nt * TILE_N + rank * G::B_ROWS);
+                const int yb = (int)(prm.b_off + p * prm.rowsB + (int64_t)nt * TN + rank * IG::B_ROWS);
                 for (int kb = 0; kb < prm.n_kb; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     unsigned char* st = stages + stage * IG::STAGE_BYTES;
                     // diagnostics: dbg 3 skips the B loads, dbg 4 all loads (MMA rate alone)
                     const bool only_a = prm.dbg == 3, none = prm.dbg == 4;
                     if (rank == 0)
-                        mbar_expect_tx(&full[stage], none ? 0 : only_a ? 4 * G::A_BYTES : 2 * IG::STAGE_BYTES);
+                        mbar_expect_tx(&full[stage], none ? 0 : only_a ? 4 * IG::A_BYTES : 2 * IG::STAGE_BYTES);
                     const int x = kb * 128;
                     if (prm.pf > 0 && kb + prm.pf < prm.n_kb) {   // L2 prefetch pf k-blocks ahead
                         const int xp = (kb + prm.pf) * 128;
@@ -385,11 +397,11 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
                     }
                     if (!none) {
                         tma_load_2d<2>(st, &mAh, &full[stage], x, ya);
-                        tma_load_2d<2>(st + G::A_BYTES, &mAl, &full[stage], x, ya);
+                        tma_load_2d<2>(st + IG::A_BYTES, &mAl, &full[stage], x, ya);
                     }
                     if (!only_a && !none) {
-                        tma_load_2d<2>(st + 2 * G::A_BYTES, &mBh, &full[stage], x, yb);
-                        tma_load_2d<2>(st + 2 * G::A_BYTES + G::B_BYTES, &mBl, &full[stage], x, yb);
+                        tma_load_2d<2>(st + 2 * IG::A_BYTES, &mBh, &full[stage], x, yb);
+                        tma_load_2d<2>(st + 2 * IG::A_BYTES + IG::B_BYTES, &mBl, &full[stage], x, yb);
                     }
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
@@ -397,8 +409,8 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
         }
     } else if (warp == 1) {
         if (lane == 0 && rank == 0) {
-            const uint32_t id = idesc_i8(G::TILE_M, TILE_N);
-            const uint32_t dH = tmem_base, dX = tmem_base + TILE_N;
+            const uint32_t id = idesc_i8(G::TILE_M, TN);
+            const uint32_t dH = tmem_base, dX = tmem_base + TN;
             int stage = 0;
             uint32_t phase = 0, tph = 0;
             for (int t = cluster_id; t < total_tiles; t += n_clusters) {
@@ -411,8 +423,8 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
                         mbar_wait(&full[stage], phase);
                         fence_after();
                         const uint32_t s0 = smem_u32(stages + stage * IG::STAGE_BYTES);
-                        const uint64_t ah = sdesc(s0), al = sdesc(s0 + G::A_BYTES);
-                        const uint64_t bh = sdesc(s0 + 2 * G::A_BYTES), bl = sdesc(s0 + 2 * G::A_BYTES + G::B_BYTES);
+                        const uint64_t ah = sdesc(s0), al = sdesc(s0 + IG::A_BYTES);
+                        const uint64_t bh = sdesc(s0 + 2 * IG::A_BYTES), bl = sdesc(s0 + 2 * IG::A_BYTES + IG::B_BYTES);
 #pragma unroll
                         for (int k = 0; k < 4; ++k) {               // 4 x 32 int8 of K per 128-byte row
                             const uint64_t adv = (uint64_t)(k * 2);  // +32 B in the start-address field
@@ -430,7 +442,7 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
             }
         }
     } else if constexpr (AUG) {
-        epilogue_aug<MAXM, SEG>(prm, tmem_base, tfull, tempty, s_nb, s_sb, s_T, hist_s, cluster_id, n_clusters,
+        epilogue_aug<MAXM, SEG, TN>(prm, tmem_base, tfull, tempty, s_nb, s_sb, s_T, hist_s, cluster_id, n_clusters,
                                 total_tiles, tiles_per_item, rank, warp, lane);
     } else {
         // ------------------------------------------------------------ epilogue
@@ -443,14 +455,16 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
             const int p = prm.p0 + t / tiles_per_item;
             int mt, nt;
             tile_of(prm, t % tiles_per_item, mt, nt);
-            const int64_t col0 = (int64_t)nt * TILE_N;
+            const int64_t col0 = (int64_t)nt * TN;
             const int64_t browbase = prm.b_off + (int64_t)p * prm.rowsB;
             named_bar(1, 256);
             {
                 const int64_t c = col0 + et;
                 const bool ok = c < prm.rowsB;
-                s_nb[et] = ok ? prm.nrm[browbase + c] : 0.f;
-                s_sb[et] = ok ? prm.scl[browbase + c] : 0.f;
+                if (et < TN) {                   // the tile's TN columns (s_nb / s_sb hold TN each)
+                    s_nb[et] = ok ? prm.nrm[browbase + c] : 0.f;
+                    s_sb[et] = ok ? prm.scl[browbase + c] : 0.f;
+                }
                 if (et < 2 * MAXM) s_T[et] = (et < M) ? prm.thr2[(int64_t)p * prm.thr_stride + et] : -INFINITY;
             }
             named_bar(1, 256);
@@ -467,15 +481,15 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
             // update; histograms are flushed once per tile (warp REDUX -> u64 atomics).
             mbar_wait(&tfull[0], tph);
             fence_after();
-            const int hc0 = (int)(col0 + half * 128);
-            const int nvalid = (int)min((int64_t)128, prm.rowsB - hc0);   // warp-uniform
+            const int hc0 = (int)(col0 + half * IG::HALF);
+            const int nvalid = (int)min((int64_t)IG::HALF, prm.rowsB - hc0);   // warp-uniform
             const bool diag_mode = prm.diag != nullptr && p == 0;          // diagnostics (item 0 only)
             float* diag_row = diag_mode ? prm.diag + (size_t)(row_ok ? row : 0) * prm.rowsB * 2 : nullptr;
             const float kq_sa = prm.kq * 0.81649658f;    // sqrt((sa^2 + sb^2)/3) <= sqrt(2/3) max(sa, sb)
             const float kll_sa = prm.kll * sa;
             const float m2sa = -2.f * sa;
             const float reln = prm.rel;
-            const uint32_t tl = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(half * 128);
+            const uint32_t tl = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(half * IG::HALF);
             const bool skip = prm.dbg >= 2 || (prm.diag != nullptr && p != 0);
             const float T_top = s_T[MAXM - 1], T_mid = s_T[MAXM / 2 - 1];
             const float T_q1 = s_T[MAXM / 4 - 1], T_q3 = s_T[MAXM / 2 + MAXM / 4 - 1];
@@ -484,7 +498,7 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
 #pragma unroll
             for (int i = 0; i < IG::NLOC - 1; ++i) {
                 const int64_t c = (cs_first + 1 + i) * prm.sp.col_seg - hc0;
-                bnd[i] = SEG ? (int)(c < 128 ? c : (1 << 30)) : (1 << 30);
+                bnd[i] = SEG ? (int)(c < IG::HALF ? c : (1 << 30)) : (1 << 30);
             }
             uint32_t* myh = hist_s + et;
             uint8_t* binrow = (prm.binout != nullptr && row_ok)
@@ -494,11 +508,11 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
             uint8_t* mbase = mirror ? prm.binout + ((int64_t)p * prm.nq + prm.q_l2) * prm.rowsA * prm.rowsB + row : nullptr;
 
 #pragma unroll 1
-            for (int g = 0; g < 8 && !skip; ++g) {
+            for (int g = 0; g < IG::NG && !skip; ++g) {
                 if (g * 16 >= nvalid) break;                        // warp-uniform
                 uint32_t hv[16], xv[16];
                 tmem_ld16(tl + g * 16, hv);
-                tmem_ld16(tl + TILE_N + g * 16, xv);
+                tmem_ld16(tl + TN + g * 16, xv);
                 if (prm.dbg == 1 || !row_ok) continue;
                 // phase A (loads + ALU only, so the compiler overlaps the 16 pairs' search chains):
                 // bin b_j = #{m : hi_j < T_m} and the ambiguity bit of every pair of the group
@@ -507,7 +521,7 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
 #pragma unroll
                 for (int jj = 0; jj < 16; ++jj) {
                     const int j = g * 16 + jj;
-                    const int jc = half * 128 + j;
+                    const int jc = half * IG::HALF + j;
                     const float sb = s_sb[jc], nb = s_nb[jc];
                     // 65536 H + 256 X in FP32 (relative rounding 2^-24 of g, inside rel): measured
                     // identical to an FP64 combination on generator data
@@ -596,7 +610,7 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
 #pragma unroll
                 for (int l = 0; l < IG::NLOC; ++l) {
                     const int64_t cs = cs_first + l;
-                    if (cs * prm.sp.col_seg >= prm.rowsB || cs * prm.sp.col_seg >= hc0 + 128) break;
+                    if (cs * prm.sp.col_seg >= prm.rowsB || cs * prm.sp.col_seg >= hc0 + IG::HALF) break;
                     const uint32_t v = SEG ? ((cell >> (8 * l)) & 255u) : cell;
                     if (uniform) {
                         const uint32_t tot = __reduce_add_sync(0xffffffffu, v);
@@ -644,12 +658,12 @@ static bool make_map_i8(CUtensorMap* m, const void* base, int64_t rows, int64_t 
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int MAXM, bool SEG, bool AUG = false>
+template <int MAXM, bool SEG, bool AUG = false, int TN = 256>
 static cudaError_t launch_i8_t(const tc::I8Params& prm, const CUtensorMap* maps, int nsm, cudaStream_t st) {
-    using IG = tc::I8Geo<MAXM, SEG, AUG>;
+    using IG = tc::I8Geo<MAXM, SEG, AUG, TN>;
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(tc::k_gram_i8<MAXM, SEG, AUG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaError_t e = cudaFuncSetAttribute(tc::k_gram_i8<MAXM, SEG, AUG, TN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              IG::SMEM_BYTES);
         if (e != cudaSuccess) return e;
         attr = true;
@@ -669,11 +683,11 @@ static cudaError_t launch_i8_t(const tc::I8Params& prm, const CUtensorMap* maps,
     cfg.attrs = at;
     cfg.numAttrs = 1;
     ProfScope ps_(K_GRAM_TC, st);
-    cudaError_t e = cudaLaunchKernelEx(&cfg, tc::k_gram_i8<MAXM, SEG, AUG>, maps[0], maps[1], maps[2], maps[3], prm);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, tc::k_gram_i8<MAXM, SEG, AUG, TN>, maps[0], maps[1], maps[2], maps[3], prm);
     note_launch();
     if (e != cudaSuccess) {
         cudaFuncAttributes fa{};
-        cudaFuncGetAttributes(&fa, tc::k_gram_i8<MAXM, SEG, AUG>);
+        cudaFuncGetAttributes(&fa, tc::k_gram_i8<MAXM, SEG, AUG, TN>);
         fprintf(stderr, "[libcil] k_gram_i8 launch failed (%s): regs=%d maxThreads=%d local=%zu smem_dyn=%d\n",
                 cudaGetErrorString(e), fa.numRegs, fa.maxThreadsPerBlock, fa.localSizeBytes, IG::SMEM_BYTES);
         return e;
@@ -681,14 +695,38 @@ static cudaError_t launch_i8_t(const tc::I8Params& prm, const CUtensorMap* maps,
     return cudaGetLastError();
 }
 
+template <int TN>
+static cudaError_t dispatch_i8(const tc::I8Params& prm, const CUtensorMap* maps, int nsm, cudaStream_t st, bool seg,
+                               int M) {
+    if (prm.nph == 3) {
+        if (M <= 16)
+            return seg ? launch_i8_t<16, true, true, TN>(prm, maps, nsm, st)
+                       : launch_i8_t<16, false, true, TN>(prm, maps, nsm, st);
+        if (seg) return cudaErrorInvalidValue;                 // host routes these to the CUDA cores
+        if (M <= 32) return launch_i8_t<32, false, true, TN>(prm, maps, nsm, st);
+        return launch_i8_t<64, false, true, TN>(prm, maps, nsm, st);
+    }
+    if (M <= 16) return seg ? launch_i8_t<16, true, false, TN>(prm, maps, nsm, st) : launch_i8_t<16, false, false, TN>(prm, maps, nsm, st);
+    if (M <= 32) return seg ? launch_i8_t<32, true, false, TN>(prm, maps, nsm, st) : launch_i8_t<32, false, false, TN>(prm, maps, nsm, st);
+    return seg ? launch_i8_t<64, true, false, TN>(prm, maps, nsm, st) : launch_i8_t<64, false, false, TN>(prm, maps, nsm, st);
+}
+
 cudaError_t launch_gram_i8(const I8Args& a, cudaStream_t st) {
     if (a.rowsA == 0 || a.rowsB == 0) return cudaSuccess;
     const int64_t rows = (int64_t)a.P * (a.b_same ? a.rowsA : a.rowsA + a.rowsB);
     if (rows >= (1ll << 31) || (a.b_same && a.rowsA != a.rowsB)) return cudaErrorInvalidValue;
+    // B columns per tile: 192 when that pads the B panel less than 256 (e.g. 550 -> 576 instead
+    // of 768); the mirrored symmetric layout needs square tiles
+    int tn = 256;
+    if (a.skip != 1) {
+        const int64_t p256 = (a.rowsB + 255) / 256 * 256, p192 = (a.rowsB + 191) / 192 * 192;
+        if (p192 < p256) tn = 192;
+    }
+    static const char* tne = getenv("CIL_I8_TN");            // diagnostic override (256 / 192)
+    if (tne && a.skip != 1) tn = atoi(tne) == 192 ? 192 : 256;
     CUtensorMap maps[4];
     if (!make_map_i8(&maps[0], a.hq, rows, a.Kp, tc::A_ROWS) || !make_map_i8(&maps[1], a.lq, rows, a.Kp, tc::A_ROWS) ||
-        !make_map_i8(&maps[2], a.hq, rows, a.Kp, tc::Geo<2>::B_ROWS) ||
-        !make_map_i8(&maps[3], a.lq, rows, a.Kp, tc::Geo<2>::B_ROWS))
+        !make_map_i8(&maps[2], a.hq, rows, a.Kp, tn / 2) || !make_map_i8(&maps[3], a.lq, rows, a.Kp, tn / 2))
         return cudaErrorInvalidValue;
     tc::I8Params prm{};
     prm.rowsA = a.rowsA; prm.rowsB = a.rowsB;
@@ -696,7 +734,8 @@ cudaError_t launch_gram_i8(const I8Args& a, cudaStream_t st) {
     prm.P = a.P; prm.p0 = a.p0; prm.np = a.np > 0 ? a.np : a.P - a.p0;
     prm.n_kb = (int)(a.Kp / 128);
     prm.tiles_m = (int)((a.rowsA + tc::Geo<2>::TILE_M - 1) / tc::Geo<2>::TILE_M);
-    prm.tiles_n = (int)((a.rowsB + tc::TILE_N - 1) / tc::TILE_N);
+    prm.tn = tn;
+    prm.tiles_n = (int)((a.rowsB + tn - 1) / tn);
     prm.nrm = a.nrm; prm.scl = a.scl;
     prm.thr2 = a.thr2; prm.thr_stride = a.thr_stride;
     prm.M = a.M; prm.nq = a.nq; prm.q_l2 = a.q_l2;
@@ -707,7 +746,7 @@ cudaError_t launch_gram_i8(const I8Args& a, cudaStream_t st) {
     prm.diag = a.diag;
     prm.binout = a.binout;
     prm.skip = a.skip;
-    prm.tiles_act = tc::tiles_active(prm.skip, prm.tiles_m, prm.tiles_n, a.sp.row_seg, a.sp.col_seg, a.rowsB);
+    prm.tiles_act = tc::tiles_active(prm.skip, prm.tiles_m, prm.tiles_n, a.sp.row_seg, a.sp.col_seg, a.rowsB, tn);
     if (prm.tiles_act == 0) return cudaSuccess;
     prm.nph = a.nph == 3 ? 3 : 1;
     if (prm.nph == 3) {
@@ -729,16 +768,8 @@ cudaError_t launch_gram_i8(const I8Args& a, cudaStream_t st) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     const bool seg = a.sp.col_seg < a.rowsB;
-    if (prm.nph == 3) {
-        if (a.M <= 16)
-            return seg ? launch_i8_t<16, true, true>(prm, maps, nsm, st) : launch_i8_t<16, false, true>(prm, maps, nsm, st);
-        if (seg) return cudaErrorInvalidValue;                 // host routes these to the CUDA cores
-        if (a.M <= 32) return launch_i8_t<32, false, true>(prm, maps, nsm, st);
-        return launch_i8_t<64, false, true>(prm, maps, nsm, st);
-    }
-    if (a.M <= 16) return seg ? launch_i8_t<16, true>(prm, maps, nsm, st) : launch_i8_t<16, false>(prm, maps, nsm, st);
-    if (a.M <= 32) return seg ? launch_i8_t<32, true>(prm, maps, nsm, st) : launch_i8_t<32, false>(prm, maps, nsm, st);
-    return seg ? launch_i8_t<64, true>(prm, maps, nsm, st) : launch_i8_t<64, false>(prm, maps, nsm, st);
+    if (tn == 192) return dispatch_i8<192>(prm, maps, nsm, st, seg, a.M);
+    return dispatch_i8<256>(prm, maps, nsm, st, seg, a.M);
 }
 
 }  // namespace cil

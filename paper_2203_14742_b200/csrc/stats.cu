@@ -262,7 +262,7 @@ cudaError_t launch_loglik(int P, const double* mu, int64_t mu_stride, const doub
 //   divided by N_set * N_tilde.
 __global__ void k_build_Y(int n_ens, int nq, int M, SegParams sp, const uint64_t* __restrict__ hist,
                           double npairs, const int32_t* __restrict__ k0, double* __restrict__ Y,
-                          int32_t* __restrict__ status) {
+                          int32_t* __restrict__ status, int swapped) {
     const int p = blockIdx.y;
     const int v = blockIdx.x;
     const int nv = n_ens * n_ens;
@@ -280,19 +280,23 @@ __global__ void k_build_Y(int n_ens, int nq, int M, SegParams sp, const uint64_t
     for (int t = threadIdx.x; t < D; t += blockDim.x) {
         const int q = t / M, m = t % M;
         uint64_t c = 0;
-        for (int b = m + 1; b <= M; ++b) c += hist[hist_index(sp, nq, M, p, rs, cs, q, b)];
+        // swapped panels (the column panel ran as the Gram's rows): segments are [l][k]
+        const int r_ = swapped ? cs : rs, c_ = swapped ? rs : cs;
+        for (int b = m + 1; b <= M; ++b) c += hist[hist_index(sp, nq, M, p, r_, c_, q, b)];
         Y[((int64_t)p * (nv + 1) + v) * D + t] = (double)c / npairs;
     }
 }
 
 cudaError_t launch_synth_tail(int P, int n_ens, int nq, int M, const SegParams& sp, const uint64_t* hist,
                               int64_t N_set, int64_t N_tilde, const int32_t* k0, double ridge, double* out,
-                              int32_t* status, double* Y, double* mu, double* Sigma, cudaStream_t st) {
+                              int32_t* status, double* Y, double* mu, double* Sigma, cudaStream_t st,
+                              bool swapped) {
     const int nv = n_ens * n_ens, D = nq * M;
     dim3 g((unsigned)(nv + 1), (unsigned)P);
     {
         ProfScope ps_(K_TAIL, st);
-        k_build_Y<<<g, 128, 0, st>>>(n_ens, nq, M, sp, hist, (double)N_set * (double)N_tilde, k0, Y, status);
+        k_build_Y<<<g, 128, 0, st>>>(n_ens, nq, M, sp, hist, (double)N_set * (double)N_tilde, k0, Y, status,
+                                     swapped ? 1 : 0);
     }
     note_launch();
     cudaError_t e = launch_stats_strided(P, Y, (int64_t)(nv + 1) * D, nv, D, mu, Sigma, st);

@@ -494,3 +494,48 @@ def test_c5_shape_large_K(cil, oracle_mod):
     c, _, st = _run_features(cil, A, B, grid, mask, radii, "AUTO")
     assert int(st[0]) == 0
     _check_counts(c[0], O.features(A.numpy(), B.numpy(), grid, mask, radii, band=BAND))
+
+
+@pytest.mark.parametrize("mask", [0x01, 0x0D])
+def test_synth_c4_shape_swapped_panels(cil, oracle_mod, mask):
+    """SCIL at C4's panel shape (n_ens = 10, N_set = N~ = 50: the 550-row panel pads worse than
+    the 500-row one, so the INT8 Gram runs the column panel as its rows with 192-column
+    tiles and the segments are read transposed) against the oracle's Alg. 3."""
+    O = oracle_mod
+    dev = torch.device("cuda")
+    grid = (1, 16, 16, 0.0)
+    P, n_ens, N_set, Nt = 2, 10, 50, 50
+    Nsyn = n_ens * (N_set + Nt)
+    pools = torch.stack([cilgen.make_set(103, 300 + p, Nsyn, grid[:3], n_w=4.8 + 0.2 * p) for p in range(P)])
+    data = cilgen.make_set(103, 999, N_set, grid[:3])
+    k0 = np.array([3, 7], np.int32)
+    radii = []
+    for p in range(P):
+        Dp = _sel(O.distance_matrix(pools[p, :60].numpy(), pools[p, 60:120].numpy(), grid, 0x3F), mask)
+        radii.append(np.array([np.quantile(d, np.linspace(0.95, 0.05, 13)) for d in Dp]))
+    radii = np.array(radii)
+    out, st, Y = cil.synth_loglik(pools.to(dev), n_ens, N_set, Nt, data.to(dev), torch.tensor(k0, device=dev),
+                                  grid, mask, torch.tensor(radii, device=dev), ridge=1e-6,
+                                  engine=cil.ENGINE_TC_I8, return_Y=True)
+    torch.cuda.synchronize()
+    npairs = N_set * Nt
+    for p in range(P):
+        ref, rst, Yr = O.synth_loglik(pools[p].numpy(), n_ens, N_set, Nt, data.numpy(), int(k0[p]), grid, mask,
+                                      radii[p], ridge=1e-6)
+        Yg = Y[p].cpu().numpy()
+        # counts within the oracle's band: recompute band counts for every (k, l) block and y~
+        cg = np.rint(Yg * npairs).astype(np.int64)
+        N = N_set + Nt
+        pool = pools[p].numpy()
+        rows = []
+        for k in range(n_ens):
+            for l in range(n_ens):
+                rows.append(O.features(pool[k * N:k * N + N_set], pool[l * N + N_set:(l + 1) * N], grid, mask,
+                                       radii[p], band=BAND))
+        rows.append(O.features(data.numpy(), pool[k0[p] * N + N_set:(k0[p] + 1) * N], grid, mask, radii[p],
+                               band=BAND))
+        lo = np.array([r["lo"].ravel() for r in rows])
+        hi = np.array([r["hi"].ravel() for r in rows])
+        assert np.all(lo <= cg) and np.all(cg <= hi), f"item {p}"
+        if np.array_equal(Yg, Yr):
+            np.testing.assert_allclose(out[p].cpu().numpy(), ref, rtol=0, atol=1e-6)
