@@ -219,6 +219,7 @@ struct I8Args {
     int q_tc[3];                         // histogram slot of L2, W12, W12SUM (-1: not requested)
     float ih;                            // 1/h
     int skip;                            // tile skipping: 0 none, 1 symmetric bins, 2 Alg. 1 triangle
+    int sm_budget;                       // SMs the persistent grid may occupy (0 = all)
 };
 cudaError_t launch_gram_i8(const I8Args& a, cudaStream_t st);
 cudaError_t launch_pack_i8_aug(int P, const RowSrc& src, int64_t rows, const AugGeom& g, const int64_t* kp,

@@ -767,6 +767,7 @@ cudaError_t launch_gram_i8(const I8Args& a, cudaStream_t st) {
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (a.sm_budget > 0 && a.sm_budget < nsm) nsm = a.sm_budget;
     const bool seg = a.sp.col_seg < a.rowsB;
     if (tn == 192) return dispatch_i8<192>(prm, maps, nsm, st, seg, a.M);
     return dispatch_i8<256>(prm, maps, nsm, st, seg, a.M);
