@@ -610,7 +610,11 @@ def bench_c7(cil, args, world, rank, dev, engine, stream):
     ms = timed(step, steps, stream)
     _capi.prof_enable(False)
     prof = _capi.prof_read()
-    ms_step = ms / steps
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_step = float(t.item()) / steps
     nv = n_ens * (n_ens - 1) // 2
     return {"workload": cfg["workload"], "metric": "training vectors/s", "value": world * nv / (ms_step * 1e-3),
             "ms_per_step": round(ms_step, 3), "steps": steps,

@@ -43,7 +43,7 @@ __global__ void __launch_bounds__(kRsThreads) k_resample(const uint8_t* __restri
                                                           int nq, int M, int n_rep, const int32_t* __restrict__ I1,
                                                           int64_t n1, const int32_t* __restrict__ I2, int64_t n2,
                                                           uint64_t* __restrict__ counts, double* __restrict__ y,
-                                                          int64_t y_item_stride) {
+                                                          int64_t y_item_stride, int32_t* __restrict__ status) {
     extern __shared__ uint32_t rs_smem[];
     uint32_t* hs = rs_smem;                                   // [M+1][kRsThreads]
     uint32_t* m1 = hs + (M + 1) * kRsThreads;                 // [round_up(N, 4)]
@@ -57,15 +57,18 @@ __global__ void __launch_bounds__(kRsThreads) k_resample(const uint8_t* __restri
     for (int64_t a = tid; a < N; a += kRsThreads) m1[a] = 0u;
     for (int64_t b = tid; b < Nt16; b += kRsThreads) m2[b] = 0u;
     __syncthreads();
+    bool bad = false;
     for (int64_t i = tid; i < n1; i += kRsThreads) {
         const int32_t r = __ldg(&i1[i]);
         if (r >= 0 && r < N) atomicAdd(&m1[r], 1u);          // invalid draws: flagged, skipped
+        else bad = true;
     }
     for (int64_t j = tid; j < n2; j += kRsThreads) {
         const int32_t c = __ldg(&i2[j]);
         if (c >= 0 && c < Nt) atomicAdd(&m2[c], 1u);
+        else bad = true;
     }
-    __syncthreads();
+    if (__syncthreads_or(bad) && tid == 0) atomicOr(&status[p], CIL_ITEM_BADINDEX);
     // compact list of the distinct drawn rows (order irrelevant: integer sums)
     __shared__ int nrows;
     int32_t* rows = reinterpret_cast<int32_t*>(m2 + Nt16);   // [min(N, n1)]
@@ -144,10 +147,7 @@ __global__ void __launch_bounds__(kRsThreads) k_resample(const uint8_t* __restri
 cudaError_t launch_resample(int P, const uint8_t* bins, int64_t N, int64_t Nt, int nq, int M, int n_rep,
                             const int32_t* I1, int64_t n1, const int32_t* I2, int64_t n2, uint64_t* counts,
                             double* y, int64_t y_item_stride, int32_t* status, cudaStream_t st) {
-    cudaError_t e = launch_check_index(P, I1, (int64_t)n_rep * n1, N, status, st);
-    if (e != cudaSuccess) return e;
-    e = launch_check_index(P, I2, (int64_t)n_rep * n2, Nt, status, st);
-    if (e != cudaSuccess) return e;
+    cudaError_t e = cudaSuccess;
     const size_t smem = sizeof(uint32_t) * ((size_t)(M + 1) * kRsThreads + (size_t)((N + 3) & ~3ll) + (size_t)((Nt + 15) & ~15ll) +
                                             (size_t)(n1 < N ? n1 : N));
     if (smem > 200 * 1024) return cudaErrorInvalidValue;     // N + Nt <= ~47 k (host-checked)
@@ -159,7 +159,8 @@ cudaError_t launch_resample(int P, const uint8_t* bins, int64_t N, int64_t Nt, i
     }
     dim3 grid((unsigned)n_rep, (unsigned)P);
     ProfScope ps_(K_RESAMPLE, st);
-    k_resample<<<grid, kRsThreads, smem, st>>>(bins, N, Nt, nq, M, n_rep, I1, n1, I2, n2, counts, y, y_item_stride);
+    k_resample<<<grid, kRsThreads, smem, st>>>(bins, N, Nt, nq, M, n_rep, I1, n1, I2, n2, counts, y, y_item_stride,
+                                               status);
     note_launch();
     return cudaGetLastError();
 }
