@@ -12,6 +12,14 @@ C ABI, minus the prefix):
     bin_matrix(A, B, grid, mask, radii)             -> bins[P,n_meas,N,Nt] uint8 (bootstrap)
     resample_counts(bins, I1, I2, M)                -> counts, y               (Alg. A1/A2 step 2)
     synth_loglik_boot(pools, data, N_set, I1, I2, J, grid, mask, radii)         (Alg. A2)
+    mcil_boot_stats(data, grid, mask, radii, I1, I2) -> mu_0, Sigma_0          (Alg. A1)
+    train_vectors(X, n_ens, grid, mask, radii)      -> Y [P, C(n_ens,2), D]     (Alg. 1/2 steps 1-2)
+    distance_range(A, B, grid, mask), radii_from_range(rng, M, law)            (PAPER.md:109, 246)
+    minmax_scale(X, grid)                           -> scaled patterns
+    gaussianity_chi2(Y)                             -> chi^2 statistic
+    sharding.sharded_features / ring_features / gather_vectors                 (multi-GPU, §8(e))
+
+Grid = (S, H, W[, h[, gs]]): gs = species mask of the derivative terms.
 
 Measures (bit order = concatenation order): L2, LINF, W12SUM, W12,
 W1INF, W1INFSUM (Eqs. (5)-(10)).
