@@ -90,7 +90,12 @@ template <int MAXM, bool SEG, bool AUG = false, int TN = 256> struct I8Geo {
     // per kind.
     static constexpr int NLOC = SEG ? 4 : 1;
     static constexpr int NKIND = AUG ? 3 : 1;
-    static constexpr int HIST_BYTES = (AUG && SEG ? 3 : 1) * (MAXM + 1) * 256 * 4;
+    // epilogue warps: 14 (3-4 per SM sub-partition, more latency hiding while the MMA waits)
+    // for the one-phase engine, 8 for the three-phase one (its register budget)
+    static constexpr int NEPI = AUG ? 8 : 14;
+    static constexpr int NET = 32 * NEPI;                           // epilogue threads
+    static constexpr int NTHR = 64 + NET;
+    static constexpr int HIST_BYTES = (AUG && SEG ? 3 : 1) * (MAXM + 1) * NET * 4;
     static constexpr int FIXED = 1024 /*align*/ + 1024 /*barriers*/ + 3 * TN * 4 /*norms, sigma, spare*/ +
                                  NKIND * 2 * MAXM * 4 + HIST_BYTES;
     static constexpr int STAGES = (3 * STAGE_BYTES + FIXED <= 227 * 1024) ? 3 : 2;
@@ -321,7 +326,7 @@ __device__ __forceinline__ void epilogue_aug(const I8Params& prm, uint32_t tmem_
 }
 
 template <int MAXM, bool SEG, bool AUG, int TN>
-__global__ void __maxnreg__(168)
+__global__ void __maxnreg__(AUG ? 168 : 128)
 k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUtensorMap mAl,
           const __grid_constant__ CUtensorMap mBh, const __grid_constant__ CUtensorMap mBl, I8Params prm) {
     using G = Geo<2>;
@@ -351,7 +356,7 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
         mbar_init(&tfull[0], 1);
-        mbar_init(&tempty[0], 16);                        // 8 epilogue warps x 2 CTAs
+        mbar_init(&tempty[0], 2 * IG::NEPI);              // epilogue warps x 2 CTAs
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&mAh) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&mAl) : "memory");
@@ -364,7 +369,7 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
     }
     if (warp >= 2)
-        for (int i = threadIdx.x - 64; i < IG::HIST_BYTES / 4; i += 256) reinterpret_cast<uint32_t*>(hist_s)[i] = 0u;
+        for (int i = threadIdx.x - 64; i < IG::HIST_BYTES / 4; i += IG::NET) reinterpret_cast<uint32_t*>(hist_s)[i] = 0u;
     fence_before();
     cluster_sync();
     fence_after();
@@ -446,9 +451,16 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
                                 total_tiles, tiles_per_item, rank, warp, lane);
     } else {
         // ------------------------------------------------------------ epilogue
+        // warp w reads TMEM lanes 32 (w % 4) .. +31 (its quarter); the NEPI epilogue warps split
+        // each quarter's TN columns into contiguous 16-column groups
         const int quarter = warp & 3;
-        const int half = (warp - 2) >> 2;
-        const int et = threadIdx.x - 64;              // 0..255
+        const int ew = warp - 2;
+        const int e0 = (quarter + 2) & 3;             // first epilogue warp of this quarter
+        const int nwq = (IG::NEPI - e0 + 3) / 4;      // epilogue warps in this quarter
+        const int kq = ew >> 2;                       // index within the quarter
+        const int g0 = kq * (TN / 16) / nwq, g1 = (kq + 1) * (TN / 16) / nwq;
+        const int ncol = (g1 - g0) * 16;
+        const int et = threadIdx.x - 64;              // 0..NET-1
         const int M = prm.M;
         uint32_t tph = 0;
         for (int t = cluster_id; t < total_tiles; t += n_clusters) {
@@ -457,7 +469,7 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
             tile_of(prm, t % tiles_per_item, mt, nt);
             const int64_t col0 = (int64_t)nt * TN;
             const int64_t browbase = prm.b_off + (int64_t)p * prm.rowsB;
-            named_bar(1, 256);
+            named_bar(1, IG::NET);
             {
                 const int64_t c = col0 + et;
                 const bool ok = c < prm.rowsB;
@@ -467,7 +479,7 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
                 }
                 if (et < 2 * MAXM) s_T[et] = (et < M) ? prm.thr2[(int64_t)p * prm.thr_stride + et] : -INFINITY;
             }
-            named_bar(1, 256);
+            named_bar(1, IG::NET);
             const int64_t row = (int64_t)mt * G::TILE_M + rank * A_ROWS + quarter * 32 + lane;
             const bool row_ok = row < prm.rowsA;
             const int64_t arow = (int64_t)p * prm.rowsA + (row_ok ? row : 0);
@@ -481,15 +493,15 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
             // update; histograms are flushed once per tile (warp REDUX -> u64 atomics).
             mbar_wait(&tfull[0], tph);
             fence_after();
-            const int hc0 = (int)(col0 + half * IG::HALF);
-            const int nvalid = (int)min((int64_t)IG::HALF, prm.rowsB - hc0);   // warp-uniform
+            const int hc0 = (int)(col0 + g0 * 16);
+            const int nvalid = (int)min((int64_t)ncol, prm.rowsB - hc0);     // warp-uniform
             const bool diag_mode = prm.diag != nullptr && p == 0;          // diagnostics (item 0 only)
             float* diag_row = diag_mode ? prm.diag + (size_t)(row_ok ? row : 0) * prm.rowsB * 2 : nullptr;
             const float kq_sa = prm.kq * 0.81649658f;    // sqrt((sa^2 + sb^2)/3) <= sqrt(2/3) max(sa, sb)
             const float kll_sa = prm.kll * sa;
             const float m2sa = -2.f * sa;
             const float reln = prm.rel;
-            const uint32_t tl = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(half * IG::HALF);
+            const uint32_t tl = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(g0 * 16);
             const bool skip = prm.dbg >= 2 || (prm.diag != nullptr && p != 0);
             const float T_top = s_T[MAXM - 1], T_mid = s_T[MAXM / 2 - 1];
             const float T_q1 = s_T[MAXM / 4 - 1], T_q3 = s_T[MAXM / 2 + MAXM / 4 - 1];
@@ -498,7 +510,7 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
 #pragma unroll
             for (int i = 0; i < IG::NLOC - 1; ++i) {
                 const int64_t c = (cs_first + 1 + i) * prm.sp.col_seg - hc0;
-                bnd[i] = SEG ? (int)(c < IG::HALF ? c : (1 << 30)) : (1 << 30);
+                bnd[i] = SEG ? (int)(c < ncol ? c : (1 << 30)) : (1 << 30);
             }
             uint32_t* myh = hist_s + et;
             uint8_t* binrow = (prm.binout != nullptr && row_ok)
@@ -508,7 +520,7 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
             uint8_t* mbase = mirror ? prm.binout + ((int64_t)p * prm.nq + prm.q_l2) * prm.rowsA * prm.rowsB + row : nullptr;
 
 #pragma unroll 1
-            for (int g = 0; g < IG::NG && !skip; ++g) {
+            for (int g = 0; g < g1 - g0 && !skip; ++g) {
                 if (g * 16 >= nvalid) break;                        // warp-uniform
                 uint32_t hv[16], xv[16];
                 tmem_ld16(tl + g * 16, hv);
@@ -521,7 +533,7 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
 #pragma unroll
                 for (int jj = 0; jj < 16; ++jj) {
                     const int j = g * 16 + jj;
-                    const int jc = half * IG::HALF + j;
+                    const int jc = g0 * 16 + j;
                     const float sb = s_sb[jc], nb = s_nb[jc];
                     // 65536 H + 256 X in FP32 (relative rounding 2^-24 of g, inside rel): measured
                     // identical to an FP64 combination on generator data
@@ -580,7 +592,7 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
 #pragma unroll
                     for (int jj = 0; jj < 16; ++jj)
                         if (g * 16 + jj < nvalid)
-                            atomicAdd(myh + ((bin[jj] & 255) << 8), SEG ? 1u << ((bin[jj] >> 5) & 24) : 1u);
+                            atomicAdd(myh + (bin[jj] & 255) * IG::NET, SEG ? 1u << ((bin[jj] >> 5) & 24) : 1u);
                 }
                 if (amb) {                                  // rare (~1e-4 of the pairs)
 #pragma unroll
@@ -605,12 +617,12 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
             const bool uniform = __all_sync(0xffffffffu, rs == rs0 || !row_ok);
             myh[0] = 0u;                                    // bin 0 (outside every radius) is not kept
             for (int bb = 1; bb <= M; ++bb) {
-                const uint32_t cell = myh[bb << 8];
-                myh[bb << 8] = 0u;
+                const uint32_t cell = myh[bb * IG::NET];
+                myh[bb * IG::NET] = 0u;
 #pragma unroll
                 for (int l = 0; l < IG::NLOC; ++l) {
                     const int64_t cs = cs_first + l;
-                    if (cs * prm.sp.col_seg >= prm.rowsB || cs * prm.sp.col_seg >= hc0 + IG::HALF) break;
+                    if (cs * prm.sp.col_seg >= prm.rowsB || cs * prm.sp.col_seg >= hc0 + ncol) break;
                     const uint32_t v = SEG ? ((cell >> (8 * l)) & 255u) : cell;
                     if (uniform) {
                         const uint32_t tot = __reduce_add_sync(0xffffffffu, v);
@@ -672,7 +684,7 @@ static cudaError_t launch_i8_t(const tc::I8Params& prm, const CUtensorMap* maps,
     const int clusters = (int)(tiles < nsm / 2 ? tiles : nsm / 2);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)(clusters * 2));
-    cfg.blockDim = dim3(tc::NTHREADS);
+    cfg.blockDim = dim3(IG::NTHR);
     cfg.dynamicSmemBytes = IG::SMEM_BYTES;
     cfg.stream = st;
     cudaLaunchAttribute at[1];
