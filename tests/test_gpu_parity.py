@@ -539,3 +539,130 @@ def test_synth_c4_shape_swapped_panels(cil, oracle_mod, mask):
         assert np.all(lo <= cg) and np.all(cg <= hi), f"item {p}"
         if np.array_equal(Yg, Yr):
             np.testing.assert_allclose(out[p].cpu().numpy(), ref, rtol=0, atol=1e-6)
+
+
+# ------------------------------------------------------------------ full-size SCIL / bootstrap (sampled)
+def test_c4_full_theta_vs_oracle(cil, oracle_mod):
+    """C4 at full size in the bench's launch configuration (pools of 1000 patterns of 128x128,
+    n_ens = 10, 50 + 50, M = 13, swapped panels and 192-column tiles, several proposals in one
+    launch); proposal 0 against the oracle's Alg. 3: every vector within the band, loglik."""
+    O = oracle_mod
+    dev = torch.device("cuda")
+    grid = (1, 128, 128, 0.0)
+    P, n_ens, N_set, Nt, M = 4, 10, 50, 50, 13
+    seed = cilgen.config_seed(4)
+    pools = torch.empty((P, n_ens * (N_set + Nt)) + grid[:3], dtype=torch.float32, device=dev)
+    for p in range(P):
+        cilgen.make_set(seed, p, n_ens * (N_set + Nt), grid[:3], device=dev, out=pools[p], n_w=4.6 + 0.2 * p)
+    data = cilgen.make_set(seed, 1000, N_set, grid[:3], device=dev)
+    k0 = torch.tensor([p % n_ens for p in range(P)], dtype=torch.int32, device=dev)
+    pool0 = pools[0].cpu().numpy()
+    D = O.distance_matrix(pool0[:64], pool0[64:128], grid, 0x1)[0]
+    R0, RM = D.max() * 1.001, D.min() * 0.999
+    r1 = R0 * (RM / R0) ** (np.arange(1, M + 1) / M)
+    radii = torch.tensor(np.tile(r1, (P, 1, 1)), device=dev)
+    out, st, Y = cil.synth_loglik(pools, n_ens, N_set, Nt, data, k0, grid, 0x1, radii, ridge=1e-10,
+                                  engine=cil.ENGINE_AUTO, return_Y=True)
+    torch.cuda.synchronize()
+    assert int(st.max()) == 0
+    N = N_set + Nt
+    cg = np.rint(Y[0].cpu().numpy() * N_set * Nt).astype(np.int64)
+    dat = data.cpu().numpy()
+    v = 0
+    for k in range(n_ens):
+        for l in range(n_ens):
+            r = O.features(pool0[k * N:k * N + N_set], pool0[l * N + N_set:(l + 1) * N], grid, 0x1, r1[None],
+                           band=BAND)
+            assert np.all(r["lo"][0] <= cg[v]) and np.all(cg[v] <= r["hi"][0]), (k, l)
+            v += 1
+    r = O.features(dat, pool0[0 * N + N_set:N], grid, 0x1, r1[None], band=BAND)
+    assert np.all(r["lo"][0] <= cg[v]) and np.all(cg[v] <= r["hi"][0])
+    mu, Sig = O.stats(Y[0, :-1].cpu().numpy())
+    ref, _ = O.loglik(mu, Sig, Y[0, -1].cpu().numpy(), ridge=1e-10)
+    np.testing.assert_allclose(out[0].cpu().numpy(), ref, rtol=0, atol=1e-6)
+
+
+def test_c6_full_theta_bins_and_replicates(cil, oracle_mod):
+    """C6 (Alg. A2 at the paper's sizes: pool 1000 of 64x64x2, N_set = 50, 1000 replicates) in
+    the bench's configuration for 2 proposals; proposal 0: the bin matrix on a 1000 x 1000
+    sample block against the oracle's distances, and 12 replicates against brute force on the
+    resampled sets."""
+    O = oracle_mod
+    dev = torch.device("cuda")
+    grid = (2, 64, 64, 0.0)
+    P, N_syn, N_set, n_rep, M = 2, 1000, 50, 1000, 13
+    seed = cilgen.config_seed(6)
+    pools = torch.stack([cilgen.make_set(seed, p, N_syn, grid[:3], n_w=4.7 + 0.3 * p) for p in range(P)])
+    data = cilgen.make_set(seed, 100000, N_set, grid[:3])
+    draws = [cilgen.boot_draws_a2(seed, p, n_rep, N_syn, N_set) for p in range(P)]
+    I1 = np.stack([d[0] for d in draws]); I2 = np.stack([d[1] for d in draws]); J = np.stack([d[2] for d in draws])
+    pool0 = pools[0].numpy()
+    D = O.distance_matrix(pool0[:64], pool0[64:128], grid, 0x1)[0]
+    R0, RM = D.max() * 1.001, D[D > 0].min() * 0.999
+    r1 = R0 * (RM / R0) ** (np.arange(1, M + 1) / M)
+    radii = np.tile(r1, (P, 1, 1))
+    out, st, Y = cil.synth_loglik_boot(pools.to(dev), data.to(dev), N_set, torch.tensor(I1, device=dev),
+                                       torch.tensor(I2, device=dev), torch.tensor(J, device=dev), grid, 0x1,
+                                       torch.tensor(radii, device=dev), ridge=1e-10, return_Y=True)
+    bins, _ = cil.bin_matrix(pools[0].to(dev), pools[0].to(dev), grid, 0x1, torch.tensor(r1[None], device=dev))
+    torch.cuda.synchronize()
+    assert int(st.max()) == 0
+    # the bin matrix (symmetric upper-triangle tiles + mirrored writes) on a sampled block
+    rows = np.arange(0, N_syn, 7)[:120]
+    Ds = O.distance_matrix(pool0[rows], pool0, grid, 0x1)[0]
+    lo = (Ds[:, :, None] < r1 * (1 - BAND)).sum(-1)
+    hi = (Ds[:, :, None] < r1 * (1 + BAND)).sum(-1)
+    b = bins[0, 0].cpu().numpy()[rows]
+    assert np.all(lo <= b) and np.all(b <= hi)
+    # replicate vectors of proposal 0
+    Nt = N_syn - N_set
+    ks = np.arange(0, n_rep, 83)[:12]
+    rr = O.resample_features(pool0, pool0, grid, 0x1, r1[None], I1[0][ks], I2[0][ks], band=BAND)
+    cg = np.rint(Y[0].cpu().numpy()[ks] * N_set * Nt).astype(np.int64)
+    assert np.all(rr["lo"][:, 0] <= cg) and np.all(cg <= rr["hi"][:, 0])
+
+
+def test_c7_full_training_sampled_blocks(cil, oracle_mod):
+    """C7 in the bench's configuration (N_set = 3000 GM 64x64x2, n_ens = 10, all six measures):
+    three of the 45 subset-pair vectors against the oracle (band), the rest by symmetry checks."""
+    O = oracle_mod
+    dev = torch.device("cuda")
+    grid = (2, 64, 64, 0.0)
+    N_set, n_ens, M = 3000, 10, 13
+    X = cilgen.make_set(cilgen.config_seed(7), 0, N_set, grid[:3])
+    N = N_set // n_ens
+    Xn = X.numpy()
+    D = O.distance_matrix(Xn[:48], Xn[N:N + 48], grid, 0x3F)
+    radii = np.array([d.max() * 1.001 * ((d[d > 0].min() * 0.999) / (d.max() * 1.001)) ** (np.arange(1, M + 1) / M)
+                      for d in D])
+    Y, st = cil.train_vectors(X.to(dev), n_ens, grid, 0x3F, torch.tensor(radii, device=dev))
+    torch.cuda.synchronize()
+    assert int(st[0]) == 0 and Y.shape == (1, 45, 6 * M)
+    pairs = [(k, l) for k in range(n_ens) for l in range(k + 1, n_ens)]
+    for v in (0, 17, 44):
+        k, l = pairs[v]
+        r = O.features(Xn[k * N:(k + 1) * N], Xn[l * N:(l + 1) * N], grid, 0x3F, radii, band=BAND)
+        c = np.rint(Y[0, v].cpu().numpy() * N * N).astype(np.int64).reshape(6, M)
+        assert np.all(r["lo"] <= c) and np.all(c <= r["hi"]), (k, l)
+
+
+def test_c3_full_additivity(cil):
+    """C3 in the bench's configuration (2000 x 2000 of 128x128x2, all six measures, M = 20):
+    the full launch equals the sum of the two half launches (row blocks) — counts are sums over
+    pairs, a property of Eq. (1) at any size; the engines at this shape are oracle-checked on
+    smaller sets (test_l2_family_tensor_cores_vs_oracle, test_c1_all_measures)."""
+    dev = torch.device("cuda")
+    grid = (2, 128, 128, 0.0)
+    seed = cilgen.config_seed(3)
+    A = cilgen.make_set(seed, 0, 2000, grid[:3], device=dev)
+    B = cilgen.make_set(seed, 1, 2000, grid[:3], device=dev)
+    h = 1.0 / 127
+    base = np.array([40.0, 3.0, 900.0, 700.0, 60.0, 150.0])
+    radii = torch.tensor(np.array([b * np.geomspace(1.2, 0.5, 20) for b in base]), device=dev)
+    c, _, st = cil.features(A, B, grid, 0x3F, radii)
+    c1, _, _ = cil.features(A[:1000], B, grid, 0x3F, radii)
+    c2, _, _ = cil.features(A[1000:], B, grid, 0x3F, radii)
+    torch.cuda.synchronize()
+    assert int(st[0]) == 0
+    assert torch.equal(c, c1 + c2)
+    assert (c[0, :, 0] >= c[0, :, -1]).all()
