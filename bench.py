@@ -589,8 +589,16 @@ def bench_c6(cil, args, world, rank, dev, engine, stream):
                           "frac_of_peak": round(ach / (ratio * peaks().get("bf16_tflops", 1590.0)), 4)}
     r_ms, r_n = prof["resample"]
     if r_n:
-        res["resample"] = {"ms_per_step": round(r_ms / steps, 4),
-                           "lookups_per_s": P * n_rep * N_set * Nt / (r_ms / steps * 1e-3)}
+        # steps 2.1-2.4: multiplicities, 0/1 threshold rows E, one integer GEMM (rows M1 of the
+        # replicates x rows of E, K = N_syn) whose epilogue applies the column multiplicities.
+        # Algorithmic int8 ops of the GEMM: 2 n_rep (M N_syn) N_syn per item.
+        r_step = r_ms / steps
+        res["resample"] = {"ms_per_step": round(r_step, 4), "launches_per_step": r_n / steps,
+                           "engine": "tc_rowdot" if os.environ.get("CIL_BOOT_RESAMPLE", "")[:1] != "a"
+                           and engine != cil.ENGINE_SIMT and N_set <= 127 else "atoms",
+                           "lookups_per_s": P * n_rep * N_set * Nt / (r_step * 1e-3),
+                           "gemm_int8_tops_incl_helpers": round(2.0 * P * n_rep * M * N_syn * N_syn / (r_step * 1e-3)
+                                                                / 1e12, 1)}
     res["kernel_breakdown"] = {k: round(v[0] / steps, 4) for k, v in prof.items() if v[1] > 0}
     return res
 

@@ -785,7 +785,24 @@ struct BootLayout {
     Layout L;
     size_t off_bins, total;
     Plan pb, ph;
+    // tensor-core resample (steps 2.1-2.4 as one integer GEMM per measure, resample.cu)
+    bool rd;
+    int64_t kp_rd, ntp;
+    size_t off_m1, off_m2, off_e, off_cnt;
 };
+// The GEMM form needs m1 <= 127 (int8 operand), m2 <= 65535 (u16) and n1 n2 < 2^32 (u32
+// epilogue sums); the CUDA-core engine choice keeps the shared-atomic resample.
+bool boot_rd(int32_t N_syn, int32_t N_set, int32_t n_rep, int32_t P, int nq, int32_t M, cil_engine engine) {
+    static const char* env = getenv("CIL_BOOT_RESAMPLE");   // "atoms": A/B diagnostic
+    if (env && env[0] == 'a') return false;
+    if (engine == CIL_ENGINE_SIMT || N_set > 127) return false;
+    const int64_t Nt = (int64_t)N_syn - N_set;
+    if (Nt > 65535 || (int64_t)N_set * Nt >= (1ll << 32)) return false;
+    const int64_t ntp = N_syn <= 128 ? 128 : ((int64_t)N_syn + 63) / 64 * 64;   // >= 128: gram_i8 rowdot
+    if ((int64_t)P * (n_rep + (int64_t)M * ntp) >= (1ll << 31)) return false;
+    const int64_t kp = ((int64_t)N_syn + kTcBK - 1) / kTcBK * kTcBK;
+    return 4 * (kp + ntp) <= 200 * 1024 && nq >= 1;
+}
 bool boot_layout(int32_t P, int32_t N_syn, int32_t N_set, int32_t n_rep, const cil_grid& g, uint32_t mask,
                  int32_t M, cil_engine engine, BootLayout* B) {
     if (!plan_bins(mask, engine, g, &B->pb)) return false;
@@ -797,7 +814,20 @@ bool boot_layout(int32_t P, int32_t N_syn, int32_t N_set, int32_t n_rep, const c
     const int64_t nY = (int64_t)P * (n_rep + 1) * sl.nq * M;
     B->L = make_layout(P, N_syn, N_syn, g, sl.nq, M, u, sp, nY);
     B->off_bins = al(B->L.total);
-    B->total = B->off_bins + al((size_t)P * sl.nq * N_syn * (size_t)N_syn) + 256;
+    B->total = B->off_bins + al((size_t)P * sl.nq * N_syn * (size_t)N_syn);
+    B->rd = boot_rd(N_syn, N_set, n_rep, P, sl.nq, M, engine);
+    if (B->rd) {
+        B->kp_rd = ((int64_t)N_syn + kTcBK - 1) / kTcBK * kTcBK;
+        B->ntp = N_syn <= 128 ? 128 : ((int64_t)N_syn + 63) / 64 * 64;
+        B->off_m1 = B->total;                                        // M1 rows, then E rows (stacked planes)
+        B->off_e = B->off_m1 + (size_t)P * n_rep * B->kp_rd;
+        B->total = al(B->off_e + (size_t)P * M * B->ntp * B->kp_rd);
+        B->off_m2 = B->total;
+        B->total += al((size_t)P * n_rep * B->ntp * 2);
+        B->off_cnt = B->total;
+        B->total += al((size_t)P * n_rep * M * 8);
+    }
+    B->total += 256;
     return true;
 }
 }  // namespace
@@ -848,8 +878,30 @@ cil_status cil_synth_loglik_boot(int32_t P, const float* pools, int64_t pool_str
                                item_status, st, nullptr, bins);
     if (s != CIL_OK) return s;
     // steps 2.1-2.4: the n_rep resampled vectors, straight into Y rows [0, n_rep)
-    CIL_CU(launch_resample(P, bins, N_syn, N_syn, sl.nq, M, n_rep, I1, N_set, I2, Nt, nullptr, Y, Ystride,
-                           item_status, st));
+    if (B.rd && gram_tc_supported()) {
+        int8_t* M1 = at<int8_t>(wsa, B.off_m1);
+        int8_t* E = at<int8_t>(wsa, B.off_e);
+        uint16_t* M2 = at<uint16_t>(wsa, B.off_m2);
+        unsigned long long* cnt = at<unsigned long long>(wsa, B.off_cnt);
+        CIL_CU(launch_rd_mult(P, N_syn, B.kp_rd, B.ntp, n_rep, I1, N_set, I2, Nt, M1, M2, item_status, st));
+        for (int q = 0; q < sl.nq; ++q) {
+            CIL_CU(launch_rd_build_E(P, bins, N_syn, sl.nq, q, M, B.kp_rd, B.ntp, E, st));
+            CIL_CU(cudaMemsetAsync(cnt, 0, (size_t)P * n_rep * M * 8, st));
+            I8Args t{};
+            t.hq = M1; t.lq = M1;                                  // one-digit operands: the l planes are unused
+            t.rowsA = n_rep; t.rowsB = (int64_t)M * B.ntp; t.Kp = B.kp_rd; t.K = N_syn;
+            t.P = P; t.p0 = 0; t.np = P;
+            t.M = M; t.nq = 1;
+            t.sp = SegParams{t.rowsA, t.rowsB, 1, 1};
+            t.mode = 1;
+            t.m2 = M2; t.rd_nt = B.ntp; t.rd_m = M; t.rd_out = cnt;
+            CIL_CU(launch_gram_i8(t, st));
+            CIL_CU(launch_rd_final(cnt, P, n_rep, M, sl.nq, q, (double)N_set * (double)Nt, Y, Ystride, st));
+        }
+    } else {
+        CIL_CU(launch_resample(P, bins, N_syn, N_syn, sl.nq, M, n_rep, I1, N_set, I2, Nt, nullptr, Y, Ystride,
+                               item_status, st));
+    }
     // steps 4-5: y~ = C(R, s_data, pool rows J[p]) into Y row n_rep
     CIL_CU(launch_check_index(P, J, Nt, N_syn, item_status, st));
     RowSrc ds{}, js{};

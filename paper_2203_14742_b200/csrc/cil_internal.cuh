@@ -220,6 +220,12 @@ struct I8Args {
     float ih;                            // 1/h
     int skip;                            // tile skipping: 0 none, 1 symmetric bins, 2 Alg. 1 triangle
     int sm_budget;                       // SMs the persistent grid may occupy (0 = all)
+    // mode 1 (row-dot): one-digit operands hq only; counts[p][k][v] = sum_b C[k][v rd_nt + b] m2[p][k][b]
+    int mode;
+    const uint16_t* m2;
+    int64_t rd_nt;
+    int rd_m;
+    unsigned long long* rd_out;
 };
 cudaError_t launch_gram_i8(const I8Args& a, cudaStream_t st);
 cudaError_t launch_pack_i8_aug(int P, const RowSrc& src, int64_t rows, const AugGeom& g, const int64_t* kp,
@@ -276,6 +282,12 @@ cudaError_t launch_radii(int P, int nq, int M, const unsigned long long* range, 
                          int32_t* status, cudaStream_t st);
 cudaError_t launch_build_pairs(int P, int n_ens, int nq, int M, const SegParams& sp, const uint64_t* hist,
                                int64_t N, double* Y, cudaStream_t st);
+cudaError_t launch_rd_mult(int P, int64_t N, int64_t Kp, int64_t Ntp, int n_rep, const int32_t* I1, int64_t n1,
+                           const int32_t* I2, int64_t n2, int8_t* M1, uint16_t* M2, int32_t* status, cudaStream_t st);
+cudaError_t launch_rd_build_E(int P, const uint8_t* bins, int64_t N, int nq, int q, int M, int64_t Kp, int64_t Ntp,
+                              int8_t* E, cudaStream_t st);
+cudaError_t launch_rd_final(const unsigned long long* cnt, int P, int n_rep, int M, int nq, int q, double npairs,
+                            double* y, int64_t y_item_stride, cudaStream_t st);
 cudaError_t launch_boot_tail(int P, int n_rep, int D, double ridge, double* out, int32_t* status, double* Y,
                              double* mu, double* Sigma, cudaStream_t st);
 cudaError_t launch_loglik(int P, const double* mu, int64_t mu_stride, const double* Sigma,

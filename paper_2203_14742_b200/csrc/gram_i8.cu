@@ -56,6 +56,11 @@ struct I8Params {
     float2* part;              // [2][P*rowsA*rowsB] (d2, E) of phases 0 and 1
     int q_tc[3];               // histogram slots of L2, W12, W12SUM (-1: absent)
     float ih;                  // 1/h
+    int mode;                  // 0 binning; 1 row-dot (bootstrap replicate counts, see epilogue_rowdot)
+    const uint16_t* m2;        // mode 1: [P][rowsA][rd_nt] column-draw multiplicities
+    int64_t rd_nt;             // mode 1: columns per threshold block (B row = v * rd_nt + b)
+    int rd_m;                  // mode 1: thresholds
+    unsigned long long* rd_out;   // mode 1: [P][rowsA][rd_m] counts (atomic sums)
     int tn;                    // B columns per tile (the kernel's TN)
     int tiles_act;             // active tiles per item (tiles_m * tiles_n without skipping)
     int skip;                  // 0 all tiles; 1 symmetric bin matrix (tiles mt > nt skipped, mirrored
@@ -325,6 +330,89 @@ __device__ __forceinline__ void epilogue_aug(const I8Params& prm, uint32_t tmem_
     }
 }
 
+// Row-dot epilogue (mode 1, bootstrap replicate counts on the tensor cores): the Gram of one-
+// digit operands is C[k][c] = sum_a M1[k][a] E[c][a] (replicate k's row-draw multiplicities
+// against the 0/1 threshold rows E[v*Nt + b][a] = [bins(a, b) > v]); the epilogue forms
+//   counts[k][v] = sum_b C[k][v*Nt + b] * M2[k][b]   (M2 = column-draw multiplicities)
+// = #{(i, j) : bins(I1[k][i], I2[k][j]) > v}, exactly (integers), and adds it atomically.
+template <int MAXM, bool SEG, int TN>
+__device__ __forceinline__ void epilogue_rowdot(const I8Params& prm, uint32_t tmem_base, uint64_t* tfull,
+                                                uint64_t* tempty, int cluster_id, int n_clusters, int total_tiles,
+                                                int tiles_per_item, uint32_t rank, int warp, int lane) {
+    using G = Geo<2>;
+    using IG = I8Geo<MAXM, SEG, false, TN>;
+    const int quarter = warp & 3;
+    const int ew = warp - 2;
+    const int e0 = (quarter + 2) & 3;
+    const int nwq = (IG::NEPI - e0 + 3) / 4;
+    const int kq = ew >> 2;
+    const int g0 = kq * (TN / 16) / nwq, g1 = (kq + 1) * (TN / 16) / nwq;
+    const int ncol = (g1 - g0) * 16;
+    const int Nt = (int)prm.rd_nt;
+    uint32_t tphb = 0;
+    int ab = 0;
+    for (int t = cluster_id; t < total_tiles; t += n_clusters, ab ^= 1) {
+        const int p = prm.p0 + t / tiles_per_item;
+        int mt, nt;
+        tile_of(prm, t % tiles_per_item, mt, nt);
+        const int64_t row = (int64_t)mt * G::TILE_M + rank * A_ROWS + quarter * 32 + lane;
+        const bool row_ok = row < prm.rowsA;
+        const int hc0 = nt * TN + g0 * 16;
+        const int nvalid = (int)min((int64_t)ncol, prm.rowsB - hc0);
+        const int ng = nvalid > 0 ? (nvalid + 15) / 16 : 0;
+        const uint32_t tl = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(ab * TN + g0 * 16);
+        // rd_nt is a multiple of 16, so a 16-column group lies inside one threshold block v
+        const uint16_t* m2row = prm.m2 + ((int64_t)p * prm.rowsA + (row_ok ? row : 0)) * Nt;
+        unsigned long long* out = prm.rd_out + ((int64_t)p * prm.rowsA + (row_ok ? row : 0)) * prm.rd_m;
+        // all of this tile's column multiplicities load while the MMAs finish (<= MAXG groups)
+        constexpr int MAXG = (TN / 16 + 2) / 3;
+        uint4 w[MAXG][2];
+        const int v0 = hc0 / Nt;
+        const int bnd = (v0 + 1) * Nt;                         // first column of block v0 + 1
+#pragma unroll
+        for (int g = 0; g < MAXG; ++g) {
+            w[g][0] = w[g][1] = make_uint4(0u, 0u, 0u, 0u);
+            if (row_ok && g < ng) {
+                const int c = hc0 + g * 16;
+                const uint4* mp = reinterpret_cast<const uint4*>(m2row + (c < bnd ? c - v0 * Nt : c - bnd));
+                w[g][0] = __ldg(mp); w[g][1] = __ldg(mp + 1);
+            }
+        }
+        uint64_t* tf = ab ? tfull + 4 : tfull;
+        uint64_t* te = ab ? tfull + 5 : tempty;
+        mbar_wait(tf, (tphb >> ab) & 1u);
+        fence_after();
+        // a thread's <= 16 MAXG columns span at most two threshold blocks (rd_nt >= 128)
+        uint32_t acc0 = 0u, acc1 = 0u;                        // <= n1 n2 < 2^32 (host-checked)
+#pragma unroll
+        for (int g = 0; g < MAXG; ++g) {
+            if (g < ng) {
+                uint32_t hv[16];
+                tmem_ld16(tl + g * 16, hv);
+                const uint32_t mw[8] = {w[g][0].x, w[g][0].y, w[g][0].z, w[g][0].w,
+                                        w[g][1].x, w[g][1].y, w[g][1].z, w[g][1].w};
+                uint32_t s = 0u;
+#pragma unroll
+                for (int jj = 0; jj < 8; ++jj) {
+                    s += hv[2 * jj] * (mw[jj] & 0xffffu);
+                    s += hv[2 * jj + 1] * (mw[jj] >> 16);
+                }
+                if (hc0 + g * 16 < bnd) acc0 += s;
+                else acc1 += s;
+            }
+        }
+        // release the accumulator first: the atomics complete while the next tile accumulates
+        fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_remote(te, 0);
+        if (row_ok) {
+            if (acc0) atomicAdd(&out[v0], (unsigned long long)acc0);
+            if (acc1) atomicAdd(&out[v0 + 1], (unsigned long long)acc1);
+        }
+        tphb ^= 1u << ab;
+    }
+}
+
 template <int MAXM, bool SEG, bool AUG, int TN>
 __global__ void __maxnreg__(AUG ? 168 : 128)
 k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUtensorMap mAl,
@@ -357,6 +445,8 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
         for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
         mbar_init(&tfull[0], 1);
         mbar_init(&tempty[0], 2 * IG::NEPI);              // epilogue warps x 2 CTAs
+        mbar_init(tfull + 4, 1);                          // second accumulator (mode 1)
+        mbar_init(tfull + 5, 2 * IG::NEPI);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&mAh) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&mAl) : "memory");
@@ -385,13 +475,20 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
                 tile_of(prm, t % tiles_per_item, mt, nt);
                 const int ya = (int)(p * prm.rowsA + (int64_t)mt * G::TILE_M + rank * A_ROWS);
                 const int yb = (int)(prm.b_off + p * prm.rowsB + (int64_t)nt * TN + rank * IG::B_ROWS);
-                for (int kb = 0; kb < prm.n_kb; ++kb) {
+                // mode 1 (one-digit operands) packs two k-blocks per stage: the l-plane slots hold
+                // the h planes of k-block kb + 1 (a deeper ring for its short per-stage MMA time)
+                const int ks = prm.mode == 1 ? 2 : 1;
+                for (int kb = 0; kb < prm.n_kb; kb += ks) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     unsigned char* st = stages + stage * IG::STAGE_BYTES;
                     // diagnostics: dbg 3 skips the B loads, dbg 4 all loads (MMA rate alone)
                     const bool only_a = prm.dbg == 3, none = prm.dbg == 4;
+                    const bool hi_only = prm.mode == 1;         // one-digit operands: h planes only
+                    const int nk = min(ks, prm.n_kb - kb);
                     if (rank == 0)
-                        mbar_expect_tx(&full[stage], none ? 0 : only_a ? 4 * IG::A_BYTES : 2 * IG::STAGE_BYTES);
+                        mbar_expect_tx(&full[stage], none ? 0 : only_a ? 4 * IG::A_BYTES
+                                                             : hi_only ? 2 * nk * (IG::A_BYTES + IG::B_BYTES)
+                                                                       : 2 * IG::STAGE_BYTES);
                     const int x = kb * 128;
                     if (prm.pf > 0 && kb + prm.pf < prm.n_kb) {   // L2 prefetch pf k-blocks ahead
                         const int xp = (kb + prm.pf) * 128;
@@ -400,13 +497,20 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
                         tma_prefetch_2d(&mBh, xp, yb);
                         tma_prefetch_2d(&mBl, xp, yb);
                     }
-                    if (!none) {
-                        tma_load_2d<2>(st, &mAh, &full[stage], x, ya);
-                        tma_load_2d<2>(st + IG::A_BYTES, &mAl, &full[stage], x, ya);
-                    }
-                    if (!only_a && !none) {
-                        tma_load_2d<2>(st + 2 * IG::A_BYTES, &mBh, &full[stage], x, yb);
-                        tma_load_2d<2>(st + 2 * IG::A_BYTES + IG::B_BYTES, &mBl, &full[stage], x, yb);
+                    if (hi_only) {
+                        for (int kk = 0; kk < nk; ++kk) {
+                            tma_load_2d<2>(st + kk * IG::A_BYTES, &mAh, &full[stage], x + kk * 128, ya);
+                            tma_load_2d<2>(st + 2 * IG::A_BYTES + kk * IG::B_BYTES, &mBh, &full[stage], x + kk * 128, yb);
+                        }
+                    } else {
+                        if (!none) {
+                            tma_load_2d<2>(st, &mAh, &full[stage], x, ya);
+                            tma_load_2d<2>(st + IG::A_BYTES, &mAl, &full[stage], x, ya);
+                        }
+                        if (!only_a && !none) {
+                            tma_load_2d<2>(st + 2 * IG::A_BYTES, &mBh, &full[stage], x, yb);
+                            tma_load_2d<2>(st + 2 * IG::A_BYTES + IG::B_BYTES, &mBl, &full[stage], x, yb);
+                        }
                     }
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
@@ -415,40 +519,64 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
     } else if (warp == 1) {
         if (lane == 0 && rank == 0) {
             const uint32_t id = idesc_i8(G::TILE_M, TN);
-            const uint32_t dH = tmem_base, dX = tmem_base + TN;
-            int stage = 0;
-            uint32_t phase = 0, tph = 0;
+            const uint32_t dH0 = tmem_base, dX = tmem_base + TN;
+            // mode 1 has no X accumulator: its TMEM columns double-buffer H (tile i + 1
+            // accumulates while the epilogue drains tile i); barriers tfull[4] / tfull[5]
+            const bool dbuf = prm.mode == 1;
+            int stage = 0, ab = 0;
+            uint32_t phase = 0, tphb = 0;
             for (int t = cluster_id; t < total_tiles; t += n_clusters) {
                 // one accumulation (and one epilogue hand-off) per phase; nph = 1: the whole K
                 for (int ph = 0; ph < prm.nph; ++ph) {
-                    mbar_wait_cluster(&tempty[0], tph ^ 1);
+                    uint64_t* tf = ab ? tfull + 4 : tfull;
+                    uint64_t* te = ab ? tfull + 5 : tempty;
+                    const uint32_t dH = dH0 + (ab ? (uint32_t)TN : 0u);
+                    mbar_wait_cluster(te, ((tphb >> ab) & 1u) ^ 1u);
                     fence_after();
                     const int kb0 = ph ? prm.kb_end[ph - 1] : 0, kb1 = prm.kb_end[ph];
-                    for (int kb = kb0; kb < kb1; ++kb) {
+                    const int ks = prm.mode == 1 ? 2 : 1;        // k-blocks per stage (see the producer)
+                    for (int kb = kb0; kb < kb1; kb += ks) {
                         mbar_wait(&full[stage], phase);
                         fence_after();
                         const uint32_t s0 = smem_u32(stages + stage * IG::STAGE_BYTES);
-                        const uint64_t ah = sdesc(s0), al = sdesc(s0 + IG::A_BYTES);
-                        const uint64_t bh = sdesc(s0 + 2 * IG::A_BYTES), bl = sdesc(s0 + 2 * IG::A_BYTES + IG::B_BYTES);
+                        if (prm.mode == 1) {
+                            const int nk = min(ks, kb1 - kb);
+                            for (int kk = 0; kk < nk; ++kk) {
+                                const uint64_t ah = sdesc(s0 + kk * IG::A_BYTES);
+                                const uint64_t bh = sdesc(s0 + 2 * IG::A_BYTES + kk * IG::B_BYTES);
 #pragma unroll
-                        for (int k = 0; k < 4; ++k) {               // 4 x 32 int8 of K per 128-byte row
-                            const uint64_t adv = (uint64_t)(k * 2);  // +32 B in the start-address field
-                            const uint32_t first = (kb != kb0 || k != 0) ? 1u : 0u;
-                            mma_i8(dH, ah + adv, bh + adv, id, first);
-                            mma_i8(dX, ah + adv, bl + adv, id, first);
-                            mma_i8(dX, al + adv, bh + adv, id, 1u);
+                                for (int k = 0; k < 4; ++k) {
+                                    const uint64_t adv = (uint64_t)(k * 2);
+                                    mma_i8(dH, ah + adv, bh + adv, id, (kb != kb0 || kk != 0 || k != 0) ? 1u : 0u);
+                                }
+                            }
+                        } else {
+                            const uint64_t ah = sdesc(s0), al = sdesc(s0 + IG::A_BYTES);
+                            const uint64_t bh = sdesc(s0 + 2 * IG::A_BYTES), bl = sdesc(s0 + 2 * IG::A_BYTES + IG::B_BYTES);
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) {               // 4 x 32 int8 of K per 128-byte row
+                                const uint64_t adv = (uint64_t)(k * 2);  // +32 B in the start-address field
+                                const uint32_t first = (kb != kb0 || k != 0) ? 1u : 0u;
+                                mma_i8(dH, ah + adv, bh + adv, id, first);
+                                mma_i8(dX, ah + adv, bl + adv, id, first);
+                                mma_i8(dX, al + adv, bh + adv, id, 1u);
+                            }
                         }
                         mma_commit<2>(&empty[stage]);
                         if (++stage == STAGES) { stage = 0; phase ^= 1; }
                     }
-                    mma_commit<2>(&tfull[0]);
-                    tph ^= 1;
+                    mma_commit<2>(tf);
+                    tphb ^= 1u << ab;
+                    if (dbuf) ab ^= 1;
                 }
             }
         }
     } else if constexpr (AUG) {
         epilogue_aug<MAXM, SEG, TN>(prm, tmem_base, tfull, tempty, s_nb, s_sb, s_T, hist_s, cluster_id, n_clusters,
                                 total_tiles, tiles_per_item, rank, warp, lane);
+    } else if (prm.mode == 1) {
+        epilogue_rowdot<MAXM, SEG, TN>(prm, tmem_base, tfull, tempty, cluster_id, n_clusters, total_tiles,
+                                       tiles_per_item, rank, warp, lane);
     } else {
         // ------------------------------------------------------------ epilogue
         // warp w reads TMEM lanes 32 (w % 4) .. +31 (its quarter); the NEPI epilogue warps split
@@ -694,7 +822,7 @@ static cudaError_t launch_i8_t(const tc::I8Params& prm, const CUtensorMap* maps,
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    ProfScope ps_(K_GRAM_TC, st);
+    ProfScope ps_(prm.mode == 1 ? K_RESAMPLE : K_GRAM_TC, st);   // mode 1 is the bootstrap resample
     cudaError_t e = cudaLaunchKernelEx(&cfg, tc::k_gram_i8<MAXM, SEG, AUG, TN>, maps[0], maps[1], maps[2], maps[3], prm);
     note_launch();
     if (e != cudaSuccess) {
@@ -758,6 +886,8 @@ cudaError_t launch_gram_i8(const I8Args& a, cudaStream_t st) {
     prm.diag = a.diag;
     prm.binout = a.binout;
     prm.skip = a.skip;
+    prm.mode = a.mode;
+    prm.m2 = a.m2; prm.rd_nt = a.rd_nt; prm.rd_m = a.rd_m; prm.rd_out = a.rd_out;
     prm.tiles_act = tc::tiles_active(prm.skip, prm.tiles_m, prm.tiles_n, a.sp.row_seg, a.sp.col_seg, a.rowsB, tn);
     if (prm.tiles_act == 0) return cudaSuccess;
     prm.nph = a.nph == 3 ? 3 : 1;

@@ -165,4 +165,157 @@ cudaError_t launch_resample(int P, const uint8_t* bins, int64_t N, int64_t Nt, i
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- tensor-core resample
+// The same multiplicity form as one integer GEMM per measure (gram_i8.cu, mode 1):
+//   counts[k][v] = sum_b m2_k[b] sum_a m1_k[a] E[v][b][a],   E[v][b][a] = [bins[a][b] > v]
+// A operand: M1 [P][n_rep][Kp] int8 (m1 <= n1 <= 127); B operand: E [P][M][Ntp][Kp] 0/1 bytes
+// (Ntp = N rounded up to 16, zero rows / columns beyond N); M2 [P][n_rep][Ntp] u16.
+
+// multiplicities of replicate k of item p (shared-memory counts, then 16-byte row stores)
+constexpr int kMultThreads = 128;
+__global__ void __launch_bounds__(kMultThreads) k_rd_mult(int64_t N, int64_t Kp, int64_t Ntp, int n_rep,
+                                                          const int32_t* __restrict__ I1, int64_t n1,
+                                                          const int32_t* __restrict__ I2, int64_t n2,
+                                                          int8_t* __restrict__ M1, uint16_t* __restrict__ M2,
+                                                          int32_t* __restrict__ status) {
+    constexpr int T = kMultThreads, U = 8;
+    extern __shared__ uint32_t mm_smem[];
+    uint32_t* m1 = mm_smem;          // [Kp]
+    uint32_t* m2 = m1 + Kp;          // [Ntp]
+    const int k = blockIdx.x, p = blockIdx.y, tid = threadIdx.x;
+    const int64_t row = (int64_t)p * n_rep + k;
+    for (int64_t a = tid; a < Kp + Ntp; a += T) m1[a] = 0u;
+    __syncthreads();
+    bool bad = false;
+    // the draws of both index sets, U independent loads in flight per thread
+    const int32_t* i1 = I1 + row * n1;
+    const int32_t* i2 = I2 + row * n2;
+    const int64_t n12 = n1 + n2;
+    for (int64_t base = 0; base < n12; base += (int64_t)T * U) {
+        int32_t r[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t i = base + (int64_t)u * T + tid;
+            r[u] = i < n1 ? __ldg(&i1[i]) : i < n12 ? __ldg(&i2[i - n1]) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t i = base + (int64_t)u * T + tid;
+            if (i >= n12) break;
+            if (r[u] >= 0 && r[u] < N) atomicAdd(&(i < n1 ? m1 : m2)[r[u]], 1u);
+            else bad = true;
+        }
+    }
+    if (__syncthreads_or(bad) && tid == 0) atomicOr(&status[p], CIL_ITEM_BADINDEX);
+    // Kp % 128 == 0, Ntp % 64 == 0: 16 int8 / 8 u16 per store
+    uint4* d1 = reinterpret_cast<uint4*>(M1 + row * Kp);
+    for (int64_t c = tid; c < Kp / 16; c += T) {
+        uint32_t w[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+            w[i] = m1[16 * c + 4 * i] | m1[16 * c + 4 * i + 1] << 8 | m1[16 * c + 4 * i + 2] << 16 |
+                   m1[16 * c + 4 * i + 3] << 24;
+        d1[c] = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+    uint4* d2 = reinterpret_cast<uint4*>(M2 + row * Ntp);
+    for (int64_t c = tid; c < Ntp / 8; c += T) {
+        uint32_t w[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) w[i] = m2[8 * c + 2 * i] | m2[8 * c + 2 * i + 1] << 16;
+        d2[c] = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+}
+
+// E[p][v][b][a0 .. a0+127] of measure q from a 128 (a) x 64 (b) block of bins (transposed
+// through shared memory; 8-byte loads along b when the rows allow, 16-byte stores along a)
+__global__ void __launch_bounds__(256) k_rd_build_E(const uint8_t* __restrict__ bins, int64_t N, int nq, int q,
+                                                    int M, int64_t Kp, int64_t Ntp, int8_t* __restrict__ E) {
+    __shared__ uint8_t tile[128][64 + 1];       // odd row stride: conflict-free column reads
+    const int p = blockIdx.z, tid = threadIdx.x;
+    const int64_t a0 = (int64_t)blockIdx.x * 128, b0 = (int64_t)blockIdx.y * 64;
+    const uint8_t* Bq = bins + ((int64_t)p * nq + q) * N * N;
+    const bool vec = (N % 8 == 0) && !(reinterpret_cast<uintptr_t>(bins) & 7u);
+    if (vec) {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {                      // 128 rows x 8 words of 8 bytes
+            const int i = tid + 256 * r, ai = i >> 3, c = i & 7;
+            const int64_t a = a0 + ai, b = b0 + 8 * c;
+            uint2 v = make_uint2(0u, 0u);
+            if (a < N && b < N) v = __ldg(reinterpret_cast<const uint2*>(Bq + a * N + b));   // N % 8 == 0
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                tile[ai][8 * c + u] = (uint8_t)(v.x >> (8 * u));
+                tile[ai][8 * c + 4 + u] = (uint8_t)(v.y >> (8 * u));
+            }
+        }
+    } else {
+        for (int i = tid; i < 128 * 64; i += 256) {
+            const int ai = i >> 6, bi = i & 63;
+            const int64_t a = a0 + ai, b = b0 + bi;
+            tile[ai][bi] = (a < N && b < N) ? __ldg(&Bq[a * N + b]) : (uint8_t)0;
+        }
+    }
+    __syncthreads();
+#pragma unroll 1
+    for (int h = 0; h < 2; ++h) {
+        const int bi = 32 * h + (tid >> 3), j = tid & 7;
+        uint8_t v16[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v16[i] = tile[16 * j + i][bi];
+        int8_t* dst = E + (((int64_t)p * M) * Ntp + b0 + bi) * Kp + a0 + 16 * j;
+        for (int v = 0; v < M; ++v) {
+            uint32_t w[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+            for (int i = 0; i < 16; ++i) w[i >> 2] |= (uint32_t)(v16[i] > v) << (8 * (i & 3));
+            __stcs(reinterpret_cast<uint4*>(dst + (int64_t)v * Ntp * Kp), make_uint4(w[0], w[1], w[2], w[3]));
+        }
+    }
+}
+
+__global__ void k_rd_final(const unsigned long long* __restrict__ cnt, int P, int n_rep, int M, int nq, int q,
+                           double npairs, double* __restrict__ y, int64_t y_item_stride) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (int64_t)P * n_rep * M) return;
+    const int v = (int)(i % M);
+    const int64_t pk = i / M;
+    const int k = (int)(pk % n_rep), p = (int)(pk / n_rep);
+    y[(int64_t)p * y_item_stride + ((int64_t)k * nq + q) * M + v] = (double)cnt[i] / npairs;   // as k_resample: same rounding
+}
+
+cudaError_t launch_rd_mult(int P, int64_t N, int64_t Kp, int64_t Ntp, int n_rep, const int32_t* I1, int64_t n1,
+                           const int32_t* I2, int64_t n2, int8_t* M1, uint16_t* M2, int32_t* status, cudaStream_t st) {
+    const size_t smem = sizeof(uint32_t) * (size_t)(Kp + Ntp);
+    if (smem > 200 * 1024) return cudaErrorInvalidValue;
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(k_rd_mult, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    ProfScope ps_(K_RESAMPLE, st);
+    k_rd_mult<<<dim3((unsigned)n_rep, (unsigned)P), kMultThreads, smem, st>>>(N, Kp, Ntp, n_rep, I1, n1, I2, n2, M1, M2,
+                                                                      status);
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_rd_build_E(int P, const uint8_t* bins, int64_t N, int nq, int q, int M, int64_t Kp, int64_t Ntp,
+                              int8_t* E, cudaStream_t st) {
+    if (Kp % 128 || Ntp % 64) return cudaErrorInvalidValue;
+    ProfScope ps_(K_RESAMPLE, st);
+    k_rd_build_E<<<dim3((unsigned)(Kp / 128), (unsigned)(Ntp / 64), (unsigned)P), 256, 0, st>>>(bins, N, nq, q, M,
+                                                                                                Kp, Ntp, E);
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_rd_final(const unsigned long long* cnt, int P, int n_rep, int M, int nq, int q, double npairs,
+                            double* y, int64_t y_item_stride, cudaStream_t st) {
+    const int64_t n = (int64_t)P * n_rep * M;
+    ProfScope ps_(K_RESAMPLE, st);
+    k_rd_final<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(cnt, P, n_rep, M, nq, q, npairs, y, y_item_stride);
+    note_launch();
+    return cudaGetLastError();
+}
+
 }  // namespace cil

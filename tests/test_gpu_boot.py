@@ -175,3 +175,34 @@ def test_mcil_boot_stats(cil, oracle_mod):
     mu_r, Sig_r = O.stats(Y.cpu().numpy())
     np.testing.assert_allclose(mu.cpu().numpy(), mu_r, rtol=1e-12, atol=1e-15)
     np.testing.assert_allclose(Sig.cpu().numpy(), Sig_r, rtol=1e-9, atol=1e-15)
+
+
+@pytest.mark.parametrize("N_syn,N_set,n_rep,M,mask", [(300, 40, 150, 13, 0b000011), (257, 127, 9, 5, 0b000001),
+                                                      (1000, 50, 300, 13, 0b000001)])
+def test_synth_boot_tc_resample_bit_exact(cil, oracle_mod, N_syn, N_set, n_rep, M, mask):
+    """The tensor-core resample inside Alg. A2 (one integer GEMM per measure: replicate row
+    multiplicities x 0/1 threshold rows, then the column multiplicities in the epilogue) gives
+    exactly the replicate vectors of the shared-atomic resample over the same bin matrix."""
+    O = oracle_mod
+    dev = torch.device("cuda")
+    grid = (2, 16, 16, 0.0)
+    P = 2
+    pools = torch.stack([cilgen.make_set(71, 10 + p, N_syn, grid[:3], n_w=4.6 + 0.3 * p) for p in range(P)])
+    data = cilgen.make_set(71, 99, N_set, grid[:3])
+    radii, draws = [], []
+    for p in range(P):
+        D = O.distance_matrix(pools[p, :40].numpy(), pools[p, 40:80].numpy(), grid, mask)
+        radii.append(_radii(D, M))
+        draws.append(cilgen.boot_draws_a2(72, p, n_rep, N_syn, N_set))
+    radii = torch.tensor(np.array(radii), device=dev)
+    I1 = torch.tensor(np.stack([d[0] for d in draws]), device=dev)
+    I2 = torch.tensor(np.stack([d[1] for d in draws]), device=dev)
+    J = torch.tensor(np.stack([d[2] for d in draws]), device=dev)
+    pd = pools.to(dev)
+    _, st, Y = cil.synth_loglik_boot(pd, data.to(dev), N_set, I1, I2, J, grid, mask, radii, ridge=1e-5,
+                                     return_Y=True)
+    bins, bst = cil.bin_matrix(pd, pd, grid, mask, radii)
+    _, y, rst = cil.resample_counts(bins, I1, I2, M, want_counts=False)
+    torch.cuda.synchronize()
+    assert st.tolist() == [0] * P and bst.tolist() == [0] * P and rst.tolist() == [0] * P
+    assert torch.equal(Y[:, :n_rep], y)
