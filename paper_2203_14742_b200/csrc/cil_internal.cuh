@@ -220,6 +220,9 @@ struct I8Args {
     float ih;                            // 1/h
     int skip;                            // tile skipping: 0 none, 1 symmetric bins, 2 Alg. 1 triangle
     int sm_budget;                       // SMs the persistent grid may occupy (0 = all)
+    // explicit plane offsets (rows): A rows at a_off + p rowsA, B rows at b_off + p rowsB
+    bool offs_set;
+    int64_t a_off, b_off;
     // mode 1 (row-dot): one-digit operands hq only; counts[p][k][v] = sum_b C[k][v rd_nt + b] m2[p][k][b]
     int mode;
     const uint16_t* m2;

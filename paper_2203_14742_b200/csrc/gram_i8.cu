@@ -24,6 +24,7 @@
 #include <stdlib.h>
 
 
+#include <algorithm>
 #include "cil_internal.cuh"
 #include "tc_common.cuh"
 
@@ -33,6 +34,7 @@ namespace tc {
 struct I8Params {
     int64_t rowsA, rowsB;
     int64_t b_off;             // first B row in the stacked planes: P*rowsA, or 0 when B = A (packed once)
+    int64_t a_off;             // first A row in the stacked planes (0 unless the caller places A after B)
     int P, p0, np;
     int n_kb;
     int tiles_m, tiles_n;
@@ -187,7 +189,7 @@ __device__ __forceinline__ void epilogue_aug(const I8Params& prm, uint32_t tmem_
         const int64_t browbase = prm.b_off + (int64_t)p * prm.rowsB;
         const int64_t row = (int64_t)mt * G::TILE_M + rank * A_ROWS + quarter * 32 + lane;
         const bool row_ok = row < prm.rowsA;
-        const int64_t arow = (int64_t)p * prm.rowsA + (row_ok ? row : 0);
+        const int64_t arow = prm.a_off + (int64_t)p * prm.rowsA + (row_ok ? row : 0);
         const int hc0 = (int)(col0 + half * IG::HALF);
         const int nvalid = (int)min((int64_t)IG::HALF, prm.rowsB - hc0);
         const uint32_t tl = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(half * IG::HALF);
@@ -447,6 +449,7 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
         mbar_init(&tempty[0], 2 * IG::NEPI);              // epilogue warps x 2 CTAs
         mbar_init(tfull + 4, 1);                          // second accumulator (mode 1)
         mbar_init(tfull + 5, 2 * IG::NEPI);
+        for (int s = 0; s < 2 * STAGES; ++s) { mbar_init(tfull + 6 + s, 1); mbar_init(tfull + 6 + 2 * STAGES + s, 1); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&mAh) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&mAl) : "memory");
@@ -467,28 +470,35 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
 
     if (warp == 0) {
         if (lane == 0) {
-            int stage = 0;
-            uint32_t phase = 0;
+            int stage = 0, slot1 = 0;
+            uint32_t phase = 0, ph1 = 0;
             for (int t = cluster_id; t < total_tiles; t += n_clusters) {
                 const int p = prm.p0 + t / tiles_per_item;
                 int mt, nt;
                 tile_of(prm, t % tiles_per_item, mt, nt);
-                const int ya = (int)(p * prm.rowsA + (int64_t)mt * G::TILE_M + rank * A_ROWS);
+                const int ya = (int)(prm.a_off + p * prm.rowsA + (int64_t)mt * G::TILE_M + rank * A_ROWS);
                 const int yb = (int)(prm.b_off + p * prm.rowsB + (int64_t)nt * TN + rank * IG::B_ROWS);
-                // mode 1 (one-digit operands) packs two k-blocks per stage: the l-plane slots hold
-                // the h planes of k-block kb + 1 (a deeper ring for its short per-stage MMA time)
-                const int ks = prm.mode == 1 ? 2 : 1;
-                for (int kb = 0; kb < prm.n_kb; kb += ks) {
+                if (prm.mode == 1) {
+                    // one-digit operands: the stage memory is a ring of 2 STAGES (A_h | B_h) slots,
+                    // a deeper ring for the short per-k-block MMA time (barriers tfull[6 ..])
+                    for (int kb = 0; kb < prm.n_kb; ++kb) {
+                        mbar_wait(tfull + 6 + 2 * STAGES + slot1, ph1 ^ 1);
+                        unsigned char* st = stages + slot1 * (IG::A_BYTES + IG::B_BYTES);
+                        uint64_t* f = tfull + 6 + slot1;
+                        if (rank == 0) mbar_expect_tx(f, 2 * (IG::A_BYTES + IG::B_BYTES));
+                        tma_load_2d<2>(st, &mAh, f, kb * 128, ya);
+                        tma_load_2d<2>(st + IG::A_BYTES, &mBh, f, kb * 128, yb);
+                        if (++slot1 == 2 * STAGES) { slot1 = 0; ph1 ^= 1; }
+                    }
+                    continue;
+                }
+                for (int kb = 0; kb < prm.n_kb; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     unsigned char* st = stages + stage * IG::STAGE_BYTES;
                     // diagnostics: dbg 3 skips the B loads, dbg 4 all loads (MMA rate alone)
                     const bool only_a = prm.dbg == 3, none = prm.dbg == 4;
-                    const bool hi_only = prm.mode == 1;         // one-digit operands: h planes only
-                    const int nk = min(ks, prm.n_kb - kb);
                     if (rank == 0)
-                        mbar_expect_tx(&full[stage], none ? 0 : only_a ? 4 * IG::A_BYTES
-                                                             : hi_only ? 2 * nk * (IG::A_BYTES + IG::B_BYTES)
-                                                                       : 2 * IG::STAGE_BYTES);
+                        mbar_expect_tx(&full[stage], none ? 0 : only_a ? 4 * IG::A_BYTES : 2 * IG::STAGE_BYTES);
                     const int x = kb * 128;
                     if (prm.pf > 0 && kb + prm.pf < prm.n_kb) {   // L2 prefetch pf k-blocks ahead
                         const int xp = (kb + prm.pf) * 128;
@@ -497,20 +507,13 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
                         tma_prefetch_2d(&mBh, xp, yb);
                         tma_prefetch_2d(&mBl, xp, yb);
                     }
-                    if (hi_only) {
-                        for (int kk = 0; kk < nk; ++kk) {
-                            tma_load_2d<2>(st + kk * IG::A_BYTES, &mAh, &full[stage], x + kk * 128, ya);
-                            tma_load_2d<2>(st + 2 * IG::A_BYTES + kk * IG::B_BYTES, &mBh, &full[stage], x + kk * 128, yb);
-                        }
-                    } else {
-                        if (!none) {
-                            tma_load_2d<2>(st, &mAh, &full[stage], x, ya);
-                            tma_load_2d<2>(st + IG::A_BYTES, &mAl, &full[stage], x, ya);
-                        }
-                        if (!only_a && !none) {
-                            tma_load_2d<2>(st + 2 * IG::A_BYTES, &mBh, &full[stage], x, yb);
-                            tma_load_2d<2>(st + 2 * IG::A_BYTES + IG::B_BYTES, &mBl, &full[stage], x, yb);
-                        }
+                    if (!none) {
+                        tma_load_2d<2>(st, &mAh, &full[stage], x, ya);
+                        tma_load_2d<2>(st + IG::A_BYTES, &mAl, &full[stage], x, ya);
+                    }
+                    if (!only_a && !none) {
+                        tma_load_2d<2>(st + 2 * IG::A_BYTES, &mBh, &full[stage], x, yb);
+                        tma_load_2d<2>(st + 2 * IG::A_BYTES + IG::B_BYTES, &mBl, &full[stage], x, yb);
                     }
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
@@ -522,9 +525,8 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
             const uint32_t dH0 = tmem_base, dX = tmem_base + TN;
             // mode 1 has no X accumulator: its TMEM columns double-buffer H (tile i + 1
             // accumulates while the epilogue drains tile i); barriers tfull[4] / tfull[5]
-            const bool dbuf = prm.mode == 1;
-            int stage = 0, ab = 0;
-            uint32_t phase = 0, tphb = 0;
+            int stage = 0, ab = 0, slot1 = 0;
+            uint32_t phase = 0, tphb = 0, ph1 = 0;
             for (int t = cluster_id; t < total_tiles; t += n_clusters) {
                 // one accumulation (and one epilogue hand-off) per phase; nph = 1: the whole K
                 for (int ph = 0; ph < prm.nph; ++ph) {
@@ -534,23 +536,28 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
                     mbar_wait_cluster(te, ((tphb >> ab) & 1u) ^ 1u);
                     fence_after();
                     const int kb0 = ph ? prm.kb_end[ph - 1] : 0, kb1 = prm.kb_end[ph];
-                    const int ks = prm.mode == 1 ? 2 : 1;        // k-blocks per stage (see the producer)
-                    for (int kb = kb0; kb < kb1; kb += ks) {
+                    if (prm.mode == 1) {
+                        for (int kb = kb0; kb < kb1; ++kb) {
+                            mbar_wait(tfull + 6 + slot1, ph1);
+                            fence_after();
+                            const uint32_t s0 = smem_u32(stages + slot1 * (IG::A_BYTES + IG::B_BYTES));
+                            const uint64_t ah = sdesc(s0), bh = sdesc(s0 + IG::A_BYTES);
+#pragma unroll
+                            for (int k = 0; k < 4; ++k)
+                                mma_i8(dH, ah + (uint64_t)(k * 2), bh + (uint64_t)(k * 2), id, (kb != kb0 || k != 0) ? 1u : 0u);
+                            mma_commit<2>(tfull + 6 + 2 * STAGES + slot1);
+                            if (++slot1 == 2 * STAGES) { slot1 = 0; ph1 ^= 1; }
+                        }
+                        mma_commit<2>(tf);
+                        tphb ^= 1u << ab;
+                        ab ^= 1;
+                        continue;
+                    }
+                    for (int kb = kb0; kb < kb1; ++kb) {
                         mbar_wait(&full[stage], phase);
                         fence_after();
                         const uint32_t s0 = smem_u32(stages + stage * IG::STAGE_BYTES);
-                        if (prm.mode == 1) {
-                            const int nk = min(ks, kb1 - kb);
-                            for (int kk = 0; kk < nk; ++kk) {
-                                const uint64_t ah = sdesc(s0 + kk * IG::A_BYTES);
-                                const uint64_t bh = sdesc(s0 + 2 * IG::A_BYTES + kk * IG::B_BYTES);
-#pragma unroll
-                                for (int k = 0; k < 4; ++k) {
-                                    const uint64_t adv = (uint64_t)(k * 2);
-                                    mma_i8(dH, ah + adv, bh + adv, id, (kb != kb0 || kk != 0 || k != 0) ? 1u : 0u);
-                                }
-                            }
-                        } else {
+                        {
                             const uint64_t ah = sdesc(s0), al = sdesc(s0 + IG::A_BYTES);
                             const uint64_t bh = sdesc(s0 + 2 * IG::A_BYTES), bl = sdesc(s0 + 2 * IG::A_BYTES + IG::B_BYTES);
 #pragma unroll
@@ -567,7 +574,6 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
                     }
                     mma_commit<2>(tf);
                     tphb ^= 1u << ab;
-                    if (dbuf) ab ^= 1;
                 }
             }
         }
@@ -610,7 +616,7 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
             named_bar(1, IG::NET);
             const int64_t row = (int64_t)mt * G::TILE_M + rank * A_ROWS + quarter * 32 + lane;
             const bool row_ok = row < prm.rowsA;
-            const int64_t arow = (int64_t)p * prm.rowsA + (row_ok ? row : 0);
+            const int64_t arow = prm.a_off + (int64_t)p * prm.rowsA + (row_ok ? row : 0);
             const float na = row_ok ? __ldg(&prm.nrm[arow]) : 0.f;
             const float sa = row_ok ? __ldg(&prm.scl[arow]) : 0.f;
 
@@ -853,7 +859,11 @@ static cudaError_t dispatch_i8(const tc::I8Params& prm, const CUtensorMap* maps,
 
 cudaError_t launch_gram_i8(const I8Args& a, cudaStream_t st) {
     if (a.rowsA == 0 || a.rowsB == 0) return cudaSuccess;
-    const int64_t rows = (int64_t)a.P * (a.b_same ? a.rowsA : a.rowsA + a.rowsB);
+    int64_t rows = (int64_t)a.P * (a.b_same ? a.rowsA : a.rowsA + a.rowsB);
+    if (a.offs_set) {
+        if (a.b_same || a.a_off < 0 || a.b_off < 0) return cudaErrorInvalidValue;
+        rows = std::max(a.a_off + (int64_t)a.P * a.rowsA, a.b_off + (int64_t)a.P * a.rowsB);
+    }
     if (rows >= (1ll << 31) || (a.b_same && a.rowsA != a.rowsB)) return cudaErrorInvalidValue;
     // B columns per tile: 192 when that pads the B panel less than 256 (e.g. 550 -> 576 instead
     // of 768); the mirrored symmetric layout needs square tiles
@@ -870,7 +880,8 @@ cudaError_t launch_gram_i8(const I8Args& a, cudaStream_t st) {
         return cudaErrorInvalidValue;
     tc::I8Params prm{};
     prm.rowsA = a.rowsA; prm.rowsB = a.rowsB;
-    prm.b_off = a.b_same ? 0 : (int64_t)a.P * a.rowsA;
+    prm.b_off = a.offs_set ? a.b_off : a.b_same ? 0 : (int64_t)a.P * a.rowsA;
+    prm.a_off = a.offs_set ? a.a_off : 0;
     prm.P = a.P; prm.p0 = a.p0; prm.np = a.np > 0 ? a.np : a.P - a.p0;
     prm.n_kb = (int)(a.Kp / 128);
     prm.tiles_m = (int)((a.rowsA + tc::Geo<2>::TILE_M - 1) / tc::Geo<2>::TILE_M);

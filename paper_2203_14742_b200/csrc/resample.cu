@@ -51,7 +51,8 @@ __global__ void __launch_bounds__(kRsThreads) k_resample(const uint8_t* __restri
     __shared__ uint32_t red[8][kMaxM + 1];
     const int k = blockIdx.x, p = blockIdx.y;
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    const int32_t* i1 = I1 + ((int64_t)p * n_rep + k) * n1;
+    // I1 == nullptr: the identity draw (every row a < n1 once; the y~ counts of Alg. A2 step 4)
+    const int32_t* i1 = I1 ? I1 + ((int64_t)p * n_rep + k) * n1 : nullptr;
     const int32_t* i2 = I2 + ((int64_t)p * n_rep + k) * n2;
     const int64_t Nt16 = (Nt + 15) & ~(int64_t)15;
     for (int64_t a = tid; a < N; a += kRsThreads) m1[a] = 0u;
@@ -59,7 +60,7 @@ __global__ void __launch_bounds__(kRsThreads) k_resample(const uint8_t* __restri
     __syncthreads();
     bool bad = false;
     for (int64_t i = tid; i < n1; i += kRsThreads) {
-        const int32_t r = __ldg(&i1[i]);
+        const int32_t r = i1 ? __ldg(&i1[i]) : (int32_t)i;
         if (r >= 0 && r < N) atomicAdd(&m1[r], 1u);          // invalid draws: flagged, skipped
         else bad = true;
     }
