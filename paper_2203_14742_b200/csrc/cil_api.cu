@@ -798,7 +798,7 @@ bool boot_rd(int32_t N_syn, int32_t N_set, int32_t n_rep, int32_t P, int nq, int
     if (engine == CIL_ENGINE_SIMT || N_set > 127) return false;
     const int64_t Nt = (int64_t)N_syn - N_set;
     if (Nt > 65535 || (int64_t)N_set * Nt >= (1ll << 32)) return false;
-    const int64_t ntp = N_syn <= 128 ? 128 : ((int64_t)N_syn + 63) / 64 * 64;   // >= 128: gram_i8 rowdot
+    const int64_t ntp = ((int64_t)N_syn + 255) / 256 * 256;   // gram_i8 mode 1: b-blocks of 256
     if ((int64_t)P * (n_rep + (int64_t)M * ntp) >= (1ll << 31)) return false;
     const int64_t kp = ((int64_t)N_syn + kTcBK - 1) / kTcBK * kTcBK;
     return 4 * (kp + ntp) <= 200 * 1024 && nq >= 1;
@@ -818,7 +818,7 @@ bool boot_layout(int32_t P, int32_t N_syn, int32_t N_set, int32_t n_rep, const c
     B->rd = boot_rd(N_syn, N_set, n_rep, P, sl.nq, M, engine);
     if (B->rd) {
         B->kp_rd = ((int64_t)N_syn + kTcBK - 1) / kTcBK * kTcBK;
-        B->ntp = N_syn <= 128 ? 128 : ((int64_t)N_syn + 63) / 64 * 64;
+        B->ntp = ((int64_t)N_syn + 255) / 256 * 256;
         B->off_m1 = B->total;                                        // M1 rows, then E rows (stacked planes)
         B->off_e = B->off_m1 + (size_t)P * n_rep * B->kp_rd;
         B->total = al(B->off_e + (size_t)P * M * B->ntp * B->kp_rd);

@@ -332,6 +332,54 @@ __device__ __forceinline__ void epilogue_aug(const I8Params& prm, uint32_t tmem_
     }
 }
 
+// mode 1 barriers after tfull[6]: the streaming ring (2 STAGES full + 2 STAGES empty) or, with
+// the A panel resident, a_full, a_empty, then kRdSlots B full + kRdSlots B empty
+constexpr int kRdSlots = 16;
+constexpr int kRdBars = 2 + 2 * kRdSlots;
+// Tile sequence of one cluster in mode 1 (the same for producer, MMA and epilogue).
+// Resident A: clusters form groups of tiles_m; cluster (g, mt) keeps tile row mt and walks the
+// group's contiguous range of (item, nt) columns, so the tiles_m clusters of a group read each
+// B tile at about the same time (one HBM read of B, A loaded once per item).  Streaming: the
+// persistent stride of the other modes.
+struct RdSeq {
+    bool resA;
+    int n, mt, c0, tiles_n, stride, first;
+    __device__ __forceinline__ void init(const I8Params& prm, bool resA_, int cluster_id, int n_clusters,
+                                         int total_tiles) {
+        resA = resA_;
+        tiles_n = prm.tiles_n;
+        if (resA) {
+            const int G = n_clusters / prm.tiles_m;
+            const int g = cluster_id / prm.tiles_m;
+            mt = cluster_id % prm.tiles_m;
+            const int C = prm.np * prm.tiles_n;
+            c0 = g < G ? (int)((int64_t)g * C / G) : 0;
+            n = g < G ? (int)((int64_t)(g + 1) * C / G) - c0 : 0;
+        } else {
+            first = cluster_id;
+            stride = n_clusters;
+            n = cluster_id < total_tiles ? (total_tiles - 1 - cluster_id) / n_clusters + 1 : 0;
+        }
+    }
+    __device__ __forceinline__ void get(const I8Params& prm, int i, int tiles_per_item, int& p, int& mt_, int& nt) const {
+        if (resA) {
+            const int c = c0 + i;
+            p = prm.p0 + c / tiles_n;
+            nt = c % tiles_n;
+            mt_ = mt;
+        } else {
+            const int t = first + i * stride;
+            p = prm.p0 + t / tiles_per_item;
+            tile_of(prm, t % tiles_per_item, mt_, nt);
+        }
+    }
+};
+template <typename IG, int STAGES>
+__device__ __forceinline__ bool rd_resident_a(const I8Params& prm, int n_clusters) {
+    return prm.skip == 0 && prm.tiles_m <= n_clusters &&
+           prm.n_kb * IG::A_BYTES + 2 * IG::B_BYTES <= STAGES * IG::STAGE_BYTES;
+}
+
 // Row-dot epilogue (mode 1, bootstrap replicate counts on the tensor cores): the Gram of one-
 // digit operands is C[k][c] = sum_a M1[k][a] E[c][a] (replicate k's row-draw multiplicities
 // against the 0/1 threshold rows E[v*Nt + b][a] = [bins(a, b) > v]); the epilogue forms
@@ -350,67 +398,76 @@ __device__ __forceinline__ void epilogue_rowdot(const I8Params& prm, uint32_t tm
     const int kq = ew >> 2;
     const int g0 = kq * (TN / 16) / nwq, g1 = (kq + 1) * (TN / 16) / nwq;
     const int ncol = (g1 - g0) * 16;
+    // B rows are b-major: row (bt, v, i) = bt M TN + v TN + i holds column b = bt TN + i of
+    // threshold v, so tile nt is (bt, v) = (nt / M, nt % M), all its columns share v, and the
+    // column multiplicities of a thread stay in registers across the M tiles of one b-block
     const int Nt = (int)prm.rd_nt;
+    const int Mv = prm.rd_m;
+    constexpr int MAXG = (TN / 16 + 2) / 3;
+    uint4 w[MAXG][2];
+    int64_t wkey = -1;                                        // (item, row, bt) of the cached weights
     uint32_t tphb = 0;
     int ab = 0;
-    for (int t = cluster_id; t < total_tiles; t += n_clusters, ab ^= 1) {
-        const int p = prm.p0 + t / tiles_per_item;
-        int mt, nt;
-        tile_of(prm, t % tiles_per_item, mt, nt);
+    RdSeq seq;
+    seq.init(prm, rd_resident_a<IG, IG::STAGES>(prm, n_clusters), cluster_id, n_clusters, total_tiles);
+    for (int i = 0; i < seq.n; ++i, ab ^= 1) {
+        int p, mt, nt;
+        seq.get(prm, i, tiles_per_item, p, mt, nt);
         const int64_t row = (int64_t)mt * G::TILE_M + rank * A_ROWS + quarter * 32 + lane;
         const bool row_ok = row < prm.rowsA;
-        const int hc0 = nt * TN + g0 * 16;
-        const int nvalid = (int)min((int64_t)ncol, prm.rowsB - hc0);
-        const int ng = nvalid > 0 ? (nvalid + 15) / 16 : 0;
+        const int bt = nt / Mv, v = nt - bt * Mv;
+        const int ng = prm.dbg == 1 ? 0 : g1 - g0;           // dbg 1: hand-off only
         const uint32_t tl = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(ab * TN + g0 * 16);
-        // rd_nt is a multiple of 16, so a 16-column group lies inside one threshold block v
-        const uint16_t* m2row = prm.m2 + ((int64_t)p * prm.rowsA + (row_ok ? row : 0)) * Nt;
-        unsigned long long* out = prm.rd_out + ((int64_t)p * prm.rowsA + (row_ok ? row : 0)) * prm.rd_m;
-        // all of this tile's column multiplicities load while the MMAs finish (<= MAXG groups)
-        constexpr int MAXG = (TN / 16 + 2) / 3;
-        uint4 w[MAXG][2];
-        const int v0 = hc0 / Nt;
-        const int bnd = (v0 + 1) * Nt;                         // first column of block v0 + 1
+        const int64_t key = ((int64_t)p * prm.tiles_m + mt) * (prm.tiles_n / Mv) + bt;
+        if (key != wkey) {                                    // new b-block: load this thread's weights
+            wkey = key;
+            const uint16_t* m2row = prm.m2 + ((int64_t)p * prm.rowsA + (row_ok ? row : 0)) * Nt + bt * TN + g0 * 16;
 #pragma unroll
-        for (int g = 0; g < MAXG; ++g) {
-            w[g][0] = w[g][1] = make_uint4(0u, 0u, 0u, 0u);
-            if (row_ok && g < ng) {
-                const int c = hc0 + g * 16;
-                const uint4* mp = reinterpret_cast<const uint4*>(m2row + (c < bnd ? c - v0 * Nt : c - bnd));
-                w[g][0] = __ldg(mp); w[g][1] = __ldg(mp + 1);
+            for (int g = 0; g < MAXG; ++g) {
+                w[g][0] = w[g][1] = make_uint4(0u, 0u, 0u, 0u);
+                if (row_ok && g < ng && prm.dbg != 5) {       // dbg 5: no weight loads (diagnostic)
+                    const uint4* mp = reinterpret_cast<const uint4*>(m2row + g * 16);
+                    w[g][0] = __ldg(mp); w[g][1] = __ldg(mp + 1);
+                }
             }
         }
         uint64_t* tf = ab ? tfull + 4 : tfull;
         uint64_t* te = ab ? tfull + 5 : tempty;
         mbar_wait(tf, (tphb >> ab) & 1u);
         fence_after();
-        // a thread's <= 16 MAXG columns span at most two threshold blocks (rd_nt >= 128)
-        uint32_t acc0 = 0u, acc1 = 0u;                        // <= n1 n2 < 2^32 (host-checked)
+        uint32_t acc = 0u;                                    // <= n1 n2 < 2^32 (host-checked)
+        // two groups per TMEM load (one wait::ld per 32 columns)
 #pragma unroll
-        for (int g = 0; g < MAXG; ++g) {
-            if (g < ng) {
-                uint32_t hv[16];
-                tmem_ld16(tl + g * 16, hv);
-                const uint32_t mw[8] = {w[g][0].x, w[g][0].y, w[g][0].z, w[g][0].w,
-                                        w[g][1].x, w[g][1].y, w[g][1].z, w[g][1].w};
-                uint32_t s = 0u;
-#pragma unroll
-                for (int jj = 0; jj < 8; ++jj) {
-                    s += hv[2 * jj] * (mw[jj] & 0xffffu);
-                    s += hv[2 * jj + 1] * (mw[jj] >> 16);
+        for (int g2 = 0; g2 < MAXG; g2 += 2) {
+            if (g2 < ng) {
+                uint32_t hv[32];
+                if (g2 + 1 < ng) {
+                    tmem_ld32(tl + g2 * 16, hv);
+                } else {                                      // odd tail: never read past the warp's range
+                    uint32_t (&lo)[16] = *reinterpret_cast<uint32_t(*)[16]>(&hv[0]);
+                    tmem_ld16(tl + g2 * 16, lo);
                 }
-                if (hc0 + g * 16 < bnd) acc0 += s;
-                else acc1 += s;
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int g = g2 + h;
+                    if (g < MAXG && g < ng) {
+                        const uint32_t mw[8] = {w[g][0].x, w[g][0].y, w[g][0].z, w[g][0].w,
+                                                w[g][1].x, w[g][1].y, w[g][1].z, w[g][1].w};
+#pragma unroll
+                        for (int jj = 0; jj < 8; ++jj) {
+                            acc += hv[16 * h + 2 * jj] * (mw[jj] & 0xffffu);
+                            acc += hv[16 * h + 2 * jj + 1] * (mw[jj] >> 16);
+                        }
+                    }
+                }
             }
         }
-        // release the accumulator first: the atomics complete while the next tile accumulates
+        // release the accumulator first: the atomic completes while the next tile accumulates
         fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_remote(te, 0);
-        if (row_ok) {
-            if (acc0) atomicAdd(&out[v0], (unsigned long long)acc0);
-            if (acc1) atomicAdd(&out[v0 + 1], (unsigned long long)acc1);
-        }
+        if (row_ok && acc)
+            atomicAdd(prm.rd_out + ((int64_t)p * prm.rowsA + row) * Mv + v, (unsigned long long)acc);
         tphb ^= 1u << ab;
     }
 }
@@ -449,7 +506,7 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
         mbar_init(&tempty[0], 2 * IG::NEPI);              // epilogue warps x 2 CTAs
         mbar_init(tfull + 4, 1);                          // second accumulator (mode 1)
         mbar_init(tfull + 5, 2 * IG::NEPI);
-        for (int s = 0; s < 2 * STAGES; ++s) { mbar_init(tfull + 6 + s, 1); mbar_init(tfull + 6 + 2 * STAGES + s, 1); }
+        for (int s = 6; s < 6 + kRdBars; ++s) mbar_init(tfull + s, 1);   // mode-1 rings (count 1 each)
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&mAh) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&mAl) : "memory");
@@ -470,28 +527,59 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
 
     if (warp == 0) {
         if (lane == 0) {
-            int stage = 0, slot1 = 0;
-            uint32_t phase = 0, ph1 = 0;
-            for (int t = cluster_id; t < total_tiles; t += n_clusters) {
+            int stage = 0;
+            uint32_t phase = 0;
+            if (prm.mode == 1) {
+                // one-digit operands (h planes only).  A resident: the A row block (all k-blocks)
+                // stays in shared memory while the cluster's consecutive tiles stream B through a
+                // ring; otherwise the stage memory is a ring of 2 STAGES (A_h | B_h) slots.
+                const bool resA = rd_resident_a<IG, STAGES>(prm, n_clusters);
+                const int nsb = min(kRdSlots, (STAGES * IG::STAGE_BYTES - prm.n_kb * IG::A_BYTES) / IG::B_BYTES);
+                unsigned char* bring = stages + prm.n_kb * IG::A_BYTES;
+                int key_prev = -1, sb = 0;
+                uint32_t aph = 0, bph = 0;
+                RdSeq seq;
+                seq.init(prm, resA, cluster_id, n_clusters, total_tiles);
+                for (int i = 0; i < seq.n; ++i) {
+                    int p, mt, nt;
+                    seq.get(prm, i, tiles_per_item, p, mt, nt);
+                    const int ya = (int)(prm.a_off + p * prm.rowsA + (int64_t)mt * G::TILE_M + rank * A_ROWS);
+                    const int yb = (int)(prm.b_off + p * prm.rowsB + (int64_t)nt * TN + rank * IG::B_ROWS);
+                    if (resA) {
+                        const int key = p * prm.tiles_m + mt;
+                        if (key != key_prev) {
+                            mbar_wait(tfull + 7, aph ^ 1);
+                            if (rank == 0) mbar_expect_tx(tfull + 6, 2 * prm.n_kb * IG::A_BYTES);
+                            for (int kb = 0; kb < prm.n_kb; ++kb)
+                                tma_load_2d<2>(stages + kb * IG::A_BYTES, &mAh, tfull + 6, kb * 128, ya);
+                            aph ^= 1;
+                            key_prev = key;
+                        }
+                        for (int kb = 0; kb < prm.n_kb; ++kb) {
+                            mbar_wait(tfull + 8 + kRdSlots + sb, bph ^ 1);
+                            if (rank == 0) mbar_expect_tx(tfull + 8 + sb, 2 * IG::B_BYTES);
+                            tma_load_2d<2>(bring + sb * IG::B_BYTES, &mBh, tfull + 8 + sb, kb * 128, yb);
+                            if (++sb == nsb) { sb = 0; bph ^= 1; }
+                        }
+                    } else {
+                        for (int kb = 0; kb < prm.n_kb; ++kb) {
+                            mbar_wait(tfull + 6 + 2 * STAGES + sb, bph ^ 1);
+                            unsigned char* st = stages + sb * (IG::A_BYTES + IG::B_BYTES);
+                            uint64_t* f = tfull + 6 + sb;
+                            if (rank == 0) mbar_expect_tx(f, 2 * (IG::A_BYTES + IG::B_BYTES));
+                            tma_load_2d<2>(st, &mAh, f, kb * 128, ya);
+                            tma_load_2d<2>(st + IG::A_BYTES, &mBh, f, kb * 128, yb);
+                            if (++sb == 2 * STAGES) { sb = 0; bph ^= 1; }
+                        }
+                    }
+                }
+            }
+            for (int t = cluster_id; t < total_tiles && prm.mode != 1; t += n_clusters) {
                 const int p = prm.p0 + t / tiles_per_item;
                 int mt, nt;
                 tile_of(prm, t % tiles_per_item, mt, nt);
                 const int ya = (int)(prm.a_off + p * prm.rowsA + (int64_t)mt * G::TILE_M + rank * A_ROWS);
                 const int yb = (int)(prm.b_off + p * prm.rowsB + (int64_t)nt * TN + rank * IG::B_ROWS);
-                if (prm.mode == 1) {
-                    // one-digit operands: the stage memory is a ring of 2 STAGES (A_h | B_h) slots,
-                    // a deeper ring for the short per-k-block MMA time (barriers tfull[6 ..])
-                    for (int kb = 0; kb < prm.n_kb; ++kb) {
-                        mbar_wait(tfull + 6 + 2 * STAGES + slot1, ph1 ^ 1);
-                        unsigned char* st = stages + slot1 * (IG::A_BYTES + IG::B_BYTES);
-                        uint64_t* f = tfull + 6 + slot1;
-                        if (rank == 0) mbar_expect_tx(f, 2 * (IG::A_BYTES + IG::B_BYTES));
-                        tma_load_2d<2>(st, &mAh, f, kb * 128, ya);
-                        tma_load_2d<2>(st + IG::A_BYTES, &mBh, f, kb * 128, yb);
-                        if (++slot1 == 2 * STAGES) { slot1 = 0; ph1 ^= 1; }
-                    }
-                    continue;
-                }
                 for (int kb = 0; kb < prm.n_kb; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     unsigned char* st = stages + stage * IG::STAGE_BYTES;
@@ -525,9 +613,65 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
             const uint32_t dH0 = tmem_base, dX = tmem_base + TN;
             // mode 1 has no X accumulator: its TMEM columns double-buffer H (tile i + 1
             // accumulates while the epilogue drains tile i); barriers tfull[4] / tfull[5]
-            int stage = 0, ab = 0, slot1 = 0;
-            uint32_t phase = 0, tphb = 0, ph1 = 0;
-            for (int t = cluster_id; t < total_tiles; t += n_clusters) {
+            int stage = 0, ab = 0;
+            uint32_t phase = 0, tphb = 0;
+            if (prm.mode == 1) {                            // see the producer
+                const bool resA = rd_resident_a<IG, STAGES>(prm, n_clusters);
+                const int nsb = min(kRdSlots, (STAGES * IG::STAGE_BYTES - prm.n_kb * IG::A_BYTES) / IG::B_BYTES);
+                unsigned char* bring = stages + prm.n_kb * IG::A_BYTES;
+                int key_prev = -1, sb = 0;
+                uint32_t aph = 0, bph = 0;
+                RdSeq seq;
+                seq.init(prm, resA, cluster_id, n_clusters, total_tiles);
+                for (int i = 0; i < seq.n; ++i) {
+                    uint64_t* tf = ab ? tfull + 4 : tfull;
+                    uint64_t* te = ab ? tfull + 5 : tempty;
+                    const uint32_t dH = dH0 + (ab ? (uint32_t)TN : 0u);
+                    mbar_wait_cluster(te, ((tphb >> ab) & 1u) ^ 1u);
+                    fence_after();
+                    if (resA) {
+                        int p, mt, nt;
+                        seq.get(prm, i, tiles_per_item, p, mt, nt);
+                        const int key = p * prm.tiles_m + mt;
+                        if (key != key_prev) {
+                            if (key_prev >= 0) mma_commit<2>(tfull + 7);   // the old A block is free once its MMAs end
+                            mbar_wait(tfull + 6, aph);
+                            fence_after();
+                            aph ^= 1;
+                            key_prev = key;
+                        }
+                    }
+                    for (int kb = 0; kb < prm.n_kb; ++kb) {
+                        uint64_t ah, bh;
+                        if (resA) {
+                            mbar_wait(tfull + 8 + sb, bph);
+                            fence_after();
+                            ah = sdesc(smem_u32(stages + kb * IG::A_BYTES));
+                            bh = sdesc(smem_u32(bring + sb * IG::B_BYTES));
+                        } else {
+                            mbar_wait(tfull + 6 + sb, bph);
+                            fence_after();
+                            const uint32_t s0 = smem_u32(stages + sb * (IG::A_BYTES + IG::B_BYTES));
+                            ah = sdesc(s0);
+                            bh = sdesc(s0 + IG::A_BYTES);
+                        }
+#pragma unroll
+                        for (int k = 0; k < 4; ++k)
+                            mma_i8(dH, ah + (uint64_t)(k * 2), bh + (uint64_t)(k * 2), id, (kb != 0 || k != 0) ? 1u : 0u);
+                        if (resA) {
+                            mma_commit<2>(tfull + 8 + kRdSlots + sb);
+                            if (++sb == nsb) { sb = 0; bph ^= 1; }
+                        } else {
+                            mma_commit<2>(tfull + 6 + 2 * STAGES + sb);
+                            if (++sb == 2 * STAGES) { sb = 0; bph ^= 1; }
+                        }
+                    }
+                    mma_commit<2>(tf);
+                    tphb ^= 1u << ab;
+                    ab ^= 1;
+                }
+            }
+            for (int t = cluster_id; t < total_tiles && prm.mode != 1; t += n_clusters) {
                 // one accumulation (and one epilogue hand-off) per phase; nph = 1: the whole K
                 for (int ph = 0; ph < prm.nph; ++ph) {
                     uint64_t* tf = ab ? tfull + 4 : tfull;
@@ -536,23 +680,6 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
                     mbar_wait_cluster(te, ((tphb >> ab) & 1u) ^ 1u);
                     fence_after();
                     const int kb0 = ph ? prm.kb_end[ph - 1] : 0, kb1 = prm.kb_end[ph];
-                    if (prm.mode == 1) {
-                        for (int kb = kb0; kb < kb1; ++kb) {
-                            mbar_wait(tfull + 6 + slot1, ph1);
-                            fence_after();
-                            const uint32_t s0 = smem_u32(stages + slot1 * (IG::A_BYTES + IG::B_BYTES));
-                            const uint64_t ah = sdesc(s0), bh = sdesc(s0 + IG::A_BYTES);
-#pragma unroll
-                            for (int k = 0; k < 4; ++k)
-                                mma_i8(dH, ah + (uint64_t)(k * 2), bh + (uint64_t)(k * 2), id, (kb != kb0 || k != 0) ? 1u : 0u);
-                            mma_commit<2>(tfull + 6 + 2 * STAGES + slot1);
-                            if (++slot1 == 2 * STAGES) { slot1 = 0; ph1 ^= 1; }
-                        }
-                        mma_commit<2>(tf);
-                        tphb ^= 1u << ab;
-                        ab ^= 1;
-                        continue;
-                    }
                     for (int kb = kb0; kb < kb1; ++kb) {
                         mbar_wait(&full[stage], phase);
                         fence_after();
@@ -868,12 +995,13 @@ cudaError_t launch_gram_i8(const I8Args& a, cudaStream_t st) {
     // B columns per tile: 192 when that pads the B panel less than 256 (e.g. 550 -> 576 instead
     // of 768); the mirrored symmetric layout needs square tiles
     int tn = 256;
-    if (a.skip != 1) {
+    if (a.skip != 1 && a.mode != 1) {                         // mode 1: the b-major B layout assumes 256
         const int64_t p256 = (a.rowsB + 255) / 256 * 256, p192 = (a.rowsB + 191) / 192 * 192;
         if (p192 < p256) tn = 192;
     }
     static const char* tne = getenv("CIL_I8_TN");            // diagnostic override (256 / 192)
-    if (tne && a.skip != 1) tn = atoi(tne) == 192 ? 192 : 256;
+    if (tne && a.skip != 1 && a.mode != 1) tn = atoi(tne) == 192 ? 192 : 256;
+    if (a.mode == 1 && (a.rd_nt % 256 || a.rowsB != (int64_t)a.rd_m * a.rd_nt)) return cudaErrorInvalidValue;
     CUtensorMap maps[4];
     if (!make_map_i8(&maps[0], a.hq, rows, a.Kp, tc::A_ROWS) || !make_map_i8(&maps[1], a.lq, rows, a.Kp, tc::A_ROWS) ||
         !make_map_i8(&maps[2], a.hq, rows, a.Kp, tn / 2) || !make_map_i8(&maps[3], a.lq, rows, a.Kp, tn / 2))

@@ -169,8 +169,9 @@ cudaError_t launch_resample(int P, const uint8_t* bins, int64_t N, int64_t Nt, i
 // ---------------------------------------------------------------- tensor-core resample
 // The same multiplicity form as one integer GEMM per measure (gram_i8.cu, mode 1):
 //   counts[k][v] = sum_b m2_k[b] sum_a m1_k[a] E[v][b][a],   E[v][b][a] = [bins[a][b] > v]
-// A operand: M1 [P][n_rep][Kp] int8 (m1 <= n1 <= 127); B operand: E [P][M][Ntp][Kp] 0/1 bytes
-// (Ntp = N rounded up to 16, zero rows / columns beyond N); M2 [P][n_rep][Ntp] u16.
+// A operand: M1 [P][n_rep][Kp] int8 (m1 <= n1 <= 127); B operand: E [P][Ntp/256][M][256][Kp] 0/1
+// bytes (b-major blocks of 256 columns)
+// (Ntp = N rounded up to 256, zero rows / columns beyond N); M2 [P][n_rep][Ntp] u16.
 
 // multiplicities of replicate k of item p (shared-memory counts, then 16-byte row stores)
 constexpr int kMultThreads = 128;
@@ -185,7 +186,7 @@ __global__ void __launch_bounds__(kMultThreads) k_rd_mult(int64_t N, int64_t Kp,
     uint32_t* m2 = m1 + Kp;          // [Ntp]
     const int k = blockIdx.x, p = blockIdx.y, tid = threadIdx.x;
     const int64_t row = (int64_t)p * n_rep + k;
-    for (int64_t a = tid; a < Kp + Ntp; a += T) m1[a] = 0u;
+    for (int64_t a = tid; a < (Kp + Ntp) / 4; a += T) reinterpret_cast<uint4*>(m1)[a] = make_uint4(0u, 0u, 0u, 0u);
     __syncthreads();
     bool bad = false;
     // the draws of both index sets, U independent loads in flight per thread
@@ -210,24 +211,25 @@ __global__ void __launch_bounds__(kMultThreads) k_rd_mult(int64_t N, int64_t Kp,
     if (__syncthreads_or(bad) && tid == 0) atomicOr(&status[p], CIL_ITEM_BADINDEX);
     // Kp % 128 == 0, Ntp % 64 == 0: 16 int8 / 8 u16 per store
     uint4* d1 = reinterpret_cast<uint4*>(M1 + row * Kp);
+    const uint4* s1 = reinterpret_cast<const uint4*>(m1);
     for (int64_t c = tid; c < Kp / 16; c += T) {
         uint32_t w[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
-            w[i] = m1[16 * c + 4 * i] | m1[16 * c + 4 * i + 1] << 8 | m1[16 * c + 4 * i + 2] << 16 |
-                   m1[16 * c + 4 * i + 3] << 24;
+        for (int i = 0; i < 4; ++i) {
+            const uint4 v = s1[4 * c + i];
+            w[i] = v.x | v.y << 8 | v.z << 16 | v.w << 24;
+        }
         d1[c] = make_uint4(w[0], w[1], w[2], w[3]);
     }
     uint4* d2 = reinterpret_cast<uint4*>(M2 + row * Ntp);
+    const uint4* s2 = reinterpret_cast<const uint4*>(m2);
     for (int64_t c = tid; c < Ntp / 8; c += T) {
-        uint32_t w[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) w[i] = m2[8 * c + 2 * i] | m2[8 * c + 2 * i + 1] << 16;
-        d2[c] = make_uint4(w[0], w[1], w[2], w[3]);
+        const uint4 v0 = s2[2 * c], v1 = s2[2 * c + 1];
+        d2[c] = make_uint4(v0.x | v0.y << 16, v0.z | v0.w << 16, v1.x | v1.y << 16, v1.z | v1.w << 16);
     }
 }
 
-// E[p][v][b][a0 .. a0+127] of measure q from a 128 (a) x 64 (b) block of bins (transposed
+// E rows (v, b) of measure q, columns a0 .. a0+127, from a 128 (a) x 64 (b) block of bins (transposed
 // through shared memory; 8-byte loads along b when the rows allow, 16-byte stores along a)
 __global__ void __launch_bounds__(256) k_rd_build_E(const uint8_t* __restrict__ bins, int64_t N, int nq, int q,
                                                     int M, int64_t Kp, int64_t Ntp, int8_t* __restrict__ E) {
@@ -263,12 +265,14 @@ __global__ void __launch_bounds__(256) k_rd_build_E(const uint8_t* __restrict__ 
         uint8_t v16[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) v16[i] = tile[16 * j + i][bi];
-        int8_t* dst = E + (((int64_t)p * M) * Ntp + b0 + bi) * Kp + a0 + 16 * j;
+        // b-major rows (gram_i8 mode 1): row (bt, v, i) = bt M 256 + v 256 + i for b = 256 bt + i
+        const int64_t b = b0 + bi;
+        int8_t* dst = E + ((int64_t)p * M * Ntp + (b >> 8) * M * 256 + (b & 255)) * Kp + a0 + 16 * j;
         for (int v = 0; v < M; ++v) {
             uint32_t w[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
             for (int i = 0; i < 16; ++i) w[i >> 2] |= (uint32_t)(v16[i] > v) << (8 * (i & 3));
-            __stcs(reinterpret_cast<uint4*>(dst + (int64_t)v * Ntp * Kp), make_uint4(w[0], w[1], w[2], w[3]));
+            __stcs(reinterpret_cast<uint4*>(dst + (int64_t)v * 256 * Kp), make_uint4(w[0], w[1], w[2], w[3]));
         }
     }
 }
@@ -302,7 +306,7 @@ cudaError_t launch_rd_mult(int P, int64_t N, int64_t Kp, int64_t Ntp, int n_rep,
 
 cudaError_t launch_rd_build_E(int P, const uint8_t* bins, int64_t N, int nq, int q, int M, int64_t Kp, int64_t Ntp,
                               int8_t* E, cudaStream_t st) {
-    if (Kp % 128 || Ntp % 64) return cudaErrorInvalidValue;
+    if (Kp % 128 || Ntp % 256) return cudaErrorInvalidValue;
     ProfScope ps_(K_RESAMPLE, st);
     k_rd_build_E<<<dim3((unsigned)(Kp / 128), (unsigned)(Ntp / 64), (unsigned)P), 256, 0, st>>>(bins, N, nq, q, M,
                                                                                                 Kp, Ntp, E);
