@@ -178,7 +178,12 @@ def test_mcil_boot_stats(cil, oracle_mod):
 
 
 @pytest.mark.parametrize("N_syn,N_set,n_rep,M,mask", [(300, 40, 150, 13, 0b000011), (257, 127, 9, 5, 0b000001),
-                                                      (1000, 50, 300, 13, 0b000001)])
+                                                      (1000, 50, 300, 13, 0b000001),
+                                                      # K = 1700: the A row block does not fit in shared
+                                                      # memory -> the streaming ring of the GEMM
+                                                      (1700, 60, 40, 6, 0b000001),
+                                                      # n1 = 128 > 127: the shared-atomic fallback
+                                                      (300, 128, 20, 7, 0b000001)])
 def test_synth_boot_tc_resample_bit_exact(cil, oracle_mod, N_syn, N_set, n_rep, M, mask):
     """The tensor-core resample inside Alg. A2 (one integer GEMM per measure: replicate row
     multiplicities x 0/1 threshold rows, then the column multiplicities in the epilogue) gives
