@@ -801,7 +801,7 @@ bool boot_rd(int32_t N_syn, int32_t N_set, int32_t n_rep, int32_t P, int nq, int
     const int64_t ntp = ((int64_t)N_syn + 255) / 256 * 256;   // gram_i8 mode 1: b-blocks of 256
     if ((int64_t)P * (n_rep + (int64_t)M * ntp) >= (1ll << 31)) return false;
     const int64_t kp = ((int64_t)N_syn + kTcBK - 1) / kTcBK * kTcBK;
-    return 4 * (kp + ntp) <= 200 * 1024 && nq >= 1;
+    return 2 * (kp + ntp) * 4 <= 200 * 1024 && nq >= 1;     // k_rd_mult: 4 warps x (kp + ntp) u16
 }
 bool boot_layout(int32_t P, int32_t N_syn, int32_t N_set, int32_t n_rep, const cil_grid& g, uint32_t mask,
                  int32_t M, cil_engine engine, BootLayout* B) {

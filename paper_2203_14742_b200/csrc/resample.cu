@@ -174,59 +174,58 @@ cudaError_t launch_resample(int P, const uint8_t* bins, int64_t N, int64_t Nt, i
 // (Ntp = N rounded up to 256, zero rows / columns beyond N); M2 [P][n_rep][Ntp] u16.
 
 // multiplicities of replicate k of item p (shared-memory counts, then 16-byte row stores)
-constexpr int kMultThreads = 128;
-__global__ void __launch_bounds__(kMultThreads) k_rd_mult(int64_t N, int64_t Kp, int64_t Ntp, int n_rep,
-                                                          const int32_t* __restrict__ I1, int64_t n1,
-                                                          const int32_t* __restrict__ I2, int64_t n2,
-                                                          int8_t* __restrict__ M1, uint16_t* __restrict__ M2,
-                                                          int32_t* __restrict__ status) {
-    constexpr int T = kMultThreads, U = 8;
+// One warp per replicate (4 per CTA): the multiplicities are u16 halves of shared 32-bit words
+// (atomicAdd of 1 << 16 (idx & 1): m1 <= n1 <= 127, m2 <= n2 <= 65535, host-checked), so the
+// M2 row is a straight copy of the words and no CTA-wide barrier is needed.
+constexpr int kMultWarps = 4;
+__global__ void __launch_bounds__(32 * kMultWarps) k_rd_mult(int64_t N, int64_t Kp, int64_t Ntp, int n_rep,
+                                                             const int32_t* __restrict__ I1, int64_t n1,
+                                                             const int32_t* __restrict__ I2, int64_t n2,
+                                                             int8_t* __restrict__ M1, uint16_t* __restrict__ M2,
+                                                             int32_t* __restrict__ status) {
+    constexpr int U = 8;
     extern __shared__ uint32_t mm_smem[];
-    uint32_t* m1 = mm_smem;          // [Kp]
-    uint32_t* m2 = m1 + Kp;          // [Ntp]
-    const int k = blockIdx.x, p = blockIdx.y, tid = threadIdx.x;
-    const int64_t row = (int64_t)p * n_rep + k;
-    for (int64_t a = tid; a < (Kp + Ntp) / 4; a += T) reinterpret_cast<uint4*>(m1)[a] = make_uint4(0u, 0u, 0u, 0u);
-    __syncthreads();
+    const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+    const int k = blockIdx.x * kMultWarps + wq, p = blockIdx.y;
+    if (k >= n_rep) return;                                   // whole warps only
+    const int64_t words = (Kp + Ntp) / 2;
+    uint32_t* m1 = mm_smem + wq * words;                      // [Kp / 2] u16 pairs
+    uint32_t* m2 = m1 + Kp / 2;                               // [Ntp / 2]
+    for (int64_t a = lane; a < words / 4; a += 32) reinterpret_cast<uint4*>(m1)[a] = make_uint4(0u, 0u, 0u, 0u);
+    __syncwarp();
     bool bad = false;
-    // the draws of both index sets, U independent loads in flight per thread
+    const int64_t row = (int64_t)p * n_rep + k;
     const int32_t* i1 = I1 + row * n1;
     const int32_t* i2 = I2 + row * n2;
     const int64_t n12 = n1 + n2;
-    for (int64_t base = 0; base < n12; base += (int64_t)T * U) {
+    for (int64_t base = 0; base < n12; base += 32 * U) {
         int32_t r[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const int64_t i = base + (int64_t)u * T + tid;
+            const int64_t i = base + u * 32 + lane;
             r[u] = i < n1 ? __ldg(&i1[i]) : i < n12 ? __ldg(&i2[i - n1]) : 0;
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const int64_t i = base + (int64_t)u * T + tid;
+            const int64_t i = base + u * 32 + lane;
             if (i >= n12) break;
-            if (r[u] >= 0 && r[u] < N) atomicAdd(&(i < n1 ? m1 : m2)[r[u]], 1u);
+            if (r[u] >= 0 && r[u] < N) atomicAdd(&(i < n1 ? m1 : m2)[r[u] >> 1], 1u << (16 * (r[u] & 1)));
             else bad = true;
         }
     }
-    if (__syncthreads_or(bad) && tid == 0) atomicOr(&status[p], CIL_ITEM_BADINDEX);
-    // Kp % 128 == 0, Ntp % 64 == 0: 16 int8 / 8 u16 per store
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(&status[p], CIL_ITEM_BADINDEX);
+    __syncwarp();
+    // Kp % 128 == 0, Ntp % 256 == 0: 16 int8 / 8 u16 per 16-byte store
     uint4* d1 = reinterpret_cast<uint4*>(M1 + row * Kp);
     const uint4* s1 = reinterpret_cast<const uint4*>(m1);
-    for (int64_t c = tid; c < Kp / 16; c += T) {
-        uint32_t w[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const uint4 v = s1[4 * c + i];
-            w[i] = v.x | v.y << 8 | v.z << 16 | v.w << 24;
-        }
-        d1[c] = make_uint4(w[0], w[1], w[2], w[3]);
+    for (int64_t c = lane; c < Kp / 16; c += 32) {
+        const uint4 v0 = s1[2 * c], v1 = s1[2 * c + 1];         // 16 u16 counts
+        auto pk = [](uint32_t x, uint32_t y) { return (x & 0xffu) | (x >> 16) << 8 | (y & 0xffu) << 16 | (y >> 16) << 24; };
+        d1[c] = make_uint4(pk(v0.x, v0.y), pk(v0.z, v0.w), pk(v1.x, v1.y), pk(v1.z, v1.w));
     }
     uint4* d2 = reinterpret_cast<uint4*>(M2 + row * Ntp);
     const uint4* s2 = reinterpret_cast<const uint4*>(m2);
-    for (int64_t c = tid; c < Ntp / 8; c += T) {
-        const uint4 v0 = s2[2 * c], v1 = s2[2 * c + 1];
-        d2[c] = make_uint4(v0.x | v0.y << 16, v0.z | v0.w << 16, v1.x | v1.y << 16, v1.z | v1.w << 16);
-    }
+    for (int64_t c = lane; c < Ntp / 8; c += 32) d2[c] = s2[c];
 }
 
 // E rows (v, b) of measure q, columns a0 .. a0+127, from a 128 (a) x 64 (b) block of bins (transposed
@@ -289,8 +288,8 @@ __global__ void k_rd_final(const unsigned long long* __restrict__ cnt, int P, in
 
 cudaError_t launch_rd_mult(int P, int64_t N, int64_t Kp, int64_t Ntp, int n_rep, const int32_t* I1, int64_t n1,
                            const int32_t* I2, int64_t n2, int8_t* M1, uint16_t* M2, int32_t* status, cudaStream_t st) {
-    const size_t smem = sizeof(uint32_t) * (size_t)(Kp + Ntp);
-    if (smem > 200 * 1024) return cudaErrorInvalidValue;
+    const size_t smem = sizeof(uint32_t) * (size_t)(Kp + Ntp) / 2 * kMultWarps;
+    if (smem > 200 * 1024 || Kp % 128 || Ntp % 256) return cudaErrorInvalidValue;
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(k_rd_mult, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -298,8 +297,8 @@ cudaError_t launch_rd_mult(int P, int64_t N, int64_t Kp, int64_t Ntp, int n_rep,
         attr = true;
     }
     ProfScope ps_(K_RESAMPLE, st);
-    k_rd_mult<<<dim3((unsigned)n_rep, (unsigned)P), kMultThreads, smem, st>>>(N, Kp, Ntp, n_rep, I1, n1, I2, n2, M1, M2,
-                                                                      status);
+    k_rd_mult<<<dim3((unsigned)((n_rep + kMultWarps - 1) / kMultWarps), (unsigned)P), 32 * kMultWarps, smem, st>>>(
+        N, Kp, Ntp, n_rep, I1, n1, I2, n2, M1, M2, status);
     note_launch();
     return cudaGetLastError();
 }
