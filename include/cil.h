@@ -7,7 +7,10 @@
  *    buffer; the library never allocates device memory.  Scratch comes from a
  *    caller-provided workspace sized by the matching *_workspace_size() call.
  *  - Calls are asynchronous on `stream` (a cudaStream_t passed as void*; NULL =
- *    legacy default stream).  They never synchronise the device.
+ *    legacy default stream).  They never synchronise the device and never allocate, so a
+ *    call (or a whole step of calls) can be captured into a CUDA graph and replayed on new
+ *    contents of the same buffers (tests/test_gpu_graph.py); the one-time kernel attribute
+ *    setup happens on a call's first (eager) use.
  *  - The return value reports HOST-side validation only: CIL_OK, CIL_EINVAL (bad
  *    argument), CIL_EUNSUPPORTED (a valid request this build does not support),
  *    CIL_ECUDA (a launch failed; cil_last_cuda_error() has the cudaError_t).
