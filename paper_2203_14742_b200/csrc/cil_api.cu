@@ -905,10 +905,11 @@ cil_status cil_synth_loglik_boot(int32_t P, const float* pools, int64_t pool_str
     // steps 4-5: y~ = C(R, s_data, pool rows J[p]) into Y row n_rep
     CIL_CU(launch_check_index(P, J, Nt, N_syn, item_status, st));
     if (B.pb.tc && B.pb.split == 3 && !B.pb.aug && !B.pb.simt_mask && gram_tc_supported()) {
-        // The pool rows are already packed (INT8 planes, centred on the item's pool): bin the
-        // s_data rows against ALL pool rows with those planes (only s_data is packed), then
-        // count with the multiplicities of J:  C(R, s_data, pool[J]) = sum_b #{j : J_j = b} [...]
-        // (the resample kernel with one replicate, identity rows, column draws J).
+        // The pool rows are already packed (INT8 planes, centred on the item's pool): bin ALL
+        // pool rows (A, 4 tiles of 256) against the s_data rows (B, one 64-wide tile) with
+        // those planes (only s_data is packed), then count with the multiplicities of J:
+        // C(R, s_data, pool[J]) = sum_b #{j : J_j = b} [...] (the resample kernel with one
+        // replicate, identity rows, column draws J, on the transposed [s_data][pool] output).
         const int64_t K = (int64_t)g.S * g.H * g.W;
         const Layout& L = B.L;
         float* center = at<float>(wsa, L.off_center);
@@ -923,11 +924,13 @@ cil_status cil_synth_loglik_boot(int32_t P, const float* pools, int64_t pool_str
         CIL_CU(cudaMemsetAsync(ctr, 0, sizeof(uint32_t), st));
         CIL_CU(launch_pack_i8(P, ds, N_set, K, L.Kp, center, hi + a_off * L.Kp, lo + a_off * L.Kp, nrm + a_off,
                               q4 + a_off, item_status, st));
-        SegParams sph{N_set, N_syn, 1, 1};
+        const bool narrow = N_set <= 64;                           // s_data as a 64-wide B tile
+        SegParams sph = narrow ? SegParams{N_syn, N_set, 1, 1} : SegParams{N_set, N_syn, 1, 1};
         I8Args t{};
         t.hq = hi; t.lq = lo; t.nrm = nrm; t.scl = q4;
-        t.rowsA = N_set; t.rowsB = N_syn; t.Kp = L.Kp; t.K = K;
-        t.offs_set = true; t.a_off = a_off; t.b_off = 0;
+        t.rowsA = narrow ? N_syn : N_set; t.rowsB = narrow ? N_set : N_syn; t.Kp = L.Kp; t.K = K;
+        t.offs_set = true; t.a_off = narrow ? 0 : a_off; t.b_off = narrow ? a_off : 0;
+        t.tn_force = narrow ? 64 : 0;
         t.P = P; t.p0 = 0; t.np = P;
         t.thr2 = at<float>(wsa, L.off_thr2); t.thr_stride = 3 * M; t.M = M; t.q_l2 = sl.q_l2; t.nq = sl.nq;
         t.sp = sph; t.hist = at<uint64_t>(wsa, L.off_hist);
@@ -935,19 +938,20 @@ cil_status cil_synth_loglik_boot(int32_t P, const float* pools, int64_t pool_str
         t.kq = 20.0f;                                             // the INT8 bound, as in run_engines
         t.kll = (float)(8.0 * 2.0 * (128.0 * 128.0 / 3.0) * sqrt((double)K));
         t.rel = (float)ldexp(1.0, -21);
-        t.binout = bins;                                          // [P][nq][N_set][N_syn]
+        t.binout = bins;                                          // [P][nq][N_set][N_syn] either way
+        t.bin_t = narrow;                                         // (narrow: the transposed output)
         CIL_CU(launch_gram_i8(t, st));
         BinParams bp{};
         bp.h = grid_h(g);
         bp.w = g.H > 1 ? bp.h * bp.h : bp.h;
         RecheckArgs r{};
-        r.asrc = ds; r.bsrc = ps; r.K = K;
+        r.asrc = narrow ? ps : ds; r.bsrc = narrow ? ds : ps; r.K = K;
         r.thr = at<double>(wsa, L.off_thr); r.thr_stride = (int64_t)sl.nq * M; r.w = bp.w;
         r.M = M; r.nq = sl.nq; r.q_l2 = sl.q_l2;
         r.sp = sph; r.hist = at<uint64_t>(wsa, L.off_hist);
         r.list = at<uint4>(wsa, L.off_list); r.ctr = ctr; r.cap = L.list_cap;
         r.status = item_status; r.P = P;
-        r.binout = bins; r.rowsA = N_set; r.rowsB = N_syn; r.mirror = false;
+        r.binout = bins; r.rowsA = t.rowsA; r.rowsB = t.rowsB; r.mirror = false; r.transpose = narrow;
         for (int a = 0; a < 3; ++a) r.q_tc[a] = -1;
         r.S = g.S; r.H = g.H; r.W = g.W; r.h = bp.h; r.gs = g.gs;
         CIL_CU(launch_recheck(r, st));

@@ -223,6 +223,10 @@ struct I8Args {
     // explicit plane offsets (rows): A rows at a_off + p rowsA, B rows at b_off + p rowsB
     bool offs_set;
     int64_t a_off, b_off;
+    // B columns per tile forced to 64 (a narrow B panel, e.g. the 50 s_data rows of Alg. A2's
+    // y~ against the pool as A; modes 0 without segments / three phases only); 0 = automatic
+    int tn_force;
+    bool bin_t;          // bin-matrix mode: write the transposed matrix [P][nq][rowsB][rowsA] instead
     // mode 1 (row-dot): one-digit operands hq only; counts[p][k][v] = sum_b C[k][v rd_nt + b] m2[p][k][b]
     int mode;
     const uint16_t* m2;
@@ -251,6 +255,7 @@ struct RecheckArgs {
     int P;
     uint8_t* binout;     // non-null: write the exact bin to bins[p][q_l2][i][j] instead of moving counts
     bool mirror;         // symmetric bin matrix: also write [j][i]
+    bool transpose;      // write bins[p][q_l2][j][i] only (matches I8Args.bin_t)
     int64_t rowsA, rowsB;
     // entries of the three-phase engine carry the measure kind in bits 8-15 of .w
     // (0 L2, 1 W12, 2 W12SUM); q_tc = their histogram slots, S/H/W the grid, h the spacing

@@ -59,6 +59,7 @@ struct I8Params {
     int q_tc[3];               // histogram slots of L2, W12, W12SUM (-1: absent)
     float ih;                  // 1/h
     int mode;                  // 0 binning; 1 row-dot (bootstrap replicate counts, see epilogue_rowdot)
+    int bin_t;                 // bin-matrix mode: write binout transposed ([p][q][col][row], stride rowsA)
     const uint16_t* m2;        // mode 1: [P][rowsA][rd_nt] column-draw multiplicities
     int64_t rd_nt;             // mode 1: columns per threshold block (B row = v * rd_nt + b)
     int rd_m;                  // mode 1: thresholds
@@ -777,6 +778,10 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
             uint8_t* binrow = (prm.binout != nullptr && row_ok)
                                   ? prm.binout + (((int64_t)p * prm.nq + prm.q_l2) * prm.rowsA + row) * prm.rowsB
                                   : nullptr;
+            // transposed output: entry (col, row) at stride rowsA (lanes = consecutive rows: coalesced)
+            uint8_t* tbase = (binrow != nullptr && prm.bin_t)
+                                 ? prm.binout + ((int64_t)p * prm.nq + prm.q_l2) * prm.rowsA * prm.rowsB + row
+                                 : nullptr;
             const bool mirror = binrow != nullptr && prm.skip == 1 && mt < nt;
             uint8_t* mbase = mirror ? prm.binout + ((int64_t)p * prm.nq + prm.q_l2) * prm.rowsA * prm.rowsB + row : nullptr;
 
@@ -830,7 +835,11 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
                 if (diag_mode) continue;
                 // phase B: per-thread histogram increments (fire-and-forget shared atomics), or
                 // in bin-matrix mode the 16 provisional bins of the group as bytes
-                if (binrow != nullptr) {
+                if (tbase != nullptr) {
+#pragma unroll
+                    for (int jj = 0; jj < 16; ++jj)
+                        if (g * 16 + jj < nvalid) tbase[(int64_t)(hc0 + g * 16 + jj) * prm.rowsA] = (uint8_t)(bin[jj] & 255);
+                } else if (binrow != nullptr) {
                     uint8_t* dst = binrow + hc0 + g * 16;
                     if (g * 16 + 16 <= nvalid && ((reinterpret_cast<uintptr_t>(dst) & 15u) == 0)) {
                         uint32_t wv[4];
@@ -1002,6 +1011,10 @@ cudaError_t launch_gram_i8(const I8Args& a, cudaStream_t st) {
     static const char* tne = getenv("CIL_I8_TN");            // diagnostic override (256 / 192)
     if (tne && a.skip != 1 && a.mode != 1) tn = atoi(tne) == 192 ? 192 : 256;
     if (a.mode == 1 && (a.rd_nt % 256 || a.rowsB != (int64_t)a.rd_m * a.rd_nt)) return cudaErrorInvalidValue;
+    if (a.tn_force == 64) {
+        if (a.skip != 0 || a.mode != 0 || a.nph == 3) return cudaErrorInvalidValue;
+        tn = 64;
+    }
     CUtensorMap maps[4];
     if (!make_map_i8(&maps[0], a.hq, rows, a.Kp, tc::A_ROWS) || !make_map_i8(&maps[1], a.lq, rows, a.Kp, tc::A_ROWS) ||
         !make_map_i8(&maps[2], a.hq, rows, a.Kp, tn / 2) || !make_map_i8(&maps[3], a.lq, rows, a.Kp, tn / 2))
@@ -1026,6 +1039,8 @@ cudaError_t launch_gram_i8(const I8Args& a, cudaStream_t st) {
     prm.binout = a.binout;
     prm.skip = a.skip;
     prm.mode = a.mode;
+    prm.bin_t = a.bin_t ? 1 : 0;
+    if (a.bin_t && (a.skip != 0 || !a.binout)) return cudaErrorInvalidValue;
     prm.m2 = a.m2; prm.rd_nt = a.rd_nt; prm.rd_m = a.rd_m; prm.rd_out = a.rd_out;
     prm.tiles_act = tc::tiles_active(prm.skip, prm.tiles_m, prm.tiles_n, a.sp.row_seg, a.sp.col_seg, a.rowsB, tn);
     if (prm.tiles_act == 0) return cudaSuccess;
@@ -1050,6 +1065,12 @@ cudaError_t launch_gram_i8(const I8Args& a, cudaStream_t st) {
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     if (a.sm_budget > 0 && a.sm_budget < nsm) nsm = a.sm_budget;
     const bool seg = a.sp.col_seg < a.rowsB;
+    if (tn == 64) {
+        if (seg || prm.nph == 3 || prm.mode != 0) return cudaErrorInvalidValue;
+        if (a.M <= 16) return launch_i8_t<16, false, false, 64>(prm, maps, nsm, st);
+        if (a.M <= 32) return launch_i8_t<32, false, false, 64>(prm, maps, nsm, st);
+        return launch_i8_t<64, false, false, 64>(prm, maps, nsm, st);
+    }
     if (tn == 192) return dispatch_i8<192>(prm, maps, nsm, st, seg, a.M);
     return dispatch_i8<256>(prm, maps, nsm, st, seg, a.M);
 }

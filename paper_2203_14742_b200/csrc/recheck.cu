@@ -112,7 +112,9 @@ __global__ void __launch_bounds__(256) k_recheck(RecheckArgs a) {
             const double* R = a.thr + p * a.thr_stride + (int64_t)ql * a.M;
             int b = 0;
             while (b < a.M && s < R[b] * R[b] / a.w) ++b;
-            if (a.binout) {
+            if (a.binout && a.transpose) {              // [p][q][j][i] (the engine's transposed output)
+                a.binout[(((int64_t)p * a.nq + a.q_l2) * a.rowsB + j) * a.rowsA + i] = (uint8_t)b;
+            } else if (a.binout) {
                 a.binout[(((int64_t)p * a.nq + a.q_l2) * a.rowsA + i) * a.rowsB + j] = (uint8_t)b;
                 if (a.mirror) a.binout[(((int64_t)p * a.nq + a.q_l2) * a.rowsA + j) * a.rowsB + i] = (uint8_t)b;
             } else if (b != b_lo) {

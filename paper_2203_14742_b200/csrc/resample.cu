@@ -53,7 +53,7 @@ __global__ void __launch_bounds__(kRsThreads) k_resample(const uint8_t* __restri
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     // I1 == nullptr: the identity draw (every row a < n1 once; the y~ counts of Alg. A2 step 4)
     const int32_t* i1 = I1 ? I1 + ((int64_t)p * n_rep + k) * n1 : nullptr;
-    const int32_t* i2 = I2 + ((int64_t)p * n_rep + k) * n2;
+    const int32_t* i2 = I2 ? I2 + ((int64_t)p * n_rep + k) * n2 : nullptr;   // nullptr: identity columns
     const int64_t Nt16 = (Nt + 15) & ~(int64_t)15;
     for (int64_t a = tid; a < N; a += kRsThreads) m1[a] = 0u;
     for (int64_t b = tid; b < Nt16; b += kRsThreads) m2[b] = 0u;
@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(kRsThreads) k_resample(const uint8_t* __restri
         else bad = true;
     }
     for (int64_t j = tid; j < n2; j += kRsThreads) {
-        const int32_t c = __ldg(&i2[j]);
+        const int32_t c = i2 ? __ldg(&i2[j]) : (int32_t)j;
         if (c >= 0 && c < Nt) atomicAdd(&m2[c], 1u);
         else bad = true;
     }

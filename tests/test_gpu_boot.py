@@ -211,3 +211,11 @@ def test_synth_boot_tc_resample_bit_exact(cil, oracle_mod, N_syn, N_set, n_rep, 
     torch.cuda.synchronize()
     assert st.tolist() == [0] * P and bst.tolist() == [0] * P and rst.tolist() == [0] * P
     assert torch.equal(Y[:, :n_rep], y)
+    # y~ (Alg. A2 steps 4-5, computed from the pool's planes with the multiplicities of J) equals
+    # the plain features of (s_data, pool[J]) — exact counts on both sides
+    dd = data.to(dev)
+    pj = torch.stack([pd[p][J[p].long()] for p in range(P)])
+    _, yt, tst = cil.features(dd.unsqueeze(0).expand(P, *dd.shape).contiguous(), pj, grid, mask, radii)
+    torch.cuda.synchronize()
+    assert tst.tolist() == [0] * P
+    assert torch.equal(Y[:, n_rep], yt.reshape(P, -1))
