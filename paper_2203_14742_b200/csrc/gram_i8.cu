@@ -12,13 +12,18 @@
 //   E = k_q d sqrt((sigma_a^2 + sigma_b^2)/3) + k_ll sigma_a sigma_b sqrt(K) + rel (n_a + n_b);
 // pairs with a threshold T_m = R_m^2/w inside (d^2 - E, d^2 + E] go to the exact FP64 re-check.
 //
-// Kernel anatomy (persistent CTA pairs, cta_group::2, 256 x 256 tiles, 320 threads):
-//   warp 0      TMA producer (h and l tiles of A and B, 128-byte SWIZZLE_128B rows, 3 stages)
-//   warp 1      TMEM allocator + single-thread MMA issuer (leader CTA): HH -> cols [0,256),
-//               HL, LH -> cols [256,512)
-//   warps 2..9  epilogue: tcgen05.ld of H and X -> FP32 d^2 of 128 pairs per thread in registers
-//               -> branch-free threshold compares, cumulative per-thread counters -> warp REDUX
-//               -> u64 atomics per (row segment, column segment).
+// Kernel anatomy (persistent CTA pairs, cta_group::2, 256 x TN tiles, TN in {256, 192, 64}):
+//   warp 0      TMA producer (h and l tiles of A and B, 128-byte SWIZZLE_128B rows, 2-3 stages)
+//   warp 1      TMEM allocator + single-thread MMA issuer (leader CTA): HH -> cols [0,TN),
+//               HL, LH -> cols [TN,2 TN)
+//   warps 2..15 epilogue (14 warps; 8 for the three-phase AUG engine): tcgen05.ld of H and X ->
+//               FP32 d^2 and its bound E per pair -> binary search over the thresholds ->
+//               per-thread shared histograms [bin][thread] (fire-and-forget ATOMS), flushed per
+//               tile as warp sums -> u64 atomics per (row segment, column segment); or, in
+//               bin-matrix mode, the bins as bytes (row-major, mirrored for a symmetric matrix,
+//               or transposed); ambiguous pairs -> the re-check list.
+//   mode 1      (bootstrap resample, epilogue_rowdot): h planes only, one MMA per k-step, TMEM
+//               double-buffered, A row block resident, weights applied in the epilogue.
 #include <cuda.h>
 #include <stdio.h>
 #include <stdlib.h>
@@ -84,7 +89,8 @@ __host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
 
 template <int MAXM, bool SEG, bool AUG = false, int TN = 256> struct I8Geo {
     // tile = 256 A rows (CTA pair) x TN B columns (TN = 256, or 192 to cut padding of ~550-row
-    // panels); each CTA stages 128 A rows and TN/2 B rows per 128-byte K block
+    // panels, or 64 for a narrow B panel such as Alg. A2's 50 s_data rows); each CTA stages 128
+    // A rows and TN/2 B rows per 128-byte K block
     static constexpr int B_ROWS = TN / 2;
     static constexpr int A_BYTES = A_ROWS * ROW_BYTES;
     static constexpr int B_BYTES = B_ROWS * ROW_BYTES;
