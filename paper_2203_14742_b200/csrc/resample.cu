@@ -4,8 +4,11 @@
 // row draws I1[p][k][i] and column draws I2[p][k][j] (with repetition):
 //   counts[q][m] = #{(i, j) : bins[p][q][I1[i]][I2[j]] > m}           (Eq. (1), strict <:
 //   bins = #{m : d < R_m}, so d < R_m  <=>  bins > m for decreasing radii)
-// One CTA per (k, p); per-thread shared histograms [bin][thread] updated with
-// fire-and-forget shared atomics (no address conflicts), reduced once per measure.
+// k_resample: one CTA per (k, p); per-thread shared histograms [bin][thread] updated with
+// fire-and-forget shared atomics (no address conflicts), reduced once per measure.  The
+// default inside cil_synth_loglik_boot is the tensor-core form at the end of this file
+// (k_rd_mult, k_rd_build_E, gram_i8.cu mode 1, k_rd_final); k_resample serves
+// cil_resample_counts, the fallback, and the one-replicate y~ counts.
 #include "cil_internal.cuh"
 
 namespace cil {
