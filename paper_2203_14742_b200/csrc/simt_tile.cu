@@ -10,7 +10,7 @@
 //   W1inf = max(m_0,m_x,m_y), W1infsum = m_0+m_x+m_y     (readings R1-R4)
 // and bin b = #{m : d < R_m} (strict <) into a per-segment histogram.
 //
-// Tiling: CTA = 128 threads = 32 A-rows x 64 B-rows of pairs, 4x4 pairs per
+// Tiling: CTA = 128 threads = 8 RI A-rows x 64 B-rows of pairs, RI x 4 pairs per (RI = 8 for the max family alone, else 4)
 // thread; k-chunks of 32 floats double-buffered in smem with cp.async (rows
 // padded to 36 floats -> conflict-free LDS.128).
 #include "cil_internal.cuh"
@@ -18,7 +18,7 @@
 namespace cil {
 
 namespace {
-constexpr int TA = 32, TB = 64, BK = kSimtBK, LDS = BK + 4;
+constexpr int TB = 64, BK = kSimtBK, LDS = BK + 4;   // TA = 8 RI rows per CTA (template)
 constexpr int NTHR = 128;
 constexpr int FLUSH = 4;   // chunks between FP32 -> FP64 flushes (128 elements per pair)
 
@@ -39,16 +39,18 @@ __device__ __forceinline__ float absmax3(float m, float x, float y) {
 }
 }  // namespace
 
-template <bool DO_MAX, bool DO_SUM>
-__global__ void __launch_bounds__(NTHR, DO_SUM ? 2 : 4) k_simt(SimtArgs a) {
+template <bool DO_MAX, bool DO_SUM, int RI>
+__global__ void __launch_bounds__(NTHR, (DO_SUM || RI == 8) ? 2 : 4) k_simt(SimtArgs a) {
+    constexpr int TA = 8 * RI;     // A rows per CTA: RI x 4 pairs per thread
+    constexpr int NP = RI * 4;     // pairs per thread
     extern __shared__ __align__(16) unsigned char smem_raw[];
     float* As = reinterpret_cast<float*>(smem_raw);                 // [2][TA][LDS]
     float* Bs = As + 2 * TA * LDS;                                   // [2][TB][LDS]
     double* thr_s = reinterpret_cast<double*>(Bs + 2 * TB * LDS);    // [nq*M]
     // per-thread region results for regions 0 and 1 (region 2 stays in registers)
-    double* rs_sum = thr_s + kMaxMeas * kMaxM;                       // [2][16][NTHR]
-    float* rs_max = reinterpret_cast<float*>(rs_sum + (DO_SUM ? 2 * 16 * NTHR : 0));  // [2][16][NTHR]
-    uint32_t* hist_s = reinterpret_cast<uint32_t*>(rs_max + (DO_MAX ? 2 * 16 * NTHR : 0));
+    double* rs_sum = thr_s + kMaxMeas * kMaxM;                       // [2][NP][NTHR]
+    float* rs_max = reinterpret_cast<float*>(rs_sum + (DO_SUM ? 2 * NP * NTHR : 0));  // [2][NP][NTHR]
+    uint32_t* hist_s = reinterpret_cast<uint32_t*>(rs_max + (DO_MAX ? 2 * NP * NTHR : 0));
 
     const int p = blockIdx.z;
     if (a.status[p] & CIL_ITEM_BADRADII) return;
@@ -82,7 +84,7 @@ __global__ void __launch_bounds__(NTHR, DO_SUM ? 2 : 4) k_simt(SimtArgs a) {
 
     auto load_chunk = [&](int c, int buf) {
         const int64_t k0 = (int64_t)c * BK;
-        // A: 32 rows x 8 x 16B = 256 copies, 2 per thread
+        // A: TA rows x 8 x 16B, TA / 16 copies per thread
 #pragma unroll
         for (int t = 0; t < (TA * BK / 4) / NTHR; ++t) {
             const int idx = tid + t * NTHR;
@@ -102,11 +104,11 @@ __global__ void __launch_bounds__(NTHR, DO_SUM ? 2 : 4) k_simt(SimtArgs a) {
         cp_async_commit();
     };
 
-    float2 acc[4][4];      // FP32 chunk sums (even, odd elements)
-    double tot[4][4];      // FP64 region sums
-    float mx[4][4];        // region maxima
+    float2 acc[RI][4];     // FP32 chunk sums (even, odd elements)
+    double tot[RI][4];     // FP64 region sums
+    float mx[RI][4];       // region maxima
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < RI; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             acc[i][j] = make_float2(0.f, 0.f);
@@ -129,13 +131,13 @@ __global__ void __launch_bounds__(NTHR, DO_SUM ? 2 : 4) k_simt(SimtArgs a) {
         const float* Bb = Bs + buf * TB * LDS;
 #pragma unroll 2
         for (int kk = 0; kk < BK; kk += 4) {
-            float4 av[4], bv[4];
+            float4 av[RI], bv[4];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) av[i] = *reinterpret_cast<const float4*>(Ab + (ty + 8 * i) * LDS + kk);
+            for (int i = 0; i < RI; ++i) av[i] = *reinterpret_cast<const float4*>(Ab + (ty + 8 * i) * LDS + kk);
 #pragma unroll
             for (int j = 0; j < 4; ++j) bv[j] = *reinterpret_cast<const float4*>(Bb + (tx + 16 * j) * LDS + kk);
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
+            for (int i = 0; i < RI; ++i)
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
                     const float2 d0 = sub2(make_float2(av[i].x, av[i].y), make_float2(bv[j].x, bv[j].y));
@@ -155,7 +157,7 @@ __global__ void __launch_bounds__(NTHR, DO_SUM ? 2 : 4) k_simt(SimtArgs a) {
         if (DO_SUM && (++since_flush == FLUSH || region_end)) {
             since_flush = 0;
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
+            for (int i = 0; i < RI; ++i)
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
                     tot[i][j] += (double)acc[i][j].x + (double)acc[i][j].y;
@@ -164,10 +166,10 @@ __global__ void __launch_bounds__(NTHR, DO_SUM ? 2 : 4) k_simt(SimtArgs a) {
         }
         if (region_end && c + 1 < nchunks) {
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
+            for (int i = 0; i < RI; ++i)
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
-                    const int e = (region * 16 + i * 4 + j) * NTHR + tid;
+                    const int e = (region * NP + i * 4 + j) * NTHR + tid;
                     if (DO_SUM) { rs_sum[e] = tot[i][j]; tot[i][j] = 0.0; }
                     if (DO_MAX) { rs_max[e] = mx[i][j]; mx[i][j] = 0.f; }
                 }
@@ -180,7 +182,7 @@ __global__ void __launch_bounds__(NTHR, DO_SUM ? 2 : 4) k_simt(SimtArgs a) {
     const double h = a.bp.h, w = a.bp.w, ih = 1.0 / h, ih2 = 1.0 / (h * h);
     const int nreg = a.g.nreg;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < RI; ++i) {
         const int64_t gi = row0 + ty + 8 * i;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
@@ -191,7 +193,7 @@ __global__ void __launch_bounds__(NTHR, DO_SUM ? 2 : 4) k_simt(SimtArgs a) {
             for (int r = 0; r < 3; ++r) {
                 if (r >= nreg) break;
                 const bool last = (r == nreg - 1);
-                const int e = (r * 16 + i * 4 + j) * NTHR + tid;
+                const int e = (r * NP + i * 4 + j) * NTHR + tid;
                 if (DO_SUM) s[r] = last ? tot[i][j] : rs_sum[e];
                 if (DO_MAX) m[r] = last ? (double)mx[i][j] : (double)rs_max[e];
             }
@@ -247,41 +249,48 @@ __global__ void __launch_bounds__(NTHR, DO_SUM ? 2 : 4) k_simt(SimtArgs a) {
     }
 }
 
-static size_t simt_smem(bool do_max, bool do_sum, int hist_cap) {
-    size_t s = sizeof(float) * 2 * (TA + TB) * LDS + sizeof(double) * kMaxMeas * kMaxM;
-    if (do_sum) s += sizeof(double) * 2 * 16 * NTHR;
-    if (do_max) s += sizeof(float) * 2 * 16 * NTHR;
+static size_t simt_smem(bool do_max, bool do_sum, int ri, int hist_cap) {
+    size_t s = sizeof(float) * 2 * (8 * ri + TB) * LDS + sizeof(double) * kMaxMeas * kMaxM;
+    if (do_sum) s += sizeof(double) * 2 * 4 * ri * NTHR;
+    if (do_max) s += sizeof(float) * 2 * 4 * ri * NTHR;
     s += sizeof(uint32_t) * hist_cap;
     return s;
 }
 
-template <bool X, bool Y>
+template <bool X, bool Y, int RI>
 static cudaError_t launch_simt_t(const SimtArgs& a_in, cudaStream_t st) {
     // shared histogram sized for the segments one tile can touch (else global atomics)
+    constexpr int TA = 8 * RI;
     SimtArgs a = a_in;
     const int64_t nrs = (TA + a.sp.row_seg - 1) / a.sp.row_seg + 1, ncs = (TB + a.sp.col_seg - 1) / a.sp.col_seg + 1;
     const int64_t need = nrs * ncs * a.bp.nq * (a.bp.M + 1);
     a.hist_cap = (int)(need < 4096 ? need : 4096);
-    const size_t sm = simt_smem(X, Y, a.hist_cap);
+    const size_t sm = simt_smem(X, Y, RI, a.hist_cap);
     static bool attr_done = false;   // benign race: idempotent attribute set
     if (!attr_done) {
-        cudaError_t e = cudaFuncSetAttribute(k_simt<X, Y>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)simt_smem(X, Y, 4096));
+        cudaError_t e = cudaFuncSetAttribute(k_simt<X, Y, RI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)simt_smem(X, Y, RI, 4096));
         if (e != cudaSuccess) return e;
         attr_done = true;
     }
     dim3 grid((unsigned)((a.rowsB + TB - 1) / TB), (unsigned)((a.rowsA + TA - 1) / TA), (unsigned)a.P);
     ProfScope ps_(K_SIMT, st);
-    k_simt<X, Y><<<grid, NTHR, sm, st>>>(a);
+    k_simt<X, Y, RI><<<grid, NTHR, sm, st>>>(a);
     note_launch();
     return cudaGetLastError();
 }
 
 cudaError_t launch_simt(const SimtArgs& a, cudaStream_t st) {
     if (a.rowsA == 0 || a.rowsB == 0) return cudaSuccess;
-    if (a.do_max && a.do_sum) return launch_simt_t<true, true>(a, st);
-    if (a.do_max) return launch_simt_t<true, false>(a, st);
-    return launch_simt_t<false, true>(a, st);
+    if (a.do_max && a.do_sum) return launch_simt_t<true, true, 4>(a, st);
+    if (a.do_max) {
+        // max family alone: 8 x 4 pairs per thread (12 LDS.128 per 128 element-pairs instead of
+        // 8 per 64); diagnostic override CIL_SIMT_RI=4
+        static const char* ri = getenv("CIL_SIMT_RI");
+        if (ri && ri[0] == '4') return launch_simt_t<true, false, 4>(a, st);
+        return launch_simt_t<true, false, 8>(a, st);
+    }
+    return launch_simt_t<false, true, 4>(a, st);
 }
 
 }  // namespace cil
