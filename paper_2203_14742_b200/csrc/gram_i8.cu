@@ -74,7 +74,8 @@ struct I8Params {
     int skip;                  // 0 all tiles; 1 symmetric bin matrix (tiles mt > nt skipped, mirrored
                                // by mt < nt); 2 only tiles meeting a block k < l (Alg. 1 triangle)
     int dbg;                   // diagnostic timing knob (CIL_DEBUG_I8): 1 skip binning, 2 skip the epilogue,
-                               // 3 also skip the B loads, 4 all loads
+                               // 3 also skip the B loads, 4 all loads; mode 1: 1 hand-off only,
+                               // 5 no weight loads, 6 streaming ring instead of the resident A
 };
 
 __device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
@@ -383,7 +384,7 @@ struct RdSeq {
 };
 template <typename IG, int STAGES>
 __device__ __forceinline__ bool rd_resident_a(const I8Params& prm, int n_clusters) {
-    return prm.skip == 0 && prm.tiles_m <= n_clusters &&
+    return prm.skip == 0 && prm.tiles_m <= n_clusters && prm.dbg != 6 &&     // dbg 6: streaming ring
            prm.n_kb * IG::A_BYTES + 2 * IG::B_BYTES <= STAGES * IG::STAGE_BYTES;
 }
 
