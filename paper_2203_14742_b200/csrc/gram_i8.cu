@@ -542,8 +542,12 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
                 // stays in shared memory while the cluster's consecutive tiles stream B through a
                 // ring; otherwise the stage memory is a ring of 2 STAGES (A_h | B_h) slots.
                 const bool resA = rd_resident_a<IG, STAGES>(prm, n_clusters);
-                const int nsb = min(kRdSlots, (STAGES * IG::STAGE_BYTES - prm.n_kb * IG::A_BYTES) / IG::B_BYTES);
+                // B slots: the stage memory after the A block, then the epilogue scratch that mode 1
+                // does not use (norm / threshold staging and the histograms after the barriers)
+                const int nsb0 = (STAGES * IG::STAGE_BYTES - prm.n_kb * IG::A_BYTES) / IG::B_BYTES;
+                const int nsb = min(kRdSlots, nsb0 + (IG::FIXED - 2048) / IG::B_BYTES);
                 unsigned char* bring = stages + prm.n_kb * IG::A_BYTES;
+                unsigned char* bextra = stages + STAGES * IG::STAGE_BYTES + 1024 - nsb0 * IG::B_BYTES;
                 int key_prev = -1, sb = 0;
                 uint32_t aph = 0, bph = 0;
                 RdSeq seq;
@@ -566,7 +570,8 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
                         for (int kb = 0; kb < prm.n_kb; ++kb) {
                             mbar_wait(tfull + 8 + kRdSlots + sb, bph ^ 1);
                             if (rank == 0) mbar_expect_tx(tfull + 8 + sb, 2 * IG::B_BYTES);
-                            tma_load_2d<2>(bring + sb * IG::B_BYTES, &mBh, tfull + 8 + sb, kb * 128, yb);
+                            tma_load_2d<2>((sb < nsb0 ? bring : bextra) + sb * IG::B_BYTES, &mBh, tfull + 8 + sb,
+                                           kb * 128, yb);
                             if (++sb == nsb) { sb = 0; bph ^= 1; }
                         }
                     } else {
@@ -625,8 +630,12 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
             uint32_t phase = 0, tphb = 0;
             if (prm.mode == 1) {                            // see the producer
                 const bool resA = rd_resident_a<IG, STAGES>(prm, n_clusters);
-                const int nsb = min(kRdSlots, (STAGES * IG::STAGE_BYTES - prm.n_kb * IG::A_BYTES) / IG::B_BYTES);
+                // B slots: the stage memory after the A block, then the epilogue scratch that mode 1
+                // does not use (norm / threshold staging and the histograms after the barriers)
+                const int nsb0 = (STAGES * IG::STAGE_BYTES - prm.n_kb * IG::A_BYTES) / IG::B_BYTES;
+                const int nsb = min(kRdSlots, nsb0 + (IG::FIXED - 2048) / IG::B_BYTES);
                 unsigned char* bring = stages + prm.n_kb * IG::A_BYTES;
+                unsigned char* bextra = stages + STAGES * IG::STAGE_BYTES + 1024 - nsb0 * IG::B_BYTES;
                 int key_prev = -1, sb = 0;
                 uint32_t aph = 0, bph = 0;
                 RdSeq seq;
@@ -655,7 +664,7 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
                             mbar_wait(tfull + 8 + sb, bph);
                             fence_after();
                             ah = sdesc(smem_u32(stages + kb * IG::A_BYTES));
-                            bh = sdesc(smem_u32(bring + sb * IG::B_BYTES));
+                            bh = sdesc(smem_u32((sb < nsb0 ? bring : bextra) + sb * IG::B_BYTES));
                         } else {
                             mbar_wait(tfull + 6 + sb, bph);
                             fence_after();
