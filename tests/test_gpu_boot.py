@@ -183,7 +183,11 @@ def test_mcil_boot_stats(cil, oracle_mod):
                                                       # memory -> the streaming ring of the GEMM
                                                       (1700, 60, 40, 6, 0b000001),
                                                       # n1 = 128 > 127: the shared-atomic fallback
-                                                      (300, 128, 20, 7, 0b000001)])
+                                                      (300, 128, 20, 7, 0b000001),
+                                                      # y~ edges: one data pattern; the 64-wide s_data
+                                                      # tile full; one row past it (the wide layout)
+                                                      (200, 1, 30, 5, 0b000001), (200, 64, 30, 5, 0b000001),
+                                                      (200, 65, 30, 5, 0b000001)])
 def test_synth_boot_tc_resample_bit_exact(cil, oracle_mod, N_syn, N_set, n_rep, M, mask):
     """The tensor-core resample inside Alg. A2 (one integer GEMM per measure: replicate row
     multiplicities x 0/1 threshold rows, then the column multiplicities in the epilogue) gives
