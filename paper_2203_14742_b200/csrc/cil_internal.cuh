@@ -1,6 +1,7 @@
 // cil_internal.cuh — shared device/host definitions of libcil (CUDA path only).
 // Nothing here is shared with oracle/: the oracle is an independent program.
 #pragma once
+#include <atomic>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <stdint.h>
@@ -8,6 +9,24 @@
 #include "../../include/cil.h"
 
 namespace cil {
+
+// One-time, per-device setting of a kernel's maximum dynamic shared memory (thread-safe;
+// a bit per device, so a process driving several GPUs sets it on each).
+struct SmemAttrOnce {
+    std::atomic<unsigned long long> mask{0ull};
+    template <typename F>
+    cudaError_t ensure(F* fn, int bytes) {
+        int dev = 0;
+        cudaError_t e = cudaGetDevice(&dev);
+        if (e != cudaSuccess) return e;
+        const unsigned long long bit = 1ull << (dev & 63);
+        if (mask.load(std::memory_order_acquire) & bit) return cudaSuccess;
+        e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+        if (e == cudaSuccess) mask.fetch_or(bit, std::memory_order_release);
+        return e;
+    }
+};
+
 
 constexpr int kMaxM = 64;        // radii per measure
 constexpr int kMaxMeas = 6;

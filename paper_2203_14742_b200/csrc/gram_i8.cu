@@ -959,13 +959,8 @@ static bool make_map_i8(CUtensorMap* m, const void* base, int64_t rows, int64_t 
 template <int MAXM, bool SEG, bool AUG = false, int TN = 256>
 static cudaError_t launch_i8_t(const tc::I8Params& prm, const CUtensorMap* maps, int nsm, cudaStream_t st) {
     using IG = tc::I8Geo<MAXM, SEG, AUG, TN>;
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(tc::k_gram_i8<MAXM, SEG, AUG, TN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             IG::SMEM_BYTES);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    static SmemAttrOnce attr;
+    if (cudaError_t e = attr.ensure(tc::k_gram_i8<MAXM, SEG, AUG, TN>, IG::SMEM_BYTES); e != cudaSuccess) return e;
     const int64_t tiles = (int64_t)prm.np * prm.tiles_act;
     const int clusters = (int)(tiles < nsm / 2 ? tiles : nsm / 2);
     cudaLaunchConfig_t cfg{};

@@ -378,13 +378,8 @@ static bool make_map(CUtensorMap* m, const void* base, int split, int64_t rows, 
 template <int MAXM, int CG>
 static cudaError_t launch_t(const tc::TcParams& prm, const CUtensorMap* maps, int nsm, cudaStream_t st) {
     using G = tc::Geo<CG>;
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(tc::k_gram_tc<MAXM, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             G::SMEM_BYTES);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    static SmemAttrOnce attr;
+    if (cudaError_t e = attr.ensure(tc::k_gram_tc<MAXM, CG>, G::SMEM_BYTES); e != cudaSuccess) return e;
     const int64_t tiles = (int64_t)prm.np * prm.tiles_m * prm.tiles_n;
     const int clusters = (int)(tiles < nsm / CG ? tiles : nsm / CG);   // nsm = SM budget of this launch
     cudaLaunchConfig_t cfg{};

@@ -155,12 +155,8 @@ cudaError_t launch_resample(int P, const uint8_t* bins, int64_t N, int64_t Nt, i
     const size_t smem = sizeof(uint32_t) * ((size_t)(M + 1) * kRsThreads + (size_t)((N + 3) & ~3ll) + (size_t)((Nt + 15) & ~15ll) +
                                             (size_t)(n1 < N ? n1 : N));
     if (smem > 200 * 1024) return cudaErrorInvalidValue;     // N + Nt <= ~47 k (host-checked)
-    static bool attr = false;
-    if (!attr) {
-        e = cudaFuncSetAttribute(k_resample, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    static SmemAttrOnce attr;
+    if ((e = attr.ensure(k_resample, 200 * 1024)) != cudaSuccess) return e;
     dim3 grid((unsigned)n_rep, (unsigned)P);
     ProfScope ps_(K_RESAMPLE, st);
     k_resample<<<grid, kRsThreads, smem, st>>>(bins, N, Nt, nq, M, n_rep, I1, n1, I2, n2, counts, y, y_item_stride,
@@ -293,12 +289,8 @@ cudaError_t launch_rd_mult(int P, int64_t N, int64_t Kp, int64_t Ntp, int n_rep,
                            const int32_t* I2, int64_t n2, int8_t* M1, uint16_t* M2, int32_t* status, cudaStream_t st) {
     const size_t smem = sizeof(uint32_t) * (size_t)(Kp + Ntp) / 2 * kMultWarps;
     if (smem > 200 * 1024 || Kp % 128 || Ntp % 256) return cudaErrorInvalidValue;
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_rd_mult, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    static SmemAttrOnce attr;
+    if (cudaError_t e = attr.ensure(k_rd_mult, 200 * 1024); e != cudaSuccess) return e;
     ProfScope ps_(K_RESAMPLE, st);
     k_rd_mult<<<dim3((unsigned)((n_rep + kMultWarps - 1) / kMultWarps), (unsigned)P), 32 * kMultWarps, smem, st>>>(
         N, Kp, Ntp, n_rep, I1, n1, I2, n2, M1, M2, status);

@@ -266,13 +266,8 @@ static cudaError_t launch_simt_t(const SimtArgs& a_in, cudaStream_t st) {
     const int64_t need = nrs * ncs * a.bp.nq * (a.bp.M + 1);
     a.hist_cap = (int)(need < 4096 ? need : 4096);
     const size_t sm = simt_smem(X, Y, RI, a.hist_cap);
-    static bool attr_done = false;   // benign race: idempotent attribute set
-    if (!attr_done) {
-        cudaError_t e = cudaFuncSetAttribute(k_simt<X, Y, RI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)simt_smem(X, Y, RI, 4096));
-        if (e != cudaSuccess) return e;
-        attr_done = true;
-    }
+    static SmemAttrOnce attr;
+    if (cudaError_t e = attr.ensure(k_simt<X, Y, RI>, (int)simt_smem(X, Y, RI, 4096)); e != cudaSuccess) return e;
     dim3 grid((unsigned)((a.rowsB + TB - 1) / TB), (unsigned)((a.rowsA + TA - 1) / TA), (unsigned)a.P);
     ProfScope ps_(K_SIMT, st);
     k_simt<X, Y, RI><<<grid, NTHR, sm, st>>>(a);

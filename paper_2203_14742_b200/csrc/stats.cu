@@ -125,13 +125,8 @@ static cudaError_t launch_stats_strided(int P, const double* Y, int64_t y_stride
     ProfScope ps_(K_TAIL, st);
     const size_t smem = sizeof(double) * (size_t)n * D;
     if (smem <= (size_t)kStatsSmem) {
-        static bool attr = false;
-        if (!attr) {
-            const cudaError_t e =
-                cudaFuncSetAttribute(k_stats_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, kStatsSmem);
-            if (e != cudaSuccess) return e;
-            attr = true;
-        }
+        static SmemAttrOnce attr;
+        if (const cudaError_t e = attr.ensure(k_stats_smem, kStatsSmem); e != cudaSuccess) return e;
         k_stats_smem<<<P, 256, smem, st>>>(Y, y_stride, n, D, mu, Sigma);
         note_launch();
         return cudaGetLastError();
@@ -235,13 +230,10 @@ static cudaError_t launch_loglik_strided(int P, const double* mu, int64_t mu_str
                                          double ridge, double* out, int32_t* status,
                                          const int32_t* status_in, cudaStream_t st) {
     const size_t smem = sizeof(double) * ((size_t)D * (D + 1) / 2 + D);
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_loglik, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)(sizeof(double) * ((size_t)kMaxD * (kMaxD + 1) / 2 + kMaxD)));
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    static SmemAttrOnce attr;
+    if (cudaError_t e = attr.ensure(k_loglik, (int)(sizeof(double) * ((size_t)kMaxD * (kMaxD + 1) / 2 + kMaxD)));
+        e != cudaSuccess)
+        return e;
     ProfScope ps_(K_TAIL, st);
     k_loglik<<<P, kLogThreads, smem, st>>>(mu, mu_stride, Sigma, Sigma_stride, y, y_stride, D, ridge, out,
                                            status, status_in);
