@@ -23,7 +23,8 @@
  *    [S][H][W] ("pattern-major then component-major then row-major");
  *    K = S*H*W, pattern p of a set starts at base + p*ld (ld >= K, in floats).
  *  - Thread-safe: no global mutable state besides a once-per-device kernel
- *    attribute setup.
+ *    attribute setup (atomic), a thread-local launch counter and the opt-in
+ *    profiling diagnostics (cil_prof_*).
  */
 #ifndef CIL_H
 #define CIL_H
