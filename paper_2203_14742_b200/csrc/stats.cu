@@ -83,7 +83,8 @@ __global__ void k_cov(const double* __restrict__ Y, int64_t y_stride, int n, int
 // the same two-pass sums as k_mean / k_cov, with the n-long sums split over the lanes of a
 // warp (one warp per column a, then one warp per pair b <= a) and reduced by shuffles.
 constexpr int kStatsSmem = 200 * 1024;
-__global__ void __launch_bounds__(256) k_stats_smem(const double* __restrict__ Y, int64_t y_stride, int n, int D,
+constexpr int kStatsThreads = 512;
+__global__ void __launch_bounds__(kStatsThreads) k_stats_smem(const double* __restrict__ Y, int64_t y_stride, int n, int D,
                                                     double* __restrict__ mu, double* __restrict__ Sigma) {
     extern __shared__ double ys[];                   // [n][D], centred in place after pass 1
     __shared__ double mus[kMaxD];
@@ -105,7 +106,7 @@ __global__ void __launch_bounds__(256) k_stats_smem(const double* __restrict__ Y
     __syncthreads();
     const int npair = D * (D + 1) / 2;
     for (int t = w; t < npair; t += nw) {
-        int a = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);    // t = a(a+1)/2 + b, b <= a
+        int a = (int)((sqrtf(8.f * t + 1.f) - 1.f) * 0.5f);  // t = a(a+1)/2 + b, b <= a (corrected below)
         while (a * (a + 1) / 2 > t) --a;
         while ((a + 1) * (a + 2) / 2 <= t) ++a;
         const int b = t - a * (a + 1) / 2;
@@ -127,7 +128,7 @@ static cudaError_t launch_stats_strided(int P, const double* Y, int64_t y_stride
     if (smem <= (size_t)kStatsSmem) {
         static SmemAttrOnce attr;
         if (const cudaError_t e = attr.ensure(k_stats_smem, kStatsSmem); e != cudaSuccess) return e;
-        k_stats_smem<<<P, 256, smem, st>>>(Y, y_stride, n, D, mu, Sigma);
+        k_stats_smem<<<P, kStatsThreads, smem, st>>>(Y, y_stride, n, D, mu, Sigma);
         note_launch();
         return cudaGetLastError();
     }
@@ -155,6 +156,7 @@ __global__ void __launch_bounds__(kLogThreads) k_loglik(const double* __restrict
     extern __shared__ double sm[];
     double* L = sm;                                   // D(D+1)/2
     double* z = L + (int64_t)D * (D + 1) / 2;         // D
+    double* rinv = z + D;                             // D: 1 / L_ii
     __shared__ double piv;
     __shared__ int fail;
     const int p = blockIdx.x;
@@ -201,20 +203,28 @@ __global__ void __launch_bounds__(kLogThreads) k_loglik(const double* __restrict
         }
         return;
     }
-    // forward substitution z = L^{-1} r (warp 0), quad = z^T z, logdet = 2 sum ln L_ii
+    // forward substitution z = L^{-1} r (warp 0), quad = z^T z, logdet = 2 sum ln L_ii; the
+    // logarithms and pivot reciprocals are formed in parallel, off the substitution's chain
     if (warp == 0) {
-        double quad = 0.0, logdet = 0.0;
+        double logdet = 0.0;
+        for (int i = lane; i < D; i += 32) {
+            const double lii = L[i * (i + 1) / 2 + i];
+            logdet += 2.0 * log(lii);
+            rinv[i] = 1.0 / lii;
+        }
+        for (int o = 16; o > 0; o >>= 1) logdet += __shfl_xor_sync(0xffffffffu, logdet, o);
+        __syncwarp();
+        double quad = 0.0;
         for (int i = 0; i < D; ++i) {
             const int di = i * (i + 1) / 2;
             double s = 0.0;
             for (int k = lane; k < i; k += 32) s += L[di + k] * z[k];
             for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-            const double zi = (z[i] - s) / L[di + i];
+            const double zi = (z[i] - s) * rinv[i];
             __syncwarp();
             if (lane == 0) z[i] = zi;
             __syncwarp();
             quad += zi * zi;
-            logdet += 2.0 * log(L[di + i]);
         }
         if (lane == 0) {
             out[3 * p + 0] = quad;
@@ -229,9 +239,9 @@ static cudaError_t launch_loglik_strided(int P, const double* mu, int64_t mu_str
                                          int64_t Sigma_stride, const double* y, int64_t y_stride, int D,
                                          double ridge, double* out, int32_t* status,
                                          const int32_t* status_in, cudaStream_t st) {
-    const size_t smem = sizeof(double) * ((size_t)D * (D + 1) / 2 + D);
+    const size_t smem = sizeof(double) * ((size_t)D * (D + 1) / 2 + 2 * D);
     static SmemAttrOnce attr;
-    if (cudaError_t e = attr.ensure(k_loglik, (int)(sizeof(double) * ((size_t)kMaxD * (kMaxD + 1) / 2 + kMaxD)));
+    if (cudaError_t e = attr.ensure(k_loglik, (int)(sizeof(double) * ((size_t)kMaxD * (kMaxD + 1) / 2 + 2 * kMaxD)));
         e != cudaSuccess)
         return e;
     ProfScope ps_(K_TAIL, st);
