@@ -274,10 +274,13 @@ __device__ __forceinline__ void epilogue_aug(const I8Params& prm, uint32_t tmem_
                             v = p0.x + (p1.x + d2) * ih2;
                             e = p0.y + (p1.y + E) * ih2 + v * 2.4e-7f;
                         } else {
-                            // |sqrt(u) - sqrt(d)| <= E / max(sqrt d, sqrt E) for |u - d| <= E
+                            // |u - d| <= E  =>  |sqrt u - sqrt d| = |u - d| / (sqrt u + sqrt d)
+                            //   <= min(sqrt E, E / (sqrt u + sqrt max(u - E, 0)))   (d >= u - E)
                             const float r0 = sqrtf(p0.x), rx = sqrtf(p1.x), ry = sqrtf(d2);
-                            const float e0 = p0.y / fmaxf(r0, sqrtf(p0.y)), ex = p1.y / fmaxf(rx, sqrtf(p1.y)),
-                                        ey = E / fmaxf(ry, sqrtf(E));
+                            auto eb = [](float u, float r, float Eu) {
+                                return fminf(sqrtf(Eu), Eu / fmaxf(r + sqrtf(fmaxf(u - Eu, 0.f)), 1e-30f));
+                            };
+                            const float e0 = eb(p0.x, r0, p0.y), ex = eb(p1.x, rx, p1.y), ey = eb(d2, ry, E);
                             v = r0 + (rx + ry) * ih;
                             e = e0 + (ex + ey) * ih + v * 2.4e-7f;
                         }
