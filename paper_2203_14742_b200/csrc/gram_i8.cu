@@ -802,6 +802,7 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
                                  ? prm.binout + ((int64_t)p * prm.nq + prm.q_l2) * prm.rowsA * prm.rowsB + row
                                  : nullptr;
             const bool mirror = binrow != nullptr && prm.skip == 1 && mt < nt;
+            const bool diag_sym = binrow != nullptr && prm.skip == 1 && mt == nt;
             uint8_t* mbase = mirror ? prm.binout + ((int64_t)p * prm.nq + prm.q_l2) * prm.rowsA * prm.rowsB + row : nullptr;
 
 #pragma unroll 1
@@ -887,6 +888,9 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
 #pragma unroll
                     for (int jj = 0; jj < 16; ++jj) {
                         if (!((amb >> jj) & 1u)) continue;
+                        // symmetric bin matrix, diagonal tile: (i, j) and (j, i) are both here and
+                        // the re-check writes both orders, so list each unordered pair once
+                        if (diag_sym && hc0 + g * 16 + jj < row) continue;
                         const uint32_t idx = atomicAdd(prm.ctr, 1u);
                         if (idx < prm.cap)
                             prm.list[idx] = make_uint4((uint32_t)p, (uint32_t)row, (uint32_t)(hc0 + g * 16 + jj),
