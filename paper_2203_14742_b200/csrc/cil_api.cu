@@ -313,6 +313,7 @@ cil_status run_engines(int P, const RowSrc& asrc, const RowSrc& bsrc, int64_t ro
         a.binout = binout;
         a.range = range;
         a.tri = tile_skip == 2;
+        a.sym = binout != nullptr && same_rows(asrc, bsrc) && rowsA == rowsB;
         CIL_CU(launch_simt(a, st));
     }
     if (pl.tc) {

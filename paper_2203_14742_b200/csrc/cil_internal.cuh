@@ -182,6 +182,8 @@ struct SimtArgs {
     uint8_t* binout;                          // non-null: bins[p][q][i][j] instead of counts
     unsigned long long* range;                // non-null: [P][nq][2] min (d > 0) / max of d as FP64 bits
     bool tri;                                 // skip tiles without a block k < l (Alg. 1 training)
+    bool sym;                                 // bin matrix of a panel against itself: tiles with
+                                              // i > j only are skipped, computed (i, j) also written at (j, i)
     int hist_cap;                             // shared histogram entries (set by the launcher)
 };
 cudaError_t launch_simt(const SimtArgs& a, cudaStream_t st);

@@ -58,6 +58,8 @@ __global__ void __launch_bounds__(NTHR, (DO_SUM || RI == 8) ? 2 : 4) k_simt(Simt
     const int64_t col0 = (int64_t)blockIdx.x * TB;
     // Alg. 1 triangle: a tile without any block k < l has nothing to count
     if (a.tri && row0 / a.sp.row_seg >= (min(col0 + TB, a.rowsB) - 1) / a.sp.col_seg) return;
+    // symmetric bin matrix: the strictly lower tiles come from the mirrored writes
+    if (a.sym && row0 >= col0 + TB) return;
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
     const int ty = (warp >> 1) * 4 + (lane >> 3);   // 0..7
@@ -222,6 +224,9 @@ __global__ void __launch_bounds__(NTHR, (DO_SUM || RI == 8) ? 2 : 4) k_simt(Simt
                 while (b < M && d < T[b]) ++b;
                 if (a.binout) {              // bin-matrix mode (bootstrap, Alg. A1 / A2)
                     a.binout[(((int64_t)p * nq + q) * a.rowsA + gi) * a.rowsB + gj] = (uint8_t)b;
+                    // d(i, j) and d(j, i) are bit-identical here (exact negations, same order), so
+                    // a straddling tile writing both orders writes equal bytes
+                    if (a.sym) a.binout[(((int64_t)p * nq + q) * a.rowsA + gj) * a.rowsB + gi] = (uint8_t)b;
                     continue;
                 }
                 if (b == 0) continue;

@@ -223,3 +223,24 @@ def test_synth_boot_tc_resample_bit_exact(cil, oracle_mod, N_syn, N_set, n_rep, 
     torch.cuda.synchronize()
     assert tst.tolist() == [0] * P
     assert torch.equal(Y[:, n_rep], yt.reshape(P, -1))
+
+
+@pytest.mark.parametrize("engine_name", ["ENGINE_SIMT", "ENGINE_AUTO"])
+def test_bin_matrix_symmetric_skip_equals_full(cil, engine_name):
+    """A panel against itself (the pool x pool bin matrix) computes one triangle and mirrors it;
+    the result equals the full computation on a separate copy of the panel, and is symmetric."""
+    dev = torch.device("cuda")
+    grid = (2, 16, 16, 0.0)
+    P, N, M = 2, 333, 9
+    mask = 0b111111
+    engine = getattr(cil, engine_name)
+    pools = torch.stack([cilgen.make_set(91, p, N, grid[:3]) for p in range(P)]).to(dev)
+    from oracle import oracle as O
+    D = O.distance_matrix(pools[0, :40].cpu().numpy(), pools[0, 40:80].cpu().numpy(), grid, mask)
+    radii = torch.tensor(np.stack([_radii(D, M)] * P), device=dev)
+    b_sym, s1 = cil.bin_matrix(pools, pools, grid, mask, radii, engine=engine)
+    b_full, s2 = cil.bin_matrix(pools, pools.clone(), grid, mask, radii, engine=engine)
+    torch.cuda.synchronize()
+    assert s1.tolist() == [0] * P and s2.tolist() == [0] * P
+    assert torch.equal(b_sym, b_sym.transpose(2, 3))
+    assert torch.equal(b_sym, b_full)
