@@ -137,7 +137,7 @@ bool plan_bins(uint32_t mask, cil_engine engine, const cil_grid& g, Plan* out) {
     if (engine == CIL_ENGINE_TC_3XBF16 || engine == CIL_ENGINE_TC_3XTF32) return false;
     const int64_t K = (int64_t)g.S * g.H * g.W;
     const cil_engine e = (engine == CIL_ENGINE_SIMT || K > 65536) ? CIL_ENGINE_SIMT : CIL_ENGINE_TC_I8;
-    *out = make_plan(mask, e, g, 1ll << 40, 0, 1, /*allow_aug=*/false);
+    *out = make_plan(mask, e, g, 1ll << 40, 0, 1, /*allow_aug=*/true);
     return true;
 }
 
@@ -330,7 +330,6 @@ cil_status run_engines(int P, const RowSrc& asrc, const RowSrc& bsrc, int64_t ro
         int q_tc[3] = {-1, -1, -1};
         if (pl.aug) {
             // ---- three-phase INT8 engine: L2, W12, W12SUM from the Grams of [x~ | D_x x~ | D_y x~]
-            if (binout) return CIL_EUNSUPPORTED;
             for (int q = 0; q < sl.nq; ++q) {
                 if (sl.slot[q] == 0) q_tc[0] = q;
                 if (sl.slot[q] == 3) q_tc[1] = q;
@@ -368,7 +367,9 @@ cil_status run_engines(int P, const RowSrc& asrc, const RowSrc& bsrc, int64_t ro
             t.part = at<float>(ws, L.off_part);
             t.ih = (float)(1.0 / bp.h);
             t.diag = diag;
-            t.skip = b_same ? tile_skip : 0;
+            t.binout = binout;
+            // symmetric bin matrix of one panel against itself: the upper tile triangle, mirrored
+            t.skip = (binout && b_same) ? 1 : (b_same ? tile_skip : 0);
             CIL_CU(launch_gram_i8(t, st));
         } else if (pl.split == 3) {
             // ---- INT8 two-digit engine (default): exact int32 accumulation
@@ -444,7 +445,7 @@ cil_status run_engines(int P, const RowSrc& asrc, const RowSrc& bsrc, int64_t ro
         r.list = list; r.ctr = ctr; r.cap = L.list_cap;
         r.status = status; r.P = P;
         r.binout = binout; r.rowsA = rowsA; r.rowsB = rowsB;
-        r.mirror = binout != nullptr && pl.split == 3 && !pl.aug && same_rows(asrc, bsrc) && rowsA == rowsB;
+        r.mirror = binout != nullptr && pl.split == 3 && same_rows(asrc, bsrc) && rowsA == rowsB;
         for (int a = 0; a < 3; ++a) r.q_tc[a] = q_tc[a];
         r.S = g.S; r.H = g.H; r.W = g.W; r.h = bp.h; r.gs = g.gs;
         CIL_CU(launch_recheck(r, st));

@@ -294,10 +294,18 @@ __device__ __forceinline__ void epilogue_aug(const I8Params& prm, uint32_t tmem_
                         }
                         const float* T = s_T + k * 2 * MAXM;
                         const int b = bin_search<MAXM>(v + e, T);
-                        if (SEG)
+                        if (prm.binout != nullptr) {      // bin-matrix mode (bootstrap), measure q_tc[k]
+                            uint8_t* bm = prm.binout + ((int64_t)p * prm.nq + prm.q_tc[k]) * prm.rowsA * prm.rowsB;
+                            const int64_t col = hc0 + j;
+                            bm[row * prm.rowsB + col] = (uint8_t)b;
+                            if (prm.skip == 1 && mt < nt) bm[col * prm.rowsB + row] = (uint8_t)b;   // mirror
+                            // a diagonal tile of a symmetric matrix lists each unordered pair once
+                            if (prm.skip == 1 && mt == nt && col < row) continue;
+                        } else if (SEG) {
                             atomicAdd(myh + ((k * (MAXM + 1) + b) << 8), 1u << (8 * lcs));
-                        else
+                        } else {
                             atomicAdd(myh + (b << 8), 1u << (8 * k));
+                        }
                         if (v - e < T[b]) {
                             const uint32_t idx = atomicAdd(prm.ctr, 1u);
                             if (idx < prm.cap)
@@ -312,6 +320,7 @@ __device__ __forceinline__ void epilogue_aug(const I8Params& prm, uint32_t tmem_
             if (lane == 0) mbar_arrive_remote(&tempty[0], 0);
             tph ^= 1;
         }
+        if (prm.binout != nullptr) continue;           // bin-matrix mode: no histograms
         // ---- flush the per-thread histograms of the requested kinds
         const int64_t rs = row_ok ? row / prm.sp.row_seg : 0;
         const int64_t rs0 = __shfl_sync(0xffffffffu, rs, 0);

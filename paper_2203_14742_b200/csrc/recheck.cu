@@ -68,7 +68,10 @@ __global__ void __launch_bounds__(256) k_recheck(RecheckArgs a) {
                 const double* R = a.thr + p * a.thr_stride + (int64_t)q * a.M;
                 int b = 0;
                 while (b < a.M && d < R[b]) ++b;
-                if (b != b_lo) {
+                if (a.binout) {                          // bin-matrix mode: the exact bin, both orders
+                    a.binout[(((int64_t)p * a.nq + q) * a.rowsA + i) * a.rowsB + j] = (uint8_t)b;
+                    if (a.mirror) a.binout[(((int64_t)p * a.nq + q) * a.rowsA + j) * a.rowsB + i] = (uint8_t)b;
+                } else if (b != b_lo) {
                     const int64_t rs = i / a.sp.row_seg, cs = j / a.sp.col_seg;
                     unsigned long long* Hh = (unsigned long long*)a.hist;
                     if (b_lo > 0) atomicAdd(&Hh[hist_index(a.sp, a.nq, a.M, p, rs, cs, q, b_lo)], ~0ull);
@@ -113,10 +116,10 @@ __global__ void __launch_bounds__(256) k_recheck(RecheckArgs a) {
             int b = 0;
             while (b < a.M && s < R[b] * R[b] / a.w) ++b;
             if (a.binout && a.transpose) {              // [p][q][j][i] (the engine's transposed output)
-                a.binout[(((int64_t)p * a.nq + a.q_l2) * a.rowsB + j) * a.rowsA + i] = (uint8_t)b;
+                a.binout[(((int64_t)p * a.nq + ql) * a.rowsB + j) * a.rowsA + i] = (uint8_t)b;
             } else if (a.binout) {
-                a.binout[(((int64_t)p * a.nq + a.q_l2) * a.rowsA + i) * a.rowsB + j] = (uint8_t)b;
-                if (a.mirror) a.binout[(((int64_t)p * a.nq + a.q_l2) * a.rowsA + j) * a.rowsB + i] = (uint8_t)b;
+                a.binout[(((int64_t)p * a.nq + ql) * a.rowsA + i) * a.rowsB + j] = (uint8_t)b;
+                if (a.mirror) a.binout[(((int64_t)p * a.nq + ql) * a.rowsA + j) * a.rowsB + i] = (uint8_t)b;
             } else if (b != b_lo) {
                 const int64_t rs = i / a.sp.row_seg, cs = j / a.sp.col_seg;
                 unsigned long long* H = (unsigned long long*)a.hist;

@@ -113,7 +113,7 @@ def test_resample_bad_index(cil):
     assert st.tolist() == [0, cil.ITEM_BADINDEX]
 
 
-@pytest.mark.parametrize("mask", [0b000001, 0b000011])
+@pytest.mark.parametrize("mask", [0b000001, 0b000011, 0b001101])   # 0b001101: the three-phase bins
 def test_synth_boot_vs_oracle(cil, oracle_mod, mask):
     """Alg. A2 end to end (bins, resampling, mu/Sigma, y~, loglik) for 3 proposals."""
     O = oracle_mod
@@ -178,6 +178,7 @@ def test_mcil_boot_stats(cil, oracle_mod):
 
 
 @pytest.mark.parametrize("N_syn,N_set,n_rep,M,mask", [(300, 40, 150, 13, 0b000011), (257, 127, 9, 5, 0b000001),
+                                                      (300, 40, 100, 9, 0b001101),
                                                       (1000, 50, 300, 13, 0b000001),
                                                       # K = 1700: the A row block does not fit in shared
                                                       # memory -> the streaming ring of the GEMM
