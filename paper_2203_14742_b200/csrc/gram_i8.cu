@@ -821,28 +821,38 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
                 tmem_ld16(tl + g * 16, hv);
                 tmem_ld16(tl + TN + g * 16, xv);
                 if (prm.dbg == 1 || !row_ok) continue;
-                // phase A (loads + ALU only, so the compiler overlaps the 16 pairs' search chains):
-                // bin b_j = #{m : hi_j < T_m} and the ambiguity bit of every pair of the group
+                // (d^2, E) of pair jj of the group
+                auto d2_E = [&](int jj, float& d2, float& E) {
+                    const int jc = g0 * 16 + g * 16 + jj;
+                    const float sb = s_sb[jc], nb = s_nb[jc];
+                    // 65536 H + 256 X in FP32 (relative rounding 2^-24 of g, inside rel): measured
+                    // identical to an FP64 combination on generator data
+                    const float gi = fmaf((float)(int)hv[jj], 65536.f, (float)(int)xv[jj] * 256.f);
+                    d2 = fmaf(m2sa * sb, gi, na + nb);
+                    const float dd = fmaxf(d2, 1e-30f);
+                    E = fmaf(kq_sa * sqrt_approx(dd), fmaxf(sa, sb), fmaf(kll_sa, sb, reln * (na + nb)));
+                };
+                if (diag_mode) {                            // diagnostics: (d^2, E) of every pair, no binning
+#pragma unroll
+                    for (int jj = 0; jj < 16; ++jj) {
+                        float d2, E;
+                        d2_E(jj, d2, E);
+                        if (g * 16 + jj < nvalid) {
+                            diag_row[2 * (hc0 + g * 16 + jj)] = d2;
+                            diag_row[2 * (hc0 + g * 16 + jj) + 1] = E;
+                        }
+                    }
+                    continue;
+                }
+                // phase A (loads + ALU only, branch-free, so the compiler overlaps the 16 pairs' search
+                // chains): bin b_j = #{m : hi_j < T_m} and the ambiguity bit of every pair of the group
                 int bin[16];                                // b | (local column segment << 8)
                 uint32_t amb = 0;
 #pragma unroll
                 for (int jj = 0; jj < 16; ++jj) {
                     const int j = g * 16 + jj;
-                    const int jc = g0 * 16 + j;
-                    const float sb = s_sb[jc], nb = s_nb[jc];
-                    // 65536 H + 256 X in FP32 (relative rounding 2^-24 of g, inside rel): measured
-                    // identical to an FP64 combination on generator data
-                    const float gi = fmaf((float)(int)hv[jj], 65536.f, (float)(int)xv[jj] * 256.f);
-                    const float d2 = fmaf(m2sa * sb, gi, na + nb);
-                    const float dd = fmaxf(d2, 1e-30f);
-                    const float E = fmaf(kq_sa * sqrt_approx(dd), fmaxf(sa, sb), fmaf(kll_sa, sb, reln * (na + nb)));
-                    if (diag_mode) {
-                        if (j < nvalid) {
-                            diag_row[2 * (hc0 + j)] = d2;
-                            diag_row[2 * (hc0 + j) + 1] = E;
-                        }
-                        continue;
-                    }
+                    float d2, E;
+                    d2_E(jj, d2, E);
                     const float hi = d2 + E, lo = d2 - E;
                     // binary search over the decreasing thresholds (s_T[MAXM..2 MAXM) = -inf):
                     // two levels from registers, the remaining log2(MAXM) - 2 from shared memory
@@ -861,7 +871,6 @@ k_gram_i8(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUten
                     // a threshold in (lo, hi]: provisional bin b, exact re-check
                     amb |= (lo < s_T[b] && j < nvalid) ? (1u << jj) : 0u;
                 }
-                if (diag_mode) continue;
                 // phase B: per-thread histogram increments (fire-and-forget shared atomics), or
                 // in bin-matrix mode the 16 provisional bins of the group as bytes
                 if (tbase != nullptr) {

@@ -378,23 +378,34 @@ cudaError_t launch_pack_i8(int P, const RowSrc& src, int64_t rows, int64_t K, in
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    auto pf = [&](int nt) {
-        int per_sm = 0;                                          // resident CTAs per SM
-        switch (nt) {
-            case 256: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pack_i8r<8, 256>, 256, 0); break;
-            case 512: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pack_i8r<8, 512>, 512, 0); break;
-            default: per_sm = 2048 / nt;
-        }
+    // prefetch distance in CTAs for a kernel's resident CTAs per SM
+    auto pf = [&](const void* fn, int nt) {
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, nt, 0);
         return (int64_t)pf_x8 * nsm * (per_sm > 0 ? per_sm : 1) / 8;
     };
+    // diagnostic override of the row-kernel shape for 8192 < Kp <= 16384 (CIL_PACK_VAR:
+    // 1 = 16 float4 x 256 threads, 2 = 4 float4 x 1024 threads, 3 = the two-pass kernel)
+    static const char* pve = getenv("CIL_PACK_VAR");
+    const int pvar = pve ? atoi(pve) : 0;
     if (Kp <= 4096)
-        k_pack_i8r<4, 256><<<grid, 256, 0, st>>>(src, rows, K, Kp, center, hq, lq, nrm, scl, status, pf(256));
+        k_pack_i8r<4, 256><<<grid, 256, 0, st>>>(src, rows, K, Kp, center, hq, lq, nrm, scl, status,
+                                                 pf((const void*)k_pack_i8r<4, 256>, 256));
     else if (Kp <= 8192)
-        k_pack_i8r<8, 256><<<grid, 256, 0, st>>>(src, rows, K, Kp, center, hq, lq, nrm, scl, status, pf(256));
-    else if (Kp <= 16384)
-        k_pack_i8r<8, 512><<<grid, 512, 0, st>>>(src, rows, K, Kp, center, hq, lq, nrm, scl, status, pf(512));
-    else if (Kp <= 32768)
-        k_pack_i8r<8, 1024><<<grid, 1024, 0, st>>>(src, rows, K, Kp, center, hq, lq, nrm, scl, status, pf(1024));
+        k_pack_i8r<8, 256><<<grid, 256, 0, st>>>(src, rows, K, Kp, center, hq, lq, nrm, scl, status,
+                                                 pf((const void*)k_pack_i8r<8, 256>, 256));
+    else if (Kp <= 16384 && pvar == 1)
+        k_pack_i8r<16, 256><<<grid, 256, 0, st>>>(src, rows, K, Kp, center, hq, lq, nrm, scl, status,
+                                                  pf((const void*)k_pack_i8r<16, 256>, 256));
+    else if (Kp <= 16384 && pvar == 2)
+        k_pack_i8r<4, 1024><<<grid, 1024, 0, st>>>(src, rows, K, Kp, center, hq, lq, nrm, scl, status,
+                                                   pf((const void*)k_pack_i8r<4, 1024>, 1024));
+    else if (Kp <= 16384 && pvar != 3)
+        k_pack_i8r<8, 512><<<grid, 512, 0, st>>>(src, rows, K, Kp, center, hq, lq, nrm, scl, status,
+                                                 pf((const void*)k_pack_i8r<8, 512>, 512));
+    else if (Kp <= 32768 && pvar != 3)
+        k_pack_i8r<8, 1024><<<grid, 1024, 0, st>>>(src, rows, K, Kp, center, hq, lq, nrm, scl, status,
+                                                   pf((const void*)k_pack_i8r<8, 1024>, 1024));
     else
         k_pack_i8<<<grid, 256, 0, st>>>(src, rows, K, Kp, center, hq, lq, nrm, scl, status);
     note_launch();
