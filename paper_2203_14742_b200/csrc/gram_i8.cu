@@ -1037,12 +1037,25 @@ cudaError_t launch_gram_i8(const I8Args& a, cudaStream_t st) {
         rows = std::max(a.a_off + (int64_t)a.P * a.rowsA, a.b_off + (int64_t)a.P * a.rowsB);
     }
     if (rows >= (1ll << 31) || (a.b_same && a.rowsA != a.rowsB)) return cudaErrorInvalidValue;
-    // B columns per tile: 192 when that pads the B panel less than 256 (e.g. 550 -> 576 instead
-    // of 768); the mirrored symmetric layout needs square tiles
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (a.sm_budget > 0 && a.sm_budget < nsm) nsm = a.sm_budget;
+    // B columns per tile: 192 when that costs fewer column-waves of the persistent grid than 256
+    // (waves = ceil(tiles / CTA pairs); a 192-column tile is charged 5 % extra for its A feed):
+    // less padding (a 550-row panel: 576 instead of 768 columns) or a better last wave (C7's 75
+    // k < l tiles on 74 CTA pairs: 100 tiles of 192).  The mirrored symmetric layout needs square
+    // tiles, mode 1's b-major B layout assumes 256.
     int tn = 256;
-    if (a.skip != 1 && a.mode != 1) {                         // mode 1: the b-major B layout assumes 256
-        const int64_t p256 = (a.rowsB + 255) / 256 * 256, p192 = (a.rowsB + 191) / 192 * 192;
-        if (p192 < p256) tn = 192;
+    if (a.skip != 1 && a.mode != 1) {
+        const int64_t np = a.np > 0 ? a.np : a.P - a.p0;
+        const int64_t tm = (a.rowsA + tc::Geo<2>::TILE_M - 1) / tc::Geo<2>::TILE_M;
+        auto waves = [&](int t) {
+            const int64_t tiles = np * tc::tiles_active(a.skip, (int)tm, (int)((a.rowsB + t - 1) / t), a.sp.row_seg,
+                                                        a.sp.col_seg, a.rowsB, t);
+            return (tiles + nsm / 2 - 1) / (nsm / 2);
+        };
+        if ((double)waves(192) * 192 * 1.05 < (double)waves(256) * 256) tn = 192;
     }
     static const char* tne = getenv("CIL_I8_TN");            // diagnostic override (256 / 192)
     if (tne && a.skip != 1 && a.mode != 1) tn = atoi(tne) == 192 ? 192 : 256;
@@ -1096,10 +1109,6 @@ cudaError_t launch_gram_i8(const I8Args& a, cudaStream_t st) {
         static const char* pfe = getenv("CIL_I8_PF");
         prm.pf = pfe ? atoi(pfe) : 0;
     }
-    int dev = 0, nsm = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    if (a.sm_budget > 0 && a.sm_budget < nsm) nsm = a.sm_budget;
     const bool seg = a.sp.col_seg < a.rowsB;
     if (tn == 64) {
         if (seg || prm.nph == 3 || prm.mode != 0) return cudaErrorInvalidValue;
