@@ -39,7 +39,9 @@ __device__ __forceinline__ float absmax3(float m, float x, float y) {
 }
 }  // namespace
 
-template <bool DO_MAX, bool DO_SUM, int RI>
+// SYM (bin matrix of a panel against itself) is a template flag so that the counting kernels'
+// code is not touched by the mirrored writes (as a runtime flag it cost the max family 16 %)
+template <bool DO_MAX, bool DO_SUM, int RI, bool SYM>
 __global__ void __launch_bounds__(NTHR, (DO_SUM || RI == 8) ? 2 : 4) k_simt(SimtArgs a) {
     constexpr int TA = 8 * RI;     // A rows per CTA: RI x 4 pairs per thread
     constexpr int NP = RI * 4;     // pairs per thread
@@ -59,7 +61,7 @@ __global__ void __launch_bounds__(NTHR, (DO_SUM || RI == 8) ? 2 : 4) k_simt(Simt
     // Alg. 1 triangle: a tile without any block k < l has nothing to count
     if (a.tri && row0 / a.sp.row_seg >= (min(col0 + TB, a.rowsB) - 1) / a.sp.col_seg) return;
     // symmetric bin matrix: the strictly lower tiles come from the mirrored writes
-    if (a.sym && row0 >= col0 + TB) return;
+    if (SYM && row0 >= col0 + TB) return;
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
     const int ty = (warp >> 1) * 4 + (lane >> 3);   // 0..7
@@ -226,7 +228,7 @@ __global__ void __launch_bounds__(NTHR, (DO_SUM || RI == 8) ? 2 : 4) k_simt(Simt
                     a.binout[(((int64_t)p * nq + q) * a.rowsA + gi) * a.rowsB + gj] = (uint8_t)b;
                     // d(i, j) and d(j, i) are bit-identical here (exact negations, same order), so
                     // a straddling tile writing both orders writes equal bytes
-                    if (a.sym) a.binout[(((int64_t)p * nq + q) * a.rowsA + gj) * a.rowsB + gi] = (uint8_t)b;
+                    if (SYM) a.binout[(((int64_t)p * nq + q) * a.rowsA + gj) * a.rowsB + gi] = (uint8_t)b;
                     continue;
                 }
                 if (b == 0) continue;
@@ -262,7 +264,7 @@ static size_t simt_smem(bool do_max, bool do_sum, int ri, int hist_cap) {
     return s;
 }
 
-template <bool X, bool Y, int RI>
+template <bool X, bool Y, int RI, bool SYM>
 static cudaError_t launch_simt_t(const SimtArgs& a_in, cudaStream_t st) {
     // shared histogram sized for the segments one tile can touch (else global atomics)
     constexpr int TA = 8 * RI;
@@ -272,25 +274,30 @@ static cudaError_t launch_simt_t(const SimtArgs& a_in, cudaStream_t st) {
     a.hist_cap = (int)(need < 4096 ? need : 4096);
     const size_t sm = simt_smem(X, Y, RI, a.hist_cap);
     static SmemAttrOnce attr;
-    if (cudaError_t e = attr.ensure(k_simt<X, Y, RI>, (int)simt_smem(X, Y, RI, 4096)); e != cudaSuccess) return e;
+    if (cudaError_t e = attr.ensure(k_simt<X, Y, RI, SYM>, (int)simt_smem(X, Y, RI, 4096)); e != cudaSuccess) return e;
     dim3 grid((unsigned)((a.rowsB + TB - 1) / TB), (unsigned)((a.rowsA + TA - 1) / TA), (unsigned)a.P);
     ProfScope ps_(K_SIMT, st);
-    k_simt<X, Y, RI><<<grid, NTHR, sm, st>>>(a);
+    k_simt<X, Y, RI, SYM><<<grid, NTHR, sm, st>>>(a);
     note_launch();
     return cudaGetLastError();
 }
 
-cudaError_t launch_simt(const SimtArgs& a, cudaStream_t st) {
-    if (a.rowsA == 0 || a.rowsB == 0) return cudaSuccess;
-    if (a.do_max && a.do_sum) return launch_simt_t<true, true, 4>(a, st);
+template <bool SYM>
+static cudaError_t launch_simt_s(const SimtArgs& a, cudaStream_t st) {
+    if (a.do_max && a.do_sum) return launch_simt_t<true, true, 4, SYM>(a, st);
     if (a.do_max) {
         // max family alone: 8 x 4 pairs per thread (12 LDS.128 per 128 element-pairs instead of
         // 8 per 64); diagnostic override CIL_SIMT_RI=4
         static const char* ri = getenv("CIL_SIMT_RI");
-        if (ri && ri[0] == '4') return launch_simt_t<true, false, 4>(a, st);
-        return launch_simt_t<true, false, 8>(a, st);
+        if (ri && ri[0] == '4') return launch_simt_t<true, false, 4, SYM>(a, st);
+        return launch_simt_t<true, false, 8, SYM>(a, st);
     }
-    return launch_simt_t<false, true, 4>(a, st);
+    return launch_simt_t<false, true, 4, SYM>(a, st);
+}
+
+cudaError_t launch_simt(const SimtArgs& a, cudaStream_t st) {
+    if (a.rowsA == 0 || a.rowsB == 0) return cudaSuccess;
+    return a.sym ? launch_simt_s<true>(a, st) : launch_simt_s<false>(a, st);
 }
 
 }  // namespace cil
