@@ -1,0 +1,103 @@
+"""GPU parity on near-duplicate pattern sets ("What's weak" 1).
+
+B = A + eps * N(0, 1) (seeded) puts pairs (i, i) at distances ~eps sqrt(K) while the other
+pairs keep the data's scale; the radii follow the paper's recipe R_0 = max, R_M = the
+minimum distance of any two patterns (readings R5, R16), computed with the
+library's own cil_distance_range + cil_radii_from_range, so thresholds sit right at the
+near-duplicate distances.  Every engine and all six measures (Eqs. (5)-(10))
+must give the oracle's counts (strict <, Eq. (1)) up to the north-star band:
+lo <= gpu <= hi, where lo / hi count the pairs below R (1 -/+ 1e-6).
+
+This is the regime in which an error bound that is only statistical fails: the two rows'
+rounding errors (and low quantisation digits) coincide instead of averaging out.
+"""
+import numpy as np
+import pytest
+import torch
+
+import cilgen
+
+pytestmark = pytest.mark.gpu
+
+BAND = 1e-6
+ENGINES = ["SIMT", "TC_3XBF16", "TC_3XTF32", "TC_I8", "AUTO"]
+GRIDS = {"1d_64x2": (2, 1, 64, 0.0), "64x64x2": (2, 64, 64, 0.0), "128x128": (1, 128, 128, 0.0)}
+ROWS = {"1d_64x2": 48, "64x64x2": 24, "128x128": 16}
+PROFILES = ["GM", "FHN", "scaled"]
+EPS = [0.0, 1e-6, 1e-4, 1e-3, 1e-2]
+
+
+@pytest.fixture(scope="module")
+def cil():
+    if not torch.cuda.is_available():
+        pytest.skip("needs CUDA")
+    import paper_2203_14742_b200 as cil
+    return cil
+
+
+def near_dup_sets(grid, profile, eps, n, seed=20314742):
+    """A: n generator patterns; B: the first n - n//4 rows of A plus eps N(0,1) noise, then
+    n//4 unrelated patterns (so near duplicates and ordinary pairs share each tile)."""
+    prof = "GM" if profile == "scaled" else profile
+    A = cilgen.make_set(seed, 0, n, grid[:3], prof, scaled=(profile == "scaled"))
+    nd = n - n // 4
+    rng = np.random.default_rng(seed + int(eps * 1e9) + 7)
+    noise = rng.standard_normal((nd,) + tuple(A.shape[1:])).astype(np.float64)
+    Bd = (A[:nd].double() + eps * torch.from_numpy(noise)).float()
+    Bo = cilgen.make_set(seed, 1, n // 4, grid[:3], prof, scaled=(profile == "scaled"))
+    return A, torch.cat([Bd, Bo])
+
+
+def _check(gpu, ref, what):
+    ok = np.all(ref["lo"] <= gpu) and np.all(gpu <= ref["hi"])
+    assert ok, (f"{what}\ngpu    {gpu.tolist()}\noracle {ref['counts'].tolist()}\n"
+                f"lo     {ref['lo'].tolist()}\nhi     {ref['hi'].tolist()}")
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("profile", PROFILES)
+@pytest.mark.parametrize("gname", list(GRIDS))
+def test_near_duplicates_all_measures(cil, oracle_mod, engine, profile, gname):
+    O = oracle_mod
+    grid = GRIDS[gname]
+    mask, M = 0x3F, 12
+    dev = torch.device("cuda")
+    for eps in EPS:
+        A, B = near_dup_sets(grid, profile, eps, ROWS[gname])
+        Ad, Bd = A.to(dev), B.to(dev)
+        rng, st0 = cil.distance_range(Ad, Bd, grid, mask)
+        radii, st1 = cil.radii_from_range(rng, M, "power", 1e-3)
+        radii = radii[0]
+        c, _, st = cil.features(Ad, Bd, grid, mask, radii, engine=getattr(cil, "ENGINE_" + engine))
+        torch.cuda.synchronize()
+        assert int(st0[0]) == 0 and int(st1[0]) == 0 and int(st[0]) == 0, (eps, int(st0[0]), int(st1[0]), int(st[0]))
+        ref = O.features(A.numpy(), B.numpy(), grid, mask, radii.cpu().numpy(), band=BAND)
+        _check(c[0].cpu().numpy(), ref, f"{engine} {profile} {gname} eps={eps}")
+
+
+@pytest.mark.parametrize("engine", ["TC_I8", "AUTO", "SIMT"])
+def test_near_duplicates_bin_matrix(cil, oracle_mod, engine):
+    """The bootstrap's bin matrix (Alg. A1 / A2) on near-duplicate pools: every entry equals
+    #{m : d < R_m} of the oracle distance unless d is within 1e-6 of a radius."""
+    O = oracle_mod
+    grid = (2, 32, 32, 0.0)
+    mask, M = 0x3F, 10
+    dev = torch.device("cuda")
+    for eps in (0.0, 1e-6, 1e-3):
+        A, B = near_dup_sets(grid, "FHN", eps, 40)
+        rng, _ = cil.distance_range(A.to(dev), B.to(dev), grid, mask)
+        radii, _ = cil.radii_from_range(rng, M)
+        radii = radii[0]
+        bins, st = cil.bin_matrix(A.to(dev), B.to(dev), grid, mask, radii, engine=getattr(cil, "ENGINE_" + engine))
+        torch.cuda.synchronize()
+        assert int(st[0]) == 0
+        D = O.distance_matrix(A.numpy(), B.numpy(), grid, mask)
+        R = radii.cpu().numpy()
+        for q in range(6):
+            exact = (D[q][..., None] < R[q]).sum(-1)
+            lo = (D[q][..., None] < R[q] * (1 - BAND)).sum(-1)
+            hi = (D[q][..., None] < R[q] * (1 + BAND)).sum(-1)
+            g = bins[0, q].cpu().numpy().astype(np.int64)
+            bad = (g < lo) | (g > hi)
+            assert not bad.any(), (engine, eps, q, np.argwhere(bad)[:5].tolist(), exact[bad][:5].tolist(),
+                                   g[bad][:5].tolist())
