@@ -86,24 +86,21 @@ struct Plan {
     int nreg = 1;
 };
 
-// split: 1 = 3xBF16, 2 = 3xTF32, 3 = two-digit INT8.  AUTO takes INT8 when its exact int32
-// accumulation cannot overflow (K <= 65536) and its per-thread segment histograms fit
-// (column segments of >= 43 columns: a 128-column half meets <= 4), else 3xBF16.
-bool i8_ok(const cil_grid& g, int64_t col_seg, int64_t rowsB) {
-    const int64_t K = (int64_t)g.S * g.H * g.W;
-    return K <= 65536 && (col_seg >= rowsB || col_seg >= 43);
-}
+// split: 1 = 3xBF16, 2 = 3xTF32, 3 = three-digit INT8 (gram3.cu).  The INT8 engine takes any K
+// (exact int32 accumulation in chunks of 65536) and column segments of >= 21 columns (its
+// per-thread byte histograms); otherwise AUTO / TC_I8 run L2 on the CUDA cores, whose bounds are
+// rigorous too.  The float split engines are explicit options only.
+constexpr int64_t kMinSegI8 = 21;
+bool i8_ok(int64_t col_seg, int64_t rowsB) { return col_seg >= rowsB || col_seg >= kMinSegI8; }
 // The L2-type family (L2, W12, W12SUM) on the three-phase INT8 engine when the
-// request has W12 or W12SUM, the engine is AUTO / TC_I8, every block fits the exact int32
-// accumulation and the per-thread histograms fit (column segments: M <= 16).
+// request has W12 or W12SUM, the engine is AUTO / TC_I8, and the per-thread histograms fit
+// (column segments: >= 21 columns and M <= 32).
 bool aug_ok(uint32_t mask, cil_engine engine, const cil_grid& g, int64_t col_seg, int64_t rowsB, int M) {
     if (!(mask & (CIL_W12 | CIL_W12SUM))) return false;
     if (engine != CIL_ENGINE_AUTO && engine != CIL_ENGINE_TC_I8) return false;
     if (g.W < 2) return false;
-    const int64_t K = (int64_t)g.S * g.H * g.W;
-    if (K > 65536) return false;                               // Kx, Ky < K
     const bool seg = col_seg < rowsB;
-    if (seg && (col_seg < 43 || M > 16)) return false;
+    if (seg && (col_seg < kMinSegI8 || M > 32)) return false;
     return M <= 64;
 }
 Plan make_plan(uint32_t mask, cil_engine engine, const cil_grid& g, int64_t col_seg = 1ll << 40,
@@ -119,10 +116,8 @@ Plan make_plan(uint32_t mask, cil_engine engine, const cil_grid& g, int64_t col_
         pl.nreg = (pl.simt_mask & (CIL_W1INF | CIL_W1INFSUM)) ? (g.H > 1 ? 3 : 2) : 1;
         return pl;
     }
-    const bool want_tc = (mask & CIL_L2) && engine != CIL_ENGINE_SIMT;
-    pl.tc = want_tc;
     pl.split = (engine == CIL_ENGINE_TC_3XTF32) ? 2 : (engine == CIL_ENGINE_TC_3XBF16) ? 1 : 3;
-    if (pl.split == 3 && !i8_ok(g, col_seg, rowsB)) pl.split = 1;
+    pl.tc = (mask & CIL_L2) && engine != CIL_ENGINE_SIMT && (pl.split != 3 || i8_ok(col_seg, rowsB));
     pl.simt_mask = pl.tc ? (mask & ~(uint32_t)CIL_L2) : mask;
     pl.do_max = pl.simt_mask & (CIL_LINF | CIL_W1INF | CIL_W1INFSUM);
     pl.do_sum = pl.simt_mask & (CIL_L2 | CIL_W12SUM | CIL_W12);
@@ -131,12 +126,11 @@ Plan make_plan(uint32_t mask, cil_engine engine, const cil_grid& g, int64_t col_
     return pl;
 }
 
-// Bin-matrix mode (bootstrap): L2 on the INT8 engine when its accumulation is exact, else on
-// the CUDA cores; the float split engines have no bin-matrix epilogue.
+// Bin-matrix mode (bootstrap): L2 (and W12 / W12SUM) on the INT8 engine, the rest on the CUDA cores;
+// the float split engines have no bin-matrix epilogue.
 bool plan_bins(uint32_t mask, cil_engine engine, const cil_grid& g, Plan* out) {
     if (engine == CIL_ENGINE_TC_3XBF16 || engine == CIL_ENGINE_TC_3XTF32) return false;
-    const int64_t K = (int64_t)g.S * g.H * g.W;
-    const cil_engine e = (engine == CIL_ENGINE_SIMT || K > 65536) ? CIL_ENGINE_SIMT : CIL_ENGINE_TC_I8;
+    const cil_engine e = engine == CIL_ENGINE_SIMT ? CIL_ENGINE_SIMT : CIL_ENGINE_TC_I8;
     *out = make_plan(mask, e, g, 1ll << 40, 0, 1, /*allow_aug=*/true);
     return true;
 }
@@ -146,7 +140,7 @@ Plan plan_union(const Plan& a, const Plan& b) {
     Plan u = a;
     u.tc = a.tc || b.tc;
     u.aug = a.aug || b.aug;
-    // operand element size: split 2 (tf32) 4 B > split 1 (bf16) 2 B > split 3 (int8) 1 B
+    // operand element size: split 2 (tf32) 4 B > split 1 (bf16) 2 B > split 3 (int8 digits)
     auto esz = [](const Plan& p) { return !p.tc ? 0 : p.split == 2 ? 4 : p.split == 3 ? 1 : 2; };
     u.split = esz(a) >= esz(b) ? a.split : b.split;
     u.simt_mask = a.simt_mask | b.simt_mask;
@@ -159,11 +153,14 @@ Plan plan_union(const Plan& a, const Plan& b) {
 // Workspace carve-up (identical in the size query and in the call).
 struct Layout {
     size_t off_thr, off_thr2, off_hist, off_ctr, off_list, off_center, off_hi, off_lo, off_nrm, off_q4,
-        off_aug, off_Y, off_mu, off_sig, off_part, total;
+        off_aug, off_rowstat, off_Y, off_mu, off_sig, off_part, total;
     int64_t hist_elems = 0;
     uint32_t list_cap = 0;
     int64_t Kp = 0;
     int64_t kp[4] = {0, 0, 0, 0};   // three-phase engine: block starts of the augmented planes, kp[3] = row length
+    int64_t rows_cap = 0;           // rows of the operand planes (A panels then B panels)
+    int64_t Krow = 0;               // bytes per plane row (INT8 engine)
+    int nph = 1;
     AugGeom geom{};
 };
 
@@ -176,38 +173,48 @@ Layout make_layout(int P, int64_t rowsA, int64_t rowsB, const cil_grid& g, int n
     auto take = [&](size_t bytes) { size_t r = o; o = al(o + bytes); return r; };
     const int64_t K = (int64_t)g.S * g.H * g.W;
     L.off_thr = take(sizeof(double) * (size_t)P * nq * M);
-    L.off_thr2 = take(sizeof(float) * (size_t)P * 3 * M);      // [P][kind][M] tensor-core thresholds
+    L.off_thr2 = take(sizeof(float) * (size_t)P * 8 * M);      // [P][8][M] tensor-core thresholds (k_prep)
     L.hist_elems = (int64_t)P * sp.n_rs * sp.n_cs * nq * (M + 1);
     L.off_hist = take(sizeof(uint64_t) * (size_t)L.hist_elems);
     L.off_ctr = take(sizeof(uint32_t) * 2);
     const int64_t rows = (int64_t)P * (rowsA + rowsB);
-    if (pl.tc) {
-        const double pairs = (double)P * rowsA * rowsB;
-        const double cap = fmin(pairs, pairs / 256.0 + 65536.0);
-        L.list_cap = (uint32_t)fmin(cap, 4.0e9);
-        L.Kp = round_up(K, kTcBK);
-        const size_t esz = pl.split == 2 ? 4 : (pl.split == 3 ? 1 : 2);
-        int64_t Krow = L.Kp;
-        if (pl.aug) {
-            const AugGeom ag = make_aug_geom(g.S, g.H, g.W, 3);
-            L.kp[0] = 0;
-            L.kp[1] = L.Kp;
-            L.kp[2] = L.kp[1] + round_up(ag.Kx, kTcBK);
-            L.kp[3] = L.kp[2] + round_up(ag.Ky, kTcBK);
-            Krow = L.kp[3];
-            L.list_cap = (uint32_t)fmin(fmin(pairs, 3.0 * pairs / 256.0 + 65536.0), 4.0e9);
-        }
+    L.rows_cap = rows;
+    if (pl.tc || pl.simt_mask) {
+        // re-check list (16 B per entry): 1/128 of the (pair, measure) cases + 256 k; beyond that the
+        // exact fallback of recheck.cu runs instead (counts stay exact)
+        const double cases = (double)P * rowsA * rowsB * nq;
+        L.list_cap = (uint32_t)fmin(fmin(cases, cases / 128.0 + 262144.0), 1.0e9);
         L.off_list = take(16 * (size_t)L.list_cap);
+    }
+    if (pl.tc) {
+        L.Kp = round_up(K, kTcBK);
         L.off_center = take(sizeof(float) * (size_t)P * L.Kp);
-        L.off_hi = take(esz * (size_t)rows * Krow);
-        L.off_lo = take(esz * (size_t)rows * Krow);
-        L.off_nrm = take(sizeof(float) * (size_t)rows * (pl.aug ? 4 : 1));
-        L.off_q4 = take(sizeof(float) * (size_t)rows * (pl.aug ? 4 : 1));
-        if (pl.aug) L.off_part = take(sizeof(float) * 4 * (size_t)P * rowsA * rowsB);
+        if (pl.split == 3) {
+            L.Krow = L.Kp;
+            if (pl.aug) {
+                const AugGeom ag = make_aug_geom(g.S, g.H, g.W, 3);
+                L.kp[0] = 0;
+                L.kp[1] = L.Kp;
+                L.kp[2] = L.kp[1] + round_up(ag.Kx, kTcBK);
+                L.kp[3] = L.kp[2] + round_up(ag.Ky, kTcBK);
+                L.Krow = L.kp[3];
+                L.nph = 3;
+            }
+            L.off_hi = take((size_t)3 * rows * L.Krow);                       // digit planes h, m, l
+            L.off_nrm = take(sizeof(float) * 8 * (size_t)rows * L.nph);        // per-row metadata
+            if (pl.aug) L.off_part = take(sizeof(float) * 4 * (size_t)P * rowsA * rowsB);
+        } else {
+            const size_t esz = pl.split == 2 ? 4 : 2;
+            L.off_hi = take(esz * (size_t)rows * L.Kp);
+            L.off_lo = take(esz * (size_t)rows * L.Kp);
+            L.off_nrm = take(sizeof(float) * (size_t)rows);
+            L.off_q4 = take(sizeof(float) * (size_t)rows);
+        }
     }
     if (pl.simt_mask) {
         L.geom = make_aug_geom(g.S, g.H, g.W, pl.nreg, g.gs);
         L.off_aug = take(sizeof(float) * (size_t)rows * L.geom.off[3]);
+        L.off_rowstat = take(sizeof(float) * 4 * (size_t)rows);
     }
     if (nY > 0) {
         L.off_Y = take(sizeof(double) * (size_t)nY);
@@ -268,6 +275,36 @@ cil_status check_sets(int32_t P, const float* A, int64_t strideA, int64_t lda, i
     return CIL_OK;
 }
 
+// 1/h (or 1/h^2) as the FP32 neighbours below and above the FP64 value
+void f32_bracket(double v, float* rd, float* ru) {
+    const float f = (float)v;
+    *rd = (double)f <= v ? f : nextafterf(f, -INFINITY);
+    *ru = (double)f >= v ? f : nextafterf(f, INFINITY);
+    *rd = nextafterf(*rd, -INFINITY);       // one more ulp each way for the FP64 rounding of v itself
+    *ru = nextafterf(*ru, INFINITY);
+}
+
+RecheckArgs recheck_args(const RowSrc& asrc, const RowSrc& bsrc, int64_t K, const cil_grid& g, const Slots& sl, int M,
+                         const BinParams& bp, const SegParams& sp, const Layout& L, void* ws, int32_t* status, int P,
+                         uint8_t* binout, int64_t rowsA, int64_t rowsB, uint32_t mask) {
+    RecheckArgs r{};
+    r.asrc = asrc; r.bsrc = bsrc; r.K = K;
+    r.thr = at<double>(ws, L.off_thr); r.thr_stride = (int64_t)sl.nq * M;
+    r.w = bp.w; r.h = bp.h;
+    r.M = M; r.nq = sl.nq;
+    for (int k = 0; k < 6; ++k) r.qslot[k] = -1;
+    for (int q = 0; q < sl.nq; ++q) r.qslot[sl.slot[q]] = q;
+    r.kinds = mask;
+    r.sp = sp;
+    r.hist = at<uint64_t>(ws, L.off_hist);
+    r.list = at<uint4>(ws, L.off_list); r.ctr = at<uint32_t>(ws, L.off_ctr); r.cap = L.list_cap;
+    r.status = status; r.P = P;
+    r.binout = binout; r.rowsA = rowsA; r.rowsB = rowsB;
+    r.mirror = binout != nullptr && same_rows(asrc, bsrc) && rowsA == rowsB;
+    r.S = g.S; r.H = g.H; r.W = g.W; r.gs = g.gs;
+    return r;
+}
+
 // Core: counts for P items of (row panel x col panel), into the workspace histogram.
 cil_status run_engines(int P, const RowSrc& asrc, const RowSrc& bsrc, int64_t rowsA, int64_t rowsB,
                        const cil_grid& g, uint32_t mask, const Slots& sl, int M, const Plan& pl,
@@ -286,15 +323,19 @@ cil_status run_engines(int P, const RowSrc& asrc, const RowSrc& bsrc, int64_t ro
     float* thr2 = pl.tc ? at<float>(ws, L.off_thr2) : nullptr;
     uint64_t* hist = at<uint64_t>(ws, L.off_hist);
     uint32_t* ctr = at<uint32_t>(ws, L.off_ctr);
+    uint4* list = L.list_cap ? at<uint4>(ws, L.off_list) : nullptr;
     CIL_CU(launch_prep(P, sl.nq, M, radii, radii_stride, bp, thr, thr2, status, hist, L.hist_elems, ctr, st,
                        keep_status));
     if (rowsA == 0 || rowsB == 0) return CIL_OK;
+    const bool b_same = same_rows(asrc, bsrc) && rowsA == rowsB;
 
     if (pl.simt_mask) {
         float* aug = at<float>(ws, L.off_aug);
         float* augB = aug + (size_t)P * rowsA * L.geom.off[3];
-        CIL_CU(launch_pack_aug(P, asrc, rowsA, L.geom, aug, status, st));
-        CIL_CU(launch_pack_aug(P, bsrc, rowsB, L.geom, augB, status, st));
+        float* statA = at<float>(ws, L.off_rowstat);
+        float* statB = statA + (size_t)P * rowsA * 4;
+        CIL_CU(launch_pack_aug(P, asrc, rowsA, L.geom, aug, statA, status, st));
+        CIL_CU(launch_pack_aug(P, bsrc, rowsB, L.geom, augB, statB, status, st));
         SimtArgs a{};
         a.Aaug = aug; a.Baug = augB;
         a.rowsA = rowsA; a.rowsB = rowsB; a.Kaug = L.geom.off[3];
@@ -313,99 +354,69 @@ cil_status run_engines(int P, const RowSrc& asrc, const RowSrc& bsrc, int64_t ro
         a.binout = binout;
         a.range = range;
         a.tri = tile_skip == 2;
-        a.sym = binout != nullptr && same_rows(asrc, bsrc) && rowsA == rowsB;
+        a.sym = binout != nullptr && b_same;
+        a.statA = statA; a.statB = statB;
+        a.list = list; a.ctr = ctr; a.cap = L.list_cap;
         CIL_CU(launch_simt(a, st));
     }
     if (pl.tc) {
         if (!gram_tc_supported()) return CIL_EUNSUPPORTED;
-        const size_t esz = pl.split == 2 ? 4 : (pl.split == 3 ? 1 : 2);
         float* center = at<float>(ws, L.off_center);
-        char* hi = at<char>(ws, L.off_hi);
-        char* lo = at<char>(ws, L.off_lo);
-        float* nrm = at<float>(ws, L.off_nrm);
-        float* q4 = at<float>(ws, L.off_q4);      // (sum x~^4)^(1/4) for the float splits, sigma for INT8
-        const size_t offB = (size_t)P * rowsA;
-        uint4* list = at<uint4>(ws, L.off_list);
         CIL_CU(launch_center(P, bsrc, rowsB < 16 ? rowsB : 16, K, L.Kp, center, st));
-        int q_tc[3] = {-1, -1, -1};
-        if (pl.aug) {
-            // ---- three-phase INT8 engine: L2, W12, W12SUM from the Grams of [x~ | D_x x~ | D_y x~]
+        if (pl.split == 3) {
+            // ---- three-digit INT8 engine (default): L2, or with pl.aug L2, W12, W12SUM from the
+            // Grams of [x~ | D_x x~ | D_y x~]; exact integer accumulation, worst-case bound
+            int8_t* planes = at<int8_t>(ws, L.off_hi);
+            float* meta = at<float>(ws, L.off_nrm);
+            const int64_t pstride = L.rows_cap * L.Krow;
+            const int64_t offB = b_same ? 0 : (int64_t)P * rowsA;
+            if (pl.aug) {
+                const AugGeom ag = make_aug_geom(g.S, g.H, g.W, 3, g.gs);
+                CIL_CU(launch_pack3_aug(P, asrc, rowsA, ag, L.kp, center, L.Kp, planes, pstride, 0, meta, status, st));
+                if (!b_same)
+                    CIL_CU(launch_pack3_aug(P, bsrc, rowsB, ag, L.kp, center, L.Kp, planes, pstride, offB, meta, status,
+                                            st));
+            } else {
+                CIL_CU(launch_pack3(P, asrc, rowsA, K, L.Kp, center, planes, pstride, 0, meta, status, st));
+                if (!b_same)
+                    CIL_CU(launch_pack3(P, bsrc, rowsB, K, L.Kp, center, planes, pstride, offB, meta, status, st));
+            }
+            G3Args t{};
+            t.planes = planes; t.rows_tot = L.rows_cap; t.Kp = L.Krow; t.meta = meta;
+            t.rowsA = rowsA; t.rowsB = rowsB; t.a_off = 0; t.b_off = offB;
+            t.P = P; t.p0 = 0; t.np = P;
+            t.nph = pl.aug ? 3 : 1;
+            if (pl.aug) {
+                for (int a = 0; a < 3; ++a) { t.ph_beg[a] = L.kp[a]; t.ph_end[a] = L.kp[a + 1]; }
+            } else {
+                t.ph_beg[0] = 0; t.ph_end[0] = L.Krow;
+            }
+            t.thr = thr2; t.thr_stride = 8 * M;
+            t.M = M; t.nq = sl.nq; t.q_l2 = sl.q_l2;
+            t.q_k[0] = t.q_k[1] = t.q_k[2] = -1;
             for (int q = 0; q < sl.nq; ++q) {
-                if (sl.slot[q] == 0) q_tc[0] = q;
-                if (sl.slot[q] == 3) q_tc[1] = q;
-                if (sl.slot[q] == 2) q_tc[2] = q;
+                if (sl.slot[q] == 0) t.q_k[0] = q;
+                if (sl.slot[q] == 3) t.q_k[1] = q;
+                if (sl.slot[q] == 2) t.q_k[2] = q;
             }
-            const AugGeom ag = make_aug_geom(g.S, g.H, g.W, 3, g.gs);
-            const int64_t Kr = L.kp[3];
-            const bool b_same = same_rows(asrc, bsrc) && rowsA == rowsB;
-            CIL_CU(launch_pack_i8_aug(P, asrc, rowsA, ag, L.kp, center, L.Kp, reinterpret_cast<int8_t*>(hi),
-                                      reinterpret_cast<int8_t*>(lo), Kr, nrm, q4, status, st));
-            if (!b_same)
-                CIL_CU(launch_pack_i8_aug(P, bsrc, rowsB, ag, L.kp, center, L.Kp,
-                                          reinterpret_cast<int8_t*>(hi + offB * Kr),
-                                          reinterpret_cast<int8_t*>(lo + offB * Kr), Kr, nrm + offB * 4,
-                                          q4 + offB * 4, status, st));
-            I8Args t{};
-            t.hq = reinterpret_cast<const int8_t*>(hi); t.lq = reinterpret_cast<const int8_t*>(lo);
-            t.rowsA = rowsA; t.rowsB = rowsB; t.Kp = Kr; t.K = K;
-            t.P = P; t.p0 = 0; t.np = P;
-            t.thr2 = thr2; t.thr_stride = 3 * M; t.M = M; t.q_l2 = sl.q_l2; t.nq = sl.nq;
             t.sp = sp; t.hist = hist;
-            t.recheck = list; t.recheck_ctr = ctr; t.recheck_cap = L.list_cap;
-            t.kq = 20.0f;
-            t.rel = (float)ldexp(1.0, -21);
-            t.b_same = b_same;
-            t.nph = 3;
-            const int64_t klen[3] = {ag.K, ag.Kx, ag.Ky};
-            for (int a = 0; a < 3; ++a) {
-                t.kb_end[a] = (int)(L.kp[a + 1] / kTcBK);
-                t.kll3[a] = (float)(8.0 * 2.0 * (128.0 * 128.0 / 3.0) * sqrt((double)klen[a]));
-                t.q_tc[a] = q_tc[a];
-            }
-            t.kll = t.kll3[0];
-            t.nrm3 = nrm; t.scl3 = q4;
-            t.part = at<float>(ws, L.off_part);
-            t.ih = (float)(1.0 / bp.h);
-            t.diag = diag;
+            t.list = list; t.ctr = ctr; t.cap = L.list_cap;
+            f32_bracket(1.0 / bp.h, &t.ih_rd, &t.ih_ru);
+            f32_bracket(1.0 / (bp.h * bp.h), &t.ih2_rd, &t.ih2_ru);
+            t.part = pl.aug ? at<float>(ws, L.off_part) : nullptr;
             t.binout = binout;
-            // symmetric bin matrix of one panel against itself: the upper tile triangle, mirrored
             t.skip = (binout && b_same) ? 1 : (b_same ? tile_skip : 0);
-            CIL_CU(launch_gram_i8(t, st));
-        } else if (pl.split == 3) {
-            // ---- INT8 two-digit engine (default): exact int32 accumulation
-            // B = A (pool x pool bin matrices of the bootstrap): the rows are packed once
-            const bool b_same = same_rows(asrc, bsrc) && rowsA == rowsB;
-            if (b_same)
-                CIL_CU(launch_pack_i8(P, asrc, rowsA, K, L.Kp, center, reinterpret_cast<int8_t*>(hi),
-                                      reinterpret_cast<int8_t*>(lo), nrm, q4, status, st));
-            else
-                CIL_CU(launch_pack_i8_pair(P, asrc, rowsA, bsrc, rowsB, K, L.Kp, center,
-                                           reinterpret_cast<int8_t*>(hi), reinterpret_cast<int8_t*>(lo), nrm, q4,
-                                           status, st));
-            I8Args t{};
-            t.hq = reinterpret_cast<const int8_t*>(hi); t.lq = reinterpret_cast<const int8_t*>(lo);
-            t.nrm = nrm; t.scl = q4;
-            t.rowsA = rowsA; t.rowsB = rowsB; t.Kp = L.Kp; t.K = K;
-            t.P = P; t.p0 = 0; t.np = P;
-            t.thr2 = thr2; t.thr_stride = 3 * M; t.M = M; t.q_l2 = sl.q_l2; t.nq = sl.nq;
-            t.sp = sp; t.hist = hist;
-            t.recheck = list; t.recheck_ctr = ctr; t.recheck_cap = L.list_cap;
-            // E = kq d sqrt((s_a^2 + s_b^2)/3) + kll s_a s_b + rel (n_a + n_b): 20 sigma of the operand
-            // quantisation (uniform error, variance s^2/12 per element, d^2 error 2 u.(da - db)), 8 sigma
-            // of the dropped LL digit product (Gaussian-like: mean |LL| / (sqrt(K) E[l^2]) = 0.80 measured) (E[l^2] ~ 128^2/3, x2 for d^2), FP32 rounding of d^2, the
-            // norms and the thresholds (measured max error / E ~ 0.2).
-            t.kq = 20.0f;
-            t.kll = (float)(8.0 * 2.0 * (128.0 * 128.0 / 3.0) * sqrt((double)K));
-            t.rel = (float)ldexp(1.0, -21);
             t.diag = diag;
-            t.binout = binout;
-            t.b_same = b_same;
-            // symmetric bin matrix of one panel against itself: the upper tile triangle, mirrored
-            t.skip = (binout && b_same) ? 1 : (b_same ? tile_skip : 0);
-            CIL_CU(launch_gram_i8(t, st));
+            CIL_CU(launch_gram3(t, st));
         } else {
             // ---- 3xBF16 / 3xTF32 split engine (histogram mode only)
             if (binout) return CIL_EUNSUPPORTED;
+            const size_t esz = pl.split == 2 ? 4 : 2;
+            char* hi = at<char>(ws, L.off_hi);
+            char* lo = at<char>(ws, L.off_lo);
+            float* nrm = at<float>(ws, L.off_nrm);
+            float* q4 = at<float>(ws, L.off_q4);
+            const size_t offB = (size_t)P * rowsA;
             CIL_CU(launch_pack_tc(P, asrc, rowsA, K, L.Kp, center, pl.split, hi, lo, nrm, q4, status, st));
             CIL_CU(launch_pack_tc(P, bsrc, rowsB, K, L.Kp, center, pl.split, hi + offB * L.Kp * esz,
                                   lo + offB * L.Kp * esz, nrm + offB, q4 + offB, status, st));
@@ -413,18 +424,13 @@ cil_status run_engines(int P, const RowSrc& asrc, const RowSrc& bsrc, int64_t ro
             t.hi = hi; t.lo = lo; t.nrm = nrm; t.q4 = q4;
             t.rowsA = rowsA; t.rowsB = rowsB; t.Kp = L.Kp; t.K = K;
             t.P = P; t.split = pl.split;
-            t.thr2 = thr2; t.thr_stride = 3 * M; t.M = M;
+            t.thr2 = thr2 + 6 * M; t.thr_stride = 8 * M; t.M = M;
             t.q_l2 = sl.q_l2; t.nq = sl.nq;
             t.sp = sp; t.hist = hist;
             t.recheck = list; t.recheck_ctr = ctr; t.recheck_cap = L.list_cap;
             t.status = status;
-            {   // diagnostic overrides for A/B measurements (defaults: CTA pairs, 4-k-block chunks)
-                static const char* cg = getenv("CIL_TC_CTA_GROUP");
-                static const char* ck = getenv("CIL_TC_CHUNK_KB");
-                t.cta_group = (cg && cg[0] == '1') ? 1 : 2;
-                t.chunk_kb = ck ? atoi(ck) : 4;
-                if (t.chunk_kb < 1) t.chunk_kb = 1;
-            }
+            t.cta_group = 2;
+            t.chunk_kb = 4;
             // E = k1 q_a q_b + rel (n_a + n_b): k1 = 8 sigma of the split residual (2^-16 per product
             // for 3xBF16, 2^-20 for 3xTF32, x2 for d^2); rel = truncation over the 12*chunk_kb MMA steps
             // of one chunk + RN adds of the chunk partials + FP32 evaluation / threshold rounding.
@@ -436,27 +442,12 @@ cil_status run_engines(int P, const RowSrc& asrc, const RowSrc& bsrc, int64_t ro
             t.p0 = 0; t.np = P; t.sm_budget = 0;
             CIL_CU(launch_gram_tc(t, st));
         }
-        if (diag) return CIL_OK;
-        RecheckArgs r{};
-        r.asrc = asrc; r.bsrc = bsrc; r.K = K;
-        r.thr = thr; r.thr_stride = (int64_t)sl.nq * M; r.w = bp.w;
-        r.M = M; r.nq = sl.nq; r.q_l2 = sl.q_l2;
-        r.sp = sp; r.hist = hist;
-        r.list = list; r.ctr = ctr; r.cap = L.list_cap;
-        r.status = status; r.P = P;
-        r.binout = binout; r.rowsA = rowsA; r.rowsB = rowsB;
-        r.mirror = binout != nullptr && pl.split == 3 && same_rows(asrc, bsrc) && rowsA == rowsB;
-        for (int a = 0; a < 3; ++a) r.q_tc[a] = q_tc[a];
-        r.S = g.S; r.H = g.H; r.W = g.W; r.h = bp.h; r.gs = g.gs;
-        CIL_CU(launch_recheck(r, st));
-        static const char* dbg = getenv("CIL_DEBUG_RECHECK");   // diagnostic: synchronising count print
-        if (dbg && dbg[0] == '1') {
-            uint32_t n = 0;
-            cudaMemcpyAsync(&n, ctr, sizeof(n), cudaMemcpyDeviceToHost, st);
-            cudaStreamSynchronize(st);
-            fprintf(stderr, "[libcil] re-checked pairs: %u of %.0f (%.2e)\n", n, (double)P * rowsA * rowsB,
-                    n / ((double)P * rowsA * rowsB));
-        }
+    }
+    if (diag || range) return CIL_OK;
+    if (L.list_cap) {
+        const RecheckArgs r = recheck_args(asrc, bsrc, K, g, sl, M, bp, sp, L, ws, status, P, binout, rowsA, rowsB,
+                                           mask);
+        CIL_CU(launch_recheck(r, L.hist_elems, st));
     }
     return CIL_OK;
 }
@@ -537,7 +528,7 @@ cil_status cil_loglik(int32_t P, const double* mu, int64_t mu_stride, const doub
 }
 
 namespace {
-// SCIL panel geometry.  The Gram tiles 256 rows x (256 or 192) columns; when the row panel
+// SCIL panel geometry.  The INT8 Gram tiles 256 rows x 128 columns; when the row panel
 // ((n_ens+1) N_set rows, e.g. 550) pads worse on the 256-row axis than the column panel
 // (n_ens N~, e.g. 500), the panels are swapped (the column panel runs as the Gram's rows;
 // segments become [l][k], k_build_Y reads them transposed).  Only for the INT8 engine.
@@ -547,10 +538,7 @@ struct SynthGeo {
     SegParams sp;
     Plan pl;
 };
-int64_t pad_cols(int64_t n) {
-    const int64_t a = (n + 255) / 256 * 256, b = (n + 191) / 192 * 192;
-    return a < b ? a : b;
-}
+int64_t pad_cols(int64_t n) { return (n + 127) / 128 * 128; }
 SynthGeo synth_geo(int32_t n_ens, int32_t N_set, int32_t N_tilde, const cil_grid& g, uint32_t mask, int32_t M,
                    cil_engine engine) {
     SynthGeo s{};
@@ -665,9 +653,8 @@ cil_status cil_distance_range(int32_t P, const float* A, int64_t strideA, int64_
     if (ws_bytes < L.total + 512) return CIL_ENOMEM;
     void* wsa = reinterpret_cast<void*>(((uintptr_t)ws + 255) & ~(uintptr_t)255);
     double* r = at<double>(wsa, L.total);                 // a dummy radius per measure (not binned)
-    const double ones[kMaxMeas] = {1.0, 1.0, 1.0, 1.0, 1.0, 1.0};
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    CIL_CU(cudaMemcpyAsync(r, ones, sizeof(double) * sl.nq, cudaMemcpyHostToDevice, st));
+    CIL_CU(launch_fill_f64(r, sl.nq, 1.0, st));          // device-side: stays asynchronous and capturable
     unsigned long long* rg = reinterpret_cast<unsigned long long*>(range);   // non-negative FP64 bits: ordered
     CIL_CU(launch_range_init(P, sl.nq, rg, st));
     RowSrc as{}, bs{};
@@ -915,48 +902,38 @@ cil_status cil_synth_loglik_boot(int32_t P, const float* pools, int64_t pool_str
         const int64_t K = (int64_t)g.S * g.H * g.W;
         const Layout& L = B.L;
         float* center = at<float>(wsa, L.off_center);
-        int8_t* hi = at<int8_t>(wsa, L.off_hi);
-        int8_t* lo = at<int8_t>(wsa, L.off_lo);
-        float* nrm = at<float>(wsa, L.off_nrm);
-        float* q4 = at<float>(wsa, L.off_q4);
+        int8_t* planes = at<int8_t>(wsa, L.off_hi);
+        float* meta = at<float>(wsa, L.off_nrm);
         uint32_t* ctr = at<uint32_t>(wsa, L.off_ctr);
-        const int64_t a_off = (int64_t)P * N_syn;                 // data planes after the pool planes
+        const int64_t a_off = (int64_t)P * N_syn;                 // data rows after the pool rows
         RowSrc ds{};
         ds.base = data; ds.stride = 0; ds.ld = ld_data; ds.rows = N_set; ds.mode = MODE_PLAIN;
         CIL_CU(cudaMemsetAsync(ctr, 0, sizeof(uint32_t), st));
-        CIL_CU(launch_pack_i8(P, ds, N_set, K, L.Kp, center, hi + a_off * L.Kp, lo + a_off * L.Kp, nrm + a_off,
-                              q4 + a_off, item_status, st));
+        CIL_CU(launch_pack3(P, ds, N_set, K, L.Kp, center, planes, L.rows_cap * L.Krow, a_off, meta, item_status, st));
         const bool narrow = N_set <= 64;                           // s_data as a 64-wide B tile
         SegParams sph = narrow ? SegParams{N_syn, N_set, 1, 1} : SegParams{N_set, N_syn, 1, 1};
-        I8Args t{};
-        t.hq = hi; t.lq = lo; t.nrm = nrm; t.scl = q4;
-        t.rowsA = narrow ? N_syn : N_set; t.rowsB = narrow ? N_set : N_syn; t.Kp = L.Kp; t.K = K;
-        t.offs_set = true; t.a_off = narrow ? 0 : a_off; t.b_off = narrow ? a_off : 0;
+        G3Args t{};
+        t.planes = planes; t.rows_tot = L.rows_cap; t.Kp = L.Krow; t.meta = meta;
+        t.rowsA = narrow ? N_syn : N_set; t.rowsB = narrow ? N_set : N_syn;
+        t.a_off = narrow ? 0 : a_off; t.b_off = narrow ? a_off : 0;
         t.tn_force = narrow ? 64 : 0;
         t.P = P; t.p0 = 0; t.np = P;
-        t.thr2 = at<float>(wsa, L.off_thr2); t.thr_stride = 3 * M; t.M = M; t.q_l2 = sl.q_l2; t.nq = sl.nq;
+        t.nph = 1; t.ph_beg[0] = 0; t.ph_end[0] = L.Krow;
+        t.thr = at<float>(wsa, L.off_thr2); t.thr_stride = 8 * M; t.M = M; t.q_l2 = sl.q_l2; t.nq = sl.nq;
+        t.q_k[0] = sl.q_l2; t.q_k[1] = t.q_k[2] = -1;
         t.sp = sph; t.hist = at<uint64_t>(wsa, L.off_hist);
-        t.recheck = at<uint4>(wsa, L.off_list); t.recheck_ctr = ctr; t.recheck_cap = L.list_cap;
-        t.kq = 20.0f;                                             // the INT8 bound, as in run_engines
-        t.kll = (float)(8.0 * 2.0 * (128.0 * 128.0 / 3.0) * sqrt((double)K));
-        t.rel = (float)ldexp(1.0, -21);
+        t.list = at<uint4>(wsa, L.off_list); t.ctr = ctr; t.cap = L.list_cap;
         t.binout = bins;                                          // [P][nq][N_set][N_syn] either way
         t.bin_t = narrow;                                         // (narrow: the transposed output)
-        CIL_CU(launch_gram_i8(t, st));
+        CIL_CU(launch_gram3(t, st));
         BinParams bp{};
         bp.h = grid_h(g);
         bp.w = g.H > 1 ? bp.h * bp.h : bp.h;
-        RecheckArgs r{};
-        r.asrc = narrow ? ps : ds; r.bsrc = narrow ? ds : ps; r.K = K;
-        r.thr = at<double>(wsa, L.off_thr); r.thr_stride = (int64_t)sl.nq * M; r.w = bp.w;
-        r.M = M; r.nq = sl.nq; r.q_l2 = sl.q_l2;
-        r.sp = sph; r.hist = at<uint64_t>(wsa, L.off_hist);
-        r.list = at<uint4>(wsa, L.off_list); r.ctr = ctr; r.cap = L.list_cap;
-        r.status = item_status; r.P = P;
-        r.binout = bins; r.rowsA = t.rowsA; r.rowsB = t.rowsB; r.mirror = false; r.transpose = narrow;
-        for (int a = 0; a < 3; ++a) r.q_tc[a] = -1;
-        r.S = g.S; r.H = g.H; r.W = g.W; r.h = bp.h; r.gs = g.gs;
-        CIL_CU(launch_recheck(r, st));
+        RecheckArgs r = recheck_args(narrow ? ps : ds, narrow ? ds : ps, K, g, sl, M, bp, sph, L, wsa, item_status, P,
+                                     bins, t.rowsA, t.rowsB, CIL_L2);
+        r.mirror = false;
+        r.transpose = narrow;
+        CIL_CU(launch_recheck(r, 0, st));
         CIL_CU(launch_resample(P, bins, N_set, N_syn, sl.nq, M, 1, nullptr, N_set, J, Nt, nullptr,
                                Y + (int64_t)n_rep * D, Ystride, item_status, st));
         CIL_CU(launch_boot_tail(P, n_rep, D, ridge, out, item_status, Y, at<double>(wsa, B.L.off_mu),
@@ -997,9 +974,8 @@ cil_status cil_diag_gram(const float* A, int64_t lda, int64_t N, const float* B,
     void* wsa = reinterpret_cast<void*>(((uintptr_t)ws + 255) & ~(uintptr_t)255);
     // a single dummy radius (the diagnostic path does not bin); it lives past the layout
     double* r = at<double>(wsa, L.total);
-    const double one = 1.0;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    CIL_CU(cudaMemcpyAsync(r, &one, sizeof(double), cudaMemcpyHostToDevice, st));
+    CIL_CU(launch_fill_f64(r, 1, 1.0, st));
     int32_t* status = reinterpret_cast<int32_t*>(r + 1);
     RowSrc as{}, bs{};
     as.base = A; as.ld = lda; as.rows = N; as.mode = MODE_PLAIN;
@@ -1025,9 +1001,8 @@ cil_status cil_diag_gram_family(const float* A, int64_t lda, int64_t N, const fl
     if (ws_bytes < L.total + 512) return CIL_ENOMEM;
     void* wsa = reinterpret_cast<void*>(((uintptr_t)ws + 255) & ~(uintptr_t)255);
     double* r = at<double>(wsa, L.total);                 // one dummy radius per measure (not binned)
-    const double ones[3] = {1.0, 1.0, 1.0};
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    CIL_CU(cudaMemcpyAsync(r, ones, sizeof(ones), cudaMemcpyHostToDevice, st));
+    CIL_CU(launch_fill_f64(r, 3, 1.0, st));
     int32_t* status = reinterpret_cast<int32_t*>(r + 3);
     RowSrc as{}, bs{};
     as.base = A; as.ld = lda; as.rows = N; as.mode = MODE_PLAIN;

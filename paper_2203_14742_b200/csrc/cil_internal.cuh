@@ -147,12 +147,13 @@ struct ProfScope {
 namespace cil {
 
 // pack.cu
+cudaError_t launch_fill_f64(double* p, int n, double v, cudaStream_t st);
 cudaError_t launch_prep(int P, int nq, int M, const double* radii, int64_t radii_stride,
                         const BinParams& bp, double* thr, float* thr2_l2, int32_t* status,
                         uint64_t* hist, int64_t hist_elems, uint32_t* recheck_ctr, cudaStream_t st,
                         bool keep_status = false);
 cudaError_t launch_pack_aug(int P, const RowSrc& src, int64_t rows, const AugGeom& g,
-                            float* out, int32_t* status, cudaStream_t st);
+                            float* out, float* rowstat, int32_t* status, cudaStream_t st);
 cudaError_t launch_center(int P, const RowSrc& colsrc, int64_t nrows_center, int64_t K, int64_t Kp,
                           float* center, cudaStream_t st);
 cudaError_t launch_pack_tc(int P, const RowSrc& src, int64_t rows, int64_t K, int64_t Kp,
@@ -185,6 +186,8 @@ struct SimtArgs {
     bool sym;                                 // bin matrix of a panel against itself: tiles with
                                               // i > j only are skipped, computed (i, j) also written at (j, i)
     int hist_cap;                             // shared histogram entries (set by the launcher)
+    const float* statA; const float* statB;   // [P][rows][4] per-row derivative stats (k_pack_aug)
+    uint4* list; uint32_t* ctr; uint32_t cap; // re-check list: (p, i, j, b_lo | measure id << 8)
 };
 cudaError_t launch_simt(const SimtArgs& a, cudaStream_t st);
 
@@ -256,6 +259,38 @@ struct I8Args {
     unsigned long long* rd_out;
 };
 cudaError_t launch_gram_i8(const I8Args& a, cudaStream_t st);
+
+// gram3.cu (three-digit INT8 engine, the default L2 / L2-family engine; worst-case error bound)
+struct G3Args {
+    const int8_t* planes;                // [3][rows_tot][Kp] digits h, m, l (A panels then B panels)
+    int64_t rows_tot, Kp;
+    const float* meta;                   // [rows_tot][nph][8]: n, sigma, r, alpha, beta
+    int64_t rowsA, rowsB, a_off, b_off;  // A rows at a_off + p rowsA, B rows at b_off + p rowsB
+    int P, p0, np;
+    int nph;                             // 1 (L2) or 3 (value, D_x, D_y blocks: L2, W12, W12SUM)
+    int64_t ph_beg[3], ph_end[3];        // K byte ranges of the phases (multiples of 64, contiguous)
+    const float* thr;                    // [P][8][M] (k_prep)
+    int64_t thr_stride;
+    int M, nq, q_l2;
+    int q_k[3];                          // three-phase: slots of L2, W12, W12SUM (-1: absent)
+    SegParams sp;
+    uint64_t* hist;
+    uint4* list; uint32_t* ctr; uint32_t cap;
+    float ih_rd, ih_ru, ih2_rd, ih2_ru;  // 1/h and 1/h^2 rounded down / up
+    float* part;                         // three-phase partials [2][P rowsA rowsB] float2
+    uint8_t* binout;                     // non-null: bins [p][q][i][j] (or [p][q][j][i] with bin_t)
+    bool bin_t;
+    int skip;                            // 0 all tiles; 1 symmetric bin matrix; 2 Alg. 1 blocks k < l
+    int tn_force;                        // 64: narrow B panel (<= 64 rows)
+    float* diag;                         // diagnostics: (lo, hi) per pair of item 0, no binning
+};
+cudaError_t launch_gram3(const G3Args& a, cudaStream_t st);
+cudaError_t launch_pack3(int P, const RowSrc& src, int64_t rows, int64_t K, int64_t Kp, const float* center,
+                         int8_t* planes, int64_t plane_stride, int64_t row0, float* meta, int32_t* status,
+                         cudaStream_t st);
+cudaError_t launch_pack3_aug(int P, const RowSrc& src, int64_t rows, const AugGeom& g, const int64_t* kp,
+                             const float* center, int64_t Kc, int8_t* planes, int64_t plane_stride, int64_t row0,
+                             float* meta, int32_t* status, cudaStream_t st);
 cudaError_t launch_pack_i8_aug(int P, const RowSrc& src, int64_t rows, const AugGeom& g, const int64_t* kp,
                                const float* center, int64_t Kc, int8_t* hq, int8_t* lq, int64_t Kp_aug,
                                float* nrm3, float* scl3, int32_t* status, cudaStream_t st);
@@ -265,27 +300,25 @@ bool gram_tc_supported();
 struct RecheckArgs {
     RowSrc asrc, bsrc;
     int64_t K;
-    const double* thr;   // FP64 thresholds of slot q_l2 are thr[p*thr_stride + q_l2*M + m] (R)
+    const double* thr;   // FP64 radii: slot q of item p at thr[p*thr_stride + q*M + m]
     int64_t thr_stride;
-    double w;
-    int M, nq, q_l2;
+    double w, h;         // quadrature weight h^dim, grid spacing
+    int M, nq;
+    int qslot[6];        // histogram / bin slot of measure id k (bit order), -1 if not requested
+    uint32_t kinds;      // measure ids requested (bit k)
     SegParams sp;
     uint64_t* hist;
-    const uint4* list; const uint32_t* ctr; uint32_t cap;
+    const uint4* list; const uint32_t* ctr; uint32_t cap;   // entries (p, i, j, b_lo | kind << 8)
     int32_t* status;
     int P;
-    uint8_t* binout;     // non-null: write the exact bin to bins[p][q_l2][i][j] instead of moving counts
+    uint8_t* binout;     // non-null: write the exact bin to bins[p][q][i][j] instead of moving counts
     bool mirror;         // symmetric bin matrix: also write [j][i]
-    bool transpose;      // write bins[p][q_l2][j][i] only (matches I8Args.bin_t)
+    bool transpose;      // write bins[p][q][j][i] only (the INT8 engine's transposed narrow output)
     int64_t rowsA, rowsB;
-    // entries of the three-phase engine carry the measure kind in bits 8-15 of .w
-    // (0 L2, 1 W12, 2 W12SUM); q_tc = their histogram slots, S/H/W the grid, h the spacing
-    int q_tc[3];
     int S, H, W;
-    double h;
     uint32_t gs;
 };
-cudaError_t launch_recheck(const RecheckArgs& a, cudaStream_t st);
+cudaError_t launch_recheck(const RecheckArgs& a, int64_t hist_elems, cudaStream_t st);
 
 // stats.cu
 cudaError_t launch_finalize(int P, int nq, int M, const SegParams& sp, const uint64_t* hist,

@@ -1,0 +1,1150 @@
+// gram3.cu — step a1 (pack) and a2 (L2 Gram + fused binning) of the hot path, default engine,
+// and the L2-type family of SURVEY §8(f) 2, on tcgen05 kind::i8 with a WORST-CASE error bound.
+//
+// What it computes: for every pair (i, j) of an item, the L2 distance d = |a_i - b_j| of the caller's
+// FP32 patterns (Eq. (5)) — or, in three-phase mode, the block distances of the
+// augmented rows [x | D_x x | D_y x] that W12 (Eq. (8)) and W12SUM (Eq. (7)) are made of — and
+// the count #{(i, j) : d < R_m} of Eq. (1) (strict <), without writing the N x Nt
+// distance matrix anywhere.
+//
+// Representation (k_pack3_*): per row x~ = x - c (c = the item's centre, FP32), sigma = max|x~| / Q,
+// q = rint(x~ / sigma) = 2^16 h + 2^8 m + l, int8 digits h in [-63, 63], m, l in [-128, 127]
+// (22-bit fixed point, Q = 4 160 000).  Per-row metadata (8 floats):
+//   n = sigma^2 sum q^2 (exact integer sum via dp4a of the digits), sigma,
+//   r >= |x^ - (x - c)| with x^ = sigma q (quantisation AND FP32-centring residual, upper bound),
+//   alpha >= sigma |l|, beta >= 2^8 sigma |m|.
+// Gram (k_gram3): G' = 2^32 L32 + 2^24 L24 + 2^16 L16 with L32 = sum h_a h_b, L24 = sum (h_a m_b +
+// m_a h_b), L16 = sum (h_a l_b + m_a m_b + l_a h_b) accumulated EXACTLY in three int32 TMEM
+// accumulators, six MMAs per 32-byte K step (|L16| <= 32512 K < 2^31 for K <= 65536; longer K runs in
+// chunks whose FP32 partials are summed in a fourth TMEM column block).  The dropped digit products
+// obey |G - G'| <= 2^8 (|m_a||l_b| + |l_a||m_b|) + |l_a||l_b| (Cauchy-Schwarz), so with the FP32
+// evaluation d~^2 = n_a + n_b - 2 sigma_a sigma_b G':
+//   |d_q^2 - d~^2| <= Delta = 2 (alpha_a alpha_b + alpha_a beta_b + beta_a alpha_b) + rel (n_a + n_b)
+// (d_q = |x^_a - x^_b|; rel >= the FP32 rounding of d~^2) and |d - d_q| <= rho = r_a + r_b (triangle
+// inequality), hence for EVERY input
+//   d in [ sqrt(max(d~^2 - Delta, 0)) - rho ,  sqrt(d~^2 + Delta) + rho ]
+// evaluated with directed rounding (__f*_rd / __f*_ru).  A pair is binned in-kernel when no radius
+// lies in its interval; otherwise it is listed for the exact FP64 re-check (recheck.cu).  Counts are
+// therefore those of the plain definition (reading R13).
+//
+// Kernel anatomy (persistent CTA pairs, cta_group::2, tiles of 256 A rows x TN B columns, TN = 128
+// (64 for a narrow B panel); TMEM columns [0,TN) L32, [TN,2TN) L24, [2TN,3TN) L16, [3TN,4TN) the
+// chunk partial):
+//   warp 0      TMA producer: one 3-D box (64 K-bytes x rows x 3 planes, SWIZZLE_64B) for A and one
+//               for B per stage, 4-6 stages
+//   warp 1      TMEM allocator + single-thread MMA issuer (leader CTA)
+//   warps 2..   epilogue (12 warps; 8 in three-phase mode): tcgen05.ld of the accumulators ->
+//               interval of d -> binary search over the radii -> per-thread shared histograms
+//               (fire-and-forget ATOMS, flushed per tile as warp sums -> u64 atomics), or the bins as
+//               bytes (bootstrap bin matrices); ambiguous pairs -> the re-check list.
+#include <cuda.h>
+#include <stdio.h>
+
+#include <algorithm>
+
+#include "cil_internal.cuh"
+#include "tc_common.cuh"
+
+namespace cil {
+namespace g3 {
+using tc::cluster_rank;
+using tc::cluster_sync;
+using tc::fence_after;
+using tc::fence_before;
+using tc::mbar_arrive_remote;
+using tc::mbar_expect_tx;
+using tc::mbar_init;
+using tc::mbar_wait;
+using tc::mbar_wait_cluster;
+using tc::named_bar;
+using tc::smem_u32;
+using tc::tmem_ld16;
+
+constexpr int KS = 64;          // K bytes per pipeline stage (one SWIZZLE_64B row)
+constexpr int AR = 128;         // A rows per CTA (M = 256 per CTA pair)
+constexpr int TILE_M = 256;
+constexpr int MAXSEG = 24;
+
+struct Params {
+    int64_t rowsA, rowsB, a_off, b_off;
+    int P, p0, np;
+    int tiles_m, tiles_n, tiles_act, tn, skip;
+    int nseg;
+    int seg_end[MAXSEG];               // K-block (64 B) end of each segment
+    uint8_t seg_ph[MAXSEG], seg_first[MAXSEG], seg_last[MAXSEG], seg_empty[MAXSEG];
+    int nph;
+    const float* meta;                 // [rows_tot][nph][8]
+    const float* thr;                  // [P][8][M]: kind k (L2 R/sqrt(w), W12 R^2/w, W12SUM R/sqrt(w)) at
+                                       // rows 2k (rounded down) and 2k+1 (rounded up)
+    int64_t thr_stride;
+    int M, nq, q_l2;
+    int q_k[3];                        // histogram slots of L2, W12, W12SUM (-1: not requested)
+    SegParams sp;
+    unsigned long long* hist;
+    uint4* list; uint32_t* ctr; uint32_t cap;
+    float rel;                         // FP32 evaluation bound of d~^2 relative to n_a + n_b
+    float ih_rd, ih_ru, ih2_rd, ih2_ru;  // 1/h, 1/h^2 rounded down / up
+    float2* part;                      // three-phase: [2][P rowsA rowsB] (lo, hi) of phases 0 and 1
+    uint8_t* binout;
+    int bin_t;
+    float* diag;                       // diagnostics: per pair (lo, hi), item 0 only, no binning
+};
+
+template <int TN, int MAXM, bool SEG, bool AUG> struct Geo3 {
+    static constexpr int BR = TN / 2;                           // B rows per CTA
+    static constexpr int A_PL = AR * KS;                        // 8 KB per plane
+    static constexpr int B_PL = BR * KS;
+    static constexpr int STAGE = 3 * (A_PL + B_PL);             // 36 KB (TN 128)
+    static constexpr int NEPI = AUG ? 8 : 12;
+    static constexpr int NET = 32 * NEPI;
+    static constexpr int NTHR = 64 + NET;
+    // per-thread histograms [bin][thread] of u32 cells (bank = thread): with column segments byte l
+    // counts local segment l (a thread's <= 64 columns of a tile meet <= 4 segments of >= 21
+    // columns); three-phase without segments: byte k counts kind k; with segments one array per kind
+    static constexpr int NLOC = SEG ? 4 : 1;
+    static constexpr int NHA = (AUG && SEG) ? 3 : 1;
+    static constexpr int HIST = NHA * (MAXM + 1) * NET * 4;
+    static constexpr int NPHM = AUG ? 3 : 1;
+    static constexpr int COLB = NPHM * TN * 20;                 // float4 (sigma, n, alpha, beta) + r
+    static constexpr int THRB = 3 * 2 * 2 * MAXM * 4;           // [kind][rd/ru][2 MAXM]
+    static constexpr int FIXED = 1024 + 1024 + COLB + THRB + HIST;
+    static constexpr int FIT = (227 * 1024 - FIXED) / STAGE;
+    static constexpr int STAGES = FIT > 6 ? 6 : FIT;
+    static constexpr int SMEM = STAGES * STAGE + FIXED;
+    static constexpr int TCOLS = 4 * TN <= 256 ? 256 : 512;
+    static_assert(FIT >= 2, "shared memory");
+};
+
+// K-major SWIZZLE_64B shared-memory matrix descriptor (sm_100 version 1): start >> 4, LBO 1 (unused),
+// SBO = 512 B between 8-row core groups, layout type 4 (SWIZZLE_64B) at bits [61, 64).
+__device__ __forceinline__ uint64_t sdesc64(uint32_t saddr) {
+    return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(512 >> 4) << 32) |
+           ((uint64_t)1 << 46) | ((uint64_t)4 << 61);
+}
+__host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
+    return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+__device__ __forceinline__ void mma_i8(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+    asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                 "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+                 "l"(a), "l"(b), "r"(id), "r"(acc));
+}
+// 3-D TMA box (64 K-bytes x rows x 3 digit planes); both CTAs of the pair signal the leader's barrier
+__device__ __forceinline__ void tma3(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes "
+        "[%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(x), "r"(y), "r"(0), "r"(smem_u32(bar) & 0xFEFFFFFFu)
+        : "memory");
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+        "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+        "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+        : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// Tile enumeration.  With skipping, the active tiles of tile row mt are a suffix [start, tiles_n):
+//   skip 1 (symmetric bin matrix, mirrored writes): the tiles holding a column >= the row tile's first row;
+//   skip 2 (Alg. 1: blocks k < l only): the first tile whose last column lies in a later column
+//          segment than the row tile's first row.
+__host__ __device__ inline int row_start(int skip, int mt, int64_t row_seg, int64_t col_seg, int64_t rowsB, int tn) {
+    if (skip == 1) return (int)((int64_t)mt * TILE_M / tn);
+    const int64_t k0 = (int64_t)mt * TILE_M / row_seg;
+    const int64_t need = (k0 + 1) * col_seg;
+    if (need > rowsB - 1) return 1 << 30;
+    return (int)(need / tn);
+}
+__host__ __device__ inline int tiles_active(int skip, int tiles_m, int tiles_n, int64_t row_seg, int64_t col_seg,
+                                            int64_t rowsB, int tn) {
+    if (skip == 0) return tiles_m * tiles_n;
+    int n = 0;
+    for (int mt = 0; mt < tiles_m; ++mt) {
+        const int s = row_start(skip, mt, row_seg, col_seg, rowsB, tn);
+        if (s < tiles_n) n += tiles_n - s;
+    }
+    return n;
+}
+__device__ __forceinline__ void tile_of(const Params& prm, int u, int& mt, int& nt) {
+    if (prm.skip == 0) { mt = u / prm.tiles_n; nt = u % prm.tiles_n; return; }
+    for (mt = 0; mt < prm.tiles_m; ++mt) {
+        const int s = row_start(prm.skip, mt, prm.sp.row_seg, prm.sp.col_seg, prm.rowsB, prm.tn);
+        const int c = s < prm.tiles_n ? prm.tiles_n - s : 0;
+        if (u < c) { nt = s + u; return; }
+        u -= c;
+    }
+    mt = nt = 0;
+}
+
+// b = #{m : v < T_m} over decreasing thresholds T[0..MAXM) padded with -inf to 2 MAXM
+template <int MAXM>
+__device__ __forceinline__ int bin_search(float v, const float* T) {
+    int b = 0;
+#pragma unroll
+    for (int s = MAXM; s >= 1; s >>= 1)
+        if (v < T[b + s - 1]) b += s;
+    return b;
+}
+
+// Row metadata of one phase
+struct RowV {
+    float n, s, r, al, be;
+};
+__device__ __forceinline__ RowV row_meta(const float* meta, int64_t row, int nph, int ph) {
+    const float4 v = __ldg(reinterpret_cast<const float4*>(meta + (row * nph + ph) * 8));
+    const float r = __ldg(meta + (row * nph + ph) * 8 + 4);
+    RowV o;
+    o.n = v.x; o.s = v.y; o.r = v.z; o.al = v.w; o.be = r;
+    return o;
+}
+
+// Interval [dn, up] of the distance of one pair (see the header).  g = G' / 2^32 (FP32).
+// Every operation is symmetric in (a, b), so d(i, j) and d(j, i) give bit-identical intervals.
+__device__ __forceinline__ void pair_interval(float g, const RowV& A, float sb, float nb, float alb, float beb,
+                                              float rb, float rel, float& lo2, float& hi2, float& rho) {
+    const float nn = A.n + nb;
+    const float d2 = fmaf(A.s * sb * -8589934592.f, g, nn);           // -2^33 sigma_a sigma_b G'/2^32
+    const float x = __fadd_ru(__fmul_ru(A.al, beb), __fmul_ru(A.be, alb));
+    const float z = __fmaf_ru(A.al, alb, x);
+    const float delta = __fmaf_ru(2.f, z, __fmul_ru(rel, nn));
+    hi2 = __fadd_ru(d2, delta);
+    lo2 = __fsub_rd(d2, delta);
+    rho = __fadd_ru(A.r, rb);
+}
+
+// Epilogue (all modes).  One tile at a time: stage the column metadata and thresholds, drain every
+// K segment (chunk partials into TMEM columns [3TN, 4TN); a phase's last chunk -> intervals),
+// bin, list ambiguous pairs, flush the histograms.
+template <int TN, int MAXM, bool SEG, bool AUG>
+__device__ __forceinline__ void epilogue(const Params& prm, uint32_t tmem_base, uint64_t* tfull, uint64_t* tempty,
+                                         float4* s_c4, float* s_cr, float* s_T, uint32_t* hist_s, int cluster_id,
+                                         int n_clusters, int total_tiles, uint32_t rank, int warp, int lane) {
+    using GG = Geo3<TN, MAXM, SEG, AUG>;
+    constexpr int NET = GG::NET;
+    const int quarter = warp & 3;
+    const int ew = warp - 2;
+    const int e0 = (quarter + 2) & 3;
+    const int nwq = (GG::NEPI - e0 + 3) / 4;
+    const int kq = ew >> 2;
+    const int g0 = kq * (TN / 16) / nwq, g1 = (kq + 1) * (TN / 16) / nwq;
+    const int ncol = (g1 - g0) * 16;
+    const int et = threadIdx.x - 64;
+    const int M = prm.M;
+    const int nph = prm.nph;
+    const int64_t npairs = (int64_t)prm.P * prm.rowsA * prm.rowsB;
+    uint32_t* myh = hist_s + et;
+    uint32_t tph = 0;
+    for (int t = cluster_id; t < total_tiles; t += n_clusters) {
+        const int p = prm.p0 + t / prm.tiles_act;
+        int mt, nt;
+        tile_of(prm, t % prm.tiles_act, mt, nt);
+        const int64_t col0 = (int64_t)nt * TN;
+        const int64_t browbase = prm.b_off + (int64_t)p * prm.rowsB;
+        named_bar(1, NET);
+        for (int i = et; i < nph * TN; i += NET) {
+            const int ph = i / TN, c = i % TN;
+            const int64_t j = col0 + c;
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            float r = 0.f;
+            if (j < prm.rowsB) {
+                const RowV b = row_meta(prm.meta, browbase + j, nph, ph);
+                v = make_float4(b.s, b.n, b.al, b.be);
+                r = b.r;
+            }
+            s_c4[ph * TN + c] = v;
+            s_cr[ph * TN + c] = r;
+        }
+        if (et < 2 * MAXM) {
+            // kinds: 0 L2 (R/sqrt(w)), 1 W12 (R^2/w), 2 W12SUM (R/sqrt(w)); [kind][rd, ru][2 MAXM]
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                const bool on = et < M && (AUG ? prm.q_k[k] >= 0 : k == 0);
+                const float* T = prm.thr + (int64_t)p * prm.thr_stride;
+                s_T[(k * 2 + 0) * 2 * MAXM + et] = on ? T[(2 * k) * M + et] : -INFINITY;
+                s_T[(k * 2 + 1) * 2 * MAXM + et] = on ? T[(2 * k + 1) * M + et] : -INFINITY;
+            }
+        }
+        named_bar(1, NET);
+        const int64_t row = (int64_t)mt * TILE_M + rank * AR + quarter * 32 + lane;
+        const bool row_ok = row < prm.rowsA;
+        const int64_t arow = prm.a_off + (int64_t)p * prm.rowsA + (row_ok ? row : 0);
+        const int hc0 = (int)(col0 + g0 * 16);
+        const int nvalid = (int)min((int64_t)ncol, prm.rowsB - hc0);
+        const uint32_t tl = tmem_base + ((uint32_t)(quarter * 32) << 16);
+        const int64_t cs_first = hc0 >= 0 ? (int64_t)hc0 / prm.sp.col_seg : 0;
+        int bnd[GG::NLOC > 1 ? GG::NLOC - 1 : 1];
+#pragma unroll
+        for (int i = 0; i < GG::NLOC - 1; ++i) {
+            const int64_t c = (cs_first + 1 + i) * prm.sp.col_seg - hc0;
+            bnd[i] = SEG ? (int)(c < ncol ? c : (1 << 30)) : (1 << 30);
+        }
+        const bool diag_item = prm.diag != nullptr && p == 0;
+        const bool no_bin = prm.diag != nullptr;
+        // bin-matrix mode: symmetric layouts mirror tiles fully above the diagonal; in the diagonal
+        // band both orders are computed here and the re-check list takes col >= row only
+        const bool sym_up = prm.skip == 1 && (int64_t)(mt + 1) * TILE_M <= (int64_t)nt * TN;
+        const bool sym_band = prm.skip == 1 && !sym_up;
+        const int64_t pbase = (int64_t)p * prm.rowsA * prm.rowsB + (row_ok ? row : 0) * prm.rowsB;
+        RowV A = row_meta(prm.meta, arow, nph, 0);
+
+        for (int s = 0; s < prm.nseg; ++s) {
+            const int ph = prm.seg_ph[s];
+            const bool first = prm.seg_first[s], last = prm.seg_last[s], emp = prm.seg_empty[s];
+            if (AUG && first && ph > 0) A = row_meta(prm.meta, arow, nph, ph);
+            mbar_wait(&tfull[0], tph);
+            fence_after();
+#pragma unroll 1
+            for (int gi = 0; gi < g1 - g0; ++gi) {
+                if (gi * 16 >= nvalid) break;                       // warp-uniform
+                const int tcol = (g0 + gi) * 16;
+                float gv[16];
+                if (emp) {
+#pragma unroll
+                    for (int jj = 0; jj < 16; ++jj) gv[jj] = 0.f;
+                } else {
+                    uint32_t v32[16], v24[16], v16[16];
+                    tmem_ld16(tl + tcol, v32);
+                    tmem_ld16(tl + TN + tcol, v24);
+                    tmem_ld16(tl + 2 * TN + tcol, v16);
+#pragma unroll
+                    for (int jj = 0; jj < 16; ++jj)
+                        gv[jj] = fmaf((float)(int)v16[jj], 1.52587890625e-05f,
+                                      fmaf((float)(int)v24[jj], 0.00390625f, (float)(int)v32[jj]));
+                    if (!first) {
+                        uint32_t vr[16];
+                        tmem_ld16(tl + 3 * TN + tcol, vr);
+#pragma unroll
+                        for (int jj = 0; jj < 16; ++jj) gv[jj] += __uint_as_float(vr[jj]);
+                    }
+                }
+                if (!last) {                                        // a chunk of a longer phase: keep the partial
+                    uint32_t vr[16];
+#pragma unroll
+                    for (int jj = 0; jj < 16; ++jj) vr[jj] = __float_as_uint(gv[jj]);
+                    tmem_st16(tl + 3 * TN + tcol, vr);
+                    continue;
+                }
+                if (!row_ok) continue;
+                const float4* c4 = s_c4 + ph * TN;
+                const float* cr = s_cr + ph * TN;
+                if (!AUG) {
+                    // ---- one phase: the L2 distance; bin on the upper end, list if a radius is inside
+                    const float* Tlo = s_T;                      // kind 0, rounded down
+                    const float* Thi = s_T + 2 * MAXM;           // kind 0, rounded up
+                    int bins[16];
+                    uint32_t amb = 0;
+#pragma unroll
+                    for (int jj = 0; jj < 16; ++jj) {
+                        const int jc = tcol + jj;
+                        const float4 cb = c4[jc];
+                        float lo2, hi2, rho;
+                        pair_interval(gv[jj], A, cb.x, cb.y, cb.z, cb.w, cr[jc], prm.rel, lo2, hi2, rho);
+                        const float up = __fadd_ru(__fsqrt_ru(fmaxf(hi2, 0.f)), rho);
+                        if (diag_item) {
+                            if (gi * 16 + jj < nvalid) {
+                                const float dn = fmaxf(__fsub_rd(__fsqrt_rd(fmaxf(lo2, 0.f)), rho), 0.f);
+                                float* dg = prm.diag + ((int64_t)row * prm.rowsB + hc0 + gi * 16 + jj) * 2;
+                                dg[0] = dn;
+                                dg[1] = up;
+                            }
+                            continue;
+                        }
+                        const int b = bin_search<MAXM>(up, Tlo);
+                        // a radius R_b possibly above d: d >= sqrt(lo2) - rho, so d < R_b is possible iff
+                        // sqrt(lo2) < R_b + rho  <=>  lo2 < (R_b + rho)^2
+                        const float u = __fadd_ru(Thi[b], rho);
+                        const bool a = u > 0.f && lo2 < __fmul_ru(u, u);
+                        int lcs = 0;
+                        if (SEG) {
+#pragma unroll
+                            for (int i = 0; i < GG::NLOC - 1; ++i) lcs += (gi * 16 + jj >= bnd[i]) ? 1 : 0;
+                        }
+                        bins[jj] = b | (lcs << 8);
+                        amb |= (a && gi * 16 + jj < nvalid) ? (1u << jj) : 0u;
+                    }
+                    if (no_bin) continue;
+                    if (prm.binout != nullptr) {
+                        const int64_t mb = ((int64_t)p * prm.nq + prm.q_l2) * prm.rowsA * prm.rowsB;
+#pragma unroll
+                        for (int jj = 0; jj < 16; ++jj) {
+                            if (gi * 16 + jj >= nvalid) break;
+                            const int64_t col = hc0 + gi * 16 + jj;
+                            const uint8_t bv = (uint8_t)(bins[jj] & 255);
+                            if (prm.bin_t) prm.binout[mb + col * prm.rowsA + row] = bv;
+                            else prm.binout[mb + row * prm.rowsB + col] = bv;
+                            if (sym_up) prm.binout[mb + col * prm.rowsB + row] = bv;
+                        }
+                    } else {
+#pragma unroll
+                        for (int jj = 0; jj < 16; ++jj)
+                            if (gi * 16 + jj < nvalid)
+                                atomicAdd(myh + (bins[jj] & 255) * NET, SEG ? 1u << ((bins[jj] >> 5) & 24) : 1u);
+                    }
+                    if (amb) {
+#pragma unroll
+                        for (int jj = 0; jj < 16; ++jj) {
+                            if (!((amb >> jj) & 1u)) continue;
+                            const int64_t col = hc0 + gi * 16 + jj;
+                            if (sym_band && col < row) continue;
+                            const uint32_t idx = atomicAdd(prm.ctr, 1u);
+                            if (idx < prm.cap)
+                                prm.list[idx] = make_uint4((uint32_t)p, (uint32_t)row, (uint32_t)col,
+                                                           (uint32_t)(bins[jj] & 255));   // kind 0 (L2)
+                        }
+                    }
+                } else {
+                    // ---- three phases: block intervals; phases 0, 1 parked, phase 2 forms the measures
+#pragma unroll 4
+                    for (int jj = 0; jj < 16; ++jj) {
+                        if (gi * 16 + jj >= nvalid) break;
+                        const int jc = tcol + jj;
+                        const int64_t col = hc0 + gi * 16 + jj;
+                        const float4 cb = c4[jc];
+                        float lo2, hi2, rho;
+                        pair_interval(gv[jj], A, cb.x, cb.y, cb.z, cb.w, cr[jc], prm.rel, lo2, hi2, rho);
+                        const float up = __fadd_ru(__fsqrt_ru(fmaxf(hi2, 0.f)), rho);
+                        const float dn = fmaxf(__fsub_rd(__fsqrt_rd(fmaxf(lo2, 0.f)), rho), 0.f);
+                        const int64_t pi = pbase + col;
+                        if (ph < 2) {
+                            prm.part[ph * npairs + pi] = make_float2(dn, up);
+                            continue;
+                        }
+                        const float2 p0 = prm.part[pi], p1 = prm.part[npairs + pi];
+                        int lcs = 0;
+                        if (SEG) {
+#pragma unroll
+                            for (int i = 0; i < GG::NLOC - 1; ++i) lcs += (gi * 16 + jj >= bnd[i]) ? 1 : 0;
+                        }
+#pragma unroll
+                        for (int k = 0; k < 3; ++k) {
+                            if (prm.q_k[k] < 0) continue;
+                            float vlo, vhi;
+                            if (k == 0) {                        // L2 / sqrt(w) = d_0
+                                vlo = p0.x; vhi = p0.y;
+                            } else if (k == 1) {                 // W12^2 / w = d_0^2 + (d_x^2 + d_y^2) / h^2
+                                vlo = __fmaf_rd(__fmaf_rd(p1.x, p1.x, __fmul_rd(dn, dn)), prm.ih2_rd, __fmul_rd(p0.x, p0.x));
+                                vhi = __fmaf_ru(__fmaf_ru(p1.y, p1.y, __fmul_ru(up, up)), prm.ih2_ru, __fmul_ru(p0.y, p0.y));
+                            } else {                             // W12SUM / sqrt(w) = d_0 + (d_x + d_y) / h
+                                vlo = __fmaf_rd(__fadd_rd(p1.x, dn), prm.ih_rd, p0.x);
+                                vhi = __fmaf_ru(__fadd_ru(p1.y, up), prm.ih_ru, p0.y);
+                            }
+                            if (diag_item) {
+                                float* dg = prm.diag + (((int64_t)k * prm.rowsA + row) * prm.rowsB + col) * 2;
+                                dg[0] = vlo;
+                                dg[1] = vhi;
+                                continue;
+                            }
+                            if (no_bin) continue;
+                            const float* Tlo = s_T + (k * 2) * 2 * MAXM;
+                            const float* Thi = s_T + (k * 2 + 1) * 2 * MAXM;
+                            const int b = bin_search<MAXM>(vhi, Tlo);
+                            if (prm.binout != nullptr) {
+                                uint8_t* bm = prm.binout + ((int64_t)p * prm.nq + prm.q_k[k]) * prm.rowsA * prm.rowsB;
+                                bm[row * prm.rowsB + col] = (uint8_t)b;
+                                if (sym_up) bm[col * prm.rowsB + row] = (uint8_t)b;
+                                if (sym_band && col < row) continue;
+                            } else if (SEG) {
+                                atomicAdd(myh + (k * (MAXM + 1) + b) * NET, 1u << (8 * lcs));
+                            } else {
+                                atomicAdd(myh + b * NET, 1u << (8 * k));
+                            }
+                            if (vlo < Thi[b]) {
+                                const uint32_t idx = atomicAdd(prm.ctr, 1u);
+                                // measure ids (bit order): L2 0, W12SUM 2, W12 3
+                                const uint32_t kind = k == 0 ? 0u : k == 1 ? 3u : 2u;
+                                if (idx < prm.cap)
+                                    prm.list[idx] = make_uint4((uint32_t)p, (uint32_t)row, (uint32_t)col,
+                                                               (uint32_t)b | (kind << 8));
+                            }
+                        }
+                    }
+                }
+            }
+            if (!last) tmem_wait_st();
+            fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_remote(&tempty[0], 0);
+            tph ^= 1;
+        }
+        if (prm.binout != nullptr || no_bin) continue;
+        // ---- flush the per-thread histograms (warp sums -> global u64 atomics) and reset them
+        const int64_t rs = row_ok ? row / prm.sp.row_seg : 0;
+        const int64_t rs0 = __shfl_sync(0xffffffffu, rs, 0);
+        const bool uniform = __all_sync(0xffffffffu, rs == rs0 || !row_ok);
+        for (int bb = 0; bb <= M; ++bb) {
+#pragma unroll
+            for (int k = 0; k < (AUG ? 3 : 1); ++k) {
+                uint32_t* cp = (AUG && SEG) ? myh + (k * (MAXM + 1) + bb) * NET : myh + bb * NET;
+                const uint32_t cell = *cp;
+                if ((AUG && SEG) || k == (AUG ? 2 : 0)) *cp = 0u;
+                const int q = AUG ? prm.q_k[k] : prm.q_l2;
+                if (bb == 0 || q < 0) continue;                  // bin 0 (outside every radius) is not kept
+#pragma unroll
+                for (int l = 0; l < GG::NLOC; ++l) {
+                    const int64_t cs = cs_first + l;
+                    if (cs * prm.sp.col_seg >= prm.rowsB || cs * prm.sp.col_seg >= hc0 + ncol) break;
+                    const uint32_t v = SEG ? ((cell >> (8 * l)) & 255u) : (AUG ? ((cell >> (8 * k)) & 255u) : cell);
+                    if (uniform) {
+                        const uint32_t tot = __reduce_add_sync(0xffffffffu, v);
+                        if (lane == 0 && tot)
+                            atomicAdd(&prm.hist[hist_index(prm.sp, prm.nq, M, p, rs0, cs, q, bb)],
+                                      (unsigned long long)tot);
+                    } else if (v) {
+                        atomicAdd(&prm.hist[hist_index(prm.sp, prm.nq, M, p, rs, cs, q, bb)], (unsigned long long)v);
+                    }
+                }
+            }
+        }
+    }
+}
+
+template <int TN, int MAXM, bool SEG, bool AUG>
+__global__ void __launch_bounds__(Geo3<TN, MAXM, SEG, AUG>::NTHR, 1)
+k_gram3(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mB, Params prm) {
+    using GG = Geo3<TN, MAXM, SEG, AUG>;
+    constexpr int STAGES = GG::STAGES;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    unsigned char* stages = smem;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * GG::STAGE);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tfull = empty + STAGES;
+    uint64_t* tempty = tfull + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+    float4* s_c4 = reinterpret_cast<float4*>(smem + STAGES * GG::STAGE + 1024);
+    float* s_cr = reinterpret_cast<float*>(s_c4 + GG::NPHM * TN);
+    float* s_T = s_cr + GG::NPHM * TN;
+    uint32_t* hist_s = reinterpret_cast<uint32_t*>(s_T + 3 * 2 * 2 * MAXM);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_rank();
+    const int cluster_id = blockIdx.x / 2, n_clusters = gridDim.x / 2;
+    const int total_tiles = prm.np * prm.tiles_act;
+    const int n_kb = prm.seg_end[prm.nseg - 1];
+
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+        mbar_init(&tfull[0], 1);
+        mbar_init(&tempty[0], 2 * GG::NEPI);                 // epilogue warps x 2 CTAs
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&mA) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&mB) : "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(GG::TCOLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+    if (warp >= 2)
+        for (int i = threadIdx.x - 64; i < GG::HIST / 4; i += GG::NET) hist_s[i] = 0u;
+    fence_before();
+    cluster_sync();
+    fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = cluster_id; t < total_tiles; t += n_clusters) {
+                const int p = prm.p0 + t / prm.tiles_act;
+                int mt, nt;
+                tile_of(prm, t % prm.tiles_act, mt, nt);
+                const int ya = (int)(prm.a_off + p * prm.rowsA + (int64_t)mt * TILE_M + rank * AR);
+                const int yb = (int)(prm.b_off + p * prm.rowsB + (int64_t)nt * TN + rank * GG::BR);
+                for (int kb = 0; kb < n_kb; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    unsigned char* st = stages + stage * GG::STAGE;
+                    if (rank == 0) mbar_expect_tx(&full[stage], 2 * GG::STAGE);
+                    tma3(st, &mA, &full[stage], kb * KS, ya);
+                    tma3(st + 3 * GG::A_PL, &mB, &full[stage], kb * KS, yb);
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0 && rank == 0) {
+            const uint32_t id = idesc_i8(TILE_M, TN);
+            const uint32_t d32 = tmem_base, d24 = tmem_base + TN, d16 = tmem_base + 2 * TN;
+            int stage = 0;
+            uint32_t phase = 0, tph = 0;
+            for (int t = cluster_id; t < total_tiles; t += n_clusters) {
+                for (int s = 0; s < prm.nseg; ++s) {
+                    mbar_wait_cluster(&tempty[0], tph ^ 1);
+                    fence_after();
+                    const int kb0 = s ? prm.seg_end[s - 1] : 0, kb1 = prm.seg_end[s];
+                    for (int kb = kb0; kb < kb1; ++kb) {
+                        mbar_wait(&full[stage], phase);
+                        fence_after();
+                        const uint32_t sa = smem_u32(stages + stage * GG::STAGE);
+                        const uint32_t sb = sa + 3 * GG::A_PL;
+                        const uint64_t ah = sdesc64(sa), am = sdesc64(sa + GG::A_PL), al = sdesc64(sa + 2 * GG::A_PL);
+                        const uint64_t bh = sdesc64(sb), bm = sdesc64(sb + GG::B_PL), bl = sdesc64(sb + 2 * GG::B_PL);
+#pragma unroll
+                        for (int k = 0; k < KS / 32; ++k) {          // 32 int8 of K per MMA
+                            const uint64_t adv = (uint64_t)(k * 2);  // +32 B in the start-address field
+                            const uint32_t acc = (kb != kb0 || k != 0) ? 1u : 0u;
+                            mma_i8(d32, ah + adv, bh + adv, id, acc);
+                            mma_i8(d24, ah + adv, bm + adv, id, acc);
+                            mma_i8(d24, am + adv, bh + adv, id, 1u);
+                            mma_i8(d16, ah + adv, bl + adv, id, acc);
+                            mma_i8(d16, am + adv, bm + adv, id, 1u);
+                            mma_i8(d16, al + adv, bh + adv, id, 1u);
+                        }
+                        tc::mma_commit<2>(&empty[stage]);
+                        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                    }
+                    tc::mma_commit<2>(&tfull[0]);
+                    tph ^= 1;
+                }
+            }
+        }
+    } else {
+        epilogue<TN, MAXM, SEG, AUG>(prm, tmem_base, tfull, tempty, s_c4, s_cr, s_T, hist_s, cluster_id, n_clusters,
+                                     total_tiles, rank, warp, lane);
+    }
+    __syncthreads();
+    cluster_sync();
+    if (warp == 1) {
+        fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(GG::TCOLS));
+    }
+}
+
+// ------------------------------------------------------------------------------------ pack
+// Quantisation constant: |q| <= Q (1 + 2^-22) < 2^22 (the magic-constant rint is exact) and
+// (q + 128) >> 8 in [-16250, 16250], so h = (t1 + 128) >> 8 in [-63, 63].
+constexpr float kQ = 4160000.f;
+// Rows whose centred maximum lies outside [2^-38, 2^40] would under/overflow FP32 in the epilogue;
+// they are packed as exact-only (r = +inf: every pair of theirs goes to the FP64 re-check).
+constexpr float kMinMax = 3.637978807091713e-12f, kMaxMax = 1.099511627776e12f;
+
+__device__ __forceinline__ uint32_t pack4(int a, int b, int c, int d) {
+    return (uint32_t)(a & 255) | ((uint32_t)(b & 255) << 8) | ((uint32_t)(c & 255) << 16) | ((uint32_t)d << 24);
+}
+
+// Quantise 4 values: digit words (h, m, l bytes), residual sum of squares, exact digit dot products
+// S[0..5] = (hh, hm, hl, mm, ml, ll) via dp4a.
+__device__ __forceinline__ void quant4(const float4 t, float sg, float inv, uint32_t& wh, uint32_t& wm, uint32_t& wl,
+                                       float& e2, int (&S)[6]) {
+    const float tv[4] = {t.x, t.y, t.z, t.w};
+    int hh[4], mm[4], ll[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const float rr = fmaf(tv[i], inv, 12582912.f);
+        const int q = __float_as_int(rr) - 0x4B400000;
+        const float qf = rr - 12582912.f;
+        const float e = fmaf(-sg, qf, tv[i]);                 // x~ - sigma q, one rounding
+        e2 = fmaf(e, e, e2);
+        const int t1 = (q + 128) >> 8;
+        const int h = (t1 + 128) >> 8;
+        ll[i] = q - (t1 << 8);
+        mm[i] = t1 - (h << 8);
+        hh[i] = h;
+    }
+    wh = pack4(hh[0], hh[1], hh[2], hh[3]);
+    wm = pack4(mm[0], mm[1], mm[2], mm[3]);
+    wl = pack4(ll[0], ll[1], ll[2], ll[3]);
+    S[0] = __dp4a((int)wh, (int)wh, S[0]);
+    S[1] = __dp4a((int)wh, (int)wm, S[1]);
+    S[2] = __dp4a((int)wh, (int)wl, S[2]);
+    S[3] = __dp4a((int)wm, (int)wm, S[3]);
+    S[4] = __dp4a((int)wm, (int)wl, S[4]);
+    S[5] = __dp4a((int)wl, (int)wl, S[5]);
+}
+
+// Row metadata from the block sums (one thread).  cnt = elements of the block; tn2 = |x~|^2 of the
+// FP32 values the block was formed from (bounds the FP32 rounding of the block values, see below).
+__device__ __forceinline__ void write_meta(float* out, float sg, const long long (&S)[6], double e2, double slack_norm2,
+                                           bool exact_only) {
+    // sum q^2 = 2^32 hh + 2^25 hm + 2^17 hl + 2^16 mm + 2^9 ml + ll, exactly
+    const long long Q = S[0] * (1ll << 32) + S[1] * (1ll << 25) + S[2] * (1ll << 17) + S[3] * (1ll << 16) +
+                        S[4] * (1ll << 9) + S[5];
+    const double s = (double)sg;
+    const double n = (double)Q * s * s;
+    // residual: |e'| from FP32 sums of <= 2048 terms per thread (relative error < 2^-12 on e2, which
+    // also covers the rounding of each e'), plus the FP32 rounding of the block values relative to the
+    // exact (x - c) ones, <= 2^-24 (1 + 2^-23) per unit of slack_norm (counted twice for safety)
+    const double r = sqrt(e2 * (1.0 + 1.0 / 4096.0)) * (1.0 + 1e-12) + sqrt(slack_norm2) * (1.0 + 1e-6) * 1.2e-7;
+    out[0] = (float)n;
+    out[1] = sg;
+    out[2] = exact_only ? INFINITY : __double2float_ru(r);
+    out[3] = __double2float_ru(s * sqrt((double)S[5]) * (1.0 + 1e-12));
+    out[4] = __double2float_ru(256.0 * s * sqrt((double)S[3]) * (1.0 + 1e-12));
+    out[5] = 0.f; out[6] = 0.f; out[7] = 0.f;
+}
+
+// One CTA per row, the whole row in registers (NV float4 per thread, NT threads): x~ = x - c, max,
+// quantise, store the three digit planes, exact digit sums, residual.
+template <int NV, int NT>
+__global__ void __launch_bounds__(NT) k_pack3(RowSrc src, int64_t rows, int64_t K, int64_t Kp, const float* __restrict__ center,
+                                              int8_t* __restrict__ planes, int64_t plane_stride, int64_t row0,
+                                              float* __restrict__ meta, int32_t* __restrict__ status) {
+    const int64_t p = blockIdx.y;
+    const int64_t r = blockIdx.x;
+    const float* x = row_ptr(src, p, r);
+    const float* c = center + p * Kp;
+    const int64_t orow = row0 + p * rows + r;
+    __shared__ float red[NT / 32];
+    __shared__ double redd[NT / 32][8];
+    float4 v[NV];
+    float mx = 0.f, nfa = 0.f;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+        const int64_t k = ((int64_t)i * NT + threadIdx.x) * 4;
+        if (k < K) {
+            const float4 xv = __ldg(reinterpret_cast<const float4*>(x + k));
+            const float4 cv = __ldg(reinterpret_cast<const float4*>(c + k));
+            nfa = fmaf(xv.x, 0.f, fmaf(xv.y, 0.f, fmaf(xv.z, 0.f, fmaf(xv.w, 0.f, nfa))));
+            v[i] = make_float4(xv.x - cv.x, xv.y - cv.y, xv.z - cv.z, xv.w - cv.w);
+        } else {
+            v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v[i].x), fabsf(v[i].y)), fmaxf(fabsf(v[i].z), fabsf(v[i].w))));
+    }
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
+    const bool anynf = __syncthreads_or(nfa != nfa);
+    if (ln == 0) red[w] = mx;
+    __syncthreads();
+    mx = 0.f;
+#pragma unroll
+    for (int i = 0; i < NT / 32; ++i) mx = fmaxf(mx, red[i]);
+    const bool exact_only = mx > 0.f && !(mx >= kMinMax && mx <= kMaxMax);
+    const float sg = (mx >= kMinMax && mx <= kMaxMax) ? mx / kQ : 1.f;
+    const float inv = 1.f / sg;
+    int S[6] = {0, 0, 0, 0, 0, 0};
+    float e2 = 0.f, t2 = 0.f;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+        const int64_t k = ((int64_t)i * NT + threadIdx.x) * 4;
+        if (k >= Kp) continue;
+        uint32_t wh = 0, wm = 0, wl = 0;
+        if (!exact_only) quant4(v[i], sg, inv, wh, wm, wl, e2, S);
+        else e2 = fmaf(v[i].x, v[i].x, fmaf(v[i].y, v[i].y, fmaf(v[i].z, v[i].z, fmaf(v[i].w, v[i].w, e2))));
+        t2 = fmaf(v[i].x, v[i].x, fmaf(v[i].y, v[i].y, fmaf(v[i].z, v[i].z, fmaf(v[i].w, v[i].w, t2))));
+        int8_t* o = planes + orow * Kp + k;
+        *reinterpret_cast<uint32_t*>(o) = wh;
+        *reinterpret_cast<uint32_t*>(o + plane_stride) = wm;
+        *reinterpret_cast<uint32_t*>(o + 2 * plane_stride) = wl;
+    }
+    double acc[8];
+#pragma unroll
+    for (int i = 0; i < 6; ++i) acc[i] = (double)S[i];
+    acc[6] = (double)e2;
+    acc[7] = (double)t2;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+        for (int o = 16; o > 0; o >>= 1) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], o);
+    if (ln == 0)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) redd[w][i] = acc[i];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        long long Sl[6];
+        double e = 0.0, tt = 0.0;
+        for (int i = 0; i < 6; ++i) {
+            double s = 0.0;
+            for (int j = 0; j < NT / 32; ++j) s += redd[j][i];
+            Sl[i] = (long long)s;                               // exact: |sums| < 2^53
+        }
+        for (int j = 0; j < NT / 32; ++j) { e += redd[j][6]; tt += redd[j][7]; }
+        write_meta(meta + orow * 8, sg, Sl, e, tt * (1.0 + 1.0 / 4096.0), exact_only);
+        if (anynf) atomicOr(&status[p], CIL_ITEM_NONFINITE);
+    }
+}
+
+// Rows too long for registers (K > 32768): pass 1 streams the row for max|x~| and the centred
+// norm, pass 2 re-reads it (L2-resident: one row per CTA) to quantise.  Same arithmetic as k_pack3.
+__global__ void __launch_bounds__(1024) k_pack3_2p(RowSrc src, int64_t rows, int64_t K, int64_t Kp,
+                                                   const float* __restrict__ center, int8_t* __restrict__ planes,
+                                                   int64_t plane_stride, int64_t row0, float* __restrict__ meta,
+                                                   int32_t* __restrict__ status) {
+    constexpr int NT = 1024;
+    const int64_t p = blockIdx.y;
+    const int64_t r = blockIdx.x;
+    const float* x = row_ptr(src, p, r);
+    const float* c = center + p * Kp;
+    const int64_t orow = row0 + p * rows + r;
+    __shared__ float red[NT / 32];
+    __shared__ double redd[NT / 32][8];
+    float mx = 0.f, nfa = 0.f;
+    for (int64_t k = (int64_t)threadIdx.x * 4; k < K; k += NT * 4) {
+        const float4 xv = __ldg(reinterpret_cast<const float4*>(x + k));
+        const float4 cv = __ldg(reinterpret_cast<const float4*>(c + k));
+        nfa = fmaf(xv.x, 0.f, fmaf(xv.y, 0.f, fmaf(xv.z, 0.f, fmaf(xv.w, 0.f, nfa))));
+        mx = fmaxf(mx, fmaxf(fmaxf(fabsf(xv.x - cv.x), fabsf(xv.y - cv.y)), fmaxf(fabsf(xv.z - cv.z), fabsf(xv.w - cv.w))));
+    }
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
+    const bool anynf = __syncthreads_or(nfa != nfa);
+    if (ln == 0) red[w] = mx;
+    __syncthreads();
+    mx = 0.f;
+    for (int i = 0; i < NT / 32; ++i) mx = fmaxf(mx, red[i]);
+    const bool exact_only = mx > 0.f && !(mx >= kMinMax && mx <= kMaxMax);
+    const float sg = (mx >= kMinMax && mx <= kMaxMax) ? mx / kQ : 1.f;
+    const float inv = 1.f / sg;
+    int S[6] = {0, 0, 0, 0, 0, 0};
+    long long SL[6] = {0, 0, 0, 0, 0, 0};
+    float e2 = 0.f, t2 = 0.f;
+    int cnt = 0;
+    for (int64_t k = (int64_t)threadIdx.x * 4; k < Kp; k += NT * 4) {
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (k < K) {
+            const float4 xv = __ldg(reinterpret_cast<const float4*>(x + k));
+            const float4 cv = __ldg(reinterpret_cast<const float4*>(c + k));
+            v = make_float4(xv.x - cv.x, xv.y - cv.y, xv.z - cv.z, xv.w - cv.w);
+        }
+        uint32_t wh = 0, wm = 0, wl = 0;
+        if (!exact_only) quant4(v, sg, inv, wh, wm, wl, e2, S);
+        else e2 = fmaf(v.x, v.x, fmaf(v.y, v.y, fmaf(v.z, v.z, fmaf(v.w, v.w, e2))));
+        t2 = fmaf(v.x, v.x, fmaf(v.y, v.y, fmaf(v.z, v.z, fmaf(v.w, v.w, t2))));
+        int8_t* o = planes + orow * Kp + k;
+        *reinterpret_cast<uint32_t*>(o) = wh;
+        *reinterpret_cast<uint32_t*>(o + plane_stride) = wm;
+        *reinterpret_cast<uint32_t*>(o + 2 * plane_stride) = wl;
+        if (++cnt == 64) {                                  // keep the int32 digit sums far from overflow
+            for (int i = 0; i < 6; ++i) { SL[i] += S[i]; S[i] = 0; }
+            cnt = 0;
+        }
+    }
+    double acc[8];
+    for (int i = 0; i < 6; ++i) acc[i] = (double)(SL[i] + S[i]);
+    acc[6] = (double)e2;
+    acc[7] = (double)t2;
+    for (int i = 0; i < 8; ++i)
+        for (int o = 16; o > 0; o >>= 1) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], o);
+    if (ln == 0)
+        for (int i = 0; i < 8; ++i) redd[w][i] = acc[i];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        long long Sl[6];
+        double e = 0.0, tt = 0.0;
+        for (int i = 0; i < 6; ++i) {
+            double s = 0.0;
+            for (int j = 0; j < NT / 32; ++j) s += redd[j][i];
+            Sl[i] = (long long)s;
+        }
+        for (int j = 0; j < NT / 32; ++j) { e += redd[j][6]; tt += redd[j][7]; }
+        write_meta(meta + orow * 8, sg, Sl, e, tt * (1.0 + 1.0 / 4096.0), exact_only);
+        if (anynf) atomicOr(&status[p], CIL_ITEM_NONFINITE);
+    }
+}
+
+// Three-phase pack: row x~ = x - c expanded into the blocks value x~ (K), D_x x~ = x~[s][r][c+1] -
+// x~[s][r][c] (S H (W-1)) and D_y x~ = x~[s][r+1][c] - x~[s][r][c] (S (H-1) W) (forward differences,
+// last node omitted, reading R3; raw differences, 1/h applied to the distances; species masked by
+// g.gs get 0 derivatives, reading R18), each quantised with its own scale into the three planes at
+// columns kp[a] + idx.  Residual bound of a derivative block: the FP32 difference of FP32-centred
+// values deviates from the exact (x - c) difference by <= 2^-24 (|D x~| + |x~_1| + |x~_0|) per
+// element, hence the slack norm |D x~| + 2 |x~|.
+__global__ void __launch_bounds__(256) k_pack3_aug(RowSrc src, int64_t rows, AugGeom g, int64_t kp0, int64_t kp1,
+                                                   int64_t kp2, int64_t kp3, const float* __restrict__ center,
+                                                   int64_t Kc, int8_t* __restrict__ planes, int64_t plane_stride,
+                                                   int64_t Krow, int64_t row0, float* __restrict__ meta,
+                                                   int32_t* __restrict__ status) {
+    const int64_t p = blockIdx.y;
+    const int64_t r = blockIdx.x;
+    const float* x = row_ptr(src, p, r);
+    const float* c = center + p * Kc;
+    const int64_t orow = row0 + p * rows + r;
+    const int W = g.W, H = g.H, SH = g.S * g.H;
+    __shared__ float red[3][8];
+    __shared__ double redd[8][3][8];
+    const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
+    auto xt = [&](int64_t e) -> float { return __ldg(x + e) - __ldg(c + e); };
+    float m0 = 0.f, mx = 0.f, my = 0.f, nfa = 0.f;
+    for (int sr = w; sr < SH; sr += 8) {
+        const bool grad = g.gs == 0 || ((g.gs >> (sr / H)) & 1u);
+        const bool has_dy = grad && (sr % H) + 1 < H;
+        const int64_t base = (int64_t)sr * W;
+        for (int c0 = 0; c0 < W; c0 += 32) {
+            const int col = c0 + ln;
+            const bool in = col < W;
+            const float xv = in ? __ldg(x + base + col) : 0.f;
+            nfa = fmaf(xv, 0.f, nfa);
+            const float xe = in ? xv - __ldg(c + base + col) : 0.f;
+            float xn = __shfl_down_sync(0xffffffffu, xe, 1);
+            if (ln == 31 && col + 1 < W) xn = xt(base + col + 1);
+            m0 = fmaxf(m0, fabsf(xe));
+            if (grad && col + 1 < W) mx = fmaxf(mx, fabsf(xn - xe));
+            if (has_dy && in) my = fmaxf(my, fabsf(xt(base + W + col) - xe));
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        m0 = fmaxf(m0, __shfl_xor_sync(0xffffffffu, m0, o));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        my = fmaxf(my, __shfl_xor_sync(0xffffffffu, my, o));
+    }
+    const bool anynf = __syncthreads_or(nfa != nfa);
+    if (ln == 0) { red[0][w] = m0; red[1][w] = mx; red[2][w] = my; }
+    __syncthreads();
+    float sg[3], inv[3];
+    bool ex[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        float m = 0.f;
+        for (int i = 0; i < 8; ++i) m = fmaxf(m, red[a][i]);
+        const bool ok = m >= kMinMax && m <= kMaxMax;
+        ex[a] = m > 0.f && !ok;
+        sg[a] = ok ? m / kQ : 1.f;
+        inv[a] = 1.f / sg[a];
+    }
+    int8_t* ph = planes + orow * Krow;
+    int S[3][6];
+    float e2[3] = {0.f, 0.f, 0.f}, t2[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int i = 0; i < 6; ++i) S[a][i] = 0;
+    // one value at a time (the block layouts are not 4-aligned); dp4a on the value in byte 0
+    auto put = [&](int a, int64_t col, float v) {
+        int hh = 0, mm = 0, ll = 0;
+        if (!ex[a]) {
+            const float rr = fmaf(v, inv[a], 12582912.f);
+            const int q = __float_as_int(rr) - 0x4B400000;
+            const float e = fmaf(-sg[a], rr - 12582912.f, v);
+            e2[a] = fmaf(e, e, e2[a]);
+            const int t1 = (q + 128) >> 8;
+            hh = (t1 + 128) >> 8;
+            ll = q - (t1 << 8);
+            mm = t1 - (hh << 8);
+            S[a][0] += hh * hh; S[a][1] += hh * mm; S[a][2] += hh * ll;
+            S[a][3] += mm * mm; S[a][4] += mm * ll; S[a][5] += ll * ll;
+        } else {
+            e2[a] = fmaf(v, v, e2[a]);
+        }
+        t2[a] = fmaf(v, v, t2[a]);
+        ph[col] = (int8_t)hh;
+        ph[col + plane_stride] = (int8_t)mm;
+        ph[col + 2 * plane_stride] = (int8_t)ll;
+    };
+    for (int sr = w; sr < SH; sr += 8) {
+        const int s = sr / H;
+        const bool grad = g.gs == 0 || ((g.gs >> s) & 1u);
+        const bool has_dy = (sr % H) + 1 < H;
+        const int64_t base = (int64_t)sr * W;
+        for (int c0 = 0; c0 < W; c0 += 32) {
+            const int col = c0 + ln;
+            const bool in = col < W;
+            const float xe = in ? xt(base + col) : 0.f;
+            float xn = __shfl_down_sync(0xffffffffu, xe, 1);
+            if (ln == 31 && col + 1 < W) xn = xt(base + col + 1);
+            if (!in) continue;
+            put(0, kp0 + base + col, xe);
+            if (col + 1 < W) put(1, kp1 + (int64_t)sr * (W - 1) + col, grad ? xn - xe : 0.f);
+            if (has_dy) put(2, kp2 + base - (int64_t)s * W + col, grad ? xt(base + W + col) - xe : 0.f);
+        }
+    }
+    const int64_t len[3] = {g.K, g.Kx, g.Ky}, beg[3] = {kp0, kp1, kp2}, end[3] = {kp1, kp2, kp3};
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+        for (int64_t col = beg[a] + len[a] + threadIdx.x; col < end[a]; col += 256) {
+            ph[col] = 0; ph[col + plane_stride] = 0; ph[col + 2 * plane_stride] = 0;
+        }
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        double acc[8];
+#pragma unroll
+        for (int i = 0; i < 6; ++i) acc[i] = (double)S[a][i];
+        acc[6] = (double)e2[a];
+        acc[7] = (double)t2[a];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            for (int o = 16; o > 0; o >>= 1) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], o);
+            if (ln == 0) redd[w][a][i] = acc[i];
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < 3) {
+        const int a = threadIdx.x;
+        long long Sl[6];
+        double e = 0.0, tt[3] = {0.0, 0.0, 0.0};
+        for (int i = 0; i < 6; ++i) {
+            double s = 0.0;
+            for (int j = 0; j < 8; ++j) s += redd[j][a][i];
+            Sl[i] = (long long)s;
+        }
+        for (int j = 0; j < 8; ++j) {
+            e += redd[j][a][6];
+            for (int b = 0; b < 3; ++b) tt[b] += redd[j][b][7];
+        }
+        // value block: the FP32 centring error only (|x~|); derivative blocks: |D x~| + 2 |x~|
+        const double slack = a == 0 ? tt[0] : (sqrt(tt[a]) + 2.0 * sqrt(tt[0])) * (sqrt(tt[a]) + 2.0 * sqrt(tt[0]));
+        write_meta(meta + (orow * 3 + a) * 8, sg[a], Sl, e, slack * (1.0 + 1.0 / 4096.0), ex[a]);
+    }
+    if (threadIdx.x == 0 && anynf) atomicOr(&status[p], CIL_ITEM_NONFINITE);
+}
+
+}  // namespace g3
+
+// ------------------------------------------------------------------ host side
+cudaError_t launch_pack3(int P, const RowSrc& src, int64_t rows, int64_t K, int64_t Kp, const float* center,
+                         int8_t* planes, int64_t plane_stride, int64_t row0, float* meta, int32_t* status,
+                         cudaStream_t st) {
+    if (rows == 0) return cudaSuccess;
+    dim3 grid((unsigned)rows, (unsigned)P);
+    ProfScope ps_(K_PACK, st);
+    if (Kp <= 1024)
+        g3::k_pack3<1, 256><<<grid, 256, 0, st>>>(src, rows, K, Kp, center, planes, plane_stride, row0, meta, status);
+    else if (Kp <= 4096)
+        g3::k_pack3<4, 256><<<grid, 256, 0, st>>>(src, rows, K, Kp, center, planes, plane_stride, row0, meta, status);
+    else if (Kp <= 8192)
+        g3::k_pack3<8, 256><<<grid, 256, 0, st>>>(src, rows, K, Kp, center, planes, plane_stride, row0, meta, status);
+    else if (Kp <= 16384)
+        g3::k_pack3<8, 512><<<grid, 512, 0, st>>>(src, rows, K, Kp, center, planes, plane_stride, row0, meta, status);
+    else if (Kp <= 32768)
+        g3::k_pack3<8, 1024><<<grid, 1024, 0, st>>>(src, rows, K, Kp, center, planes, plane_stride, row0, meta, status);
+    else
+        g3::k_pack3_2p<<<grid, 1024, 0, st>>>(src, rows, K, Kp, center, planes, plane_stride, row0, meta, status);
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pack3_aug(int P, const RowSrc& src, int64_t rows, const AugGeom& g, const int64_t* kp,
+                             const float* center, int64_t Kc, int8_t* planes, int64_t plane_stride, int64_t row0,
+                             float* meta, int32_t* status, cudaStream_t st) {
+    if (rows == 0) return cudaSuccess;
+    dim3 grid((unsigned)rows, (unsigned)P);
+    ProfScope ps_(K_PACK, st);
+    g3::k_pack3_aug<<<grid, 256, 0, st>>>(src, rows, g, kp[0], kp[1], kp[2], kp[3], center, Kc, planes, plane_stride,
+                                          kp[3], row0, meta, status);
+    note_launch();
+    return cudaGetLastError();
+}
+
+typedef CUresult (*PFN_encodeTiled_g3)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                       const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                       CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+// 3-D map over the digit planes [3][rows_tot][Kp] (u8): box 64 x box_rows x 3, SWIZZLE_64B
+static bool make_map3(CUtensorMap* m, const void* base, int64_t rows_tot, int64_t Kp, int box_rows) {
+    static PFN_encodeTiled_g3 enc = nullptr;
+    if (!enc) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return false;
+        enc = reinterpret_cast<PFN_encodeTiled_g3>(p);
+    }
+    cuuint64_t dims[3] = {(cuuint64_t)Kp, (cuuint64_t)rows_tot, 3};
+    cuuint64_t strides[2] = {(cuuint64_t)Kp, (cuuint64_t)(rows_tot * Kp)};
+    cuuint32_t box[3] = {(cuuint32_t)g3::KS, (cuuint32_t)box_rows, 3u};
+    cuuint32_t es[3] = {1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(base), dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int TN, int MAXM, bool SEG, bool AUG>
+static cudaError_t launch_g3_t(const g3::Params& prm, const CUtensorMap* maps, int nsm, cudaStream_t st) {
+    using GG = g3::Geo3<TN, MAXM, SEG, AUG>;
+    static SmemAttrOnce attr;
+    if (cudaError_t e = attr.ensure(g3::k_gram3<TN, MAXM, SEG, AUG>, GG::SMEM); e != cudaSuccess) return e;
+    const int64_t tiles = (int64_t)prm.np * prm.tiles_act;
+    const int clusters = (int)(tiles < nsm / 2 ? tiles : nsm / 2);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)(clusters * 2));
+    cfg.blockDim = dim3(GG::NTHR);
+    cfg.dynamicSmemBytes = GG::SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    ProfScope ps_(K_GRAM_TC, st);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, g3::k_gram3<TN, MAXM, SEG, AUG>, maps[0], maps[1], prm);
+    note_launch();
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+}
+
+template <int TN, bool AUG>
+static cudaError_t dispatch_g3(const g3::Params& prm, const CUtensorMap* maps, int nsm, cudaStream_t st, bool seg,
+                               int M) {
+    if (M <= 16) return seg ? launch_g3_t<TN, 16, true, AUG>(prm, maps, nsm, st) : launch_g3_t<TN, 16, false, AUG>(prm, maps, nsm, st);
+    if (M <= 32) return seg ? launch_g3_t<TN, 32, true, AUG>(prm, maps, nsm, st) : launch_g3_t<TN, 32, false, AUG>(prm, maps, nsm, st);
+    if constexpr (AUG) {
+        if (seg) return cudaErrorInvalidValue;              // the host routes these to the CUDA cores
+        return launch_g3_t<TN, 64, false, AUG>(prm, maps, nsm, st);
+    } else {
+        return seg ? launch_g3_t<TN, 64, true, AUG>(prm, maps, nsm, st) : launch_g3_t<TN, 64, false, AUG>(prm, maps, nsm, st);
+    }
+}
+
+cudaError_t launch_gram3(const G3Args& a, cudaStream_t st) {
+    if (a.rowsA == 0 || a.rowsB == 0) return cudaSuccess;
+    if (a.rows_tot >= (1ll << 31) || a.Kp % g3::KS) return cudaErrorInvalidValue;
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const int tn = a.tn_force == 64 ? 64 : 128;
+    if (tn == 64 && (a.skip != 0 || a.nph != 1)) return cudaErrorInvalidValue;
+    CUtensorMap maps[2];
+    if (!make_map3(&maps[0], a.planes, a.rows_tot, a.Kp, g3::AR) || !make_map3(&maps[1], a.planes, a.rows_tot, a.Kp, tn / 2))
+        return cudaErrorInvalidValue;
+    g3::Params prm{};
+    prm.rowsA = a.rowsA; prm.rowsB = a.rowsB; prm.a_off = a.a_off; prm.b_off = a.b_off;
+    prm.P = a.P; prm.p0 = a.p0; prm.np = a.np > 0 ? a.np : a.P - a.p0;
+    prm.tn = tn; prm.skip = a.skip;
+    prm.tiles_m = (int)((a.rowsA + g3::TILE_M - 1) / g3::TILE_M);
+    prm.tiles_n = (int)((a.rowsB + tn - 1) / tn);
+    prm.tiles_act = g3::tiles_active(a.skip, prm.tiles_m, prm.tiles_n, a.sp.row_seg, a.sp.col_seg, a.rowsB, tn);
+    if (prm.tiles_act == 0) return cudaSuccess;
+    // K segments: each phase's k-blocks in chunks of <= 65536 bytes (exact int32 accumulation)
+    prm.nph = a.nph == 3 ? 3 : 1;
+    int ns = 0, max_chunks = 1;
+    for (int ph = 0; ph < prm.nph; ++ph) {
+        const int kb0 = (int)(a.ph_beg[ph] / g3::KS), kb1 = (int)(a.ph_end[ph] / g3::KS);
+        const int per = 65536 / g3::KS;
+        const int nch = kb1 > kb0 ? (kb1 - kb0 + per - 1) / per : 1;
+        max_chunks = std::max(max_chunks, nch);
+        for (int c = 0; c < nch; ++c) {
+            if (ns >= g3::MAXSEG) return cudaErrorInvalidValue;
+            prm.seg_end[ns] = std::min(kb1, kb0 + (c + 1) * per);
+            prm.seg_ph[ns] = (uint8_t)ph;
+            prm.seg_first[ns] = c == 0;
+            prm.seg_last[ns] = c == nch - 1;
+            prm.seg_empty[ns] = kb1 == kb0;
+            ++ns;
+        }
+        if (a.ph_beg[ph] != (ph ? a.ph_end[ph - 1] : 0)) return cudaErrorInvalidValue;   // contiguous phases
+    }
+    prm.nseg = ns;
+    prm.meta = a.meta;
+    prm.thr = a.thr; prm.thr_stride = a.thr_stride;
+    prm.M = a.M; prm.nq = a.nq; prm.q_l2 = a.q_l2;
+    for (int k = 0; k < 3; ++k) prm.q_k[k] = a.q_k[k];
+    prm.sp = a.sp;
+    prm.hist = reinterpret_cast<unsigned long long*>(a.hist);
+    prm.list = a.list; prm.ctr = a.ctr; prm.cap = a.cap;
+    // FP32 evaluation of d~^2 = n_a + n_b - 2 s G': n (1 ulp each), their sum, the sigma product,
+    // the digit combination (3 ulp) and one per chunk partial, the FMA; 16 + chunks ulps covers it
+    prm.rel = (float)ldexp(16.0 + 2.0 * max_chunks, -24);
+    prm.ih_rd = a.ih_rd; prm.ih_ru = a.ih_ru; prm.ih2_rd = a.ih2_rd; prm.ih2_ru = a.ih2_ru;
+    prm.part = reinterpret_cast<float2*>(a.part);
+    prm.binout = a.binout;
+    prm.bin_t = a.bin_t ? 1 : 0;
+    if (a.bin_t && (a.skip != 0 || !a.binout || prm.nph != 1)) return cudaErrorInvalidValue;
+    prm.diag = a.diag;
+    const bool seg = a.sp.col_seg < a.rowsB;
+    if (seg && a.sp.col_seg < 21) return cudaErrorInvalidValue;
+    if (tn == 64) {
+        if (seg) return cudaErrorInvalidValue;
+        if (a.M <= 16) return launch_g3_t<64, 16, false, false>(prm, maps, nsm, st);
+        if (a.M <= 32) return launch_g3_t<64, 32, false, false>(prm, maps, nsm, st);
+        return launch_g3_t<64, 64, false, false>(prm, maps, nsm, st);
+    }
+    if (prm.nph == 3) return dispatch_g3<128, true>(prm, maps, nsm, st, seg, a.M);
+    return dispatch_g3<128, false>(prm, maps, nsm, st, seg, a.M);
+}
+
+}  // namespace cil

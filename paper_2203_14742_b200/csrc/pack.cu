@@ -34,14 +34,21 @@ __global__ void k_prep(int P, int nq, int M, const double* __restrict__ radii, i
         thr[(int64_t)p * nq * M + t] = r;
     }
     if (thr2_l2 != nullptr) {
-        // tensor-core thresholds [p][kind][M] (FP32): kind 0 L2 and kind 1 W12 compare the
-        // unweighted sums of squares with R^2/w, kind 2 W12SUM compares W12SUM/sqrt(w) with R/sqrt(w)
+        // tensor-core thresholds [p][8][M] (FP32), rigorously bracketed for the INT8 engine's interval
+        // tests: row 2k = rounded down, 2k + 1 = rounded up, for kind k = 0: L2 as R / sqrt(w) (the
+        // engine bins the distance of the unweighted sums), 1: W12 as R^2 / w, 2: W12SUM as R / sqrt(w);
+        // row 6: L2 as R^2 / w (nearest; the float split engines)
+        const double sw = sqrt(bp.w);
         for (int q = 0; q < nq; ++q) {
             const int kind = bp.slot[q] == 0 ? 0 : bp.slot[q] == 3 ? 1 : bp.slot[q] == 2 ? 2 : -1;
             if (kind < 0) continue;
             for (int m = threadIdx.x; m < M; m += blockDim.x) {
                 const double r = R[q * M + m];
-                thr2_l2[((int64_t)p * 3 + kind) * M + m] = (float)(kind == 2 ? r / sqrt(bp.w) : r * r / bp.w);
+                const double v = kind == 1 ? r * r / bp.w : r / sw;
+                float* T = thr2_l2 + (int64_t)p * 8 * M;
+                T[(2 * kind) * M + m] = __double2float_rd(v * (1.0 - 1e-15));
+                T[(2 * kind + 1) * M + m] = __double2float_ru(v * (1.0 + 1e-15));
+                if (kind == 0) T[6 * M + m] = (float)(r * r / bp.w);
             }
         }
     }
@@ -61,6 +68,17 @@ cudaError_t launch_prep(int P, int nq, int M, const double* radii, int64_t radii
     }
     ProfScope ps_(K_PREP, st);
     k_prep<<<P, 128, 0, st>>>(P, nq, M, radii, radii_stride, bp, thr, thr2_l2, status, keep_status ? 1 : 0);
+    note_launch();
+    return cudaGetLastError();
+}
+
+// Fill n doubles with v (device-side constants such as dummy radii: no pageable host copy, so the
+// call stays asynchronous and capturable into a CUDA graph).
+__global__ void k_fill_f64(double* p, int n, double v) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) p[i] = v;
+}
+cudaError_t launch_fill_f64(double* p, int n, double v, cudaStream_t st) {
+    k_fill_f64<<<1, 64, 0, st>>>(p, n, v);
     note_launch();
     return cudaGetLastError();
 }
@@ -596,9 +614,13 @@ cudaError_t launch_minmax(int64_t n, const float* X, int64_t ldx, float* Y, int6
 
 // ---------------------------------------------------------------------- aug pack
 // One CTA per panel row: out = [x (K) | D_x x (S*H*(W-1)) | D_y x (S*(H-1)*W)], each
-// region zero-padded to a multiple of kSimtBK, plain FP32 differences.
+// region zero-padded to a multiple of kSimtBK, plain FP32 differences.  rowstat[row] = {max |D_x x|,
+// max |D_y x|, |D_x x|, |D_y x|} of the stored FP32 differences (rounded up): the CUDA-core engine's
+// error bound for the derivative terms needs them (the stored differences are rounded, so the
+// engine's D(a) - D(b) is off the exact D(a - b) by <= 2^-24 (|D a| + |D b|) per element).
 __global__ void __launch_bounds__(256) k_pack_aug(RowSrc src, int64_t rows, AugGeom g,
-                                                  float* __restrict__ out, int32_t* __restrict__ status) {
+                                                  float* __restrict__ out, float* __restrict__ rowstat,
+                                                  int32_t* __restrict__ status) {
     const int64_t p = blockIdx.y;
     const int64_t r = blockIdx.x;
     const float* x = row_ptr(src, p, r);
@@ -614,6 +636,8 @@ __global__ void __launch_bounds__(256) k_pack_aug(RowSrc src, int64_t rows, AugG
     // derivative regions: warp per grid row (s, r), lanes along the columns, no index division
     const int W = g.W, H = g.H, SH = g.S * g.H;
     const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
+    float mxx = 0.f, myy = 0.f;
+    double sxx = 0.0, syy = 0.0;
     if (g.nreg >= 2) {
         for (int sr = w; sr < SH; sr += 8) {
             const int64_t base = (int64_t)sr * W;
@@ -622,23 +646,52 @@ __global__ void __launch_bounds__(256) k_pack_aug(RowSrc src, int64_t rows, AugG
             const bool grad = g.gs == 0 || ((g.gs >> s) & 1u);     // species mask (R18): else 0
             for (int c = ln; c < W; c += 32) {
                 const float xe = __ldg(x + base + c);
-                if (c + 1 < W) o[g.off[1] + (int64_t)sr * (W - 1) + c] = grad ? __ldg(x + base + c + 1) - xe : 0.f;
-                if (has_dy) o[g.off[2] + base - (int64_t)s * W + c] = grad ? __ldg(x + base + W + c) - xe : 0.f;
+                if (c + 1 < W) {
+                    const float dx = grad ? __ldg(x + base + c + 1) - xe : 0.f;
+                    o[g.off[1] + (int64_t)sr * (W - 1) + c] = dx;
+                    mxx = fmaxf(mxx, fabsf(dx));
+                    sxx += (double)dx * (double)dx;
+                }
+                if (has_dy) {
+                    const float dy = grad ? __ldg(x + base + W + c) - xe : 0.f;
+                    o[g.off[2] + base - (int64_t)s * W + c] = dy;
+                    myy = fmaxf(myy, fabsf(dy));
+                    syy += (double)dy * (double)dy;
+                }
             }
         }
         for (int64_t t = g.Kx + threadIdx.x; t < g.off[2] - g.off[1]; t += 256) o[g.off[1] + t] = 0.f;
         if (g.nreg >= 3)
             for (int64_t t = g.Ky + threadIdx.x; t < g.off[3] - g.off[2]; t += 256) o[g.off[2] + t] = 0.f;
     }
+    if (rowstat != nullptr) {
+        __shared__ float smx[2][8];
+        __shared__ double ssx[2][8];
+        for (int off = 16; off > 0; off >>= 1) {
+            mxx = fmaxf(mxx, __shfl_xor_sync(0xffffffffu, mxx, off));
+            myy = fmaxf(myy, __shfl_xor_sync(0xffffffffu, myy, off));
+            sxx += __shfl_xor_sync(0xffffffffu, sxx, off);
+            syy += __shfl_xor_sync(0xffffffffu, syy, off);
+        }
+        if (ln == 0) { smx[0][w] = mxx; smx[1][w] = myy; ssx[0][w] = sxx; ssx[1][w] = syy; }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            float a = 0.f, b = 0.f;
+            double c = 0.0, d = 0.0;
+            for (int i = 0; i < 8; ++i) { a = fmaxf(a, smx[0][i]); b = fmaxf(b, smx[1][i]); c += ssx[0][i]; d += ssx[1][i]; }
+            float4 v = make_float4(a, b, __double2float_ru(sqrt(c) * (1.0 + 1e-12)), __double2float_ru(sqrt(d) * (1.0 + 1e-12)));
+            *reinterpret_cast<float4*>(rowstat + (p * rows + r) * 4) = v;
+        }
+    }
     if (__syncthreads_or(nfa != nfa) && threadIdx.x == 0) atomicOr(&status[p], CIL_ITEM_NONFINITE);
 }
 
-cudaError_t launch_pack_aug(int P, const RowSrc& src, int64_t rows, const AugGeom& g, float* out,
+cudaError_t launch_pack_aug(int P, const RowSrc& src, int64_t rows, const AugGeom& g, float* out, float* rowstat,
                             int32_t* status, cudaStream_t st) {
     if (rows == 0) return cudaSuccess;
     dim3 grid((unsigned)rows, (unsigned)P);
     ProfScope ps_(K_PACK, st);
-    k_pack_aug<<<grid, 256, 0, st>>>(src, rows, g, out, status);
+    k_pack_aug<<<grid, 256, 0, st>>>(src, rows, g, out, rowstat, status);
     note_launch();
     return cudaGetLastError();
 }

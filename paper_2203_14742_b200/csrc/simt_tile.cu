@@ -183,15 +183,33 @@ __global__ void __launch_bounds__(NTHR, (DO_SUM || RI == 8) ? 2 : 4) k_simt(Simt
     }
 
     // ------------------------------------------------------------- epilogue
+    // Measures in FP64 from the region results, each with a rigorous bound E of its error against
+    // the exact FP64 value of the plain definition (u = 2^-24):
+    //  - value region: differences fl(a - b) carry relative error u; the max is then exact up to u
+    //    (rounding is monotone), the FP32 sums of <= 64 squares carry relative error <= 67 u
+    //    (FFMA chains of 64 terms, flushed to FP64), i.e. <= 34 u on a_0 = sqrt(w s_0);
+    //  - derivative regions: the stored differences D a, D b are themselves rounded, so each element
+    //    of D a - D b is within u (|D a| + |D b|) + u |result| of the exact D(a - b): the max moves by
+    //    <= u (max|D a| + max|D b|) + u m, the root of the sum by <= u (|D a| + |D b|) + 35 u sqrt(s)
+    //    (per-row max / norm of the stored differences: statA / statB);
+    //  - the measures combine these monotonically (sums add bounds, max takes the max, the
+    //    Euclidean combination of W12 is 1-Lipschitz in each part).
+    // A pair is binned at the upper end d + E and listed for the FP64 re-check when a radius lies in
+    // (d - E, d + E] (recheck.cu) — the counts are those of the plain definition.
     const double h = a.bp.h, w = a.bp.w, ih = 1.0 / h, ih2 = 1.0 / (h * h);
+    const double U = 5.9604644775390625e-08;            // 2^-24
     const int nreg = a.g.nreg;
 #pragma unroll
     for (int i = 0; i < RI; ++i) {
         const int64_t gi = row0 + ty + 8 * i;
+        float4 sa = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (gi < a.rowsA && nreg > 1) sa = __ldg(reinterpret_cast<const float4*>(a.statA + ((int64_t)p * a.rowsA + gi) * 4));
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             const int64_t gj = col0 + tx + 16 * j;
             if (gi >= a.rowsA || gj >= a.rowsB) continue;
+            float4 sb = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (nreg > 1) sb = __ldg(reinterpret_cast<const float4*>(a.statB + ((int64_t)p * a.rowsB + gj) * 4));
             double s[3] = {0.0, 0.0, 0.0}, m[3] = {0.0, 0.0, 0.0};
 #pragma unroll
             for (int r = 0; r < 3; ++r) {
@@ -201,20 +219,29 @@ __global__ void __launch_bounds__(NTHR, (DO_SUM || RI == 8) ? 2 : 4) k_simt(Simt
                 if (DO_SUM) s[r] = last ? tot[i][j] : rs_sum[e];
                 if (DO_MAX) m[r] = last ? (double)mx[i][j] : (double)rs_max[e];
             }
+            const double sw = sqrt(w);
             const double a0 = sqrt(w * s[0]), ax = sqrt(w * s[1] * ih2), ay = sqrt(w * s[2] * ih2);
             const double m0 = m[0], mxx = m[1] * ih, myy = m[2] * ih;
+            const double ea0 = 34.0 * U * a0;
+            const double eax = sw * ih * (35.0 * U * sqrt(s[1]) + 1.0001 * U * ((double)sa.z + (double)sb.z));
+            const double eay = sw * ih * (35.0 * U * sqrt(s[2]) + 1.0001 * U * ((double)sa.w + (double)sb.w));
+            const double em0 = 1.0001 * U * m0;
+            const double emx = ih * (1.0001 * U * ((double)sa.x + (double)sb.x) + 2.0 * U * m[1]);
+            const double emy = ih * (1.0001 * U * ((double)sa.y + (double)sb.y) + 2.0 * U * m[2]);
             const int64_t rs = gi / a.sp.row_seg, cs = gj / a.sp.col_seg;
             for (int q = 0; q < nq; ++q) {
                 if (!((a.qmask >> q) & 1u)) continue;
-                double d;
-                switch (a.bp.slot[q]) {
-                    case 0: d = a0; break;
-                    case 1: d = m0; break;
-                    case 2: d = a0 + ax + ay; break;
-                    case 3: d = sqrt(a0 * a0 + ax * ax + ay * ay); break;
-                    case 4: d = fmax(m0, fmax(mxx, myy)); break;
-                    default: d = m0 + mxx + myy; break;
+                const int kind = a.bp.slot[q];
+                double d, E;
+                switch (kind) {
+                    case 0: d = a0; E = ea0; break;
+                    case 1: d = m0; E = em0; break;
+                    case 2: d = a0 + ax + ay; E = ea0 + eax + eay; break;
+                    case 3: d = sqrt(a0 * a0 + ax * ax + ay * ay); E = ea0 + eax + eay; break;
+                    case 4: d = fmax(m0, fmax(mxx, myy)); E = fmax(em0, fmax(emx, emy)); break;
+                    default: d = m0 + mxx + myy; E = em0 + emx + emy; break;
                 }
+                E += 1e-14 * d;                  // FP64 evaluation of d and of the bound
                 if (a.range) {               // distance-range mode (adaptive radii)
                     unsigned long long* rg = a.range + ((int64_t)p * nq + q) * 2;
                     if (d > 0.0) atomicMin(&rg[0], (unsigned long long)__double_as_longlong(d));
@@ -222,8 +249,14 @@ __global__ void __launch_bounds__(NTHR, (DO_SUM || RI == 8) ? 2 : 4) k_simt(Simt
                     continue;
                 }
                 const double* T = thr_s + q * M;
+                const double hi = d + E;
                 int b = 0;
-                while (b < M && d < T[b]) ++b;
+                while (b < M && hi < T[b]) ++b;
+                if (b < M && d - E < T[b] && !(SYM && gi > gj)) {
+                    const uint32_t idx = atomicAdd(a.ctr, 1u);
+                    if (idx < a.cap)
+                        a.list[idx] = make_uint4((uint32_t)p, (uint32_t)gi, (uint32_t)gj, (uint32_t)b | ((uint32_t)kind << 8));
+                }
                 if (a.binout) {              // bin-matrix mode (bootstrap, Alg. A1 / A2)
                     a.binout[(((int64_t)p * nq + q) * a.rowsA + gi) * a.rowsB + gj] = (uint8_t)b;
                     // d(i, j) and d(j, i) are bit-identical here (exact negations, same order), so

@@ -166,23 +166,56 @@ def test_translation_invariance_tc(cil):
             assert torch.equal(c, base), (shift, eng)
 
 
-@pytest.mark.parametrize("engine", ["TC_3XBF16", "TC_3XTF32", "TC_I8"])
-@pytest.mark.parametrize("case", ["C2", "C4", "offset", "C1"])
-def test_gram_error_bound(cil, oracle_mod, engine, case):
-    """The tensor-core d^2 error must stay well inside the per-pair bound E that decides
-    which pairs are re-checked exactly (DESIGN.md §6 L2 engine)."""
-    O = oracle_mod
-    dev = torch.device("cuda")
+def _bound_case(case, seed):
+    """(A, B, grid) of the error-bound tests; 'neardup*' are near-duplicate pairs."""
     if case == "C2":
         grid, N, Nt, shift = (2, 64, 64, 0.0), 128, 500, 0.0
     elif case == "C4":
         grid, N, Nt, shift = (1, 128, 128, 0.0), 96, 300, 0.0
     elif case == "C1":
         grid, N, Nt, shift = (1, 32, 32, 0.0), 20, 20, 0.0
+    elif case == "1D":
+        grid, N, Nt, shift = (2, 1, 64, 0.0), 60, 90, 0.0
+    elif case.startswith("neardup"):
+        grid = (2, 64, 64, 0.0)
+        eps = {"neardup0": 0.0, "neardup6": 1e-6, "neardup3": 1e-3}[case]
+        A = cilgen.make_set(seed, 0, 64, grid[:3], "FHN")
+        rng = np.random.default_rng(seed)
+        B = (A.double() + eps * torch.from_numpy(rng.standard_normal(tuple(A.shape)))).float()
+        return A, torch.cat([B, cilgen.make_set(seed, 1, 64, grid[:3], "FHN")]), grid
     else:
         grid, N, Nt, shift = (2, 32, 32, 0.0), 100, 300, 50.0     # large common offset: centring stress
-    A = cilgen.make_set(31, 0, N, grid[:3]) + shift
-    B = cilgen.make_set(31, 1, Nt, grid[:3]) + shift
+    A = cilgen.make_set(seed, 0, N, grid[:3]) + shift
+    B = cilgen.make_set(seed, 1, Nt, grid[:3]) + shift
+    return A, B, grid
+
+
+@pytest.mark.parametrize("case", ["C2", "C4", "offset", "C1", "neardup0", "neardup6", "neardup3"])
+def test_gram_error_bound_i8(cil, oracle_mod, case):
+    """The INT8 engine's per-pair interval [lo, hi] of the (unweighted) L2 distance must contain the
+    exact FP64 distance for EVERY pair — worst-case bound, near-duplicates included (R13)."""
+    O = oracle_mod
+    dev = torch.device("cuda")
+    A, B, grid = _bound_case(case, 31)
+    iv = cil.diag_gram(A.to(dev), B.to(dev), grid, cil.ENGINE_TC_I8).cpu().numpy().astype(np.float64)
+    h = 1.0 / (grid[2] - 1)
+    w = h * h
+    exact = O.distance_matrix(A.numpy(), B.numpy(), grid, 0x1)[0] / np.sqrt(w)
+    lo, hi = iv[..., 0], iv[..., 1]
+    assert np.all(lo <= exact) and np.all(exact <= hi), (np.argwhere(~((lo <= exact) & (exact <= hi)))[:5],)
+    pos = exact > 0
+    print(f"{case}: median (hi-lo)/d = {np.median((hi - lo)[pos] / exact[pos]):.3e}, "
+          f"max = {((hi - lo)[pos] / exact[pos]).max():.3e}")
+
+
+@pytest.mark.parametrize("engine", ["TC_3XBF16", "TC_3XTF32"])
+@pytest.mark.parametrize("case", ["C2", "C4", "offset", "C1"])
+def test_gram_error_bound(cil, oracle_mod, engine, case):
+    """The float split engines' d^2 error must stay well inside their per-pair bound E that decides
+    which pairs are re-checked exactly (float split engines)."""
+    O = oracle_mod
+    dev = torch.device("cuda")
+    A, B, grid = _bound_case(case, 31)
     d2E = cil.diag_gram(A.to(dev), B.to(dev), grid, _engine(cil, engine)).cpu().numpy().astype(np.float64)
     h = 1.0 / (grid[2] - 1)
     w = h * h
@@ -319,34 +352,24 @@ def test_l2_family_tensor_cores_vs_oracle(cil, oracle_mod, engine):
     _check_counts(c[0].cpu().numpy(), ref)
 
 
-@pytest.mark.parametrize("case", ["C2", "C4", "offset", "C1", "1D"])
+@pytest.mark.parametrize("case", ["C2", "C4", "offset", "C1", "1D", "neardup0", "neardup6", "neardup3"])
 def test_gram_family_error_bound(cil, oracle_mod, case):
-    """The three-phase engine's values of L2^2/w, W12^2/w and W12SUM/sqrt(w) must stay well
-    inside their per-pair bounds (L2-type family on tensor cores)."""
+    """The three-phase engine's intervals of L2/sqrt(w), W12^2/w and W12SUM/sqrt(w) must contain the
+    exact FP64 values for every pair (worst-case bound, L2-type family on tensor cores)."""
     O = oracle_mod
     dev = torch.device("cuda")
-    if case == "C2":
-        grid, N, Nt, shift = (2, 64, 64, 0.0), 96, 300, 0.0
-    elif case == "C4":
-        grid, N, Nt, shift = (1, 128, 128, 0.0), 64, 200, 0.0
-    elif case == "C1":
-        grid, N, Nt, shift = (1, 32, 32, 0.0), 20, 20, 0.0
-    elif case == "1D":
-        grid, N, Nt, shift = (2, 1, 64, 0.0), 60, 90, 0.0
-    else:
-        grid, N, Nt, shift = (2, 32, 32, 0.0), 100, 300, 50.0
-    A = cilgen.make_set(33, 0, N, grid[:3]) + shift
-    B = cilgen.make_set(33, 1, Nt, grid[:3]) + shift
-    vE = cil.diag_gram_family(A.to(dev), B.to(dev), grid).cpu().numpy().astype(np.float64)
+    A, B, grid = _bound_case(case, 33)
+    iv = cil.diag_gram_family(A.to(dev), B.to(dev), grid).cpu().numpy().astype(np.float64)
     h = 1.0 / (grid[2] - 1)
     w = h * h if grid[1] > 1 else h
     D = O.distance_matrix(A.numpy(), B.numpy(), grid, 0x0D)        # L2, W12SUM, W12 (bit order)
-    exact = [D[0] ** 2 / w, D[2] ** 2 / w, D[1] / np.sqrt(w)]       # kinds 0 L2, 1 W12, 2 W12SUM
+    exact = [D[0] / np.sqrt(w), D[2] ** 2 / w, D[1] / np.sqrt(w)]   # kinds 0 L2, 1 W12, 2 W12SUM
     for k, name in enumerate(["L2", "W12", "W12SUM"]):
-        err = np.abs(vE[k, ..., 0] - exact[k])
-        ratio = err / vE[k, ..., 1]
-        print(f"{case} {name}: max err/E = {ratio.max():.3e}, median E/value = {np.median(vE[k, ..., 1] / exact[k]):.3e}")
-        assert ratio.max() < 0.25, name
+        lo, hi = iv[k, ..., 0], iv[k, ..., 1]
+        ok = (lo <= exact[k]) & (exact[k] <= hi)
+        pos = exact[k] > 0
+        print(f"{case} {name}: median (hi-lo)/v = {np.median((hi - lo)[pos] / exact[k][pos]):.3e}")
+        assert ok.all(), (name, np.argwhere(~ok)[:5].tolist())
 
 
 def test_synth_l2_family_segmented_tensor_cores(cil, oracle_mod):
