@@ -154,13 +154,36 @@ def timed(fn, steps, stream):
 
 
 def engine_used(engine: str, K: int) -> str:
-    """The L2 engine AUTO resolves to (include/cil.h): INT8 when K <= 65536."""
+    """The L2 engine AUTO resolves to (include/cil.h): the three-digit INT8 engine (any K)."""
     if engine == "AUTO":
-        return "TC_I8" if K <= 65536 else "TC_3XBF16"
+        return "TC_I8"
     return engine
 
 
-DTYPES = {"TC_I8": "int8 two-digit fixed point / int32 accumulate / f64 stats",
+I8_PEAKS_FILE = os.path.join(ROOT, "profiles", "r02_measured_peaks.json")
+
+
+def tensor_peak(used: str):
+    """(dense peak TOP/s, where it comes from, MMA products issued per K element and pair) of the
+    engine's tensor-core kind.  int8 / tf32: our own cuBLAS measurement on this pool's B200
+    (tools/measure_peaks.py -> profiles/r02_measured_peaks.json, burst); bf16: MEASURED_PEAKS.json."""
+    pk = peaks()
+    if used == "TC_I8":
+        try:
+            return (json.load(open(I8_PEAKS_FILE))["int8"]["burst_tops"],
+                    "profiles/r02_measured_peaks.json int8 burst (torch._int_mm 8192^3)", 6)
+        except Exception:
+            return 2.0 * pk.get("bf16_tflops", 1590.0), "MEASURED_PEAKS.json bf16_tflops x 2 (nominal i8:bf16)", 6
+    if used == "TC_3XTF32":
+        try:
+            return (json.load(open(I8_PEAKS_FILE))["tf32"]["burst_tops"],
+                    "profiles/r02_measured_peaks.json tf32 burst", 3)
+        except Exception:
+            return 0.5 * pk.get("bf16_tflops", 1590.0), "MEASURED_PEAKS.json bf16_tflops x 0.5", 3
+    return pk.get("bf16_tflops", 1590.0), "MEASURED_PEAKS.json bf16_tflops (burst)", 3
+
+
+DTYPES = {"TC_I8": "int8 three-digit (22-bit) fixed point / int32 accumulate / f64 stats",
           "TC_3XBF16": "bf16x3 split / f32 accumulate / f64 stats",
           "TC_3XTF32": "tf32x3 split / f32 accumulate / f64 stats",
           "SIMT": "f32 differences / f64 sums"}
@@ -316,21 +339,20 @@ def main():
     roof_gram = None
     if gram_n > 0:
         per_launch_ms = gram_ms / gram_n
-        # split-accounted: 3 products per K element and pair (hi.hi + hi.lo + lo.hi, or HH + HL + LH)
-        flops = 3 * 2.0 * P * N * Nt * K
+        # split-accounted: the engine issues `nprod` MMA products per K element and pair (INT8: the six
+        # digit products hh, hm, mh, hl, mm, lh; float splits: hi.hi + hi.lo + lo.hi)
+        peak, psrc, nprod = tensor_peak(used)
+        flops = nprod * 2.0 * P * N * Nt * K
         achieved = flops / (per_launch_ms * 1e-3) / 1e12
-        ratio, kind = {"TC_I8": (2.0, "INT8 kind::i8 (HH + HL + LH), peak = bf16 x 2 (nominal i8:bf16)"),
-                       "TC_3XBF16": (1.0, "3xBF16 kind::f16"),
-                       "TC_3XTF32": (0.5, "3xTF32 kind::tf32, peak = bf16 x 0.5 (nominal tf32:bf16)")}[used]
-        bf16_peak = pk.get("bf16_tflops", 1590.0)
-        peak = bf16_peak * ratio
-        roof_gram = {"kernel": "k_gram_i8 / k_gram_tc: tcgen05 Gram + fused binning, " + kind,
-                     "bound": "tensor", "achieved": round(achieved, 2), "peak": peak,
+        kind = {"TC_I8": "INT8 kind::i8, 6 digit products (22-bit fixed point, exact int32)",
+                "TC_3XBF16": "3xBF16 kind::f16", "TC_3XTF32": "3xTF32 kind::tf32"}[used]
+        roof_gram = {"kernel": "k_gram3 / k_gram_tc: tcgen05 Gram + fused binning, " + kind,
+                     "bound": "tensor", "achieved": round(achieved, 2), "peak": round(peak, 1),
                      "unit": "TOP/s" if used == "TC_I8" else "TFLOP/s",
                      "frac": round(achieved / peak, 4),
-                     "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst) x %.1f" % ratio,
-                     "frac_vs_sustained": round(achieved / (pk.get("bf16_tflops_sustained", bf16_peak) * ratio), 4),
-                     "flops_per_launch": flops, "algorithmic_1x_flops_per_launch": flops / 3,
+                     "peak_source": psrc,
+                     "flops_per_launch": flops, "algorithmic_1x_flops_per_launch": flops / nprod,
+                     "frac_algorithmic_1x": round(achieved / nprod / peak, 4),
                      "kernel_ms_per_launch": round(per_launch_ms, 4),
                      "kernel_share_of_step": round(gram_ms / ms, 4),
                      "traffic": traffic_for("C2_gram")}
@@ -345,11 +367,11 @@ def main():
         Kp = (K + 127) // 128 * 128
         rows = P * (N + Nt)
         nbytes = rows * 4.0 * K
-        design_bytes = rows * (4.0 * K + 2.0 * Kp + 8) + P * min(Nt, 16) * 4.0 * K
+        design_bytes = rows * (4.0 * K + 3.0 * Kp + 32) + P * min(Nt, 16) * 4.0 * K
         sec = pack_ms / args.steps * 1e-3
         achieved = nbytes / sec / 1e9
         hbm = pk.get("hbm_gbs", 6547.0)
-        roof_pack = {"kernel": "k_center + 2 x k_pack_i8r: centre, sigma = max|x~|/32639, INT8 digit planes h, l, norms",
+        roof_pack = {"kernel": "k_center + 2 x k_pack3: centre, sigma = max|x~|/Q, three INT8 digit planes h, m, l, row metadata",
                      "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
                      "frac": round(achieved / hbm, 4), "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)",
                      "algorithmic_bytes_per_step": nbytes,
@@ -546,11 +568,14 @@ def bench_c3(args, dev):
     g_ms, g_n = prof["gram_tc"]
     if g_n and tc_family:
         per = g_ms / g_n
-        ops = 3 * 2.0 * N * N * Kaug                          # three-phase Gram over [x | D_x x | D_y x]
+        peak, psrc, nprod = tensor_peak("TC_I8")
+        # Alg. 1 computes only the tiles meeting a block k < l: the k < l blocks hold N^2 (1 - 1/n_ens) / 2 pairs
+        uniq = N * N * (1.0 - 1.0 / cfg["n_ens"]) / 2.0
+        ops = nprod * 2.0 * uniq * Kaug                      # three-phase Gram over [x | D_x x | D_y x]
         ach = ops / (per * 1e-3) / 1e12
         res["gram_tc"] = {"engine": "TC_I8 three-phase (L2, W12, W12SUM)", "ms_per_launch": round(per, 3),
-                          "achieved_tops": round(ach, 1),
-                          "frac_of_peak": round(ach / (2.0 * peaks().get("bf16_tflops", 1590.0)), 4)}
+                          "achieved_tops_on_needed_pairs": round(ach, 1), "peak": round(peak, 1), "peak_source": psrc,
+                          "frac_of_peak": round(ach / peak, 4)}
     print(json.dumps(res), flush=True)
 
 
@@ -608,12 +633,21 @@ def bench_c6(cil, args, world, rank, dev, engine, stream):
     if g_n:
         per_step = g_ms / steps
         # both Gram launches of a step: the pool x pool bin matrix and the y~ counts (s_data x pool[J])
-        ach = 3 * 2.0 * P * (N_syn * N_syn + N_set * Nt) * K / (per_step * 1e-3) / 1e12
         used = engine_used(args.engine, K)
-        ratio = {"TC_I8": 2.0, "TC_3XBF16": 1.0, "TC_3XTF32": 0.5}.get(used, 1.0)
+        peak, psrc, nprod = tensor_peak(used)
+        # issued: the pool x pool bin matrix runs the tile upper triangle (256 x 128 tiles, tile row mt
+        # from column tile 2 mt on), the y~ leg one 64-column tile per 256 pool rows; unique: the
+        # N_syn (N_syn + 1) / 2 pool pairs + the N_set x N_syn y~ pairs the method needs
+        tm, tn = -(-N_syn // 256), -(-N_syn // 128)
+        issued = P * (sum(tn - 2 * m for m in range(tm)) * 256 * 128 + tm * 256 * 64)
+        unique = P * (N_syn * (N_syn + 1) / 2 + N_set * N_syn)
+        t_s = per_step * 1e-3
         res["gram_tc"] = {"engine": used, "ms_per_step": round(per_step, 4), "launches_per_step": g_n / steps,
-                          "achieved_tops": round(ach, 1),
-                          "frac_of_peak": round(ach / (ratio * peaks().get("bf16_tflops", 1590.0)), 4)}
+                          "achieved_tops_issued": round(nprod * 2.0 * issued * K / t_s / 1e12, 1),
+                          "frac_of_peak_issued": round(nprod * 2.0 * issued * K / t_s / 1e12 / peak, 4),
+                          "achieved_tops_unique_pairs": round(nprod * 2.0 * unique * K / t_s / 1e12, 1),
+                          "frac_of_peak_unique_pairs": round(nprod * 2.0 * unique * K / t_s / 1e12 / peak, 4),
+                          "peak": round(peak, 1), "peak_source": psrc}
     r_ms, r_n = prof["resample"]
     if r_n:
         # steps 2.1-2.4: multiplicities, 0/1 threshold rows E, one integer GEMM (rows M1 of the
@@ -713,11 +747,11 @@ def bench_c4(cil, args, world, rank, dev, engine, stream):
            "nonzero_status": int((st != 0).sum())}
     if g_n:
         per = g_ms / g_n
-        ach = 3 * 2.0 * P * rowsA * rowsB * K / (per * 1e-3) / 1e12
         used = engine_used(args.engine, K)
-        ratio = {"TC_I8": 2.0, "TC_3XBF16": 1.0, "TC_3XTF32": 0.5}.get(used, 1.0)
+        peak, psrc, nprod = tensor_peak(used)
+        ach = nprod * 2.0 * P * rowsA * rowsB * K / (per * 1e-3) / 1e12
         res["gram_tc"] = {"engine": used, "ms_per_launch": round(per, 4), "achieved_tops": round(ach, 1),
-                          "frac_of_peak": round(ach / (ratio * peaks().get("bf16_tflops", 1590.0)), 4)}
+                          "peak": round(peak, 1), "peak_source": psrc, "frac_of_peak": round(ach / peak, 4)}
     res["kernel_breakdown"] = {k: round(v[0] / steps, 4) for k, v in prof.items() if v[1] > 0}
     return res
 

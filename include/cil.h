@@ -334,6 +334,13 @@ CIL_API cil_status cil_diag_gram_family(const float* A, int64_t lda, int64_t N, 
  * stream, synchronous).  Returns 0, or -1 on a CUDA error. */
 CIL_API int32_t cil_diag_alu_ceiling(int32_t mix, int32_t iters, double* element_pairs_per_s, double* ms);
 
+/* cil_diag_sqrt_approx_error — DIAGNOSTIC: exhaustive check of the hardware square-root
+ * approximation (sqrt.approx.f32) that the INT8 engine's interval bounds use with a 2^-21
+ * inflation: over every normal positive FP32 x, the largest relative error above (max_rel_up) and
+ * below (max_rel_down) the correctly rounded FP64 square root.  Allocates 16 B of device memory and
+ * synchronises (diagnostic only).  Returns 0, or -1 on a CUDA error. */
+CIL_API int32_t cil_diag_sqrt_approx_error(double* max_rel_up, double* max_rel_down);
+
 /* ------------------------------------------------------------------------ */
 /* Kernel timing (diagnostics, used by bench.py for the live roofline).  While enabled on
  * the calling host thread, every kernel the library launches is bracketed by CUDA events

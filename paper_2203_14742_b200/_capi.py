@@ -62,6 +62,8 @@ def _load():
     lib.cil_normalize.restype = ctypes.c_int
     lib.cil_diag_alu_ceiling.argtypes = [i32, i32, P, P]
     lib.cil_diag_alu_ceiling.restype = i32
+    lib.cil_diag_sqrt_approx_error.argtypes = [P, P]
+    lib.cil_diag_sqrt_approx_error.restype = i32
     lib.cil_prof_enable.argtypes = [i32]
     lib.cil_prof_enable.restype = None
     lib.cil_prof_read.argtypes = [P, P]
@@ -90,7 +92,7 @@ lib = _load()
 
 EXPORTED = ["cil_features_workspace_size", "cil_features", "cil_stats", "cil_loglik",
             "cil_synth_workspace_size", "cil_synth_loglik", "cil_status_string", "cil_last_cuda_error",
-            "cil_version", "cil_last_launch_count", "cil_diag_gram", "cil_prof_enable", "cil_prof_read", "cil_normalize", "cil_diag_alu_ceiling",
+            "cil_version", "cil_last_launch_count", "cil_diag_gram", "cil_prof_enable", "cil_prof_read", "cil_normalize", "cil_diag_alu_ceiling", "cil_diag_sqrt_approx_error",
             "cil_bin_matrix_workspace_size", "cil_bin_matrix", "cil_resample_counts",
             "cil_synth_boot_workspace_size", "cil_synth_loglik_boot", "cil_diag_gram_family",
             "cil_train_workspace_size", "cil_train_vectors", "cil_range_workspace_size", "cil_distance_range",
@@ -104,6 +106,17 @@ def alu_ceiling(mix: int = 0, iters: int = 20000):
     if lib.cil_diag_alu_ceiling(mix, iters, ctypes.byref(eps), ctypes.byref(ms)) != 0:
         raise CilError("cil_diag_alu_ceiling failed")
     return eps.value, ms.value
+
+
+
+def sqrt_approx_error():
+    """(max relative error above, below) of sqrt.approx.f32 over every normal positive FP32 input
+    (exhaustive; diagnostic — the INT8 engine's interval bounds assume < 2^-21)."""
+    up, dn = ctypes.c_double(), ctypes.c_double()
+    if lib.cil_diag_sqrt_approx_error(ctypes.byref(up), ctypes.byref(dn)) != 0:
+        raise CilError("cil_diag_sqrt_approx_error failed")
+    return up.value, dn.value
+
 
 KERNEL_CLASSES = ["prep", "pack", "gram_tc", "simt_tile", "recheck", "tail", "resample"]
 

@@ -15,6 +15,9 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
          "--expt-relaxed-constexpr"]
+# build-time experiment defines (tools/g3_exp.sh builds scratch variants on the GPU box; never set
+# for the product build)
+FLAGS += os.environ.get("CIL_BUILD_DEFINES", "").split()
 
 
 def _sources():

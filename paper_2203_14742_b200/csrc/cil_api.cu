@@ -94,13 +94,13 @@ constexpr int64_t kMinSegI8 = 21;
 bool i8_ok(int64_t col_seg, int64_t rowsB) { return col_seg >= rowsB || col_seg >= kMinSegI8; }
 // The L2-type family (L2, W12, W12SUM) on the three-phase INT8 engine when the
 // request has W12 or W12SUM, the engine is AUTO / TC_I8, and the per-thread histograms fit
-// (column segments: >= 21 columns and M <= 32).
+// (column segments: >= 21 columns and M <= 16).
 bool aug_ok(uint32_t mask, cil_engine engine, const cil_grid& g, int64_t col_seg, int64_t rowsB, int M) {
     if (!(mask & (CIL_W12 | CIL_W12SUM))) return false;
     if (engine != CIL_ENGINE_AUTO && engine != CIL_ENGINE_TC_I8) return false;
     if (g.W < 2) return false;
     const bool seg = col_seg < rowsB;
-    if (seg && (col_seg < kMinSegI8 || M > 32)) return false;
+    if (seg && (col_seg < kMinSegI8 || M > 16)) return false;
     return M <= 64;
 }
 Plan make_plan(uint32_t mask, cil_engine engine, const cil_grid& g, int64_t col_seg = 1ll << 40,

@@ -5,6 +5,8 @@
 //   mix 1: FADD2 + FMNMX3(|.|)                (max family only)
 //   mix 2: FADD2 + FFMA2                       (L2 family only)
 // Same register micro-tile as k_simt (4 x 4 pairs per thread, float4 operands), no memory.
+#include <string.h>
+
 #include "cil_internal.cuh"
 
 namespace cil {
@@ -58,7 +60,48 @@ __global__ void __launch_bounds__(128) k_alu_mix(float* out, int iters, float se
     if (s == 12345.678f) out[threadIdx.x] = s;   // keep the work observable
 }
 
+// ---------------------------------------------------------------------------------------------
+// Exhaustive check of the hardware square-root approximation the INT8 engine's interval bounds rely
+// on (gram3.cu): for EVERY normal positive FP32 x, the relative error of sqrt.approx.f32 against
+// the (FP64, correctly rounded) square root.  The engine inflates by 2^-21, so the bound holds for
+// all inputs iff both maxima stay below 2^-21 (tests/test_gpu_parity.py pins them below 2^-22).
+__global__ void k_sqrt_approx_err(unsigned long long* up, unsigned long long* down) {
+    double e_up = 0.0, e_dn = 0.0;
+    const uint32_t lo = 0x00800000u, hi = 0x7F7FFFFFu;
+    for (uint64_t b = lo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; b <= hi;
+         b += (uint64_t)gridDim.x * blockDim.x) {
+        const float x = __uint_as_float((uint32_t)b);
+        float s;
+        asm("sqrt.approx.f32 %0, %1;" : "=f"(s) : "f"(x));
+        const double r = (double)s / sqrt((double)x) - 1.0;
+        e_up = fmax(e_up, r);
+        e_dn = fmax(e_dn, -r);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        e_up = fmax(e_up, __shfl_xor_sync(0xffffffffu, e_up, o));
+        e_dn = fmax(e_dn, __shfl_xor_sync(0xffffffffu, e_dn, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMax(up, (unsigned long long)__double_as_longlong(e_up));     // non-negative: bit order = value order
+        atomicMax(down, (unsigned long long)__double_as_longlong(e_dn));
+    }
+}
+
 }  // namespace cil
+
+extern "C" int32_t cil_diag_sqrt_approx_error(double* max_rel_up, double* max_rel_down) {
+    unsigned long long* d = nullptr;
+    if (cudaMalloc(&d, 16) != cudaSuccess) return -1;
+    cudaMemset(d, 0, 16);
+    cil::k_sqrt_approx_err<<<148 * 16, 256>>>(d, d + 1);
+    unsigned long long h[2] = {0, 0};
+    const cudaError_t e = cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    if (e != cudaSuccess) return -1;
+    memcpy(max_rel_up, &h[0], 8);
+    memcpy(max_rel_down, &h[1], 8);
+    return 0;
+}
 
 extern "C" CIL_API int32_t cil_diag_alu_ceiling(int32_t mix, int32_t iters, double* element_pairs_per_s,
                                                 double* ms) {

@@ -60,7 +60,13 @@ using tc::named_bar;
 using tc::smem_u32;
 using tc::tmem_ld16;
 
-constexpr int KS = 64;          // K bytes per pipeline stage (one SWIZZLE_64B row)
+// Build-time experiment switch (never set in the product build; tools/g3_exp.sh):
+//   1 = the epilogue only hands the accumulators back (MMA + operand feed alone)
+//   2 = no TMA loads (MMA + epilogue on whatever the stages hold)   3 = both (MMA alone)
+#ifndef CIL_G3_EXP
+#define CIL_G3_EXP 0
+#endif
+constexpr int KS = 128;         // K bytes per pipeline stage (one SWIZZLE_128B row)
 constexpr int AR = 128;         // A rows per CTA (M = 256 per CTA pair)
 constexpr int TILE_M = 256;
 constexpr int MAXSEG = 24;
@@ -92,35 +98,32 @@ struct Params {
 
 template <int TN, int MAXM, bool SEG, bool AUG> struct Geo3 {
     static constexpr int BR = TN / 2;                           // B rows per CTA
-    static constexpr int A_PL = AR * KS;                        // 8 KB per plane
+    static constexpr int A_PL = AR * KS;                        // 16 KB per plane
     static constexpr int B_PL = BR * KS;
-    static constexpr int STAGE = 3 * (A_PL + B_PL);             // 36 KB (TN 128)
-    static constexpr int NEPI = AUG ? 8 : 12;
+    static constexpr int STAGE = 3 * (A_PL + B_PL);             // 72 KB (TN 128)
+    static constexpr int NEPI = 8;
     static constexpr int NET = 32 * NEPI;
     static constexpr int NTHR = 64 + NET;
-    // per-thread histograms [bin][thread] of u32 cells (bank = thread): with column segments byte l
-    // counts local segment l (a thread's <= 64 columns of a tile meet <= 4 segments of >= 21
-    // columns); three-phase without segments: byte k counts kind k; with segments one array per kind
+    // per-thread histograms of u32 cells [word][thread] (bank = thread), byte-packed (a thread bins
+    // <= 64 pairs per tile and kind, flushed every tile):
+    //   no segments: byte (b & 3) of word b >> 2 counts bin b (three-phase: one array per kind);
+    //   column segments: word b, byte l counts local segment l (a thread's <= 64 columns of a tile
+    //   meet <= 4 segments of >= 21 columns; three-phase: one array per kind)
     static constexpr int NLOC = SEG ? 4 : 1;
-    static constexpr int NHA = (AUG && SEG) ? 3 : 1;
-    static constexpr int HIST = NHA * (MAXM + 1) * NET * 4;
+    static constexpr int NKA = AUG ? 3 : 1;
+    static constexpr int HWORDS = SEG ? (MAXM + 1) : (MAXM + 4) / 4;
+    static constexpr int HIST = NKA * HWORDS * NET * 4;
     static constexpr int NPHM = AUG ? 3 : 1;
     static constexpr int COLB = NPHM * TN * 20;                 // float4 (sigma, n, alpha, beta) + r
     static constexpr int THRB = 3 * 2 * 2 * MAXM * 4;           // [kind][rd/ru][2 MAXM]
     static constexpr int FIXED = 1024 + 1024 + COLB + THRB + HIST;
     static constexpr int FIT = (227 * 1024 - FIXED) / STAGE;
-    static constexpr int STAGES = FIT > 6 ? 6 : FIT;
+    static constexpr int STAGES = FIT > 4 ? 4 : FIT;
     static constexpr int SMEM = STAGES * STAGE + FIXED;
     static constexpr int TCOLS = 4 * TN <= 256 ? 256 : 512;
     static_assert(FIT >= 2, "shared memory");
 };
 
-// K-major SWIZZLE_64B shared-memory matrix descriptor (sm_100 version 1): start >> 4, LBO 1 (unused),
-// SBO = 512 B between 8-row core groups, layout type 4 (SWIZZLE_64B) at bits [61, 64).
-__device__ __forceinline__ uint64_t sdesc64(uint32_t saddr) {
-    return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(512 >> 4) << 32) |
-           ((uint64_t)1 << 46) | ((uint64_t)4 << 61);
-}
 __host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
     return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
@@ -129,7 +132,7 @@ __device__ __forceinline__ void mma_i8(uint32_t d, uint64_t a, uint64_t b, uint3
                  "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
                  "l"(a), "l"(b), "r"(id), "r"(acc));
 }
-// 3-D TMA box (64 K-bytes x rows x 3 digit planes); both CTAs of the pair signal the leader's barrier
+// 3-D TMA box (128 K-bytes x rows x 3 digit planes, SWIZZLE_128B); both CTAs of the pair signal the leader's barrier
 __device__ __forceinline__ void tma3(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y) {
     asm volatile(
         "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes "
@@ -201,8 +204,25 @@ __device__ __forceinline__ RowV row_meta(const float* meta, int64_t row, int nph
     return o;
 }
 
-// Interval [dn, up] of the distance of one pair (see the header).  g = G' / 2^32 (FP32).
-// Every operation is symmetric in (a, b), so d(i, j) and d(j, i) give bit-identical intervals.
+// sqrt with a rigorous one-sided bound: the hardware approximation (sqrt.approx.f32) inflated /
+// deflated by 2^-21, directed rounding.  Its relative error is below 2^-22 for every normal input
+// (checked exhaustively on the device: cil_diag_sqrt_approx_error, tests/test_gpu_parity.py);
+// inputs below FLT_MIN are raised to it (upper) or give 0 (lower).
+__device__ __forceinline__ float sqrt_up(float x) {
+    float s;
+    asm("sqrt.approx.f32 %0, %1;" : "=f"(s) : "f"(fmaxf(x, 1.17549435e-38f)));
+    return __fmul_ru(s, 1.000000476837158203125f);           // 1 + 2^-21
+}
+__device__ __forceinline__ float sqrt_dn(float x) {
+    if (!(x >= 1.17549435e-38f)) return 0.f;
+    float s;
+    asm("sqrt.approx.f32 %0, %1;" : "=f"(s) : "f"(x));
+    return __fmul_rd(s, 0.999999523162841796875f);           // 1 - 2^-21
+}
+
+// Bounds of the squared distance of the quantised rows (see the header): lo2 <= d_q^2 <= hi2,
+// and rho = r_a + r_b.  g = G' / 2^32 (FP32).  Every operation is symmetric in (a, b), so d(i, j)
+// and d(j, i) give bit-identical results.
 __device__ __forceinline__ void pair_interval(float g, const RowV& A, float sb, float nb, float alb, float beb,
                                               float rb, float rel, float& lo2, float& hi2, float& rho) {
     const float nn = A.n + nb;
@@ -215,9 +235,11 @@ __device__ __forceinline__ void pair_interval(float g, const RowV& A, float sb, 
     rho = __fadd_ru(A.r, rb);
 }
 
-// Epilogue (all modes).  One tile at a time: stage the column metadata and thresholds, drain every
-// K segment (chunk partials into TMEM columns [3TN, 4TN); a phase's last chunk -> intervals),
-// bin, list ambiguous pairs, flush the histograms.
+// Epilogue (all modes).  Per tile: stage the column metadata and thresholds; per K segment, read
+// the three accumulators, combine them (+ the running chunk partial) into one FP32 value per pair in
+// TMEM columns [3TN, 4TN) and hand the accumulators back at once (the MMAs of the next segment or
+// tile run while this one is binned); at a phase's last segment, bin from those columns, list
+// ambiguous pairs, and finally flush the per-thread histograms.
 template <int TN, int MAXM, bool SEG, bool AUG>
 __device__ __forceinline__ void epilogue(const Params& prm, uint32_t tmem_base, uint64_t* tfull, uint64_t* tempty,
                                          float4* s_c4, float* s_cr, float* s_T, uint32_t* hist_s, int cluster_id,
@@ -274,6 +296,7 @@ __device__ __forceinline__ void epilogue(const Params& prm, uint32_t tmem_base, 
         const int hc0 = (int)(col0 + g0 * 16);
         const int nvalid = (int)min((int64_t)ncol, prm.rowsB - hc0);
         const uint32_t tl = tmem_base + ((uint32_t)(quarter * 32) << 16);
+        const uint32_t tg = tl + 3 * TN;                         // combined FP32 values / chunk partials
         const int64_t cs_first = hc0 >= 0 ? (int64_t)hc0 / prm.sp.col_seg : 0;
         int bnd[GG::NLOC > 1 ? GG::NLOC - 1 : 1];
 #pragma unroll
@@ -296,40 +319,47 @@ __device__ __forceinline__ void epilogue(const Params& prm, uint32_t tmem_base, 
             if (AUG && first && ph > 0) A = row_meta(prm.meta, arow, nph, ph);
             mbar_wait(&tfull[0], tph);
             fence_after();
+            // ---- drain: g = 2^-32 G' (+ the running partial) into TMEM columns [3TN, 4TN)
 #pragma unroll 1
-            for (int gi = 0; gi < g1 - g0; ++gi) {
+            for (int gi = 0; gi < ((CIL_G3_EXP & 1) ? 0 : g1 - g0); ++gi) {
                 if (gi * 16 >= nvalid) break;                       // warp-uniform
                 const int tcol = (g0 + gi) * 16;
-                float gv[16];
+                uint32_t vr[16];
                 if (emp) {
 #pragma unroll
-                    for (int jj = 0; jj < 16; ++jj) gv[jj] = 0.f;
+                    for (int jj = 0; jj < 16; ++jj) vr[jj] = 0u;
                 } else {
                     uint32_t v32[16], v24[16], v16[16];
                     tmem_ld16(tl + tcol, v32);
                     tmem_ld16(tl + TN + tcol, v24);
                     tmem_ld16(tl + 2 * TN + tcol, v16);
+                    if (!first) tmem_ld16(tg + tcol, vr);
 #pragma unroll
-                    for (int jj = 0; jj < 16; ++jj)
-                        gv[jj] = fmaf((float)(int)v16[jj], 1.52587890625e-05f,
-                                      fmaf((float)(int)v24[jj], 0.00390625f, (float)(int)v32[jj]));
-                    if (!first) {
-                        uint32_t vr[16];
-                        tmem_ld16(tl + 3 * TN + tcol, vr);
-#pragma unroll
-                        for (int jj = 0; jj < 16; ++jj) gv[jj] += __uint_as_float(vr[jj]);
+                    for (int jj = 0; jj < 16; ++jj) {
+                        float gv = fmaf((float)(int)v16[jj], 1.52587890625e-05f,
+                                        fmaf((float)(int)v24[jj], 0.00390625f, (float)(int)v32[jj]));
+                        if (!first) gv += __uint_as_float(vr[jj]);
+                        vr[jj] = __float_as_uint(gv);
                     }
                 }
-                if (!last) {                                        // a chunk of a longer phase: keep the partial
-                    uint32_t vr[16];
-#pragma unroll
-                    for (int jj = 0; jj < 16; ++jj) vr[jj] = __float_as_uint(gv[jj]);
-                    tmem_st16(tl + 3 * TN + tcol, vr);
-                    continue;
-                }
+                tmem_st16(tg + tcol, vr);
+            }
+            tmem_wait_st();
+            fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_remote(&tempty[0], 0);      // the accumulators are free again
+            tph ^= 1;
+            if (!last || (CIL_G3_EXP & 1)) continue;
+            // ---- a phase's last segment: intervals and bins from the combined values
+            const float4* c4 = s_c4 + ph * TN;
+            const float* cr = s_cr + ph * TN;
+#pragma unroll 1
+            for (int gi = 0; gi < g1 - g0; ++gi) {
+                if (gi * 16 >= nvalid) break;                       // warp-uniform
+                const int tcol = (g0 + gi) * 16;
+                uint32_t vr[16];
+                tmem_ld16(tg + tcol, vr);
                 if (!row_ok) continue;
-                const float4* c4 = s_c4 + ph * TN;
-                const float* cr = s_cr + ph * TN;
                 if (!AUG) {
                     // ---- one phase: the L2 distance; bin on the upper end, list if a radius is inside
                     const float* Tlo = s_T;                      // kind 0, rounded down
@@ -341,11 +371,11 @@ __device__ __forceinline__ void epilogue(const Params& prm, uint32_t tmem_base, 
                         const int jc = tcol + jj;
                         const float4 cb = c4[jc];
                         float lo2, hi2, rho;
-                        pair_interval(gv[jj], A, cb.x, cb.y, cb.z, cb.w, cr[jc], prm.rel, lo2, hi2, rho);
-                        const float up = __fadd_ru(__fsqrt_ru(fmaxf(hi2, 0.f)), rho);
+                        pair_interval(__uint_as_float(vr[jj]), A, cb.x, cb.y, cb.z, cb.w, cr[jc], prm.rel, lo2, hi2, rho);
+                        const float up = __fadd_ru(sqrt_up(hi2), rho);
                         if (diag_item) {
                             if (gi * 16 + jj < nvalid) {
-                                const float dn = fmaxf(__fsub_rd(__fsqrt_rd(fmaxf(lo2, 0.f)), rho), 0.f);
+                                const float dn = fmaxf(__fsub_rd(sqrt_dn(lo2), rho), 0.f);
                                 float* dg = prm.diag + ((int64_t)row * prm.rowsB + hc0 + gi * 16 + jj) * 2;
                                 dg[0] = dn;
                                 dg[1] = up;
@@ -381,7 +411,8 @@ __device__ __forceinline__ void epilogue(const Params& prm, uint32_t tmem_base, 
 #pragma unroll
                         for (int jj = 0; jj < 16; ++jj)
                             if (gi * 16 + jj < nvalid)
-                                atomicAdd(myh + (bins[jj] & 255) * NET, SEG ? 1u << ((bins[jj] >> 5) & 24) : 1u);
+                                atomicAdd(myh + (SEG ? (bins[jj] & 255) : ((bins[jj] & 255) >> 2)) * NET,
+                                          SEG ? 1u << ((bins[jj] >> 5) & 24) : 1u << (8 * (bins[jj] & 3)));
                     }
                     if (amb) {
 #pragma unroll
@@ -404,9 +435,9 @@ __device__ __forceinline__ void epilogue(const Params& prm, uint32_t tmem_base, 
                         const int64_t col = hc0 + gi * 16 + jj;
                         const float4 cb = c4[jc];
                         float lo2, hi2, rho;
-                        pair_interval(gv[jj], A, cb.x, cb.y, cb.z, cb.w, cr[jc], prm.rel, lo2, hi2, rho);
-                        const float up = __fadd_ru(__fsqrt_ru(fmaxf(hi2, 0.f)), rho);
-                        const float dn = fmaxf(__fsub_rd(__fsqrt_rd(fmaxf(lo2, 0.f)), rho), 0.f);
+                        pair_interval(__uint_as_float(vr[jj]), A, cb.x, cb.y, cb.z, cb.w, cr[jc], prm.rel, lo2, hi2, rho);
+                        const float up = __fadd_ru(sqrt_up(hi2), rho);
+                        const float dn = fmaxf(__fsub_rd(sqrt_dn(lo2), rho), 0.f);
                         const int64_t pi = pbase + col;
                         if (ph < 2) {
                             prm.part[ph * npairs + pi] = make_float2(dn, up);
@@ -447,9 +478,9 @@ __device__ __forceinline__ void epilogue(const Params& prm, uint32_t tmem_base, 
                                 if (sym_up) bm[col * prm.rowsB + row] = (uint8_t)b;
                                 if (sym_band && col < row) continue;
                             } else if (SEG) {
-                                atomicAdd(myh + (k * (MAXM + 1) + b) * NET, 1u << (8 * lcs));
+                                atomicAdd(myh + (k * GG::HWORDS + b) * NET, 1u << (8 * lcs));
                             } else {
-                                atomicAdd(myh + b * NET, 1u << (8 * k));
+                                atomicAdd(myh + (k * GG::HWORDS + (b >> 2)) * NET, 1u << (8 * (b & 3)));
                             }
                             if (vlo < Thi[b]) {
                                 const uint32_t idx = atomicAdd(prm.ctr, 1u);
@@ -463,11 +494,6 @@ __device__ __forceinline__ void epilogue(const Params& prm, uint32_t tmem_base, 
                     }
                 }
             }
-            if (!last) tmem_wait_st();
-            fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive_remote(&tempty[0], 0);
-            tph ^= 1;
         }
         if (prm.binout != nullptr || no_bin) continue;
         // ---- flush the per-thread histograms (warp sums -> global u64 atomics) and reset them
@@ -476,17 +502,18 @@ __device__ __forceinline__ void epilogue(const Params& prm, uint32_t tmem_base, 
         const bool uniform = __all_sync(0xffffffffu, rs == rs0 || !row_ok);
         for (int bb = 0; bb <= M; ++bb) {
 #pragma unroll
-            for (int k = 0; k < (AUG ? 3 : 1); ++k) {
-                uint32_t* cp = (AUG && SEG) ? myh + (k * (MAXM + 1) + bb) * NET : myh + bb * NET;
+            for (int k = 0; k < GG::NKA; ++k) {
+                const int wd = SEG ? bb : (bb >> 2);
+                uint32_t* cp = myh + (k * GG::HWORDS + wd) * NET;
                 const uint32_t cell = *cp;
-                if ((AUG && SEG) || k == (AUG ? 2 : 0)) *cp = 0u;
+                if (SEG || (bb & 3) == 3 || bb == M) *cp = 0u;   // word done: reset
                 const int q = AUG ? prm.q_k[k] : prm.q_l2;
                 if (bb == 0 || q < 0) continue;                  // bin 0 (outside every radius) is not kept
 #pragma unroll
                 for (int l = 0; l < GG::NLOC; ++l) {
                     const int64_t cs = cs_first + l;
                     if (cs * prm.sp.col_seg >= prm.rowsB || cs * prm.sp.col_seg >= hc0 + ncol) break;
-                    const uint32_t v = SEG ? ((cell >> (8 * l)) & 255u) : (AUG ? ((cell >> (8 * k)) & 255u) : cell);
+                    const uint32_t v = SEG ? ((cell >> (8 * l)) & 255u) : ((cell >> (8 * (bb & 3))) & 255u);
                     if (uniform) {
                         const uint32_t tot = __reduce_add_sync(0xffffffffu, v);
                         if (lane == 0 && tot)
@@ -517,7 +544,7 @@ k_gram3(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensor
     float4* s_c4 = reinterpret_cast<float4*>(smem + STAGES * GG::STAGE + 1024);
     float* s_cr = reinterpret_cast<float*>(s_c4 + GG::NPHM * TN);
     float* s_T = s_cr + GG::NPHM * TN;
-    uint32_t* hist_s = reinterpret_cast<uint32_t*>(s_T + 3 * 2 * 2 * MAXM);
+    uint32_t* hist_s = reinterpret_cast<uint32_t*>(s_T + 3 * 2 * 2 * MAXM);   // GG::HIST bytes
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_rank();
@@ -558,9 +585,13 @@ k_gram3(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensor
                 for (int kb = 0; kb < n_kb; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     unsigned char* st = stages + stage * GG::STAGE;
-                    if (rank == 0) mbar_expect_tx(&full[stage], 2 * GG::STAGE);
-                    tma3(st, &mA, &full[stage], kb * KS, ya);
-                    tma3(st + 3 * GG::A_PL, &mB, &full[stage], kb * KS, yb);
+                    if (CIL_G3_EXP & 2) {
+                        if (rank == 0) mbar_expect_tx(&full[stage], 0);
+                    } else {
+                        if (rank == 0) mbar_expect_tx(&full[stage], 2 * GG::STAGE);
+                        tma3(st, &mA, &full[stage], kb * KS, ya);
+                        tma3(st + 3 * GG::A_PL, &mB, &full[stage], kb * KS, yb);
+                    }
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
             }
@@ -581,8 +612,8 @@ k_gram3(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensor
                         fence_after();
                         const uint32_t sa = smem_u32(stages + stage * GG::STAGE);
                         const uint32_t sb = sa + 3 * GG::A_PL;
-                        const uint64_t ah = sdesc64(sa), am = sdesc64(sa + GG::A_PL), al = sdesc64(sa + 2 * GG::A_PL);
-                        const uint64_t bh = sdesc64(sb), bm = sdesc64(sb + GG::B_PL), bl = sdesc64(sb + 2 * GG::B_PL);
+                        const uint64_t ah = tc::sdesc(sa), am = tc::sdesc(sa + GG::A_PL), al = tc::sdesc(sa + 2 * GG::A_PL);
+                        const uint64_t bh = tc::sdesc(sb), bm = tc::sdesc(sb + GG::B_PL), bl = tc::sdesc(sb + 2 * GG::B_PL);
 #pragma unroll
                         for (int k = 0; k < KS / 32; ++k) {          // 32 int8 of K per MMA
                             const uint64_t adv = (uint64_t)(k * 2);  // +32 B in the start-address field
@@ -622,32 +653,22 @@ constexpr float kQ = 4160000.f;
 // they are packed as exact-only (r = +inf: every pair of theirs goes to the FP64 re-check).
 constexpr float kMinMax = 3.637978807091713e-12f, kMaxMax = 1.099511627776e12f;
 
-__device__ __forceinline__ uint32_t pack4(int a, int b, int c, int d) {
-    return (uint32_t)(a & 255) | ((uint32_t)(b & 255) << 8) | ((uint32_t)(c & 255) << 16) | ((uint32_t)d << 24);
-}
-
-// Quantise 4 values: digit words (h, m, l bytes), residual sum of squares, exact digit dot products
-// S[0..5] = (hh, hm, hl, mm, ml, ll) via dp4a.
-__device__ __forceinline__ void quant4(const float4 t, float sg, float inv, uint32_t& wh, uint32_t& wm, uint32_t& wl,
-                                       float& e2, int (&S)[6]) {
-    const float tv[4] = {t.x, t.y, t.z, t.w};
-    int hh[4], mm[4], ll[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const float rr = fmaf(tv[i], inv, 12582912.f);
-        const int q = __float_as_int(rr) - 0x4B400000;
-        const float qf = rr - 12582912.f;
-        const float e = fmaf(-sg, qf, tv[i]);                 // x~ - sigma q, one rounding
-        e2 = fmaf(e, e, e2);
-        const int t1 = (q + 128) >> 8;
-        const int h = (t1 + 128) >> 8;
-        ll[i] = q - (t1 << 8);
-        mm[i] = t1 - (h << 8);
-        hh[i] = h;
-    }
-    wh = pack4(hh[0], hh[1], hh[2], hh[3]);
-    wm = pack4(mm[0], mm[1], mm[2], mm[3]);
-    wl = pack4(ll[0], ll[1], ll[2], ll[3]);
+// Quantise 4 values: q = rint(t / sigma) by one FFMA with the 1.5 * 2^23 constant (exact rint of
+// t * inv for |t * inv| < 2^22), raw = its bit pattern = q + 0x4B400000.  The balanced digits come
+// straight from byte lanes: l = byte 0 of q = byte 0 of raw, m = byte 1 of (q + 128) = byte 1 of
+// (raw + 128), h = byte 2 of (q + 32896) = byte 2 of (raw - 0x4B3F7F80) (q = 2^16 h + 2^8 m + l,
+// h = (q + 32896) >> 16, m = ((q + 128) >> 8) - 2^8 h).  Digit words are gathered with byte
+// permutes; S[0..5] += the exact digit dot products (hh, hm, hl, mm, ml, ll) by dp4a.
+__device__ __forceinline__ void quant4(const float4 t, float inv, uint32_t& wh, uint32_t& wm, uint32_t& wl,
+                                       int (&S)[6]) {
+    const uint32_t r0 = __float_as_uint(fmaf(t.x, inv, 12582912.f));
+    const uint32_t r1 = __float_as_uint(fmaf(t.y, inv, 12582912.f));
+    const uint32_t r2 = __float_as_uint(fmaf(t.z, inv, 12582912.f));
+    const uint32_t r3 = __float_as_uint(fmaf(t.w, inv, 12582912.f));
+    wl = __byte_perm(__byte_perm(r0, r1, 0x0040), __byte_perm(r2, r3, 0x0040), 0x5410);
+    wm = __byte_perm(__byte_perm(r0 + 128u, r1 + 128u, 0x0051), __byte_perm(r2 + 128u, r3 + 128u, 0x0051), 0x5410);
+    const uint32_t c = 0x4B3F7F80u;
+    wh = __byte_perm(__byte_perm(r0 - c, r1 - c, 0x0062), __byte_perm(r2 - c, r3 - c, 0x0062), 0x5410);
     S[0] = __dp4a((int)wh, (int)wh, S[0]);
     S[1] = __dp4a((int)wh, (int)wm, S[1]);
     S[2] = __dp4a((int)wh, (int)wl, S[2]);
@@ -656,109 +677,123 @@ __device__ __forceinline__ void quant4(const float4 t, float sg, float inv, uint
     S[5] = __dp4a((int)wl, (int)wl, S[5]);
 }
 
-// Row metadata from the block sums (one thread).  cnt = elements of the block; tn2 = |x~|^2 of the
-// FP32 values the block was formed from (bounds the FP32 rounding of the block values, see below).
-__device__ __forceinline__ void write_meta(float* out, float sg, const long long (&S)[6], double e2, double slack_norm2,
-                                           bool exact_only) {
+// NaN-propagating 3-input |.|-max (FMNMX3 with |.| operands): a NaN input poisons the row maximum
+__device__ __forceinline__ float absmax3_nan(float m, float a, float b) {
+    float r;
+    asm("max.NaN.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(m), "f"(fabsf(a)), "f"(fabsf(b)));
+    return r;
+}
+
+// Row metadata from the block's digit sums (one thread).  cnt = elements of the block; tslack =
+// extra FP32-rounding slack of the block values beyond the centring of the values themselves
+// (derivative blocks: 2^-24 * 2 |x~|, see k_pack3_aug).  The quantisation residual is bounded
+// analytically: q = rint(t inv) gives |t - sigma q| <= sigma/2 + delta |t| with delta = |1 - sigma inv|
+// (exact in FP64), so |e| <= (sigma/2 sqrt(cnt) + delta sqrt(n)) / (1 - delta) (|t| <= sqrt(n) + |e|);
+// the centring t = fl(x - c) adds <= 2^-24 |t| per element.
+__device__ __forceinline__ void write_meta(float* out, float sg, float inv, const long long (&S)[6], double cnt,
+                                           double tslack, bool exact_only, double tnorm_exact_only) {
     // sum q^2 = 2^32 hh + 2^25 hm + 2^17 hl + 2^16 mm + 2^9 ml + ll, exactly
     const long long Q = S[0] * (1ll << 32) + S[1] * (1ll << 25) + S[2] * (1ll << 17) + S[3] * (1ll << 16) +
                         S[4] * (1ll << 9) + S[5];
     const double s = (double)sg;
     const double n = (double)Q * s * s;
-    // residual: |e'| from FP32 sums of <= 2048 terms per thread (relative error < 2^-12 on e2, which
-    // also covers the rounding of each e'), plus the FP32 rounding of the block values relative to the
-    // exact (x - c) ones, <= 2^-24 (1 + 2^-23) per unit of slack_norm (counted twice for safety)
-    const double r = sqrt(e2 * (1.0 + 1.0 / 4096.0)) * (1.0 + 1e-12) + sqrt(slack_norm2) * (1.0 + 1e-6) * 1.2e-7;
+    const double delta = fabs(1.0 - (double)sg * (double)inv);
+    const double e = (0.5 * s * sqrt(cnt) + delta * sqrt(n)) / (1.0 - delta);
+    const double r = exact_only ? INFINITY
+                                : (e + 5.9604644775390625e-08 * 1.001 * (sqrt(n) + e) + tslack) * (1.0 + 1e-9);
+    (void)tnorm_exact_only;
     out[0] = (float)n;
     out[1] = sg;
-    out[2] = exact_only ? INFINITY : __double2float_ru(r);
+    out[2] = __double2float_ru(r);
     out[3] = __double2float_ru(s * sqrt((double)S[5]) * (1.0 + 1e-12));
     out[4] = __double2float_ru(256.0 * s * sqrt((double)S[3]) * (1.0 + 1e-12));
     out[5] = 0.f; out[6] = 0.f; out[7] = 0.f;
 }
 
 // One CTA per row, the whole row in registers (NV float4 per thread, NT threads): x~ = x - c, max,
-// quantise, store the three digit planes, exact digit sums, residual.
+// quantise, store the three digit planes, exact digit sums.  Thread 0 prefetches the row pf_dist
+// CTAs ahead into L2 (cp.async.bulk.prefetch), so HBM keeps streaming while resident CTAs reduce /
+// quantise / store.
 template <int NV, int NT>
 __global__ void __launch_bounds__(NT) k_pack3(RowSrc src, int64_t rows, int64_t K, int64_t Kp, const float* __restrict__ center,
                                               int8_t* __restrict__ planes, int64_t plane_stride, int64_t row0,
-                                              float* __restrict__ meta, int32_t* __restrict__ status) {
+                                              float* __restrict__ meta, int32_t* __restrict__ status, int64_t pf_dist) {
     const int64_t p = blockIdx.y;
     const int64_t r = blockIdx.x;
     const float* x = row_ptr(src, p, r);
     const float* c = center + p * Kp;
     const int64_t orow = row0 + p * rows + r;
+    if (threadIdx.x == 0 && pf_dist > 0) {
+        const int64_t lin = (int64_t)blockIdx.y * gridDim.x + blockIdx.x + pf_dist;
+        if (lin < (int64_t)gridDim.x * gridDim.y) {
+            const float* xn = row_ptr(src, lin / gridDim.x, lin % gridDim.x);
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(xn), "r"((uint32_t)(K * 4)) : "memory");
+        }
+    }
     __shared__ float red[NT / 32];
-    __shared__ double redd[NT / 32][8];
+    __shared__ long long redl[NT / 32][6];
     float4 v[NV];
-    float mx = 0.f, nfa = 0.f;
+    float mx = 0.f;
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
         const int64_t k = ((int64_t)i * NT + threadIdx.x) * 4;
         if (k < K) {
             const float4 xv = __ldg(reinterpret_cast<const float4*>(x + k));
             const float4 cv = __ldg(reinterpret_cast<const float4*>(c + k));
-            nfa = fmaf(xv.x, 0.f, fmaf(xv.y, 0.f, fmaf(xv.z, 0.f, fmaf(xv.w, 0.f, nfa))));
             v[i] = make_float4(xv.x - cv.x, xv.y - cv.y, xv.z - cv.z, xv.w - cv.w);
         } else {
             v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
         }
-        mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v[i].x), fabsf(v[i].y)), fmaxf(fabsf(v[i].z), fabsf(v[i].w))));
+        mx = absmax3_nan(absmax3_nan(mx, v[i].x, v[i].y), v[i].z, v[i].w);
     }
-    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    for (int o = 16; o > 0; o >>= 1) {
+        const float t = __shfl_xor_sync(0xffffffffu, mx, o);
+        asm("max.NaN.f32 %0, %0, %1;" : "+f"(mx) : "f"(t));
+    }
     const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
-    const bool anynf = __syncthreads_or(nfa != nfa);
     if (ln == 0) red[w] = mx;
     __syncthreads();
     mx = 0.f;
 #pragma unroll
-    for (int i = 0; i < NT / 32; ++i) mx = fmaxf(mx, red[i]);
-    const bool exact_only = mx > 0.f && !(mx >= kMinMax && mx <= kMaxMax);
-    const float sg = (mx >= kMinMax && mx <= kMaxMax) ? mx / kQ : 1.f;
+    for (int i = 0; i < NT / 32; ++i) asm("max.NaN.f32 %0, %0, %1;" : "+f"(mx) : "f"(red[i]));
+    const bool nonfinite = !(mx <= 3.0e38f);                    // NaN or Inf somewhere in the row
+    const bool ok = mx >= kMinMax && mx <= kMaxMax;
+    const bool exact_only = mx > 0.f && !ok;
+    const float sg = ok ? mx / kQ : 1.f;
     const float inv = 1.f / sg;
     int S[6] = {0, 0, 0, 0, 0, 0};
-    float e2 = 0.f, t2 = 0.f;
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
         const int64_t k = ((int64_t)i * NT + threadIdx.x) * 4;
         if (k >= Kp) continue;
         uint32_t wh = 0, wm = 0, wl = 0;
-        if (!exact_only) quant4(v[i], sg, inv, wh, wm, wl, e2, S);
-        else e2 = fmaf(v[i].x, v[i].x, fmaf(v[i].y, v[i].y, fmaf(v[i].z, v[i].z, fmaf(v[i].w, v[i].w, e2))));
-        t2 = fmaf(v[i].x, v[i].x, fmaf(v[i].y, v[i].y, fmaf(v[i].z, v[i].z, fmaf(v[i].w, v[i].w, t2))));
+        if (ok) quant4(v[i], inv, wh, wm, wl, S);
         int8_t* o = planes + orow * Kp + k;
         *reinterpret_cast<uint32_t*>(o) = wh;
         *reinterpret_cast<uint32_t*>(o + plane_stride) = wm;
         *reinterpret_cast<uint32_t*>(o + 2 * plane_stride) = wl;
     }
-    double acc[8];
 #pragma unroll
-    for (int i = 0; i < 6; ++i) acc[i] = (double)S[i];
-    acc[6] = (double)e2;
-    acc[7] = (double)t2;
-#pragma unroll
-    for (int i = 0; i < 8; ++i)
-        for (int o = 16; o > 0; o >>= 1) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], o);
-    if (ln == 0)
-#pragma unroll
-        for (int i = 0; i < 8; ++i) redd[w][i] = acc[i];
+    for (int i = 0; i < 6; ++i) {
+        long long a = S[i];
+        for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+        if (ln == 0) redl[w][i] = a;
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
         long long Sl[6];
-        double e = 0.0, tt = 0.0;
         for (int i = 0; i < 6; ++i) {
-            double s = 0.0;
-            for (int j = 0; j < NT / 32; ++j) s += redd[j][i];
-            Sl[i] = (long long)s;                               // exact: |sums| < 2^53
+            long long a = 0;
+            for (int j = 0; j < NT / 32; ++j) a += redl[j][i];
+            Sl[i] = a;
         }
-        for (int j = 0; j < NT / 32; ++j) { e += redd[j][6]; tt += redd[j][7]; }
-        write_meta(meta + orow * 8, sg, Sl, e, tt * (1.0 + 1.0 / 4096.0), exact_only);
-        if (anynf) atomicOr(&status[p], CIL_ITEM_NONFINITE);
+        write_meta(meta + orow * 8, sg, inv, Sl, (double)K, 0.0, exact_only, 0.0);
+        if (nonfinite) atomicOr(&status[p], CIL_ITEM_NONFINITE);
     }
 }
 
-// Rows too long for registers (K > 32768): pass 1 streams the row for max|x~| and the centred
-// norm, pass 2 re-reads it (L2-resident: one row per CTA) to quantise.  Same arithmetic as k_pack3.
+// Rows too long for registers (K > 32768): pass 1 streams the row for max|x~|, pass 2 re-reads it
+// (L2-resident: one row per CTA) to quantise.  Same arithmetic as k_pack3.
 __global__ void __launch_bounds__(1024) k_pack3_2p(RowSrc src, int64_t rows, int64_t K, int64_t Kp,
                                                    const float* __restrict__ center, int8_t* __restrict__ planes,
                                                    int64_t plane_stride, int64_t row0, float* __restrict__ meta,
@@ -770,27 +805,29 @@ __global__ void __launch_bounds__(1024) k_pack3_2p(RowSrc src, int64_t rows, int
     const float* c = center + p * Kp;
     const int64_t orow = row0 + p * rows + r;
     __shared__ float red[NT / 32];
-    __shared__ double redd[NT / 32][8];
-    float mx = 0.f, nfa = 0.f;
+    __shared__ long long redl[NT / 32][6];
+    float mx = 0.f;
     for (int64_t k = (int64_t)threadIdx.x * 4; k < K; k += NT * 4) {
         const float4 xv = __ldg(reinterpret_cast<const float4*>(x + k));
         const float4 cv = __ldg(reinterpret_cast<const float4*>(c + k));
-        nfa = fmaf(xv.x, 0.f, fmaf(xv.y, 0.f, fmaf(xv.z, 0.f, fmaf(xv.w, 0.f, nfa))));
-        mx = fmaxf(mx, fmaxf(fmaxf(fabsf(xv.x - cv.x), fabsf(xv.y - cv.y)), fmaxf(fabsf(xv.z - cv.z), fabsf(xv.w - cv.w))));
+        mx = absmax3_nan(absmax3_nan(mx, xv.x - cv.x, xv.y - cv.y), xv.z - cv.z, xv.w - cv.w);
     }
-    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    for (int o = 16; o > 0; o >>= 1) {
+        const float t = __shfl_xor_sync(0xffffffffu, mx, o);
+        asm("max.NaN.f32 %0, %0, %1;" : "+f"(mx) : "f"(t));
+    }
     const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
-    const bool anynf = __syncthreads_or(nfa != nfa);
     if (ln == 0) red[w] = mx;
     __syncthreads();
     mx = 0.f;
-    for (int i = 0; i < NT / 32; ++i) mx = fmaxf(mx, red[i]);
-    const bool exact_only = mx > 0.f && !(mx >= kMinMax && mx <= kMaxMax);
-    const float sg = (mx >= kMinMax && mx <= kMaxMax) ? mx / kQ : 1.f;
+    for (int i = 0; i < NT / 32; ++i) asm("max.NaN.f32 %0, %0, %1;" : "+f"(mx) : "f"(red[i]));
+    const bool nonfinite = !(mx <= 3.0e38f);
+    const bool ok = mx >= kMinMax && mx <= kMaxMax;
+    const bool exact_only = mx > 0.f && !ok;
+    const float sg = ok ? mx / kQ : 1.f;
     const float inv = 1.f / sg;
     int S[6] = {0, 0, 0, 0, 0, 0};
     long long SL[6] = {0, 0, 0, 0, 0, 0};
-    float e2 = 0.f, t2 = 0.f;
     int cnt = 0;
     for (int64_t k = (int64_t)threadIdx.x * 4; k < Kp; k += NT * 4) {
         float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -800,9 +837,7 @@ __global__ void __launch_bounds__(1024) k_pack3_2p(RowSrc src, int64_t rows, int
             v = make_float4(xv.x - cv.x, xv.y - cv.y, xv.z - cv.z, xv.w - cv.w);
         }
         uint32_t wh = 0, wm = 0, wl = 0;
-        if (!exact_only) quant4(v, sg, inv, wh, wm, wl, e2, S);
-        else e2 = fmaf(v.x, v.x, fmaf(v.y, v.y, fmaf(v.z, v.z, fmaf(v.w, v.w, e2))));
-        t2 = fmaf(v.x, v.x, fmaf(v.y, v.y, fmaf(v.z, v.z, fmaf(v.w, v.w, t2))));
+        if (ok) quant4(v, inv, wh, wm, wl, S);
         int8_t* o = planes + orow * Kp + k;
         *reinterpret_cast<uint32_t*>(o) = wh;
         *reinterpret_cast<uint32_t*>(o + plane_stride) = wm;
@@ -812,26 +847,21 @@ __global__ void __launch_bounds__(1024) k_pack3_2p(RowSrc src, int64_t rows, int
             cnt = 0;
         }
     }
-    double acc[8];
-    for (int i = 0; i < 6; ++i) acc[i] = (double)(SL[i] + S[i]);
-    acc[6] = (double)e2;
-    acc[7] = (double)t2;
-    for (int i = 0; i < 8; ++i)
-        for (int o = 16; o > 0; o >>= 1) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], o);
-    if (ln == 0)
-        for (int i = 0; i < 8; ++i) redd[w][i] = acc[i];
+    for (int i = 0; i < 6; ++i) {
+        long long a = SL[i] + S[i];
+        for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+        if (ln == 0) redl[w][i] = a;
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
         long long Sl[6];
-        double e = 0.0, tt = 0.0;
         for (int i = 0; i < 6; ++i) {
-            double s = 0.0;
-            for (int j = 0; j < NT / 32; ++j) s += redd[j][i];
-            Sl[i] = (long long)s;
+            long long a = 0;
+            for (int j = 0; j < NT / 32; ++j) a += redl[j][i];
+            Sl[i] = a;
         }
-        for (int j = 0; j < NT / 32; ++j) { e += redd[j][6]; tt += redd[j][7]; }
-        write_meta(meta + orow * 8, sg, Sl, e, tt * (1.0 + 1.0 / 4096.0), exact_only);
-        if (anynf) atomicOr(&status[p], CIL_ITEM_NONFINITE);
+        write_meta(meta + orow * 8, sg, inv, Sl, (double)K, 0.0, exact_only, 0.0);
+        if (nonfinite) atomicOr(&status[p], CIL_ITEM_NONFINITE);
     }
 }
 
@@ -854,7 +884,7 @@ __global__ void __launch_bounds__(256) k_pack3_aug(RowSrc src, int64_t rows, Aug
     const int64_t orow = row0 + p * rows + r;
     const int W = g.W, H = g.H, SH = g.S * g.H;
     __shared__ float red[3][8];
-    __shared__ double redd[8][3][8];
+    __shared__ long long redd[8][3][6];
     const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
     auto xt = [&](int64_t e) -> float { return __ldg(x + e) - __ldg(c + e); };
     float m0 = 0.f, mx = 0.f, my = 0.f, nfa = 0.f;
@@ -896,29 +926,22 @@ __global__ void __launch_bounds__(256) k_pack3_aug(RowSrc src, int64_t rows, Aug
     }
     int8_t* ph = planes + orow * Krow;
     int S[3][6];
-    float e2[3] = {0.f, 0.f, 0.f}, t2[3] = {0.f, 0.f, 0.f};
 #pragma unroll
     for (int a = 0; a < 3; ++a)
 #pragma unroll
         for (int i = 0; i < 6; ++i) S[a][i] = 0;
-    // one value at a time (the block layouts are not 4-aligned); dp4a on the value in byte 0
+    // one value at a time (the block layouts are not 4-aligned); digits from the byte lanes of the
+    // rint result (see quant4)
     auto put = [&](int a, int64_t col, float v) {
         int hh = 0, mm = 0, ll = 0;
         if (!ex[a]) {
-            const float rr = fmaf(v, inv[a], 12582912.f);
-            const int q = __float_as_int(rr) - 0x4B400000;
-            const float e = fmaf(-sg[a], rr - 12582912.f, v);
-            e2[a] = fmaf(e, e, e2[a]);
-            const int t1 = (q + 128) >> 8;
-            hh = (t1 + 128) >> 8;
-            ll = q - (t1 << 8);
-            mm = t1 - (hh << 8);
+            const uint32_t raw = __float_as_uint(fmaf(v, inv[a], 12582912.f));
+            ll = (int)(signed char)(raw & 255u);
+            mm = (int)(signed char)(((raw + 128u) >> 8) & 255u);
+            hh = (int)(signed char)(((raw - 0x4B3F7F80u) >> 16) & 255u);
             S[a][0] += hh * hh; S[a][1] += hh * mm; S[a][2] += hh * ll;
             S[a][3] += mm * mm; S[a][4] += mm * ll; S[a][5] += ll * ll;
-        } else {
-            e2[a] = fmaf(v, v, e2[a]);
         }
-        t2[a] = fmaf(v, v, t2[a]);
         ph[col] = (int8_t)hh;
         ph[col + plane_stride] = (int8_t)mm;
         ph[col + 2 * plane_stride] = (int8_t)ll;
@@ -947,37 +970,32 @@ __global__ void __launch_bounds__(256) k_pack3_aug(RowSrc src, int64_t rows, Aug
             ph[col] = 0; ph[col + plane_stride] = 0; ph[col + 2 * plane_stride] = 0;
         }
 #pragma unroll
-    for (int a = 0; a < 3; ++a) {
-        double acc[8];
+    for (int a = 0; a < 3; ++a)
 #pragma unroll
-        for (int i = 0; i < 6; ++i) acc[i] = (double)S[a][i];
-        acc[6] = (double)e2[a];
-        acc[7] = (double)t2[a];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            for (int o = 16; o > 0; o >>= 1) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], o);
-            if (ln == 0) redd[w][a][i] = acc[i];
-        }
-    }
-    __syncthreads();
-    if (threadIdx.x < 3) {
-        const int a = threadIdx.x;
-        long long Sl[6];
-        double e = 0.0, tt[3] = {0.0, 0.0, 0.0};
         for (int i = 0; i < 6; ++i) {
-            double s = 0.0;
-            for (int j = 0; j < 8; ++j) s += redd[j][a][i];
-            Sl[i] = (long long)s;
+            long long v = S[a][i];
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (ln == 0) redd[w][a][i] = v;
         }
-        for (int j = 0; j < 8; ++j) {
-            e += redd[j][a][6];
-            for (int b = 0; b < 3; ++b) tt[b] += redd[j][b][7];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        // value block first: its centred norm bounds the FP32 slack of the derivative blocks
+        // (|fl(t1 - t0) - exact| <= 2^-24 (|D x~| + |t1| + |t0|) per element, |t| <= sqrt(n_0) + r_0)
+        double tnorm = 0.0;
+        for (int a = 0; a < 3; ++a) {
+            long long Sl[6];
+            for (int i = 0; i < 6; ++i) {
+                long long v = 0;
+                for (int j = 0; j < 8; ++j) v += redd[j][a][i];
+                Sl[i] = v;
+            }
+            const double slack = a == 0 ? 0.0 : 2.0 * 5.9604644775390625e-08 * 1.001 * tnorm;
+            float* out = meta + (orow * 3 + a) * 8;
+            write_meta(out, sg[a], inv[a], Sl, (double)len[a], slack, ex[a], 0.0);
+            if (a == 0) tnorm = sqrt((double)out[0]) * (1.0 + 1e-6) + (double)out[2];
         }
-        // value block: the FP32 centring error only (|x~|); derivative blocks: |D x~| + 2 |x~|
-        const double slack = a == 0 ? tt[0] : (sqrt(tt[a]) + 2.0 * sqrt(tt[0])) * (sqrt(tt[a]) + 2.0 * sqrt(tt[0]));
-        write_meta(meta + (orow * 3 + a) * 8, sg[a], Sl, e, slack * (1.0 + 1.0 / 4096.0), ex[a]);
+        if (anynf) atomicOr(&status[p], CIL_ITEM_NONFINITE);
     }
-    if (threadIdx.x == 0 && anynf) atomicOr(&status[p], CIL_ITEM_NONFINITE);
 }
 
 }  // namespace g3
@@ -989,18 +1007,31 @@ cudaError_t launch_pack3(int P, const RowSrc& src, int64_t rows, int64_t K, int6
     if (rows == 0) return cudaSuccess;
     dim3 grid((unsigned)rows, (unsigned)P);
     ProfScope ps_(K_PACK, st);
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    // L2 prefetch distance: half a wave of resident CTAs ahead
+    auto pf = [&](const void* fn, int nt) {
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, nt, 0);
+        return (int64_t)nsm * (per_sm > 0 ? per_sm : 1) / 2;
+    };
+#define PACK3(NV, NT)                                                                                             \
+    g3::k_pack3<NV, NT><<<grid, NT, 0, st>>>(src, rows, K, Kp, center, planes, plane_stride, row0, meta, status, \
+                                             pf((const void*)g3::k_pack3<NV, NT>, NT))
     if (Kp <= 1024)
-        g3::k_pack3<1, 256><<<grid, 256, 0, st>>>(src, rows, K, Kp, center, planes, plane_stride, row0, meta, status);
+        PACK3(1, 256);
     else if (Kp <= 4096)
-        g3::k_pack3<4, 256><<<grid, 256, 0, st>>>(src, rows, K, Kp, center, planes, plane_stride, row0, meta, status);
+        PACK3(4, 256);
     else if (Kp <= 8192)
-        g3::k_pack3<8, 256><<<grid, 256, 0, st>>>(src, rows, K, Kp, center, planes, plane_stride, row0, meta, status);
+        PACK3(8, 256);
     else if (Kp <= 16384)
-        g3::k_pack3<8, 512><<<grid, 512, 0, st>>>(src, rows, K, Kp, center, planes, plane_stride, row0, meta, status);
+        PACK3(8, 512);
     else if (Kp <= 32768)
-        g3::k_pack3<8, 1024><<<grid, 1024, 0, st>>>(src, rows, K, Kp, center, planes, plane_stride, row0, meta, status);
+        PACK3(8, 1024);
     else
         g3::k_pack3_2p<<<grid, 1024, 0, st>>>(src, rows, K, Kp, center, planes, plane_stride, row0, meta, status);
+#undef PACK3
     note_launch();
     return cudaGetLastError();
 }
@@ -1021,7 +1052,7 @@ typedef CUresult (*PFN_encodeTiled_g3)(CUtensorMap*, CUtensorMapDataType, cuuint
                                        const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                        CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-// 3-D map over the digit planes [3][rows_tot][Kp] (u8): box 64 x box_rows x 3, SWIZZLE_64B
+// 3-D map over the digit planes [3][rows_tot][Kp] (u8): box 128 x box_rows x 3, SWIZZLE_128B
 static bool make_map3(CUtensorMap* m, const void* base, int64_t rows_tot, int64_t Kp, int box_rows) {
     static PFN_encodeTiled_g3 enc = nullptr;
     if (!enc) {
@@ -1037,7 +1068,7 @@ static bool make_map3(CUtensorMap* m, const void* base, int64_t rows_tot, int64_
     cuuint32_t box[3] = {(cuuint32_t)g3::KS, (cuuint32_t)box_rows, 3u};
     cuuint32_t es[3] = {1, 1, 1};
     return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(base), dims, strides, box, es,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -1071,11 +1102,12 @@ template <int TN, bool AUG>
 static cudaError_t dispatch_g3(const g3::Params& prm, const CUtensorMap* maps, int nsm, cudaStream_t st, bool seg,
                                int M) {
     if (M <= 16) return seg ? launch_g3_t<TN, 16, true, AUG>(prm, maps, nsm, st) : launch_g3_t<TN, 16, false, AUG>(prm, maps, nsm, st);
-    if (M <= 32) return seg ? launch_g3_t<TN, 32, true, AUG>(prm, maps, nsm, st) : launch_g3_t<TN, 32, false, AUG>(prm, maps, nsm, st);
     if constexpr (AUG) {
         if (seg) return cudaErrorInvalidValue;              // the host routes these to the CUDA cores
+        if (M <= 32) return launch_g3_t<TN, 32, false, AUG>(prm, maps, nsm, st);
         return launch_g3_t<TN, 64, false, AUG>(prm, maps, nsm, st);
     } else {
+        if (M <= 32) return seg ? launch_g3_t<TN, 32, true, AUG>(prm, maps, nsm, st) : launch_g3_t<TN, 32, false, AUG>(prm, maps, nsm, st);
         return seg ? launch_g3_t<TN, 64, true, AUG>(prm, maps, nsm, st) : launch_g3_t<TN, 64, false, AUG>(prm, maps, nsm, st);
     }
 }

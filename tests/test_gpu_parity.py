@@ -190,6 +190,15 @@ def _bound_case(case, seed):
     return A, B, grid
 
 
+def test_sqrt_approx_exhaustive(cil):
+    """The INT8 engine evaluates sqrt with the hardware approximation and inflates by 2^-21
+    (gram3.cu); over EVERY normal positive FP32 input its relative error must stay below that."""
+    from paper_2203_14742_b200 import _capi
+    up, dn = _capi.sqrt_approx_error()
+    print(f"sqrt.approx.f32: max rel error above {up:.3e}, below {dn:.3e} (2^-22 = {2.0 ** -22:.3e})")
+    assert up < 2.0 ** -22 and dn < 2.0 ** -22
+
+
 @pytest.mark.parametrize("case", ["C2", "C4", "offset", "C1", "neardup0", "neardup6", "neardup3"])
 def test_gram_error_bound_i8(cil, oracle_mod, case):
     """The INT8 engine's per-pair interval [lo, hi] of the (unweighted) L2 distance must contain the

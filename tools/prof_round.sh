@@ -10,10 +10,10 @@ case $what in
     ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${tag}_launches.csv \
         $CMD > gpurun_out/${tag}_ncu_launches.log 2>&1 ;;
   gram)
-    ncu --set full --clock-control none --import-source on -k regex:k_gram_i8 -s 3 -c 1 \
+    ncu --set full --clock-control none --import-source on -k regex:k_gram3 -s 3 -c 1 \
         -o gpurun_out/${tag}_gram $CMD > gpurun_out/${tag}_ncu_gram.log 2>&1 ;;
   pack)
-    ncu --set full --clock-control none --import-source on -k "regex:k_pack_i8r|k_center" -s 9 -c 3 \
+    ncu --set full --clock-control none --import-source on -k "regex:k_pack3|k_center" -s 9 -c 3 \
         -o gpurun_out/${tag}_pack $CMD > gpurun_out/${tag}_ncu_pack.log 2>&1 ;;
 esac
 echo ${what}_rc=$?
