@@ -11,7 +11,7 @@ for k in ("roofline", "roofline_other"):
     if r:
         print(" ", k, r["kernel"][:40], r["achieved"], r["unit"], "frac", r["frac"], "share", r.get("kernel_share_of_step"))
 for k in d:
-    if k.startswith("secondary"):
+    if k.startswith("secondary") and isinstance(d[k], dict):
         s = d[k]
         print(k, s["workload"][:3], round(s["value"], 1), s["ms_per_step"], s.get("kernel_breakdown"),
               {a: b for a, b in (s.get("gram_tc") or {}).items() if "frac" in a})
