@@ -54,6 +54,25 @@ def log(*a):
 
 
 # --------------------------------------------------------------------------- setup
+def launch_ranks(args):
+    """--gpus N without a torchrun environment: re-launch this command as N ranks (one process per
+    GPU, torch.distributed.run, rendezvous on 127.0.0.1).  Under torchrun, WORLD_SIZE must equal N."""
+    world = os.environ.get("WORLD_SIZE")
+    if world is None:
+        if args.gpus > 1:
+            import socket
+            sk = socket.socket()
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+            sk.close()
+            cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+                   "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+            log(f"[bench] launching {args.gpus} ranks: {' '.join(cmd)}")
+            os.execv(sys.executable, cmd)
+    elif int(world) != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; launch with matching values")
+
+
 def dist_setup():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -90,7 +109,14 @@ class ClockSampler:
     def __init__(self, device_index):
         self.dev = device_index
         self.proc = None
-        self.lines = []
+        self.lines = []                    # (time, csv line)
+        self.t0 = self.t1 = None           # the timed region (mark_start / mark_end)
+
+    def mark_start(self):
+        self.t0 = time.time()
+
+    def mark_end(self):
+        self.t1 = time.time()
 
     def __enter__(self):
         try:
@@ -110,7 +136,7 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
 
     def __exit__(self, *a):
         if self.proc is not None:
@@ -121,9 +147,15 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
+        """Clocks under load: the samples inside the timed region when there are >= 3 of them (the
+        sampler runs from before the warm-up, so a short timed region still has neighbours),
+        else every sample from the warm-up start to the end of the timed region."""
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        inside = [ln for t, ln in self.lines if self.t0 is not None and self.t0 <= t <= (self.t1 or t)]
+        window = "timed region" if len(inside) >= 3 else "warm-up + timed region"
+        use = inside if len(inside) >= 3 else [ln for t, ln in self.lines if self.t1 is None or t <= self.t1 + 0.06]
+        for ln in use:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 7:
                 continue
@@ -138,7 +170,7 @@ class ClockSampler:
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)), "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "window": window, "interval_ms": 50}
 
 
 def timed(fn, steps, stream):
@@ -189,6 +221,16 @@ DTYPES = {"TC_I8": "int8 three-digit (22-bit) fixed point / int32 accumulate / f
           "SIMT": "f32 differences / f64 sums"}
 
 
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def peaks():
     try:
         return json.load(open(PEAKS_FILE))
@@ -237,10 +279,15 @@ def main():
     ap.add_argument("--no-c4", action="store_true")
     ap.add_argument("--no-c6", action="store_true")
     ap.add_argument("--no-c7", action="store_true")
+    ap.add_argument("--no-c5", action="store_true")
+    ap.add_argument("--c5-rows", type=int, default=20000, help="C5 rows per set (BASELINE configs[4]: 20000)")
+    ap.add_argument("--c5-mask", type=lambda v: int(v, 0), default=0x3F, help="C5 measures (default all six)")
+    ap.add_argument("--c5-steps", type=int, default=2)
     ap.add_argument("--config", default="C2", choices=["C2", "C3"],
                     help="C2 = the headline bench line; C3 = evidence run of the CUDA-core measures")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    launch_ranks(args)
 
     cfg = C2
     grid, P, N, Nt, M, mask = cfg["grid"], cfg["P"], cfg["N"], cfg["Nt"], cfg["M"], cfg["mask"]
@@ -299,23 +346,26 @@ def main():
         launches[0] += n
         return out, lst
 
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    clk = ClockSampler(local).__enter__()             # sampling from before the warm-up
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     if int(st.max()) != 0:
         log(f"[bench] WARNING item status {st.unique().tolist()}")
 
-    def barrier():
-        if world > 1:
-            import torch.distributed as dist
-            dist.barrier()
-
     # ---- timed region (device time, max over ranks)
     launches[0] = 0
     barrier()
     _capi.prof_enable(True)
-    with ClockSampler(local) as clk:
-        ms = timed(step, args.steps, stream)
+    clk.mark_start()
+    ms = timed(step, args.steps, stream)
+    clk.mark_end()
+    clk.__exit__()
     _capi.prof_enable(False)
     prof = _capi.prof_read()
     barrier()
@@ -386,6 +436,9 @@ def main():
     roof_other = [r for r in cands if r is not roof]
     kshares = {k: {"ms_per_step": round(v[0] / args.steps, 4), "launches_per_step": v[1] / args.steps}
                for k, v in prof.items() if v[1] > 0}
+    listed, _cap = cil.recheck_count(P, N, Nt, grid, mask, M, engine, ws=ws)
+    recheck = {"cases_per_step": listed, "fraction_of_pairs": listed / float(P * N * Nt),
+               "note": "(pair, measure) cases whose rigorous interval contained a radius -> exact FP64 re-check"}
 
     # ---- end-to-end through the public API with HOST buffers
     e2e = None
@@ -454,13 +507,18 @@ def main():
     c7 = None
     if not args.no_c7:
         c7 = bench_c7(cil, args, world, rank, dev, engine, stream)
-
     # ---- CPU baseline: the oracle as it stands, bounded sample, rank 0 at N = 1 only
     cpu = None
     if not args.no_cpu and world == 1 and rank == 0:
         rate, cores, sample, dt = oracle_sample_rate(A, B, grid, mask, radii_np[None, :])
         cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample,
-               "seconds": round(dt, 2)}
+               "seconds": round(dt, 2), "cpu_model": cpu_model()}
+    c5 = None
+    if not args.no_c5:
+        del A, B
+        torch.cuda.empty_cache()
+        c5 = bench_c5(cil, args, world, rank, dev, engine, stream)
+
 
     if rank == 0:
         line = {
@@ -480,11 +538,13 @@ def main():
             "roofline": roof,
             "roofline_other": roof_other[0] if roof_other else None,
             "kernel_breakdown": kshares,
+            "recheck": recheck,
             "e2e": e2e,
             "cpu_baseline": cpu,
             "secondary": c4,
             "secondary_bootstrap": c6,
             "secondary_train": c7,
+            "secondary_c5": c5,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -519,6 +579,93 @@ def pilot_radii_all(A0, B0, grid, M, mask):
             R0, RM = float(d[q].max()) * 1.001, float(d[q].min()) * 0.999
             out.append(R0 * (RM / R0) ** (np.arange(1, M + 1) / M))
     return np.array(out)
+
+
+def bench_c5(cil, args, world, rank, dev, engine, stream):
+    """C5 (BASELINE configs[4]): ONE large cross-set pair, N = Nt = 20000 patterns of 256x256x2,
+    L2 + the alternative measures (default all six), M = 20, the pair space row-block sharded over
+    the ranks (north star): rank r takes A rows row_range(N, G, r) against all of B
+    (sharding.sharded_features) and the int64 count vectors are all-reduced over NCCL — the only
+    exchange.  Strong scaling (total work fixed).  The counts are printed so runs at different G can
+    be compared: integer sums are order-free and every rank's engines see the same B, so they must
+    be bit-identical for every G."""
+    import hashlib
+
+    import torch.distributed as dist
+
+    from paper_2203_14742_b200 import _capi, sharding
+    grid, M, mask = (2, 256, 256), 20, args.c5_mask
+    N = Nt = args.c5_rows
+    seed = cilgen.config_seed(5)
+    lo, hi = sharding.row_range(N, world, rank)
+    K = grid[0] * grid[1] * grid[2]
+    nq = bin(mask).count("1")
+    need_ws = cil.features_workspace_size(1, hi - lo, Nt, grid, mask, M, engine)
+    need = need_ws + 4 * K * ((hi - lo) + Nt)
+    free = torch.cuda.mem_get_info(dev)[0]
+    res = {"workload": f"C5: one cross-set pair of {N} x {Nt} GM 256x256x2 patterns, measures mask {mask:#x}, M={M}, "
+                       f"rows sharded over {world} GPU(s), NCCL all_reduce of the int64 counts (BASELINE configs[4])",
+           "metric": "pattern-pair distances/s (all measures of the mask per pair)", "scaling": "strong",
+           "rows_this_rank": [lo, hi], "bytes_needed_per_rank": need, "bytes_free": free}
+    flag = torch.tensor([1 if need < 0.92 * free else 0], dtype=torch.int32, device=dev)
+    if world > 1:
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+    if int(flag.item()) == 0:
+        res["skipped"] = "insufficient device memory on some rank"
+        return res
+    t0 = time.time()
+    A = cilgen.make_set(seed, 0, hi - lo, grid, device=dev, row0=lo)
+    B = cilgen.make_set(seed, 1, Nt, grid, device=dev)
+    P0a = cilgen.make_set(seed, 0, 64, grid, device=dev)
+    radii = torch.tensor(pilot_radii_all(P0a, B[:64], grid, M, mask), dtype=torch.float64, device=dev)
+    del P0a
+    torch.cuda.synchronize()
+    log(f"[bench] rank {rank}: generated C5 rows [{lo}, {hi}) + B ({Nt}) in {time.time() - t0:.1f}s")
+    ws = cil.Workspace()
+
+    last = [None]
+
+    def step():
+        last[0] = sharding.sharded_features(A, B, grid, mask, radii, N, engine=engine, ws=ws)
+        return last[0]
+
+    step()                                               # warm-up (kernel attributes, workspace)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    _capi.prof_enable(True)
+    steps = max(1, args.c5_steps)
+    ms = timed(step, steps, stream)
+    _capi.prof_enable(False)
+    prof = _capi.prof_read()
+    if world > 1:
+        dist.barrier()
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_step = float(t.item()) / steps
+    counts, y, st = last[0]
+    torch.cuda.synchronize()
+    listed, cap = cil.recheck_count(1, hi - lo, Nt, grid, mask, M, engine, ws=ws)
+    c = counts[0].cpu().numpy().astype(np.int64)
+    pk_i8, psrc, nprod = tensor_peak("TC_I8")
+    kb = {k: round(v[0] / steps, 3) for k, v in prof.items() if v[1] > 0}
+    res.update({"value": N * Nt / (ms_step * 1e-3), "ms_per_step": round(ms_step, 2), "steps": steps, "warmup": 1,
+                "item_status": int(st[0].item()),
+                "counts": c.tolist(), "counts_sha256": hashlib.sha256(c.tobytes()).hexdigest()[:16],
+                "recheck_cases_this_rank": listed, "recheck_fraction_this_rank": listed / float((hi - lo) * Nt * nq),
+                "kernel_breakdown_this_rank": kb})
+    if prof["gram_tc"][1]:
+        g_ms = prof["gram_tc"][0] / steps
+        S_, H_, W_ = grid
+        Kaug = K + S_ * H_ * (W_ - 1) + S_ * (H_ - 1) * W_ if mask & 0x0C else K
+        ops = nprod * 2.0 * (hi - lo) * Nt * Kaug
+        res["gram_tc_this_rank"] = {"ms": round(g_ms, 2), "achieved_tops": round(ops / (g_ms * 1e-3) / 1e12, 1),
+                                    "peak": round(pk_i8, 1), "peak_source": psrc,
+                                    "frac": round(ops / (g_ms * 1e-3) / 1e12 / pk_i8, 4)}
+    del A, B, ws
+    torch.cuda.empty_cache()
+    return res
 
 
 def bench_c3(args, dev):
@@ -655,8 +802,7 @@ def bench_c6(cil, args, world, rank, dev, engine, stream):
         # Algorithmic int8 ops of the GEMM: 2 n_rep (M N_syn) N_syn per item.
         r_step = r_ms / steps
         res["resample"] = {"ms_per_step": round(r_step, 4), "launches_per_step": r_n / steps,
-                           "engine": "tc_rowdot" if os.environ.get("CIL_BOOT_RESAMPLE", "")[:1] != "a"
-                           and engine != cil.ENGINE_SIMT and N_set <= 127 else "atoms",
+                           "engine": "tc_rowdot" if engine != cil.ENGINE_SIMT and N_set <= 127 else "atoms",
                            "lookups_per_s": P * n_rep * N_set * Nt / (r_step * 1e-3),
                            "gemm_int8_tops_incl_helpers": round(2.0 * P * n_rep * M * N_syn * N_syn / (r_step * 1e-3)
                                                                 / 1e12, 1)}

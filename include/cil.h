@@ -131,6 +131,14 @@ CIL_API cil_status cil_features(int32_t P,
                         uint64_t* counts, double* y, int32_t* item_status,
                         cil_engine engine, void* ws, size_t ws_bytes, void* stream);
 
+/* cil_features_recheck_count — DIAGNOSTIC (synchronises): the number of (pair, measure) cases the
+ * last cil_features call on this workspace listed for the exact FP64 re-check (the engines' rigorous
+ * intervals contained a radius), and the list capacity (beyond it the exact all-pairs fallback runs
+ * and the items carry CIL_ITEM_OVERFLOW).  Arguments as cil_features_workspace_size plus the workspace. */
+CIL_API cil_status cil_features_recheck_count(int32_t P, int64_t N, int64_t Nt, cil_grid g, uint32_t dist_mask,
+                                              int32_t M, cil_engine engine, const void* ws, uint64_t* listed,
+                                              uint64_t* capacity);
+
 /* ------------------------------------------------------------------------ */
 /* cil_normalize — y[i] = (double)counts[i] / npairs for i < n (the 1/(N x N~) of Eq. (1),
  * PAPER.md:98).  Used after an all-reduce of row-block-sharded counts (each rank's
@@ -174,7 +182,8 @@ CIL_API cil_status cil_loglik(int32_t P, const double* mu, int64_t mu_stride,
  *   n_ens^2 vectors;  y~ = C(R_p, s_data, s^{k0[p],2}) (Eq. (13));
  *   out[p] = {quad, logdet, loglik} of y~ under N(mu_theta, Sigma_theta + ridge I).
  *  data   [N_set][K] (row stride ld_data), the observed patterns s_data.
- *  k0     [P] int32 in [0, n_ens), device (the caller draws it).
+ *  k0     [P] int32 in [0, n_ens), device (the caller draws it); a k0 outside that
+ *         range sets CIL_ITEM_BADINDEX on the item (y~ then uses subset 0).
  *  radii  [P][n_meas][M], device (per-theta radii).
  *  Y_out  nullable [P][n_ens*n_ens + 1][n_meas*M] FP64: the vectors, y~ last.
  * Constraints: n_ens >= 2, N_set >= 1, N_tilde >= 1, D = n_meas*M <= 192.

@@ -154,6 +154,17 @@ def features(A, B, grid, mask, radii, *, engine=ENGINE_AUTO, want_y=True, stream
     return counts, (y if want_y else None), status
 
 
+def recheck_count(P, N, Nt, grid, mask, M, engine=ENGINE_AUTO, ws: Workspace | None = None):
+    """DIAGNOSTIC (synchronises): (listed, capacity) of the exact re-check list of the last features()
+    call on the workspace `ws` (the default workspace if None)."""
+    import ctypes
+    w = (ws or _default_ws).buf
+    listed, cap = ctypes.c_uint64(), ctypes.c_uint64()
+    check(lib.cil_features_recheck_count(P, N, Nt, _grid(grid), mask, M, engine, w.data_ptr(), ctypes.byref(listed),
+                                         ctypes.byref(cap)), "cil_features_recheck_count")
+    return int(listed.value), int(cap.value)
+
+
 def normalize(counts, npairs: float, *, stream=None):
     """y = counts / npairs on the device (cil_normalize; Eq. (1) normalisation)."""
     c = counts.contiguous()

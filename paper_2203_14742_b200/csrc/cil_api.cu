@@ -500,6 +500,22 @@ cil_status cil_features(int32_t P, const float* A, int64_t strideA, int64_t lda,
     return CIL_OK;
 }
 
+cil_status cil_features_recheck_count(int32_t P, int64_t N, int64_t Nt, cil_grid g, uint32_t dist_mask, int32_t M,
+                                      cil_engine engine, const void* ws, uint64_t* listed, uint64_t* capacity) {
+    if (P < 1 || N < 0 || Nt < 0 || M < 1 || !ws || !listed || !capacity || check_grid(g, dist_mask) != CIL_OK)
+        return CIL_EINVAL;
+    const Slots sl = slots_of(dist_mask);
+    const Plan pl = make_plan(dist_mask, engine, g, Nt > 0 ? Nt : 1, Nt, M);
+    SegParams sp{N > 0 ? N : 1, Nt > 0 ? Nt : 1, 1, 1};
+    const Layout L = make_layout(P, N, Nt, g, sl.nq, M, pl, sp, 0);
+    const void* wsa = reinterpret_cast<const void*>(((uintptr_t)ws + 255) & ~(uintptr_t)255);
+    uint32_t c = 0;
+    CIL_CU(cudaMemcpy(&c, reinterpret_cast<const char*>(wsa) + L.off_ctr, sizeof(c), cudaMemcpyDeviceToHost));
+    *listed = c;
+    *capacity = L.list_cap;
+    return CIL_OK;
+}
+
 cil_status cil_normalize(int64_t n, const uint64_t* counts, double npairs, double* y, void* stream) {
     t_launches = 0;
     if (n < 0 || (n > 0 && (!counts || !y)) || !(npairs > 0.0)) return CIL_EINVAL;
@@ -782,12 +798,10 @@ struct BootLayout {
 // The GEMM form needs m1 <= 127 (int8 operand), m2 <= 65535 (u16) and n1 n2 < 2^32 (u32
 // epilogue sums); the CUDA-core engine choice keeps the shared-atomic resample.
 bool boot_rd(int32_t N_syn, int32_t N_set, int32_t n_rep, int32_t P, int nq, int32_t M, cil_engine engine) {
-    static const char* env = getenv("CIL_BOOT_RESAMPLE");   // "atoms": A/B diagnostic
-    if (env && env[0] == 'a') return false;
     if (engine == CIL_ENGINE_SIMT || N_set > 127) return false;
     const int64_t Nt = (int64_t)N_syn - N_set;
     if (Nt > 65535 || (int64_t)N_set * Nt >= (1ll << 32)) return false;
-    const int64_t ntp = ((int64_t)N_syn + 255) / 256 * 256;   // gram_i8 mode 1: b-blocks of 256
+    const int64_t ntp = ((int64_t)N_syn + 255) / 256 * 256;   // rowdot.cu: b-blocks of 256
     if ((int64_t)P * (n_rep + (int64_t)M * ntp) >= (1ll << 31)) return false;
     const int64_t kp = ((int64_t)N_syn + kTcBK - 1) / kTcBK * kTcBK;
     return 2 * (kp + ntp) * 4 <= 200 * 1024 && nq >= 1;     // k_rd_mult: 4 warps x (kp + ntp) u16
@@ -876,15 +890,12 @@ cil_status cil_synth_loglik_boot(int32_t P, const float* pools, int64_t pool_str
         for (int q = 0; q < sl.nq; ++q) {
             CIL_CU(launch_rd_build_E(P, bins, N_syn, sl.nq, q, M, B.kp_rd, B.ntp, E, st));
             CIL_CU(cudaMemsetAsync(cnt, 0, (size_t)P * n_rep * M * 8, st));
-            I8Args t{};
-            t.hq = M1; t.lq = M1;                                  // one-digit operands: the l planes are unused
-            t.rowsA = n_rep; t.rowsB = (int64_t)M * B.ntp; t.Kp = B.kp_rd; t.K = N_syn;
-            t.P = P; t.p0 = 0; t.np = P;
-            t.M = M; t.nq = 1;
-            t.sp = SegParams{t.rowsA, t.rowsB, 1, 1};
-            t.mode = 1;
-            t.m2 = M2; t.rd_nt = B.ntp; t.rd_m = M; t.rd_out = cnt;
-            CIL_CU(launch_gram_i8(t, st));
+            RowdotArgs t{};
+            t.ops = M1;                                            // M1 rows, then the E rows (stacked)
+            t.rowsA = n_rep; t.rowsB = (int64_t)M * B.ntp; t.Kp = B.kp_rd;
+            t.P = P;
+            t.m2 = M2; t.rd_nt = B.ntp; t.rd_m = M; t.out = cnt;
+            CIL_CU(launch_rowdot(t, st));
             CIL_CU(launch_rd_final(cnt, P, n_rep, M, sl.nq, q, (double)N_set * (double)Nt, Y, Ystride, st));
         }
     } else {

@@ -160,11 +160,6 @@ cudaError_t launch_pack_tc(int P, const RowSrc& src, int64_t rows, int64_t K, in
                            const float* center, int split, void* hi, void* lo, float* nrm, float* q4,
                            int32_t* status, cudaStream_t st);
 
-cudaError_t launch_pack_i8(int P, const RowSrc& src, int64_t rows, int64_t K, int64_t Kp, const float* center,
-                           int8_t* hq, int8_t* lq, float* nrm, float* scl, int32_t* status, cudaStream_t st);
-cudaError_t launch_pack_i8_pair(int P, const RowSrc& asrc, int64_t rowsA, const RowSrc& bsrc, int64_t rowsB,
-                                int64_t K, int64_t Kp, const float* center, int8_t* hq, int8_t* lq, float* nrm,
-                                float* scl, int32_t* status, cudaStream_t st);
 
 // simt_tile.cu
 struct SimtArgs {
@@ -216,49 +211,17 @@ struct TcArgs {
 };
 cudaError_t launch_gram_tc(const TcArgs& a, cudaStream_t st);
 
-// gram_i8.cu (INT8 two-digit engine)
-struct I8Args {
-    const int8_t* hq; const int8_t* lq;  // stacked [P*rowsA + P*rowsB][Kp] digits (A panels then B panels)
-    const float* nrm; const float* scl;  // stacked: sigma^2 sum q^2, sigma
-    int64_t rowsA, rowsB, Kp, K;
-    int P, p0, np;
-    const float* thr2;
-    int64_t thr_stride;
-    int M, q_l2, nq;
-    SegParams sp;
-    uint64_t* hist;
-    uint4* recheck; uint32_t* recheck_ctr; uint32_t recheck_cap;
-    float kq, kll, rel;
-    float* diag;
-    uint8_t* binout;                     // non-null: bins[p][q_l2][i][j] instead of counts
-    bool b_same;                         // B panel = A panel (rows packed once, B reads the A planes)
-    // ---- three-phase mode (the L2 family on tensor cores): the planes hold the
-    // augmented rows [x~ | D_x x~ | D_y x~], each block padded to 128 columns and quantised with
-    // its own scale; phase a = the Gram of block a (k-blocks [kb_end[a-1], kb_end[a]))
-    int nph;                             // 1 (value block only, L2) or 3
-    int kb_end[3];
-    const float* nrm3; const float* scl3;   // [rows][4]: block norms / scales (nph == 3)
-    float kll3[3];                       // kll of each block (sqrt of its length)
-    float* part;                         // [P*rowsA*rowsB][4] FP32 phase partials (d2_0, E_0, d2_x, E_x)
-    int q_tc[3];                         // histogram slot of L2, W12, W12SUM (-1: not requested)
-    float ih;                            // 1/h
-    int skip;                            // tile skipping: 0 none, 1 symmetric bins, 2 Alg. 1 triangle
-    int sm_budget;                       // SMs the persistent grid may occupy (0 = all)
-    // explicit plane offsets (rows): A rows at a_off + p rowsA, B rows at b_off + p rowsB
-    bool offs_set;
-    int64_t a_off, b_off;
-    // B columns per tile forced to 64 (a narrow B panel, e.g. the 50 s_data rows of Alg. A2's
-    // y~ against the pool as A; modes 0 without segments / three phases only); 0 = automatic
-    int tn_force;
-    bool bin_t;          // bin-matrix mode: write the transposed matrix [P][nq][rowsB][rowsA] instead
-    // mode 1 (row-dot): one-digit operands hq only; counts[p][k][v] = sum_b C[k][v rd_nt + b] m2[p][k][b]
-    int mode;
-    const uint16_t* m2;
+// rowdot.cu (bootstrap replicate counts as an integer GEMM, Alg. A1 / A2)
+struct RowdotArgs {
+    const int8_t* ops;                   // stacked operand rows: P*rowsA multiplicity rows M1, then P*rowsB rows E
+    int64_t rowsA, rowsB, Kp;            // rowsB = rd_m * rd_nt (b-major E rows)
+    int P;
+    const uint16_t* m2;                  // [P][rowsA][rd_nt] column multiplicities
     int64_t rd_nt;
     int rd_m;
-    unsigned long long* rd_out;
+    unsigned long long* out;             // [P][rowsA][rd_m] counts (accumulated atomically)
 };
-cudaError_t launch_gram_i8(const I8Args& a, cudaStream_t st);
+cudaError_t launch_rowdot(const RowdotArgs& a, cudaStream_t st);
 
 // gram3.cu (three-digit INT8 engine, the default L2 / L2-family engine; worst-case error bound)
 struct G3Args {
@@ -291,9 +254,6 @@ cudaError_t launch_pack3(int P, const RowSrc& src, int64_t rows, int64_t K, int6
 cudaError_t launch_pack3_aug(int P, const RowSrc& src, int64_t rows, const AugGeom& g, const int64_t* kp,
                              const float* center, int64_t Kc, int8_t* planes, int64_t plane_stride, int64_t row0,
                              float* meta, int32_t* status, cudaStream_t st);
-cudaError_t launch_pack_i8_aug(int P, const RowSrc& src, int64_t rows, const AugGeom& g, const int64_t* kp,
-                               const float* center, int64_t Kc, int8_t* hq, int8_t* lq, int64_t Kp_aug,
-                               float* nrm3, float* scl3, int32_t* status, cudaStream_t st);
 bool gram_tc_supported();
 
 // recheck.cu

@@ -215,357 +215,6 @@ cudaError_t launch_pack_tc(int P, const RowSrc& src, int64_t rows, int64_t K, in
     return cudaGetLastError();
 }
 
-// ------------------------------------------------------------------- INT8 pack
-// Two-digit fixed point per row for the kind::i8 tensor-core engine:
-//   x~ = x - c (FP32);  sigma = max|x~| / 32639
-//   q = rint(x~ / sigma) in [-32639, 32639];  h = floor((q + 128) / 256) in [-127, 127];
-//   l = q - 256 h in [-128, 127]
-// so x~ ~= sigma (256 h + l) with |error| <= sigma / 2.  nrm = sigma^2 sum q^2 (the exact norm of the
-// quantised row, FP64 -> FP32), scl = sigma.  The quantisation is a perturbation of the operands; its
-// effect on d^2 is bounded statistically by the epilogue's E.
-__global__ void __launch_bounds__(256) k_pack_i8(RowSrc src, int64_t rows, int64_t K, int64_t Kp,
-                                                 const float* __restrict__ center, int8_t* __restrict__ hq,
-                                                 int8_t* __restrict__ lq, float* __restrict__ nrm,
-                                                 float* __restrict__ scl, int32_t* __restrict__ status) {
-    const int64_t p = blockIdx.y;
-    const int64_t r = blockIdx.x;
-    const float* x = row_ptr(src, p, r);
-    const float* c = center + p * Kp;
-    const int64_t orow = p * rows + r;
-    __shared__ float red[32];
-    __shared__ double redd[32];
-    __shared__ int nf;
-    if (threadIdx.x == 0) nf = 0;
-    // pass 1: max |x~| (the row stays in L1/L2 for pass 2)
-    float mx = 0.f;
-    bool nonfinite = false;
-    for (int64_t k = (int64_t)threadIdx.x * 4; k < K; k += (int64_t)blockDim.x * 4) {
-        const float4 xv = __ldg(reinterpret_cast<const float4*>(x + k));
-        const float4 cv = *reinterpret_cast<const float4*>(c + k);
-        nonfinite |= !(isfinite(xv.x) && isfinite(xv.y) && isfinite(xv.z) && isfinite(xv.w));
-        mx = fmaxf(mx, fmaxf(fmaxf(fabsf(xv.x - cv.x), fabsf(xv.y - cv.y)), fmaxf(fabsf(xv.z - cv.z), fabsf(xv.w - cv.w))));
-    }
-    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
-    __syncthreads();
-    if (nonfinite) atomicOr(&nf, 1);
-    if (ln == 0) red[w] = mx;
-    __syncthreads();
-    mx = 0.f;
-    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) mx = fmaxf(mx, red[i]);
-    // sigma = max|x~| / 32639 (sigma = 1 for an all-zero row).  An exact (not power-of-two) scale:
-    // measured 2.5x smaller quantisation error on generator data; q is clamped.
-    const float sigma = (mx > 0.f && isfinite(mx)) ? mx / 32639.f : 1.f;
-    const float inv = 1.f / sigma;
-    // pass 2: quantise, split, store; exact sum of q^2
-    double s2 = 0.0;
-    for (int64_t k = (int64_t)threadIdx.x * 4; k < Kp; k += (int64_t)blockDim.x * 4) {
-        char4 hv = make_char4(0, 0, 0, 0), lv = make_char4(0, 0, 0, 0);
-        if (k < K) {
-            const float4 xv = __ldg(reinterpret_cast<const float4*>(x + k));
-            const float4 cv = *reinterpret_cast<const float4*>(c + k);
-            const float e[4] = {xv.x - cv.x, xv.y - cv.y, xv.z - cv.z, xv.w - cv.w};
-            int hh[4], ll[4];
-#pragma unroll
-            for (int t = 0; t < 4; ++t) {
-                const int q = isfinite(e[t]) ? max(-32639, min(32639, __float2int_rn(e[t] * inv))) : 0;
-                const int h = (q + 128) >> 8;          // floor((q + 128) / 256): l = q - 256 h in [-128, 127]
-                hh[t] = h;
-                ll[t] = q - 256 * h;
-                s2 += (double)q * (double)q;
-            }
-            hv = make_char4((signed char)hh[0], (signed char)hh[1], (signed char)hh[2], (signed char)hh[3]);
-            lv = make_char4((signed char)ll[0], (signed char)ll[1], (signed char)ll[2], (signed char)ll[3]);
-        }
-        *reinterpret_cast<char4*>(hq + orow * Kp + k) = hv;
-        *reinterpret_cast<char4*>(lq + orow * Kp + k) = lv;
-    }
-    for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
-    if (ln == 0) redd[w] = s2;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double a = 0.0;
-        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) a += redd[i];
-        nrm[orow] = (float)(a * (double)sigma * (double)sigma);
-        scl[orow] = sigma;
-        if (nf) atomicOr(&status[p], CIL_ITEM_NONFINITE);
-    }
-}
-
-// rint(e * inv) as q (the 1.5 * 2^23 constant: one FFMA, ties to even, exact for |q| < 2^22;
-// |e * inv| <= 32639 by construction of sigma), then the two signed digits h = (q + 128) >> 8,
-// l = q - 256 h, and q^2 (4 x 32639^2 < 2^32).  Non-finite e gives garbage digits, never a
-// fault; the item is flagged NONFINITE by the caller.
-__device__ __forceinline__ void quant4(const float4 e, float inv, char4& h4, char4& l4, uint32_t& sq) {
-    const float ev[4] = {e.x, e.y, e.z, e.w};
-    int hh[4], ll[4];
-#pragma unroll
-    for (int t = 0; t < 4; ++t) {
-        const int q = __float_as_int(fmaf(ev[t], inv, 12582912.f)) - 0x4B400000;
-        const int h = (q + 128) >> 8;
-        hh[t] = h;
-        ll[t] = q - 256 * h;
-        sq += (uint32_t)(q * q);
-    }
-    h4 = make_char4((signed char)hh[0], (signed char)hh[1], (signed char)hh[2], (signed char)hh[3]);
-    l4 = make_char4((signed char)ll[0], (signed char)ll[1], (signed char)ll[2], (signed char)ll[3]);
-}
-
-// Single-pass variant: the whole row is held in registers (NV float4 per thread, NT threads,
-// K <= NV * NT * 4), so HBM is read once; same arithmetic as k_pack_i8.
-template <int NV, int NT>
-__global__ void __launch_bounds__(NT) k_pack_i8r(RowSrc src, int64_t rows, int64_t K, int64_t Kp,
-                                                  const float* __restrict__ center, int8_t* __restrict__ hq,
-                                                  int8_t* __restrict__ lq, float* __restrict__ nrm,
-                                                  float* __restrict__ scl, int32_t* __restrict__ status,
-                                                  int64_t pf_dist) {
-    const int64_t p = blockIdx.y;
-    const int64_t r = blockIdx.x;
-    const float* x = row_ptr(src, p, r);
-    const float* c = center + p * Kp;
-    const int64_t orow = p * rows + r;
-    if (threadIdx.x == 0 && pf_dist > 0) {
-        // L2 prefetch of the row the CTA pf_dist launches later will read (about two waves
-        // ahead), so HBM keeps streaming while resident CTAs reduce / quantise / store
-        const int64_t lin = (int64_t)blockIdx.y * gridDim.x + blockIdx.x + pf_dist;
-        if (lin < (int64_t)gridDim.x * gridDim.y) {
-            const float* xn = row_ptr(src, lin / gridDim.x, lin % gridDim.x);
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(xn), "r"((uint32_t)(K * 4)) : "memory");
-        }
-    }
-    __shared__ float red[NT / 32];
-    __shared__ unsigned long long redd[NT / 32];
-    float4 v[NV];
-    float mx = 0.f, nfa = 0.f;                // nfa = sum of x * 0: NaN iff some x is not finite
-#pragma unroll
-    for (int i = 0; i < NV; ++i) {
-        const int64_t k = ((int64_t)i * NT + threadIdx.x) * 4;
-        if (k < K) {
-            const float4 xv = __ldg(reinterpret_cast<const float4*>(x + k));
-            const float4 cv = __ldg(reinterpret_cast<const float4*>(c + k));
-            nfa = fmaf(xv.x, 0.f, fmaf(xv.y, 0.f, fmaf(xv.z, 0.f, fmaf(xv.w, 0.f, nfa))));
-            v[i] = make_float4(xv.x - cv.x, xv.y - cv.y, xv.z - cv.z, xv.w - cv.w);
-        } else {
-            v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-        mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v[i].x), fabsf(v[i].y)), fmaxf(fabsf(v[i].z), fabsf(v[i].w))));
-    }
-    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
-    const bool anynf = __syncthreads_or(nfa != nfa);
-    if (ln == 0) red[w] = mx;
-    __syncthreads();
-    mx = 0.f;
-#pragma unroll
-    for (int i = 0; i < NT / 32; ++i) mx = fmaxf(mx, red[i]);
-    const float sigma = (mx > 0.f && isfinite(mx)) ? mx / 32639.f : 1.f;
-    const float inv = 1.f / sigma;
-    unsigned long long s2 = 0ull;
-#pragma unroll
-    for (int i = 0; i < NV; ++i) {
-        const int64_t k = ((int64_t)i * NT + threadIdx.x) * 4;
-        if (k >= Kp) continue;
-        char4 h4, l4;
-        uint32_t sq = 0;
-        quant4(v[i], inv, h4, l4, sq);
-        s2 += sq;
-        *reinterpret_cast<char4*>(hq + orow * Kp + k) = h4;
-        *reinterpret_cast<char4*>(lq + orow * Kp + k) = l4;
-    }
-    for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
-    if (ln == 0) redd[w] = s2;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned long long a = 0ull;
-#pragma unroll
-        for (int i = 0; i < NT / 32; ++i) a += redd[i];
-        nrm[orow] = (float)((double)a * (double)sigma * (double)sigma);
-        scl[orow] = sigma;
-        if (anynf) atomicOr(&status[p], CIL_ITEM_NONFINITE);
-    }
-}
-
-cudaError_t launch_pack_i8(int P, const RowSrc& src, int64_t rows, int64_t K, int64_t Kp, const float* center,
-                           int8_t* hq, int8_t* lq, float* nrm, float* scl, int32_t* status, cudaStream_t st) {
-    if (rows == 0) return cudaSuccess;
-    dim3 grid((unsigned)rows, (unsigned)P);
-    ProfScope ps_(K_PACK, st);
-    // prefetch distance: PF_X8 / 8 resident-CTA waves ahead (diagnostic override CIL_PACK_PF)
-    static const char* pfe = getenv("CIL_PACK_PF");
-    const int pf_x8 = pfe ? atoi(pfe) : 4;
-    int dev = 0, nsm = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    // prefetch distance in CTAs for a kernel's resident CTAs per SM
-    auto pf = [&](const void* fn, int nt) {
-        int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, nt, 0);
-        return (int64_t)pf_x8 * nsm * (per_sm > 0 ? per_sm : 1) / 8;
-    };
-    // diagnostic override of the row-kernel shape for 8192 < Kp <= 16384 (CIL_PACK_VAR:
-    // 1 = 16 float4 x 256 threads, 2 = 4 float4 x 1024 threads, 3 = the two-pass kernel)
-    static const char* pve = getenv("CIL_PACK_VAR");
-    const int pvar = pve ? atoi(pve) : 0;
-    if (Kp <= 4096)
-        k_pack_i8r<4, 256><<<grid, 256, 0, st>>>(src, rows, K, Kp, center, hq, lq, nrm, scl, status,
-                                                 pf((const void*)k_pack_i8r<4, 256>, 256));
-    else if (Kp <= 8192)
-        k_pack_i8r<8, 256><<<grid, 256, 0, st>>>(src, rows, K, Kp, center, hq, lq, nrm, scl, status,
-                                                 pf((const void*)k_pack_i8r<8, 256>, 256));
-    else if (Kp <= 16384 && pvar == 1)
-        k_pack_i8r<16, 256><<<grid, 256, 0, st>>>(src, rows, K, Kp, center, hq, lq, nrm, scl, status,
-                                                  pf((const void*)k_pack_i8r<16, 256>, 256));
-    else if (Kp <= 16384 && pvar == 2)
-        k_pack_i8r<4, 1024><<<grid, 1024, 0, st>>>(src, rows, K, Kp, center, hq, lq, nrm, scl, status,
-                                                   pf((const void*)k_pack_i8r<4, 1024>, 1024));
-    else if (Kp <= 16384 && pvar != 3)
-        k_pack_i8r<8, 512><<<grid, 512, 0, st>>>(src, rows, K, Kp, center, hq, lq, nrm, scl, status,
-                                                 pf((const void*)k_pack_i8r<8, 512>, 512));
-    else if (Kp <= 32768 && pvar != 3)
-        k_pack_i8r<8, 1024><<<grid, 1024, 0, st>>>(src, rows, K, Kp, center, hq, lq, nrm, scl, status,
-                                                   pf((const void*)k_pack_i8r<8, 1024>, 1024));
-    else
-        k_pack_i8<<<grid, 256, 0, st>>>(src, rows, K, Kp, center, hq, lq, nrm, scl, status);
-    note_launch();
-    return cudaGetLastError();
-}
-
-// Both panels (A rows then B rows in the stacked layout the Gram's TMA maps expect).
-cudaError_t launch_pack_i8_pair(int P, const RowSrc& asrc, int64_t rowsA, const RowSrc& bsrc, int64_t rowsB,
-                                int64_t K, int64_t Kp, const float* center, int8_t* hq, int8_t* lq, float* nrm,
-                                float* scl, int32_t* status, cudaStream_t st) {
-    const int64_t offB = (int64_t)P * rowsA;
-    const cudaError_t e = launch_pack_i8(P, asrc, rowsA, K, Kp, center, hq, lq, nrm, scl, status, st);
-    if (e != cudaSuccess) return e;
-    return launch_pack_i8(P, bsrc, rowsB, K, Kp, center, hq + offB * Kp, lq + offB * Kp, nrm + offB, scl + offB,
-                          status, st);
-}
-
-// ------------------------------------------------------------- INT8 augmented pack
-// Three-phase tensor-core route for the L2-type family: row x~ = x - c
-// is expanded into the blocks  value x~ (K),  D_x x~ = x~[s][r][c+1] - x~[s][r][c]
-// (S*H*(W-1), c < W-1),  D_y x~ = x~[s][r+1][c] - x~[s][r][c]  (S*(H-1)*W, r < H-1)
-// (forward differences, last node omitted, reading R3; raw differences, the 1/h is applied
-// to the distances), each block quantised with its own scale sigma_a = max|block| / 32639
-// into the two INT8 digits (h, l) at columns kp[a] + idx, zero-padded to kp[a+1];
-// norms n_a = sigma_a^2 sum q^2 (exact integer sum).  One CTA per row, two passes over the
-// (L1/L2-resident) row: block maxima, then quantisation.
-__global__ void __launch_bounds__(256) k_pack_i8_aug(RowSrc src, int64_t rows, AugGeom g, int64_t kp0, int64_t kp1,
-                                                     int64_t kp2, int64_t kp3, const float* __restrict__ center,
-                                                     int64_t Kc, int8_t* __restrict__ hq, int8_t* __restrict__ lq,
-                                                     int64_t Kp_aug, float* __restrict__ nrm3,
-                                                     float* __restrict__ scl3, int32_t* __restrict__ status) {
-    const int64_t p = blockIdx.y;
-    const int64_t r = blockIdx.x;
-    const float* x = row_ptr(src, p, r);
-    const float* c = center + p * Kc;
-    const int64_t orow = p * rows + r;
-    const int W = g.W, H = g.H, SH = g.S * g.H;
-    __shared__ float red[3][8];
-    __shared__ unsigned long long redd[3][8];
-    const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
-    // warp per grid row (s, r), lanes along the columns (no index division); the D_x neighbour
-    // comes from the next lane, the D_y neighbour from the next grid row (L1-resident)
-    auto xt = [&](int64_t e) -> float { return __ldg(x + e) - __ldg(c + e); };
-    float m0 = 0.f, mx = 0.f, my = 0.f, nfa = 0.f;
-    for (int sr = w; sr < SH; sr += 8) {
-        const bool grad = g.gs == 0 || ((g.gs >> (sr / H)) & 1u);    // species mask (R18)
-        const bool has_dy = grad && (sr % H) + 1 < H;
-        const int64_t base = (int64_t)sr * W;
-        for (int c0 = 0; c0 < W; c0 += 32) {
-            const int col = c0 + ln;
-            const bool in = col < W;
-            const float xv = in ? __ldg(x + base + col) : 0.f;
-            nfa = fmaf(xv, 0.f, nfa);
-            const float xe = in ? xv - __ldg(c + base + col) : 0.f;
-            float xn = __shfl_down_sync(0xffffffffu, xe, 1);
-            if (ln == 31 && col + 1 < W) xn = xt(base + col + 1);
-            m0 = fmaxf(m0, fabsf(xe));
-            if (grad && col + 1 < W) mx = fmaxf(mx, fabsf(xn - xe));
-            if (has_dy && in) my = fmaxf(my, fabsf(xt(base + W + col) - xe));
-        }
-    }
-    for (int o = 16; o > 0; o >>= 1) {
-        m0 = fmaxf(m0, __shfl_xor_sync(0xffffffffu, m0, o));
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-        my = fmaxf(my, __shfl_xor_sync(0xffffffffu, my, o));
-    }
-    const bool anynf = __syncthreads_or(nfa != nfa);
-    if (ln == 0) { red[0][w] = m0; red[1][w] = mx; red[2][w] = my; }
-    __syncthreads();
-    float sg[3], inv[3];
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-        float m = 0.f;
-        for (int i = 0; i < 8; ++i) m = fmaxf(m, red[a][i]);
-        sg[a] = (m > 0.f && isfinite(m)) ? m / 32639.f : 1.f;
-        inv[a] = 1.f / sg[a];
-    }
-    int8_t* ho = hq + orow * Kp_aug;
-    int8_t* lo = lq + orow * Kp_aug;
-    uint64_t s2[3] = {0ull, 0ull, 0ull};
-    auto put = [&](int a, int64_t col, float v) {
-        const int q = __float_as_int(fmaf(v, inv[a], 12582912.f)) - 0x4B400000;
-        const int hd = (q + 128) >> 8;
-        ho[col] = (int8_t)hd;
-        lo[col] = (int8_t)(q - 256 * hd);
-        s2[a] += (uint64_t)((uint32_t)(q * q));
-    };
-    for (int sr = w; sr < SH; sr += 8) {
-        const int s = sr / H;
-        const bool grad = g.gs == 0 || ((g.gs >> s) & 1u);
-        const bool has_dy = (sr % H) + 1 < H;
-        const int64_t base = (int64_t)sr * W;
-        for (int c0 = 0; c0 < W; c0 += 32) {
-            const int col = c0 + ln;
-            const bool in = col < W;
-            const float xe = in ? xt(base + col) : 0.f;
-            float xn = __shfl_down_sync(0xffffffffu, xe, 1);
-            if (ln == 31 && col + 1 < W) xn = xt(base + col + 1);
-            if (!in) continue;
-            put(0, kp0 + base + col, xe);
-            if (col + 1 < W) put(1, kp1 + (int64_t)sr * (W - 1) + col, grad ? xn - xe : 0.f);
-            if (has_dy) put(2, kp2 + base - (int64_t)s * W + col, grad ? xt(base + W + col) - xe : 0.f);
-        }
-    }
-    // zero padding of every block
-    const int64_t len[3] = {g.K, g.Kx, g.Ky}, beg[3] = {kp0, kp1, kp2}, end[3] = {kp1, kp2, kp3};
-#pragma unroll
-    for (int a = 0; a < 3; ++a)
-        for (int64_t col = beg[a] + len[a] + threadIdx.x; col < end[a]; col += 256) { ho[col] = 0; lo[col] = 0; }
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-        uint64_t v = s2[a];
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (ln == 0) redd[a][w] = v;
-    }
-    __syncthreads();
-    if (threadIdx.x < 3) {
-        const int a = threadIdx.x;
-        unsigned long long v = 0ull;
-        for (int i = 0; i < 8; ++i) v += redd[a][i];
-        nrm3[orow * 4 + a] = (float)((double)v * (double)sg[a] * (double)sg[a]);
-        scl3[orow * 4 + a] = sg[a];
-    }
-    if (threadIdx.x == 0) {
-        nrm3[orow * 4 + 3] = 0.f;
-        scl3[orow * 4 + 3] = 0.f;
-        if (anynf) atomicOr(&status[p], CIL_ITEM_NONFINITE);
-    }
-}
-
-cudaError_t launch_pack_i8_aug(int P, const RowSrc& src, int64_t rows, const AugGeom& g, const int64_t* kp,
-                               const float* center, int64_t Kc, int8_t* hq, int8_t* lq, int64_t Kp_aug,
-                               float* nrm3, float* scl3, int32_t* status, cudaStream_t st) {
-    if (rows == 0) return cudaSuccess;
-    dim3 grid((unsigned)rows, (unsigned)P);
-    ProfScope ps_(K_PACK, st);
-    k_pack_i8_aug<<<grid, 256, 0, st>>>(src, rows, g, kp[0], kp[1], kp[2], kp[3], center, Kc, hq, lq, Kp_aug, nrm3,
-                                        scl3, status);
-    note_launch();
-    return cudaGetLastError();
-}
-
 // ------------------------------------------------------------- min-max scaling
 // Scaled-pattern mode: per pattern and species s,
 //   y_s(x) = (s(x) - s_min) / (s_max - s_min)  over the species' H x W grid values,

@@ -7,7 +7,7 @@
 // k_resample: one CTA per (k, p); per-thread shared histograms [bin][thread] updated with
 // fire-and-forget shared atomics (no address conflicts), reduced once per measure.  The
 // default inside cil_synth_loglik_boot is the tensor-core form at the end of this file
-// (k_rd_mult, k_rd_build_E, gram_i8.cu mode 1, k_rd_final); k_resample serves
+// (k_rd_mult, k_rd_build_E, rowdot.cu, k_rd_final); k_resample serves
 // cil_resample_counts, the fallback, and the one-replicate y~ counts.
 #include "cil_internal.cuh"
 
@@ -166,7 +166,7 @@ cudaError_t launch_resample(int P, const uint8_t* bins, int64_t N, int64_t Nt, i
 }
 
 // ---------------------------------------------------------------- tensor-core resample
-// The same multiplicity form as one integer GEMM per measure (gram_i8.cu, mode 1):
+// The same multiplicity form as one integer GEMM per measure (rowdot.cu):
 //   counts[k][v] = sum_b m2_k[b] sum_a m1_k[a] E[v][b][a],   E[v][b][a] = [bins[a][b] > v]
 // A operand: M1 [P][n_rep][Kp] int8 (m1 <= n1 <= 127); B operand: E [P][Ntp/256][M][256][Kp] 0/1
 // bytes (b-major blocks of 256 columns)
@@ -263,7 +263,7 @@ __global__ void __launch_bounds__(256) k_rd_build_E(const uint8_t* __restrict__ 
         uint8_t v16[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) v16[i] = tile[16 * j + i][bi];
-        // b-major rows (gram_i8 mode 1): row (bt, v, i) = bt M 256 + v 256 + i for b = 256 bt + i
+        // b-major rows (rowdot.cu): row (bt, v, i) = bt M 256 + v 256 + i for b = 256 bt + i
         const int64_t b = b0 + bi;
         int8_t* dst = E + ((int64_t)p * M * Ntp + (b >> 8) * M * 256 + (b & 255)) * Kp + a0 + 16 * j;
         for (int v = 0; v < M; ++v) {

@@ -319,10 +319,7 @@ template <bool SYM>
 static cudaError_t launch_simt_s(const SimtArgs& a, cudaStream_t st) {
     if (a.do_max && a.do_sum) return launch_simt_t<true, true, 4, SYM>(a, st);
     if (a.do_max) {
-        // max family alone: 8 x 4 pairs per thread (12 LDS.128 per 128 element-pairs instead of
-        // 8 per 64); diagnostic override CIL_SIMT_RI=4
-        static const char* ri = getenv("CIL_SIMT_RI");
-        if (ri && ri[0] == '4') return launch_simt_t<true, false, 4, SYM>(a, st);
+        // max family alone: 8 x 4 pairs per thread (12 LDS.128 per 128 element-pairs instead of 8 per 64)
         return launch_simt_t<true, false, 8, SYM>(a, st);
     }
     return launch_simt_t<false, true, 4, SYM>(a, st);

@@ -79,15 +79,16 @@ __global__ void k_cov(const double* __restrict__ Y, int64_t y_stride, int n, int
     }
 }
 
-// Fused mu + Sigma for one item per CTA when Y[p] fits in shared memory (n*D*8 <= 200 KB):
+// Fused mu + Sigma for one item per CTA when Y[p] and mu fit in shared memory ((n+1)*D*8 <= 200 KB;
+// any D — the means live in the same dynamic allocation, after Y):
 // the same two-pass sums as k_mean / k_cov, with the n-long sums split over the lanes of a
 // warp (one warp per column a, then one warp per pair b <= a) and reduced by shuffles.
 constexpr int kStatsSmem = 200 * 1024;
 constexpr int kStatsThreads = 512;
 __global__ void __launch_bounds__(kStatsThreads) k_stats_smem(const double* __restrict__ Y, int64_t y_stride, int n, int D,
                                                     double* __restrict__ mu, double* __restrict__ Sigma) {
-    extern __shared__ double ys[];                   // [n][D], centred in place after pass 1
-    __shared__ double mus[kMaxD];
+    extern __shared__ double ys[];                   // [n][D], centred in place after pass 1, then mu[D]
+    double* mus = ys + (size_t)n * D;
     const int p = blockIdx.x, lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const double* Yp = Y + (int64_t)p * y_stride;
     for (int i = threadIdx.x; i < n * D; i += blockDim.x) ys[i] = Yp[i];
@@ -124,7 +125,7 @@ __global__ void __launch_bounds__(kStatsThreads) k_stats_smem(const double* __re
 static cudaError_t launch_stats_strided(int P, const double* Y, int64_t y_stride, int n, int D,
                                         double* mu, double* Sigma, cudaStream_t st) {
     ProfScope ps_(K_TAIL, st);
-    const size_t smem = sizeof(double) * (size_t)n * D;
+    const size_t smem = sizeof(double) * ((size_t)n + 1) * D;
     if (smem <= (size_t)kStatsSmem) {
         static SmemAttrOnce attr;
         if (const cudaError_t e = attr.ensure(k_stats_smem, kStatsSmem); e != cudaSuccess) return e;
@@ -274,8 +275,8 @@ __global__ void k_build_Y(int n_ens, int nq, int M, SegParams sp, const uint64_t
     else {
         rs = n_ens;
         cs = k0[p];
-        if (cs < 0 || cs >= n_ens) {
-            if (threadIdx.x == 0) atomicOr(&status[p], CIL_ITEM_BADRADII);
+        if (cs < 0 || cs >= n_ens) {                 // k0 outside [0, n_ens): an index outside its set
+            if (threadIdx.x == 0) atomicOr(&status[p], CIL_ITEM_BADINDEX);
             cs = 0;
         }
     }

@@ -1,4 +1,4 @@
-// tc_common.cuh — device helpers shared by the tensor-core engines (gram_tc.cu, gram_i8.cu):
+// tc_common.cuh — device helpers shared by the tensor-core engines (gram_tc.cu, gram3.cu, rowdot.cu):
 // mbarrier / TMA / tcgen05 (MMA, commit, TMEM ld/st) wrappers and the tile geometry.
 #pragma once
 #include <cuda.h>

@@ -31,6 +31,18 @@ def item_range(p: int, world: int, rank: int) -> tuple[int, int]:
     return row_range(p, world, rank)
 
 
+def or_status(status: torch.Tensor, *, group=None) -> torch.Tensor:
+    """Bitwise OR of the per-item status words over the group (NCCL has no BOR reduction: the bits
+    are split into 0/1 planes, all-reduced with MAX, and recombined)."""
+    world, _ = _world(group)
+    if world == 1:
+        return status
+    sh = torch.arange(8, device=status.device, dtype=status.dtype)
+    planes = (status.unsqueeze(-1) >> sh) & 1
+    dist.all_reduce(planes, op=dist.ReduceOp.MAX, group=group)
+    return (planes << sh).sum(-1).to(status.dtype)
+
+
 def _world(group):
     if not dist.is_available() or not dist.is_initialized():
         return 1, 0
@@ -53,7 +65,7 @@ def sharded_features(A_local, B, grid, mask, radii, N_total: int, *, group=None,
     world, _ = _world(group)
     if world > 1:
         dist.all_reduce(counts, op=dist.ReduceOp.SUM, group=group)
-        dist.all_reduce(status, op=dist.ReduceOp.MAX, group=group)   # bits are sticky per rank
+        status = or_status(status, group=group)
     npairs = float(N_total) * float(B.shape[0])
     if normalize_fn is None:
         from . import normalize as normalize_fn
@@ -100,14 +112,14 @@ def ring_features(A_local, B_local, grid, mask, radii, N_total: int, Nt_total: i
             reqs.append(dist.irecv(nxt, (rank - 1) % world, group=group))
         c, _, st = features_fn(A_local, cur[:sizes[src]], grid, mask, radii, want_y=False, **kw)
         counts = c if counts is None else counts + c
-        status = st if status is None else torch.maximum(status, st)
+        status = st if status is None else torch.bitwise_or(status, st)
         for r in reqs:
             r.wait()
         cur, nxt = nxt, cur
         src = (src - 1) % world
     if world > 1:
         dist.all_reduce(counts, op=dist.ReduceOp.SUM, group=group)
-        dist.all_reduce(status, op=dist.ReduceOp.MAX, group=group)
+        status = or_status(status, group=group)
     npairs = float(N_total) * float(Nt_total)
     if normalize_fn is None:
         from . import normalize as normalize_fn

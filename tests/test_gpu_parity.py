@@ -261,6 +261,19 @@ def test_stats_loglik(cil, oracle_mod):
         np.testing.assert_allclose(out2[p].cpu().numpy(), ref, rtol=0, atol=1e-6)
 
 
+@pytest.mark.parametrize("n,D", [(45, 384), (45, 13), (3, 700), (200, 300)])
+def test_stats_large_D(cil, oracle_mod, n, D):
+    """mu / Sigma for D beyond the loglik limit (6 measures x 64 radii = 384 values, the
+    45 vectors of Alg. 1 with n_ens = 10) — both the shared-memory and the global kernels."""
+    O = oracle_mod
+    rng = np.random.default_rng(D)
+    Y = rng.random((n, D)) * 0.5 + np.linspace(0.9, 0.1, D)
+    mu, Sig = cil.stats(torch.tensor(Y, device="cuda"))
+    mu_r, Sig_r = O.stats(Y)
+    assert np.max(np.abs(mu.cpu().numpy() - mu_r)) <= 1e-6 * np.max(np.abs(mu_r))
+    assert np.max(np.abs(Sig.cpu().numpy() - Sig_r)) <= 1e-6 * np.max(np.abs(Sig_r))
+
+
 def test_loglik_notpd_and_large_D(cil, oracle_mod):
     O = oracle_mod
     dev = torch.device("cuda")
@@ -513,8 +526,8 @@ def test_gradient_species_mask(cil, oracle_mod, engine, grid):
 
 
 def test_c5_shape_large_K(cil, oracle_mod):
-    """C5-shaped patterns (256x256x2, K = 131072 > 65536: AUTO takes the chunked 3xBF16 engine
-    for L2, the CUDA cores for the rest), ragged 200 x 150 pairs, L2 + W12 + Linf."""
+    """C5-shaped patterns (256x256x2, K = 131072 > 65536: the INT8 engine accumulates in two exact
+    K chunks, the three-phase family in two chunks per block), ragged 200 x 150 pairs, L2 + W12 + Linf."""
     O = oracle_mod
     dev = torch.device("cuda")
     grid = (2, 256, 256, 0.0)
@@ -524,6 +537,53 @@ def test_c5_shape_large_K(cil, oracle_mod):
     D = O.distance_matrix(A[:30].numpy(), B[:30].numpy(), grid, mask)
     radii = np.array([np.quantile(d, np.linspace(0.97, 0.03, 12)) for d in D])
     c, _, st = _run_features(cil, A, B, grid, mask, radii, "AUTO")
+    assert int(st[0]) == 0
+    _check_counts(c[0], O.features(A.numpy(), B.numpy(), grid, mask, radii, band=BAND))
+
+
+def test_c5_row_sample_all_measures(cil, oracle_mod):
+    """C5 (BASELINE configs[4]) at its full K_aug: 64 rows of A x 1000 rows of B of the bench's
+    256x256x2 sets (seed of config 5), all six measures, M = 20, against the oracle."""
+    O = oracle_mod
+    grid = (2, 256, 256, 0.0)
+    seed = cilgen.config_seed(5)
+    A = cilgen.make_set(seed, 0, 64, grid[:3])
+    B = cilgen.make_set(seed, 1, 1000, grid[:3])
+    D = O.distance_matrix(A[:24].numpy(), B[:200].numpy(), grid, 0x3F)
+    radii = np.array([np.quantile(d, np.linspace(0.98, 0.02, 20)) for d in D])
+    c, _, st = _run_features(cil, A, B, grid, 0x3F, radii, "AUTO")
+    assert int(st[0]) == 0
+    _check_counts(c[0], O.features(A.numpy(), B.numpy(), grid, 0x3F, radii, band=BAND))
+
+
+@pytest.mark.parametrize("engine", ["AUTO", "SIMT"])
+def test_c3_row_sample_all_measures(cil, oracle_mod, engine):
+    """C3 (BASELINE configs[2]): 32 rows of A x all 2000 rows of B of the bench's 128x128x2 sets,
+    all six measures, M = 20, against the oracle (the bench times 2000 x 2000)."""
+    O = oracle_mod
+    grid = (2, 128, 128, 0.0)
+    seed = cilgen.config_seed(3)
+    A = cilgen.make_set(seed, 0, 32, grid[:3])
+    B = cilgen.make_set(seed, 1, 2000, grid[:3])
+    D = O.distance_matrix(A[:16].numpy(), B[:300].numpy(), grid, 0x3F)
+    radii = np.array([np.quantile(d, np.linspace(0.98, 0.02, 20)) for d in D])
+    c, _, st = _run_features(cil, A, B, grid, 0x3F, radii, engine)
+    assert int(st[0]) == 0
+    _check_counts(c[0], O.features(A.numpy(), B.numpy(), grid, 0x3F, radii, band=BAND))
+
+
+@pytest.mark.parametrize("engine", ["TC_I8", "AUTO", "SIMT"])
+@pytest.mark.parametrize("mask", [0x01, 0x0D, 0x3F])
+def test_many_radii(cil, oracle_mod, engine, mask):
+    """M = 48 radii (the MAXM = 64 instantiations of the INT8 engines, one- and three-phase), with
+    ragged 300 x 270 sets spanning several tiles, radii at dense quantiles of the distances."""
+    O = oracle_mod
+    grid = (2, 24, 24, 0.0)
+    A = cilgen.make_set(57, 0, 300, grid[:3])
+    B = cilgen.make_set(57, 1, 270, grid[:3])
+    D = _sel(O.distance_matrix(A[:60].numpy(), B[:60].numpy(), grid, 0x3F), mask)
+    radii = np.array([np.quantile(d, np.linspace(0.99, 0.01, 48)) for d in D])
+    c, _, st = _run_features(cil, A, B, grid, mask, radii, engine)
     assert int(st[0]) == 0
     _check_counts(c[0], O.features(A.numpy(), B.numpy(), grid, mask, radii, band=BAND))
 

@@ -52,7 +52,11 @@ def _worker(rank, world, port, q):
         Pl = 3
         y_local = torch.full((Pl, 4), float(rank)) + torch.arange(Pl * 4, dtype=torch.float64).view(Pl, 4)
         Y = sharding.gather_vectors(y_local)
-        q.put((rank, counts.numpy(), y.numpy(), Y.numpy(), (lo, hi)))
+        # item status words are OR-ed across ranks (rank r reports bit r of NONFINITE / NOTPD /
+        # BADRADII / OVERFLOW: a MAX reduction would drop the lower bits)
+        st_local = torch.tensor([1 << rank, 0, (1 << rank) | 16], dtype=torch.int32)
+        st_or = sharding.or_status(st_local)
+        q.put((rank, counts.numpy(), y.numpy(), Y.numpy(), (lo, hi), st_or.numpy()))
     finally:
         dist.destroy_process_group()
 
@@ -77,9 +81,12 @@ def test_sharded_counts_equal_unsharded(oracle_mod, world):
     radii = np.array([np.geomspace(3.0, 0.5, 6), np.geomspace(3.0, 0.3, 6)])
     full = oracle_mod.features(A, B, grid, 0b11, radii, band=0.0)
     ranges = [r[4] for r in res]
+    want = sum(1 << r for r in range(world))
+    for r in res:
+        assert r[5].tolist() == [want, 0, want | 16]
     assert ranges[0][0] == 0 and ranges[-1][1] == 23
     assert all(ranges[i][1] == ranges[i + 1][0] for i in range(world - 1))
-    for rank, counts, y, Y, _ in res:
+    for rank, counts, y, Y, _, _ in res:
         np.testing.assert_array_equal(counts[0], full["counts"])          # identical on every rank
         np.testing.assert_array_equal(y[0], full["counts"] / (23 * 9))
         assert Y.shape == (world * 3, 4)
