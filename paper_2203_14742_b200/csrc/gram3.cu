@@ -118,7 +118,11 @@ template <int TN, int MAXM, bool SEG, bool AUG> struct Geo3 {
     static constexpr int THRB = 3 * 2 * 2 * MAXM * 4;           // [kind][rd/ru][2 MAXM]
     static constexpr int FIXED = 1024 + 1024 + COLB + THRB + HIST;
     static constexpr int FIT = (227 * 1024 - FIXED) / STAGE;
+#ifdef CIL_G3_MAXSTAGES
+    static constexpr int STAGES = FIT > CIL_G3_MAXSTAGES ? CIL_G3_MAXSTAGES : FIT;   // experiment builds only
+#else
     static constexpr int STAGES = FIT > 4 ? 4 : FIT;
+#endif
     static constexpr int SMEM = STAGES * STAGE + FIXED;
     static constexpr int TCOLS = 4 * TN <= 256 ? 256 : 512;
     static_assert(FIT >= 2, "shared memory");
