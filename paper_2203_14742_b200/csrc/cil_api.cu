@@ -8,6 +8,8 @@
 
 #include "cil_internal.cuh"
 
+#include <nvtx3/nvToolsExt.h>
+
 #include <vector>
 
 namespace cil {
@@ -36,13 +38,24 @@ static cudaEvent_t ev_get() {
     return e;
 }
 
+// NVTX ranges: one per public call (NvtxScope below) and one per kernel class launch (ProfScope),
+// visible in Nsight timelines; no-ops when no tool is attached (NVTX v3, header-only)
+static const char* const kClassName[K_NCLASS] = {"cil:prep",     "cil:pack", "cil:gram_tc", "cil:simt_tile",
+                                                 "cil:recheck",  "cil:tail", "cil:resample"};
+struct NvtxScope {
+    explicit NvtxScope(const char* name) { nvtxRangePushA(name); }
+    ~NvtxScope() { nvtxRangePop(); }
+};
+
 ProfScope::ProfScope(int c, cudaStream_t s) : cls(c), st(s), ev0(nullptr) {
+    nvtxRangePushA(kClassName[c]);
     if (!t_prof_on) return;
     cudaEvent_t e = ev_get();
     cudaEventRecord(e, s);
     ev0 = e;
 }
 ProfScope::~ProfScope() {
+    nvtxRangePop();
     if (!ev0) return;
     cudaEvent_t e = ev_get();
     cudaEventRecord(e, st);
@@ -470,6 +483,7 @@ cil_status cil_features(int32_t P, const float* A, int64_t strideA, int64_t lda,
                         const double* radii, int64_t radii_stride, int32_t M, uint64_t* counts, double* y,
                         int32_t* item_status, cil_engine engine, void* ws, size_t ws_bytes, void* stream) {
     t_launches = 0;
+    NvtxScope nv_("cil_status");
     if (P < 1 || N < 0 || Nt < 0 || M < 1 || M > kMaxM) return CIL_EINVAL;
     if (check_grid(g, dist_mask) != CIL_OK) return CIL_EINVAL;
     if ((int)engine < 0 || (int)engine > 4) return CIL_EINVAL;
@@ -518,6 +532,7 @@ cil_status cil_features_recheck_count(int32_t P, int64_t N, int64_t Nt, cil_grid
 
 cil_status cil_normalize(int64_t n, const uint64_t* counts, double npairs, double* y, void* stream) {
     t_launches = 0;
+    NvtxScope nv_("cil_status");
     if (n < 0 || (n > 0 && (!counts || !y)) || !(npairs > 0.0)) return CIL_EINVAL;
     CIL_CU(launch_normalize(n, counts, npairs, y, reinterpret_cast<cudaStream_t>(stream)));
     return CIL_OK;
@@ -526,6 +541,7 @@ cil_status cil_normalize(int64_t n, const uint64_t* counts, double npairs, doubl
 cil_status cil_stats(int32_t P, const double* Y, int32_t n, int32_t D, double* mu, double* Sigma,
                      void* stream) {
     t_launches = 0;
+    NvtxScope nv_("cil_status");
     if (P < 1 || n < 2 || D < 1 || !Y || !mu || !Sigma) return CIL_EINVAL;
     CIL_CU(launch_stats(P, Y, n, D, mu, Sigma, reinterpret_cast<cudaStream_t>(stream)));
     return CIL_OK;
@@ -535,6 +551,7 @@ cil_status cil_loglik(int32_t P, const double* mu, int64_t mu_stride, const doub
                       const double* y_obs, int32_t D, double ridge, double* out, int32_t* item_status,
                       void* stream) {
     t_launches = 0;
+    NvtxScope nv_("cil_status");
     if (P < 1 || D < 1 || !mu || !Sigma || !y_obs || !out || !item_status) return CIL_EINVAL;
     if (D > kMaxD) return CIL_EUNSUPPORTED;
     if (mu_stride < 0 || Sigma_stride < 0 || !(ridge >= 0.0)) return CIL_EINVAL;
@@ -593,6 +610,7 @@ cil_status cil_synth_loglik(int32_t P, const float* pools, int64_t pool_stride, 
                             double ridge, double* out, int32_t* item_status, double* Y_out, cil_engine engine,
                             void* ws, size_t ws_bytes, void* stream) {
     t_launches = 0;
+    NvtxScope nv_("cil_status");
     if (P < 1 || n_ens < 2 || N_set < 1 || N_tilde < 1 || M < 1 || M > kMaxM) return CIL_EINVAL;
     if (check_grid(g, dist_mask) != CIL_OK) return CIL_EINVAL;
     if ((int)engine < 0 || (int)engine > 4) return CIL_EINVAL;
@@ -637,6 +655,7 @@ cil_status cil_synth_loglik(int32_t P, const float* pools, int64_t pool_stride, 
 cil_status cil_minmax_scale(int64_t n, const float* X, int64_t ldx, float* Y, int64_t ldy, cil_grid g,
                             void* stream) {
     t_launches = 0;
+    NvtxScope nv_("cil_status");
     if (n < 0 || g.S < 1 || g.H < 1 || g.W < 1) return CIL_EINVAL;
     const int64_t K = (int64_t)g.S * g.H * g.W;
     if (n > 0 && (!X || !Y || ldx < K || ldy < K)) return CIL_EINVAL;
@@ -657,6 +676,7 @@ cil_status cil_distance_range(int32_t P, const float* A, int64_t strideA, int64_
                               int64_t strideB, int64_t ldb, int64_t Nt, cil_grid g, uint32_t dist_mask,
                               double* range, int32_t* item_status, void* ws, size_t ws_bytes, void* stream) {
     t_launches = 0;
+    NvtxScope nv_("cil_status");
     if (P < 1 || N < 1 || Nt < 1) return CIL_EINVAL;
     if (check_grid(g, dist_mask) != CIL_OK) return CIL_EINVAL;
     if (!range || !item_status || !ws) return CIL_EINVAL;
@@ -683,6 +703,7 @@ cil_status cil_distance_range(int32_t P, const float* A, int64_t strideA, int64_
 cil_status cil_radii_from_range(int32_t P, int32_t n_meas, int32_t M, const double* range, int32_t law,
                                 double margin, double* radii, int32_t* item_status, void* stream) {
     t_launches = 0;
+    NvtxScope nv_("cil_status");
     if (P < 1 || n_meas < 1 || n_meas > kMaxMeas || M < 1 || M > kMaxM || (law != 0 && law != 1)) return CIL_EINVAL;
     if (!range || !radii || !item_status || !(margin >= 0.0 && margin < 1.0)) return CIL_EINVAL;
     CIL_CU(launch_radii(P, n_meas, M, reinterpret_cast<const unsigned long long*>(range), law, margin, radii,
@@ -706,6 +727,7 @@ cil_status cil_train_vectors(int32_t P, const float* X, int64_t stride, int64_t 
                              double* Y, int32_t* item_status, cil_engine engine, void* ws, size_t ws_bytes,
                              void* stream) {
     t_launches = 0;
+    NvtxScope nv_("cil_status");
     if (P < 1 || n_ens < 2 || N < 1 || M < 1 || M > kMaxM) return CIL_EINVAL;
     if (check_grid(g, dist_mask) != CIL_OK) return CIL_EINVAL;
     if ((int)engine < 0 || (int)engine > 4) return CIL_EINVAL;
@@ -748,6 +770,7 @@ cil_status cil_bin_matrix(int32_t P, const float* A, int64_t strideA, int64_t ld
                           const double* radii, int64_t radii_stride, int32_t M, uint8_t* bins,
                           int32_t* item_status, cil_engine engine, void* ws, size_t ws_bytes, void* stream) {
     t_launches = 0;
+    NvtxScope nv_("cil_status");
     if (P < 1 || N < 0 || Nt < 0 || M < 1 || M > kMaxM) return CIL_EINVAL;
     if (check_grid(g, dist_mask) != CIL_OK) return CIL_EINVAL;
     if ((int)engine < 0 || (int)engine > 4) return CIL_EINVAL;
@@ -774,6 +797,7 @@ cil_status cil_resample_counts(int32_t P, const uint8_t* bins, int64_t N, int64_
                                uint64_t* counts, double* y, int64_t y_item_stride, int32_t* item_status,
                                void* stream) {
     t_launches = 0;
+    NvtxScope nv_("cil_status");
     if (P < 1 || N < 1 || Nt < 1 || n_meas < 1 || n_meas > kMaxMeas || M < 1 || M > kMaxM) return CIL_EINVAL;
     if (n_rep < 1 || n1 < 1 || n2 < 1 || !bins || !I1 || !I2 || !item_status || (!counts && !y)) return CIL_EINVAL;
     if (y_item_stride < 0 || (y && y_item_stride > 0 && y_item_stride < (int64_t)n_rep * n_meas * M))
@@ -850,6 +874,7 @@ cil_status cil_synth_loglik_boot(int32_t P, const float* pools, int64_t pool_str
                                  int32_t* item_status, double* Y_out, cil_engine engine, void* ws, size_t ws_bytes,
                                  void* stream) {
     t_launches = 0;
+    NvtxScope nv_("cil_status");
     if (P < 1 || N_set < 1 || N_syn <= N_set || n_rep < 2 || M < 1 || M > kMaxM) return CIL_EINVAL;
     if (check_grid(g, dist_mask) != CIL_OK) return CIL_EINVAL;
     if ((int)engine < 0 || (int)engine > 4) return CIL_EINVAL;
@@ -970,6 +995,7 @@ cil_status cil_synth_loglik_boot(int32_t P, const float* pools, int64_t pool_str
 cil_status cil_diag_gram(const float* A, int64_t lda, int64_t N, const float* B, int64_t ldb, int64_t Nt,
                          cil_grid g, cil_engine engine, float* d2E, void* ws, size_t ws_bytes, void* stream) {
     t_launches = 0;
+    NvtxScope nv_("cil_status");
     if (N < 1 || Nt < 1 || !A || !B || !d2E || !ws) return CIL_EINVAL;
     if (engine != CIL_ENGINE_TC_3XBF16 && engine != CIL_ENGINE_TC_3XTF32 && engine != CIL_ENGINE_TC_I8)
         return CIL_EINVAL;
@@ -997,6 +1023,7 @@ cil_status cil_diag_gram(const float* A, int64_t lda, int64_t N, const float* B,
 cil_status cil_diag_gram_family(const float* A, int64_t lda, int64_t N, const float* B, int64_t ldb, int64_t Nt,
                                 cil_grid g, float* vE, void* ws, size_t ws_bytes, void* stream) {
     t_launches = 0;
+    NvtxScope nv_("cil_status");
     if (N < 1 || Nt < 1 || !A || !B || !vE || !ws) return CIL_EINVAL;
     const uint32_t mask = CIL_L2 | CIL_W12SUM | CIL_W12;
     if (check_grid(g, mask) != CIL_OK) return CIL_EINVAL;
