@@ -350,6 +350,12 @@ CIL_API int32_t cil_diag_alu_ceiling(int32_t mix, int32_t iters, double* element
  * synchronises (diagnostic only).  Returns 0, or -1 on a CUDA error. */
 CIL_API int32_t cil_diag_sqrt_approx_error(double* max_rel_up, double* max_rel_down);
 
+/* cil_diag_bounds_violations — DIAGNOSTIC: in a bounds-checked build (-DCIL_BOUNDS_CHECK, used in
+ * place of compute-sanitizer, which this GPU pool does not allow) the number of out-of-range global
+ * accesses the INT8 engine, the CUDA-core engine and the re-check detected since load (synchronous);
+ * -1 in the normal build. */
+CIL_API int64_t cil_diag_bounds_violations(void);
+
 /* ------------------------------------------------------------------------ */
 /* Kernel timing (diagnostics, used by bench.py for the live roofline).  While enabled on
  * the calling host thread, every kernel the library launches is bracketed by CUDA events

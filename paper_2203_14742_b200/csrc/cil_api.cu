@@ -315,6 +315,7 @@ RecheckArgs recheck_args(const RowSrc& asrc, const RowSrc& bsrc, int64_t K, cons
     r.binout = binout; r.rowsA = rowsA; r.rowsB = rowsB;
     r.mirror = binout != nullptr && same_rows(asrc, bsrc) && rowsA == rowsB;
     r.S = g.S; r.H = g.H; r.W = g.W; r.gs = g.gs;
+    r.hist_elems = L.hist_elems;
     return r;
 }
 
@@ -420,6 +421,7 @@ cil_status run_engines(int P, const RowSrc& asrc, const RowSrc& bsrc, int64_t ro
             t.binout = binout;
             t.skip = (binout && b_same) ? 1 : (b_same ? tile_skip : 0);
             t.diag = diag;
+            t.hist_elems = L.hist_elems;
             CIL_CU(launch_gram3(t, st));
         } else {
             // ---- 3xBF16 / 3xTF32 split engine (histogram mode only)
@@ -1075,6 +1077,14 @@ int32_t cil_prof_read(double* ms, int64_t* launches) {
     }
     t_prof->clear();
     return K_NCLASS;
+}
+
+int64_t cil_diag_bounds_violations(void) {
+#ifdef CIL_BOUNDS_CHECK
+    return (int64_t)oob_gram3() + oob_recheck() + oob_simt();
+#else
+    return -1;
+#endif
 }
 
 int32_t cil_last_cuda_error(void) { return t_last_cuda; }

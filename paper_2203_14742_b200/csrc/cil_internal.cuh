@@ -28,6 +28,32 @@ struct SmemAttrOnce {
 };
 
 
+// Bounds-checked builds (-DCIL_BOUNDS_CHECK, tools/bounds_check.sh; compute-sanitizer is closed on
+// this pool): CIL_CHECK counts index violations of the engines' computed global accesses in a
+// per-translation-unit device counter (no trap, so a violation cannot take the GPU down);
+// cil_diag_bounds_violations() sums the counters.  Compiled out otherwise.
+#ifdef CIL_BOUNDS_CHECK
+static __device__ unsigned int cil_oob_count;
+#define CIL_CHECK(c)                                   \
+    do {                                               \
+        if (!(c)) atomicAdd(&cil_oob_count, 1u);       \
+    } while (0)
+#define CIL_OOB_READER(fn)                                                               \
+    unsigned int fn() {                                                                  \
+        unsigned int v = 0;                                                              \
+        return cudaMemcpyFromSymbol(&v, cil_oob_count, sizeof(v)) == cudaSuccess ? v : ~0u; \
+    }
+#else
+#define CIL_CHECK(c) \
+    do {             \
+    } while (0)
+#define CIL_OOB_READER(fn) \
+    unsigned int fn() { return 0u; }
+#endif
+unsigned int oob_gram3();
+unsigned int oob_recheck();
+unsigned int oob_simt();
+
 constexpr int kMaxM = 64;        // radii per measure
 constexpr int kMaxMeas = 6;
 constexpr int kMaxD = 192;       // n_meas * M for loglik (packed Cholesky factor in smem)
@@ -246,6 +272,7 @@ struct G3Args {
     int skip;                            // 0 all tiles; 1 symmetric bin matrix; 2 Alg. 1 blocks k < l
     int tn_force;                        // 64: narrow B panel (<= 64 rows)
     float* diag;                         // diagnostics: (lo, hi) per pair of item 0, no binning
+    int64_t hist_elems;                  // histogram size (bounds-checked builds)
 };
 cudaError_t launch_gram3(const G3Args& a, cudaStream_t st);
 cudaError_t launch_pack3(int P, const RowSrc& src, int64_t rows, int64_t K, int64_t Kp, const float* center,
@@ -277,6 +304,7 @@ struct RecheckArgs {
     int64_t rowsA, rowsB;
     int S, H, W;
     uint32_t gs;
+    int64_t hist_elems;  // bounds-checked builds
 };
 cudaError_t launch_recheck(const RecheckArgs& a, int64_t hist_elems, cudaStream_t st);
 

@@ -94,6 +94,7 @@ struct Params {
     uint8_t* binout;
     int bin_t;
     float* diag;                       // diagnostics: per pair (lo, hi), item 0 only, no binning
+    int64_t hist_elems;                // bounds-checked builds only
 };
 
 template <int TN, int MAXM, bool SEG, bool AUG> struct Geo3 {
@@ -407,6 +408,8 @@ __device__ __forceinline__ void epilogue(const Params& prm, uint32_t tmem_base, 
                             if (gi * 16 + jj >= nvalid) break;
                             const int64_t col = hc0 + gi * 16 + jj;
                             const uint8_t bv = (uint8_t)(bins[jj] & 255);
+                            CIL_CHECK(row < prm.rowsA && col < prm.rowsB && mb + prm.rowsA * prm.rowsB <=
+                                      (int64_t)prm.P * prm.nq * prm.rowsA * prm.rowsB);
                             if (prm.bin_t) prm.binout[mb + col * prm.rowsA + row] = bv;
                             else prm.binout[mb + row * prm.rowsB + col] = bv;
                             if (sym_up) prm.binout[mb + col * prm.rowsB + row] = bv;
@@ -444,6 +447,7 @@ __device__ __forceinline__ void epilogue(const Params& prm, uint32_t tmem_base, 
                         const float dn = fmaxf(__fsub_rd(sqrt_dn(lo2), rho), 0.f);
                         const int64_t pi = pbase + col;
                         if (ph < 2) {
+                            CIL_CHECK(pi >= 0 && pi < npairs && col < prm.rowsB);
                             prm.part[ph * npairs + pi] = make_float2(dn, up);
                             continue;
                         }
@@ -478,6 +482,7 @@ __device__ __forceinline__ void epilogue(const Params& prm, uint32_t tmem_base, 
                             const int b = bin_search<MAXM>(vhi, Tlo);
                             if (prm.binout != nullptr) {
                                 uint8_t* bm = prm.binout + ((int64_t)p * prm.nq + prm.q_k[k]) * prm.rowsA * prm.rowsB;
+                                CIL_CHECK(row < prm.rowsA && col < prm.rowsB && prm.q_k[k] < prm.nq);
                                 bm[row * prm.rowsB + col] = (uint8_t)b;
                                 if (sym_up) bm[col * prm.rowsB + row] = (uint8_t)b;
                                 if (sym_band && col < row) continue;
@@ -518,6 +523,8 @@ __device__ __forceinline__ void epilogue(const Params& prm, uint32_t tmem_base, 
                     const int64_t cs = cs_first + l;
                     if (cs * prm.sp.col_seg >= prm.rowsB || cs * prm.sp.col_seg >= hc0 + ncol) break;
                     const uint32_t v = SEG ? ((cell >> (8 * l)) & 255u) : ((cell >> (8 * (bb & 3))) & 255u);
+                    CIL_CHECK(hist_index(prm.sp, prm.nq, M, p, uniform ? rs0 : rs, cs, q, bb) < prm.hist_elems &&
+                              cs < prm.sp.n_cs && (uniform ? rs0 : rs) < prm.sp.n_rs);
                     if (uniform) {
                         const uint32_t tot = __reduce_add_sync(0xffffffffu, v);
                         if (lane == 0 && tot)
@@ -773,6 +780,7 @@ __global__ void __launch_bounds__(NT) k_pack3(RowSrc src, int64_t rows, int64_t 
         uint32_t wh = 0, wm = 0, wl = 0;
         if (ok) quant4(v[i], inv, wh, wm, wl, S);
         int8_t* o = planes + orow * Kp + k;
+        CIL_CHECK(orow * Kp + k + 4 <= plane_stride);
         *reinterpret_cast<uint32_t*>(o) = wh;
         *reinterpret_cast<uint32_t*>(o + plane_stride) = wm;
         *reinterpret_cast<uint32_t*>(o + 2 * plane_stride) = wl;
@@ -843,6 +851,7 @@ __global__ void __launch_bounds__(1024) k_pack3_2p(RowSrc src, int64_t rows, int
         uint32_t wh = 0, wm = 0, wl = 0;
         if (ok) quant4(v, inv, wh, wm, wl, S);
         int8_t* o = planes + orow * Kp + k;
+        CIL_CHECK(orow * Kp + k + 4 <= plane_stride);
         *reinterpret_cast<uint32_t*>(o) = wh;
         *reinterpret_cast<uint32_t*>(o + plane_stride) = wm;
         *reinterpret_cast<uint32_t*>(o + 2 * plane_stride) = wl;
@@ -1171,6 +1180,7 @@ cudaError_t launch_gram3(const G3Args& a, cudaStream_t st) {
     prm.bin_t = a.bin_t ? 1 : 0;
     if (a.bin_t && (a.skip != 0 || !a.binout || prm.nph != 1)) return cudaErrorInvalidValue;
     prm.diag = a.diag;
+    prm.hist_elems = a.hist_elems;
     const bool seg = a.sp.col_seg < a.rowsB;
     if (seg && a.sp.col_seg < 21) return cudaErrorInvalidValue;
     if (tn == 64) {
@@ -1182,5 +1192,7 @@ cudaError_t launch_gram3(const G3Args& a, cudaStream_t st) {
     if (prm.nph == 3) return dispatch_g3<128, true>(prm, maps, nsm, st, seg, a.M);
     return dispatch_g3<128, false>(prm, maps, nsm, st, seg, a.M);
 }
+
+CIL_OOB_READER(oob_gram3)
 
 }  // namespace cil

@@ -105,6 +105,7 @@ __device__ double measure(int k, const double sub[6], double w, double h) {
 __device__ void settle(const RecheckArgs& a, int64_t p, int64_t i, int64_t j, int kind, int b_lo, double d,
                        bool add_only) {
     const int q = a.qslot[kind];
+    CIL_CHECK(kind >= 0 && kind < 6 && q >= 0 && q < a.nq && p < a.P && i < a.rowsA && j < a.rowsB);
     const double* R = a.thr + p * a.thr_stride + (int64_t)q * a.M;
     int b = 0;
     while (b < a.M && d < R[b]) ++b;
@@ -116,6 +117,7 @@ __device__ void settle(const RecheckArgs& a, int64_t p, int64_t i, int64_t j, in
     } else {
         const int64_t rs = i / a.sp.row_seg, cs = j / a.sp.col_seg;
         unsigned long long* H = (unsigned long long*)a.hist;
+        CIL_CHECK(hist_index(a.sp, a.nq, a.M, p, rs, cs, q, a.M) < a.hist_elems);
         if (add_only) {
             if (b > 0) atomicAdd(&H[hist_index(a.sp, a.nq, a.M, p, rs, cs, q, b)], 1ull);
         } else if (b != b_lo) {
@@ -179,5 +181,7 @@ cudaError_t launch_recheck(const RecheckArgs& a, int64_t hist_elems, cudaStream_
     note_launch();
     return cudaGetLastError();
 }
+
+CIL_OOB_READER(oob_recheck)
 
 }  // namespace cil

@@ -258,6 +258,7 @@ __global__ void __launch_bounds__(NTHR, (DO_SUM || RI == 8) ? 2 : 4) k_simt(Simt
                         a.list[idx] = make_uint4((uint32_t)p, (uint32_t)gi, (uint32_t)gj, (uint32_t)b | ((uint32_t)kind << 8));
                 }
                 if (a.binout) {              // bin-matrix mode (bootstrap, Alg. A1 / A2)
+                    CIL_CHECK(gi < a.rowsA && gj < a.rowsB && q < nq);
                     a.binout[(((int64_t)p * nq + q) * a.rowsA + gi) * a.rowsB + gj] = (uint8_t)b;
                     // d(i, j) and d(j, i) are bit-identical here (exact negations, same order), so
                     // a straddling tile writing both orders writes equal bytes
@@ -269,6 +270,7 @@ __global__ void __launch_bounds__(NTHR, (DO_SUM || RI == 8) ? 2 : 4) k_simt(Simt
                     const int loc = (int)((rs - rs0) * ncs + (cs - cs0));
                     atomicAdd(&hist_s[(loc * nq + q) * (M + 1) + b], 1u);
                 } else {
+                    CIL_CHECK(rs < a.sp.n_rs && cs < a.sp.n_cs);
                     atomicAdd((unsigned long long*)&a.hist[hist_index(a.sp, nq, M, p, rs, cs, q, b)], 1ull);
                 }
             }
@@ -329,5 +331,7 @@ cudaError_t launch_simt(const SimtArgs& a, cudaStream_t st) {
     if (a.rowsA == 0 || a.rowsB == 0) return cudaSuccess;
     return a.sym ? launch_simt_s<true>(a, st) : launch_simt_s<false>(a, st);
 }
+
+CIL_OOB_READER(oob_simt)
 
 }  // namespace cil

@@ -80,6 +80,25 @@ def main():
     o, st = cil.loglik(mu, Sig, Y[0, :3], ridge=1e-9)
     torch.cuda.synchronize()
     print("stats/loglik", st.tolist())
+    # K > 65536 (two exact int32 chunks per phase, the two-pass pack), all six measures
+    g5 = (2, 256, 256, 0.0)
+    A = cilgen.make_set(cilgen.config_seed(5), 0, 10, g5[:3], device=dev)
+    B = cilgen.make_set(cilgen.config_seed(5), 1, 12, g5[:3], device=dev)
+    R5 = radii_for(A, B, g5, cil.ALL, 6)
+    for m in (cil.L2, cil.ALL):
+        c, y, st = cil.features(A, B, g5, m, R5 if m == cil.ALL else R5[:1])
+        torch.cuda.synchronize()
+        print("C5-tiny", hex(m), int(st[0]), c[0, :, 3].tolist())
+    # near-duplicates (every pair of (i, i) within 1e-6 of each other)
+    Bn = (A.double() + 1e-6 * torch.randn(A.shape, device=dev, dtype=torch.float64)).float()
+    c, y, st = cil.features(A, Bn, g5, cil.ALL, radii_for(A, Bn, g5, cil.ALL, 6))
+    torch.cuda.synchronize()
+    print("near-dup", int(st[0]), c[0, :, -1].tolist())
+    from paper_2203_14742_b200 import _capi
+    v = int(_capi.lib.cil_diag_bounds_violations())
+    print("bounds violations:", v, "(-1 = not a bounds-checked build)")
+    if v > 0:
+        sys.exit(3)
 
 
 if __name__ == "__main__":
