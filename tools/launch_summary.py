@@ -18,7 +18,7 @@ def main(path, cmd):
         if r.get("Metric Name") != "gpu__time_duration.sum":
             continue
         k = r["Kernel Name"]
-        if "cil::" not in k and "tc::" not in k:
+        if not any(t in k for t in ("cil::", "tc::", "g3::", "rd::")):
             continue
         k = short(k)
         us = float(r["Metric Value"]) / (1000.0 if r["Metric Unit"] == "ns" else 1.0)
