@@ -17,8 +17,9 @@
  *    Data-dependent conditions are written to item_status[] on the device:
  *    CIL_ITEM_NONFINITE (an input pattern value is NaN/Inf), CIL_ITEM_NOTPD (a
  *    Cholesky pivot <= 0), CIL_ITEM_BADRADII (radii not > 0 and strictly
- *    decreasing), CIL_ITEM_OVERFLOW (the L2 re-check list overflowed: counts of
- *    that item are not trustworthy; enlarge the workspace).  Bits OR together.
+ *    decreasing), CIL_ITEM_OVERFLOW (the exact re-check list overflowed and the exact
+ *    all-pairs fallback ran instead: counts are still exact, the call was slower).  Bits OR
+ *    together.
  *  - Patterns are FP32, one pattern = S species x H rows x W columns, row-major
  *    [S][H][W] ("pattern-major then component-major then row-major");
  *    K = S*H*W, pattern p of a set starts at base + p*ld (ld >= K, in floats).
@@ -75,20 +76,25 @@ typedef enum {
 } cil_dist;
 #define CIL_ALL_DISTS 0x3Fu
 
-/* Engine for the L2 measure (all other measures always run on the CUDA-core
- * tile engine).  TC_* = tcgen05 tensor-core Gram g = a~.b~ of centred operands
- * in split precision (hi.hi + hi.lo + lo.hi), d^2 = |a~|^2 + |b~|^2 - 2g, with
- * every pair whose d^2 lies within the engine's error bound of a threshold
- * re-evaluated exactly (FP64) — so counts are exact either way.  SIMT = FP32
- * differences on CUDA cores with FP64-flushed sums. */
+/* Engine for the L2-type measures (the max family L-inf, W1-inf, W1-inf-sum always runs on the
+ * CUDA-core tile engine).  Every engine decides a (pair, radius) in-kernel only when the radius lies
+ * outside an interval of the measure that contains its exact FP64 value (reading R13);
+ * the others are re-evaluated exactly in FP64, so the counts are those of the plain definition.
+ *  TC_I8     three-digit INT8 fixed point per row (x~ = sigma (2^16 h + 2^8 m + l), 22 bits), six
+ *            exact int32 tcgen05 kind::i8 products per K step, a WORST-CASE interval (Cauchy-Schwarz
+ *            on the dropped digit products, rigorous residual norms, directed rounding) — valid for
+ *            every input; any K (exact chunks of 65536); L2 alone, or L2 + W12 + W12SUM from the
+ *            augmented rows [x | D_x x | D_y x].  Column segments (SCIL blocks) need >= 21 columns
+ *            (M <= 16 for W12 / W12SUM), else the measures run on the CUDA cores.
+ *  SIMT      FP32 differences on CUDA cores, FP64-flushed sums, rigorous rounding bounds.
+ *  TC_3XBF16 / TC_3XTF32  float split (hi.hi + hi.lo + lo.hi, FP32 tensor accumulation): explicit
+ *            options only, their bound is statistical (not worst-case). */
 typedef enum {
-    CIL_ENGINE_AUTO = 0,      /* TC_I8 when K <= 65536 and column segments >= 43 (SCIL blocks), else TC_3XBF16 */
+    CIL_ENGINE_AUTO = 0,      /* TC_I8 where it applies, else the CUDA cores (never the float splits) */
     CIL_ENGINE_TC_3XBF16 = 1,
     CIL_ENGINE_TC_3XTF32 = 2,
     CIL_ENGINE_SIMT = 3,
-    CIL_ENGINE_TC_I8 = 4      /* two-digit INT8 fixed point per row (x~ = sigma (256 h + l)), exact int32
-                                 tcgen05 kind::i8 accumulation; K <= 65536, column segments >= 43
-                                 (else it runs as TC_3XBF16) */
+    CIL_ENGINE_TC_I8 = 4
 } cil_engine;
 
 typedef struct {
@@ -317,9 +323,9 @@ CIL_API cil_status cil_synth_loglik_boot(int32_t P, const float* pools, int64_t 
 
 /* ------------------------------------------------------------------------ */
 /* cil_diag_gram — DIAGNOSTIC (not on the hot path): runs the tensor-core L2 engine on one
- * set pair without binning and writes d2E[i][j][0] = the engine's FP32 d^2(i,j) (unweighted
- * sum of squares) and d2E[i][j][1] = its error bound E(i,j) (see cil_engine).  Used by the
- * tests to measure the Gram error against FP64.  engine must be TC_3XBF16, TC_3XTF32 or TC_I8;
+ * set pair without binning.  TC_I8: d2E[i][j] = (lo, hi), the engine's interval of the unweighted
+ * distance |a_i - b_j| (it must contain the exact value for every pair).  TC_3XBF16 / TC_3XTF32:
+ * d2E[i][j] = (the FP32 d^2, its statistical error bound E).  engine must be TC_3XBF16, TC_3XTF32 or TC_I8;
  * d2E [N][Nt][2] FP32 device; ws_bytes >= cil_features_workspace_size(1, N, Nt, g, CIL_L2,
  * 1, engine) + 512.
  * ------------------------------------------------------------------------ */
@@ -328,9 +334,9 @@ CIL_API cil_status cil_diag_gram(const float* A, int64_t lda, int64_t N, const f
                                  size_t ws_bytes, void* stream);
 
 /* cil_diag_gram_family — DIAGNOSTIC: the three-phase INT8 engine (L2, W12SUM, W12 on tensor
- * cores) on one set pair without binning: vE[k][i][j][0] = its FP32 value and vE[k][i][j][1]
- * its error bound for kind k = 0: L2^2/w (unweighted sum of squares), 1: W12^2/w, 2: W12SUM/sqrt(w).
- * vE [3][N][Nt][2] FP32 device; needs W >= 2 and K <= 65536; ws_bytes >=
+ * cores) on one set pair without binning: vE[k][i][j] = (lo, hi), its interval of kind k = 0:
+ * L2/sqrt(w) (the unweighted distance), 1: W12^2/w, 2: W12SUM/sqrt(w).
+ * vE [3][N][Nt][2] FP32 device; needs W >= 2; ws_bytes >=
  * cil_features_workspace_size(1, N, Nt, g, CIL_L2|CIL_W12SUM|CIL_W12, 1, CIL_ENGINE_TC_I8) + 512.
  * ------------------------------------------------------------------------ */
 CIL_API cil_status cil_diag_gram_family(const float* A, int64_t lda, int64_t N, const float* B, int64_t ldb,

@@ -380,8 +380,9 @@ def synth_loglik_boot(pools, data, N_set, I1, I2, J, grid, mask, radii, ridge: f
 
 
 def diag_gram(A, B, grid, engine=ENGINE_TC_3XBF16, *, stream=None):
-    """DIAGNOSTIC: the tensor-core engine's FP32 d^2 and error bound E for every pair
-    of one set pair, shape [N, Nt, 2] (no binning).  Not on the hot path."""
+    """DIAGNOSTIC: per pair of one set pair, shape [N, Nt, 2] (no binning; not on the hot path):
+    TC_I8 -> the engine's interval (lo, hi) of the unweighted L2 distance; TC_3XBF16 / TC_3XTF32 ->
+    the FP32 d^2 and its statistical bound E."""
     S, H, W = int(grid[0]), int(grid[1]), int(grid[2])
     K = S * H * W
     A2, B2 = A.reshape(A.shape[0], -1).contiguous(), B.reshape(B.shape[0], -1).contiguous()
@@ -496,8 +497,8 @@ def gaussianity_chi2(Y, *, bins: int = 10, ridge: float = 0.0, stream=None):
 
 
 def diag_gram_family(A, B, grid, *, stream=None):
-    """DIAGNOSTIC: the three-phase INT8 engine's FP32 values and bounds for every pair of one
-    set pair, shape [3, N, Nt, 2] for (L2^2/w, W12^2/w, W12SUM/sqrt(w)).  Not on the hot path."""
+    """DIAGNOSTIC: the three-phase INT8 engine's intervals (lo, hi) for every pair of one set pair,
+    shape [3, N, Nt, 2] for (L2/sqrt(w), W12^2/w, W12SUM/sqrt(w)).  Not on the hot path."""
     S, H, W = int(grid[0]), int(grid[1]), int(grid[2])
     K = S * H * W
     A2, B2 = A.reshape(A.shape[0], -1).contiguous(), B.reshape(B.shape[0], -1).contiguous()
