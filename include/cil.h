@@ -246,7 +246,7 @@ CIL_API cil_status cil_radii_from_range(int32_t P, int32_t n_meas, int32_t M, co
  * mu_0, Sigma_0 (step 3) are cil_stats of the n_ens*(n_ens-1)/2 vectors of an item.
  * radii [P or shared][n_meas][M] (radii_stride 0 = shared); Y [P][n_ens(n_ens-1)/2][n_meas*M]
  * FP64 device.  Engines as cil_features (AUTO: INT8 tensor cores for the L2-type family when
- * N >= 43 columns per subset, else CUDA cores / 3xBF16).
+ * N >= 21 columns per subset, else CUDA cores).
  * ------------------------------------------------------------------------ */
 CIL_API size_t cil_train_workspace_size(int32_t P, int32_t n_ens, int32_t N, cil_grid g, uint32_t dist_mask,
                                         int32_t M, cil_engine engine);
@@ -268,9 +268,9 @@ CIL_API cil_status cil_train_vectors(int32_t P, const float* X, int64_t stride, 
  *   bins[p][q][i][j] = #{m : d_q(A_p,i , B_p,j) < radii[p*radii_stride + q*M + m]}  in [0, M]
  * (radii strictly decreasing, so d < R_m  <=>  bins > m).  Arguments as cil_features;
  * strideA / strideB may be 0 (the same set for every item).  bins [P][n_meas][N][Nt] uint8,
- * device, row-major, written completely.  engine: AUTO / TC_I8 (L2 on the INT8 tensor-core
- * engine when K <= 65536 — pairs within its error bound of a radius are re-evaluated in
- * FP64 — else on the CUDA cores) or SIMT; TC_3XBF16 / TC_3XTF32 -> CIL_EUNSUPPORTED.
+ * device, row-major, written completely.  engine: AUTO / TC_I8 (L2, W12, W12SUM on the INT8
+ * tensor-core engine, the max family on the CUDA cores; every pair whose interval contains a radius
+ * is re-evaluated in FP64) or SIMT; TC_3XBF16 / TC_3XTF32 -> CIL_EUNSUPPORTED.
  * ------------------------------------------------------------------------ */
 CIL_API size_t cil_bin_matrix_workspace_size(int32_t P, int64_t N, int64_t Nt, cil_grid g, uint32_t dist_mask,
                                              int32_t M, cil_engine engine);
