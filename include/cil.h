@@ -362,6 +362,11 @@ CIL_API int32_t cil_diag_sqrt_approx_error(double* max_rel_up, double* max_rel_d
  * -1 in the normal build. */
 CIL_API int64_t cil_diag_bounds_violations(void);
 
+/* cil_diag_limit_recheck_list — DIAGNOSTIC: on the calling host thread, cap the exact re-check list of
+ * subsequent calls at `limit` entries (< 0: no cap), so tests can force the exact all-pairs fallback
+ * that runs when the list overflows (counts stay exact; items get CIL_ITEM_OVERFLOW). */
+CIL_API void cil_diag_limit_recheck_list(int64_t limit);
+
 /* ------------------------------------------------------------------------ */
 /* Kernel timing (diagnostics, used by bench.py for the live roofline).  While enabled on
  * the calling host thread, every kernel the library launches is bracketed by CUDA events

@@ -14,6 +14,9 @@
 
 namespace cil {
 static thread_local int32_t t_last_cuda = 0;
+// diagnostics (cil_diag_limit_recheck_list): cap the re-check list below its allocated capacity on this
+// thread so tests can exercise the exact all-pairs fallback; < 0 = no limit
+static thread_local int64_t t_list_limit = -1;
 static thread_local int32_t t_launches = 0;
 void note_launch(int n) { t_launches += n; }
 
@@ -338,6 +341,7 @@ cil_status run_engines(int P, const RowSrc& asrc, const RowSrc& bsrc, int64_t ro
     uint64_t* hist = at<uint64_t>(ws, L.off_hist);
     uint32_t* ctr = at<uint32_t>(ws, L.off_ctr);
     uint4* list = L.list_cap ? at<uint4>(ws, L.off_list) : nullptr;
+    const uint32_t cap = (t_list_limit >= 0 && t_list_limit < (int64_t)L.list_cap) ? (uint32_t)t_list_limit : L.list_cap;
     CIL_CU(launch_prep(P, sl.nq, M, radii, radii_stride, bp, thr, thr2, status, hist, L.hist_elems, ctr, st,
                        keep_status));
     if (rowsA == 0 || rowsB == 0) return CIL_OK;
@@ -370,7 +374,7 @@ cil_status run_engines(int P, const RowSrc& asrc, const RowSrc& bsrc, int64_t ro
         a.tri = tile_skip == 2;
         a.sym = binout != nullptr && b_same;
         a.statA = statA; a.statB = statB;
-        a.list = list; a.ctr = ctr; a.cap = L.list_cap;
+        a.list = list; a.ctr = ctr; a.cap = cap;
         CIL_CU(launch_simt(a, st));
     }
     if (pl.tc) {
@@ -414,7 +418,7 @@ cil_status run_engines(int P, const RowSrc& asrc, const RowSrc& bsrc, int64_t ro
                 if (sl.slot[q] == 2) t.q_k[2] = q;
             }
             t.sp = sp; t.hist = hist;
-            t.list = list; t.ctr = ctr; t.cap = L.list_cap;
+            t.list = list; t.ctr = ctr; t.cap = cap;
             f32_bracket(1.0 / bp.h, &t.ih_rd, &t.ih_ru);
             f32_bracket(1.0 / (bp.h * bp.h), &t.ih2_rd, &t.ih2_ru);
             t.part = pl.aug ? at<float>(ws, L.off_part) : nullptr;
@@ -442,7 +446,7 @@ cil_status run_engines(int P, const RowSrc& asrc, const RowSrc& bsrc, int64_t ro
             t.thr2 = thr2 + 6 * M; t.thr_stride = 8 * M; t.M = M;
             t.q_l2 = sl.q_l2; t.nq = sl.nq;
             t.sp = sp; t.hist = hist;
-            t.recheck = list; t.recheck_ctr = ctr; t.recheck_cap = L.list_cap;
+            t.recheck = list; t.recheck_ctr = ctr; t.recheck_cap = cap;
             t.status = status;
             t.cta_group = 2;
             t.chunk_kb = 4;
@@ -460,8 +464,8 @@ cil_status run_engines(int P, const RowSrc& asrc, const RowSrc& bsrc, int64_t ro
     }
     if (diag || range) return CIL_OK;
     if (L.list_cap) {
-        const RecheckArgs r = recheck_args(asrc, bsrc, K, g, sl, M, bp, sp, L, ws, status, P, binout, rowsA, rowsB,
-                                           mask);
+        RecheckArgs r = recheck_args(asrc, bsrc, K, g, sl, M, bp, sp, L, ws, status, P, binout, rowsA, rowsB, mask);
+        r.cap = cap;
         CIL_CU(launch_recheck(r, L.hist_elems, st));
     }
     return CIL_OK;
@@ -1078,6 +1082,8 @@ int32_t cil_prof_read(double* ms, int64_t* launches) {
     t_prof->clear();
     return K_NCLASS;
 }
+
+void cil_diag_limit_recheck_list(int64_t limit) { t_list_limit = limit; }
 
 int64_t cil_diag_bounds_violations(void) {
 #ifdef CIL_BOUNDS_CHECK

@@ -101,3 +101,45 @@ def test_near_duplicates_bin_matrix(cil, oracle_mod, engine):
             bad = (g < lo) | (g > hi)
             assert not bad.any(), (engine, eps, q, np.argwhere(bad)[:5].tolist(), exact[bad][:5].tolist(),
                                    g[bad][:5].tolist())
+
+
+@pytest.mark.parametrize("engine", ["AUTO", "SIMT"])
+@pytest.mark.parametrize("mode", ["features", "bins"])
+def test_recheck_list_overflow_fallback(cil, oracle_mod, engine, mode):
+    """The exact re-check list capped at 2 entries (diagnostic hook): the exact all-pairs fallback of
+    recheck.cu must still give the oracle's counts / bins, with CIL_ITEM_OVERFLOW set."""
+    from paper_2203_14742_b200 import _capi
+    O = oracle_mod
+    grid = (2, 16, 16, 0.0)
+    mask, M = 0x3F, 10
+    A, B = near_dup_sets(grid, "GM", 1e-6, 24)
+    dev = torch.device("cuda")
+    rng, _ = cil.distance_range(A.to(dev), B.to(dev), grid, mask)
+    radii, _ = cil.radii_from_range(rng, M)
+    radii = radii[0]
+    _capi.lib.cil_diag_limit_recheck_list(2)
+    try:
+        if mode == "features":
+            c, _, st = cil.features(A.to(dev), B.to(dev), grid, mask, radii, engine=getattr(cil, "ENGINE_" + engine))
+        else:
+            # symmetric (mirrored) bin matrix of A against itself, radii AT pair distances of A (ties:
+            # every such pair is ambiguous for every engine, so the capped list overflows)
+            DA = O.distance_matrix(A.numpy(), A.numpy(), grid, mask)
+            radii = torch.tensor(np.stack([np.sort(np.unique(DA[q][DA[q] > 0]))[::-1][2:2 + 3 * M:3] for q in range(6)]),
+                                 device=dev)
+            bins, st = cil.bin_matrix(A.to(dev), A.to(dev), grid, mask, radii, engine=getattr(cil, "ENGINE_" + engine))
+        torch.cuda.synchronize()
+    finally:
+        _capi.lib.cil_diag_limit_recheck_list(-1)
+    assert int(st[0]) & cil.ITEM_OVERFLOW
+    if mode == "features":
+        _check(c[0].cpu().numpy(), O.features(A.numpy(), B.numpy(), grid, mask, radii.cpu().numpy(), band=BAND),
+               f"overflow fallback {engine}")
+    else:
+        D = O.distance_matrix(A.numpy(), A.numpy(), grid, mask)
+        R = radii.cpu().numpy()
+        for q in range(6):
+            lo = (D[q][..., None] < R[q] * (1 - BAND)).sum(-1)
+            hi = (D[q][..., None] < R[q] * (1 + BAND)).sum(-1)
+            g = bins[0, q].cpu().numpy().astype(np.int64)
+            assert ((g >= lo) & (g <= hi)).all(), (engine, q)
