@@ -1,7 +1,7 @@
 #!/bin/bash
 # One ncu pass per gpurun call (each after the same command exits 0 without ncu):
 #   tools/prof_round.sh launches|gram|pack  [tag]
-CMD="python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu --no-c4 --no-c6 --no-c7"
+CMD="python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu --no-c4 --no-c6 --no-c7 --no-c3 --no-c5"
 what=$1; tag=${2:-r01}
 mkdir -p gpurun_out
 $CMD > gpurun_out/${tag}_plain_${what}.log 2>&1 || { echo plain_failed; exit 1; }
