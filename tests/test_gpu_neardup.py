@@ -143,3 +143,30 @@ def test_recheck_list_overflow_fallback(cil, oracle_mod, engine, mode):
             hi = (D[q][..., None] < R[q] * (1 + BAND)).sum(-1)
             g = bins[0, q].cpu().numpy().astype(np.int64)
             assert ((g >= lo) & (g <= hi)).all(), (engine, q)
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("kind", ["binary", "quantised"])
+def test_binary_and_quantised_patterns(cil, oracle_mod, engine, kind):
+    """Thresholded (0/1) and coarsely quantised (multiples of 1/8) patterns: many pairs
+    share most of their values exactly, equal distances are frequent (ties land in the band), and
+    the low digits of two rows coincide — the regime a statistical bound misjudges."""
+    O = oracle_mod
+    grid = (2, 32, 32, 0.0)
+    mask, M = 0x3F, 12
+    dev = torch.device("cuda")
+    A = cilgen.make_set(777, 0, 40, grid[:3], "FHN")
+    B = cilgen.make_set(777, 1, 36, grid[:3], "FHN")
+    if kind == "binary":
+        A, B = (A > 0.1).float(), (B > 0.1).float()
+    else:
+        A, B = torch.round(A * 8) / 8, torch.round(B * 8) / 8
+    B[:10] = A[:10]                                         # exact duplicates too
+    rng, _ = cil.distance_range(A.to(dev), B.to(dev), grid, mask)
+    radii, _ = cil.radii_from_range(rng, M)
+    radii = radii[0]
+    c, _, st = cil.features(A.to(dev), B.to(dev), grid, mask, radii, engine=getattr(cil, "ENGINE_" + engine))
+    torch.cuda.synchronize()
+    assert int(st[0]) == 0
+    _check(c[0].cpu().numpy(), O.features(A.numpy(), B.numpy(), grid, mask, radii.cpu().numpy(), band=BAND),
+           f"{engine} {kind}")

@@ -150,3 +150,14 @@ def test_ring_pass_counts_equal_unsharded(oracle_mod, world):
     for rank, counts, y in res:
         np.testing.assert_array_equal(counts[0], full["counts"])
         np.testing.assert_array_equal(y[0], full["counts"] / (17 * 11))
+
+
+def test_bench_rank_mismatch_fails_loudly():
+    """bench.py --gpus N under a torchrun environment with another WORLD_SIZE must refuse to run
+    (--gpus was silently ignored)."""
+    import subprocess
+    import sys
+    env = dict(os.environ, WORLD_SIZE="2", RANK="0", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "1", "--impl", "reference"],
+                       env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode != 0 and "WORLD_SIZE=2" in (r.stderr + r.stdout)
