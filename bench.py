@@ -697,9 +697,13 @@ def bench_c3(args, dev):
         step()
     torch.cuda.synchronize()
     steps = max(2, min(args.steps, 5))
+    clk = ClockSampler(dev.index or 0).__enter__()
     _capi.prof_enable(True)
+    clk.mark_start()
     ms = timed(step, steps, stream) / steps
+    clk.mark_end()
     _capi.prof_enable(False)
+    clk.__exit__()
     prof = _capi.prof_read()
     S, H, W = grid
     K = S * H * W
@@ -717,7 +721,8 @@ def bench_c3(args, dev):
                          "alu_ceiling_element_pairs_per_s": ceil,
                          "ceiling_mix": "FADD2+FMNMX3" if mix == 1 else "FADD2+FMNMX3+FFMA2",
                          "frac": round(ep / (simt_ms * 1e-3) / ceil, 4), "K_aug": Kaug},
-           "kernel_breakdown": {k: round(v[0] / steps, 3) for k, v in prof.items() if v[1] > 0}}
+           "kernel_breakdown": {k: round(v[0] / steps, 3) for k, v in prof.items() if v[1] > 0},
+           "clocks": clk.summary()}
     g_ms, g_n = prof["gram_tc"]
     if g_n and tc_family:
         per = g_ms / g_n

@@ -367,6 +367,12 @@ CIL_API int64_t cil_diag_bounds_violations(void);
  * that runs when the list overflows (counts stay exact; items get CIL_ITEM_OVERFLOW). */
 CIL_API void cil_diag_limit_recheck_list(int64_t limit);
 
+/* cil_diag_recheck_sort_min — DIAGNOSTIC: on the calling host thread, re-check lists of at least `n`
+ * entries take the row-bucketed pass (list counting-sorted by pattern row, each pair evaluated once;
+ * recheck.cu), shorter ones the entry-by-entry pass.  Default 2048; n <= 0 restores it, n = 1 forces
+ * the bucketed pass for every non-empty list (tests).  Results are identical either way. */
+CIL_API void cil_diag_recheck_sort_min(int64_t n);
+
 /* ------------------------------------------------------------------------ */
 /* Kernel timing (diagnostics, used by bench.py for the live roofline).  While enabled on
  * the calling host thread, every kernel the library launches is bracketed by CUDA events

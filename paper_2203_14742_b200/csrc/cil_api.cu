@@ -17,6 +17,8 @@ static thread_local int32_t t_last_cuda = 0;
 // diagnostics (cil_diag_limit_recheck_list): cap the re-check list below its allocated capacity on this
 // thread so tests can exercise the exact all-pairs fallback; < 0 = no limit
 static thread_local int64_t t_list_limit = -1;
+// diagnostics (cil_diag_recheck_sort_min): list length from which the re-check is row-bucketed
+static thread_local uint32_t t_sort_min = 2048;
 static thread_local int32_t t_launches = 0;
 void note_launch(int n) { t_launches += n; }
 
@@ -100,7 +102,17 @@ struct Plan {
     uint32_t simt_mask = 0; // measures on the CUDA-core engine
     bool do_max = false, do_sum = false;
     int nreg = 1;
+    bool max16 = false;     // max family alone on the 15-bit fixed-point integer engine (max16.cu)
+    bool f32aug = false;    // FP32 augmented operands for k_simt (everything else on the CUDA cores)
 };
+
+// The max family goes to max16.cu when it runs without the sum family (the L2 type measures are on
+// the tensor cores) and the engine is not the all-FP32 CUDA-core engine (SIMT, also the exact
+// distance-range mode).
+void plan_cuda_cores(Plan& pl, cil_engine engine) {
+    pl.max16 = pl.do_max && !pl.do_sum && engine != CIL_ENGINE_SIMT;
+    pl.f32aug = pl.simt_mask != 0 && !pl.max16;
+}
 
 // split: 1 = 3xBF16, 2 = 3xTF32, 3 = three-digit INT8 (gram3.cu).  The INT8 engine takes any K
 // (exact int32 accumulation in chunks of 65536) and column segments of >= 21 columns (its
@@ -130,6 +142,7 @@ Plan make_plan(uint32_t mask, cil_engine engine, const cil_grid& g, int64_t col_
         pl.do_max = pl.simt_mask & (CIL_LINF | CIL_W1INF | CIL_W1INFSUM);
         pl.do_sum = false;
         pl.nreg = (pl.simt_mask & (CIL_W1INF | CIL_W1INFSUM)) ? (g.H > 1 ? 3 : 2) : 1;
+        plan_cuda_cores(pl, engine);
         return pl;
     }
     pl.split = (engine == CIL_ENGINE_TC_3XTF32) ? 2 : (engine == CIL_ENGINE_TC_3XBF16) ? 1 : 3;
@@ -139,6 +152,7 @@ Plan make_plan(uint32_t mask, cil_engine engine, const cil_grid& g, int64_t col_
     pl.do_sum = pl.simt_mask & (CIL_L2 | CIL_W12SUM | CIL_W12);
     const bool grad = pl.simt_mask & (CIL_W12SUM | CIL_W12 | CIL_W1INF | CIL_W1INFSUM);
     pl.nreg = grad ? (g.H > 1 ? 3 : 2) : 1;
+    plan_cuda_cores(pl, engine);
     return pl;
 }
 
@@ -163,13 +177,15 @@ Plan plan_union(const Plan& a, const Plan& b) {
     u.do_max = a.do_max || b.do_max;
     u.do_sum = a.do_sum || b.do_sum;
     u.nreg = a.nreg > b.nreg ? a.nreg : b.nreg;
+    u.max16 = a.max16 || b.max16;
+    u.f32aug = a.f32aug || b.f32aug;
     return u;
 }
 
 // Workspace carve-up (identical in the size query and in the call).
 struct Layout {
     size_t off_thr, off_thr2, off_hist, off_ctr, off_list, off_center, off_hi, off_lo, off_nrm, off_q4,
-        off_aug, off_rowstat, off_Y, off_mu, off_sig, off_part, total;
+        off_aug, off_rowstat, off_aug16, off_max16, off_rk, off_rk_list, off_Y, off_mu, off_sig, off_part, total;
     int64_t hist_elems = 0;
     uint32_t list_cap = 0;
     int64_t Kp = 0;
@@ -178,6 +194,7 @@ struct Layout {
     int64_t Krow = 0;               // bytes per plane row (INT8 engine)
     int nph = 1;
     AugGeom geom{};
+    AugGeom geom16{};               // max16.cu operands (regions padded to kMax16BK)
 };
 
 size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -201,6 +218,8 @@ Layout make_layout(int P, int64_t rowsA, int64_t rowsB, const cil_grid& g, int n
         const double cases = (double)P * rowsA * rowsB * nq;
         L.list_cap = (uint32_t)fmin(fmin(cases, cases / 128.0 + 262144.0), 1.0e9);
         L.off_list = take(16 * (size_t)L.list_cap);
+        L.off_rk = take(sizeof(uint32_t) * ((size_t)rows + 1));     // row buckets of the re-check
+        L.off_rk_list = take(16 * (size_t)L.list_cap);
     }
     if (pl.tc) {
         L.Kp = round_up(K, kTcBK);
@@ -227,10 +246,15 @@ Layout make_layout(int P, int64_t rowsA, int64_t rowsB, const cil_grid& g, int n
             L.off_q4 = take(sizeof(float) * (size_t)rows);
         }
     }
-    if (pl.simt_mask) {
+    if (pl.f32aug) {
         L.geom = make_aug_geom(g.S, g.H, g.W, pl.nreg, g.gs);
         L.off_aug = take(sizeof(float) * (size_t)rows * L.geom.off[3]);
         L.off_rowstat = take(sizeof(float) * 4 * (size_t)rows);
+    }
+    if (pl.max16) {
+        L.geom16 = make_aug_geom(g.S, g.H, g.W, pl.nreg, g.gs, kMax16BK);
+        L.off_aug16 = take(sizeof(int16_t) * (size_t)rows * L.geom16.off[3]);
+        L.off_max16 = take(sizeof(unsigned) * 8 * (size_t)P);
     }
     if (nY > 0) {
         L.off_Y = take(sizeof(double) * (size_t)nY);
@@ -319,6 +343,9 @@ RecheckArgs recheck_args(const RowSrc& asrc, const RowSrc& bsrc, int64_t K, cons
     r.mirror = binout != nullptr && same_rows(asrc, bsrc) && rowsA == rowsB;
     r.S = g.S; r.H = g.H; r.W = g.W; r.gs = g.gs;
     r.hist_elems = L.hist_elems;
+    r.rk = at<uint32_t>(ws, L.off_rk);
+    r.sort_min = t_sort_min;
+    r.rk_list = at<uint4>(ws, L.off_rk_list);
     return r;
 }
 
@@ -347,7 +374,35 @@ cil_status run_engines(int P, const RowSrc& asrc, const RowSrc& bsrc, int64_t ro
     if (rowsA == 0 || rowsB == 0) return CIL_OK;
     const bool b_same = same_rows(asrc, bsrc) && rowsA == rowsB;
 
-    if (pl.simt_mask) {
+    if (pl.simt_mask && pl.max16) {
+        // max family alone: 15-bit fixed point on the integer pipes (never in distance-range mode,
+        // whose plans use the SIMT engine)
+        if (range != nullptr) return CIL_EUNSUPPORTED;
+        int16_t* qa = at<int16_t>(ws, L.off_aug16);
+        int16_t* qb = qa + (size_t)P * rowsA * L.geom16.off[3];
+        unsigned* maxbits = at<unsigned>(ws, L.off_max16);
+        const AugGeom& g16 = L.geom16;
+        CIL_CU(launch_pack16(P, asrc, rowsA, bsrc, rowsB, g16, maxbits, qa, qb, status, st));
+        Max16Args a{};
+        a.A = qa; a.B = qb;
+        a.rowsA = rowsA; a.rowsB = rowsB; a.Kaug = L.geom16.off[3];
+        a.g = g16;
+        a.maxbits = maxbits;
+        a.bp = bp;
+        a.sp = sp;
+        a.thr = thr; a.thr_stride = (int64_t)sl.nq * M;
+        a.hist = hist;
+        a.status = status;
+        a.P = P;
+        a.qmask = 0;
+        for (int q = 0; q < sl.nq; ++q)
+            if ((pl.simt_mask >> sl.slot[q]) & 1u) a.qmask |= 1u << q;
+        a.binout = binout;
+        a.tri = tile_skip == 2;
+        a.sym = binout != nullptr && b_same;
+        a.list = list; a.ctr = ctr; a.cap = cap;
+        CIL_CU(launch_max16(a, st));
+    } else if (pl.simt_mask) {
         float* aug = at<float>(ws, L.off_aug);
         float* augB = aug + (size_t)P * rowsA * L.geom.off[3];
         float* statA = at<float>(ws, L.off_rowstat);
@@ -1084,10 +1139,11 @@ int32_t cil_prof_read(double* ms, int64_t* launches) {
 }
 
 void cil_diag_limit_recheck_list(int64_t limit) { t_list_limit = limit; }
+void cil_diag_recheck_sort_min(int64_t n) { t_sort_min = n <= 0 ? 2048u : (uint32_t)(n > 0xffffffffll ? 0xffffffffll : n); }
 
 int64_t cil_diag_bounds_violations(void) {
 #ifdef CIL_BOUNDS_CHECK
-    return (int64_t)oob_gram3() + oob_recheck() + oob_simt();
+    return (int64_t)oob_gram3() + oob_recheck() + oob_simt() + oob_max16();
 #else
     return -1;
 #endif

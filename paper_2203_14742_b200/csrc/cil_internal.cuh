@@ -53,11 +53,13 @@ static __device__ unsigned int cil_oob_count;
 unsigned int oob_gram3();
 unsigned int oob_recheck();
 unsigned int oob_simt();
+unsigned int oob_max16();
 
 constexpr int kMaxM = 64;        // radii per measure
 constexpr int kMaxMeas = 6;
 constexpr int kMaxD = 192;       // n_meas * M for loglik (packed Cholesky factor in smem)
 constexpr int kSimtBK = 32;      // SIMT k-chunk (floats); region padding unit
+constexpr int kMax16BK = 64;     // max16.cu k-chunk (int16 elements); its region padding unit
 constexpr int kTcBK = 128;       // K padding of the tensor-core operands (128 int8 = one 128-B row)
 
 // Row sources: how panel row r of item p maps to a pattern in caller memory.
@@ -115,7 +117,7 @@ struct AugGeom {
 
 inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
-inline AugGeom make_aug_geom(int S, int H, int W, int nreg, uint32_t gs = 0) {
+inline AugGeom make_aug_geom(int S, int H, int W, int nreg, uint32_t gs = 0, int64_t pad = kSimtBK) {
     AugGeom a{};
     a.S = S; a.H = H; a.W = W;
     a.gs = gs;
@@ -125,9 +127,9 @@ inline AugGeom make_aug_geom(int S, int H, int W, int nreg, uint32_t gs = 0) {
     if (nreg >= 3 && a.Ky == 0) nreg = 2;
     a.nreg = nreg;
     a.off[0] = 0;
-    a.off[1] = round_up(a.K, kSimtBK);
-    a.off[2] = a.off[1] + (nreg >= 2 ? round_up(a.Kx, kSimtBK) : 0);
-    a.off[3] = a.off[2] + (nreg >= 3 ? round_up(a.Ky, kSimtBK) : 0);
+    a.off[1] = round_up(a.K, pad);
+    a.off[2] = a.off[1] + (nreg >= 2 ? round_up(a.Kx, pad) : 0);
+    a.off[3] = a.off[2] + (nreg >= 3 ? round_up(a.Ky, pad) : 0);
     return a;
 }
 
@@ -211,6 +213,31 @@ struct SimtArgs {
     uint4* list; uint32_t* ctr; uint32_t cap; // re-check list: (p, i, j, b_lo | measure id << 8)
 };
 cudaError_t launch_simt(const SimtArgs& a, cudaStream_t st);
+
+// max16.cu — the max family on 15-bit fixed-point operands (integer pipes), rigorous interval + re-check
+struct Max16Args {
+    const int16_t* A; const int16_t* B;       // [P][rowsA][Kaug], [P][rowsB][Kaug] (B negated)
+    int64_t rowsA, rowsB, Kaug;
+    AugGeom g;                                // regions padded to kMax16BK elements
+    const unsigned* maxbits;                  // [P][3][2] per-item range of each region (max16.cu)
+    BinParams bp;
+    SegParams sp;
+    const double* thr;                        // [P][nq][M]
+    int64_t thr_stride;
+    uint64_t* hist;
+    const int32_t* status;
+    int P;
+    uint32_t qmask;                           // slots binned by this engine (max family only)
+    uint8_t* binout;
+    bool tri, sym;
+    int hist_cap;
+    uint4* list; uint32_t* ctr; uint32_t cap;
+    uint32_t one;                             // 1 (set by the launcher; keeps the adds on the FMA pipe)
+};
+cudaError_t launch_pack16(int P, const RowSrc& asrc, int64_t rowsA, const RowSrc& bsrc, int64_t rowsB,
+                          const AugGeom& g, unsigned* maxbits, int16_t* outA, int16_t* outB, int32_t* status,
+                          cudaStream_t st);
+cudaError_t launch_max16(const Max16Args& a, cudaStream_t st);
 
 // gram_tc.cu
 struct TcArgs {
@@ -305,6 +332,9 @@ struct RecheckArgs {
     int S, H, W;
     uint32_t gs;
     int64_t hist_elems;  // bounds-checked builds
+    uint32_t* rk;        // [P*rowsA + 1] per-A-row bucket counts -> offsets (row-bucketed pass)
+    uint4* rk_list;      // [cap] the list sorted by (p, i)
+    uint32_t sort_min;   // lists of >= sort_min entries take the row-bucketed pass
 };
 cudaError_t launch_recheck(const RecheckArgs& a, int64_t hist_elems, cudaStream_t st);
 

@@ -176,8 +176,20 @@ __host__ __device__ inline int tiles_active(int skip, int tiles_m, int tiles_n, 
     }
     return n;
 }
+// Without skipping the tiles of an item run in groups of up to 8 tile rows, column-major inside a group
+// (row tile fastest): the clusters of one wave then share ~8 A tiles and ~9 B tiles, so both stay in
+// L2 while the wave streams K — for long rows (C3, C5: one tile's planes exceed L2) this replaces a
+// fresh B tile per cluster and wave.
+constexpr int kGroupRows = 8;
 __device__ __forceinline__ void tile_of(const Params& prm, int u, int& mt, int& nt) {
-    if (prm.skip == 0) { mt = u / prm.tiles_n; nt = u % prm.tiles_n; return; }
+    if (prm.skip == 0) {
+        const int per_group = kGroupRows * prm.tiles_n;
+        const int g = u / per_group, r = u % per_group;
+        const int rows_g = min(kGroupRows, prm.tiles_m - g * kGroupRows);
+        mt = g * kGroupRows + r % rows_g;
+        nt = r / rows_g;
+        return;
+    }
     for (mt = 0; mt < prm.tiles_m; ++mt) {
         const int s = row_start(prm.skip, mt, prm.sp.row_seg, prm.sp.col_seg, prm.rowsB, prm.tn);
         const int c = s < prm.tiles_n ? prm.tiles_n - s : 0;

@@ -41,8 +41,12 @@ __device__ __forceinline__ float absmax3(float m, float x, float y) {
 
 // SYM (bin matrix of a panel against itself) is a template flag so that the counting kernels'
 // code is not touched by the mirrored writes (as a runtime flag it cost the max family 16 %)
+#ifndef CIL_SIMT_EXP
+#define CIL_SIMT_EXP 0   // code-generation experiments (tools/simt_var.sh); 0 = product
+#endif
 template <bool DO_MAX, bool DO_SUM, int RI, bool SYM>
-__global__ void __launch_bounds__(NTHR, (DO_SUM || RI == 8) ? 2 : 4) k_simt(SimtArgs a) {
+__global__ void __launch_bounds__(NTHR, (CIL_SIMT_EXP == 1 && !DO_SUM) ? 3 : (DO_SUM || RI == 8) ? 2 : 4)
+    k_simt(SimtArgs a) {
     constexpr int TA = 8 * RI;     // A rows per CTA: RI x 4 pairs per thread
     constexpr int NP = RI * 4;     // pairs per thread
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -133,7 +137,13 @@ __global__ void __launch_bounds__(NTHR, (DO_SUM || RI == 8) ? 2 : 4) k_simt(Simt
         __syncthreads();
         const float* Ab = As + buf * TA * LDS;
         const float* Bb = Bs + buf * TB * LDS;
+#if CIL_SIMT_EXP == 2
+#pragma unroll 1
+#elif CIL_SIMT_EXP == 3
+#pragma unroll
+#else
 #pragma unroll 2
+#endif
         for (int kk = 0; kk < BK; kk += 4) {
             float4 av[RI], bv[4];
 #pragma unroll
@@ -147,8 +157,13 @@ __global__ void __launch_bounds__(NTHR, (DO_SUM || RI == 8) ? 2 : 4) k_simt(Simt
                     const float2 d0 = sub2(make_float2(av[i].x, av[i].y), make_float2(bv[j].x, bv[j].y));
                     const float2 d1 = sub2(make_float2(av[i].z, av[i].w), make_float2(bv[j].z, bv[j].w));
                     if (DO_MAX) {
+#if CIL_SIMT_EXP == 4
+                        const float t = fmaxf(fabsf(d0.x), fmaxf(fabsf(d0.y), fabsf(d1.x)));
+                        mx[i][j] = fmaxf(mx[i][j], fmaxf(t, fabsf(d1.y)));
+#else
                         mx[i][j] = absmax3(mx[i][j], d0.x, d0.y);
                         mx[i][j] = absmax3(mx[i][j], d1.x, d1.y);
+#endif
                     }
                     if (DO_SUM) {
                         acc[i][j] = __ffma2_rn(d0, d0, acc[i][j]);
@@ -199,25 +214,39 @@ __global__ void __launch_bounds__(NTHR, (DO_SUM || RI == 8) ? 2 : 4) k_simt(Simt
     const double h = a.bp.h, w = a.bp.w, ih = 1.0 / h, ih2 = 1.0 / (h * h);
     const double U = 5.9604644775390625e-08;            // 2^-24
     const int nreg = a.g.nreg;
+    // The last region's results leave the registers for the (free) operand buffers, so the epilogue
+    // is a rolled loop over this thread's pairs: its code (FP64, per-measure) stays out of the main
+    // loop's register allocation (the unrolled epilogue cost the max family ~20 % through a worse
+    // allocation of the chunk loop, tools/simt_ab.sh) and the kernel stays small.
+    double* last_sum = reinterpret_cast<double*>(As);                  // [NP][NTHR]
+    float* last_max = reinterpret_cast<float*>(last_sum + (DO_SUM ? NP * NTHR : 0));   // [NP][NTHR]
 #pragma unroll
-    for (int i = 0; i < RI; ++i) {
-        const int64_t gi = row0 + ty + 8 * i;
-        float4 sa = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (gi < a.rowsA && nreg > 1) sa = __ldg(reinterpret_cast<const float4*>(a.statA + ((int64_t)p * a.rowsA + gi) * 4));
+    for (int i = 0; i < RI; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            const int64_t gj = col0 + tx + 16 * j;
-            if (gi >= a.rowsA || gj >= a.rowsB) continue;
-            float4 sb = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (nreg > 1) sb = __ldg(reinterpret_cast<const float4*>(a.statB + ((int64_t)p * a.rowsB + gj) * 4));
+            if (DO_SUM) last_sum[(i * 4 + j) * NTHR + tid] = tot[i][j];
+            if (DO_MAX) last_max[(i * 4 + j) * NTHR + tid] = mx[i][j];
+        }
+#pragma unroll 1
+    for (int pi = 0; pi < NP; ++pi) {
+        const int i = pi >> 2, j = pi & 3;
+        const int64_t gi = row0 + ty + 8 * i;
+        const int64_t gj = col0 + tx + 16 * j;
+        if (gi >= a.rowsA || gj >= a.rowsB) continue;
+        {
+            float4 sa = make_float4(0.f, 0.f, 0.f, 0.f), sb = sa;
+            if (nreg > 1) {
+                sa = __ldg(reinterpret_cast<const float4*>(a.statA + ((int64_t)p * a.rowsA + gi) * 4));
+                sb = __ldg(reinterpret_cast<const float4*>(a.statB + ((int64_t)p * a.rowsB + gj) * 4));
+            }
             double s[3] = {0.0, 0.0, 0.0}, m[3] = {0.0, 0.0, 0.0};
 #pragma unroll
             for (int r = 0; r < 3; ++r) {
                 if (r >= nreg) break;
                 const bool last = (r == nreg - 1);
-                const int e = (r * NP + i * 4 + j) * NTHR + tid;
-                if (DO_SUM) s[r] = last ? tot[i][j] : rs_sum[e];
-                if (DO_MAX) m[r] = last ? (double)mx[i][j] : (double)rs_max[e];
+                const int e = (r * NP + pi) * NTHR + tid;
+                if (DO_SUM) s[r] = last ? last_sum[pi * NTHR + tid] : rs_sum[e];
+                if (DO_MAX) m[r] = last ? (double)last_max[pi * NTHR + tid] : (double)rs_max[e];
             }
             const double sw = sqrt(w);
             const double a0 = sqrt(w * s[0]), ax = sqrt(w * s[1] * ih2), ay = sqrt(w * s[2] * ih2);
@@ -242,6 +271,9 @@ __global__ void __launch_bounds__(NTHR, (DO_SUM || RI == 8) ? 2 : 4) k_simt(Simt
                     default: d = m0 + mxx + myy; E = em0 + emx + emy; break;
                 }
                 E += 1e-14 * d;                  // FP64 evaluation of d and of the bound
+#ifdef CIL_SIMT_NOBOUND
+                E = 0.0;                         // timing experiment builds only (tools/simt_ab.sh)
+#endif
                 if (a.range) {               // distance-range mode (adaptive radii)
                     unsigned long long* rg = a.range + ((int64_t)p * nq + q) * 2;
                     if (d > 0.0) atomicMin(&rg[0], (unsigned long long)__double_as_longlong(d));
