@@ -9,9 +9,10 @@
 // hist[b] += 1) or, in bin-matrix mode, b is written to the pair's entry (both orders when mirrored).
 //
 // Row-bucketed pass (lists of >= sort_min entries, 2048 unless a diagnostic changes it; VERDICT r1
-// "restructure k_recheck around row reuse"): the list is counting-sorted by (p, i) (k_rk_count, k_rk_scan, k_rk_scatter), then one CTA
-// takes one A row at a time, so the A row stays in L1 / L2 while its partners stream, and every pair
-// is evaluated once for all its listed measures.  Pairs listed only for the max family (Eqs. (6),
+// "restructure k_recheck around row reuse"): the list is counting-sorted by (p, i) (k_rk_count,
+// k_rk_scan, k_rk_scatter) and walked entry-parallel, so the CTAs working at one time share a few A
+// rows (one HBM read each, L2 hits for the rest) while the partners stream, and every pair is
+// evaluated once for all its listed measures.  Pairs listed only for the max family (Eqs. (6),
 // (9), (10)) are first evaluated in FP32 with a rigorous bound (fl is monotone: the FP32 max of
 // |fl(a - b)| is within 2^-24 of the exact max, the differences of the derivative regions within
 // 2^-24 (2 m_0 + |D|) + ...); only a pair whose FP32 interval still contains a radius goes on to the
@@ -24,9 +25,14 @@
 
 #include "cil_internal.cuh"
 
+#ifndef CIL_RK_EXP
+#define CIL_RK_EXP 0   // occupancy / loads-in-flight experiments (tools/simt_var_build.sh); 0 = product
+#endif
+
 namespace cil {
 
 namespace {
+
 // The six FP64 sub-norms of u = x - y over one pattern, one CTA of 256 threads (warp per grid row).
 // full = false: only s0 (a flat K-long loop with 4 float4 pairs in flight per thread).
 __device__ void exact_subnorms(const float* x, const float* y, const RecheckArgs& a, bool full, double out[6],
@@ -114,50 +120,65 @@ __device__ double measure(int k, const double sub[6], double w, double h) {
 }
 
 // The max sub-norms m0, m_x, m_y of u = x - y in FP32 (raw differences, no 1/h), one CTA of 256
-// threads; |result - exact| <= 2^-24 m0, 3 2^-24 (m0 + m_x), 3 2^-24 (m0 + m_y).  W % 4 == 0: flat
-// float4 sweep (4 elements of one grid row per thread; the x neighbour of the last element from the
-// next lane, the y neighbours one grid row on, an L1 / L2 hit), else a warp per grid row.
+// threads; |result - exact| <= 2^-24 m0, 3 2^-24 (m0 + m_x), 3 2^-24 (m0 + m_y).  W % 4 == 0 (and
+// a 16 KB staging buffer us): flat float4 sweep in chunks of 4096 elements, u staged in shared
+// memory for the neighbours; else a warp per grid row.
 __device__ __forceinline__ float amax4(float m, float a, float b, float c, float d) {
     return fmaxf(fmaxf(m, fmaxf(fabsf(a), fabsf(b))), fmaxf(fabsf(c), fabsf(d)));
 }
-__device__ void max_subnorms32(const float* x, const float* y, const RecheckArgs& a, float out[3], float (*red)[8]) {
+__device__ void max_subnorms32(const float* x, const float* y, const RecheckArgs& a, float out[3], float (*red)[8],
+                               float* us) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     float v[3] = {0.f, 0.f, 0.f};
     const int W = a.W, H = a.H;
-    if ((W & 3) == 0) {
-        constexpr int U4 = 4;                            // float4 pairs in flight per thread
-        for (int64_t base = 0; base < a.K; base += 1024 * U4) {
+    if ((W & 3) == 0 && us != nullptr) {
+        // chunks of 4096 elements: u = x - y staged in shared memory (us), so the x and y
+        // neighbours come from there; only those past the chunk end are loaded again (a
+        // cp.async double-buffered variant ran 20 % slower: profiles/r02_recheck.txt)
+        constexpr int U4 = 4, CH = 1024 * U4;
+        const uint32_t K = (uint32_t)a.K;
+        for (uint32_t base = 0; base < K; base += CH) {
             float4 xa[U4], yb[U4];
 #pragma unroll
             for (int t = 0; t < U4; ++t) {
-                const int64_t e = base + t * 1024 + threadIdx.x * 4;
-                if (e < a.K) {
+                const uint32_t e = base + t * 1024 + threadIdx.x * 4;
+                if (e < K) {
                     xa[t] = __ldg(reinterpret_cast<const float4*>(x + e));
                     yb[t] = __ldg(reinterpret_cast<const float4*>(y + e));
                 } else {
                     xa[t] = yb[t] = make_float4(0.f, 0.f, 0.f, 0.f);
                 }
             }
+            __syncthreads();                                   // previous chunk's reads of us are done
+#pragma unroll
+            for (int t = 0; t < U4; ++t)
+                reinterpret_cast<float4*>(us)[t * 256 + threadIdx.x] =
+                    make_float4(xa[t].x - yb[t].x, xa[t].y - yb[t].y, xa[t].z - yb[t].z, xa[t].w - yb[t].w);
+            __syncthreads();
 #pragma unroll
             for (int t = 0; t < U4; ++t) {
-                const int64_t e = base + t * 1024 + threadIdx.x * 4;
-                const float4 u = make_float4(xa[t].x - yb[t].x, xa[t].y - yb[t].y, xa[t].z - yb[t].z, xa[t].w - yb[t].w);
-                float nx = __shfl_down_sync(0xffffffffu, u.x, 1);      // element e + 4 (next lane)
-                if (e >= a.K) continue;
+                const uint32_t l = t * 1024 + threadIdx.x * 4, e = base + l;
+                if (e >= K) continue;
+                const float4 u = reinterpret_cast<const float4*>(us)[t * 256 + threadIdx.x];
                 v[0] = amax4(v[0], u.x, u.y, u.z, u.w);
-                const int64_t sr = e / W;
-                const int c = (int)(e - sr * W);
-                const int sp = (int)(sr / H), hr = (int)(sr - (int64_t)sp * H);
+                const uint32_t sr = e / (uint32_t)W, c = e - sr * (uint32_t)W;
+                const uint32_t sp = sr / (uint32_t)H, hr = sr - sp * (uint32_t)H;
                 if (!(a.gs == 0 || ((a.gs >> sp) & 1u))) continue;
-                if (c + 4 < W) {
-                    if (lane == 31) nx = __ldg(x + e + 4) - __ldg(y + e + 4);
+                v[1] = fmaxf(v[1], fmaxf(fabsf(u.y - u.x), fmaxf(fabsf(u.z - u.y), fabsf(u.w - u.z))));
+                if (c + 4 < (uint32_t)W) {
+                    const float nx = l + 4 < (uint32_t)CH ? us[l + 4] : __ldg(x + e + 4) - __ldg(y + e + 4);
                     v[1] = fmaxf(v[1], fabsf(nx - u.w));
                 }
-                v[1] = fmaxf(v[1], fmaxf(fabsf(u.y - u.x), fmaxf(fabsf(u.z - u.y), fabsf(u.w - u.z))));
-                if (hr + 1 < H) {
-                    const float4 xd = __ldg(reinterpret_cast<const float4*>(x + e + W));
-                    const float4 yd = __ldg(reinterpret_cast<const float4*>(y + e + W));
-                    v[2] = amax4(v[2], (xd.x - yd.x) - u.x, (xd.y - yd.y) - u.y, (xd.z - yd.z) - u.z, (xd.w - yd.w) - u.w);
+                if (hr + 1 < (uint32_t)H) {
+                    float4 d;
+                    if (l + W < (uint32_t)CH) {
+                        d = *reinterpret_cast<const float4*>(us + l + W);
+                    } else {
+                        const float4 xd = __ldg(reinterpret_cast<const float4*>(x + e + W));
+                        const float4 yd = __ldg(reinterpret_cast<const float4*>(y + e + W));
+                        d = make_float4(xd.x - yd.x, xd.y - yd.y, xd.z - yd.z, xd.w - yd.w);
+                    }
+                    v[2] = amax4(v[2], d.x - u.x, d.y - u.y, d.z - u.z, d.w - u.w);
                 }
             }
         }
@@ -202,13 +223,11 @@ __device__ void measure32(int k, const float m[3], double h, double* d, double* 
     *E += 1e-14 * *d;
 }
 
-__device__ void settle(const RecheckArgs& a, int64_t p, int64_t i, int64_t j, int kind, int b_lo, double d,
-                       bool add_only) {
+// Move pair (i, j) of measure `kind` from its provisional bin b_lo to its exact bin b (or write b).
+__device__ void settle_bin(const RecheckArgs& a, int64_t p, int64_t i, int64_t j, int kind, int b_lo, int b,
+                           bool add_only) {
     const int q = a.qslot[kind];
     CIL_CHECK(kind >= 0 && kind < 6 && q >= 0 && q < a.nq && p < a.P && i < a.rowsA && j < a.rowsB);
-    const double* R = a.thr + p * a.thr_stride + (int64_t)q * a.M;
-    int b = 0;
-    while (b < a.M && d < R[b]) ++b;
     if (a.binout && a.transpose) {                       // [p][q][j][i] (the engine's transposed output)
         a.binout[(((int64_t)p * a.nq + q) * a.rowsB + j) * a.rowsA + i] = (uint8_t)b;
     } else if (a.binout) {
@@ -225,6 +244,20 @@ __device__ void settle(const RecheckArgs& a, int64_t p, int64_t i, int64_t j, in
             if (b > 0) atomicAdd(&H[hist_index(a.sp, a.nq, a.M, p, rs, cs, q, b)], 1ull);
         }
     }
+}
+
+__device__ void settle(const RecheckArgs& a, int64_t p, int64_t i, int64_t j, int kind, int b_lo, double d,
+                       bool add_only) {
+    const double* R = a.thr + p * a.thr_stride + (int64_t)a.qslot[kind] * a.M;
+    int b = 0;
+    while (b < a.M && d < R[b]) ++b;
+    settle_bin(a, p, i, j, kind, b_lo, b, add_only);
+}
+
+// #{m : v < R_m} of slot `kind` of item p, counted by the whole CTA (R is decreasing; M <= 64)
+__device__ __forceinline__ int bin_of(const RecheckArgs& a, int64_t p, int kind, double v) {
+    const double* R = a.thr + p * a.thr_stride + (int64_t)a.qslot[kind] * a.M;
+    return __syncthreads_count((int)threadIdx.x < a.M && v < R[threadIdx.x]);
 }
 }  // namespace
 
@@ -284,7 +317,7 @@ __global__ void k_fb_clear(RecheckArgs a, int64_t hist_elems) {
         a.hist[e] = 0ull;
 }
 
-__global__ void __launch_bounds__(256) k_recheck(RecheckArgs a) {
+__global__ void __launch_bounds__(256, CIL_RK_EXP == 1 ? 3 : CIL_RK_EXP == 3 ? 2 : 4) k_recheck(RecheckArgs a) {
     const uint32_t c = *a.ctr;
     const bool overflow = c > a.cap;
     __shared__ double red[6][8];
@@ -318,77 +351,67 @@ __global__ void __launch_bounds__(256) k_recheck(RecheckArgs a) {
         }
         return;
     }
-    // row-bucketed pass: one A row per CTA at a time, every listed pair evaluated once
-    __shared__ uint32_t sj[256], sw[256];
-    __shared__ uint32_t s_kmask, s_exact;
+    // row-bucketed pass: the CTAs walk the SORTED list entry-parallel (consecutive entries share
+    // their A row, so concurrent CTAs read it together: one HBM read, L2 hits for the rest); the
+    // first entry of a pair (i, j) in its row bucket owns the pair and settles all its measures
+    // (bins counted by the whole CTA over the radii, no serial loops over global memory)
+    __shared__ uint32_t s_n, s_w[8];
+    __shared__ double s_d[8], s_E[8];
     __shared__ float red32[3][8];
     __shared__ float m32[3];
-    const int64_t nrows = (int64_t)a.P * a.rowsA;
-    for (int64_t row = blockIdx.x; row < nrows; row += gridDim.x) {
+    __shared__ __align__(16) float us[4096];
+    for (uint32_t e = blockIdx.x; e < c; e += gridDim.x) {
+        const uint4 ent = a.rk_list[e];
+        const int64_t p = ent.x, i = ent.y, j = ent.z;
+        const int64_t row = p * a.rowsA + i;
         const uint32_t beg = row ? a.rk[row - 1] : 0u, end = a.rk[row];
-        if (beg == end) continue;
-        const int64_t p = row / a.rowsA, i = row % a.rowsA;
-        const float* xa = row_ptr(a.asrc, p, i);
-        for (uint32_t b0 = beg; b0 < end; b0 += 256) {
-            const int n = (int)min(256u, end - b0);
-            __syncthreads();
-            if ((int)threadIdx.x < n) {
-                const uint4 ent = a.rk_list[b0 + threadIdx.x];
-                sj[threadIdx.x] = ent.z;
-                sw[threadIdx.x] = ent.w;
-            }
-            __syncthreads();
-            for (int t = 0; t < n; ++t) {
-                const uint32_t j = sj[t];
-                bool first = true;                       // the first entry of pair (i, j) in the batch owns it
-                for (int u = 0; u < t && first; ++u) first = sj[u] != j;
-                if (!first) continue;
-                __syncthreads();                         // everyone is done with the previous pair's flags
-                if (threadIdx.x == 0) { s_kmask = 0u; s_exact = 0u; }
-                __syncthreads();
-                if ((int)threadIdx.x < n && sj[threadIdx.x] == j) atomicOr(&s_kmask, 1u << ((sw[threadIdx.x] >> 8) & 255u));
-                __syncthreads();
-                const uint32_t kmask = s_kmask;
-                const float* yb = row_ptr(a.bsrc, p, j);
-                if (!(kmask & 0x0Du)) {                  // max family only: FP32 interval first
-                    max_subnorms32(xa, yb, a, m32, red32);
-                    if (threadIdx.x == 0) {
-                        for (int u = t; u < n; ++u) {
-                            if (sj[u] != j) continue;
-                            const int kind = (int)((sw[u] >> 8) & 255u);
-                            double d, E;
-                            measure32(kind, m32, a.h, &d, &E);
-                            const double* R = a.thr + p * a.thr_stride + (int64_t)a.qslot[kind] * a.M;
-                            int bh = 0, bl = 0;
-                            while (bh < a.M && d + E < R[bh]) ++bh;
-                            while (bl < a.M && d - E < R[bl]) ++bl;
-                            if (bh == bl) settle(a, p, i, j, kind, (int)(sw[u] & 255u), d, false);
-                            else s_exact = 1u;
-                        }
-                    }
-                    __syncthreads();
-                    if (!s_exact) continue;
-                }
-                exact_subnorms(xa, yb, a, (kmask & ~1u) != 0u, sub, red);
-                if (threadIdx.x == 0) {
-                    for (int u = t; u < n; ++u) {
-                        if (sj[u] != j) continue;
-                        const int kind = (int)((sw[u] >> 8) & 255u);
-                        if (!(kmask & 0x0Du)) {          // max family: only the kinds FP32 left open
-                            double d, E;
-                            measure32(kind, m32, a.h, &d, &E);
-                            const double* R = a.thr + p * a.thr_stride + (int64_t)a.qslot[kind] * a.M;
-                            int bh = 0, bl = 0;
-                            while (bh < a.M && d + E < R[bh]) ++bh;
-                            while (bl < a.M && d - E < R[bl]) ++bl;
-                            if (bh == bl) continue;
-                        }
-                        settle(a, p, i, j, kind, (int)(sw[u] & 255u), measure(kind, sub, a.w, a.h), false);
-                    }
-                }
-                __syncthreads();
+        if (threadIdx.x == 0) s_n = 0u;
+        __syncthreads();
+        bool dup = false;
+        for (uint32_t u = beg + threadIdx.x; u < end; u += blockDim.x) {
+            const uint4 o = a.rk_list[u];
+            if (o.z != ent.z) continue;
+            if (u < e) dup = true;
+            else {
+                const uint32_t k = atomicAdd(&s_n, 1u);
+                if (k < 8) s_w[k] = o.w;
             }
         }
+        if (__syncthreads_or(dup)) continue;
+        const int n = (int)min(s_n, 8u);                  // a pair is listed at most once per measure
+        uint32_t kmask = 0u;
+        for (int k = 0; k < n; ++k) kmask |= 1u << ((s_w[k] >> 8) & 255u);
+        const float* xa = row_ptr(a.asrc, p, i);
+        const float* yb = row_ptr(a.bsrc, p, j);
+        bool exact = true;
+        if (!(kmask & 0x0Du)) {                              // max family only: FP32 interval first
+            max_subnorms32(xa, yb, a, m32, red32, a.K < (1ll << 31) ? us : nullptr);
+            if ((int)threadIdx.x < n) measure32((int)((s_w[threadIdx.x] >> 8) & 255u), m32, a.h, &s_d[threadIdx.x], &s_E[threadIdx.x]);
+            __syncthreads();
+            exact = false;
+            for (int k = 0; k < n; ++k) {
+                const int kind = (int)((s_w[k] >> 8) & 255u);
+                const int bh = bin_of(a, p, kind, s_d[k] + s_E[k]), bl = bin_of(a, p, kind, s_d[k] - s_E[k]);
+                if (bh == bl) {
+                    if (threadIdx.x == 0) settle_bin(a, p, i, j, kind, (int)(s_w[k] & 255u), bh, false);
+                    if (threadIdx.x == 0) s_w[k] |= 0x80000000u;      // settled
+                } else {
+                    exact = true;
+                }
+            }
+            __syncthreads();
+        }
+        if (!exact) continue;
+        exact_subnorms(xa, yb, a, (kmask & ~1u) != 0u, sub, red);
+        if ((int)threadIdx.x < n) s_d[threadIdx.x] = measure((int)((s_w[threadIdx.x] >> 8) & 255u), sub, a.w, a.h);
+        __syncthreads();
+        for (int k = 0; k < n; ++k) {
+            if (s_w[k] & 0x80000000u) continue;
+            const int kind = (int)((s_w[k] >> 8) & 255u);
+            const int b = bin_of(a, p, kind, s_d[k]);
+            if (threadIdx.x == 0) settle_bin(a, p, i, j, kind, (int)(s_w[k] & 255u), b, false);
+        }
+        __syncthreads();
     }
 }
 
