@@ -230,7 +230,7 @@ Layout make_layout(int P, int64_t rowsA, int64_t rowsB, const cil_grid& g, int n
                 const AugGeom ag = make_aug_geom(g.S, g.H, g.W, 3);
                 L.kp[0] = 0;
                 L.kp[1] = L.Kp;
-                L.kp[2] = L.kp[1] + round_up(ag.Kx, kTcBK);
+                L.kp[2] = L.kp[1] + round_up(ag.K, kTcBK);          // D_x rows padded to W (pack3_aug)
                 L.kp[3] = L.kp[2] + round_up(ag.Ky, kTcBK);
                 L.Krow = L.kp[3];
                 L.nph = 3;

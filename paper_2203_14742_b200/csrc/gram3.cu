@@ -984,14 +984,15 @@ __global__ void __launch_bounds__(256) k_pack3_aug(RowSrc src, int64_t rows, Aug
             if (ln == 31 && col + 1 < W) xn = xt(base + col + 1);
             if (!in) continue;
             put(0, kp0 + base + col, xe);
-            if (col + 1 < W) put(1, kp1 + (int64_t)sr * (W - 1) + col, grad ? xn - xe : 0.f);
+            put(1, kp1 + base + col, grad && col + 1 < W ? xn - xe : 0.f);   // D_x rows padded to W
             if (has_dy) put(2, kp2 + base - (int64_t)s * W + col, grad ? xt(base + W + col) - xe : 0.f);
         }
     }
     const int64_t len[3] = {g.K, g.Kx, g.Ky}, beg[3] = {kp0, kp1, kp2}, end[3] = {kp1, kp2, kp3};
+    const int64_t used[3] = {g.K, g.K, g.Ky};                   // D_x rows padded to W
 #pragma unroll
     for (int a = 0; a < 3; ++a)
-        for (int64_t col = beg[a] + len[a] + threadIdx.x; col < end[a]; col += 256) {
+        for (int64_t col = beg[a] + used[a] + threadIdx.x; col < end[a]; col += 256) {
             ph[col] = 0; ph[col + plane_stride] = 0; ph[col + 2 * plane_stride] = 0;
         }
 #pragma unroll
@@ -1012,6 +1013,138 @@ __global__ void __launch_bounds__(256) k_pack3_aug(RowSrc src, int64_t rows, Aug
             for (int i = 0; i < 6; ++i) {
                 long long v = 0;
                 for (int j = 0; j < 8; ++j) v += redd[j][a][i];
+                Sl[i] = v;
+            }
+            const double slack = a == 0 ? 0.0 : 2.0 * 5.9604644775390625e-08 * 1.001 * tnorm;
+            float* out = meta + (orow * 3 + a) * 8;
+            write_meta(out, sg[a], inv[a], Sl, (double)len[a], slack, ex[a], 0.0);
+            if (a == 0) tnorm = sqrt((double)out[0]) * (1.0 + 1e-6) + (double)out[2];
+        }
+        if (anynf) atomicOr(&status[p], CIL_ITEM_NONFINITE);
+    }
+}
+
+// k_pack3_aug for W % 4 == 0: a flat float4 sweep (4 elements of one grid row per thread, the
+// x neighbour of the 4th from the next lane, the y neighbours one grid row on from L1 / L2), two
+// passes (maxima, then quantise + store; the second reads the row from L2), one 32-bit store per
+// plane and 4 values (the D_x rows are padded to W, so every block is 4-aligned).  Same values,
+// digits, sums and metadata as k_pack3_aug.
+__global__ void __launch_bounds__(512, 2) k_pack3_aug4(RowSrc src, int64_t rows, AugGeom g, int64_t kp0, int64_t kp1,
+                                                    int64_t kp2, int64_t kp3, const float* __restrict__ center,
+                                                    int64_t Kc, int8_t* __restrict__ planes, int64_t plane_stride,
+                                                    int64_t Krow, int64_t row0, float* __restrict__ meta,
+                                                    int32_t* __restrict__ status) {
+    constexpr int NT = 512, NW = NT / 32;
+    const int64_t p = blockIdx.y;
+    const int64_t r = blockIdx.x;
+    const float* x = row_ptr(src, p, r);
+    const float* cc = center + p * Kc;
+    const int64_t orow = row0 + p * rows + r;
+    const uint32_t W = (uint32_t)g.W, H = (uint32_t)g.H, K = (uint32_t)g.K;
+    __shared__ float red[3][NW];
+    __shared__ long long redd[NW][3][6];
+    const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
+    // one float4 of x~ = x - c and its derivative float4s (0 where there is no neighbour / masked)
+    auto load = [&](uint32_t e, float4& t, float4& dx, float4& dy) {
+        const bool ok = e < K;
+        t = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (ok) {
+            const float4 xv = __ldg(reinterpret_cast<const float4*>(x + e));
+            const float4 cv = __ldg(reinterpret_cast<const float4*>(cc + e));
+            t = make_float4(xv.x - cv.x, xv.y - cv.y, xv.z - cv.z, xv.w - cv.w);
+        }
+        float nx = __shfl_down_sync(0xffffffffu, t.x, 1);
+        dx = dy = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (!ok) return;
+        const uint32_t sr = e / W, c = e - sr * W, sp = sr / H, hr = sr - sp * H;
+        if (!(g.gs == 0 || ((g.gs >> sp) & 1u))) return;
+        if (c + 4 < W && ln == 31) nx = (__ldg(x + e + 4) - __ldg(cc + e + 4));
+        dx = make_float4(t.y - t.x, t.z - t.y, t.w - t.z, c + 4 < W ? nx - t.w : 0.f);
+        if (hr + 1 < H) {
+            const float4 xv = __ldg(reinterpret_cast<const float4*>(x + e + W));
+            const float4 cv = __ldg(reinterpret_cast<const float4*>(cc + e + W));
+            dy = make_float4((xv.x - cv.x) - t.x, (xv.y - cv.y) - t.y, (xv.z - cv.z) - t.z, (xv.w - cv.w) - t.w);
+        }
+    };
+    float m0 = 0.f, mx = 0.f, my = 0.f;
+    for (uint32_t base = 0; base < K; base += NT * 4) {
+        float4 t, dx, dy;
+        load(base + threadIdx.x * 4, t, dx, dy);
+        m0 = absmax3_nan(absmax3_nan(m0, t.x, t.y), t.z, t.w);
+        mx = fmaxf(fmaxf(mx, fmaxf(fabsf(dx.x), fabsf(dx.y))), fmaxf(fabsf(dx.z), fabsf(dx.w)));
+        my = fmaxf(fmaxf(my, fmaxf(fabsf(dy.x), fabsf(dy.y))), fmaxf(fabsf(dy.z), fabsf(dy.w)));
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        const float t = __shfl_xor_sync(0xffffffffu, m0, o);
+        asm("max.NaN.f32 %0, %0, %1;" : "+f"(m0) : "f"(t));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        my = fmaxf(my, __shfl_xor_sync(0xffffffffu, my, o));
+    }
+    if (ln == 0) { red[0][w] = m0; red[1][w] = mx; red[2][w] = my; }
+    __syncthreads();
+    float sg[3], inv[3];
+    bool ex[3];
+    bool anynf = false;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        float m = 0.f;
+        for (int i = 0; i < NW; ++i) {
+            if (a == 0) asm("max.NaN.f32 %0, %0, %1;" : "+f"(m) : "f"(red[a][i]));
+            else m = fmaxf(m, red[a][i]);
+        }
+        if (a == 0) anynf = !(m <= 3.0e38f);
+        const bool ok = m >= kMinMax && m <= kMaxMax;
+        ex[a] = m > 0.f && !ok;
+        sg[a] = ok ? m / kQ : 1.f;
+        inv[a] = 1.f / sg[a];
+    }
+    int8_t* ph = planes + orow * Krow;
+    int S[3][6];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int i = 0; i < 6; ++i) S[a][i] = 0;
+    auto put4 = [&](int a, int64_t col, const float4 v) {
+        uint32_t wh = 0, wm = 0, wl = 0;
+        if (!ex[a]) quant4(v, inv[a], wh, wm, wl, S[a]);
+        CIL_CHECK(orow * Krow + col + 4 <= plane_stride);
+        *reinterpret_cast<uint32_t*>(ph + col) = wh;
+        *reinterpret_cast<uint32_t*>(ph + col + plane_stride) = wm;
+        *reinterpret_cast<uint32_t*>(ph + col + 2 * plane_stride) = wl;
+    };
+    for (uint32_t base = 0; base < K; base += NT * 4) {
+        const uint32_t e = base + threadIdx.x * 4;
+        float4 t, dx, dy;
+        load(e, t, dx, dy);
+        if (e >= K) continue;
+        const uint32_t sr = e / W, sp = sr / H, hr = sr - sp * H;
+        put4(0, kp0 + e, t);
+        put4(1, kp1 + e, dx);
+        if (hr + 1 < H) put4(2, kp2 + (int64_t)e - (int64_t)sp * W, dy);
+    }
+    const int64_t len[3] = {g.K, g.Kx, g.Ky}, beg[3] = {kp0, kp1, kp2}, end[3] = {kp1, kp2, kp3};
+    const int64_t used[3] = {g.K, g.K, g.Ky};
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+        for (int64_t col = beg[a] + used[a] + threadIdx.x; col < end[a]; col += NT) {
+            ph[col] = 0; ph[col + plane_stride] = 0; ph[col + 2 * plane_stride] = 0;
+        }
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int i = 0; i < 6; ++i) {
+            long long v = S[a][i];
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (ln == 0) redd[w][a][i] = v;
+        }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double tnorm = 0.0;
+        for (int a = 0; a < 3; ++a) {
+            long long Sl[6];
+            for (int i = 0; i < 6; ++i) {
+                long long v = 0;
+                for (int j = 0; j < NW; ++j) v += redd[j][a][i];
                 Sl[i] = v;
             }
             const double slack = a == 0 ? 0.0 : 2.0 * 5.9604644775390625e-08 * 1.001 * tnorm;
@@ -1067,8 +1200,12 @@ cudaError_t launch_pack3_aug(int P, const RowSrc& src, int64_t rows, const AugGe
     if (rows == 0) return cudaSuccess;
     dim3 grid((unsigned)rows, (unsigned)P);
     ProfScope ps_(K_PACK, st);
-    g3::k_pack3_aug<<<grid, 256, 0, st>>>(src, rows, g, kp[0], kp[1], kp[2], kp[3], center, Kc, planes, plane_stride,
-                                          kp[3], row0, meta, status);
+    if (g.W % 4 == 0 && g.K < (1ll << 31))
+        g3::k_pack3_aug4<<<grid, 512, 0, st>>>(src, rows, g, kp[0], kp[1], kp[2], kp[3], center, Kc, planes,
+                                               plane_stride, kp[3], row0, meta, status);
+    else
+        g3::k_pack3_aug<<<grid, 256, 0, st>>>(src, rows, g, kp[0], kp[1], kp[2], kp[3], center, Kc, planes,
+                                              plane_stride, kp[3], row0, meta, status);
     note_launch();
     return cudaGetLastError();
 }
