@@ -185,7 +185,7 @@ Plan plan_union(const Plan& a, const Plan& b) {
 // Workspace carve-up (identical in the size query and in the call).
 struct Layout {
     size_t off_thr, off_thr2, off_hist, off_ctr, off_list, off_center, off_hi, off_lo, off_nrm, off_q4,
-        off_aug, off_rowstat, off_aug16, off_max16, off_rk, off_rk_list, off_Y, off_mu, off_sig, off_part, total;
+        off_aug, off_rowstat, off_aug16, off_max16, off_dmax16, off_rk, off_rk_list, off_Y, off_mu, off_sig, off_part, total;
     int64_t hist_elems = 0;
     uint32_t list_cap = 0;
     int64_t Kp = 0;
@@ -255,6 +255,7 @@ Layout make_layout(int P, int64_t rowsA, int64_t rowsB, const cil_grid& g, int n
         L.geom16 = make_aug_geom(g.S, g.H, g.W, pl.nreg, g.gs, kMax16BK);
         L.off_aug16 = take(sizeof(int16_t) * (size_t)rows * L.geom16.off[3]);
         L.off_max16 = take(sizeof(unsigned) * 8 * (size_t)P);
+        L.off_dmax16 = take(sizeof(uint16_t) * 3 * (size_t)P * rowsA * rowsB);
     }
     if (nY > 0) {
         L.off_Y = take(sizeof(double) * (size_t)nY);
@@ -388,6 +389,7 @@ cil_status run_engines(int P, const RowSrc& asrc, const RowSrc& bsrc, int64_t ro
         a.rowsA = rowsA; a.rowsB = rowsB; a.Kaug = L.geom16.off[3];
         a.g = g16;
         a.maxbits = maxbits;
+        a.dmax = at<uint16_t>(ws, L.off_dmax16);
         a.bp = bp;
         a.sp = sp;
         a.thr = thr; a.thr_stride = (int64_t)sl.nq * M;

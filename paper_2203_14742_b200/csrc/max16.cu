@@ -16,7 +16,8 @@
 // pairs per SM-cycle measured, profiles/r02_maxmix.txt); packed 16-bit VIADD.16x2 + VIMNMX3.S16x2
 // max / min run at 105 (tools/maxmix2_bench.cu), and the operands are half the bytes.
 //
-// Kernel: CTA = 128 threads = 64 A rows x 64 B rows, 8 x 4 pairs per thread.  Operands are stored
+// Kernels: k_max16_reg, CTA = 128 threads = 64 A rows x 64 B rows x one region, 8 x 4 pairs per
+// thread; k_max16_bin, the binning epilogue over the per-pair region maxima.  Operands are stored
 // biased, A as q + 16384 and B as -q + 16384 (both in [384, 32384]), so ONE 32-bit integer add of two
 // packed words gives both 16-bit lanes t = q_a - q_b + 32768 in [768, 64768] with no carry between
 // the lanes — issued as IMAD on the FMA pipe, which leaves the integer ALU pipe to the
@@ -189,23 +190,24 @@ __global__ void __launch_bounds__(256) k_pack16(RowSrc src, int64_t rows, AugGeo
         for (int64_t t = g.Ky + threadIdx.x; t < g.off[3] - g.off[2]; t += 256) o[g.off[2] + t] = kBias;
 }
 
-// ----------------------------------------------------------------- the max-family tile kernel
+// ----------------------------------------------------------------- the max-family tile kernels
+// k_max16_reg: one CTA per (64 x 64 tile, region): the packed running max / min over the region's
+// chunks, then the per-pair region maximum max |q_a - q_b| (u16) to dmax[p][r][i][j] (staged in
+// shared memory, stored row-contiguous).  Splitting by region triples the work units (3072 for C3
+// instead of 1024 tiles over 444 resident CTAs), so the last partial wave costs ~3 % instead of ~12 %.
+// k_max16_bin: the epilogue over the same tile grid — interval, bin at the upper end, re-check list,
+// histogram or bin matrix.
 #ifndef CIL_M16_EXP
 #define CIL_M16_EXP 0   // code-generation experiments (tools/simt_var_build.sh); 0 = product
 #endif
 template <bool SYM>
-__global__ void __launch_bounds__(NTHR, CIL_M16_EXP == 1 ? 4 : 3) k_max16(Max16Args a) {
+__global__ void __launch_bounds__(NTHR, CIL_M16_EXP == 1 ? 4 : 3) k_max16_reg(Max16Args a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     uint32_t* As = reinterpret_cast<uint32_t*>(smem_raw);           // [2][TA][LDW]
     uint32_t* Bs = As + 2 * TA * LDW;                                // [2][TB][LDW]
-    const int nq = a.bp.nq, M = a.bp.M;
-    double* thr_s = reinterpret_cast<double*>(Bs + 2 * TB * LDW);    // [nq*M]
-    // per-pair region maxima: regions 0, 1 here, region 2 (always the last) in the free As buffer
-    uint16_t* rs = reinterpret_cast<uint16_t*>(thr_s + ((nq * M + 1) & ~1));   // [2][NP][NTHR]
-    uint32_t* hist_s = reinterpret_cast<uint32_t*>(rs + 2 * NP * NTHR);
-    auto rslot = [&](int r) { return r < 2 ? rs + r * NP * NTHR : reinterpret_cast<uint16_t*>(As); };
 
-    const int p = blockIdx.z;
+    const int nreg = a.g.nreg;
+    const int p = blockIdx.z / nreg, region = blockIdx.z % nreg;
     if (a.status[p] & CIL_ITEM_BADRADII) return;
     const int64_t row0 = (int64_t)blockIdx.y * TA;
     const int64_t col0 = (int64_t)blockIdx.x * TB;
@@ -216,20 +218,9 @@ __global__ void __launch_bounds__(NTHR, CIL_M16_EXP == 1 ? 4 : 3) k_max16(Max16A
     const int ty = (warp >> 1) * 4 + (lane >> 3);   // 0..7
     const int tx = (warp & 1) * 8 + (lane & 7);     // 0..15
 
-    for (int t = tid; t < nq * M; t += NTHR) thr_s[t] = a.thr[(int64_t)p * a.thr_stride + t];
-    const int64_t rlast = min(row0 + TA, a.rowsA) - 1, clast = min(col0 + TB, a.rowsB) - 1;
-    const int64_t rs0 = row0 / a.sp.row_seg, cs0 = col0 / a.sp.col_seg;
-    const int nrs = (int)(rlast / a.sp.row_seg - rs0 + 1), ncs = (int)(clast / a.sp.col_seg - cs0 + 1);
-    const int hist_len = nrs * ncs * nq * (M + 1);
-    const bool use_sh = hist_len <= a.hist_cap;
-    if (use_sh)
-        for (int t = tid; t < hist_len; t += NTHR) hist_s[t] = 0u;
-
     const int16_t* Ag = a.A + ((int64_t)p * a.rowsA) * a.Kaug;
     const int16_t* Bg = a.B + ((int64_t)p * a.rowsB) * a.Kaug;
-    const int nchunks = (int)(a.g.off[a.g.nreg] / kMax16BK);
-    const int c_end0 = (int)(a.g.off[1] / kMax16BK);
-    const int c_end1 = (int)(a.g.off[2] / kMax16BK);
+    const int cb = (int)(a.g.off[region] / kMax16BK), ce = (int)(a.g.off[region + 1] / kMax16BK);
 
     auto load_chunk = [&](int c, int buf) {
         const int64_t k0 = (int64_t)c * kMax16BK;
@@ -252,19 +243,17 @@ __global__ void __launch_bounds__(NTHR, CIL_M16_EXP == 1 ? 4 : 3) k_max16(Max16A
         cp_async_commit();
     };
 
-    uint32_t mx[RI][4], mn[RI][4];   // packed (2 x s16) running max / min of a - b
+    uint32_t mx[RI][4], mn[RI][4];   // packed (2 x u16) running max / min of t = q_a - q_b + 32768
 #pragma unroll
     for (int i = 0; i < RI; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) { mx[i][j] = 0u; mn[i][j] = 0xffffffffu; }
 
-#pragma unroll
-    for (int t = 0; t < 2 * NP; ++t) rs[t * NTHR + tid] = 0;     // an empty region 1 (W = 1) reads 0
     const uint32_t one = a.one;
-    load_chunk(0, 0);
-    for (int c = 0; c < nchunks; ++c) {
-        const int buf = c & 1;
-        if (c + 1 < nchunks) {
+    if (cb < ce) load_chunk(cb, 0);
+    for (int c = cb; c < ce; ++c) {
+        const int buf = (c - cb) & 1;
+        if (c + 1 < ce) {
             load_chunk(c + 1, buf ^ 1);
             cp_async_wait<1>();
         } else {
@@ -276,9 +265,9 @@ __global__ void __launch_bounds__(NTHR, CIL_M16_EXP == 1 ? 4 : 3) k_max16(Max16A
 #if CIL_M16_EXP == 2
 #pragma unroll 1
 #elif CIL_M16_EXP == 3
-#pragma unroll 4
-#else
 #pragma unroll 2
+#else
+#pragma unroll 4
 #endif
         for (int kk = 0; kk < BKW; kk += 4) {
             uint4 av[RI], bv[4];
@@ -299,21 +288,47 @@ __global__ void __launch_bounds__(NTHR, CIL_M16_EXP == 1 ? 4 : 3) k_max16(Max16A
                 }
         }
         __syncthreads();
-        const bool region_end = (c + 1 == c_end0) || (c + 1 == c_end1) || (c + 1 == nchunks);
-        if (region_end) {
-            const int region = c < c_end0 ? 0 : c < c_end1 ? 1 : 2;
-#pragma unroll
-            for (int i = 0; i < RI; ++i)
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    rslot(region)[(i * 4 + j) * NTHR + tid] = (uint16_t)absmax_pair(mx[i][j], mn[i][j]);
-                    mx[i][j] = 0u;
-                    mn[i][j] = 0xffffffffu;
-                }
-        }
     }
+    // stage the 64 x 64 region maxima (an empty region gives 0) and store them row-contiguous
+    uint16_t* tile = reinterpret_cast<uint16_t*>(As);                // [TA][TB]
+#pragma unroll
+    for (int i = 0; i < RI; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            tile[(ty + 8 * i) * TB + tx + 16 * j] = cb < ce ? (uint16_t)absmax_pair(mx[i][j], mn[i][j]) : (uint16_t)0;
+    __syncthreads();
+    uint16_t* out = a.dmax + ((int64_t)p * nreg + region) * a.rowsA * a.rowsB;
+    for (int t = tid; t < TA * TB; t += NTHR) {
+        const int r = t / TB, cc = t % TB;
+        const int64_t gi = row0 + r, gj = col0 + cc;
+        if (gi < a.rowsA && gj < a.rowsB) out[gi * a.rowsB + gj] = tile[t];
+    }
+}
 
-    // ------------------------------------------------------------- epilogue (rolled over pairs)
+template <bool SYM>
+__global__ void __launch_bounds__(256) k_max16_bin(Max16Args a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int nq = a.bp.nq, M = a.bp.M;
+    double* thr_s = reinterpret_cast<double*>(smem_raw);              // [nq*M]
+    uint32_t* hist_s = reinterpret_cast<uint32_t*>(thr_s + ((nq * M + 1) & ~1));
+
+    const int p = blockIdx.z;
+    if (a.status[p] & CIL_ITEM_BADRADII) return;
+    const int64_t row0 = (int64_t)blockIdx.y * TA;
+    const int64_t col0 = (int64_t)blockIdx.x * TB;
+    if (a.tri && row0 / a.sp.row_seg >= (min(col0 + TB, a.rowsB) - 1) / a.sp.col_seg) return;
+    if (SYM && row0 >= col0 + TB) return;
+    const int tid = threadIdx.x;
+    for (int t = tid; t < nq * M; t += 256) thr_s[t] = a.thr[(int64_t)p * a.thr_stride + t];
+    const int64_t rlast = min(row0 + TA, a.rowsA) - 1, clast = min(col0 + TB, a.rowsB) - 1;
+    const int64_t rs0 = row0 / a.sp.row_seg, cs0 = col0 / a.sp.col_seg;
+    const int nrs = (int)(rlast / a.sp.row_seg - rs0 + 1), ncs = (int)(clast / a.sp.col_seg - cs0 + 1);
+    const int hist_len = nrs * ncs * nq * (M + 1);
+    const bool use_sh = hist_len <= a.hist_cap;
+    if (use_sh)
+        for (int t = tid; t < hist_len; t += 256) hist_s[t] = 0u;
+    __syncthreads();
+
     const double h = a.bp.h, ih = 1.0 / h;
     const int nreg = a.g.nreg;
     const double s0 = scale16(a.maxbits, p, 0);
@@ -321,15 +336,15 @@ __global__ void __launch_bounds__(NTHR, CIL_M16_EXP == 1 ? 4 : 3) k_max16(Max16A
     const double sy = nreg > 2 ? scale16(a.maxbits, p, 2) * ih : 0.0;
     // per-region error: 2 (0.5 + 1e-11) s of the quantisation, FP64 products (1e-15 relative)
     const double E0 = (1.0 + 1e-9) * s0, Ex = (1.0 + 1e-9) * sx, Ey = (1.0 + 1e-9) * sy;
-#pragma unroll 1
-    for (int pi = 0; pi < NP; ++pi) {
-        const int i = pi >> 2, j = pi & 3;
-        const int64_t gi = row0 + ty + 8 * i;
-        const int64_t gj = col0 + tx + 16 * j;
+    const int64_t plane = a.rowsA * a.rowsB;
+    const uint16_t* dm = a.dmax + (int64_t)p * nreg * plane;
+    for (int t = tid; t < TA * TB; t += 256) {
+        const int64_t gi = row0 + t / TB, gj = col0 + t % TB;
         if (gi >= a.rowsA || gj >= a.rowsB) continue;
-        const double m0 = s0 * (double)rslot(0)[pi * NTHR + tid];
-        const double mxx = nreg > 1 ? sx * (double)rslot(1)[pi * NTHR + tid] : 0.0;
-        const double myy = nreg > 2 ? sy * (double)rslot(2)[pi * NTHR + tid] : 0.0;
+        const int64_t o = gi * a.rowsB + gj;
+        const double m0 = s0 * (double)dm[o];
+        const double mxx = nreg > 1 ? sx * (double)dm[plane + o] : 0.0;
+        const double myy = nreg > 2 ? sy * (double)dm[2 * plane + o] : 0.0;
         const int64_t rsg = gi / a.sp.row_seg, csg = gj / a.sp.col_seg;
         for (int q = 0; q < nq; ++q) {
             if (!((a.qmask >> q) & 1u)) continue;
@@ -368,7 +383,7 @@ __global__ void __launch_bounds__(NTHR, CIL_M16_EXP == 1 ? 4 : 3) k_max16(Max16A
     }
     if (use_sh) {
         __syncthreads();
-        for (int t = tid; t < hist_len; t += NTHR) {
+        for (int t = tid; t < hist_len; t += 256) {
             const uint32_t v = hist_s[t];
             if (v == 0u) continue;
             const int b = t % (M + 1);
@@ -380,9 +395,9 @@ __global__ void __launch_bounds__(NTHR, CIL_M16_EXP == 1 ? 4 : 3) k_max16(Max16A
     }
 }
 
-static size_t max16_smem(int hist_cap, int nqM) {
-    return sizeof(uint32_t) * 2 * (TA + TB) * LDW + sizeof(double) * ((nqM + 1) & ~1) +
-           sizeof(uint16_t) * 2 * NP * NTHR + sizeof(uint32_t) * hist_cap;
+static size_t max16_smem_reg() { return sizeof(uint32_t) * 2 * (TA + TB) * LDW; }
+static size_t max16_smem_bin(int hist_cap, int nqM) {
+    return sizeof(double) * ((nqM + 1) & ~1) + sizeof(uint32_t) * hist_cap;
 }
 
 cudaError_t launch_pack16(int P, const RowSrc& asrc, int64_t rowsA, const RowSrc& bsrc, int64_t rowsB,
@@ -407,11 +422,12 @@ static cudaError_t launch_max16_t(const Max16Args& a_in, cudaStream_t st) {
     const int64_t need = nrs * ncs * a.bp.nq * (a.bp.M + 1);
     a.hist_cap = (int)(need < 4096 ? need : 4096);
     static SmemAttrOnce attr;
-    if (cudaError_t e = attr.ensure(k_max16<SYM>, (int)max16_smem(4096, kMaxMeas * kMaxM)); e != cudaSuccess) return e;
-    dim3 grid((unsigned)((a.rowsB + TB - 1) / TB), (unsigned)((a.rowsA + TA - 1) / TA), (unsigned)a.P);
+    if (cudaError_t e = attr.ensure(k_max16_reg<SYM>, (int)max16_smem_reg()); e != cudaSuccess) return e;
+    const unsigned gx = (unsigned)((a.rowsB + TB - 1) / TB), gy = (unsigned)((a.rowsA + TA - 1) / TA);
     ProfScope ps_(K_SIMT, st);
-    k_max16<SYM><<<grid, NTHR, max16_smem(a.hist_cap, a.bp.nq * a.bp.M), st>>>(a);
-    note_launch();
+    k_max16_reg<SYM><<<dim3(gx, gy, (unsigned)(a.P * a.g.nreg)), NTHR, max16_smem_reg(), st>>>(a);
+    k_max16_bin<SYM><<<dim3(gx, gy, (unsigned)a.P), 256, max16_smem_bin(a.hist_cap, a.bp.nq * a.bp.M), st>>>(a);
+    note_launch(2);
     return cudaGetLastError();
 }
 
