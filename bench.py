@@ -711,16 +711,26 @@ def bench_c3(args, dev):
     simt_ms = prof["simt_tile"][0] / max(1, prof["simt_tile"][1])
     ep = float(N) * N * Kaug                                  # element-pairs per family per launch
     tc_family = args.engine in ("AUTO", "TC_I8")
-    mix = 1 if tc_family else 0                               # max family only / both families
+    # AUTO / TC_I8: the max family alone on the 15-bit fixed-point engine (max16.cu: IMAD +
+    # VIMNMX3.U16x2); SIMT: both families on the FP32 engine (FADD2 + FMNMX3 + FFMA2)
+    mix = 3 if tc_family else 0
     ceil, _ = _capi.alu_ceiling(mix)
+    nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+    # pipe ceiling of the fixed-point mix: VIMNMX3.U16x2 issues at 16 lanes / SMSP / cycle on the
+    # integer pipe and covers 2 element-pairs per lane -> 128 element-pairs per SM-cycle (the IMADs
+    # go to the FMA pipe at the same rate), at the maximum SM clock
+    pipe_ceil = 128.0 * nsm * 1965e6 if tc_family else None
     res = {"workload": "C3: 2000 x 2000 of 128x128x2, all six measures, M=20",
            "engine": args.engine,
            "ms_per_step": round(ms, 3), "pairs_per_s": N * N / (ms * 1e-3),
            "simt_tile": {"families": "max (Linf, W1inf, W1infsum)" if tc_family else "max + L2-type",
                          "ms_per_launch": round(simt_ms, 3), "element_pairs_per_s": ep / (simt_ms * 1e-3),
                          "alu_ceiling_element_pairs_per_s": ceil,
-                         "ceiling_mix": "FADD2+FMNMX3" if mix == 1 else "FADD2+FMNMX3+FFMA2",
-                         "frac": round(ep / (simt_ms * 1e-3) / ceil, 4), "K_aug": Kaug},
+                         "ceiling_mix": "IMAD+VIMNMX3.U16x2 (measured, register-only)" if mix == 3
+                         else "FADD2+FMNMX3+FFMA2 (measured, register-only)",
+                         "frac": round(ep / (simt_ms * 1e-3) / ceil, 4), "K_aug": Kaug,
+                         "pipe_ceiling_element_pairs_per_s": pipe_ceil,
+                         "frac_of_pipe_ceiling": round(ep / (simt_ms * 1e-3) / pipe_ceil, 4) if pipe_ceil else None},
            "kernel_breakdown": {k: round(v[0] / steps, 3) for k, v in prof.items() if v[1] > 0},
            "clocks": clk.summary()}
     g_ms, g_n = prof["gram_tc"]

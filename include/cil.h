@@ -343,10 +343,11 @@ CIL_API cil_status cil_diag_gram_family(const float* A, int64_t lda, int64_t N, 
                                         int64_t Nt, cil_grid g, float* vE, void* ws, size_t ws_bytes, void* stream);
 
 /* ------------------------------------------------------------------------ */
-/* cil_diag_alu_ceiling — DIAGNOSTIC: measured issue ceiling of the CUDA-core engine's
- * inner-loop instruction mix (mix 0: FADD2+FMNMX3+FFMA2, 1: FADD2+FMNMX3, 2: FADD2+FFMA2)
- * in element-pairs per second on the current device (register-only kernel on the legacy
- * stream, synchronous).  Returns 0, or -1 on a CUDA error. */
+/* cil_diag_alu_ceiling — DIAGNOSTIC: measured issue ceiling of the CUDA-core engines'
+ * inner-loop instruction mix (mix 0: FADD2+FMNMX3+FFMA2, 1: FADD2+FMNMX3, 2: FADD2+FFMA2 — the FP32
+ * engine; 3: IMAD + VIMNMX3.U16x2 max/min — the fixed-point max-family engine) in element-pairs per
+ * second on the current device (register-only kernel on the legacy stream, synchronous).  Returns
+ * 0, or -1 on a CUDA error. */
 CIL_API int32_t cil_diag_alu_ceiling(int32_t mix, int32_t iters, double* element_pairs_per_s, double* ms);
 
 /* cil_diag_sqrt_approx_error — DIAGNOSTIC: exhaustive check of the hardware square-root
@@ -369,7 +370,7 @@ CIL_API void cil_diag_limit_recheck_list(int64_t limit);
 
 /* cil_diag_recheck_sort_min — DIAGNOSTIC: on the calling host thread, re-check lists of at least `n`
  * entries take the row-bucketed pass (list counting-sorted by pattern row, each pair evaluated once;
- * recheck.cu), shorter ones the entry-by-entry pass.  Default 2048; n <= 0 restores it, n = 1 forces
+ * recheck.cu), shorter ones the entry-by-entry pass.  Default 8192; n <= 0 restores it, n = 1 forces
  * the bucketed pass for every non-empty list (tests).  Results are identical either way. */
 CIL_API void cil_diag_recheck_sort_min(int64_t n);
 

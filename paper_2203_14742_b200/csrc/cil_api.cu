@@ -18,7 +18,7 @@ static thread_local int32_t t_last_cuda = 0;
 // thread so tests can exercise the exact all-pairs fallback; < 0 = no limit
 static thread_local int64_t t_list_limit = -1;
 // diagnostics (cil_diag_recheck_sort_min): list length from which the re-check is row-bucketed
-static thread_local uint32_t t_sort_min = 2048;
+static thread_local uint32_t t_sort_min = 8192;   // below: the sort costs more than it saves (C2: 3.3k cases)
 static thread_local int32_t t_launches = 0;
 void note_launch(int n) { t_launches += n; }
 
@@ -1141,7 +1141,7 @@ int32_t cil_prof_read(double* ms, int64_t* launches) {
 }
 
 void cil_diag_limit_recheck_list(int64_t limit) { t_list_limit = limit; }
-void cil_diag_recheck_sort_min(int64_t n) { t_sort_min = n <= 0 ? 2048u : (uint32_t)(n > 0xffffffffll ? 0xffffffffll : n); }
+void cil_diag_recheck_sort_min(int64_t n) { t_sort_min = n <= 0 ? 8192u : (uint32_t)(n > 0xffffffffll ? 0xffffffffll : n); }
 
 int64_t cil_diag_bounds_violations(void) {
 #ifdef CIL_BOUNDS_CHECK

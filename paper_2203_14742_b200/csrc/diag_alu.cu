@@ -4,7 +4,9 @@
 //   mix 0: FADD2 + FMNMX3(|.|) + FFMA2 per two element-pairs (max and L2 families together)
 //   mix 1: FADD2 + FMNMX3(|.|)                (max family only)
 //   mix 2: FADD2 + FFMA2                       (L2 family only)
-// Same register micro-tile as k_simt (4 x 4 pairs per thread, float4 operands), no memory.
+//   mix 3: IMAD (biased packed 16-bit add) + VIMNMX3.U16x2 max / min   (max16.cu, the max family)
+// Same register micro-tiles as k_simt (4 x 4 pairs per thread, float4 operands) and k_max16_reg
+// (8 x 4 pairs, uint4 operands), no memory.
 #include <string.h>
 
 #include "cil_internal.cuh"
@@ -58,6 +60,51 @@ __global__ void __launch_bounds__(128) k_alu_mix(float* out, int iters, float se
 #pragma unroll
         for (int j = 0; j < 4; ++j) s += acc[i][j].x + acc[i][j].y + mx[i][j];
     if (s == 12345.678f) out[threadIdx.x] = s;   // keep the work observable
+}
+
+// max16.cu's inner loop: per pair and uint4 step (8 element-pairs) 4 IMAD + 2 VIMNMX3 max + 2 min
+__global__ void __launch_bounds__(128) k_alu_mix16(float* out, int iters, uint32_t seed, uint32_t one) {
+    uint4 av[8], bv[4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+        av[i] = make_uint4((seed * (i + 1)) & 0x3fff3fffu, (seed * (i + 3)) & 0x3fff3fffu,
+                           (seed * (i + 5)) & 0x3fff3fffu, (seed * (i + 7)) & 0x3fff3fffu);
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+        bv[j] = make_uint4((seed * (j + 9) + 1) & 0x3fff3fffu, (seed * (j + 11) + 3) & 0x3fff3fffu,
+                           (seed * (j + 13) + 5) & 0x3fff3fffu, (seed * (j + 15) + 7) & 0x3fff3fffu);
+    uint32_t mx[8][4], mn[8][4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) { mx[i][j] = 0u; mn[i][j] = 0xffffffffu; }
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                uint32_t d0, d1, d2, d3;
+                asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d0) : "r"(av[i].x), "r"(one), "r"(bv[j].x));
+                asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d1) : "r"(av[i].y), "r"(one), "r"(bv[j].y));
+                asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d2) : "r"(av[i].z), "r"(one), "r"(bv[j].z));
+                asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d3) : "r"(av[i].w), "r"(one), "r"(bv[j].w));
+                mx[i][j] = __vimax3_u16x2(mx[i][j], d0, d1);
+                mn[i][j] = __vimin3_u16x2(mn[i][j], d0, d1);
+                mx[i][j] = __vimax3_u16x2(mx[i][j], d2, d3);
+                mn[i][j] = __vimin3_u16x2(mn[i][j], d2, d3);
+            }
+        // perturb B (4 x 4 XOR per 256 element-pairs: ~3 % of the mix)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            bv[j].x ^= 0x00010001u; bv[j].y ^= 0x00020002u; bv[j].z ^= 0x00010001u; bv[j].w ^= 0x00020002u;
+        }
+    }
+    uint32_t sacc = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) sacc += mx[i][j] ^ mn[i][j];
+    if (sacc == 0x12345678u) out[threadIdx.x] = (float)sacc;
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -116,7 +163,8 @@ extern "C" CIL_API int32_t cil_diag_alu_ceiling(int32_t mix, int32_t iters, doub
     cudaEventCreate(&a);
     cudaEventCreate(&b);
     auto launch = [&](int n) {
-        if (mix == 1) k_alu_mix<1><<<blocks, threads>>>(out, n, 0.5f);
+        if (mix == 3) k_alu_mix16<<<nsm * 3, threads>>>(out, n, 12345u, 1u);   // k_max16_reg's occupancy
+        else if (mix == 1) k_alu_mix<1><<<blocks, threads>>>(out, n, 0.5f);
         else if (mix == 2) k_alu_mix<2><<<blocks, threads>>>(out, n, 0.5f);
         else k_alu_mix<0><<<blocks, threads>>>(out, n, 0.5f);
     };
@@ -130,8 +178,9 @@ extern "C" CIL_API int32_t cil_diag_alu_ceiling(int32_t mix, int32_t iters, doub
     cudaEventDestroy(a);
     cudaEventDestroy(b);
     if (cudaGetLastError() != cudaSuccess) return -1;
-    // element-pairs per iteration per thread: 16 pairs x 4 elements
-    const double ep = (double)blocks * threads * (double)iters * 16.0 * 4.0;
+    // element-pairs per iteration per thread: 16 pairs x 4 elements (mix 3: 32 pairs x 8 elements)
+    const double ep = mix == 3 ? (double)nsm * 3 * threads * (double)iters * 32.0 * 8.0
+                               : (double)blocks * threads * (double)iters * 16.0 * 4.0;
     *element_pairs_per_s = ep / (t * 1e-3);
     *ms = t;
     return 0;

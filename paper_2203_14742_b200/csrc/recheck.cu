@@ -8,7 +8,7 @@
 // The pair is moved from the provisional bin the engine counted it in to b (hist[b_lo] -= 1,
 // hist[b] += 1) or, in bin-matrix mode, b is written to the pair's entry (both orders when mirrored).
 //
-// Row-bucketed pass (lists of >= sort_min entries, 2048 unless a diagnostic changes it; VERDICT r1
+// Row-bucketed pass (lists of >= sort_min entries, 8192 unless a diagnostic changes it; VERDICT r1
 // "restructure k_recheck around row reuse"): the list is counting-sorted by (p, i) (k_rk_count,
 // k_rk_scan, k_rk_scatter) and walked entry-parallel, so the CTAs working at one time share a few A
 // rows (one HBM read each, L2 hits for the rest) while the partners stream, and every pair is
