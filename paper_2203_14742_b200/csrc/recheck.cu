@@ -33,13 +33,75 @@ namespace cil {
 
 namespace {
 
-// The six FP64 sub-norms of u = x - y over one pattern, one CTA of 256 threads (warp per grid row).
-// full = false: only s0 (a flat K-long loop with 4 float4 pairs in flight per thread).
+// The six FP64 sub-norms of u = x - y over one pattern, one CTA of 256 threads.
+// full = false: only s0 (a flat K-long loop with 4 float4 pairs in flight per thread); full with
+// W % 4 == 0 and a 32 KB staging buffer: a flat float4 sweep over chunks of 4096 elements of x and y
+// staged in shared memory (the x / y neighbours from there); otherwise a warp per grid row.
 __device__ void exact_subnorms(const float* x, const float* y, const RecheckArgs& a, bool full, double out[6],
-                               double (*red)[8]) {
+                               double (*red)[8], float* stage = nullptr) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     double v[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-    if (!full) {
+    if (full && stage != nullptr && (a.W & 3) == 0 && a.K < (1ll << 31)) {
+        constexpr uint32_t CH = 4096;
+        const uint32_t K = (uint32_t)a.K, W = (uint32_t)a.W, H = (uint32_t)a.H;
+        float* sx = stage;
+        float* sy = stage + CH;
+        for (uint32_t base = 0; base < K; base += CH) {
+            float4 xa[4], yb[4];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                const uint32_t e = base + t * 1024 + threadIdx.x * 4;
+                if (e < K) {
+                    xa[t] = __ldg(reinterpret_cast<const float4*>(x + e));
+                    yb[t] = __ldg(reinterpret_cast<const float4*>(y + e));
+                } else {
+                    xa[t] = yb[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+            }
+            __syncthreads();                                   // previous chunk's reads are done
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                reinterpret_cast<float4*>(sx)[t * 256 + threadIdx.x] = xa[t];
+                reinterpret_cast<float4*>(sy)[t * 256 + threadIdx.x] = yb[t];
+            }
+            __syncthreads();
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                const uint32_t l = t * 1024 + threadIdx.x * 4, e = base + l;
+                if (e >= K) continue;
+                const double u0 = (double)xa[t].x - (double)yb[t].x, u1 = (double)xa[t].y - (double)yb[t].y;
+                const double u2 = (double)xa[t].z - (double)yb[t].z, u3 = (double)xa[t].w - (double)yb[t].w;
+                v[0] += u0 * u0 + u1 * u1 + u2 * u2 + u3 * u3;
+                v[3] = fmax(v[3], fmax(fmax(fabs(u0), fabs(u1)), fmax(fabs(u2), fabs(u3))));
+                const uint32_t sr = e / W, c = e - sr * W, sp = sr / H, hr = sr - sp * H;
+                if (!(a.gs == 0 || ((a.gs >> sp) & 1u))) continue;
+                const double d0 = u1 - u0, d1 = u2 - u1, d2 = u3 - u2;
+                v[1] += d0 * d0 + d1 * d1 + d2 * d2;
+                v[4] = fmax(v[4], fmax(fmax(fabs(d0), fabs(d1)), fabs(d2)));
+                if (c + 4 < W) {
+                    const double un = l + 4 < CH ? (double)sx[l + 4] - (double)sy[l + 4]
+                                                 : (double)__ldg(x + e + 4) - (double)__ldg(y + e + 4);
+                    const double d3 = un - u3;
+                    v[1] += d3 * d3;
+                    v[4] = fmax(v[4], fabs(d3));
+                }
+                if (hr + 1 < H) {
+                    float4 xd, yd;
+                    if (l + W < CH) {
+                        xd = *reinterpret_cast<const float4*>(sx + l + W);
+                        yd = *reinterpret_cast<const float4*>(sy + l + W);
+                    } else {
+                        xd = __ldg(reinterpret_cast<const float4*>(x + e + W));
+                        yd = __ldg(reinterpret_cast<const float4*>(y + e + W));
+                    }
+                    const double e0 = ((double)xd.x - (double)yd.x) - u0, e1 = ((double)xd.y - (double)yd.y) - u1;
+                    const double e2 = ((double)xd.z - (double)yd.z) - u2, e3 = ((double)xd.w - (double)yd.w) - u3;
+                    v[2] += e0 * e0 + e1 * e1 + e2 * e2 + e3 * e3;
+                    v[5] = fmax(v[5], fmax(fmax(fabs(e0), fabs(e1)), fmax(fabs(e2), fabs(e3))));
+                }
+            }
+        }
+    } else if (!full) {
         int64_t k = (int64_t)threadIdx.x * 4;
         for (; k + 3 * 1024 < a.K; k += 4 * 1024) {
             float4 u[4], z[4];
@@ -322,6 +384,7 @@ __global__ void __launch_bounds__(256, CIL_RK_EXP == 1 ? 3 : CIL_RK_EXP == 3 ? 2
     const bool overflow = c > a.cap;
     __shared__ double red[6][8];
     __shared__ double sub[6];
+    __shared__ __align__(16) float stage[8192];           // the FP32 / FP64 sweeps' chunk staging
     if (overflow) {
         if (blockIdx.x == 0 && threadIdx.x == 0)
             for (int p = 0; p < a.P; ++p) atomicOr(&a.status[p], CIL_ITEM_OVERFLOW);
@@ -331,7 +394,7 @@ __global__ void __launch_bounds__(256, CIL_RK_EXP == 1 ? 3 : CIL_RK_EXP == 3 ? 2
             const int64_t p = e / per, i = (e % per) / a.rowsB, j = e % a.rowsB;
             if (a.mirror && j < i) continue;
             if (a.status[p] & CIL_ITEM_BADRADII) continue;
-            exact_subnorms(row_ptr(a.asrc, p, i), row_ptr(a.bsrc, p, j), a, a.kinds & ~1u, sub, red);
+            exact_subnorms(row_ptr(a.asrc, p, i), row_ptr(a.bsrc, p, j), a, a.kinds & ~1u, sub, red, stage);
             if (threadIdx.x == 0)
                 for (int k = 0; k < 6; ++k)
                     if ((a.kinds >> k) & 1u) settle(a, p, i, j, k, 0, measure(k, sub, a.w, a.h), true);
@@ -345,7 +408,7 @@ __global__ void __launch_bounds__(256, CIL_RK_EXP == 1 ? 3 : CIL_RK_EXP == 3 ? 2
             const int64_t p = ent.x, i = ent.y, j = ent.z;
             const int b_lo = (int)(ent.w & 255u);
             const int kind = (int)((ent.w >> 8) & 255u);
-            exact_subnorms(row_ptr(a.asrc, p, i), row_ptr(a.bsrc, p, j), a, kind != 0, sub, red);
+            exact_subnorms(row_ptr(a.asrc, p, i), row_ptr(a.bsrc, p, j), a, kind != 0, sub, red, stage);
             if (threadIdx.x == 0) settle(a, p, i, j, kind, b_lo, measure(kind, sub, a.w, a.h), false);
             __syncthreads();
         }
@@ -359,7 +422,6 @@ __global__ void __launch_bounds__(256, CIL_RK_EXP == 1 ? 3 : CIL_RK_EXP == 3 ? 2
     __shared__ double s_d[8], s_E[8];
     __shared__ float red32[3][8];
     __shared__ float m32[3];
-    __shared__ __align__(16) float us[4096];
     for (uint32_t e = blockIdx.x; e < c; e += gridDim.x) {
         const uint4 ent = a.rk_list[e];
         const int64_t p = ent.x, i = ent.y, j = ent.z;
@@ -385,7 +447,7 @@ __global__ void __launch_bounds__(256, CIL_RK_EXP == 1 ? 3 : CIL_RK_EXP == 3 ? 2
         const float* yb = row_ptr(a.bsrc, p, j);
         bool exact = true;
         if (!(kmask & 0x0Du)) {                              // max family only: FP32 interval first
-            max_subnorms32(xa, yb, a, m32, red32, a.K < (1ll << 31) ? us : nullptr);
+            max_subnorms32(xa, yb, a, m32, red32, a.K < (1ll << 31) ? stage : nullptr);
             if ((int)threadIdx.x < n) measure32((int)((s_w[threadIdx.x] >> 8) & 255u), m32, a.h, &s_d[threadIdx.x], &s_E[threadIdx.x]);
             __syncthreads();
             exact = false;
@@ -402,7 +464,7 @@ __global__ void __launch_bounds__(256, CIL_RK_EXP == 1 ? 3 : CIL_RK_EXP == 3 ? 2
             __syncthreads();
         }
         if (!exact) continue;
-        exact_subnorms(xa, yb, a, (kmask & ~1u) != 0u, sub, red);
+        exact_subnorms(xa, yb, a, (kmask & ~1u) != 0u, sub, red, stage);
         if ((int)threadIdx.x < n) s_d[threadIdx.x] = measure((int)((s_w[threadIdx.x] >> 8) & 255u), sub, a.w, a.h);
         __syncthreads();
         for (int k = 0; k < n; ++k) {
