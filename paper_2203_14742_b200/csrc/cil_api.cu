@@ -195,6 +195,7 @@ struct Layout {
     int nph = 1;
     AugGeom geom{};
     AugGeom geom16{};               // max16.cu operands (regions padded to kMax16BK)
+    int64_t dmax_rows_product = 0;  // P * rowsA * rowsB of the per-pair region maxima
 };
 
 size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -256,6 +257,7 @@ Layout make_layout(int P, int64_t rowsA, int64_t rowsB, const cil_grid& g, int n
         L.off_aug16 = take(sizeof(int16_t) * (size_t)rows * L.geom16.off[3]);
         L.off_max16 = take(sizeof(unsigned) * 8 * (size_t)P);
         L.off_dmax16 = take(sizeof(uint16_t) * 3 * (size_t)P * rowsA * rowsB);
+        L.dmax_rows_product = (int64_t)P * rowsA * rowsB;
     }
     if (nY > 0) {
         L.off_Y = take(sizeof(double) * (size_t)nY);
@@ -390,6 +392,7 @@ cil_status run_engines(int P, const RowSrc& asrc, const RowSrc& bsrc, int64_t ro
         a.g = g16;
         a.maxbits = maxbits;
         a.dmax = at<uint16_t>(ws, L.off_dmax16);
+        a.dmax_elems = 3 * (int64_t)L.dmax_rows_product;
         a.bp = bp;
         a.sp = sp;
         a.thr = thr; a.thr_stride = (int64_t)sl.nq * M;

@@ -234,6 +234,7 @@ struct Max16Args {
     uint4* list; uint32_t* ctr; uint32_t cap;
     uint32_t one;                             // 1 (set by the launcher; keeps the adds on the FMA pipe)
     uint16_t* dmax;                           // [P][nreg][rowsA][rowsB] per-pair region maxima (workspace)
+    int64_t dmax_elems;                       // its capacity (bounds-checked builds)
 };
 cudaError_t launch_pack16(int P, const RowSrc& asrc, int64_t rowsA, const RowSrc& bsrc, int64_t rowsB,
                           const AugGeom& g, unsigned* maxbits, int16_t* outA, int16_t* outB, int32_t* status,

@@ -301,7 +301,10 @@ __global__ void __launch_bounds__(NTHR, CIL_M16_EXP == 1 ? 4 : 3) k_max16_reg(Ma
     for (int t = tid; t < TA * TB; t += NTHR) {
         const int r = t / TB, cc = t % TB;
         const int64_t gi = row0 + r, gj = col0 + cc;
-        if (gi < a.rowsA && gj < a.rowsB) out[gi * a.rowsB + gj] = tile[t];
+        if (gi < a.rowsA && gj < a.rowsB) {
+            CIL_CHECK(((int64_t)p * nreg + region + 1) * a.rowsA * a.rowsB <= a.dmax_elems);
+            out[gi * a.rowsB + gj] = tile[t];
+        }
     }
 }
 

@@ -44,6 +44,15 @@ def main():
     c, y, st = cil.features(A, B, g3, cil.ALL, R)
     torch.cuda.synchronize()
     print("C3-small", int(st[0]), c[0, :, 10].tolist())
+    from paper_2203_14742_b200 import _capi as _c
+    _c.lib.cil_diag_recheck_sort_min(1)                   # the row-bucketed re-check on every list
+    try:
+        c2, y2, st2 = cil.features(A, B, g3, cil.ALL, R)
+        bb, stb = cil.bin_matrix(A[:100], A[:100], g3, cil.ALL, R)
+        torch.cuda.synchronize()
+    finally:
+        _c.lib.cil_diag_recheck_sort_min(0)
+    print("C3-small bucketed", int(st2[0]), int(stb[0]), bool(torch.equal(c2, c)))
     # bin matrix (bootstrap) of the same sets, all measures
     bins, st = cil.bin_matrix(A[:100], B[:90], g3, cil.ALL, R)
     torch.cuda.synchronize()
