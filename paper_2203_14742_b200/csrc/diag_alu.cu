@@ -63,7 +63,7 @@ __global__ void __launch_bounds__(128) k_alu_mix(float* out, int iters, float se
 }
 
 // max16.cu's inner loop: per pair and uint4 step (8 element-pairs) 4 IMAD + 2 VIMNMX3 max + 2 min
-__global__ void __launch_bounds__(128) k_alu_mix16(float* out, int iters, uint32_t seed, uint32_t one) {
+__global__ void __launch_bounds__(128, 3) k_alu_mix16(float* out, int iters, uint32_t seed, uint32_t one) {
     uint4 av[8], bv[4];
 #pragma unroll
     for (int i = 0; i < 8; ++i)
@@ -78,6 +78,7 @@ __global__ void __launch_bounds__(128) k_alu_mix16(float* out, int iters, uint32
     for (int i = 0; i < 8; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) { mx[i][j] = 0u; mn[i][j] = 0xffffffffu; }
+#pragma unroll 1
     for (int it = 0; it < iters; ++it) {
 #pragma unroll
         for (int i = 0; i < 8; ++i)
