@@ -418,6 +418,7 @@ __global__ void __launch_bounds__(256, CIL_RK_EXP == 1 ? 3 : CIL_RK_EXP == 3 ? 2
     // their A row, so concurrent CTAs read it together: one HBM read, L2 hits for the rest); the
     // first entry of a pair (i, j) in its row bucket owns the pair and settles all its measures
     // (bins counted by the whole CTA over the radii, no serial loops over global memory)
+    constexpr uint32_t kBucketScan = 1024;               // buckets up to this size pair their entries
     __shared__ uint32_t s_n, s_w[8];
     __shared__ double s_d[8], s_E[8];
     __shared__ float red32[3][8];
@@ -430,14 +431,19 @@ __global__ void __launch_bounds__(256, CIL_RK_EXP == 1 ? 3 : CIL_RK_EXP == 3 ? 2
         if (threadIdx.x == 0) s_n = 0u;
         __syncthreads();
         bool dup = false;
-        for (uint32_t u = beg + threadIdx.x; u < end; u += blockDim.x) {
-            const uint4 o = a.rk_list[u];
-            if (o.z != ent.z) continue;
-            if (u < e) dup = true;
-            else {
-                const uint32_t k = atomicAdd(&s_n, 1u);
-                if (k < 8) s_w[k] = o.w;
+        if (end - beg <= kBucketScan) {
+            for (uint32_t u = beg + threadIdx.x; u < end; u += blockDim.x) {
+                const uint4 o = a.rk_list[u];
+                if (o.z != ent.z) continue;
+                if (u < e) dup = true;
+                else {
+                    const uint32_t k = atomicAdd(&s_n, 1u);
+                    if (k < 8) s_w[k] = o.w;
+                }
             }
+        } else if (threadIdx.x == 0) {                       // a huge bucket: no pairing (each entry
+            s_n = 1u;                                        // settles itself; bounded work, not
+            s_w[0] = ent.w;                                  // quadratic in the bucket size)
         }
         if (__syncthreads_or(dup)) continue;
         const int n = (int)min(s_n, 8u);                  // a pair is listed at most once per measure

@@ -168,3 +168,29 @@ def test_recheck_row_bucketed(cil, oracle_mod, engine, mode):
             hi = (D[q][..., None] < radii[q] * (1 + BAND)).sum(-1)
             g = out[1][q].astype(np.int64)
             assert ((g >= lo) & (g <= hi)).all(), (engine, q)
+
+
+def test_recheck_huge_bucket(cil, oracle_mod):
+    """One A row whose every partner sits at the same distance, with radii just above and below it
+    (outside the oracle's 1e-6 band, inside the fixed-point engine's): > 1024 listed cases in one
+    row bucket, so the row-bucketed re-check settles each entry by itself (no quadratic pairing);
+    entry-by-entry and bucketed passes must give the oracle's counts."""
+    from paper_2203_14742_b200 import _capi
+    O = oracle_mod
+    grid = (1, 16, 16, 0.0)
+    rng = np.random.default_rng(11)
+    a0 = (rng.integers(0, 1024, size=(1, 1, 16, 16)) / 1024.0).astype(np.float32)
+    a1 = (rng.integers(0, 1024, size=(1, 1, 16, 16)) / 1024.0).astype(np.float32)
+    A = torch.from_numpy(np.concatenate([a0, a1]))
+    B = torch.from_numpy(np.repeat(a0 + np.float32(0.5), 1500, axis=0))      # exact: d(0, j) = 0.5 for all j
+    radii = np.tile(np.array([0.5 * (1 + 1e-5), 0.5 * (1 - 1e-5), 0.01]), (3, 1))
+    ref = O.features(A.numpy(), B.numpy(), grid, MAXF, radii, band=BAND)
+    for sort_min in (0, 1):
+        _capi.lib.cil_diag_recheck_sort_min(sort_min)
+        try:
+            c, st = _features(cil, A, B, grid, MAXF, radii)
+            listed, _ = cil.recheck_count(1, 2, 1500, grid, MAXF, 3)
+        finally:
+            _capi.lib.cil_diag_recheck_sort_min(0)
+        assert st == 0 and listed >= 3 * 1500, listed            # every (0, j) case of every measure
+        _check(c, ref, f"sort_min {sort_min}")
