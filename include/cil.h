@@ -374,6 +374,14 @@ CIL_API void cil_diag_limit_recheck_list(int64_t limit);
  * the bucketed pass for every non-empty list (tests).  Results are identical either way. */
 CIL_API void cil_diag_recheck_sort_min(int64_t n);
 
+/* cil_diag_concurrent_engines — DIAGNOSTIC: on the calling host thread, when a call has both the
+ * tensor-core family and the max family (AUTO / TC_I8 with Linf, W1inf or W1infsum), run the max
+ * family's integer-pipe engine on a library-owned side stream concurrently with the tensor-core
+ * engine (on = 1, default; the side stream is forked from and joined back into the caller's stream
+ * with events, so the call stays asynchronous and graph-capturable) or serially on the caller's
+ * stream (on = 0).  Results are identical either way. */
+CIL_API void cil_diag_concurrent_engines(int32_t on);
+
 /* ------------------------------------------------------------------------ */
 /* Kernel timing (diagnostics, used by bench.py for the live roofline).  While enabled on
  * the calling host thread, every kernel the library launches is bracketed by CUDA events

@@ -6,6 +6,8 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <mutex>
+
 #include "cil_internal.cuh"
 
 #include <nvtx3/nvToolsExt.h>
@@ -21,6 +23,50 @@ static thread_local int64_t t_list_limit = -1;
 static thread_local uint32_t t_sort_min = 8192;   // below: the sort costs more than it saves (C2: 3.3k cases)
 static thread_local int32_t t_launches = 0;
 void note_launch(int n) { t_launches += n; }
+// diagnostics (cil_diag_concurrent_engines): run the max family's engine on a side stream, concurrently
+// with the tensor-core family (default on)
+static thread_local bool t_concurrent = true;
+
+// One library-owned side stream per device (non-blocking), for the concurrent engines.
+static cudaStream_t side_stream() {
+    static std::mutex mu;
+    static cudaStream_t s[64] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+    std::lock_guard<std::mutex> g(mu);
+    if (!s[dev] && cudaStreamCreateWithFlags(&s[dev], cudaStreamNonBlocking) != cudaSuccess) s[dev] = nullptr;
+    return s[dev];
+}
+
+// Fork / join of the side stream around the engines (event-ordered, so it is CUDA-graph capturable:
+// the side stream joins the capture through the fork event and leaves it through the join).
+struct Fork {
+    cudaStream_t main, aux = nullptr;
+    bool joined = true;
+    Fork(cudaStream_t m, bool on) : main(m) {
+        if (!on || (aux = side_stream()) == nullptr) return;
+        cudaEvent_t e;
+        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) { aux = nullptr; return; }
+        cudaEventRecord(e, main);
+        cudaStreamWaitEvent(aux, e, 0);
+        cudaEventDestroy(e);
+        joined = false;
+    }
+    cudaStream_t side() const { return aux ? aux : main; }
+    void join() {
+        if (joined) return;
+        joined = true;
+        cudaEvent_t e;
+        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
+            cudaStreamSynchronize(aux);                  // cannot order by event: fall back to a host wait
+            return;
+        }
+        cudaEventRecord(e, aux);
+        cudaStreamWaitEvent(main, e, 0);
+        cudaEventDestroy(e);
+    }
+    ~Fork() { join(); }
+};
 
 // ---- optional per-kernel-class event timing (diagnostics for the roofline) ----
 struct ProfRec {
@@ -377,15 +423,19 @@ cil_status run_engines(int P, const RowSrc& asrc, const RowSrc& bsrc, int64_t ro
     if (rowsA == 0 || rowsB == 0) return CIL_OK;
     const bool b_same = same_rows(asrc, bsrc) && rowsA == rowsB;
 
+    // The max family's integer-pipe engine and the tensor-core family use different pipes and fit on
+    // one SM together (one Gram CTA + one k_max16_reg CTA): with both, the former runs on a side stream.
+    Fork fk(st, t_concurrent && pl.simt_mask && pl.max16 && pl.tc && range == nullptr && diag == nullptr);
     if (pl.simt_mask && pl.max16) {
         // max family alone: 15-bit fixed point on the integer pipes (never in distance-range mode,
         // whose plans use the SIMT engine)
         if (range != nullptr) return CIL_EUNSUPPORTED;
+        const cudaStream_t sm = fk.side();
         int16_t* qa = at<int16_t>(ws, L.off_aug16);
         int16_t* qb = qa + (size_t)P * rowsA * L.geom16.off[3];
         unsigned* maxbits = at<unsigned>(ws, L.off_max16);
         const AugGeom& g16 = L.geom16;
-        CIL_CU(launch_pack16(P, asrc, rowsA, bsrc, rowsB, g16, maxbits, qa, qb, status, st));
+        CIL_CU(launch_pack16(P, asrc, rowsA, bsrc, rowsB, g16, maxbits, qa, qb, status, sm));
         Max16Args a{};
         a.A = qa; a.B = qb;
         a.rowsA = rowsA; a.rowsB = rowsB; a.Kaug = L.geom16.off[3];
@@ -406,7 +456,7 @@ cil_status run_engines(int P, const RowSrc& asrc, const RowSrc& bsrc, int64_t ro
         a.tri = tile_skip == 2;
         a.sym = binout != nullptr && b_same;
         a.list = list; a.ctr = ctr; a.cap = cap;
-        CIL_CU(launch_max16(a, st));
+        CIL_CU(launch_max16(a, sm));
     } else if (pl.simt_mask) {
         float* aug = at<float>(ws, L.off_aug);
         float* augB = aug + (size_t)P * rowsA * L.geom.off[3];
@@ -522,6 +572,7 @@ cil_status run_engines(int P, const RowSrc& asrc, const RowSrc& bsrc, int64_t ro
             CIL_CU(launch_gram_tc(t, st));
         }
     }
+    fk.join();
     if (diag || range) return CIL_OK;
     if (L.list_cap) {
         RecheckArgs r = recheck_args(asrc, bsrc, K, g, sl, M, bp, sp, L, ws, status, P, binout, rowsA, rowsB, mask);
@@ -1144,6 +1195,7 @@ int32_t cil_prof_read(double* ms, int64_t* launches) {
 }
 
 void cil_diag_limit_recheck_list(int64_t limit) { t_list_limit = limit; }
+void cil_diag_concurrent_engines(int32_t on) { t_concurrent = on != 0; }
 void cil_diag_recheck_sort_min(int64_t n) { t_sort_min = n <= 0 ? 8192u : (uint32_t)(n > 0xffffffffll ? 0xffffffffll : n); }
 
 int64_t cil_diag_bounds_violations(void) {
