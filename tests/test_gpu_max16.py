@@ -194,3 +194,34 @@ def test_recheck_huge_bucket(cil, oracle_mod):
             _capi.lib.cil_diag_recheck_sort_min(0)
         assert st == 0 and listed >= 3 * 1500, listed            # every (0, j) case of every measure
         _check(c, ref, f"sort_min {sort_min}")
+
+
+@pytest.mark.parametrize("mode", ["features", "bins"])
+def test_concurrent_engines_identical(cil, oracle_mod, mode):
+    """The max family on the side stream concurrently with the three-phase tensor-core family gives
+    the same counts / bins as the serial order (cil_diag_concurrent_engines), and the oracle's."""
+    from paper_2203_14742_b200 import _capi
+    O = oracle_mod
+    grid = (2, 24, 24, 0.0)
+    A = cilgen.make_set(8080, 0, 150, grid[:3])
+    B = cilgen.make_set(8080, 1, 130, grid[:3])
+    D = O.distance_matrix(A[:40].numpy(), B[:40].numpy(), grid, 0x3F)
+    radii = _radii_at_distances(D, 10)
+    dev = torch.device("cuda")
+    R = torch.tensor(radii, device=dev)
+    out = []
+    for on in (0, 1):
+        _capi.lib.cil_diag_concurrent_engines(on)
+        try:
+            if mode == "features":
+                c, _, st = cil.features(A.to(dev), B.to(dev), grid, 0x3F, R)
+            else:
+                c, st = cil.bin_matrix(A.to(dev), B.to(dev), grid, 0x3F, R)
+            torch.cuda.synchronize()
+        finally:
+            _capi.lib.cil_diag_concurrent_engines(1)
+        assert int(st[0]) == 0
+        out.append(c[0].cpu().numpy())
+    assert np.array_equal(out[0], out[1])
+    if mode == "features":
+        _check(out[1], O.features(A.numpy(), B.numpy(), grid, 0x3F, radii, band=BAND), "concurrent")
