@@ -164,6 +164,21 @@ CIL_API cil_status cil_stats(int32_t P, const double* Y, int32_t n, int32_t D,
                      double* mu, double* Sigma, void* stream);
 
 /* ------------------------------------------------------------------------ */
+/* cil_gaussianity_pearson — the numerical Gaussianity check of CIL vectors:
+ * given the squared Mahalanobis distances d2 [n] (device; e.g. the quad column of cil_loglik of
+ * each vector against the vectors' own mu, Sigma), Pearson's statistic over `bins` equiprobable
+ * bins of the chi^2_D distribution: out (device double[2]) = {sum_b (c_b - n/bins)^2 / (n/bins),
+ * bins - 1}; c_b = #{k : bin of d2_k = b}, the bin of v = #{interior edges < v}.  The edges are
+ * chi^2_D quantiles b/bins computed on the host in FP64 (cil_chi2_quantile) and passed by value.
+ * 2 <= bins <= 64, n >= 1, D >= 1, else CIL_EINVAL.  Asynchronous on `stream`. */
+CIL_API cil_status cil_gaussianity_pearson(int64_t n, const double* d2, int32_t D, int32_t bins, double* out,
+                                           void* stream);
+
+/* cil_chi2_quantile — host: the prob-quantile of chi^2_D (regularised incomplete gamma, series /
+ * continued fraction in FP64, bisection to 200 steps); NaN outside D >= 1, 0 < prob < 1. */
+CIL_API double cil_chi2_quantile(int32_t D, double prob);
+
+/* ------------------------------------------------------------------------ */
 /* cil_loglik — Gaussian log-likelihood of P vectors (Eq. (4), PAPER.md:146;
  * Eq. (12)):  Sigma + ridge*I = L L^T (Cholesky, no pivoting),
  * z = L^{-1}(y - mu),  out[p] = {quad = z^T z (the paper's f), logdet = 2 sum ln L_ii,

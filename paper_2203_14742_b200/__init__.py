@@ -479,21 +479,19 @@ def train_vectors(X, n_ens, grid, mask, radii, *, engine=ENGINE_AUTO, stream=Non
 
 def gaussianity_chi2(Y, *, bins: int = 10, ridge: float = 0.0, stream=None):
     """Numerical Gaussianity check of CIL vectors: the squared Mahalanobis
-    distances d_k^2 = (y_k - mu)^T Sigma^-1 (y_k - mu) of the n vectors (cil_stats + cil_loglik,
-    on the device) against the chi^2_D distribution: Pearson's statistic over `bins`
-    equiprobable chi^2_D bins.  Returns (statistic, degrees of freedom, d2 [n])."""
-    from scipy import stats as _sps          # host-side: quantiles of chi^2_D only
+    distances d_k^2 = (y_k - mu)^T Sigma^-1 (y_k - mu) of the n vectors (cil_stats + cil_loglik) and
+    Pearson's statistic over `bins` equiprobable chi^2_D bins (cil_gaussianity_pearson), all on the
+    device.  Returns (statistic, degrees of freedom, d2 [n] on the device)."""
     Y2 = Y.to(torch.float64).contiguous()
     n, D = Y2.shape
     mu, Sig = stats(Y2, stream=stream)
     out, _ = loglik(mu, Sig, Y2, ridge, stream=stream)
-    d2 = out[:, 0].cpu().numpy()
-    edges = _sps.chi2.ppf([i / bins for i in range(1, bins)], D)
-    import numpy as _np
-    counts = _np.bincount(_np.searchsorted(edges, d2), minlength=bins)
-    expect = n / bins
-    stat = float(((counts - expect) ** 2 / expect).sum())
-    return stat, bins - 1, d2
+    d2 = out[:, 0].contiguous()
+    res = torch.empty(2, dtype=torch.float64, device=Y2.device)
+    check(lib.cil_gaussianity_pearson(n, d2.data_ptr(), D, bins, res.data_ptr(), _stream(stream)),
+          "cil_gaussianity_pearson")
+    r = res.cpu()
+    return float(r[0]), int(r[1]), d2
 
 
 def diag_gram_family(A, B, grid, *, stream=None):

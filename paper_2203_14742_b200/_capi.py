@@ -71,6 +71,10 @@ def _load():
     lib.cil_diag_recheck_sort_min.restype = None
     lib.cil_diag_concurrent_engines.argtypes = [i32]
     lib.cil_diag_concurrent_engines.restype = None
+    lib.cil_gaussianity_pearson.argtypes = [i64, P, i32, i32, P, P]
+    lib.cil_gaussianity_pearson.restype = i32
+    lib.cil_chi2_quantile.argtypes = [i32, ctypes.c_double]
+    lib.cil_chi2_quantile.restype = ctypes.c_double
     lib.cil_diag_sqrt_approx_error.argtypes = [P, P]
     lib.cil_diag_sqrt_approx_error.restype = i32
     lib.cil_prof_enable.argtypes = [i32]
@@ -101,7 +105,7 @@ lib = _load()
 
 EXPORTED = ["cil_features_workspace_size", "cil_features", "cil_stats", "cil_loglik",
             "cil_synth_workspace_size", "cil_synth_loglik", "cil_status_string", "cil_last_cuda_error",
-            "cil_version", "cil_last_launch_count", "cil_diag_gram", "cil_prof_enable", "cil_prof_read", "cil_normalize", "cil_diag_alu_ceiling", "cil_diag_sqrt_approx_error", "cil_features_recheck_count", "cil_diag_bounds_violations", "cil_diag_limit_recheck_list", "cil_diag_recheck_sort_min", "cil_diag_concurrent_engines",
+            "cil_version", "cil_last_launch_count", "cil_diag_gram", "cil_prof_enable", "cil_prof_read", "cil_normalize", "cil_diag_alu_ceiling", "cil_diag_sqrt_approx_error", "cil_features_recheck_count", "cil_diag_bounds_violations", "cil_diag_limit_recheck_list", "cil_diag_recheck_sort_min", "cil_diag_concurrent_engines", "cil_gaussianity_pearson", "cil_chi2_quantile",
             "cil_bin_matrix_workspace_size", "cil_bin_matrix", "cil_resample_counts",
             "cil_synth_boot_workspace_size", "cil_synth_loglik_boot", "cil_diag_gram_family",
             "cil_train_workspace_size", "cil_train_vectors", "cil_range_workspace_size", "cil_distance_range",

@@ -600,7 +600,7 @@ cil_status cil_features(int32_t P, const float* A, int64_t strideA, int64_t lda,
                         const double* radii, int64_t radii_stride, int32_t M, uint64_t* counts, double* y,
                         int32_t* item_status, cil_engine engine, void* ws, size_t ws_bytes, void* stream) {
     t_launches = 0;
-    NvtxScope nv_("cil_status");
+    NvtxScope nv_("cil_features");
     if (P < 1 || N < 0 || Nt < 0 || M < 1 || M > kMaxM) return CIL_EINVAL;
     if (check_grid(g, dist_mask) != CIL_OK) return CIL_EINVAL;
     if ((int)engine < 0 || (int)engine > 4) return CIL_EINVAL;
@@ -649,7 +649,7 @@ cil_status cil_features_recheck_count(int32_t P, int64_t N, int64_t Nt, cil_grid
 
 cil_status cil_normalize(int64_t n, const uint64_t* counts, double npairs, double* y, void* stream) {
     t_launches = 0;
-    NvtxScope nv_("cil_status");
+    NvtxScope nv_("cil_normalize");
     if (n < 0 || (n > 0 && (!counts || !y)) || !(npairs > 0.0)) return CIL_EINVAL;
     CIL_CU(launch_normalize(n, counts, npairs, y, reinterpret_cast<cudaStream_t>(stream)));
     return CIL_OK;
@@ -658,9 +658,66 @@ cil_status cil_normalize(int64_t n, const uint64_t* counts, double npairs, doubl
 cil_status cil_stats(int32_t P, const double* Y, int32_t n, int32_t D, double* mu, double* Sigma,
                      void* stream) {
     t_launches = 0;
-    NvtxScope nv_("cil_status");
+    NvtxScope nv_("cil_stats");
     if (P < 1 || n < 2 || D < 1 || !Y || !mu || !Sigma) return CIL_EINVAL;
     CIL_CU(launch_stats(P, Y, n, D, mu, Sigma, reinterpret_cast<cudaStream_t>(stream)));
+    return CIL_OK;
+}
+
+namespace {
+// Regularised lower incomplete gamma P(a, x) in FP64: the power series for x < a + 1, else
+// 1 - Q(a, x) from the continued fraction (modified Lentz).
+double gamma_p(double a, double x) {
+    if (!(x > 0.0)) return 0.0;
+    const double lpre = -x + a * log(x) - lgamma(a);
+    if (x < a + 1.0) {
+        double ap = a, del = 1.0 / a, sum = del;
+        for (int it = 0; it < 10000; ++it) {
+            ap += 1.0;
+            del *= x / ap;
+            sum += del;
+            if (fabs(del) < fabs(sum) * 1e-17) break;
+        }
+        return fmin(1.0, sum * exp(lpre));
+    }
+    const double tiny = 1e-300;
+    double b = x + 1.0 - a, c = 1.0 / tiny, d = 1.0 / b, h = d;
+    for (int i = 1; i < 10000; ++i) {
+        const double an = -i * (i - a);
+        b += 2.0;
+        d = an * d + b;
+        if (fabs(d) < tiny) d = tiny;
+        c = b + an / c;
+        if (fabs(c) < tiny) c = tiny;
+        d = 1.0 / d;
+        const double del = d * c;
+        h *= del;
+        if (fabs(del - 1.0) < 1e-17) break;
+    }
+    return fmax(0.0, 1.0 - exp(lpre) * h);
+}
+}  // namespace
+
+double cil_chi2_quantile(int32_t D, double prob) {
+    if (D < 1 || !(prob > 0.0) || !(prob < 1.0)) return NAN;
+    const double a = 0.5 * D;
+    double lo = 0.0, hi = fmax(1.0, 2.0 * D);
+    while (gamma_p(a, 0.5 * hi) < prob) hi *= 2.0;                // chi^2_D CDF(x) = P(D/2, x/2)
+    for (int it = 0; it < 200; ++it) {
+        const double mid = 0.5 * (lo + hi);
+        if (gamma_p(a, 0.5 * mid) < prob) lo = mid; else hi = mid;
+    }
+    return 0.5 * (lo + hi);
+}
+
+cil_status cil_gaussianity_pearson(int64_t n, const double* d2, int32_t D, int32_t bins, double* out, void* stream) {
+    t_launches = 0;
+    NvtxScope nv_("cil_gaussianity_pearson");
+    if (n < 1 || !d2 || !out || D < 1 || bins < 2 || bins > kMaxChi2Bins) return CIL_EINVAL;
+    Chi2Edges ed{};
+    ed.nb = bins;
+    for (int b = 1; b < bins; ++b) ed.e[b - 1] = cil_chi2_quantile(D, (double)b / bins);
+    CIL_CU(launch_chi2_pearson(n, d2, ed, out, reinterpret_cast<cudaStream_t>(stream)));
     return CIL_OK;
 }
 
@@ -668,7 +725,7 @@ cil_status cil_loglik(int32_t P, const double* mu, int64_t mu_stride, const doub
                       const double* y_obs, int32_t D, double ridge, double* out, int32_t* item_status,
                       void* stream) {
     t_launches = 0;
-    NvtxScope nv_("cil_status");
+    NvtxScope nv_("cil_loglik");
     if (P < 1 || D < 1 || !mu || !Sigma || !y_obs || !out || !item_status) return CIL_EINVAL;
     if (D > kMaxD) return CIL_EUNSUPPORTED;
     if (mu_stride < 0 || Sigma_stride < 0 || !(ridge >= 0.0)) return CIL_EINVAL;
@@ -727,7 +784,7 @@ cil_status cil_synth_loglik(int32_t P, const float* pools, int64_t pool_stride, 
                             double ridge, double* out, int32_t* item_status, double* Y_out, cil_engine engine,
                             void* ws, size_t ws_bytes, void* stream) {
     t_launches = 0;
-    NvtxScope nv_("cil_status");
+    NvtxScope nv_("cil_synth_loglik");
     if (P < 1 || n_ens < 2 || N_set < 1 || N_tilde < 1 || M < 1 || M > kMaxM) return CIL_EINVAL;
     if (check_grid(g, dist_mask) != CIL_OK) return CIL_EINVAL;
     if ((int)engine < 0 || (int)engine > 4) return CIL_EINVAL;
@@ -772,7 +829,7 @@ cil_status cil_synth_loglik(int32_t P, const float* pools, int64_t pool_stride, 
 cil_status cil_minmax_scale(int64_t n, const float* X, int64_t ldx, float* Y, int64_t ldy, cil_grid g,
                             void* stream) {
     t_launches = 0;
-    NvtxScope nv_("cil_status");
+    NvtxScope nv_("cil_minmax_scale");
     if (n < 0 || g.S < 1 || g.H < 1 || g.W < 1) return CIL_EINVAL;
     const int64_t K = (int64_t)g.S * g.H * g.W;
     if (n > 0 && (!X || !Y || ldx < K || ldy < K)) return CIL_EINVAL;
@@ -793,7 +850,7 @@ cil_status cil_distance_range(int32_t P, const float* A, int64_t strideA, int64_
                               int64_t strideB, int64_t ldb, int64_t Nt, cil_grid g, uint32_t dist_mask,
                               double* range, int32_t* item_status, void* ws, size_t ws_bytes, void* stream) {
     t_launches = 0;
-    NvtxScope nv_("cil_status");
+    NvtxScope nv_("cil_distance_range");
     if (P < 1 || N < 1 || Nt < 1) return CIL_EINVAL;
     if (check_grid(g, dist_mask) != CIL_OK) return CIL_EINVAL;
     if (!range || !item_status || !ws) return CIL_EINVAL;
@@ -820,7 +877,7 @@ cil_status cil_distance_range(int32_t P, const float* A, int64_t strideA, int64_
 cil_status cil_radii_from_range(int32_t P, int32_t n_meas, int32_t M, const double* range, int32_t law,
                                 double margin, double* radii, int32_t* item_status, void* stream) {
     t_launches = 0;
-    NvtxScope nv_("cil_status");
+    NvtxScope nv_("cil_radii_from_range");
     if (P < 1 || n_meas < 1 || n_meas > kMaxMeas || M < 1 || M > kMaxM || (law != 0 && law != 1)) return CIL_EINVAL;
     if (!range || !radii || !item_status || !(margin >= 0.0 && margin < 1.0)) return CIL_EINVAL;
     CIL_CU(launch_radii(P, n_meas, M, reinterpret_cast<const unsigned long long*>(range), law, margin, radii,
@@ -844,7 +901,7 @@ cil_status cil_train_vectors(int32_t P, const float* X, int64_t stride, int64_t 
                              double* Y, int32_t* item_status, cil_engine engine, void* ws, size_t ws_bytes,
                              void* stream) {
     t_launches = 0;
-    NvtxScope nv_("cil_status");
+    NvtxScope nv_("cil_train_vectors");
     if (P < 1 || n_ens < 2 || N < 1 || M < 1 || M > kMaxM) return CIL_EINVAL;
     if (check_grid(g, dist_mask) != CIL_OK) return CIL_EINVAL;
     if ((int)engine < 0 || (int)engine > 4) return CIL_EINVAL;
@@ -887,7 +944,7 @@ cil_status cil_bin_matrix(int32_t P, const float* A, int64_t strideA, int64_t ld
                           const double* radii, int64_t radii_stride, int32_t M, uint8_t* bins,
                           int32_t* item_status, cil_engine engine, void* ws, size_t ws_bytes, void* stream) {
     t_launches = 0;
-    NvtxScope nv_("cil_status");
+    NvtxScope nv_("cil_bin_matrix");
     if (P < 1 || N < 0 || Nt < 0 || M < 1 || M > kMaxM) return CIL_EINVAL;
     if (check_grid(g, dist_mask) != CIL_OK) return CIL_EINVAL;
     if ((int)engine < 0 || (int)engine > 4) return CIL_EINVAL;
@@ -914,7 +971,7 @@ cil_status cil_resample_counts(int32_t P, const uint8_t* bins, int64_t N, int64_
                                uint64_t* counts, double* y, int64_t y_item_stride, int32_t* item_status,
                                void* stream) {
     t_launches = 0;
-    NvtxScope nv_("cil_status");
+    NvtxScope nv_("cil_resample_counts");
     if (P < 1 || N < 1 || Nt < 1 || n_meas < 1 || n_meas > kMaxMeas || M < 1 || M > kMaxM) return CIL_EINVAL;
     if (n_rep < 1 || n1 < 1 || n2 < 1 || !bins || !I1 || !I2 || !item_status || (!counts && !y)) return CIL_EINVAL;
     if (y_item_stride < 0 || (y && y_item_stride > 0 && y_item_stride < (int64_t)n_rep * n_meas * M))
@@ -991,7 +1048,7 @@ cil_status cil_synth_loglik_boot(int32_t P, const float* pools, int64_t pool_str
                                  int32_t* item_status, double* Y_out, cil_engine engine, void* ws, size_t ws_bytes,
                                  void* stream) {
     t_launches = 0;
-    NvtxScope nv_("cil_status");
+    NvtxScope nv_("cil_synth_loglik_boot");
     if (P < 1 || N_set < 1 || N_syn <= N_set || n_rep < 2 || M < 1 || M > kMaxM) return CIL_EINVAL;
     if (check_grid(g, dist_mask) != CIL_OK) return CIL_EINVAL;
     if ((int)engine < 0 || (int)engine > 4) return CIL_EINVAL;
@@ -1112,7 +1169,7 @@ cil_status cil_synth_loglik_boot(int32_t P, const float* pools, int64_t pool_str
 cil_status cil_diag_gram(const float* A, int64_t lda, int64_t N, const float* B, int64_t ldb, int64_t Nt,
                          cil_grid g, cil_engine engine, float* d2E, void* ws, size_t ws_bytes, void* stream) {
     t_launches = 0;
-    NvtxScope nv_("cil_status");
+    NvtxScope nv_("cil_diag_gram");
     if (N < 1 || Nt < 1 || !A || !B || !d2E || !ws) return CIL_EINVAL;
     if (engine != CIL_ENGINE_TC_3XBF16 && engine != CIL_ENGINE_TC_3XTF32 && engine != CIL_ENGINE_TC_I8)
         return CIL_EINVAL;
@@ -1140,7 +1197,7 @@ cil_status cil_diag_gram(const float* A, int64_t lda, int64_t N, const float* B,
 cil_status cil_diag_gram_family(const float* A, int64_t lda, int64_t N, const float* B, int64_t ldb, int64_t Nt,
                                 cil_grid g, float* vE, void* ws, size_t ws_bytes, void* stream) {
     t_launches = 0;
-    NvtxScope nv_("cil_status");
+    NvtxScope nv_("cil_diag_gram_family");
     if (N < 1 || Nt < 1 || !A || !B || !vE || !ws) return CIL_EINVAL;
     const uint32_t mask = CIL_L2 | CIL_W12SUM | CIL_W12;
     if (check_grid(g, mask) != CIL_OK) return CIL_EINVAL;

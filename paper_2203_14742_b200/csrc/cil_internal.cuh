@@ -340,6 +340,14 @@ struct RecheckArgs {
 };
 cudaError_t launch_recheck(const RecheckArgs& a, int64_t hist_elems, cudaStream_t st);
 
+// stats.cu — chi^2 Gaussianity diagnostic (interior bin edges by value: no host-to-device copy)
+constexpr int kMaxChi2Bins = 64;
+struct Chi2Edges {
+    int nb;                          // bins
+    double e[kMaxChi2Bins - 1];      // interior edges, increasing
+};
+cudaError_t launch_chi2_pearson(int64_t n, const double* d2, const Chi2Edges& ed, double* out, cudaStream_t st);
+
 // stats.cu
 cudaError_t launch_finalize(int P, int nq, int M, const SegParams& sp, const uint64_t* hist,
                             uint64_t* counts, double* y, int64_t pairs_per_seg_rows,

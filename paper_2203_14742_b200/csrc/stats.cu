@@ -392,4 +392,39 @@ cudaError_t launch_radii(int P, int nq, int M, const unsigned long long* range, 
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- chi^2 Gaussianity diagnostic
+// Pearson's statistic of n squared Mahalanobis distances over the equiprobable chi^2_D bins whose
+// interior edges the host computed (cil_gaussianity_pearson): bin of d2 = #{edges < d2} (numpy's
+// searchsorted, side 'left'); out = {sum_b (c_b - n/B)^2 / (n/B), B - 1}.  One CTA.
+__global__ void __launch_bounds__(256) k_chi2_pearson(int64_t n, const double* __restrict__ d2, Chi2Edges ed,
+                                                     double* __restrict__ out) {
+    __shared__ unsigned long long cnt[kMaxChi2Bins];
+    for (int b = threadIdx.x; b < ed.nb; b += blockDim.x) cnt[b] = 0ull;
+    __syncthreads();
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const double v = d2[i];
+        int b = 0;
+        while (b < ed.nb - 1 && ed.e[b] < v) ++b;
+        atomicAdd(&cnt[b], 1ull);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const double expect = (double)n / ed.nb;
+        double stat = 0.0;
+        for (int b = 0; b < ed.nb; ++b) {
+            const double d = (double)cnt[b] - expect;
+            stat += d * d / expect;
+        }
+        out[0] = stat;
+        out[1] = (double)(ed.nb - 1);
+    }
+}
+
+cudaError_t launch_chi2_pearson(int64_t n, const double* d2, const Chi2Edges& ed, double* out, cudaStream_t st) {
+    ProfScope ps_(K_TAIL, st);
+    k_chi2_pearson<<<1, 256, 0, st>>>(n, d2, ed, out);
+    note_launch();
+    return cudaGetLastError();
+}
+
 }  // namespace cil

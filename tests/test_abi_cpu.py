@@ -93,3 +93,19 @@ def test_host_validation(capi):
                                 buf, 64, None) == EINVAL
     assert lib.cil_synth_loglik(1, fake, 0, 16, 2, 2, 2, fake, 16, fake, g, 0x3F, fake, 64, 0.0, fake, fake, None,
                                 0, buf, 64, None) == EUNSUP
+
+
+def test_chi2_quantile_host(capi):
+    """cil_chi2_quantile (host code of the Gaussianity diagnostic) against scipy's
+    chi^2 inverse CDF, and its argument validation."""
+    import math
+
+    from scipy import stats as sps
+    q = capi.lib.cil_chi2_quantile
+    for D in (1, 2, 7, 45, 192):
+        for pr in (1e-4, 0.01, 0.1, 0.5, 0.9, 0.99, 1 - 1e-6):
+            assert q(D, pr) == pytest.approx(sps.chi2.ppf(pr, D), rel=1e-10, abs=1e-12), (D, pr)
+    assert math.isnan(q(0, 0.5)) and math.isnan(q(3, 0.0)) and math.isnan(q(3, 1.0))
+    # Pearson statistic validation (no device work on invalid arguments)
+    assert capi.lib.cil_gaussianity_pearson(10, None, 3, 10, None, None) != 0
+    assert capi.lib.cil_gaussianity_pearson(10, 8, 3, 65, 8, None) != 0

@@ -461,9 +461,14 @@ def test_gaussianity_chi2(cil, oracle_mod):
     mu, Sig = O.stats(Y)
     for k in range(0, n, 37):
         out, st = O.loglik(mu, Sig, Y[k])
-        assert d2[k] == pytest.approx(out[0], rel=1e-9)
+        assert float(d2[k]) == pytest.approx(out[0], rel=1e-9)
     from scipy import stats as sps
     assert sps.chi2.sf(stat, dof) > 1e-4           # Gaussian data: no rejection at any sane level
+    # the device's Pearson statistic is the plain one on its own d2 (scipy quantiles, numpy bins)
+    d2h = d2.cpu().numpy()
+    edges = sps.chi2.ppf(np.arange(1, 10) / 10, D)
+    cnt = np.bincount(np.searchsorted(edges, d2h), minlength=10)
+    assert dof == 9 and stat == pytest.approx(float(((cnt - n / 10) ** 2 / (n / 10)).sum()), rel=1e-12)
 
 
 @pytest.mark.parametrize("law", ["power", "linear"])
