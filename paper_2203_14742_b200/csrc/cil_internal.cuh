@@ -117,6 +117,19 @@ struct AugGeom {
 
 inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
+// n / d (and n % d) for n < 2^31, d >= 1 by a multiply-high: m = floor((2^32 - 1) / d) leaves the
+// quotient short by at most 1, fixed by one compare (checked on the host for d < 5000 and random n)
+struct FastDiv {
+    uint32_t d, m;
+    __host__ __device__ explicit FastDiv(uint32_t d_) : d(d_), m(0xffffffffu / d_) {}
+    __device__ __forceinline__ uint32_t div(uint32_t n, uint32_t& r) const {
+        uint32_t q = __umulhi(n, m);
+        r = n - q * d;
+        if (r >= d) { ++q; r -= d; }
+        return q;
+    }
+};
+
 inline AugGeom make_aug_geom(int S, int H, int W, int nreg, uint32_t gs = 0, int64_t pad = kSimtBK) {
     AugGeom a{};
     a.S = S; a.H = H; a.W = W;

@@ -1041,6 +1041,7 @@ __global__ void __launch_bounds__(512, 2) k_pack3_aug4(RowSrc src, int64_t rows,
     const float* cc = center + p * Kc;
     const int64_t orow = row0 + p * rows + r;
     const uint32_t W = (uint32_t)g.W, H = (uint32_t)g.H, K = (uint32_t)g.K;
+    const FastDiv fw(W), fh(H);
     __shared__ float red[3][NW];
     __shared__ long long redd[NW][3][6];
     const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
@@ -1056,7 +1057,8 @@ __global__ void __launch_bounds__(512, 2) k_pack3_aug4(RowSrc src, int64_t rows,
         float nx = __shfl_down_sync(0xffffffffu, t.x, 1);
         dx = dy = make_float4(0.f, 0.f, 0.f, 0.f);
         if (!ok) return;
-        const uint32_t sr = e / W, c = e - sr * W, sp = sr / H, hr = sr - sp * H;
+        uint32_t c, hr;
+        const uint32_t sr = fw.div(e, c), sp = fh.div(sr, hr);
         if (!(g.gs == 0 || ((g.gs >> sp) & 1u))) return;
         if (c + 4 < W && ln == 31) nx = (__ldg(x + e + 4) - __ldg(cc + e + 4));
         dx = make_float4(t.y - t.x, t.z - t.y, t.w - t.z, c + 4 < W ? nx - t.w : 0.f);
@@ -1117,7 +1119,9 @@ __global__ void __launch_bounds__(512, 2) k_pack3_aug4(RowSrc src, int64_t rows,
         float4 t, dx, dy;
         load(e, t, dx, dy);
         if (e >= K) continue;
-        const uint32_t sr = e / W, sp = sr / H, hr = sr - sp * H;
+        uint32_t c, hr;
+        const uint32_t sr = fw.div(e, c), sp = fh.div(sr, hr);
+        (void)c;
         put4(0, kp0 + e, t);
         put4(1, kp1 + e, dx);
         if (hr + 1 < H) put4(2, kp2 + (int64_t)e - (int64_t)sp * W, dy);

@@ -24,70 +24,95 @@
 #include <cub/block/block_scan.cuh>
 
 #include "cil_internal.cuh"
+#include "tc_common.cuh"
 
-#ifndef CIL_RK_EXP
-#define CIL_RK_EXP 0   // occupancy / loads-in-flight experiments (tools/simt_var_build.sh); 0 = product
-#endif
 
 namespace cil {
 
 namespace {
+// ---- the pair sweeps' operand ring: chunks of RCH elements of x and y streamed into shared memory
+// by one thread with cp.async.bulk (TMA, 1-D) and an mbarrier per stage, RST stages in flight, so a
+// CTA keeps 3 x 2 x 8 KB of its pair's rows in flight while it computes, 4 CTAs per SM (2 CTAs with
+// 3 x 2 x 16 KB: slower; profiles/r02_recheck.txt)
+constexpr uint32_t RCH = 2048;
+constexpr int RST = 3;
+constexpr size_t kRingBytes = sizeof(float) * 2 * RCH * RST;
+struct Ring {
+    float* buf;        // [RST][2][RCH] (x chunk, y chunk)
+    uint64_t* bar;     // [RST]
+    uint32_t g;        // chunks streamed so far by this CTA (stage = g % RST, parity = (g / RST) & 1)
+};
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     tc::smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(tc::smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void ring_issue(Ring& r, uint32_t gi, const float* x, const float* y, uint32_t e0,
+                                           uint32_t len) {
+    const int st = (int)(gi % RST);
+    float* dx = r.buf + (size_t)st * 2 * RCH;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // the stage's generic reads are done
+    tc::mbar_expect_tx(&r.bar[st], 8u * len);
+    bulk_g2s(dx, x + e0, 4u * len, &r.bar[st]);
+    bulk_g2s(dx + RCH, y + e0, 4u * len, &r.bar[st]);
+}
+// Streams the K elements of x and y (16-B aligned, K % 4 == 0) through the ring; all threads call
+// f(base, sx, sy, len) once per chunk (elements [base, base + len)).
+template <class F>
+__device__ void ring_stream(Ring& r, const float* x, const float* y, uint32_t K, F f) {
+    const uint32_t nch = (K + RCH - 1) / RCH, g0 = r.g;
+    if (threadIdx.x == 0)
+        for (uint32_t c = 0; c < nch && c < (uint32_t)RST; ++c) ring_issue(r, g0 + c, x, y, c * RCH, min(RCH, K - c * RCH));
+    for (uint32_t c = 0; c < nch; ++c) {
+        const uint32_t gi = g0 + c, st = gi % RST;
+        tc::mbar_wait(&r.bar[st], (gi / RST) & 1u);
+        const float* sx = r.buf + (size_t)st * 2 * RCH;
+        f(c * RCH, sx, sx + RCH, min(RCH, K - c * RCH));
+        __syncthreads();                                   // every thread is done with the stage
+        if (threadIdx.x == 0 && c + RST < nch)
+            ring_issue(r, gi + RST, x, y, (c + RST) * RCH, min(RCH, K - (c + RST) * RCH));
+    }
+    r.g = g0 + nch;
+}
 
 // The six FP64 sub-norms of u = x - y over one pattern, one CTA of 256 threads.
 // full = false: only s0 (a flat K-long loop with 4 float4 pairs in flight per thread); full with
-// W % 4 == 0 and a 32 KB staging buffer: a flat float4 sweep over chunks of 4096 elements of x and y
-// staged in shared memory (the x / y neighbours from there); otherwise a warp per grid row.
+// W % 4 == 0 and the operand ring: a flat float4 sweep over the ring's chunks of x and y (the x / y
+// neighbours from there); otherwise a warp per grid row.
 __device__ void exact_subnorms(const float* x, const float* y, const RecheckArgs& a, bool full, double out[6],
-                               double (*red)[8], float* stage = nullptr) {
+                               double (*red)[8], Ring* ring = nullptr) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     double v[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-    if (full && stage != nullptr && (a.W & 3) == 0 && a.K < (1ll << 31)) {
-        constexpr uint32_t CH = 4096;
-        const uint32_t K = (uint32_t)a.K, W = (uint32_t)a.W, H = (uint32_t)a.H;
-        float* sx = stage;
-        float* sy = stage + CH;
-        for (uint32_t base = 0; base < K; base += CH) {
-            float4 xa[4], yb[4];
+    if (full && ring != nullptr && (a.W & 3) == 0 && a.K < (1ll << 31)) {
+        const uint32_t W = (uint32_t)a.W, H = (uint32_t)a.H;
+        const FastDiv fw(W), fh(H);
+        ring_stream(*ring, x, y, (uint32_t)a.K, [&](uint32_t base, const float* sx, const float* sy, uint32_t len) {
 #pragma unroll
-            for (int t = 0; t < 4; ++t) {
-                const uint32_t e = base + t * 1024 + threadIdx.x * 4;
-                if (e < K) {
-                    xa[t] = __ldg(reinterpret_cast<const float4*>(x + e));
-                    yb[t] = __ldg(reinterpret_cast<const float4*>(y + e));
-                } else {
-                    xa[t] = yb[t] = make_float4(0.f, 0.f, 0.f, 0.f);
-                }
-            }
-            __syncthreads();                                   // previous chunk's reads are done
-#pragma unroll
-            for (int t = 0; t < 4; ++t) {
-                reinterpret_cast<float4*>(sx)[t * 256 + threadIdx.x] = xa[t];
-                reinterpret_cast<float4*>(sy)[t * 256 + threadIdx.x] = yb[t];
-            }
-            __syncthreads();
-#pragma unroll
-            for (int t = 0; t < 4; ++t) {
+            for (int t = 0; t < (int)(RCH / 1024); ++t) {
                 const uint32_t l = t * 1024 + threadIdx.x * 4, e = base + l;
-                if (e >= K) continue;
-                const double u0 = (double)xa[t].x - (double)yb[t].x, u1 = (double)xa[t].y - (double)yb[t].y;
-                const double u2 = (double)xa[t].z - (double)yb[t].z, u3 = (double)xa[t].w - (double)yb[t].w;
+                if (l >= len) continue;
+                const float4 xa = *reinterpret_cast<const float4*>(sx + l), yb = *reinterpret_cast<const float4*>(sy + l);
+                const double u0 = (double)xa.x - (double)yb.x, u1 = (double)xa.y - (double)yb.y;
+                const double u2 = (double)xa.z - (double)yb.z, u3 = (double)xa.w - (double)yb.w;
                 v[0] += u0 * u0 + u1 * u1 + u2 * u2 + u3 * u3;
                 v[3] = fmax(v[3], fmax(fmax(fabs(u0), fabs(u1)), fmax(fabs(u2), fabs(u3))));
-                const uint32_t sr = e / W, c = e - sr * W, sp = sr / H, hr = sr - sp * H;
+                uint32_t c, hr;
+                const uint32_t sr = fw.div(e, c), sp = fh.div(sr, hr);
                 if (!(a.gs == 0 || ((a.gs >> sp) & 1u))) continue;
                 const double d0 = u1 - u0, d1 = u2 - u1, d2 = u3 - u2;
                 v[1] += d0 * d0 + d1 * d1 + d2 * d2;
                 v[4] = fmax(v[4], fmax(fmax(fabs(d0), fabs(d1)), fabs(d2)));
                 if (c + 4 < W) {
-                    const double un = l + 4 < CH ? (double)sx[l + 4] - (double)sy[l + 4]
-                                                 : (double)__ldg(x + e + 4) - (double)__ldg(y + e + 4);
+                    const double un = l + 4 < len ? (double)sx[l + 4] - (double)sy[l + 4]
+                                                  : (double)__ldg(x + e + 4) - (double)__ldg(y + e + 4);
                     const double d3 = un - u3;
                     v[1] += d3 * d3;
                     v[4] = fmax(v[4], fabs(d3));
                 }
                 if (hr + 1 < H) {
                     float4 xd, yd;
-                    if (l + W < CH) {
+                    if (l + W < len) {
                         xd = *reinterpret_cast<const float4*>(sx + l + W);
                         yd = *reinterpret_cast<const float4*>(sy + l + W);
                     } else {
@@ -100,7 +125,7 @@ __device__ void exact_subnorms(const float* x, const float* y, const RecheckArgs
                     v[5] = fmax(v[5], fmax(fmax(fabs(e0), fabs(e1)), fmax(fabs(e2), fabs(e3))));
                 }
             }
-        }
+        });
     } else if (!full) {
         int64_t k = (int64_t)threadIdx.x * 4;
         for (; k + 3 * 1024 < a.K; k += 4 * 1024) {
@@ -183,67 +208,48 @@ __device__ double measure(int k, const double sub[6], double w, double h) {
 
 // The max sub-norms m0, m_x, m_y of u = x - y in FP32 (raw differences, no 1/h), one CTA of 256
 // threads; |result - exact| <= 2^-24 m0, 3 2^-24 (m0 + m_x), 3 2^-24 (m0 + m_y).  W % 4 == 0 (and
-// a 16 KB staging buffer us): flat float4 sweep in chunks of 4096 elements, u staged in shared
-// memory for the neighbours; else a warp per grid row.
+// the operand ring): a flat float4 sweep over the ring's chunks; else a warp per grid row.
 __device__ __forceinline__ float amax4(float m, float a, float b, float c, float d) {
     return fmaxf(fmaxf(m, fmaxf(fabsf(a), fabsf(b))), fmaxf(fabsf(c), fabsf(d)));
 }
 __device__ void max_subnorms32(const float* x, const float* y, const RecheckArgs& a, float out[3], float (*red)[8],
-                               float* us) {
+                               Ring* ring) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     float v[3] = {0.f, 0.f, 0.f};
     const int W = a.W, H = a.H;
-    if ((W & 3) == 0 && us != nullptr) {
-        // chunks of 4096 elements: u = x - y staged in shared memory (us), so the x and y
-        // neighbours come from there; only those past the chunk end are loaded again (a
-        // cp.async double-buffered variant ran 20 % slower: profiles/r02_recheck.txt)
-        constexpr int U4 = 4, CH = 1024 * U4;
-        const uint32_t K = (uint32_t)a.K;
-        for (uint32_t base = 0; base < K; base += CH) {
-            float4 xa[U4], yb[U4];
+    if ((W & 3) == 0 && ring != nullptr) {
+        const uint32_t Wu = (uint32_t)W, Hu = (uint32_t)H;
+        const FastDiv fw(Wu), fh(Hu);
+        ring_stream(*ring, x, y, (uint32_t)a.K, [&](uint32_t base, const float* sx, const float* sy, uint32_t len) {
 #pragma unroll
-            for (int t = 0; t < U4; ++t) {
-                const uint32_t e = base + t * 1024 + threadIdx.x * 4;
-                if (e < K) {
-                    xa[t] = __ldg(reinterpret_cast<const float4*>(x + e));
-                    yb[t] = __ldg(reinterpret_cast<const float4*>(y + e));
-                } else {
-                    xa[t] = yb[t] = make_float4(0.f, 0.f, 0.f, 0.f);
-                }
-            }
-            __syncthreads();                                   // previous chunk's reads of us are done
-#pragma unroll
-            for (int t = 0; t < U4; ++t)
-                reinterpret_cast<float4*>(us)[t * 256 + threadIdx.x] =
-                    make_float4(xa[t].x - yb[t].x, xa[t].y - yb[t].y, xa[t].z - yb[t].z, xa[t].w - yb[t].w);
-            __syncthreads();
-#pragma unroll
-            for (int t = 0; t < U4; ++t) {
+            for (int t = 0; t < (int)(RCH / 1024); ++t) {
                 const uint32_t l = t * 1024 + threadIdx.x * 4, e = base + l;
-                if (e >= K) continue;
-                const float4 u = reinterpret_cast<const float4*>(us)[t * 256 + threadIdx.x];
+                if (l >= len) continue;
+                const float4 xa = *reinterpret_cast<const float4*>(sx + l), yb = *reinterpret_cast<const float4*>(sy + l);
+                const float4 u = make_float4(xa.x - yb.x, xa.y - yb.y, xa.z - yb.z, xa.w - yb.w);
                 v[0] = amax4(v[0], u.x, u.y, u.z, u.w);
-                const uint32_t sr = e / (uint32_t)W, c = e - sr * (uint32_t)W;
-                const uint32_t sp = sr / (uint32_t)H, hr = sr - sp * (uint32_t)H;
+                uint32_t c, hr;
+                const uint32_t sr = fw.div(e, c), sp = fh.div(sr, hr);
                 if (!(a.gs == 0 || ((a.gs >> sp) & 1u))) continue;
                 v[1] = fmaxf(v[1], fmaxf(fabsf(u.y - u.x), fmaxf(fabsf(u.z - u.y), fabsf(u.w - u.z))));
-                if (c + 4 < (uint32_t)W) {
-                    const float nx = l + 4 < (uint32_t)CH ? us[l + 4] : __ldg(x + e + 4) - __ldg(y + e + 4);
+                if (c + 4 < Wu) {
+                    const float nx = l + 4 < len ? sx[l + 4] - sy[l + 4] : __ldg(x + e + 4) - __ldg(y + e + 4);
                     v[1] = fmaxf(v[1], fabsf(nx - u.w));
                 }
-                if (hr + 1 < (uint32_t)H) {
-                    float4 d;
-                    if (l + W < (uint32_t)CH) {
-                        d = *reinterpret_cast<const float4*>(us + l + W);
+                if (hr + 1 < Hu) {
+                    float4 xd, yd;
+                    if (l + Wu < len) {
+                        xd = *reinterpret_cast<const float4*>(sx + l + Wu);
+                        yd = *reinterpret_cast<const float4*>(sy + l + Wu);
                     } else {
-                        const float4 xd = __ldg(reinterpret_cast<const float4*>(x + e + W));
-                        const float4 yd = __ldg(reinterpret_cast<const float4*>(y + e + W));
-                        d = make_float4(xd.x - yd.x, xd.y - yd.y, xd.z - yd.z, xd.w - yd.w);
+                        xd = __ldg(reinterpret_cast<const float4*>(x + e + Wu));
+                        yd = __ldg(reinterpret_cast<const float4*>(y + e + Wu));
                     }
-                    v[2] = amax4(v[2], d.x - u.x, d.y - u.y, d.z - u.z, d.w - u.w);
+                    v[2] = amax4(v[2], (xd.x - yd.x) - u.x, (xd.y - yd.y) - u.y, (xd.z - yd.z) - u.z,
+                                 (xd.w - yd.w) - u.w);
                 }
             }
-        }
+        });
     } else {
         const int SH = a.S * a.H;
         for (int sr = w; sr < SH; sr += 8) {
@@ -379,12 +385,20 @@ __global__ void k_fb_clear(RecheckArgs a, int64_t hist_elems) {
         a.hist[e] = 0ull;
 }
 
-__global__ void __launch_bounds__(256, CIL_RK_EXP == 1 ? 3 : CIL_RK_EXP == 3 ? 2 : 4) k_recheck(RecheckArgs a) {
+__global__ void __launch_bounds__(256, 4) k_recheck(RecheckArgs a) {
     const uint32_t c = *a.ctr;
     const bool overflow = c > a.cap;
     __shared__ double red[6][8];
     __shared__ double sub[6];
-    __shared__ __align__(16) float stage[8192];           // the FP32 / FP64 sweeps' chunk staging
+    extern __shared__ __align__(16) float ring_buf[];     // kRingBytes (the sweeps' operand ring)
+    __shared__ __align__(8) uint64_t ring_bar[RST];
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < RST; ++i) tc::mbar_init(&ring_bar[i], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    Ring ring{ring_buf, ring_bar, 0u};
+    Ring* rp = a.K < (1ll << 31) ? &ring : nullptr;
     if (overflow) {
         if (blockIdx.x == 0 && threadIdx.x == 0)
             for (int p = 0; p < a.P; ++p) atomicOr(&a.status[p], CIL_ITEM_OVERFLOW);
@@ -394,7 +408,7 @@ __global__ void __launch_bounds__(256, CIL_RK_EXP == 1 ? 3 : CIL_RK_EXP == 3 ? 2
             const int64_t p = e / per, i = (e % per) / a.rowsB, j = e % a.rowsB;
             if (a.mirror && j < i) continue;
             if (a.status[p] & CIL_ITEM_BADRADII) continue;
-            exact_subnorms(row_ptr(a.asrc, p, i), row_ptr(a.bsrc, p, j), a, a.kinds & ~1u, sub, red, stage);
+            exact_subnorms(row_ptr(a.asrc, p, i), row_ptr(a.bsrc, p, j), a, a.kinds & ~1u, sub, red, rp);
             if (threadIdx.x == 0)
                 for (int k = 0; k < 6; ++k)
                     if ((a.kinds >> k) & 1u) settle(a, p, i, j, k, 0, measure(k, sub, a.w, a.h), true);
@@ -408,7 +422,7 @@ __global__ void __launch_bounds__(256, CIL_RK_EXP == 1 ? 3 : CIL_RK_EXP == 3 ? 2
             const int64_t p = ent.x, i = ent.y, j = ent.z;
             const int b_lo = (int)(ent.w & 255u);
             const int kind = (int)((ent.w >> 8) & 255u);
-            exact_subnorms(row_ptr(a.asrc, p, i), row_ptr(a.bsrc, p, j), a, kind != 0, sub, red, stage);
+            exact_subnorms(row_ptr(a.asrc, p, i), row_ptr(a.bsrc, p, j), a, kind != 0, sub, red, rp);
             if (threadIdx.x == 0) settle(a, p, i, j, kind, b_lo, measure(kind, sub, a.w, a.h), false);
             __syncthreads();
         }
@@ -453,7 +467,7 @@ __global__ void __launch_bounds__(256, CIL_RK_EXP == 1 ? 3 : CIL_RK_EXP == 3 ? 2
         const float* yb = row_ptr(a.bsrc, p, j);
         bool exact = true;
         if (!(kmask & 0x0Du)) {                              // max family only: FP32 interval first
-            max_subnorms32(xa, yb, a, m32, red32, a.K < (1ll << 31) ? stage : nullptr);
+            max_subnorms32(xa, yb, a, m32, red32, rp);
             if ((int)threadIdx.x < n) measure32((int)((s_w[threadIdx.x] >> 8) & 255u), m32, a.h, &s_d[threadIdx.x], &s_E[threadIdx.x]);
             __syncthreads();
             exact = false;
@@ -470,7 +484,7 @@ __global__ void __launch_bounds__(256, CIL_RK_EXP == 1 ? 3 : CIL_RK_EXP == 3 ? 2
             __syncthreads();
         }
         if (!exact) continue;
-        exact_subnorms(xa, yb, a, (kmask & ~1u) != 0u, sub, red, stage);
+        exact_subnorms(xa, yb, a, (kmask & ~1u) != 0u, sub, red, rp);
         if ((int)threadIdx.x < n) s_d[threadIdx.x] = measure((int)((s_w[threadIdx.x] >> 8) & 255u), sub, a.w, a.h);
         __syncthreads();
         for (int k = 0; k < n; ++k) {
@@ -497,7 +511,9 @@ cudaError_t launch_recheck(const RecheckArgs& a, int64_t hist_elems, cudaStream_
     k_rk_count<<<nsm * 2, 256, 0, st>>>(a);
     k_rk_scan<<<1, 1024, 0, st>>>(a, nrows);
     k_rk_scatter<<<nsm * 2, 256, 0, st>>>(a);
-    k_recheck<<<nsm * 8, 256, 0, st>>>(a);
+    static SmemAttrOnce attr;
+    if (cudaError_t e = attr.ensure(k_recheck, (int)kRingBytes); e != cudaSuccess) return e;
+    k_recheck<<<nsm * 8, 256, kRingBytes, st>>>(a);
     note_launch(4);
     return cudaGetLastError();
 }
