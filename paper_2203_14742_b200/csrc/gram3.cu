@@ -97,11 +97,19 @@ struct Params {
     int64_t hist_elems;                // bounds-checked builds only
 };
 
+#ifndef CIL_G3_WIDE
+#define CIL_G3_WIDE 0   // 0: six N = TN MMAs per K step (product); 1: four wide MMAs (experiment builds)
+#endif
 template <int TN, int MAXM, bool SEG, bool AUG> struct Geo3 {
-    static constexpr int BR = TN / 2;                           // B rows per CTA
+    static constexpr int BR = TN / 2;                           // B rows per CTA (N = TN MMA)
     static constexpr int A_PL = AR * KS;                        // 16 KB per plane
     static constexpr int B_PL = BR * KS;
-    static constexpr int STAGE = 3 * (A_PL + B_PL);             // 72 KB (TN 128)
+    // wide layout: B per CTA = X (TN rows of one plane; rank 0: h, rank 1: m — the two halves of the
+    // N = 2 TN operand [B_h | B_m]) + Y / Z (this CTA's half of B_l / B_h, the N = TN operands)
+    static constexpr int B_X = TN * KS;
+    static constexpr int B_Y = BR * KS;
+    static constexpr int STAGE_W = 3 * A_PL + B_X + 2 * B_Y;    // 80 KB (TN 128)
+    static constexpr int STAGE_N = 3 * (A_PL + B_PL);           // 72 KB (TN 128)
     static constexpr int NEPI = 8;
     static constexpr int NET = 32 * NEPI;
     static constexpr int NTHR = 64 + NET;
@@ -118,6 +126,9 @@ template <int TN, int MAXM, bool SEG, bool AUG> struct Geo3 {
     static constexpr int COLB = NPHM * TN * 20;                 // float4 (sigma, n, alpha, beta) + r
     static constexpr int THRB = 3 * 2 * 2 * MAXM * 4;           // [kind][rd/ru][2 MAXM]
     static constexpr int FIXED = 1024 + 1024 + COLB + THRB + HIST;
+    // the wide layout needs two of its stages next to the fixed region (not: segmented MAXM = 64)
+    static constexpr bool WIDE = CIL_G3_WIDE && (227 * 1024 - FIXED) / STAGE_W >= 2;
+    static constexpr int STAGE = WIDE ? STAGE_W : STAGE_N;
     static constexpr int FIT = (227 * 1024 - FIXED) / STAGE;
 #ifdef CIL_G3_MAXSTAGES
     static constexpr int STAGES = FIT > CIL_G3_MAXSTAGES ? CIL_G3_MAXSTAGES : FIT;   // experiment builds only
@@ -136,6 +147,14 @@ __device__ __forceinline__ void mma_i8(uint32_t d, uint64_t a, uint64_t b, uint3
     asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
                  "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
                  "l"(a), "l"(b), "r"(id), "r"(acc));
+}
+// one digit plane (box 128 K-bytes x rows x 1 plane, plane z); both CTAs of the pair signal the leader's barrier
+__device__ __forceinline__ void tma1(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y, int z) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes "
+        "[%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar) & 0xFEFFFFFFu)
+        : "memory");
 }
 // 3-D TMA box (128 K-bytes x rows x 3 digit planes, SWIZZLE_128B); both CTAs of the pair signal the leader's barrier
 __device__ __forceinline__ void tma3(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y) {
@@ -553,7 +572,8 @@ __device__ __forceinline__ void epilogue(const Params& prm, uint32_t tmem_base, 
 
 template <int TN, int MAXM, bool SEG, bool AUG>
 __global__ void __launch_bounds__(Geo3<TN, MAXM, SEG, AUG>::NTHR, 1)
-k_gram3(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mB, Params prm) {
+k_gram3(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mB,
+        const __grid_constant__ CUtensorMap mB2, Params prm) {
     using GG = Geo3<TN, MAXM, SEG, AUG>;
     constexpr int STAGES = GG::STAGES;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -582,6 +602,7 @@ k_gram3(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensor
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&mA) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&mB) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&mB2) : "memory");
     }
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -604,7 +625,7 @@ k_gram3(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensor
                 int mt, nt;
                 tile_of(prm, t % prm.tiles_act, mt, nt);
                 const int ya = (int)(prm.a_off + p * prm.rowsA + (int64_t)mt * TILE_M + rank * AR);
-                const int yb = (int)(prm.b_off + p * prm.rowsB + (int64_t)nt * TN + rank * GG::BR);
+                const int yb = (int)(prm.b_off + p * prm.rowsB + (int64_t)nt * TN + (GG::WIDE ? 0 : rank * GG::BR));
                 for (int kb = 0; kb < n_kb; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     unsigned char* st = stages + stage * GG::STAGE;
@@ -613,7 +634,14 @@ k_gram3(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensor
                     } else {
                         if (rank == 0) mbar_expect_tx(&full[stage], 2 * GG::STAGE);
                         tma3(st, &mA, &full[stage], kb * KS, ya);
-                        tma3(st + 3 * GG::A_PL, &mB, &full[stage], kb * KS, yb);
+                        if constexpr (GG::WIDE) {
+                            unsigned char* sbp = st + 3 * GG::A_PL;
+                            tma1(sbp, &mB, &full[stage], kb * KS, yb, (int)rank);                            // X: h | m
+                            tma1(sbp + GG::B_X, &mB2, &full[stage], kb * KS, yb + (int)rank * GG::BR, 2);       // Y: l
+                            tma1(sbp + GG::B_X + GG::B_Y, &mB2, &full[stage], kb * KS, yb + (int)rank * GG::BR, 0);  // Z: h
+                        } else {
+                            tma3(st + 3 * GG::A_PL, &mB, &full[stage], kb * KS, yb);
+                        }
                     }
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
@@ -622,6 +650,8 @@ k_gram3(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensor
     } else if (warp == 1) {
         if (lane == 0 && rank == 0) {
             const uint32_t id = idesc_i8(TILE_M, TN);
+            const uint32_t id2 = idesc_i8(TILE_M, 2 * TN);
+            (void)id2;
             const uint32_t d32 = tmem_base, d24 = tmem_base + TN, d16 = tmem_base + 2 * TN;
             int stage = 0;
             uint32_t phase = 0, tph = 0;
@@ -636,17 +666,34 @@ k_gram3(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensor
                         const uint32_t sa = smem_u32(stages + stage * GG::STAGE);
                         const uint32_t sb = sa + 3 * GG::A_PL;
                         const uint64_t ah = tc::sdesc(sa), am = tc::sdesc(sa + GG::A_PL), al = tc::sdesc(sa + 2 * GG::A_PL);
-                        const uint64_t bh = tc::sdesc(sb), bm = tc::sdesc(sb + GG::B_PL), bl = tc::sdesc(sb + 2 * GG::B_PL);
+                        if constexpr (GG::WIDE) {
+                            // [H | X] = A_h [B_h | B_m]; L = A_h B_l; [X | L] += A_m [B_h | B_m]; L += A_l B_h:
+                            // the six digit products in four MMAs, A_h read twice instead of three times
+                            const uint64_t bx = tc::sdesc(sb), by = tc::sdesc(sb + GG::B_X),
+                                           bz = tc::sdesc(sb + GG::B_X + GG::B_Y);
 #pragma unroll
-                        for (int k = 0; k < KS / 32; ++k) {          // 32 int8 of K per MMA
-                            const uint64_t adv = (uint64_t)(k * 2);  // +32 B in the start-address field
-                            const uint32_t acc = (kb != kb0 || k != 0) ? 1u : 0u;
-                            mma_i8(d32, ah + adv, bh + adv, id, acc);
-                            mma_i8(d24, ah + adv, bm + adv, id, acc);
-                            mma_i8(d24, am + adv, bh + adv, id, 1u);
-                            mma_i8(d16, ah + adv, bl + adv, id, acc);
-                            mma_i8(d16, am + adv, bm + adv, id, 1u);
-                            mma_i8(d16, al + adv, bh + adv, id, 1u);
+                            for (int k = 0; k < KS / 32; ++k) {          // 32 int8 of K per MMA
+                                const uint64_t adv = (uint64_t)(k * 2);  // +32 B in the start-address field
+                                const uint32_t acc = (kb != kb0 || k != 0) ? 1u : 0u;
+                                mma_i8(d32, ah + adv, bx + adv, id2, acc);
+                                mma_i8(d16, ah + adv, by + adv, id, acc);
+                                mma_i8(d24, am + adv, bx + adv, id2, 1u);
+                                mma_i8(d16, al + adv, bz + adv, id, 1u);
+                            }
+                        } else {
+                            const uint64_t bh = tc::sdesc(sb), bm = tc::sdesc(sb + GG::B_PL),
+                                           bl = tc::sdesc(sb + 2 * GG::B_PL);
+#pragma unroll
+                            for (int k = 0; k < KS / 32; ++k) {          // 32 int8 of K per MMA
+                                const uint64_t adv = (uint64_t)(k * 2);  // +32 B in the start-address field
+                                const uint32_t acc = (kb != kb0 || k != 0) ? 1u : 0u;
+                                mma_i8(d32, ah + adv, bh + adv, id, acc);
+                                mma_i8(d24, ah + adv, bm + adv, id, acc);
+                                mma_i8(d24, am + adv, bh + adv, id, 1u);
+                                mma_i8(d16, ah + adv, bl + adv, id, acc);
+                                mma_i8(d16, am + adv, bm + adv, id, 1u);
+                                mma_i8(d16, al + adv, bh + adv, id, 1u);
+                            }
                         }
                         tc::mma_commit<2>(&empty[stage]);
                         if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -1219,7 +1266,7 @@ typedef CUresult (*PFN_encodeTiled_g3)(CUtensorMap*, CUtensorMapDataType, cuuint
                                        CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
 // 3-D map over the digit planes [3][rows_tot][Kp] (u8): box 128 x box_rows x 3, SWIZZLE_128B
-static bool make_map3(CUtensorMap* m, const void* base, int64_t rows_tot, int64_t Kp, int box_rows) {
+static bool make_map3(CUtensorMap* m, const void* base, int64_t rows_tot, int64_t Kp, int box_rows, int box_planes = 3) {
     static PFN_encodeTiled_g3 enc = nullptr;
     if (!enc) {
         void* p = nullptr;
@@ -1231,7 +1278,7 @@ static bool make_map3(CUtensorMap* m, const void* base, int64_t rows_tot, int64_
     }
     cuuint64_t dims[3] = {(cuuint64_t)Kp, (cuuint64_t)rows_tot, 3};
     cuuint64_t strides[2] = {(cuuint64_t)Kp, (cuuint64_t)(rows_tot * Kp)};
-    cuuint32_t box[3] = {(cuuint32_t)g3::KS, (cuuint32_t)box_rows, 3u};
+    cuuint32_t box[3] = {(cuuint32_t)g3::KS, (cuuint32_t)box_rows, (cuuint32_t)box_planes};
     cuuint32_t es[3] = {1, 1, 1};
     return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(base), dims, strides, box, es,
                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -1258,7 +1305,9 @@ static cudaError_t launch_g3_t(const g3::Params& prm, const CUtensorMap* maps, i
     cfg.attrs = at;
     cfg.numAttrs = 1;
     ProfScope ps_(K_GRAM_TC, st);
-    cudaError_t e = cudaLaunchKernelEx(&cfg, g3::k_gram3<TN, MAXM, SEG, AUG>, maps[0], maps[1], prm);
+    // maps: [0] A (3 planes), [1] B (3 planes x TN/2 rows), [2] B (1 plane x TN rows), [3] B (1 plane x TN/2)
+    cudaError_t e = GG::WIDE ? cudaLaunchKernelEx(&cfg, g3::k_gram3<TN, MAXM, SEG, AUG>, maps[0], maps[2], maps[3], prm)
+                             : cudaLaunchKernelEx(&cfg, g3::k_gram3<TN, MAXM, SEG, AUG>, maps[0], maps[1], maps[1], prm);
     note_launch();
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
@@ -1286,8 +1335,9 @@ cudaError_t launch_gram3(const G3Args& a, cudaStream_t st) {
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     const int tn = a.tn_force == 64 ? 64 : 128;
     if (tn == 64 && (a.skip != 0 || a.nph != 1)) return cudaErrorInvalidValue;
-    CUtensorMap maps[2];
-    if (!make_map3(&maps[0], a.planes, a.rows_tot, a.Kp, g3::AR) || !make_map3(&maps[1], a.planes, a.rows_tot, a.Kp, tn / 2))
+    CUtensorMap maps[4];
+    if (!make_map3(&maps[0], a.planes, a.rows_tot, a.Kp, g3::AR) || !make_map3(&maps[1], a.planes, a.rows_tot, a.Kp, tn / 2) ||
+        !make_map3(&maps[2], a.planes, a.rows_tot, a.Kp, tn, 1) || !make_map3(&maps[3], a.planes, a.rows_tot, a.Kp, tn / 2, 1))
         return cudaErrorInvalidValue;
     g3::Params prm{};
     prm.rowsA = a.rowsA; prm.rowsB = a.rowsB; prm.a_off = a.a_off; prm.b_off = a.b_off;
