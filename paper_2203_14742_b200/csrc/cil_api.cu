@@ -6,8 +6,6 @@
 #include <stdlib.h>
 #include <string.h>
 
-#include <mutex>
-
 #include "cil_internal.cuh"
 
 #include <nvtx3/nvToolsExt.h>
@@ -27,15 +25,22 @@ void note_launch(int n) { t_launches += n; }
 // with the tensor-core family (default on)
 static thread_local bool t_concurrent = true;
 
-// One library-owned side stream per device (non-blocking), for the concurrent engines.
+// One library-owned side stream per host thread and device (non-blocking), for the concurrent engines:
+// per thread, so one thread capturing a CUDA graph never shares a side stream with another thread's
+// work (a captured stream must not receive uncaptured work).  Destroyed at thread exit.
+struct SideStreams {
+    cudaStream_t s[64] = {};
+    ~SideStreams() {
+        for (cudaStream_t& x : s)
+            if (x) cudaStreamDestroy(x);
+    }
+};
 static cudaStream_t side_stream() {
-    static std::mutex mu;
-    static cudaStream_t s[64] = {};
+    static thread_local SideStreams t;
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
-    std::lock_guard<std::mutex> g(mu);
-    if (!s[dev] && cudaStreamCreateWithFlags(&s[dev], cudaStreamNonBlocking) != cudaSuccess) s[dev] = nullptr;
-    return s[dev];
+    if (!t.s[dev] && cudaStreamCreateWithFlags(&t.s[dev], cudaStreamNonBlocking) != cudaSuccess) t.s[dev] = nullptr;
+    return t.s[dev];
 }
 
 // Fork / join of the side stream around the engines (event-ordered, so it is CUDA-graph capturable:

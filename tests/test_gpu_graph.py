@@ -105,3 +105,44 @@ def test_synth_boot_graph_replay(cil):
     call()
     torch.cuda.synchronize()
     assert torch.equal(replayed, out) and not torch.equal(replayed, eager)
+
+
+def test_features_graph_replay_concurrent_engines(cil):
+    """All six measures under AUTO: the max family's engine runs on the library's side stream,
+    forked from and joined into the captured stream by events — the capture must contain it, and
+    replays must equal eager calls bit for bit."""
+    from oracle import oracle as O
+    dev = torch.device("cuda")
+    grid = (2, 24, 24, 0.0)
+    P, N, Nt, M = 2, 200, 180, 8
+    sets = [(cilgen.make_set(91, 2 * i, N, grid[:3]), cilgen.make_set(91, 2 * i + 1, Nt, grid[:3])) for i in range(2 * P)]
+    D = O.distance_matrix(sets[0][0][:40].numpy(), sets[0][1][:40].numpy(), grid, 0x3F)
+    radii = torch.tensor(np.stack([np.quantile(d[d > 0], np.linspace(0.97, 0.03, M)) for d in D]), device=dev)
+    A = torch.stack([s[0] for s in sets[:P]]).to(dev)
+    B = torch.stack([s[1] for s in sets[:P]]).to(dev)
+    ws = cil.Workspace()
+    counts = torch.empty((P, 6, M), dtype=torch.int64, device=dev)
+    y = torch.empty((P, 6, M), dtype=torch.float64, device=dev)
+    st = torch.empty((P,), dtype=torch.int32, device=dev)
+    kw = dict(engine=cil.ENGINE_AUTO, ws=ws, counts=counts, y=y, status=st)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        cil.features(A, B, grid, cil.ALL, radii, **kw)
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        cil.features(A, B, grid, cil.ALL, radii, **kw)
+    for rnd in range(2):
+        src = sets[rnd * P:(rnd + 1) * P]
+        A.copy_(torch.stack([x[0] for x in src]).to(dev))
+        B.copy_(torch.stack([x[1] for x in src]).to(dev))
+        counts.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        c_graph, s_graph = counts.clone(), st.clone()
+        c_eager, _, s_eager = cil.features(A, B, grid, cil.ALL, radii, engine=cil.ENGINE_AUTO)
+        torch.cuda.synchronize()
+        assert torch.equal(c_graph, c_eager) and torch.equal(s_graph, s_eager)
+        assert int(c_graph[:, 1].sum()) > 0 and int(c_graph[:, 0].sum()) > 0     # both families counted
