@@ -2,9 +2,9 @@
 // PAPER.md:182-190) on the CUDA cores' integer pipes, fused with radius binning (Eq. (1)).
 //
 // The three max sub-norms m_al = max_e |D_al (a - b)_e| (al in {value, D_x, D_y}) are computed on
-// 15-bit fixed-point copies of the operands: per item and region one scale s_al = max|v| / 16000
-// over both panels (A and B must share it): centre c_al = (max v + min v) / 2, half range r_al,
-// s_al = r_al / 16000, q = rint((v - c_al) / s_al) in [-16000, 16000] (a - b does not see c_al; the
+// 15-bit fixed-point copies of the operands: per item and region one scale over both panels (A and
+// B must share it): centre c_al = (max v + min v) / 2, half range r_al, s_al = r_al / 16383,
+// q = rint((v - c_al) / s_al) in [-16383, 16383] (a - b does not see c_al; the
 // differences of the derivative regions are formed in FP64 first, so q is within 0.5 + 1e-11 of
 // (v - c_al) / s_al of the EXACT v).  Then for one pair
 //     |s_al * max_e |q_a - q_b| - m_al| <= (1 + 1e-9) s_al      (max is 1-Lipschitz in the sup norm)
@@ -18,8 +18,8 @@
 //
 // Kernels: k_max16_reg, CTA = 128 threads = 64 A rows x 64 B rows x one region, 8 x 4 pairs per
 // thread; k_max16_bin, the binning epilogue over the per-pair region maxima.  Operands are stored
-// biased, A as q + 16384 and B as -q + 16384 (both in [384, 32384]), so ONE 32-bit integer add of two
-// packed words gives both 16-bit lanes t = q_a - q_b + 32768 in [768, 64768] with no carry between
+// biased, A as q + 16384 and B as -q + 16384 (both in [1, 32767]), so ONE 32-bit integer add of two
+// packed words gives both 16-bit lanes t = q_a - q_b + 32768 in [2, 65534] with no carry between
 // the lanes — issued as IMAD on the FMA pipe, which leaves the integer ALU pipe to the
 // VIMNMX3.U16x2 running max / min of t (max |a - b| = max(max t, -min t + 65536) - 32768); an
 // all-ALU VIADD.16x2 form ran at ~0.7 of this (tools/maxmix3_bench.cu).  k-chunks of 64 elements (128 B per row) double-buffered in shared
@@ -36,7 +36,7 @@ constexpr int NP = RI * 4;           // pairs per thread
 constexpr int NTHR = 128;
 constexpr int BKW = kMax16BK / 2;    // 32-bit words per row per chunk
 constexpr int LDW = BKW + 4;         // padded row stride (words)
-constexpr double kQ = 16000.0;       // |q| <= 16000: a - b stays inside int16
+constexpr double kQ = 16383.0;       // |q| <= 16383: q + 16384 in [1, 32767], t = q_a - q_b + 32768 in [2, 65534]
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
     const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
