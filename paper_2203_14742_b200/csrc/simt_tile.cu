@@ -271,9 +271,6 @@ __global__ void __launch_bounds__(NTHR, (CIL_SIMT_EXP == 1 && !DO_SUM) ? 3 : (DO
                     default: d = m0 + mxx + myy; E = em0 + emx + emy; break;
                 }
                 E += 1e-14 * d;                  // FP64 evaluation of d and of the bound
-#ifdef CIL_SIMT_NOBOUND
-                E = 0.0;                         // timing experiment builds only (tools/simt_ab.sh)
-#endif
                 if (a.range) {               // distance-range mode (adaptive radii)
                     unsigned long long* rg = a.range + ((int64_t)p * nq + q) * 2;
                     if (d > 0.0) atomicMin(&rg[0], (unsigned long long)__double_as_longlong(d));
