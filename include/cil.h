@@ -23,9 +23,12 @@
  *  - Patterns are FP32, one pattern = S species x H rows x W columns, row-major
  *    [S][H][W] ("pattern-major then component-major then row-major");
  *    K = S*H*W, pattern p of a set starts at base + p*ld (ld >= K, in floats).
+ *  - Batched calls take 1 <= P <= 21845 items (the grids put items on a 65535-wide grid
+ *    axis, three per item for the max family); more is CIL_EINVAL.  Split larger batches.
  *  - Thread-safe: no global mutable state besides a once-per-device kernel
- *    attribute setup (atomic), a thread-local launch counter and the opt-in
- *    profiling diagnostics (cil_prof_*).
+ *    attribute setup (atomic), thread-local launch counters / diagnostics settings, one
+ *    library-owned side stream per host thread and device (the concurrent engines; created
+ *    on first use), and the opt-in profiling diagnostics (cil_prof_*).
  */
 #ifndef CIL_H
 #define CIL_H

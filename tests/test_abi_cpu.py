@@ -109,3 +109,11 @@ def test_chi2_quantile_host(capi):
     # Pearson statistic validation (no device work on invalid arguments)
     assert capi.lib.cil_gaussianity_pearson(10, None, 3, 10, None, None) != 0
     assert capi.lib.cil_gaussianity_pearson(10, 8, 3, 65, 8, None) != 0
+
+
+def test_item_count_limit(capi):
+    """Batched calls take at most 21845 items (grid axis limit, three per item for the max family):
+    the workspace query refuses more (0) instead of a launch failure later."""
+    g = capi.Grid(2, 8, 8, 0.0)
+    assert capi.lib.cil_features_workspace_size(21845, 10, 10, g, 1, 5, 0) > 0
+    assert capi.lib.cil_features_workspace_size(21846, 10, 10, g, 1, 5, 0) == 0
