@@ -61,6 +61,15 @@ struct Fork {
         joined = false;
     }
     cudaStream_t side() const { return aux ? aux : main; }
+    // work enqueued on the side stream from now on starts only after the main stream's work so far
+    void side_after_main() {
+        if (joined) return;
+        cudaEvent_t e;
+        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return;
+        cudaEventRecord(e, main);
+        cudaStreamWaitEvent(aux, e, 0);
+        cudaEventDestroy(e);
+    }
     void join() {
         if (joined) return;
         joined = true;
@@ -434,6 +443,12 @@ cil_status run_engines(int P, const RowSrc& asrc, const RowSrc& bsrc, int64_t ro
     // The max family's integer-pipe engine and the tensor-core family use different pipes and fit on
     // one SM together (one Gram CTA + one k_max16_reg CTA): with both, the former runs on a side stream.
     Fork fk(st, t_concurrent && pl.simt_mask && pl.max16 && pl.tc && range == nullptr && diag == nullptr);
+    // With the concurrent engines the max family's tile kernels are enqueued after the INT8 Gram and
+    // start only once the Gram's operands are packed: the Gram's CTAs (186 KB of shared memory each)
+    // must be resident first — were the max family's CTAs there first, they would fill every SM and
+    // keep the Gram out until the end (measured: C5 Gram overlapped by only ~10 %).
+    Max16Args m16{};
+    bool m16_pending = false;
     if (pl.simt_mask && pl.max16) {
         // max family alone: 15-bit fixed point on the integer pipes (never in distance-range mode,
         // whose plans use the SIMT engine)
@@ -464,7 +479,12 @@ cil_status run_engines(int P, const RowSrc& asrc, const RowSrc& bsrc, int64_t ro
         a.tri = tile_skip == 2;
         a.sym = binout != nullptr && b_same;
         a.list = list; a.ctr = ctr; a.cap = cap;
-        CIL_CU(launch_max16(a, sm));
+        if (!fk.joined && pl.tc && pl.split == 3) {
+            m16 = a;
+            m16_pending = true;
+        } else {
+            CIL_CU(launch_max16(a, sm));
+        }
     } else if (pl.simt_mask) {
         float* aug = at<float>(ws, L.off_aug);
         float* augB = aug + (size_t)P * rowsA * L.geom.off[3];
@@ -544,7 +564,12 @@ cil_status run_engines(int P, const RowSrc& asrc, const RowSrc& bsrc, int64_t ro
             t.skip = (binout && b_same) ? 1 : (b_same ? tile_skip : 0);
             t.diag = diag;
             t.hist_elems = L.hist_elems;
+            if (m16_pending) fk.side_after_main();          // the Gram's operands are packed
             CIL_CU(launch_gram3(t, st));
+            if (m16_pending) {
+                m16_pending = false;
+                CIL_CU(launch_max16(m16, fk.side()));
+            }
         } else {
             // ---- 3xBF16 / 3xTF32 split engine (histogram mode only)
             if (binout) return CIL_EUNSUPPORTED;
@@ -580,6 +605,7 @@ cil_status run_engines(int P, const RowSrc& asrc, const RowSrc& bsrc, int64_t ro
             CIL_CU(launch_gram_tc(t, st));
         }
     }
+    if (m16_pending) CIL_CU(launch_max16(m16, fk.side()));   // (not reached: the INT8 path launches it)
     fk.join();
     if (diag || range) return CIL_OK;
     if (L.list_cap) {
