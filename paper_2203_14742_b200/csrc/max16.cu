@@ -12,18 +12,19 @@
 // re-check (recheck.cu) when a radius lies in (d - E, d + E], so the counts are those of the plain
 // definition.  For the paper's workloads the band is ~1e-4 d wide (re-check fraction in DESIGN.md).
 //
-// Why: FP32 |a - b| max costs FADD2 + FMNMX3 per two element-pairs on the FP32 pipes (57 element-
-// pairs per SM-cycle measured, profiles/r02_maxmix.txt); packed 16-bit VIADD.16x2 + VIMNMX3.S16x2
-// max / min run at 105 (tools/maxmix2_bench.cu), and the operands are half the bytes.
+// Why: FP32 |a - b| max costs FADD2 + FMNMX3 per two element-pairs and is bound by the FP32
+// subtraction rate (57 element-pairs per SM-cycle measured, profiles/r02_maxmix.txt); this mix
+// reaches 89-91 per SM-cycle register-only (tools/maxmix3_bench.cu, cil_diag_alu_ceiling(3)), and
+// the operands are half the bytes.
 //
 // Kernels: k_max16_reg, CTA = 128 threads = 64 A rows x 64 B rows x one region, 8 x 4 pairs per
 // thread; k_max16_bin, the binning epilogue over the per-pair region maxima.  Operands are stored
 // biased, A as q + 16384 and B as -q + 16384 (both in [1, 32767]), so ONE 32-bit integer add of two
 // packed words gives both 16-bit lanes t = q_a - q_b + 32768 in [2, 65534] with no carry between
 // the lanes — issued as IMAD on the FMA pipe, which leaves the integer ALU pipe to the
-// VIMNMX3.U16x2 running max / min of t (max |a - b| = max(max t, -min t + 65536) - 32768); an
-// all-ALU VIADD.16x2 form ran at ~0.7 of this (tools/maxmix3_bench.cu).  k-chunks of 64 elements (128 B per row) double-buffered in shared
-// memory with cp.async (rows padded to 144 B -> conflict-free LDS.128).
+// VIMNMX3.U16x2 running max / min of t (max |q_a - q_b| = max(max t - 32768, 32768 - min t)); an
+// all-ALU VIADD.16x2 form ran at ~0.7 of this.  k-chunks of 64 elements (128 B per row) double-
+// buffered in shared memory with cp.async (rows padded to 144 B -> conflict-free LDS.128).
 #include "cil_internal.cuh"
 
 namespace cil {
