@@ -35,10 +35,13 @@ namespace {
 // CTA keeps 3 x 2 x 8 KB of its pair's rows in flight while it computes, 4 CTAs per SM (2 CTAs with
 // 3 x 2 x 16 KB: slower; profiles/r02_recheck.txt)
 constexpr uint32_t RCH = 2048;
+constexpr uint32_t RHALO = 256;      // each chunk also brings the next grid row (W <= RHALO): every x / y
+                                     // neighbour of the chunk is in shared memory, the sweeps are branch-free
+constexpr uint32_t RSTR = RCH + RHALO;
 constexpr int RST = 3;
-constexpr size_t kRingBytes = sizeof(float) * 2 * RCH * RST;
+constexpr size_t kRingBytes = sizeof(float) * 2 * RSTR * RST;
 struct Ring {
-    float* buf;        // [RST][2][RCH] (x chunk, y chunk)
+    float* buf;        // [RST][2][RSTR] (x chunk + halo, y chunk + halo)
     uint64_t* bar;     // [RST]
     uint32_t g;        // chunks streamed so far by this CTA (stage = g % RST, parity = (g / RST) & 1)
 };
@@ -48,30 +51,35 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                  "l"(src), "r"(bytes), "r"(tc::smem_u32(bar))
                  : "memory");
 }
+// chunk [e0, e0 + len) plus the halo [e0 + len, e0 + len + min(halo, K - e0 - len))
 __device__ __forceinline__ void ring_issue(Ring& r, uint32_t gi, const float* x, const float* y, uint32_t e0,
-                                           uint32_t len) {
+                                           uint32_t len, uint32_t K, uint32_t halo) {
     const int st = (int)(gi % RST);
-    float* dx = r.buf + (size_t)st * 2 * RCH;
+    float* dx = r.buf + (size_t)st * 2 * RSTR;
+    const uint32_t n = len + min(halo, K - e0 - len);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // the stage's generic reads are done
-    tc::mbar_expect_tx(&r.bar[st], 8u * len);
-    bulk_g2s(dx, x + e0, 4u * len, &r.bar[st]);
-    bulk_g2s(dx + RCH, y + e0, 4u * len, &r.bar[st]);
+    tc::mbar_expect_tx(&r.bar[st], 8u * n);
+    bulk_g2s(dx, x + e0, 4u * n, &r.bar[st]);
+    bulk_g2s(dx + RSTR, y + e0, 4u * n, &r.bar[st]);
 }
-// Streams the K elements of x and y (16-B aligned, K % 4 == 0) through the ring; all threads call
-// f(base, sx, sy, len) once per chunk (elements [base, base + len)).
+// Streams the K elements of x and y (16-B aligned, K % 4 == 0) through the ring, each chunk with a
+// halo of `halo` (<= RHALO, % 4 == 0) further elements; all threads call f(base, sx, sy, len) once per
+// chunk (elements [base, base + len), sx / sy valid up to base + len + halo where the pattern has them;
+// reads up to RSTR stay inside the stage).
 template <class F>
-__device__ void ring_stream(Ring& r, const float* x, const float* y, uint32_t K, F f) {
+__device__ void ring_stream(Ring& r, const float* x, const float* y, uint32_t K, uint32_t halo, F f) {
     const uint32_t nch = (K + RCH - 1) / RCH, g0 = r.g;
     if (threadIdx.x == 0)
-        for (uint32_t c = 0; c < nch && c < (uint32_t)RST; ++c) ring_issue(r, g0 + c, x, y, c * RCH, min(RCH, K - c * RCH));
+        for (uint32_t c = 0; c < nch && c < (uint32_t)RST; ++c)
+            ring_issue(r, g0 + c, x, y, c * RCH, min(RCH, K - c * RCH), K, halo);
     for (uint32_t c = 0; c < nch; ++c) {
         const uint32_t gi = g0 + c, st = gi % RST;
         tc::mbar_wait(&r.bar[st], (gi / RST) & 1u);
-        const float* sx = r.buf + (size_t)st * 2 * RCH;
-        f(c * RCH, sx, sx + RCH, min(RCH, K - c * RCH));
+        const float* sx = r.buf + (size_t)st * 2 * RSTR;
+        f(c * RCH, sx, sx + RSTR, min(RCH, K - c * RCH));
         __syncthreads();                                   // every thread is done with the stage
         if (threadIdx.x == 0 && c + RST < nch)
-            ring_issue(r, gi + RST, x, y, (c + RST) * RCH, min(RCH, K - (c + RST) * RCH));
+            ring_issue(r, gi + RST, x, y, (c + RST) * RCH, min(RCH, K - (c + RST) * RCH), K, halo);
     }
     r.g = g0 + nch;
 }
@@ -84,10 +92,10 @@ __device__ void exact_subnorms(const float* x, const float* y, const RecheckArgs
                                double (*red)[8], Ring* ring = nullptr) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     double v[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-    if (full && ring != nullptr && (a.W & 3) == 0 && a.K < (1ll << 31)) {
+    if (full && ring != nullptr && (a.W & 3) == 0 && (uint32_t)a.W <= RHALO && a.K < (1ll << 31)) {
         const uint32_t W = (uint32_t)a.W, H = (uint32_t)a.H;
         const FastDiv fw(W), fh(H);
-        ring_stream(*ring, x, y, (uint32_t)a.K, [&](uint32_t base, const float* sx, const float* sy, uint32_t len) {
+        ring_stream(*ring, x, y, (uint32_t)a.K, W, [&](uint32_t base, const float* sx, const float* sy, uint32_t len) {
 #pragma unroll
             for (int t = 0; t < (int)(RCH / 1024); ++t) {
                 const uint32_t l = t * 1024 + threadIdx.x * 4, e = base + l;
@@ -99,31 +107,23 @@ __device__ void exact_subnorms(const float* x, const float* y, const RecheckArgs
                 v[3] = fmax(v[3], fmax(fmax(fabs(u0), fabs(u1)), fmax(fabs(u2), fabs(u3))));
                 uint32_t c, hr;
                 const uint32_t sr = fw.div(e, c), sp = fh.div(sr, hr);
-                if (!(a.gs == 0 || ((a.gs >> sp) & 1u))) continue;
+                const bool g = a.gs == 0 || ((a.gs >> sp) & 1u);
+                // neighbours from the stage (chunk + halo); masked where the pattern has none
                 const double d0 = u1 - u0, d1 = u2 - u1, d2 = u3 - u2;
-                v[1] += d0 * d0 + d1 * d1 + d2 * d2;
-                v[4] = fmax(v[4], fmax(fmax(fabs(d0), fabs(d1)), fabs(d2)));
-                if (c + 4 < W) {
-                    const double un = l + 4 < len ? (double)sx[l + 4] - (double)sy[l + 4]
-                                                  : (double)__ldg(x + e + 4) - (double)__ldg(y + e + 4);
-                    const double d3 = un - u3;
-                    v[1] += d3 * d3;
-                    v[4] = fmax(v[4], fabs(d3));
+                const double d3 = c + 4 < W ? ((double)sx[l + 4] - (double)sy[l + 4]) - u3 : 0.0;
+                const float4 xd = *reinterpret_cast<const float4*>(sx + l + W);
+                const float4 yd = *reinterpret_cast<const float4*>(sy + l + W);
+                const bool gy = g && hr + 1 < H;
+                const double e0 = gy ? ((double)xd.x - (double)yd.x) - u0 : 0.0;
+                const double e1 = gy ? ((double)xd.y - (double)yd.y) - u1 : 0.0;
+                const double e2 = gy ? ((double)xd.z - (double)yd.z) - u2 : 0.0;
+                const double e3 = gy ? ((double)xd.w - (double)yd.w) - u3 : 0.0;
+                if (g) {
+                    v[1] += d0 * d0 + d1 * d1 + d2 * d2 + d3 * d3;
+                    v[4] = fmax(v[4], fmax(fmax(fabs(d0), fabs(d1)), fmax(fabs(d2), fabs(d3))));
                 }
-                if (hr + 1 < H) {
-                    float4 xd, yd;
-                    if (l + W < len) {
-                        xd = *reinterpret_cast<const float4*>(sx + l + W);
-                        yd = *reinterpret_cast<const float4*>(sy + l + W);
-                    } else {
-                        xd = __ldg(reinterpret_cast<const float4*>(x + e + W));
-                        yd = __ldg(reinterpret_cast<const float4*>(y + e + W));
-                    }
-                    const double e0 = ((double)xd.x - (double)yd.x) - u0, e1 = ((double)xd.y - (double)yd.y) - u1;
-                    const double e2 = ((double)xd.z - (double)yd.z) - u2, e3 = ((double)xd.w - (double)yd.w) - u3;
-                    v[2] += e0 * e0 + e1 * e1 + e2 * e2 + e3 * e3;
-                    v[5] = fmax(v[5], fmax(fmax(fabs(e0), fabs(e1)), fmax(fabs(e2), fabs(e3))));
-                }
+                v[2] += e0 * e0 + e1 * e1 + e2 * e2 + e3 * e3;
+                v[5] = fmax(v[5], fmax(fmax(fabs(e0), fabs(e1)), fmax(fabs(e2), fabs(e3))));
             }
         });
     } else if (!full) {
@@ -217,10 +217,10 @@ __device__ void max_subnorms32(const float* x, const float* y, const RecheckArgs
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     float v[3] = {0.f, 0.f, 0.f};
     const int W = a.W, H = a.H;
-    if ((W & 3) == 0 && ring != nullptr) {
+    if ((W & 3) == 0 && W <= (int)RHALO && ring != nullptr) {
         const uint32_t Wu = (uint32_t)W, Hu = (uint32_t)H;
         const FastDiv fw(Wu), fh(Hu);
-        ring_stream(*ring, x, y, (uint32_t)a.K, [&](uint32_t base, const float* sx, const float* sy, uint32_t len) {
+        ring_stream(*ring, x, y, (uint32_t)a.K, Wu, [&](uint32_t base, const float* sx, const float* sy, uint32_t len) {
 #pragma unroll
             for (int t = 0; t < (int)(RCH / 1024); ++t) {
                 const uint32_t l = t * 1024 + threadIdx.x * 4, e = base + l;
@@ -230,24 +230,17 @@ __device__ void max_subnorms32(const float* x, const float* y, const RecheckArgs
                 v[0] = amax4(v[0], u.x, u.y, u.z, u.w);
                 uint32_t c, hr;
                 const uint32_t sr = fw.div(e, c), sp = fh.div(sr, hr);
-                if (!(a.gs == 0 || ((a.gs >> sp) & 1u))) continue;
-                v[1] = fmaxf(v[1], fmaxf(fabsf(u.y - u.x), fmaxf(fabsf(u.z - u.y), fabsf(u.w - u.z))));
-                if (c + 4 < Wu) {
-                    const float nx = l + 4 < len ? sx[l + 4] - sy[l + 4] : __ldg(x + e + 4) - __ldg(y + e + 4);
-                    v[1] = fmaxf(v[1], fabsf(nx - u.w));
-                }
-                if (hr + 1 < Hu) {
-                    float4 xd, yd;
-                    if (l + Wu < len) {
-                        xd = *reinterpret_cast<const float4*>(sx + l + Wu);
-                        yd = *reinterpret_cast<const float4*>(sy + l + Wu);
-                    } else {
-                        xd = __ldg(reinterpret_cast<const float4*>(x + e + Wu));
-                        yd = __ldg(reinterpret_cast<const float4*>(y + e + Wu));
-                    }
-                    v[2] = amax4(v[2], (xd.x - yd.x) - u.x, (xd.y - yd.y) - u.y, (xd.z - yd.z) - u.z,
-                                 (xd.w - yd.w) - u.w);
-                }
+                const bool g = a.gs == 0 || ((a.gs >> sp) & 1u);
+                // neighbours from the stage (chunk + halo); masked where the pattern has none
+                const float nx = (sx[l + 4] - sy[l + 4]) - u.w;
+                const float4 xd = *reinterpret_cast<const float4*>(sx + l + Wu);
+                const float4 yd = *reinterpret_cast<const float4*>(sy + l + Wu);
+                float dxm = fmaxf(fabsf(u.y - u.x), fmaxf(fabsf(u.z - u.y), fabsf(u.w - u.z)));
+                dxm = c + 4 < Wu ? fmaxf(dxm, fabsf(nx)) : dxm;
+                const float dym = amax4(0.f, (xd.x - yd.x) - u.x, (xd.y - yd.y) - u.y, (xd.z - yd.z) - u.z,
+                                        (xd.w - yd.w) - u.w);
+                v[1] = g ? fmaxf(v[1], dxm) : v[1];
+                v[2] = (g && hr + 1 < Hu) ? fmaxf(v[2], dym) : v[2];
             }
         });
     } else {
