@@ -101,7 +101,38 @@ __global__ void __launch_bounds__(256) k_range16(RowSrc src, int64_t rows, AugGe
     double hx = -INFINITY, lx = INFINITY, hy = -INFINITY, ly = INFINITY;
     const int W = g.W, H = g.H, SH = g.S * g.H;
     const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
-    if (g.nreg >= 2) {
+    if (g.nreg >= 2 && (W & 3) == 0 && g.K < (1ll << 31)) {
+        // flat float4 sweep: 4 elements of one grid row per thread, the x neighbour of the 4th from
+        // the next lane (lane 31: a load), the y neighbours one grid row on (an L1 / L2 hit)
+        const uint32_t K = (uint32_t)g.K, Wu = (uint32_t)W, Hu = (uint32_t)H;
+        const FastDiv fw(Wu), fh(Hu);
+        for (uint32_t base = 0; base < K; base += 1024) {
+            const uint32_t e = base + threadIdx.x * 4;
+            const bool ok = e < K;
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (ok) v = __ldg(reinterpret_cast<const float4*>(x + e));
+            float nxv = __shfl_down_sync(0xffffffffu, v.x, 1);
+            if (!ok) continue;
+            uint32_t c, hr;
+            const uint32_t sr = fw.div(e, c), sp = fh.div(sr, hr);
+            if (!(g.gs == 0 || ((g.gs >> sp) & 1u))) continue;     // species mask (R18): 0 derivatives
+            const double x0 = v.x, x1 = v.y, x2 = v.z, x3 = v.w;
+            hx = fmax(hx, fmax(fmax(x1 - x0, x2 - x1), x3 - x2));
+            lx = fmin(lx, fmin(fmin(x1 - x0, x2 - x1), x3 - x2));
+            if (c + 4 < Wu) {
+                if (ln == 31) nxv = __ldg(x + e + 4);
+                const double d = (double)nxv - x3;
+                hx = fmax(hx, d); lx = fmin(lx, d);
+            }
+            if (g.nreg >= 3 && hr + 1 < Hu) {
+                const float4 vd = __ldg(reinterpret_cast<const float4*>(x + e + Wu));
+                const double d0 = (double)vd.x - x0, d1 = (double)vd.y - x1, d2 = (double)vd.z - x2,
+                             d3 = (double)vd.w - x3;
+                hy = fmax(hy, fmax(fmax(d0, d1), fmax(d2, d3)));
+                ly = fmin(ly, fmin(fmin(d0, d1), fmin(d2, d3)));
+            }
+        }
+    } else if (g.nreg >= 2) {
         for (int sr = w; sr < SH; sr += 8) {
             const int s = sr / H;
             if (!(g.gs == 0 || ((g.gs >> s) & 1u))) continue;     // species mask (R18): 0 derivatives
@@ -171,6 +202,42 @@ __global__ void __launch_bounds__(256) k_pack16(RowSrc src, int64_t rows, AugGeo
     if (g.nreg < 2) return;
     const int W = g.W, H = g.H, SH = g.S * g.H;
     const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
+    if ((W & 3) == 0 && g.K < (1ll << 31)) {
+        // flat float4 sweep (as in k_range16): D_x rows are W - 1 long (scalar 2-byte stores), D_y
+        // rows W long (one 8-byte store per 4 values)
+        const uint32_t K = (uint32_t)g.K, Wu = (uint32_t)W, Hu = (uint32_t)H;
+        const FastDiv fw(Wu), fh(Hu);
+        auto qz = [&](double d, int k) { return (int16_t)(__double2int_rn((d - cen[k]) * inv[k]) + kBias); };
+        for (uint32_t base = 0; base < K; base += 1024) {
+            const uint32_t e = base + threadIdx.x * 4;
+            const bool ok = e < K;
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (ok) v = __ldg(reinterpret_cast<const float4*>(x + e));
+            float nxv = __shfl_down_sync(0xffffffffu, v.x, 1);
+            if (!ok) continue;
+            uint32_t c, hr;
+            const uint32_t sr = fw.div(e, c), sp = fh.div(sr, hr);
+            const bool grad = g.gs == 0 || ((g.gs >> sp) & 1u);
+            const double x0 = v.x, x1 = v.y, x2 = v.z, x3 = v.w;
+            int16_t* ox = o + g.off[1] + (int64_t)sr * (W - 1) + c;
+            ox[0] = qz(grad ? x1 - x0 : 0.0, 1);
+            ox[1] = qz(grad ? x2 - x1 : 0.0, 1);
+            ox[2] = qz(grad ? x3 - x2 : 0.0, 1);
+            if (c + 4 < Wu) {
+                if (ln == 31) nxv = __ldg(x + e + 4);
+                ox[3] = qz(grad ? (double)nxv - x3 : 0.0, 1);
+            }
+            if (g.nreg >= 3 && hr + 1 < Hu) {
+                double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
+                if (grad) {
+                    const float4 vd = __ldg(reinterpret_cast<const float4*>(x + e + Wu));
+                    d0 = (double)vd.x - x0; d1 = (double)vd.y - x1; d2 = (double)vd.z - x2; d3 = (double)vd.w - x3;
+                }
+                *reinterpret_cast<short4*>(o + g.off[2] + (int64_t)(sr - sp) * W + c) =
+                    make_short4(qz(d0, 2), qz(d1, 2), qz(d2, 2), qz(d3, 2));
+            }
+        }
+    } else {
     for (int sr = w; sr < SH; sr += 8) {
         const int s = sr / H;
         const bool grad = g.gs == 0 || ((g.gs >> s) & 1u);
@@ -185,6 +252,7 @@ __global__ void __launch_bounds__(256) k_pack16(RowSrc src, int64_t rows, AugGeo
             if (has_dy)
                 o[g.off[2] + (int64_t)sr * W - (int64_t)s * W + c] = (int16_t)(__double2int_rn((dy - cen[2]) * inv[2]) + kBias);
         }
+    }
     }
     for (int64_t t = g.Kx + threadIdx.x; t < g.off[2] - g.off[1]; t += 256) o[g.off[1] + t] = kBias;
     if (g.nreg >= 3)
