@@ -33,7 +33,6 @@ namespace {
 constexpr int TB = 64;               // B rows per CTA
 constexpr int RI = 8;                // A rows per thread (8 x 4 pairs)
 constexpr int TA = 8 * RI;           // A rows per CTA
-constexpr int NP = RI * 4;           // pairs per thread
 constexpr int NTHR = 128;
 constexpr int BKW = kMax16BK / 2;    // 32-bit words per row per chunk
 constexpr int LDW = BKW + 4;         // padded row stride (words)
