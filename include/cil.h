@@ -27,8 +27,9 @@
  *    axis, three per item for the max family); more is CIL_EINVAL.  Split larger batches.
  *  - Thread-safe: no global mutable state besides a once-per-device kernel
  *    attribute setup (atomic), thread-local launch counters / diagnostics settings, one
- *    library-owned side stream per host thread and device (the concurrent engines; created
- *    on first use), and the opt-in profiling diagnostics (cil_prof_*).
+ *    library-owned side stream (+ two events) per host thread and device for the concurrent
+ *    engines (created on the thread's first call that uses them — make it an eager call, like
+ *    the attribute setup, before capturing graphs), and the opt-in profiling diagnostics.
  */
 #ifndef CIL_H
 #define CIL_H

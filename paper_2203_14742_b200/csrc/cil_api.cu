@@ -28,59 +28,66 @@ void note_launch(int n) { t_launches += n; }
 // with the tensor-core family (default on)
 static thread_local bool t_concurrent = true;
 
-// One library-owned side stream per host thread and device (non-blocking), for the concurrent engines:
-// per thread, so one thread capturing a CUDA graph never shares a side stream with another thread's
-// work (a captured stream must not receive uncaptured work).  Destroyed at thread exit.
+// One library-owned side stream per host thread and device (non-blocking), with its two ordering
+// events, for the concurrent engines: per thread, so one thread capturing a CUDA graph never shares a
+// side stream with another thread's work (a captured stream must not receive uncaptured work).
+// Created on a thread's first call that forks (which, like the kernel attribute setup, should be an
+// eager call), destroyed at thread exit.
 struct SideStreams {
     cudaStream_t s[64] = {};
+    cudaEvent_t fork[64] = {}, join[64] = {};
     ~SideStreams() {
-        for (cudaStream_t& x : s)
-            if (x) cudaStreamDestroy(x);
+        for (int d = 0; d < 64; ++d) {
+            if (s[d]) cudaStreamDestroy(s[d]);
+            if (fork[d]) cudaEventDestroy(fork[d]);
+            if (join[d]) cudaEventDestroy(join[d]);
+        }
     }
 };
-static cudaStream_t side_stream() {
-    static thread_local SideStreams t;
+static thread_local SideStreams t_side;
+static int side_setup() {          // the device index with a ready side stream, or -1
     int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
-    if (!t.s[dev] && cudaStreamCreateWithFlags(&t.s[dev], cudaStreamNonBlocking) != cudaSuccess) t.s[dev] = nullptr;
-    return t.s[dev];
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return -1;
+    if (!t_side.s[dev]) {
+        cudaStream_t st = nullptr;
+        cudaEvent_t f = nullptr, j = nullptr;
+        if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) return -1;
+        if (cudaEventCreateWithFlags(&f, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&j, cudaEventDisableTiming) != cudaSuccess) {
+            cudaStreamDestroy(st);
+            if (f) cudaEventDestroy(f);
+            return -1;
+        }
+        t_side.s[dev] = st; t_side.fork[dev] = f; t_side.join[dev] = j;
+    }
+    return dev;
 }
 
 // Fork / join of the side stream around the engines (event-ordered, so it is CUDA-graph capturable:
 // the side stream joins the capture through the fork event and leaves it through the join).
 struct Fork {
     cudaStream_t main, aux = nullptr;
+    int dev = -1;
     bool joined = true;
     Fork(cudaStream_t m, bool on) : main(m) {
-        if (!on || (aux = side_stream()) == nullptr) return;
-        cudaEvent_t e;
-        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) { aux = nullptr; return; }
-        cudaEventRecord(e, main);
-        cudaStreamWaitEvent(aux, e, 0);
-        cudaEventDestroy(e);
+        if (!on || (dev = side_setup()) < 0) return;
+        aux = t_side.s[dev];
+        cudaEventRecord(t_side.fork[dev], main);
+        cudaStreamWaitEvent(aux, t_side.fork[dev], 0);
         joined = false;
     }
     cudaStream_t side() const { return aux ? aux : main; }
     // work enqueued on the side stream from now on starts only after the main stream's work so far
     void side_after_main() {
         if (joined) return;
-        cudaEvent_t e;
-        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return;
-        cudaEventRecord(e, main);
-        cudaStreamWaitEvent(aux, e, 0);
-        cudaEventDestroy(e);
+        cudaEventRecord(t_side.fork[dev], main);
+        cudaStreamWaitEvent(aux, t_side.fork[dev], 0);
     }
     void join() {
         if (joined) return;
         joined = true;
-        cudaEvent_t e;
-        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
-            cudaStreamSynchronize(aux);                  // cannot order by event: fall back to a host wait
-            return;
-        }
-        cudaEventRecord(e, aux);
-        cudaStreamWaitEvent(main, e, 0);
-        cudaEventDestroy(e);
+        cudaEventRecord(t_side.join[dev], aux);
+        cudaStreamWaitEvent(main, t_side.join[dev], 0);
     }
     ~Fork() { join(); }
 };
