@@ -28,8 +28,8 @@
  *  - Thread-safe: no global mutable state besides a once-per-device kernel
  *    attribute setup (atomic), thread-local launch counters / diagnostics settings, one
  *    library-owned side stream (+ two events) per host thread and device for the concurrent
- *    engines (created on the thread's first call that uses them — make it an eager call, like
- *    the attribute setup, before capturing graphs), and the opt-in profiling diagnostics.
+ *    engines (created by the thread's first features-type call on the device — make that an
+ *    eager call before capturing graphs), and the opt-in profiling diagnostics.
  */
 #ifndef CIL_H
 #define CIL_H

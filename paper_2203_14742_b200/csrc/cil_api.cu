@@ -449,6 +449,9 @@ cil_status run_engines(int P, const RowSrc& asrc, const RowSrc& bsrc, int64_t ro
 
     // The max family's integer-pipe engine and the tensor-core family use different pipes and fit on
     // one SM together (one Gram CTA + one k_max16_reg CTA): with both, the former runs on a side stream.
+    // the side stream exists after a thread's first call on a device (eager, like the kernel
+    // attribute setup), so a later call with both families can be captured into a graph
+    if (t_concurrent) side_setup();
     Fork fk(st, t_concurrent && pl.simt_mask && pl.max16 && pl.tc && range == nullptr && diag == nullptr);
     // With the concurrent engines the max family's tile kernels are enqueued after the INT8 Gram and
     // start only once the Gram's operands are packed: the Gram's CTAs (186 KB of shared memory each)

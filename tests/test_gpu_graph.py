@@ -146,3 +146,45 @@ def test_features_graph_replay_concurrent_engines(cil):
         torch.cuda.synchronize()
         assert torch.equal(c_graph, c_eager) and torch.equal(s_graph, s_eager)
         assert int(c_graph[:, 1].sum()) > 0 and int(c_graph[:, 0].sum()) > 0     # both families counted
+
+
+def test_first_concurrent_call_inside_capture(cil):
+    """On a fresh host thread whose only eager call had no max family, the first call with both
+    families (the first to fork onto the side stream, and the first use of the max family's kernels)
+    is made inside a graph capture: it must capture and replay correctly."""
+    import threading
+    from oracle import oracle as O
+    res = {}
+
+    def work():
+        try:
+            dev = torch.device("cuda")
+            grid = (2, 16, 16, 0.0)
+            A = cilgen.make_set(93, 0, 90, grid[:3]).to(dev)
+            B = cilgen.make_set(93, 1, 70, grid[:3]).to(dev)
+            D = O.distance_matrix(A[:30].cpu().numpy(), B[:30].cpu().numpy(), grid, 0x3F)
+            radii = torch.tensor(np.stack([np.quantile(d[d > 0], np.linspace(0.95, 0.05, 6)) for d in D]), device=dev)
+            ws = cil.Workspace()
+            counts = torch.empty((1, 6, 6), dtype=torch.int64, device=dev)
+            st = torch.empty((1,), dtype=torch.int32, device=dev)
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                cil.features(A, B, grid, cil.L2, radii[:1], ws=ws)              # eager, L2 only
+            torch.cuda.synchronize()
+            ws.get(cil.features_workspace_size(1, 90, 70, grid, cil.ALL, 6, cil.ENGINE_AUTO), dev)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                cil.features(A, B, grid, cil.ALL, radii, ws=ws, counts=counts, status=st)
+            counts.zero_()
+            g.replay()
+            torch.cuda.synchronize()
+            c_eager, _, _ = cil.features(A, B, grid, cil.ALL, radii)
+            torch.cuda.synchronize()
+            res["ok"] = torch.equal(counts, c_eager) and int(st[0]) == 0
+        except Exception as e:                       # surfaced by the assertion below
+            res["err"] = repr(e)
+
+    t = threading.Thread(target=work)
+    t.start()
+    t.join()
+    assert res.get("ok"), res
