@@ -225,3 +225,25 @@ def test_concurrent_engines_identical(cil, oracle_mod, mode):
     assert np.array_equal(out[0], out[1])
     if mode == "features":
         _check(out[1], O.features(A.numpy(), B.numpy(), grid, 0x3F, radii, band=BAND), "concurrent")
+
+
+def test_max16_per_item_scales(cil, oracle_mod):
+    """Several items in one call, each with its own range (the quantisation scale and centre are per
+    item and region): scales 1e-2, 1, 1e3 and offsets -50, 0, 7 in one batch, per-item radii."""
+    O = oracle_mod
+    grid = (2, 12, 16, 0.0)
+    P, N, Nt, M = 3, 70, 55, 8
+    scales, offs = (1e-2, 1.0, 1e3), (-50.0, 0.0, 7.0)
+    A = torch.stack([cilgen.make_set(55, 2 * p, N, grid[:3]) * scales[p] + offs[p] for p in range(P)])
+    B = torch.stack([cilgen.make_set(55, 2 * p + 1, Nt, grid[:3]) * scales[p] + offs[p] for p in range(P)])
+    radii = []
+    for p in range(P):
+        D = O.distance_matrix(A[p, :30].numpy(), B[p, :30].numpy(), grid, 0x3F)
+        radii.append(_radii_at_distances(D, M))
+    radii = np.stack(radii)
+    dev = torch.device("cuda")
+    c, _, st = cil.features(A.to(dev), B.to(dev), grid, 0x3F, torch.tensor(radii, device=dev))
+    torch.cuda.synchronize()
+    assert (st.cpu().numpy() == 0).all()
+    for p in range(P):
+        _check(c[p].cpu().numpy(), O.features(A[p].numpy(), B[p].numpy(), grid, 0x3F, radii[p], band=BAND), f"item {p}")
