@@ -137,12 +137,11 @@ __global__ void __launch_bounds__(NTHR, (CIL_SIMT_EXP == 1 && !DO_SUM) ? 3 : (DO
         __syncthreads();
         const float* Ab = As + buf * TA * LDS;
         const float* Bb = Bs + buf * TB * LDS;
-#if CIL_SIMT_EXP == 2
-#pragma unroll 1
-#elif CIL_SIMT_EXP == 3
+        // unroll 1 for the max family alone (28.8 vs 33.8 ms on C3, tools/simt_c3.py), 2 with sums
+#if CIL_SIMT_EXP == 3
 #pragma unroll
 #else
-#pragma unroll 2
+#pragma unroll(DO_SUM ? 2 : 1)
 #endif
         for (int kk = 0; kk < BK; kk += 4) {
             float4 av[RI], bv[4];
