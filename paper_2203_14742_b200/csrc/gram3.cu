@@ -1233,7 +1233,7 @@ cudaError_t launch_pack3(int P, const RowSrc& src, int64_t rows, int64_t K, int6
     else if (Kp <= 4096)
         PACK3(4, 256);
     else if (Kp <= 8192)
-        PACK3(8, 256);
+        PACK3(16, 128);          // C2: 1.008-1.012 ms vs 1.045-1.057 for 8 x 256 (round 2, three planes)
     else if (Kp <= 16384)
         PACK3(16, 256);          // C4: 6.03-6.09 ms vs 6.40-6.42 for 8 x 512 (round 2, three planes)
     else if (Kp <= 32768)
