@@ -179,3 +179,96 @@ def test_fuzz_synth(cil, oracle_mod, case):
             np.testing.assert_allclose(out[p].cpu().numpy(), ref2, rtol=0, atol=1e-6, err_msg=str(c))
             if np.array_equal(Yg, Yr):
                 np.testing.assert_allclose(out[p].cpu().numpy(), ref, rtol=0, atol=1e-6, err_msg=str(c))
+
+
+@pytest.mark.parametrize("case", range(300, 316))
+def test_fuzz_train_vectors(cil, oracle_mod, case):
+    """Alg. 1 / Alg. 2 training vectors on random shapes: the k < l
+    subset blocks of one panel, each within the oracle's band counts."""
+    O = oracle_mod
+    c = _draw_case(case)
+    r = np.random.default_rng(5151 + case)
+    grid, mask, M = c["grid"], c["mask"], c["M"]
+    n_ens = int(r.integers(2, 7))
+    N = int(r.integers(1, 80))
+    X = torch.stack([cilgen.make_set(c["seed"], p, n_ens * N, grid[:3]) for p in range(c["P"])])
+    D = O.distance_matrix(X[0].numpy(), X[0].numpy(), grid, mask)
+    radii = _radii(D, M, c["lo_q"], c["hi_q"])
+    dev = torch.device("cuda")
+    Y, st = cil.train_vectors(X.to(dev), n_ens, grid, mask, torch.tensor(radii, device=dev),
+                              engine=getattr(cil, "ENGINE_" + c["engine"]))
+    torch.cuda.synchronize()
+    assert np.all(st.cpu().numpy() == 0), c
+    for p in range(c["P"]):
+        ref = O.train_vectors(X[p].numpy(), n_ens, grid, mask, radii, band=BAND)
+        got = np.rint(Y[p].cpu().numpy() * N * N).astype(np.int64).reshape(ref["lo"].shape)
+        assert np.all(ref["lo"] <= got) and np.all(got <= ref["hi"]), (c, p, n_ens, N)
+
+
+@pytest.mark.parametrize("case", range(400, 416))
+def test_fuzz_distance_range_and_radii(cil, oracle_mod, case):
+    """(min positive, max) distance per measure (reading R16) and the radii laws
+    on random shapes, including sets that share rows (zero distances excluded from the minimum)."""
+    O = oracle_mod
+    c = _draw_case(case)
+    grid, mask = c["grid"], c["mask"]
+    A, B = _sets(c)
+    B[:, : min(c["N"], c["Nt"]) // 2] = A[:, : min(c["N"], c["Nt"]) // 2]
+    dev = torch.device("cuda")
+    rng, st = cil.distance_range(A.to(dev), B.to(dev), grid, mask)
+    law = ["power", "linear"][case % 2]
+    radii, st1 = cil.radii_from_range(rng, c["M"], law)
+    torch.cuda.synchronize()
+    rng, radii = rng.cpu().numpy(), radii.cpu().numpy()
+    for p in range(c["P"]):
+        ref = O.distance_range(A[p].numpy(), B[p].numpy(), grid, mask)
+        np.testing.assert_allclose(rng[p], ref, rtol=1e-6, atol=0, err_msg=str(c))
+        if np.all(np.isfinite(ref)) and np.all(ref[:, 0] > 0):
+            np.testing.assert_allclose(radii[p], O.radii_from_range(rng[p], c["M"], law), rtol=1e-12,
+                                       err_msg=str(c))
+
+
+@pytest.mark.parametrize("case", range(500, 512))
+def test_fuzz_synth_boot(cil, oracle_mod, case):
+    """Alg. A2 on random shapes and draws: replicate vectors within the band
+    (resampled sets built explicitly by the oracle), the tail within 1e-6."""
+    O = oracle_mod
+    c = _draw_case(case)
+    r = np.random.default_rng(6161 + case)
+    grid, mask = c["grid"], c["mask"]
+    nq = O.n_measures(mask)
+    P = c["P"]
+    N_set = int(r.integers(1, 30))
+    N_syn = N_set + int(r.integers(1, 90))
+    n_rep = int(r.integers(2, 40))
+    M = int(r.integers(1, min(64, 192 // nq) + 1))
+    pools = torch.stack([cilgen.make_set(c["seed"], 100 + p, N_syn, grid[:3]) for p in range(P)])
+    data = cilgen.make_set(c["seed"], 999, N_set, grid[:3])
+    radii, draws = [], []
+    for p in range(P):
+        D = O.distance_matrix(pools[p].numpy(), pools[p].numpy(), grid, mask)
+        radii.append(_radii(D, M, c["lo_q"], c["hi_q"]))
+        draws.append(cilgen.boot_draws_a2(c["seed"], p, n_rep, N_syn, N_set))
+    radii = np.array(radii)
+    I1, I2, J = (np.stack([d[i] for d in draws]) for i in range(3))
+    dev = torch.device("cuda")
+    engine = ["SIMT", "TC_I8", "AUTO"][case % 3]
+    out, st, Y = cil.synth_loglik_boot(pools.to(dev), data.to(dev), N_set, torch.tensor(I1, device=dev),
+                                       torch.tensor(I2, device=dev), torch.tensor(J, device=dev), grid, mask,
+                                       torch.tensor(radii, device=dev), ridge=1e-3,
+                                       engine=getattr(cil, "ENGINE_" + engine), return_Y=True)
+    torch.cuda.synchronize()
+    for p in range(P):
+        ref, rst, Yr = O.synth_boot(pools[p].numpy(), data.numpy(), N_set, I1[p], I2[p], J[p], grid, mask,
+                                    radii[p], ridge=1e-3)
+        Yg = Y[p].cpu().numpy()
+        rr = O.resample_features(pools[p].numpy(), pools[p].numpy(), grid, mask, radii[p], I1[p], I2[p], band=BAND)
+        cnt = np.rint(Yg[:-1] * (N_set * (N_syn - N_set))).astype(np.int64).reshape(rr["lo"].shape)
+        assert np.all(rr["lo"] <= cnt) and np.all(cnt <= rr["hi"]), (c, p)
+        assert rst == st[p].item() or not np.array_equal(Yg, Yr), (c, p, rst, st[p].item())
+        if st[p].item() == 0:
+            mu, Sig = O.stats(Yg[:-1])
+            o2, _ = O.loglik(mu, Sig, Yg[-1], ridge=1e-3)
+            np.testing.assert_allclose(out[p].cpu().numpy(), o2, rtol=0, atol=1e-6, err_msg=str(c))
+            if np.array_equal(Yg, Yr):
+                np.testing.assert_allclose(out[p].cpu().numpy(), ref, rtol=0, atol=1e-6, err_msg=str(c))
