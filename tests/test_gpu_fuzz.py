@@ -272,3 +272,33 @@ def test_fuzz_synth_boot(cil, oracle_mod, case):
             np.testing.assert_allclose(out[p].cpu().numpy(), o2, rtol=0, atol=1e-6, err_msg=str(c))
             if np.array_equal(Yg, Yr):
                 np.testing.assert_allclose(out[p].cpu().numpy(), ref, rtol=0, atol=1e-6, err_msg=str(c))
+
+
+@pytest.mark.parametrize("case", range(600, 610))
+def test_fuzz_large_K(cil, oracle_mod, case):
+    """Long patterns (K up to ~150 k: the INT8 engines' 65536-element chunks, ragged in K) with
+    few rows, all six measures on some cases, against the oracle's band counts."""
+    O = oracle_mod
+    r = np.random.default_rng(7070 + case)
+    while True:
+        S, H, W = int(r.integers(1, 4)), int(r.integers(1, 300)), int(r.integers(2, 300))
+        K = S * H * W
+        if K % 4 == 0 and 20000 <= K <= 150000:
+            break
+    grid = (S, H, W, 0.0)
+    N, Nt = int(r.integers(1, 140)), int(r.integers(1, 140))
+    mask = 0x3F if case % 2 == 0 else int(r.integers(1, 64))
+    M = int(r.choice([5, 16, 20, 33]))
+    engine = ENGINES[case % len(ENGINES)]
+    A = cilgen.make_set(case, 0, N, grid[:3], "FHN" if case % 3 == 0 else "GM")
+    B = cilgen.make_set(case, 1, Nt, grid[:3], "FHN" if case % 3 == 0 else "GM")
+    D = O.distance_matrix(A.numpy(), B.numpy(), grid, mask)
+    radii = _radii(D, M, 0.05, 0.95)
+    dev = torch.device("cuda")
+    counts, y, st = cil.features(A.to(dev), B.to(dev), grid, mask, torch.tensor(radii, device=dev),
+                                 engine=getattr(cil, "ENGINE_" + engine))
+    torch.cuda.synchronize()
+    assert int(st[0]) == 0, (grid, N, Nt, mask, M, engine)
+    ref = O.features(A.numpy(), B.numpy(), grid, mask, radii, band=BAND)
+    got = counts[0].cpu().numpy()
+    assert np.all(ref["lo"] <= got) and np.all(got <= ref["hi"]), (grid, N, Nt, hex(mask), M, engine)
