@@ -100,15 +100,23 @@ def pilot_radii(A0, B0, grid, M):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled during the timed region: NVML (the library nvidia-smi
+    reads) polled every 20 ms from a thread, each sample time-stamped when taken; nvidia-smi -lms 50
+    as the fallback (its piped output arrives in bursts, so short regions get few samples)."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
+    # NVML clocks-event reason bits (nvml.h): hw_slowdown, hw_thermal_slowdown, sw_thermal_slowdown,
+    # sw_power_cap — the order of FIELDS[3:7]
+    NVML_BITS = (0x8, 0x40, 0x20, 0x4)
 
     def __init__(self, device_index):
         self.dev = device_index
         self.proc = None
+        self.nvml = None
+        self.stop = False
+        self.interval_ms = 50
         self.lines = []                    # (time, csv line)
         self.t0 = self.t1 = None           # the timed region (mark_start / mark_end)
 
@@ -125,6 +133,18 @@ class ClockSampler:
         except Exception:
             sel = str(self.dev)
         try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = (pynvml.nvmlDeviceGetHandleByUUID(sel) if sel.startswith("GPU-")
+                 else pynvml.nvmlDeviceGetHandleByIndex(int(sel)))
+            self.nvml = (pynvml, h)
+            self.interval_ms = 20
+            self.t = threading.Thread(target=self._poll, daemon=True)
+            self.t.start()
+            return self
+        except Exception:
+            self.nvml = None
+        try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", sel, f"--query-gpu={self.FIELDS}",
                                           "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
@@ -134,11 +154,36 @@ class ClockSampler:
             self.proc = None
         return self
 
+    def _poll(self):
+        nv, h = self.nvml
+        while not self.stop:
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+                pw = nv.nvmlDeviceGetPowerUsage(h) / 1000.0
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                flags = ",".join("Active" if rs & b else "Not Active" for b in self.NVML_BITS)
+                self.lines.append((time.time(), f"{sm},{mx},{pw:.1f},{flags}"))
+            except Exception:
+                break
+            time.sleep(self.interval_ms / 1000.0)
+
+    def wait_first(self, timeout=5.0):
+        """Block until nvidia-smi has produced a sample (it takes ~0.1-1 s to start), so a short
+        timed region that follows is covered."""
+        t_end = time.time() + timeout
+        while (self.proc is not None or self.nvml is not None) and not self.lines and time.time() < t_end:
+            time.sleep(0.02)
+        return self
+
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append((time.time(), line.strip()))
 
     def __exit__(self, *a):
+        self.stop = True
+        if self.nvml is not None:
+            self.t.join(timeout=1.0)
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -170,7 +215,8 @@ class ClockSampler:
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)), "reasons": sorted(reasons),
-                "samples": len(sm), "window": window, "interval_ms": 50}
+                "samples": len(sm), "window": window, "interval_ms": self.interval_ms,
+                "source": "nvml" if self.nvml is not None else "nvidia-smi"}
 
 
 def timed(fn, steps, stream):
@@ -353,7 +399,7 @@ def main():
             import torch.distributed as dist
             dist.barrier()
 
-    clk = ClockSampler(local).__enter__()             # sampling from before the warm-up
+    clk = ClockSampler(local).__enter__().wait_first()   # sampling from before the warm-up
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -635,13 +681,17 @@ def bench_c5(cil, args, world, rank, dev, engine, stream):
         last[0] = sharding.sharded_features(A, B, grid, mask, radii, N, engine=engine, ws=ws)
         return last[0]
 
+    clk = ClockSampler(dev.index or 0).__enter__().wait_first()
     step()                                               # warm-up (kernel attributes, workspace)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     _capi.prof_enable(True)
     steps = max(1, args.c5_steps)
+    clk.mark_start()
     ms = timed(step, steps, stream)
+    clk.mark_end()
+    clk.__exit__()
     _capi.prof_enable(False)
     prof = _capi.prof_read()
     if world > 1:
@@ -659,6 +709,7 @@ def bench_c5(cil, args, world, rank, dev, engine, stream):
     res.update({"value": N * Nt / (ms_step * 1e-3), "ms_per_step": round(ms_step, 2), "steps": steps, "warmup": 1,
                 "item_status": int(st[0].item()),
                 "counts": c.tolist(), "counts_sha256": hashlib.sha256(c.tobytes()).hexdigest()[:16],
+                "clocks_this_rank": clk.summary(),
                 "recheck_cases_this_rank": listed, "recheck_fraction_this_rank": listed / float((hi - lo) * Nt * nq),
                 "kernel_breakdown_this_rank": kb})
     if prof["gram_tc"][1]:
@@ -693,11 +744,11 @@ def bench_c3(args, dev):
     def step():
         cil.features(A, B, grid, mask, radii, engine=engine, ws=ws)
 
-    for _ in range(2):
+    clk = ClockSampler(dev.index or 0).__enter__().wait_first()   # sampling from before the warm-up
+    for _ in range(3):
         step()
     torch.cuda.synchronize()
-    steps = max(2, min(args.steps, 5))
-    clk = ClockSampler(dev.index or 0).__enter__()
+    steps = max(3, min(args.steps, 20))                  # >= 0.4 s timed: >= 8 clock samples at 50 ms
     _capi.prof_enable(True)
     clk.mark_start()
     ms = timed(step, steps, stream) / steps
@@ -781,12 +832,16 @@ def bench_c6(cil, args, world, rank, dev, engine, stream):
         cil.synth_loglik_boot(pools, data, N_set, I1, I2, J, grid, cfg["mask"], radii, ridge=1e-10, engine=engine,
                               ws=ws, out=out, status=st)
 
+    clk = ClockSampler(dev.index or 0).__enter__().wait_first()
     for _ in range(args.warmup):
         step()
     steps = max(3, args.steps // 40)
     from paper_2203_14742_b200 import _capi
     _capi.prof_enable(True)
+    clk.mark_start()
     ms = timed(step, steps, stream)
+    clk.mark_end()
+    clk.__exit__()
     _capi.prof_enable(False)
     prof = _capi.prof_read()
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
@@ -832,6 +887,7 @@ def bench_c6(cil, args, world, rank, dev, engine, stream):
                            "gemm_int8_tops_incl_helpers": round(2.0 * P * n_rep * M * N_syn * N_syn / (r_step * 1e-3)
                                                                 / 1e12, 1)}
     res["kernel_breakdown"] = {k: round(v[0] / steps, 4) for k, v in prof.items() if v[1] > 0}
+    res["clocks"] = clk.summary()
     return res
 
 
@@ -850,12 +906,16 @@ def bench_c7(cil, args, world, rank, dev, engine, stream):
     def step():
         cil.train_vectors(X, n_ens, grid, mask, radii, engine=engine, ws=ws)
 
+    clk = ClockSampler(dev.index or 0).__enter__().wait_first()
     for _ in range(max(2, args.warmup)):
         step()
     steps = max(3, args.steps // 80)
     from paper_2203_14742_b200 import _capi
     _capi.prof_enable(True)
+    clk.mark_start()
     ms = timed(step, steps, stream)
+    clk.mark_end()
+    clk.__exit__()
     _capi.prof_enable(False)
     prof = _capi.prof_read()
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
@@ -879,6 +939,7 @@ def bench_c7(cil, args, world, rank, dev, engine, stream):
                           "ms_per_launch": round(per, 3), "achieved_tops_on_needed_pairs": round(ops / (per * 1e-3) / 1e12, 1),
                           "peak": round(peak, 1), "peak_source": psrc,
                           "frac_of_peak_on_needed_pairs": round(ops / (per * 1e-3) / 1e12 / peak, 4)}
+    res["clocks"] = clk.summary()
     return res
 
 
@@ -908,12 +969,16 @@ def bench_c4(cil, args, world, rank, dev, engine, stream):
         cil.synth_loglik(pools, n_ens, N_set, Nt, data, k0, grid, cfg["mask"], radii, ridge=1e-10, engine=engine,
                          ws=ws, out=out, status=st)
 
+    clk = ClockSampler(dev.index or 0).__enter__().wait_first()
     for _ in range(args.warmup):
         step()
     steps = max(3, args.steps // 10)
     from paper_2203_14742_b200 import _capi
     _capi.prof_enable(True)
+    clk.mark_start()
     ms = timed(step, steps, stream)
+    clk.mark_end()
+    clk.__exit__()
     _capi.prof_enable(False)
     prof = _capi.prof_read()
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
@@ -936,6 +1001,7 @@ def bench_c4(cil, args, world, rank, dev, engine, stream):
         res["gram_tc"] = {"engine": used, "ms_per_launch": round(per, 4), "achieved_tops": round(ach, 1),
                           "peak": round(peak, 1), "peak_source": psrc, "frac_of_peak": round(ach / peak, 4)}
     res["kernel_breakdown"] = {k: round(v[0] / steps, 4) for k, v in prof.items() if v[1] > 0}
+    res["clocks"] = clk.summary()
     return res
 
 
