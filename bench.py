@@ -454,12 +454,21 @@ def main():
                      "kernel_ms_per_launch": round(per_launch_ms, 4),
                      "kernel_share_of_step": round(gram_ms / ms, 4),
                      "traffic": traffic_for("C2_gram")}
+        if used == "TC_I8":
+            # the same cuBLAS int8 GEMM run back to back for 4 s (power-capped): the denominator for a
+            # kernel that runs inside a long, power-capped step like this one
+            try:
+                sus = json.load(open(I8_PEAKS_FILE))["int8"]["sustained_tops"]
+                roof_gram.update({"peak_sustained": round(sus, 1), "frac_of_sustained": round(achieved / sus, 4),
+                                  "peak_sustained_source": "profiles/r02_measured_peaks.json int8 sustained"})
+            except Exception:
+                pass
     pack_ms, pack_n = prof["pack"]
     roof_pack = None
     if pack_n > 0 and used == "TC_I8":
         # ALGORITHMIC bytes (SURVEY §8(d) per-unit figure: 4K bytes of FP32 read once per
-        # pattern) x the patterns of one step; the design additionally writes the two INT8 digit
-        # planes (2Kp B per pattern, read back by the Gram) and reads <= 16 centre rows per item —
+        # pattern) x the patterns of one step; the design additionally writes the three INT8 digit
+        # planes (3Kp B per pattern, read back by the Gram) and reads <= 16 centre rows per item —
         # reported separately (achieved_incl_design_bytes), and visible in `traffic` (ncu).
         # Time = the whole pack class (centre + 2 launches).
         Kp = (K + 127) // 128 * 128

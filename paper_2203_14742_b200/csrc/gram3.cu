@@ -1210,6 +1210,9 @@ __global__ void __launch_bounds__(512, 2) k_pack3_aug4(RowSrc src, int64_t rows,
 }  // namespace g3
 
 // ------------------------------------------------------------------ host side
+#ifndef CIL_PACK_EXP
+#define CIL_PACK_EXP 0   // pack shape experiments (tools/simt_var_build.sh FILE=gram3); 0 = product
+#endif
 cudaError_t launch_pack3(int P, const RowSrc& src, int64_t rows, int64_t K, int64_t Kp, const float* center,
                          int8_t* planes, int64_t plane_stride, int64_t row0, float* meta, int32_t* status,
                          cudaStream_t st) {
@@ -1234,8 +1237,21 @@ cudaError_t launch_pack3(int P, const RowSrc& src, int64_t rows, int64_t K, int6
         PACK3(4, 256);
     else if (Kp <= 8192)
         PACK3(16, 128);          // C2: 1.008-1.012 ms vs 1.045-1.057 for 8 x 256 (round 2, three planes)
-    else if (Kp <= 16384)
+    else if (Kp <= 16384) {
+#if CIL_PACK_EXP == 1
+        PACK3(32, 128);
+#elif CIL_PACK_EXP == 2
+        g3::k_pack3<16, 256><<<grid, 256, 0, st>>>(src, rows, K, Kp, center, planes, plane_stride, row0, meta, status, 0);
+#elif CIL_PACK_EXP == 3
+        g3::k_pack3<16, 256><<<grid, 256, 0, st>>>(src, rows, K, Kp, center, planes, plane_stride, row0, meta, status,
+                                                     2 * pf((const void*)g3::k_pack3<16, 256>, 256));
+#elif CIL_PACK_EXP == 4
+        g3::k_pack3<16, 256><<<grid, 256, 0, st>>>(src, rows, K, Kp, center, planes, plane_stride, row0, meta, status,
+                                                     pf((const void*)g3::k_pack3<16, 256>, 256) / 2);
+#else
         PACK3(16, 256);          // C4: 6.03-6.09 ms vs 6.40-6.42 for 8 x 512 (round 2, three planes)
+#endif
+    }
     else if (Kp <= 32768)
         PACK3(8, 1024);
     else
