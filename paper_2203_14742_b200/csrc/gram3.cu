@@ -631,6 +631,10 @@ k_gram3(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensor
                     unsigned char* st = stages + stage * GG::STAGE;
                     if (CIL_G3_EXP & 2) {
                         if (rank == 0) mbar_expect_tx(&full[stage], 0);
+                    } else if (!GG::WIDE && (CIL_G3_EXP & 12)) {       // experiment: only B (4) / only A (8)
+                        if (rank == 0) mbar_expect_tx(&full[stage], (CIL_G3_EXP & 4) ? 2 * 3 * GG::B_PL : 2 * 3 * GG::A_PL);
+                        if (CIL_G3_EXP & 8) tma3(st, &mA, &full[stage], kb * KS, ya);
+                        else tma3(st + 3 * GG::A_PL, &mB, &full[stage], kb * KS, yb);
                     } else {
                         if (rank == 0) mbar_expect_tx(&full[stage], 2 * GG::STAGE);
                         tma3(st, &mA, &full[stage], kb * KS, ya);
