@@ -720,6 +720,9 @@ k_gram3(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensor
 }
 
 // ------------------------------------------------------------------------------------ pack
+#ifndef CIL_Q4_EXP
+#define CIL_Q4_EXP 0     // 1: the earlier digit extraction (experiment builds)
+#endif
 // Quantisation constant: |q| <= Q (1 + 2^-22) < 2^22 (the magic-constant rint is exact) and
 // (q + 128) >> 8 in [-16250, 16250], so h = (t1 + 128) >> 8 in [-63, 63].
 constexpr float kQ = 4160000.f;
@@ -739,10 +742,20 @@ __device__ __forceinline__ void quant4(const float4 t, float inv, uint32_t& wh, 
     const uint32_t r1 = __float_as_uint(fmaf(t.y, inv, 12582912.f));
     const uint32_t r2 = __float_as_uint(fmaf(t.z, inv, 12582912.f));
     const uint32_t r3 = __float_as_uint(fmaf(t.w, inv, 12582912.f));
+    const uint32_t c = 0x4B3F7F80u;
+#if CIL_Q4_EXP == 1
     wl = __byte_perm(__byte_perm(r0, r1, 0x0040), __byte_perm(r2, r3, 0x0040), 0x5410);
     wm = __byte_perm(__byte_perm(r0 + 128u, r1 + 128u, 0x0051), __byte_perm(r2 + 128u, r3 + 128u, 0x0051), 0x5410);
-    const uint32_t c = 0x4B3F7F80u;
     wh = __byte_perm(__byte_perm(r0 - c, r1 - c, 0x0062), __byte_perm(r2 - c, r3 - c, 0x0062), 0x5410);
+#else
+    // u = raw - c = q + 32896 = 2^16 h + 2^8 (m + 128) + (l + 128): bytes 0 / 1 are l / m biased by 128
+    // (XOR 0x80 gives the two's-complement digit), byte 2 is h — one IADD per value for all three
+    const uint32_t u0 = r0 - c, u1 = r1 - c, u2 = r2 - c, u3 = r3 - c;
+    const uint32_t x = __byte_perm(u0, u1, 0x5140), y = __byte_perm(u2, u3, 0x5140);   // (l0 l1 m0 m1), (l2 l3 m2 m3)
+    wl = __byte_perm(x, y, 0x5410) ^ 0x80808080u;
+    wm = __byte_perm(x, y, 0x7632) ^ 0x80808080u;
+    wh = __byte_perm(__byte_perm(u0, u1, 0x0062), __byte_perm(u2, u3, 0x0062), 0x5410);
+#endif
     S[0] = __dp4a((int)wh, (int)wh, S[0]);
     S[1] = __dp4a((int)wh, (int)wm, S[1]);
     S[2] = __dp4a((int)wh, (int)wl, S[2]);
