@@ -236,10 +236,85 @@ __global__ void __launch_bounds__(kLogThreads) k_loglik(const double* __restrict
     }
 }
 
+// D <= 32: one warp per item, lane i owns row i of L (shared memory, stride 33 doubles: conflict-
+// free per half-warp phase), synchronised by __syncwarp only.  Left-looking Cholesky: at column j
+// lane j forms its pivot d_j = S_jj + ridge - sum_k L_jk^2, the lanes i > j then
+// L_ij = (S_ij - sum_k L_ik L_jk) / L_jj; forward substitution column by column (z_k broadcast
+// by shuffle, the lanes below update their right-hand sides).  Same outputs and statuses as
+// k_loglik; the general kernel's block-wide barriers per column made it latency-bound (~19 us for
+// D = 15).
+constexpr int kLogWarpItems = 4;
+__global__ void __launch_bounds__(32 * kLogWarpItems) k_loglik_warp(const double* __restrict__ mu, int64_t mu_stride,
+                                                                    const double* __restrict__ Sigma, int64_t Sigma_stride,
+                                                                    const double* __restrict__ y, int64_t y_stride, int D,
+                                                                    double ridge, double* __restrict__ out,
+                                                                    int32_t* __restrict__ status,
+                                                                    const int32_t* status_in, int P) {
+    __shared__ double Ls[kLogWarpItems][32][33];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int p = blockIdx.x * kLogWarpItems + warp;
+    if (p >= P) return;                                  // warp-uniform
+    double (*L)[33] = Ls[warp];
+    const double* S = Sigma + (int64_t)p * Sigma_stride;
+    const double* m = mu + (int64_t)p * mu_stride;
+    const double* yy = y + (int64_t)p * y_stride;
+    if (lane < D)
+        for (int k = 0; k <= lane; ++k) L[lane][k] = S[(int64_t)lane * D + k] + (k == lane ? ridge : 0.0);
+    double r = lane < D ? yy[lane] - m[lane] : 0.0;
+    __syncwarp();
+    bool fail = false;
+    for (int j = 0; j < D; ++j) {
+        double d = 0.0;
+        if (lane == j) {
+            d = L[j][j];
+            for (int k = 0; k < j; ++k) d -= L[j][k] * L[j][k];
+        }
+        d = __shfl_sync(0xffffffffu, d, j);
+        if (!(d > 0.0)) { fail = true; break; }          // warp-uniform
+        const double piv = sqrt(d);
+        if (lane == j) L[j][j] = piv;
+        if (lane > j && lane < D) {
+            double t = L[lane][j];
+            for (int k = 0; k < j; ++k) t -= L[lane][k] * L[j][k];
+            L[lane][j] = t / piv;
+        }
+        __syncwarp();
+    }
+    const int32_t base = status_in ? status_in[p] : 0;
+    if (fail) {
+        if (lane == 0) {
+            out[3 * p + 0] = out[3 * p + 1] = out[3 * p + 2] = CUDART_NAN;
+            status[p] = base | CIL_ITEM_NOTPD;
+        }
+        return;
+    }
+    double logdet = lane < D ? 2.0 * log(L[lane][lane]) : 0.0;
+    for (int o = 16; o > 0; o >>= 1) logdet += __shfl_xor_sync(0xffffffffu, logdet, o);
+    double quad = 0.0;
+    for (int k = 0; k < D; ++k) {
+        const double zk = __shfl_sync(0xffffffffu, r, k) / L[k][k];
+        if (lane > k && lane < D) r -= L[lane][k] * zk;
+        quad += zk * zk;
+    }
+    if (lane == 0) {
+        out[3 * p + 0] = quad;
+        out[3 * p + 1] = logdet;
+        out[3 * p + 2] = -0.5 * quad - 0.5 * logdet - 0.5 * D * log(2.0 * CUDART_PI);
+        status[p] = base;
+    }
+}
+
 static cudaError_t launch_loglik_strided(int P, const double* mu, int64_t mu_stride, const double* Sigma,
                                          int64_t Sigma_stride, const double* y, int64_t y_stride, int D,
                                          double ridge, double* out, int32_t* status,
                                          const int32_t* status_in, cudaStream_t st) {
+    if (D <= 32) {
+        ProfScope ps_(K_TAIL, st);
+        k_loglik_warp<<<(P + kLogWarpItems - 1) / kLogWarpItems, 32 * kLogWarpItems, 0, st>>>(
+            mu, mu_stride, Sigma, Sigma_stride, y, y_stride, D, ridge, out, status, status_in, P);
+        note_launch();
+        return cudaGetLastError();
+    }
     const size_t smem = sizeof(double) * ((size_t)D * (D + 1) / 2 + 2 * D);
     static SmemAttrOnce attr;
     if (cudaError_t e = attr.ensure(k_loglik, (int)(sizeof(double) * ((size_t)kMaxD * (kMaxD + 1) / 2 + 2 * kMaxD)));
