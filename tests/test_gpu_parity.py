@@ -293,6 +293,37 @@ def test_loglik_notpd_and_large_D(cil, oracle_mod):
     np.testing.assert_allclose(out[0].cpu().numpy(), ref, rtol=0, atol=1e-6)
 
 
+@pytest.mark.parametrize("D", [1, 2, 7, 15, 31, 32, 33, 64])
+def test_loglik_batched_sizes_and_notpd(cil, oracle_mod, D):
+    """Eq. (4) log-density over a batch of P = 9 items (the warp-per-item kernel for D <= 32 packs 4
+    items per CTA: a ragged last CTA) with per-item Sigma, two of them not positive definite."""
+    O = oracle_mod
+    dev = torch.device("cuda")
+    rng = np.random.default_rng(100 + D)
+    P = 9
+    mus = rng.standard_normal((P, D))
+    Sigs = []
+    for p in range(P):
+        X = rng.standard_normal((D, D + 3))
+        S = X @ X.T / (D + 3) + 0.1 * np.eye(D)
+        if p in (2, 7):                                  # indefinite: a pivot is clearly negative
+            v = rng.standard_normal(D)
+            S = np.outer(v, v) - 0.1 * np.eye(D) if D > 1 else -0.1 * np.eye(1)
+        Sigs.append(S)
+    Sigs = np.array(Sigs)
+    ys = mus + 0.3 * rng.standard_normal((P, D))
+    out, st = cil.loglik(torch.tensor(mus, device=dev), torch.tensor(Sigs, device=dev), torch.tensor(ys, device=dev))
+    torch.cuda.synchronize()
+    out, st = out.cpu().numpy(), st.cpu().numpy()
+    for p in range(P):
+        ref, rst = O.loglik(mus[p], Sigs[p], ys[p])
+        assert st[p] == rst, (D, p, st[p], rst)
+        if rst == 0:
+            np.testing.assert_allclose(out[p], ref, rtol=0, atol=1e-6 * max(1.0, abs(ref[2]) / 1e3))
+        else:
+            assert st[p] == cil.ITEM_NOTPD and np.isnan(out[p]).all()
+
+
 # ------------------------------------------------------------------ SCIL
 @pytest.mark.parametrize("engine", ENGINES)
 @pytest.mark.parametrize("mask", [0x1, 0x0B])
