@@ -25,6 +25,10 @@
  *    K = S*H*W, pattern p of a set starts at base + p*ld (ld >= K, in floats).
  *  - Batched calls take 1 <= P <= 21845 items (the grids put items on a 65535-wide grid
  *    axis, three per item for the max family); more is CIL_EINVAL.  Split larger batches.
+ *    A set (or a SCIL / training / bootstrap panel) holds at most 2 097 120 = 65535 x 32
+ *    patterns (the CUDA-core engines' 32-row tiles on a grid axis); more is CIL_EINVAL
+ *    (workspace queries return 0).  Larger sets: row blocks (cil_features is additive over
+ *    them, as the multi-GPU split uses).
  *  - Thread-safe: no global mutable state besides a once-per-device kernel
  *    attribute setup (atomic), thread-local launch counters / diagnostics settings, one
  *    library-owned side stream (+ two events) per host thread and device for the concurrent

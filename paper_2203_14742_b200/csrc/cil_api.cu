@@ -23,6 +23,8 @@ static thread_local int32_t t_launches = 0;
 // Items per call: grids put items on gridDim.y / .z (<= 65535), the max family's region kernel
 // three per item.
 constexpr int32_t kMaxItems = 21845;
+// Rows per set (or panel): the CUDA-core engines put 32-row A tiles on gridDim.y (<= 65535).
+constexpr int64_t kMaxRows = 65535ll * 32;
 void note_launch(int n) { t_launches += n; }
 // diagnostics (cil_diag_concurrent_engines): run the max family's engine on a side stream, concurrently
 // with the tensor-core family (default on)
@@ -632,7 +634,7 @@ extern "C" {
 
 size_t cil_features_workspace_size(int32_t P, int64_t N, int64_t Nt, cil_grid g, uint32_t dist_mask,
                                    int32_t M, cil_engine engine) {
-    if (P < 1 || P > kMaxItems || N < 0 || Nt < 0 || M < 1 || check_grid(g, dist_mask) != CIL_OK) return 0;
+    if (P < 1 || P > kMaxItems || N < 0 || Nt < 0 || N > kMaxRows || Nt > kMaxRows || M < 1 || check_grid(g, dist_mask) != CIL_OK) return 0;
     const Slots sl = slots_of(dist_mask);
     const Plan pl = make_plan(dist_mask, engine, g, Nt > 0 ? Nt : 1, Nt, M);
     SegParams sp{N > 0 ? N : 1, Nt > 0 ? Nt : 1, 1, 1};
@@ -645,7 +647,7 @@ cil_status cil_features(int32_t P, const float* A, int64_t strideA, int64_t lda,
                         int32_t* item_status, cil_engine engine, void* ws, size_t ws_bytes, void* stream) {
     t_launches = 0;
     NvtxScope nv_("cil_features");
-    if (P < 1 || P > kMaxItems || N < 0 || Nt < 0 || M < 1 || M > kMaxM) return CIL_EINVAL;
+    if (P < 1 || P > kMaxItems || N < 0 || Nt < 0 || N > kMaxRows || Nt > kMaxRows || M < 1 || M > kMaxM) return CIL_EINVAL;
     if (check_grid(g, dist_mask) != CIL_OK) return CIL_EINVAL;
     if ((int)engine < 0 || (int)engine > 4) return CIL_EINVAL;
     if (!radii || !counts || !item_status || !ws) return CIL_EINVAL;
@@ -677,7 +679,7 @@ cil_status cil_features(int32_t P, const float* A, int64_t strideA, int64_t lda,
 
 cil_status cil_features_recheck_count(int32_t P, int64_t N, int64_t Nt, cil_grid g, uint32_t dist_mask, int32_t M,
                                       cil_engine engine, const void* ws, uint64_t* listed, uint64_t* capacity) {
-    if (P < 1 || P > kMaxItems || N < 0 || Nt < 0 || M < 1 || !ws || !listed || !capacity || check_grid(g, dist_mask) != CIL_OK)
+    if (P < 1 || P > kMaxItems || N < 0 || Nt < 0 || N > kMaxRows || Nt > kMaxRows || M < 1 || !ws || !listed || !capacity || check_grid(g, dist_mask) != CIL_OK)
         return CIL_EINVAL;
     const Slots sl = slots_of(dist_mask);
     const Plan pl = make_plan(dist_mask, engine, g, Nt > 0 ? Nt : 1, Nt, M);
@@ -814,7 +816,7 @@ SynthGeo synth_geo(int32_t n_ens, int32_t N_set, int32_t N_tilde, const cil_grid
 
 size_t cil_synth_workspace_size(int32_t P, int32_t n_ens, int32_t N_set, int32_t N_tilde, cil_grid g,
                                 uint32_t dist_mask, int32_t M, cil_engine engine) {
-    if (P < 1 || P > kMaxItems || n_ens < 2 || N_set < 1 || N_tilde < 1 || M < 1 || check_grid(g, dist_mask) != CIL_OK)
+    if (P < 1 || P > kMaxItems || n_ens < 2 || N_set < 1 || N_tilde < 1 || (int64_t)(n_ens + 1) * N_set > kMaxRows || (int64_t)n_ens * N_tilde > kMaxRows || M < 1 || check_grid(g, dist_mask) != CIL_OK)
         return 0;
     const Slots sl = slots_of(dist_mask);
     const SynthGeo sg = synth_geo(n_ens, N_set, N_tilde, g, dist_mask, M, engine);
@@ -830,6 +832,7 @@ cil_status cil_synth_loglik(int32_t P, const float* pools, int64_t pool_stride, 
     t_launches = 0;
     NvtxScope nv_("cil_synth_loglik");
     if (P < 1 || P > kMaxItems || n_ens < 2 || N_set < 1 || N_tilde < 1 || M < 1 || M > kMaxM) return CIL_EINVAL;
+    if ((int64_t)(n_ens + 1) * N_set > kMaxRows || (int64_t)n_ens * N_tilde > kMaxRows) return CIL_EINVAL;
     if (check_grid(g, dist_mask) != CIL_OK) return CIL_EINVAL;
     if ((int)engine < 0 || (int)engine > 4) return CIL_EINVAL;
     if (!pools || !data || !k0 || !radii || !out || !item_status || !ws) return CIL_EINVAL;
@@ -883,7 +886,7 @@ cil_status cil_minmax_scale(int64_t n, const float* X, int64_t ldx, float* Y, in
 
 // ------------------------------------------------------------------ adaptive radii
 size_t cil_range_workspace_size(int32_t P, int64_t N, int64_t Nt, cil_grid g, uint32_t dist_mask) {
-    if (P < 1 || P > kMaxItems || N < 0 || Nt < 0 || check_grid(g, dist_mask) != CIL_OK) return 0;
+    if (P < 1 || P > kMaxItems || N < 0 || Nt < 0 || N > kMaxRows || Nt > kMaxRows || check_grid(g, dist_mask) != CIL_OK) return 0;
     const Slots sl = slots_of(dist_mask);
     const Plan pl = make_plan(dist_mask, CIL_ENGINE_SIMT, g);
     SegParams sp{N > 0 ? N : 1, Nt > 0 ? Nt : 1, 1, 1};
@@ -895,7 +898,7 @@ cil_status cil_distance_range(int32_t P, const float* A, int64_t strideA, int64_
                               double* range, int32_t* item_status, void* ws, size_t ws_bytes, void* stream) {
     t_launches = 0;
     NvtxScope nv_("cil_distance_range");
-    if (P < 1 || P > kMaxItems || N < 1 || Nt < 1) return CIL_EINVAL;
+    if (P < 1 || P > kMaxItems || N < 1 || Nt < 1 || N > kMaxRows || Nt > kMaxRows) return CIL_EINVAL;
     if (check_grid(g, dist_mask) != CIL_OK) return CIL_EINVAL;
     if (!range || !item_status || !ws) return CIL_EINVAL;
     cil_status s = check_sets(P, A, strideA, lda, N, B, strideB, ldb, Nt, g);
@@ -932,7 +935,7 @@ cil_status cil_radii_from_range(int32_t P, int32_t n_meas, int32_t M, const doub
 // ------------------------------------------------------------------ Alg. 1 / Alg. 2 training vectors
 size_t cil_train_workspace_size(int32_t P, int32_t n_ens, int32_t N, cil_grid g, uint32_t dist_mask, int32_t M,
                                 cil_engine engine) {
-    if (P < 1 || P > kMaxItems || n_ens < 2 || N < 1 || M < 1 || check_grid(g, dist_mask) != CIL_OK) return 0;
+    if (P < 1 || P > kMaxItems || n_ens < 2 || N < 1 || (int64_t)n_ens * N > kMaxRows || M < 1 || check_grid(g, dist_mask) != CIL_OK) return 0;
     const Slots sl = slots_of(dist_mask);
     const int64_t rows = (int64_t)n_ens * N;
     const Plan pl = make_plan(dist_mask, engine, g, N, rows, M);
@@ -946,7 +949,7 @@ cil_status cil_train_vectors(int32_t P, const float* X, int64_t stride, int64_t 
                              void* stream) {
     t_launches = 0;
     NvtxScope nv_("cil_train_vectors");
-    if (P < 1 || P > kMaxItems || n_ens < 2 || N < 1 || M < 1 || M > kMaxM) return CIL_EINVAL;
+    if (P < 1 || P > kMaxItems || n_ens < 2 || N < 1 || (int64_t)n_ens * N > kMaxRows || M < 1 || M > kMaxM) return CIL_EINVAL;
     if (check_grid(g, dist_mask) != CIL_OK) return CIL_EINVAL;
     if ((int)engine < 0 || (int)engine > 4) return CIL_EINVAL;
     if (!X || !radii || !Y || !item_status || !ws || radii_stride < 0 || stride < 0) return CIL_EINVAL;
@@ -975,7 +978,7 @@ cil_status cil_train_vectors(int32_t P, const float* X, int64_t stride, int64_t 
 
 size_t cil_bin_matrix_workspace_size(int32_t P, int64_t N, int64_t Nt, cil_grid g, uint32_t dist_mask, int32_t M,
                                      cil_engine engine) {
-    if (P < 1 || P > kMaxItems || N < 0 || Nt < 0 || M < 1 || check_grid(g, dist_mask) != CIL_OK) return 0;
+    if (P < 1 || P > kMaxItems || N < 0 || Nt < 0 || N > kMaxRows || Nt > kMaxRows || M < 1 || check_grid(g, dist_mask) != CIL_OK) return 0;
     Plan pl;
     if (!plan_bins(dist_mask, engine, g, &pl)) return 0;
     const Slots sl = slots_of(dist_mask);
@@ -989,7 +992,7 @@ cil_status cil_bin_matrix(int32_t P, const float* A, int64_t strideA, int64_t ld
                           int32_t* item_status, cil_engine engine, void* ws, size_t ws_bytes, void* stream) {
     t_launches = 0;
     NvtxScope nv_("cil_bin_matrix");
-    if (P < 1 || P > kMaxItems || N < 0 || Nt < 0 || M < 1 || M > kMaxM) return CIL_EINVAL;
+    if (P < 1 || P > kMaxItems || N < 0 || Nt < 0 || N > kMaxRows || Nt > kMaxRows || M < 1 || M > kMaxM) return CIL_EINVAL;
     if (check_grid(g, dist_mask) != CIL_OK) return CIL_EINVAL;
     if ((int)engine < 0 || (int)engine > 4) return CIL_EINVAL;
     if (!radii || !item_status || !ws || (N > 0 && Nt > 0 && !bins) || radii_stride < 0) return CIL_EINVAL;
@@ -1079,7 +1082,7 @@ bool boot_layout(int32_t P, int32_t N_syn, int32_t N_set, int32_t n_rep, const c
 
 size_t cil_synth_boot_workspace_size(int32_t P, int32_t N_syn, int32_t N_set, int32_t n_rep, cil_grid g,
                                      uint32_t dist_mask, int32_t M, cil_engine engine) {
-    if (P < 1 || P > kMaxItems || N_set < 1 || N_syn <= N_set || n_rep < 2 || M < 1 || check_grid(g, dist_mask) != CIL_OK) return 0;
+    if (P < 1 || P > kMaxItems || N_set < 1 || N_syn <= N_set || N_syn > kMaxRows || n_rep < 2 || M < 1 || check_grid(g, dist_mask) != CIL_OK) return 0;
     BootLayout B;
     if (!boot_layout(P, N_syn, N_set, n_rep, g, dist_mask, M, engine, &B)) return 0;
     return B.total;
@@ -1093,7 +1096,7 @@ cil_status cil_synth_loglik_boot(int32_t P, const float* pools, int64_t pool_str
                                  void* stream) {
     t_launches = 0;
     NvtxScope nv_("cil_synth_loglik_boot");
-    if (P < 1 || P > kMaxItems || N_set < 1 || N_syn <= N_set || n_rep < 2 || M < 1 || M > kMaxM) return CIL_EINVAL;
+    if (P < 1 || P > kMaxItems || N_set < 1 || N_syn <= N_set || N_syn > kMaxRows || n_rep < 2 || M < 1 || M > kMaxM) return CIL_EINVAL;
     if (check_grid(g, dist_mask) != CIL_OK) return CIL_EINVAL;
     if ((int)engine < 0 || (int)engine > 4) return CIL_EINVAL;
     if (!pools || !data || !I1 || !I2 || !J || !radii || !out || !item_status || !ws) return CIL_EINVAL;

@@ -117,3 +117,8 @@ def test_item_count_limit(capi):
     g = capi.Grid(2, 8, 8, 0.0)
     assert capi.lib.cil_features_workspace_size(21845, 10, 10, g, 1, 5, 0) > 0
     assert capi.lib.cil_features_workspace_size(21846, 10, 10, g, 1, 5, 0) == 0
+    # rows per set: 65535 x 32 (the CUDA-core engines' row-tile grid axis)
+    assert capi.lib.cil_features_workspace_size(1, 2097120, 10, g, 0x3F, 5, 0) > 0
+    assert capi.lib.cil_features_workspace_size(1, 2097121, 10, g, 0x3F, 5, 0) == 0
+    assert capi.lib.cil_features_workspace_size(1, 10, 2097121, g, 0x3F, 5, 0) == 0
+    assert capi.lib.cil_bin_matrix_workspace_size(1, 2097121, 10, g, 1, 5, 0) == 0
