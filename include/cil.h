@@ -91,9 +91,11 @@ typedef enum {
  *  TC_I8     three-digit INT8 fixed point per row (x~ = sigma (2^16 h + 2^8 m + l), 22 bits), six
  *            exact int32 tcgen05 kind::i8 products per K step, a WORST-CASE interval (Cauchy-Schwarz
  *            on the dropped digit products, rigorous residual norms, directed rounding) — valid for
- *            every input; any K (exact chunks of 65536); L2 alone, or L2 + W12 + W12SUM from the
- *            augmented rows [x | D_x x | D_y x].  Column segments (SCIL blocks) need >= 21 columns
- *            (M <= 16 for W12 / W12SUM), else the measures run on the CUDA cores.
+ *            every input; K in exact chunks of 65536, up to 24 chunks per launch (L2 alone:
+ *            K <= 1 572 864; L2 + W12 + W12SUM from the augmented rows [x | D_x x | D_y x]: the
+ *            three blocks' chunks together), longer rows run on the CUDA cores.  Column segments
+ *            (SCIL blocks) need >= 21 columns (M <= 16 for W12 / W12SUM), else the measures run
+ *            on the CUDA cores.
  *  SIMT      FP32 differences on CUDA cores, FP64-flushed sums, rigorous rounding bounds.
  *  TC_3XBF16 / TC_3XTF32  float split (hi.hi + hi.lo + lo.hi, FP32 tensor accumulation): explicit
  *            options only, their bound is statistical (not worst-case). */

@@ -192,6 +192,16 @@ void plan_cuda_cores(Plan& pl, cil_engine engine) {
 // rigorous too.  The float split engines are explicit options only.
 constexpr int64_t kMinSegI8 = 21;
 bool i8_ok(int64_t col_seg, int64_t rowsB) { return col_seg >= rowsB || col_seg >= kMinSegI8; }
+// K segments of the INT8 Gram (launch_gram3: each phase in exact int32 chunks of <= 65536 bytes,
+// an empty phase counts one): longer rows than kG3MaxSeg segments hold run on the CUDA cores
+// (nph = 1: K <= 24 x 65536; three phases: about 8 x 65536 per block)
+int i8_segments(const cil_grid& g, bool aug) {
+    auto ch = [](int64_t n) { return n > 0 ? (int)((n + 65535) / 65536) : 1; };
+    const int64_t K = (int64_t)g.S * g.H * g.W, Kp = round_up(K, kTcBK);
+    if (!aug) return ch(Kp);
+    const int64_t Ky = (int64_t)g.S * (g.H - 1) * g.W;
+    return ch(Kp) + ch(Kp) + ch(round_up(Ky, kTcBK));
+}
 // The L2-type family (L2, W12, W12SUM) on the three-phase INT8 engine when the
 // request has W12 or W12SUM, the engine is AUTO / TC_I8, and the per-thread histograms fit
 // (column segments: >= 21 columns and M <= 16).
@@ -199,6 +209,7 @@ bool aug_ok(uint32_t mask, cil_engine engine, const cil_grid& g, int64_t col_seg
     if (!(mask & (CIL_W12 | CIL_W12SUM))) return false;
     if (engine != CIL_ENGINE_AUTO && engine != CIL_ENGINE_TC_I8) return false;
     if (g.W < 2) return false;
+    if (i8_segments(g, true) > kG3MaxSeg) return false;
     const bool seg = col_seg < rowsB;
     if (seg && (col_seg < kMinSegI8 || M > 16)) return false;
     return M <= 64;
@@ -218,7 +229,8 @@ Plan make_plan(uint32_t mask, cil_engine engine, const cil_grid& g, int64_t col_
         return pl;
     }
     pl.split = (engine == CIL_ENGINE_TC_3XTF32) ? 2 : (engine == CIL_ENGINE_TC_3XBF16) ? 1 : 3;
-    pl.tc = (mask & CIL_L2) && engine != CIL_ENGINE_SIMT && (pl.split != 3 || i8_ok(col_seg, rowsB));
+    pl.tc = (mask & CIL_L2) && engine != CIL_ENGINE_SIMT &&
+            (pl.split != 3 || (i8_ok(col_seg, rowsB) && i8_segments(g, false) <= kG3MaxSeg));
     pl.simt_mask = pl.tc ? (mask & ~(uint32_t)CIL_L2) : mask;
     pl.do_max = pl.simt_mask & (CIL_LINF | CIL_W1INF | CIL_W1INFSUM);
     pl.do_sum = pl.simt_mask & (CIL_L2 | CIL_W12SUM | CIL_W12);

@@ -60,6 +60,7 @@ constexpr int kMaxMeas = 6;
 constexpr int kMaxD = 192;       // n_meas * M for loglik (packed Cholesky factor in smem)
 constexpr int kSimtBK = 32;      // SIMT k-chunk (floats); region padding unit
 constexpr int kMax16BK = 64;     // max16.cu k-chunk (int16 elements); its region padding unit
+constexpr int kG3MaxSeg = 24;     // INT8 Gram: K segments (exact int32 chunks of <= 65536 per phase) per launch
 constexpr int kTcBK = 128;       // K padding of the tensor-core operands (128 int8 = one 128-B row)
 
 // Row sources: how panel row r of item p maps to a pattern in caller memory.

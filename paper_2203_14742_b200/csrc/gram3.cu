@@ -69,7 +69,7 @@ using tc::tmem_ld16;
 constexpr int KS = 128;         // K bytes per pipeline stage (one SWIZZLE_128B row)
 constexpr int AR = 128;         // A rows per CTA (M = 256 per CTA pair)
 constexpr int TILE_M = 256;
-constexpr int MAXSEG = 24;
+constexpr int MAXSEG = kG3MaxSeg;
 
 struct Params {
     int64_t rowsA, rowsB, a_off, b_off;

@@ -293,6 +293,23 @@ def test_loglik_notpd_and_large_D(cil, oracle_mod):
     np.testing.assert_allclose(out[0].cpu().numpy(), ref, rtol=0, atol=1e-6)
 
 
+@pytest.mark.parametrize("engine", ["AUTO", "TC_I8"])
+@pytest.mark.parametrize("grid,mask", [((2, 600, 600, 0.0), 0x3F), ((1, 1300, 1300, 0.0), 0x1)])
+def test_very_long_rows(cil, oracle_mod, engine, grid, mask):
+    """Rows beyond the INT8 Gram's 24 K-segments per launch (three-phase: 2 x 600 x 600; L2 only:
+    K = 1.69 M > 24 x 65536) run on the CUDA cores and still give the oracle's counts."""
+    O = oracle_mod
+    A = cilgen.make_set(31, 0, 3, grid[:3])
+    B = cilgen.make_set(31, 1, 4, grid[:3])
+    D = O.distance_matrix(A.numpy(), B.numpy(), grid, mask)
+    radii = np.array([np.sort(d.ravel())[::-1][[1, 4, 7, 10]] * np.array([1.0001, 1.0001, 0.9999, 0.9999])
+                      for d in D])
+    ref = O.features(A.numpy(), B.numpy(), grid, mask, radii, band=BAND)
+    c, y, st = _run_features(cil, A, B, grid, mask, radii, engine)
+    assert st[0] == 0
+    _check_counts(c[0], ref)
+
+
 @pytest.mark.parametrize("D", [1, 2, 7, 15, 31, 32, 33, 64])
 def test_loglik_batched_sizes_and_notpd(cil, oracle_mod, D):
     """Eq. (4) log-density over a batch of P = 9 items (the warp-per-item kernel for D <= 32 packs 4
