@@ -28,7 +28,9 @@
  *    A set (or a SCIL / training / bootstrap panel) holds at most 2 097 120 = 65535 x 32
  *    patterns (the CUDA-core engines' 32-row tiles on a grid axis); more is CIL_EINVAL
  *    (workspace queries return 0).  Larger sets: row blocks (cil_features is additive over
- *    them, as the multi-GPU split uses).
+ *    them, as the multi-GPU split uses).  The tensor-core engines pack at most 2^31 - 1 rows
+ *    per call (P times both sets' rows; TMA coordinates are int32): above, CIL_EUNSUPPORTED —
+ *    split the batch or use CIL_ENGINE_SIMT.
  *  - Thread-safe: no global mutable state besides a once-per-device kernel
  *    attribute setup (atomic), thread-local launch counters / diagnostics settings, one
  *    library-owned side stream (+ two events) per host thread and device for the concurrent

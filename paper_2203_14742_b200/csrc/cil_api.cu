@@ -444,6 +444,8 @@ cil_status run_engines(int P, const RowSrc& asrc, const RowSrc& bsrc, int64_t ro
                        uint8_t* binout = nullptr, bool keep_status = false,
                        unsigned long long* range = nullptr, int tile_skip = 0) {
     const int64_t K = (int64_t)g.S * g.H * g.W;
+    // TMA row coordinates are int32: the tensor-core engines take < 2^31 packed rows per call
+    if (pl.tc && (int64_t)P * (rowsA + rowsB) >= (1ll << 31)) return CIL_EUNSUPPORTED;
     BinParams bp{};
     bp.nq = sl.nq;
     bp.M = M;
