@@ -5,7 +5,11 @@
  * Conventions for every call:
  *  - Pointers are DEVICE pointers unless marked [host].  The caller owns every
  *    buffer; the library never allocates device memory.  Scratch comes from a
- *    caller-provided workspace sized by the matching *_workspace_size() call.
+ *    caller-provided workspace sized by the matching *_workspace_size() call.  It grows
+ *    with the pairs of a call: the packed operands (O((N + Nt) K)), plus for the max family
+ *    on the fixed-point engine 2 bytes per pair and region (C5: 20000^2 pairs -> 2.4 GB)
+ *    and the re-check list (32 B per 128 (pair, measure) cases + 8 MB): for set pairs far
+ *    beyond C5 call in row blocks of A (the counts are additive).
  *  - Calls are asynchronous on `stream` (a cudaStream_t passed as void*; NULL =
  *    legacy default stream).  They never synchronise the device and never allocate, so a
  *    call (or a whole step of calls) can be captured into a CUDA graph and replayed on new
