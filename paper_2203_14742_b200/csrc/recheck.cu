@@ -212,6 +212,11 @@ __device__ double measure(int k, const double sub[6], double w, double h) {
 __device__ __forceinline__ float amax4(float m, float a, float b, float c, float d) {
     return fmaxf(fmaxf(m, fmaxf(fabsf(a), fabsf(b))), fmaxf(fabsf(c), fabsf(d)));
 }
+#ifndef CIL_RK_EXP
+#define CIL_RK_EXP 0     // 1: the neighbour sweep for L-inf-only pairs too (experiment builds)
+#endif
+// GRAD = false (every listed measure of the pair is L-inf): the value block only, m_x = m_y = 0.
+template <bool GRAD>
 __device__ void max_subnorms32(const float* x, const float* y, const RecheckArgs& a, float out[3], float (*red)[8],
                                Ring* ring) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -228,6 +233,7 @@ __device__ void max_subnorms32(const float* x, const float* y, const RecheckArgs
                 const float4 xa = *reinterpret_cast<const float4*>(sx + l), yb = *reinterpret_cast<const float4*>(sy + l);
                 const float4 u = make_float4(xa.x - yb.x, xa.y - yb.y, xa.z - yb.z, xa.w - yb.w);
                 v[0] = amax4(v[0], u.x, u.y, u.z, u.w);
+                if (!GRAD) continue;
                 uint32_t c, hr;
                 const uint32_t sr = fw.div(e, c), sp = fh.div(sr, hr);
                 const bool g = a.gs == 0 || ((a.gs >> sp) & 1u);
@@ -246,7 +252,7 @@ __device__ void max_subnorms32(const float* x, const float* y, const RecheckArgs
     } else {
         const int SH = a.S * a.H;
         for (int sr = w; sr < SH; sr += 8) {
-            const bool grad = a.gs == 0 || ((a.gs >> (sr / H)) & 1u);
+            const bool grad = GRAD && (a.gs == 0 || ((a.gs >> (sr / H)) & 1u));
             const bool has_dy = grad && (sr % H) + 1 < H;
             const float* xr = x + (int64_t)sr * W;
             const float* yr = y + (int64_t)sr * W;
@@ -460,7 +466,8 @@ __global__ void __launch_bounds__(256, 4) k_recheck(RecheckArgs a) {
         const float* yb = row_ptr(a.bsrc, p, j);
         bool exact = true;
         if (!(kmask & 0x0Du)) {                              // max family only: FP32 interval first
-            max_subnorms32(xa, yb, a, m32, red32, rp);
+            if ((kmask & ~0x2u) || CIL_RK_EXP == 1) max_subnorms32<true>(xa, yb, a, m32, red32, rp);
+            else max_subnorms32<false>(xa, yb, a, m32, red32, rp);        // L-inf only: no neighbours
             if ((int)threadIdx.x < n) measure32((int)((s_w[threadIdx.x] >> 8) & 255u), m32, a.h, &s_d[threadIdx.x], &s_E[threadIdx.x]);
             __syncthreads();
             exact = false;
