@@ -20,3 +20,23 @@ def oracle_mod():
     from oracle import oracle as O
     O.build()
     return O
+
+
+def pytest_sessionfinish(session, exitstatus):
+    """With CIL_REPORT_BOUNDS=1 (a -DCIL_BOUNDS_CHECK build, tools/bounds_check.sh): report the
+    device-side bounds violations the whole GPU suite triggered, and fail the run on any."""
+    if not os.environ.get("CIL_REPORT_BOUNDS"):
+        return
+    try:
+        import torch
+        if not torch.cuda.is_available():
+            return
+        from paper_2203_14742_b200 import _capi
+        torch.cuda.synchronize()
+        v = int(_capi.lib.cil_diag_bounds_violations())
+    except Exception as e:                       # noqa: BLE001
+        print(f"\nbounds violations: unavailable ({e})")
+        return
+    print(f"\nbounds violations over the suite: {v} (-1 = not a bounds-checked build)")
+    if v != 0:
+        session.exitstatus = 1
