@@ -34,11 +34,14 @@ namespace {
 // by one thread with cp.async.bulk (TMA, 1-D) and an mbarrier per stage, RST stages in flight, so a
 // CTA keeps 3 x 2 x 8 KB of its pair's rows in flight while it computes, 4 CTAs per SM (2 CTAs with
 // 3 x 2 x 16 KB: slower; profiles/r02_recheck.txt)
-constexpr uint32_t RCH = 2048;
+#ifndef CIL_RK_EXP
+#define CIL_RK_EXP 0     // experiment builds: 1 neighbour sweep for L-inf-only pairs too; 2 two stages;
+#endif                   // 3 twice the CTAs; 4 chunks of 1024
+constexpr uint32_t RCH = CIL_RK_EXP == 4 ? 1024 : 2048;
 constexpr uint32_t RHALO = 256;      // each chunk also brings the next grid row (W <= RHALO): every x / y
                                      // neighbour of the chunk is in shared memory, the sweeps are branch-free
 constexpr uint32_t RSTR = RCH + RHALO;
-constexpr int RST = 3;
+constexpr int RST = CIL_RK_EXP == 2 ? 2 : 3;
 constexpr size_t kRingBytes = sizeof(float) * 2 * RSTR * RST;
 struct Ring {
     float* buf;        // [RST][2][RSTR] (x chunk + halo, y chunk + halo)
@@ -212,9 +215,6 @@ __device__ double measure(int k, const double sub[6], double w, double h) {
 __device__ __forceinline__ float amax4(float m, float a, float b, float c, float d) {
     return fmaxf(fmaxf(m, fmaxf(fabsf(a), fabsf(b))), fmaxf(fabsf(c), fabsf(d)));
 }
-#ifndef CIL_RK_EXP
-#define CIL_RK_EXP 0     // 1: the neighbour sweep for L-inf-only pairs too (experiment builds)
-#endif
 // GRAD = false (every listed measure of the pair is L-inf): the value block only, m_x = m_y = 0.
 template <bool GRAD>
 __device__ void max_subnorms32(const float* x, const float* y, const RecheckArgs& a, float out[3], float (*red)[8],
@@ -513,7 +513,7 @@ cudaError_t launch_recheck(const RecheckArgs& a, int64_t hist_elems, cudaStream_
     k_rk_scatter<<<nsm * 2, 256, 0, st>>>(a);
     static SmemAttrOnce attr;
     if (cudaError_t e = attr.ensure(k_recheck, (int)kRingBytes); e != cudaSuccess) return e;
-    k_recheck<<<nsm * 8, 256, kRingBytes, st>>>(a);
+    k_recheck<<<nsm * (CIL_RK_EXP == 3 ? 16 : 8), 256, kRingBytes, st>>>(a);
     note_launch(4);
     return cudaGetLastError();
 }
