@@ -358,7 +358,7 @@ CIL_API cil_status cil_synth_loglik_boot(int32_t P, const float* pools, int64_t 
  * distance |a_i - b_j| (it must contain the exact value for every pair).  TC_3XBF16 / TC_3XTF32:
  * d2E[i][j] = (the FP32 d^2, its statistical error bound E).  engine must be TC_3XBF16, TC_3XTF32 or TC_I8;
  * d2E [N][Nt][2] FP32 device; ws_bytes >= cil_features_workspace_size(1, N, Nt, g, CIL_L2,
- * 1, engine) + 512.
+ * 1, engine) + 512.  Rows the engine does not take (TC_I8: more than 24 K chunks) -> CIL_EUNSUPPORTED.
  * ------------------------------------------------------------------------ */
 CIL_API cil_status cil_diag_gram(const float* A, int64_t lda, int64_t N, const float* B, int64_t ldb,
                                  int64_t Nt, cil_grid g, cil_engine engine, float* d2E, void* ws,

@@ -1240,6 +1240,7 @@ cil_status cil_diag_gram(const float* A, int64_t lda, int64_t N, const float* B,
     if (K % 4 || lda % 4 || ldb % 4 || !aligned16(A) || !aligned16(B)) return CIL_EUNSUPPORTED;
     const Slots sl = slots_of(CIL_L2);
     const Plan pl = make_plan(CIL_L2, engine, g);
+    if (!pl.tc) return CIL_EUNSUPPORTED;                  // rows beyond the engine's K segments
     SegParams sp{N, Nt, 1, 1};
     const Layout L = make_layout(1, N, Nt, g, sl.nq, 1, pl, sp, 0);
     if (ws_bytes < L.total + 512) return CIL_ENOMEM;
