@@ -797,86 +797,95 @@ __device__ __forceinline__ void write_meta(float* out, float sg, float inv, cons
     out[5] = 0.f; out[6] = 0.f; out[7] = 0.f;
 }
 
-// One CTA per row, the whole row in registers (NV float4 per thread, NT threads): x~ = x - c, max,
-// quantise, store the three digit planes, exact digit sums.  Thread 0 prefetches the row pf_dist
-// CTAs ahead into L2 (cp.async.bulk.prefetch), so HBM keeps streaming while resident CTAs reduce /
-// quantise / store.
+// A CTA packs rpc consecutive rows of one item, each row whole in registers (NV float4 per thread,
+// NT threads): x~ = x - c, max, quantise, store the three digit planes, exact digit sums.  The item's
+// centre row is staged in shared memory once per CTA (re-reading it from L2 for every row cost ~16 %
+// of the pack: an experiment build without centre loads took the C2 pack 1.02 -> 0.86 ms); thread 0
+// prefetches the CTA's next row into L2 (cp.async.bulk.prefetch) while the current one is reduced /
+// quantised / stored.
 template <int NV, int NT>
 __global__ void __launch_bounds__(NT) k_pack3(RowSrc src, int64_t rows, int64_t K, int64_t Kp, const float* __restrict__ center,
                                               int8_t* __restrict__ planes, int64_t plane_stride, int64_t row0,
-                                              float* __restrict__ meta, int32_t* __restrict__ status, int64_t pf_dist) {
+                                              float* __restrict__ meta, int32_t* __restrict__ status, int rpc) {
+    extern __shared__ float4 cs[];                        // the item's centre row, NV * NT float4 (0 past K)
     const int64_t p = blockIdx.y;
-    const int64_t r = blockIdx.x;
-    const float* x = row_ptr(src, p, r);
+    const int64_t rb = (int64_t)blockIdx.x * rpc, re = min(rows, rb + rpc);
     const float* c = center + p * Kp;
-    const int64_t orow = row0 + p * rows + r;
-    if (threadIdx.x == 0 && pf_dist > 0) {
-        const int64_t lin = (int64_t)blockIdx.y * gridDim.x + blockIdx.x + pf_dist;
-        if (lin < (int64_t)gridDim.x * gridDim.y) {
-            const float* xn = row_ptr(src, lin / gridDim.x, lin % gridDim.x);
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(xn), "r"((uint32_t)(K * 4)) : "memory");
-        }
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+        const int64_t k = ((int64_t)i * NT + threadIdx.x) * 4;
+        cs[i * NT + threadIdx.x] = k < K ? __ldg(reinterpret_cast<const float4*>(c + k)) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
+    if (threadIdx.x == 0)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(row_ptr(src, p, rb)), "r"((uint32_t)(K * 4)) : "memory");
+    __syncthreads();
     __shared__ float red[NT / 32];
     __shared__ long long redl[NT / 32][6];
-    float4 v[NV];
-    float mx = 0.f;
-#pragma unroll
-    for (int i = 0; i < NV; ++i) {
-        const int64_t k = ((int64_t)i * NT + threadIdx.x) * 4;
-        if (k < K) {
-            const float4 xv = __ldg(reinterpret_cast<const float4*>(x + k));
-            const float4 cv = __ldg(reinterpret_cast<const float4*>(c + k));
-            v[i] = make_float4(xv.x - cv.x, xv.y - cv.y, xv.z - cv.z, xv.w - cv.w);
-        } else {
-            v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-        mx = absmax3_nan(absmax3_nan(mx, v[i].x, v[i].y), v[i].z, v[i].w);
-    }
-    for (int o = 16; o > 0; o >>= 1) {
-        const float t = __shfl_xor_sync(0xffffffffu, mx, o);
-        asm("max.NaN.f32 %0, %0, %1;" : "+f"(mx) : "f"(t));
-    }
     const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
-    if (ln == 0) red[w] = mx;
-    __syncthreads();
-    mx = 0.f;
+    for (int64_t r = rb; r < re; ++r) {
+        const float* x = row_ptr(src, p, r);
+        const int64_t orow = row0 + p * rows + r;
+        if (threadIdx.x == 0 && r + 1 < re)             // the CTA's next row streams into L2 meanwhile
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(row_ptr(src, p, r + 1)),
+                         "r"((uint32_t)(K * 4)) : "memory");
+        float4 v[NV];
+        float mx = 0.f;
 #pragma unroll
-    for (int i = 0; i < NT / 32; ++i) asm("max.NaN.f32 %0, %0, %1;" : "+f"(mx) : "f"(red[i]));
-    const bool nonfinite = !(mx <= 3.0e38f);                    // NaN or Inf somewhere in the row
-    const bool ok = mx >= kMinMax && mx <= kMaxMax;
-    const bool exact_only = mx > 0.f && !ok;
-    const float sg = ok ? mx / kQ : 1.f;
-    const float inv = 1.f / sg;
-    int S[6] = {0, 0, 0, 0, 0, 0};
-#pragma unroll
-    for (int i = 0; i < NV; ++i) {
-        const int64_t k = ((int64_t)i * NT + threadIdx.x) * 4;
-        if (k >= Kp) continue;
-        uint32_t wh = 0, wm = 0, wl = 0;
-        if (ok) quant4(v[i], inv, wh, wm, wl, S);
-        int8_t* o = planes + orow * Kp + k;
-        CIL_CHECK(orow * Kp + k + 4 <= plane_stride);
-        *reinterpret_cast<uint32_t*>(o) = wh;
-        *reinterpret_cast<uint32_t*>(o + plane_stride) = wm;
-        *reinterpret_cast<uint32_t*>(o + 2 * plane_stride) = wl;
-    }
-#pragma unroll
-    for (int i = 0; i < 6; ++i) {
-        long long a = S[i];
-        for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-        if (ln == 0) redl[w][i] = a;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        long long Sl[6];
-        for (int i = 0; i < 6; ++i) {
-            long long a = 0;
-            for (int j = 0; j < NT / 32; ++j) a += redl[j][i];
-            Sl[i] = a;
+        for (int i = 0; i < NV; ++i) {
+            const int64_t k = ((int64_t)i * NT + threadIdx.x) * 4;
+            if (k < K) {
+                const float4 xv = __ldg(reinterpret_cast<const float4*>(x + k));
+                const float4 cv = cs[i * NT + threadIdx.x];
+                v[i] = make_float4(xv.x - cv.x, xv.y - cv.y, xv.z - cv.z, xv.w - cv.w);
+            } else {
+                v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            mx = absmax3_nan(absmax3_nan(mx, v[i].x, v[i].y), v[i].z, v[i].w);
         }
-        write_meta(meta + orow * 8, sg, inv, Sl, (double)K, 0.0, exact_only, 0.0);
-        if (nonfinite) atomicOr(&status[p], CIL_ITEM_NONFINITE);
+        for (int o = 16; o > 0; o >>= 1) {
+            const float t = __shfl_xor_sync(0xffffffffu, mx, o);
+            asm("max.NaN.f32 %0, %0, %1;" : "+f"(mx) : "f"(t));
+        }
+        if (ln == 0) red[w] = mx;
+        __syncthreads();
+        mx = 0.f;
+#pragma unroll
+        for (int i = 0; i < NT / 32; ++i) asm("max.NaN.f32 %0, %0, %1;" : "+f"(mx) : "f"(red[i]));
+        const bool nonfinite = !(mx <= 3.0e38f);                    // NaN or Inf somewhere in the row
+        const bool ok = mx >= kMinMax && mx <= kMaxMax;
+        const bool exact_only = mx > 0.f && !ok;
+        const float sg = ok ? mx / kQ : 1.f;
+        const float inv = 1.f / sg;
+        int S[6] = {0, 0, 0, 0, 0, 0};
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+            const int64_t k = ((int64_t)i * NT + threadIdx.x) * 4;
+            if (k >= Kp) continue;
+            uint32_t wh = 0, wm = 0, wl = 0;
+            if (ok) quant4(v[i], inv, wh, wm, wl, S);
+            int8_t* o = planes + orow * Kp + k;
+            CIL_CHECK(orow * Kp + k + 4 <= plane_stride);
+            *reinterpret_cast<uint32_t*>(o) = wh;
+            *reinterpret_cast<uint32_t*>(o + plane_stride) = wm;
+            *reinterpret_cast<uint32_t*>(o + 2 * plane_stride) = wl;
+        }
+#pragma unroll
+        for (int i = 0; i < 6; ++i) {
+            long long a = S[i];
+            for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+            if (ln == 0) redl[w][i] = a;
+        }
+        __syncthreads();      // (red is re-written only after every thread has passed this barrier)
+        if (threadIdx.x == 0) {
+            long long Sl[6];
+            for (int i = 0; i < 6; ++i) {
+                long long a = 0;
+                for (int j = 0; j < NT / 32; ++j) a += redl[j][i];
+                Sl[i] = a;
+            }
+            write_meta(meta + orow * 8, sg, inv, Sl, (double)K, 0.0, exact_only, 0.0);
+            if (nonfinite) atomicOr(&status[p], CIL_ITEM_NONFINITE);
+        }
     }
 }
 
@@ -1239,36 +1248,32 @@ cudaError_t launch_pack3(int P, const RowSrc& src, int64_t rows, int64_t K, int6
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    // L2 prefetch distance: half a wave of resident CTAs ahead
-    auto pf = [&](const void* fn, int nt) {
+    // rows per CTA: the centre row is read once per CTA; about eight waves of resident CTAs remain
+    auto rpc_for = [&](const void* fn, int nt, size_t smem) {
         int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, nt, 0);
-        return (int64_t)nsm * (per_sm > 0 ? per_sm : 1) / 2;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, nt, smem);
+        const int64_t ctas = (int64_t)nsm * (per_sm > 0 ? per_sm : 1) * 8;
+        const int64_t r = (rows * P + ctas - 1) / ctas;
+        return (int)(r < 1 ? 1 : r > 16 ? 16 : r);
     };
-#define PACK3(NV, NT)                                                                                             \
-    g3::k_pack3<NV, NT><<<grid, NT, 0, st>>>(src, rows, K, Kp, center, planes, plane_stride, row0, meta, status, \
-                                             pf((const void*)g3::k_pack3<NV, NT>, NT))
+#define PACK3(NV, NT)                                                                                              \
+    do {                                                                                                           \
+        static SmemAttrOnce attr_;                                                                                 \
+        const size_t smem_ = sizeof(float4) * (NV) * (NT);                                                         \
+        if (cudaError_t e_ = attr_.ensure(g3::k_pack3<NV, NT>, (int)smem_); e_ != cudaSuccess) return e_;          \
+        const int rpc_ = rpc_for((const void*)g3::k_pack3<NV, NT>, NT, smem_);                                    \
+        dim3 g_((unsigned)((rows + rpc_ - 1) / rpc_), (unsigned)P);                                                \
+        g3::k_pack3<NV, NT><<<g_, NT, smem_, st>>>(src, rows, K, Kp, center, planes, plane_stride, row0, meta,     \
+                                                   status, rpc_);                                                  \
+    } while (0)
     if (Kp <= 1024)
         PACK3(1, 256);
     else if (Kp <= 4096)
         PACK3(4, 256);
     else if (Kp <= 8192)
         PACK3(16, 128);          // C2: 1.008-1.012 ms vs 1.045-1.057 for 8 x 256 (round 2, three planes)
-    else if (Kp <= 16384) {
-#if CIL_PACK_EXP == 1
-        PACK3(32, 128);
-#elif CIL_PACK_EXP == 2
-        g3::k_pack3<16, 256><<<grid, 256, 0, st>>>(src, rows, K, Kp, center, planes, plane_stride, row0, meta, status, 0);
-#elif CIL_PACK_EXP == 3
-        g3::k_pack3<16, 256><<<grid, 256, 0, st>>>(src, rows, K, Kp, center, planes, plane_stride, row0, meta, status,
-                                                     2 * pf((const void*)g3::k_pack3<16, 256>, 256));
-#elif CIL_PACK_EXP == 4
-        g3::k_pack3<16, 256><<<grid, 256, 0, st>>>(src, rows, K, Kp, center, planes, plane_stride, row0, meta, status,
-                                                     pf((const void*)g3::k_pack3<16, 256>, 256) / 2);
-#else
+    else if (Kp <= 16384)
         PACK3(16, 256);          // C4: 6.03-6.09 ms vs 6.40-6.42 for 8 x 512 (round 2, three planes)
-#endif
-    }
     else if (Kp <= 32768)
         PACK3(8, 1024);
     else
