@@ -828,6 +828,7 @@ __global__ void __launch_bounds__(NT) k_pack3(RowSrc src, int64_t rows, int64_t 
         if (threadIdx.x == 0 && r + 1 < re)             // the CTA's next row streams into L2 meanwhile
             asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(row_ptr(src, p, r + 1)),
                          "r"((uint32_t)(K * 4)) : "memory");
+
         float4 v[NV];
         float mx = 0.f;
 #pragma unroll
@@ -1236,9 +1237,6 @@ __global__ void __launch_bounds__(512, 2) k_pack3_aug4(RowSrc src, int64_t rows,
 }  // namespace g3
 
 // ------------------------------------------------------------------ host side
-#ifndef CIL_PACK_EXP
-#define CIL_PACK_EXP 0   // pack shape experiments (tools/simt_var_build.sh FILE=gram3); 0 = product
-#endif
 cudaError_t launch_pack3(int P, const RowSrc& src, int64_t rows, int64_t K, int64_t Kp, const float* center,
                          int8_t* planes, int64_t plane_stride, int64_t row0, float* meta, int32_t* status,
                          cudaStream_t st) {
@@ -1248,11 +1246,13 @@ cudaError_t launch_pack3(int P, const RowSrc& src, int64_t rows, int64_t K, int6
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    // rows per CTA: the centre row is read once per CTA; about eight waves of resident CTAs remain
+    // rows per CTA: the centre row is read once per CTA; about 16 waves of resident CTAs remain (C2:
+    // 6 rows per CTA; A/B: 4, 8, 32, 64 waves and a cap of 8 rows were slower or equal; without the
+    // next-row prefetch the C2 pack takes 1.07 ms, with a second row prefetched 1.22 ms)
     auto rpc_for = [&](const void* fn, int nt, size_t smem) {
         int per_sm = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, nt, smem);
-        const int64_t ctas = (int64_t)nsm * (per_sm > 0 ? per_sm : 1) * 8;
+        const int64_t ctas = (int64_t)nsm * (per_sm > 0 ? per_sm : 1) * 16;
         const int64_t r = (rows * P + ctas - 1) / ctas;
         return (int)(r < 1 ? 1 : r > 16 ? 16 : r);
     };
