@@ -97,6 +97,9 @@ struct Params {
     int64_t hist_elems;                // bounds-checked builds only
 };
 
+#ifndef CIL_G3_NARROW
+#define CIL_G3_NARROW 1  // ragged last column tile at MMA N = round_up(columns, 16) (0: experiment builds)
+#endif
 #ifndef CIL_G3_WIDE
 #define CIL_G3_WIDE 0   // 0: six N = TN MMAs per K step (product); 1: four wide MMAs (experiment builds)
 #endif
@@ -216,6 +219,16 @@ __device__ __forceinline__ void tile_of(const Params& prm, int u, int& mt, int& 
         u -= c;
     }
     mt = nt = 0;
+}
+
+// MMA N of column tile nt: the ragged last tile issues only round_up(its columns, 16) (M = 256 takes
+// N % 16 == 0; each CTA of the pair then holds N / 2 B rows) — C4's swapped SCIL panel: 550 columns
+// = 4 x 128 + 38 run the last tile at N = 48
+template <int TN>
+__device__ __forceinline__ int tile_n(const Params& prm, int nt) {
+    if (!CIL_G3_NARROW) return TN;
+    const int64_t left = prm.rowsB - (int64_t)nt * TN;
+    return left >= TN ? TN : (int)((left + 15) / 16 * 16);
 }
 
 // b = #{m : v < T_m} over decreasing thresholds T[0..MAXM) padded with -inf to 2 MAXM
@@ -625,7 +638,8 @@ k_gram3(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensor
                 int mt, nt;
                 tile_of(prm, t % prm.tiles_act, mt, nt);
                 const int ya = (int)(prm.a_off + p * prm.rowsA + (int64_t)mt * TILE_M + rank * AR);
-                const int yb = (int)(prm.b_off + p * prm.rowsB + (int64_t)nt * TN + (GG::WIDE ? 0 : rank * GG::BR));
+                const int yb = (int)(prm.b_off + p * prm.rowsB + (int64_t)nt * TN +
+                                     (GG::WIDE ? 0 : rank * (tile_n<TN>(prm, nt) / 2)));
                 for (int kb = 0; kb < n_kb; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     unsigned char* st = stages + stage * GG::STAGE;
@@ -660,6 +674,12 @@ k_gram3(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensor
             int stage = 0;
             uint32_t phase = 0, tph = 0;
             for (int t = cluster_id; t < total_tiles; t += n_clusters) {
+                uint32_t idt = id;
+                if constexpr (!GG::WIDE) {
+                    int mt_, nt_;
+                    tile_of(prm, t % prm.tiles_act, mt_, nt_);
+                    idt = idesc_i8(TILE_M, tile_n<TN>(prm, nt_));
+                }
                 for (int s = 0; s < prm.nseg; ++s) {
                     mbar_wait_cluster(&tempty[0], tph ^ 1);
                     fence_after();
@@ -691,12 +711,12 @@ k_gram3(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensor
                             for (int k = 0; k < KS / 32; ++k) {          // 32 int8 of K per MMA
                                 const uint64_t adv = (uint64_t)(k * 2);  // +32 B in the start-address field
                                 const uint32_t acc = (kb != kb0 || k != 0) ? 1u : 0u;
-                                mma_i8(d32, ah + adv, bh + adv, id, acc);
-                                mma_i8(d24, ah + adv, bm + adv, id, acc);
-                                mma_i8(d24, am + adv, bh + adv, id, 1u);
-                                mma_i8(d16, ah + adv, bl + adv, id, acc);
-                                mma_i8(d16, am + adv, bm + adv, id, 1u);
-                                mma_i8(d16, al + adv, bh + adv, id, 1u);
+                                mma_i8(d32, ah + adv, bh + adv, idt, acc);
+                                mma_i8(d24, ah + adv, bm + adv, idt, acc);
+                                mma_i8(d24, am + adv, bh + adv, idt, 1u);
+                                mma_i8(d16, ah + adv, bl + adv, idt, acc);
+                                mma_i8(d16, am + adv, bm + adv, idt, 1u);
+                                mma_i8(d16, al + adv, bh + adv, idt, 1u);
                             }
                         }
                         tc::mma_commit<2>(&empty[stage]);
