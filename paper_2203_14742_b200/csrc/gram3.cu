@@ -97,6 +97,12 @@ struct Params {
     int64_t hist_elems;                // bounds-checked builds only
 };
 
+#ifndef CIL_PACK_WAVES
+#define CIL_PACK_WAVES 16    // k_pack3 CTAs launched per resident CTA slot (rows per CTA follow)
+#endif
+#ifndef CIL_PACK_STRIDED
+#define CIL_PACK_STRIDED 1   // k_pack3: rows j + k G per CTA (0: contiguous row blocks, experiment builds)
+#endif
 #ifndef CIL_G3_NARROW
 #define CIL_G3_NARROW 1  // ragged last column tile at MMA N = round_up(columns, 16) (0: experiment builds)
 #endif
@@ -829,7 +835,13 @@ __global__ void __launch_bounds__(NT) k_pack3(RowSrc src, int64_t rows, int64_t 
                                               float* __restrict__ meta, int32_t* __restrict__ status, int rpc) {
     extern __shared__ float4 cs[];                        // the item's centre row, NV * NT float4 (0 past K)
     const int64_t p = blockIdx.y;
-    const int64_t rb = (int64_t)blockIdx.x * rpc, re = min(rows, rb + rpc);
+#if CIL_PACK_STRIDED
+    // CTA j of the item packs rows j, j + G, j + 2G, ... (G = gridDim.x): the CTAs resident at any
+    // moment work on neighbouring rows (a compact DRAM frontier), each still reusing its centre row
+    const int64_t G = gridDim.x, rb = blockIdx.x, re = rows;
+#else
+    const int64_t G = 1, rb = (int64_t)blockIdx.x * rpc, re = min(rows, rb + rpc);
+#endif
     const float* c = center + p * Kp;
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
@@ -842,11 +854,11 @@ __global__ void __launch_bounds__(NT) k_pack3(RowSrc src, int64_t rows, int64_t 
     __shared__ float red[NT / 32];
     __shared__ long long redl[NT / 32][6];
     const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
-    for (int64_t r = rb; r < re; ++r) {
+    for (int64_t r = rb; r < re; r += G) {
         const float* x = row_ptr(src, p, r);
         const int64_t orow = row0 + p * rows + r;
-        if (threadIdx.x == 0 && r + 1 < re)             // the CTA's next row streams into L2 meanwhile
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(row_ptr(src, p, r + 1)),
+        if (threadIdx.x == 0 && r + G < re)             // the CTA's next row streams into L2 meanwhile
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(row_ptr(src, p, r + G)),
                          "r"((uint32_t)(K * 4)) : "memory");
 
         float4 v[NV];
@@ -1272,7 +1284,7 @@ cudaError_t launch_pack3(int P, const RowSrc& src, int64_t rows, int64_t K, int6
     auto rpc_for = [&](const void* fn, int nt, size_t smem) {
         int per_sm = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, nt, smem);
-        const int64_t ctas = (int64_t)nsm * (per_sm > 0 ? per_sm : 1) * 16;
+        const int64_t ctas = (int64_t)nsm * (per_sm > 0 ? per_sm : 1) * CIL_PACK_WAVES;
         const int64_t r = (rows * P + ctas - 1) / ctas;
         return (int)(r < 1 ? 1 : r > 16 ? 16 : r);
     };
