@@ -91,16 +91,19 @@ __global__ void __launch_bounds__(256) k_range16(RowSrc src, int64_t rows, AugGe
     const int64_t p = blockIdx.y, r = blockIdx.x;
     const float* x = row_ptr(src, p, r);
     float hi0 = -INFINITY, lo0 = INFINITY, nfa = 0.f;
-    for (int64_t k = (int64_t)threadIdx.x * 4; k < g.K; k += 1024) {
-        const float4 v = __ldg(reinterpret_cast<const float4*>(x + k));
-        nfa = fmaf(v.x, 0.f, fmaf(v.y, 0.f, fmaf(v.z, 0.f, fmaf(v.w, 0.f, nfa))));
-        hi0 = fmaxf(fmaxf(hi0, v.x), fmaxf(fmaxf(v.y, v.z), v.w));
-        lo0 = fminf(fminf(lo0, v.x), fminf(fminf(v.y, v.z), v.w));
-    }
     double hx = -INFINITY, lx = INFINITY, hy = -INFINITY, ly = INFINITY;
     const int W = g.W, H = g.H, SH = g.S * g.H;
     const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
-    if (g.nreg >= 2 && (W & 3) == 0 && g.K < (1ll << 31)) {
+    const bool flat = g.nreg >= 2 && (W & 3) == 0 && g.K < (1ll << 31);
+    if (!flat) {
+        for (int64_t k = (int64_t)threadIdx.x * 4; k < g.K; k += 1024) {
+            const float4 v = __ldg(reinterpret_cast<const float4*>(x + k));
+            nfa = fmaf(v.x, 0.f, fmaf(v.y, 0.f, fmaf(v.z, 0.f, fmaf(v.w, 0.f, nfa))));
+            hi0 = fmaxf(fmaxf(hi0, v.x), fmaxf(fmaxf(v.y, v.z), v.w));
+            lo0 = fminf(fminf(lo0, v.x), fminf(fminf(v.y, v.z), v.w));
+        }
+    }
+    if (flat) {                       // one sweep: the value range rides along with the derivative ranges
         // flat float4 sweep: 4 elements of one grid row per thread, the x neighbour of the 4th from
         // the next lane (lane 31: a load), the y neighbours one grid row on (an L1 / L2 hit)
         const uint32_t K = (uint32_t)g.K, Wu = (uint32_t)W, Hu = (uint32_t)H;
@@ -112,6 +115,9 @@ __global__ void __launch_bounds__(256) k_range16(RowSrc src, int64_t rows, AugGe
             if (ok) v = __ldg(reinterpret_cast<const float4*>(x + e));
             float nxv = __shfl_down_sync(0xffffffffu, v.x, 1);
             if (!ok) continue;
+            nfa = fmaf(v.x, 0.f, fmaf(v.y, 0.f, fmaf(v.z, 0.f, fmaf(v.w, 0.f, nfa))));
+            hi0 = fmaxf(fmaxf(hi0, v.x), fmaxf(fmaxf(v.y, v.z), v.w));
+            lo0 = fminf(fminf(lo0, v.x), fminf(fminf(v.y, v.z), v.w));
             uint32_t c, hr;
             const uint32_t sr = fw.div(e, c), sp = fh.div(sr, hr);
             if (!(g.gs == 0 || ((g.gs >> sp) & 1u))) continue;     // species mask (R18): 0 derivatives
