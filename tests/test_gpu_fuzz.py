@@ -10,6 +10,8 @@ oracle's band, the log-likelihood within 1e-6 of the oracle's tail on that Y, an
 whole Alg. 3 when the two Y agree; the bin matrix (Alg. A1 / A2) must give #{m : d < R_m} up to the
 same band.  The point is the shapes nobody picked by hand: ragged tails in every dimension.
 """
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -22,6 +24,13 @@ BAND = 1e-6
 ENGINES = ["SIMT", "TC_3XBF16", "TC_3XTF32", "TC_I8", "AUTO"]
 PROFILES = ["GM", "FHN", "scaled"]
 EDGE_ROWS = [1, 2, 31, 63, 64, 65, 127, 128, 129, 191, 255, 256, 257]
+
+
+def _cases(start, n):
+    """Case numbers of one fuzz family: start .. start + n - 1, plus (CIL_FUZZ_ROUNDS = R > 1, a
+    longer soak run) R - 1 further blocks of fresh draws at k * 100000 + start, k = 1 .. R - 1."""
+    rounds = max(1, int(os.environ.get("CIL_FUZZ_ROUNDS", "1")))
+    return [k * 100000 + c for k in range(rounds) for c in range(start, start + n)]
 
 
 @pytest.fixture(scope="module")
@@ -76,7 +85,7 @@ def _radii(D, M, lo_q, hi_q):
     return np.array(out)
 
 
-@pytest.mark.parametrize("case", range(100))
+@pytest.mark.parametrize("case", _cases(0, 100))
 def test_fuzz_features(cil, oracle_mod, case):
     O = oracle_mod
     c = _draw_case(case)
@@ -101,7 +110,7 @@ def test_fuzz_features(cil, oracle_mod, case):
         np.testing.assert_array_equal(y[p], counts[p] / float(c["N"] * c["Nt"]))
 
 
-@pytest.mark.parametrize("case", range(100, 130))
+@pytest.mark.parametrize("case", _cases(100, 30))
 def test_fuzz_bin_matrix(cil, oracle_mod, case):
     O = oracle_mod
     c = _draw_case(case)
@@ -127,7 +136,7 @@ def test_fuzz_bin_matrix(cil, oracle_mod, case):
             assert not bad.any(), (c, p, q, np.argwhere(bad)[:5].tolist())
 
 
-@pytest.mark.parametrize("case", range(200, 224))
+@pytest.mark.parametrize("case", _cases(200, 24))
 def test_fuzz_synth(cil, oracle_mod, case):
     O = oracle_mod
     c = _draw_case(case)
@@ -181,7 +190,7 @@ def test_fuzz_synth(cil, oracle_mod, case):
                 np.testing.assert_allclose(out[p].cpu().numpy(), ref, rtol=0, atol=1e-6, err_msg=str(c))
 
 
-@pytest.mark.parametrize("case", range(300, 316))
+@pytest.mark.parametrize("case", _cases(300, 16))
 def test_fuzz_train_vectors(cil, oracle_mod, case):
     """Alg. 1 / Alg. 2 training vectors on random shapes: the k < l
     subset blocks of one panel, each within the oracle's band counts."""
@@ -205,7 +214,7 @@ def test_fuzz_train_vectors(cil, oracle_mod, case):
         assert np.all(ref["lo"] <= got) and np.all(got <= ref["hi"]), (c, p, n_ens, N)
 
 
-@pytest.mark.parametrize("case", range(400, 416))
+@pytest.mark.parametrize("case", _cases(400, 16))
 def test_fuzz_distance_range_and_radii(cil, oracle_mod, case):
     """(min positive, max) distance per measure (reading R16) and the radii laws
     on random shapes, including sets that share rows (zero distances excluded from the minimum)."""
@@ -228,7 +237,7 @@ def test_fuzz_distance_range_and_radii(cil, oracle_mod, case):
                                        err_msg=str(c))
 
 
-@pytest.mark.parametrize("case", range(500, 512))
+@pytest.mark.parametrize("case", _cases(500, 12))
 def test_fuzz_synth_boot(cil, oracle_mod, case):
     """Alg. A2 on random shapes and draws: replicate vectors within the band
     (resampled sets built explicitly by the oracle), the tail within 1e-6."""
@@ -274,7 +283,7 @@ def test_fuzz_synth_boot(cil, oracle_mod, case):
                 np.testing.assert_allclose(out[p].cpu().numpy(), ref, rtol=0, atol=1e-6, err_msg=str(c))
 
 
-@pytest.mark.parametrize("case", range(600, 610))
+@pytest.mark.parametrize("case", _cases(600, 10))
 def test_fuzz_large_K(cil, oracle_mod, case):
     """Long patterns (K up to ~150 k: the INT8 engines' 65536-element chunks, ragged in K) with
     few rows, all six measures on some cases, against the oracle's band counts."""
