@@ -11,6 +11,8 @@ lo <= gpu <= hi, where lo / hi count the pairs below R (1 -/+ 1e-6).
 This is the regime in which an error bound that is only statistical fails: the two rows'
 rounding errors (and low quantisation digits) coincide instead of averaging out.
 """
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -25,6 +27,9 @@ GRIDS = {"1d_64x2": (2, 1, 64, 0.0), "64x64x2": (2, 64, 64, 0.0), "128x128": (1,
 ROWS = {"1d_64x2": 48, "64x64x2": 24, "128x128": 16}
 PROFILES = ["GM", "FHN", "scaled"]
 EPS = [0.0, 1e-6, 1e-4, 1e-3, 1e-2]
+# seeds of the near-duplicate sets: one by default; CIL_NEARDUP_ROUNDS = R > 1 (a longer soak run)
+# adds R - 1 further seeds
+SEEDS = [20314742 + 7919 * k for k in range(max(1, int(os.environ.get("CIL_NEARDUP_ROUNDS", "1"))))]
 
 
 @pytest.fixture(scope="module")
@@ -57,13 +62,14 @@ def _check(gpu, ref, what):
 @pytest.mark.parametrize("engine", ENGINES)
 @pytest.mark.parametrize("profile", PROFILES)
 @pytest.mark.parametrize("gname", list(GRIDS))
-def test_near_duplicates_all_measures(cil, oracle_mod, engine, profile, gname):
+@pytest.mark.parametrize("seed", SEEDS)
+def test_near_duplicates_all_measures(cil, oracle_mod, engine, profile, gname, seed):
     O = oracle_mod
     grid = GRIDS[gname]
     mask, M = 0x3F, 12
     dev = torch.device("cuda")
     for eps in EPS:
-        A, B = near_dup_sets(grid, profile, eps, ROWS[gname])
+        A, B = near_dup_sets(grid, profile, eps, ROWS[gname], seed)
         Ad, Bd = A.to(dev), B.to(dev)
         rng, st0 = cil.distance_range(Ad, Bd, grid, mask)
         radii, st1 = cil.radii_from_range(rng, M, "power", 1e-3)
@@ -147,7 +153,8 @@ def test_recheck_list_overflow_fallback(cil, oracle_mod, engine, mode):
 
 @pytest.mark.parametrize("engine", ENGINES)
 @pytest.mark.parametrize("kind", ["binary", "quantised"])
-def test_binary_and_quantised_patterns(cil, oracle_mod, engine, kind):
+@pytest.mark.parametrize("seed", [777 + k for k in range(len(SEEDS))])
+def test_binary_and_quantised_patterns(cil, oracle_mod, engine, kind, seed):
     """Thresholded (0/1) and coarsely quantised (multiples of 1/8) patterns: many pairs
     share most of their values exactly, equal distances are frequent (ties land in the band), and
     the low digits of two rows coincide — the regime a statistical bound misjudges."""
@@ -155,8 +162,8 @@ def test_binary_and_quantised_patterns(cil, oracle_mod, engine, kind):
     grid = (2, 32, 32, 0.0)
     mask, M = 0x3F, 12
     dev = torch.device("cuda")
-    A = cilgen.make_set(777, 0, 40, grid[:3], "FHN")
-    B = cilgen.make_set(777, 1, 36, grid[:3], "FHN")
+    A = cilgen.make_set(seed, 0, 40, grid[:3], "FHN")
+    B = cilgen.make_set(seed, 1, 36, grid[:3], "FHN")
     if kind == "binary":
         A, B = (A > 0.1).float(), (B > 0.1).float()
     else:
