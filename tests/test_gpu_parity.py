@@ -400,6 +400,33 @@ def test_c2_full_item_vs_oracle(cil, oracle_mod, engine):
     assert np.all((yy >= 0) & (yy <= 1)) and np.all(np.diff(yy, axis=-1) <= 0)
 
 
+def test_c2_bench_workload_every_item_vs_oracle(cil, oracle_mod):
+    """The bench's whole C2 batch (rank 0: 100 set pairs of 500 x 500, 64x64x2, L2, M = 15, the
+    pilot-block power-law radii as bench.py builds them, default engine) in the one batched launch
+    `bench.py` times: every item's counts within the oracle's band counts (~45 s of oracle time).
+    Inputs built as bench.py builds them (same seeds)."""
+    O = oracle_mod
+    dev = torch.device("cuda")
+    grid, P, N = (2, 64, 64), 100, 500
+    seed = cilgen.config_seed(2)
+    A = torch.stack([cilgen.make_set(seed, 2 * p, N, grid, device=dev) for p in range(P)])
+    B = torch.stack([cilgen.make_set(seed, 2 * p + 1, N, grid, device=dev) for p in range(P)])
+    # bench.py pilot_radii: power law over the 64 x 64 pilot block of set pair 0 (PAPER.md:109)
+    a0 = cilgen.make_set(seed, 0, 64, grid).reshape(64, -1).double().numpy()
+    b0 = cilgen.make_set(seed, 1, 64, grid).reshape(64, -1).double().numpy()
+    d = O.distance_matrix(a0, b0, grid + (0.0,), 0x1)
+    d = d[d > 0]
+    R0, RM = float(d.max()) * 1.001, float(d.min()) * 0.999
+    radii = R0 * (RM / R0) ** (np.arange(1, 16) / 15)
+    c, y, st = cil.features(A, B, grid + (0.0,), 0x1, torch.tensor(radii[None, :], device=dev))
+    torch.cuda.synchronize()
+    assert int(st.abs().sum()) == 0
+    c = c.cpu().numpy()
+    for p in range(P):
+        ref = O.features(A[p].cpu().numpy(), B[p].cpu().numpy(), grid + (0.0,), 0x1, radii, band=BAND)
+        _check_counts(c[p], ref)
+
+
 # ------------------------------------------------------------------ L2-type family on tensor cores
 @pytest.mark.parametrize("engine", ["AUTO", "TC_I8"])
 def test_l2_family_tensor_cores_vs_oracle(cil, oracle_mod, engine):
