@@ -717,7 +717,7 @@ def test_synth_c4_shape_swapped_panels(cil, oracle_mod, mask):
 def test_c4_full_theta_vs_oracle(cil, oracle_mod):
     """C4 at full size in the bench's launch configuration (pools of 1000 patterns of 128x128,
     n_ens = 10, 50 + 50, M = 13, swapped panels and 192-column tiles, several proposals in one
-    launch); proposal 0 against the oracle's Alg. 3: every vector within the band, loglik."""
+    launch); every proposal against the oracle's Alg. 3: every vector within the band, loglik."""
     O = oracle_mod
     dev = torch.device("cuda")
     grid = (1, 128, 128, 0.0)
@@ -738,20 +738,23 @@ def test_c4_full_theta_vs_oracle(cil, oracle_mod):
     torch.cuda.synchronize()
     assert int(st.max()) == 0
     N = N_set + Nt
-    cg = np.rint(Y[0].cpu().numpy() * N_set * Nt).astype(np.int64)
     dat = data.cpu().numpy()
-    v = 0
-    for k in range(n_ens):
-        for l in range(n_ens):
-            r = O.features(pool0[k * N:k * N + N_set], pool0[l * N + N_set:(l + 1) * N], grid, 0x1, r1[None],
-                           band=BAND)
-            assert np.all(r["lo"][0] <= cg[v]) and np.all(cg[v] <= r["hi"][0]), (k, l)
-            v += 1
-    r = O.features(dat, pool0[0 * N + N_set:N], grid, 0x1, r1[None], band=BAND)
-    assert np.all(r["lo"][0] <= cg[v]) and np.all(cg[v] <= r["hi"][0])
-    mu, Sig = O.stats(Y[0, :-1].cpu().numpy())
-    ref, _ = O.loglik(mu, Sig, Y[0, -1].cpu().numpy(), ridge=1e-10)
-    np.testing.assert_allclose(out[0].cpu().numpy(), ref, rtol=0, atol=1e-6)
+    for p in range(P):                      # every proposal of the launch
+        pool = pools[p].cpu().numpy()
+        cg = np.rint(Y[p].cpu().numpy() * N_set * Nt).astype(np.int64)
+        v = 0
+        for k in range(n_ens):
+            for l in range(n_ens):
+                r = O.features(pool[k * N:k * N + N_set], pool[l * N + N_set:(l + 1) * N], grid, 0x1, r1[None],
+                               band=BAND)
+                assert np.all(r["lo"][0] <= cg[v]) and np.all(cg[v] <= r["hi"][0]), (p, k, l)
+                v += 1
+        kk = p % n_ens                      # the caller's k0 (Alg. 3 line "y~ = C(R, s_data, s^{k0,2})")
+        r = O.features(dat, pool[kk * N + N_set:(kk + 1) * N], grid, 0x1, r1[None], band=BAND)
+        assert np.all(r["lo"][0] <= cg[v]) and np.all(cg[v] <= r["hi"][0]), p
+        mu, Sig = O.stats(Y[p, :-1].cpu().numpy())
+        ref, _ = O.loglik(mu, Sig, Y[p, -1].cpu().numpy(), ridge=1e-10)
+        np.testing.assert_allclose(out[p].cpu().numpy(), ref, rtol=0, atol=1e-6)
 
 
 def test_c6_full_theta_bins_and_replicates(cil, oracle_mod):
