@@ -759,9 +759,9 @@ def test_c4_full_theta_vs_oracle(cil, oracle_mod):
 
 def test_c6_full_theta_bins_and_replicates(cil, oracle_mod):
     """C6 (Alg. A2 at the paper's sizes: pool 1000 of 64x64x2, N_set = 50, 1000 replicates) in
-    the bench's configuration for 2 proposals; proposal 0: the bin matrix on a 1000 x 1000
-    sample block against the oracle's distances, and 12 replicates against brute force on the
-    resampled sets."""
+    the bench's configuration for 2 proposals: the bin matrix of proposal 0 on a sampled block
+    against the oracle's distances; for every proposal 12 replicates against brute force on the
+    resampled sets and the log-density on the GPU's own vectors."""
     O = oracle_mod
     dev = torch.device("cuda")
     grid = (2, 64, 64, 0.0)
@@ -789,12 +789,19 @@ def test_c6_full_theta_bins_and_replicates(cil, oracle_mod):
     hi = (Ds[:, :, None] < r1 * (1 + BAND)).sum(-1)
     b = bins[0, 0].cpu().numpy()[rows]
     assert np.all(lo <= b) and np.all(b <= hi)
-    # replicate vectors of proposal 0
+    # replicate vectors of every proposal (12 sampled replicates each), and the tail (mu, Sigma,
+    # Cholesky log-density) of each proposal on the GPU's own vectors
     Nt = N_syn - N_set
     ks = np.arange(0, n_rep, 83)[:12]
-    rr = O.resample_features(pool0, pool0, grid, 0x1, r1[None], I1[0][ks], I2[0][ks], band=BAND)
-    cg = np.rint(Y[0].cpu().numpy()[ks] * N_set * Nt).astype(np.int64)
-    assert np.all(rr["lo"][:, 0] <= cg) and np.all(cg <= rr["hi"][:, 0])
+    for p in range(P):
+        pool = pools[p].numpy()
+        Yg = Y[p].cpu().numpy()
+        rr = O.resample_features(pool, pool, grid, 0x1, r1[None], I1[p][ks], I2[p][ks], band=BAND)
+        cg = np.rint(Yg[ks] * N_set * Nt).astype(np.int64)
+        assert np.all(rr["lo"][:, 0] <= cg) and np.all(cg <= rr["hi"][:, 0]), p
+        mu, Sig = O.stats(Yg[:-1])
+        o2, _ = O.loglik(mu, Sig, Yg[-1], ridge=1e-10)
+        np.testing.assert_allclose(out[p].cpu().numpy(), o2, rtol=0, atol=1e-6)
 
 
 def test_c7_full_training_sampled_blocks(cil, oracle_mod):
